@@ -1,0 +1,144 @@
+/*
+ * graphmd_b200 -- C ABI of the B200-native graph-partitioned MLIP inference
+ * path (DistMLIP -> graphmd).  Drop-in for the reference's plugin API:
+ *
+ *   graphmd::Distributed::create_distributed   proj/include/graphmd/engine.hpp:51-56
+ *   graphmd::forward_distributed               proj/include/graphmd/potential.hpp:58-60
+ *   Distributed feature API (transfer, transpose, duplicates, distribute,
+ *   aggregate)                                 proj/include/graphmd/engine.hpp:74-129
+ *   graph / partition / line-graph views       engine.hpp:58-72, neighborlist.hpp:17-33,
+ *                                              partitioner.hpp:16-82, linegraph.hpp:15-54
+ *
+ * Plain C types only.  Every function returns GMD_OK (0) or an error code;
+ * the message (same text as the reference's graphmd::Error where one exists)
+ * is available from gmd_last_error(h).  Host pointers unless a flag says
+ * otherwise.  One control thread per handle (SPEC: one thread drives the API).
+ *
+ * Buffers: the handle owns all device memory, grows it on demand and reuses
+ * it across builds (per-MD-step rebuilds do not reallocate).
+ */
+#ifndef GRAPHMD_B200_H
+#define GRAPHMD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMD_OK 0
+#define GMD_ERR_CONFIG 2  /* invalid input/configuration (reference: Error) */
+#define GMD_ERR_RUNTIME 3 /* runtime failure: non-finite feature, plan misalignment */
+#define GMD_ERR_CUDA 4    /* CUDA / NCCL failure */
+#define GMD_ERR_ARG 5     /* bad handle / null pointer / index out of range */
+
+/* gmd_build flags */
+#define GMD_ALLOW_NARROW 1u   /* allow slabs narrower than the cutoff (partitioner.cpp:21-33) */
+#define GMD_INPUT_DEVICE 2u   /* pos/Z are device pointers on the handle's GPU */
+#define GMD_EQUAL_WIDTH 4u    /* BoundaryMode::kEqualWidth (partitioner.hpp:22-25) */
+
+/* gmd_forward flags */
+#define GMD_OUTPUT_DEVICE 1u  /* output pointers are device pointers */
+#define GMD_OUTPUT_F32 2u     /* per_atom / forces are float instead of double */
+
+/* feature dtypes */
+#define GMD_F32 0
+#define GMD_F64 1
+
+typedef struct gmd_handle gmd_handle;
+
+const char* gmd_version(void);
+const char* gmd_last_error(const gmd_handle* h);
+
+/* one handle per process and GPU (device ordinal) */
+int gmd_create(int device, gmd_handle** out);
+void gmd_destroy(gmd_handle* h);
+
+/* Distributed::create_distributed(system, atom_cutoff, threebody_cutoff, p,
+ * n_threads, allow_narrow, threebody_tau) -- engine.hpp:51-56.
+ * pos: n x 3 Cartesian (A), Z: n atomic numbers, lattice: 3 x 3 rows,
+ * pbc: 3 flags (NULL = fully periodic), r3 <= 0 disables the line graph.
+ * n_threads is accepted and ignored (the GPU path is deterministic). */
+int gmd_build(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z,
+              const double lattice[9], const uint8_t pbc[3], double rc, double r3,
+              double tau, int p, int n_threads, uint32_t flags);
+
+/* ToyPotentialParams (potential.hpp:15-41) as a flat fp64 blob:
+ * emb[119F] | layer_w[LFF] | layer_b[LF] | basis_proj[FK] | basis3_proj[FK] |
+ * w3[FF] | w4[FF] | readout[F].  The compiled kernels support F=16, K=8, L<=8. */
+int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
+                   const double* blob);
+/* ToyPotentialParams::init (potential.cpp:119-148), host-side */
+int64_t gmd_params_size(int F, int K, int L);
+int gmd_params_init(uint64_t seed, int F, int K, int L, double r_atom, double r3,
+                    double* blob);
+
+/* forward_distributed(dist, params, timing) -- potential.hpp:58-60.
+ * energy (1), per_atom (n), forces (n x 3), stress (9, row-major), timing (4:
+ * graph creation of the last build, feature calc, forward, backward; seconds).
+ * Any output pointer may be NULL. */
+int gmd_forward(gmd_handle* h, double* energy, void* per_atom, void* forces, double* stress,
+                double* timing, uint32_t flags);
+
+/* ---- views (parity / export; materialized on demand) -------------------- */
+int gmd_num_nodes(const gmd_handle* h, int64_t* n);
+int gmd_num_edges(const gmd_handle* h, int64_t* ne);
+int gmd_num_partitions(const gmd_handle* h, int* p);
+/* AtomGraph in canonical order; off = image_offset (n x 3 int32) */
+int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, double* dist,
+                  double* vec);
+/* system after ensure_periodic (positions n x 3, lattice 3 x 3) */
+int gmd_get_system(gmd_handle* h, double* pos, double* lattice);
+/* PartitionRule: axis and p + 1 boundaries */
+int gmd_get_rule(gmd_handle* h, int* axis, double* boundaries);
+int gmd_get_owner(gmd_handle* h, int32_t* owner);
+/* SpanLayout of partition `part` over atoms (bonds = 0) or bonds (bonds = 1) */
+int gmd_get_layout_size(gmd_handle* h, int part, int bonds, int64_t* size);
+int gmd_get_layout(gmd_handle* h, int part, int bonds, int64_t* node_array,
+                   int64_t* markers /* 2 + 2p */);
+int gmd_get_num_duplicates(gmd_handle* h, int part, int bonds, int64_t* count);
+int gmd_get_duplicates(gmd_handle* h, int part, int bonds, int64_t* pairs);
+/* AtomPartition: owned edges (ascending global id) and canonical local ends */
+int gmd_get_num_owned_edges(gmd_handle* h, int part, int64_t* count);
+int gmd_get_owned_edges(gmd_handle* h, int part, int64_t* owned, int64_t* local_src,
+                        int64_t* local_dst);
+int gmd_get_num_border_edges(gmd_handle* h, int part, int64_t* count);
+int gmd_get_border_edges(gmd_handle* h, int part, int64_t* border);
+/* PartitionedLineGraph */
+int gmd_has_line_graph(const gmd_handle* h, int* yes);
+int gmd_get_num_bonds(gmd_handle* h, int64_t* nb);
+int gmd_get_bonds(gmd_handle* h, int64_t* edge_of_bond, int32_t* bond_owner);
+int gmd_get_num_line_edges(gmd_handle* h, int part, int64_t* count);
+int gmd_get_line_edges(gmd_handle* h, int part, int64_t* pairs /* (local e, local e') */);
+
+/* ---- Distributed feature API (engine.hpp:74-129) -------------------------
+ * Per-partition blocks live in ONE device buffer: partition i's block starts
+ * at row gmd_block_offset(i) and has layout-size rows of `width` elements. */
+int gmd_block_rows(gmd_handle* h, int bonds, int64_t* total_rows);
+int gmd_block_offset(gmd_handle* h, int part, int bonds, int64_t* row0);
+int gmd_transfer(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype);
+int gmd_transfer_transpose(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype);
+int gmd_sync_duplicates(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype);
+/* host global [rows x width] <-> device blocks */
+int gmd_distribute(gmd_handle* h, int bonds, const void* host_global, void* dev_buf, int width,
+                   int dtype);
+int gmd_aggregate(gmd_handle* h, int bonds, const void* dev_buf, void* host_global, int width,
+                  int dtype);
+/* negative-control hook (engine.cpp:296): corrupt one transfer plan entry */
+int gmd_corrupt_transfer_plan_for_test(gmd_handle* h);
+
+/* ---- input synthesis helpers (system.hpp:99-149; host-side) ------------- */
+int gmd_util_rng_uniform(uint64_t seed, int64_t count, double lo, double hi, double* out);
+int gmd_util_supercell(int64_t n, const double* pos, const int32_t* Z, const double lattice[9],
+                       int rx, int ry, int rz, double amp, uint64_t seed, double* out_pos,
+                       int32_t* out_Z, double* out_lattice);
+
+/* kernel-level timing of the last gmd_forward/gmd_build (ms per phase), for
+ * the bench's roofline: names are NUL-separated in `names` */
+int gmd_profile(gmd_handle* h, int enable);
+int gmd_profile_read(gmd_handle* h, char* names, int names_cap, double* ms, int* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPHMD_B200_H */

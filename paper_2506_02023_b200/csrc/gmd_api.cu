@@ -1,0 +1,1499 @@
+// C ABI + host orchestration of the graphmd B200 path.
+//
+// gmd_build   == Distributed::create_distributed (proj/src/engine.cpp:44-65)
+// gmd_forward == forward_distributed             (proj/src/potential.cpp:563-985)
+//
+// All per-atom / per-edge work runs in the kernels of gmd_graph.cu,
+// gmd_partition.cu, gmd_linegraph.cu and gmd_model.cu; the host only does
+// O(1)/O(p) scalar geometry (3x3 lattice algebra, slab walls), sizes buffers
+// and -- for the parity views only -- reshapes device results into the
+// reference's per-partition containers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/graphmd_b200.h"
+#include "gmd_common.cuh"
+#include "gmd_graph.cuh"
+#include "gmd_model.cuh"
+#include "gmd_partition.cuh"
+
+namespace gmd {
+void launch_bond_owner(int64_t n, const int32_t* brow, const int32_t* owner, int32_t* bown,
+                       cudaStream_t s);
+void launch_bond_req(int64_t n, const int32_t* brow, const int32_t* bedge, const int32_t* esrc,
+                     const int32_t* owner, unsigned long long* breq, cudaStream_t s);
+void launch_line_count(int64_t nb, const int32_t* bedge, const int32_t* esrc, const int32_t* brow,
+                       int32_t* cnt, cudaStream_t s);
+void launch_line_fill(int64_t nb, const int32_t* bedge, const int32_t* esrc, const int32_t* brow,
+                      const int32_t* brev, const int32_t* lpos, int32_t* pairs, cudaStream_t s);
+int tb_grid_size(int64_t n);
+}  // namespace gmd
+
+using namespace gmd;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// device buffer arena: grow-only, reused across builds / steps
+// ---------------------------------------------------------------------------
+struct DBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <typename T>
+    T* get(size_t count) {
+        size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            size_t nc = std::max(bytes, cap + cap / 4);
+            GMD_CUDA(cudaMalloc(&p, nc));
+            cap = nc;
+        }
+        return static_cast<T*>(p);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// ---- host fp64 lattice algebra with the reference's operand order -------
+struct V3 {
+    double x, y, z;
+};
+inline V3 vmul(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+inline V3 vdiv(V3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
+inline double vdot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline V3 vcross(V3 a, V3 b) {
+    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+inline double vnorm(V3 a) { return std::sqrt(vdot(a, a)); }
+inline V3 row3(const double* L, int k) { return {L[3 * k], L[3 * k + 1], L[3 * k + 2]}; }
+inline double det3(const double* L) { return vdot(row3(L, 0), vcross(row3(L, 1), row3(L, 2))); }
+// Mat3::inverse (system.cpp:55-70)
+void inverse3(const double* L, double* inv) {
+    double d = det3(L);
+    if (std::abs(d) < 1e-10) raise(kConfig, "lattice is singular (|det| < 1e-10)");
+    V3 bc = vdiv(vcross(row3(L, 1), row3(L, 2)), d);
+    V3 ca = vdiv(vcross(row3(L, 2), row3(L, 0)), d);
+    V3 ab = vdiv(vcross(row3(L, 0), row3(L, 1)), d);
+    double r[9] = {bc.x, ca.x, ab.x, bc.y, ca.y, ab.y, bc.z, ca.z, ab.z};
+    std::memcpy(inv, r, sizeof r);
+}
+// perpendicular_width (system.cpp:87-93)
+double perp_width(const double* L, int axis) {
+    double area = vnorm(vcross(row3(L, (axis + 1) % 3), row3(L, (axis + 2) % 3)));
+    if (area <= 0.0) raise(kConfig, "degenerate cell");
+    return std::abs(det3(L)) / area;
+}
+
+double dec_ordered(unsigned long long u) {
+    u = (u & 0x8000000000000000ull) ? (u & ~0x8000000000000000ull) : ~u;
+    double d;
+    std::memcpy(&d, &u, 8);
+    return d;
+}
+
+// ---- small generic kernels for the feature API --------------------------
+__global__ void k_copy_rows(int64_t nr, const int32_t* __restrict__ dst_rows,
+                            const int32_t* __restrict__ src_rows, uint32_t* buf, int wwords) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nr * wwords) return;
+    int64_t k = t / wwords;
+    int c = (int)(t - k * wwords);
+    buf[(int64_t)dst_rows[k] * wwords + c] = buf[(int64_t)src_rows[k] * wwords + c];
+}
+
+template <typename T>
+__global__ void k_transpose_add(int64_t nr, const int32_t* __restrict__ to_rows,
+                                const int32_t* __restrict__ from_rows, T* buf, int width) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nr * width) return;
+    int64_t k = t / width;
+    int c = (int)(t - k * width);
+    T* a = buf + (int64_t)to_rows[k] * width + c;
+    T* b = buf + (int64_t)from_rows[k] * width + c;
+    *a += *b;
+    *b = T(0);
+}
+
+// duplicates grouped by canonical row, dups in ascending row order
+template <typename T>
+__global__ void k_dup_fold(int64_t ng, const int32_t* __restrict__ gcanon,
+                           const int32_t* __restrict__ gstart, const int32_t* __restrict__ dups,
+                           T* buf, int width) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ng * width) return;
+    int64_t g = t / width;
+    int c = (int)(t - g * width);
+    T* cr = buf + (int64_t)gcanon[g] * width + c;
+    for (int k = gstart[g]; k < gstart[g + 1]; ++k) {
+        T* d = buf + (int64_t)dups[k] * width + c;
+        *cr += *d;
+        *d = T(0);
+    }
+}
+
+__global__ void k_gather_rows(int64_t nr, const int32_t* __restrict__ idx,
+                              const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                              int wwords) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nr * wwords) return;
+    int64_t k = t / wwords;
+    int c = (int)(t - k * wwords);
+    int64_t r = idx ? idx[k] : k;
+    dst[k * wwords + c] = src[r * wwords + c];
+}
+
+// for every FROM row: the row of the same id inside the sender's TO span
+// (engine.cpp:122-143 copies TO_j[i] -> FROM_i[j] row by row)
+__global__ void k_api_src(int64_t nfrom, const int32_t* __restrict__ xdst,
+                          const int32_t* __restrict__ list_off, int p, int corrupt,
+                          int32_t* __restrict__ out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nfrom) return;
+    const int r = xdst[k], stride = 1 + 2 * p;
+    int lo = 0, hi = p - 1;  // partition: last i with list_off[i*stride] <= r
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (list_off[mid * stride] <= r) lo = mid; else hi = mid - 1;
+    }
+    const int i = lo;
+    int j = 0;
+    for (; j < p; ++j)
+        if (r < list_off[i * stride + 2 + p + j]) break;
+    const int fb = list_off[i * stride + 1 + p + j];
+    out[k] = corrupt ? list_off[j * stride] + (r - fb) : list_off[j * stride + 1 + i] + (r - fb);
+}
+
+__global__ void k_to_f32(int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
+}
+
+// --------------------------------------------------------------------------
+// host RNG of the reference (system.hpp:121-149): mt19937_64 + Box-Muller
+struct HostRng {
+    std::mt19937_64 gen;
+    bool have = false;
+    double spare = 0.0;
+    explicit HostRng(uint64_t s) : gen(s) {}
+    double uniform() { return (double)(gen() >> 11) * 0x1.0p-53; }
+    double normal() {
+        if (have) {
+            have = false;
+            return spare;
+        }
+        double u1 = 0.0;
+        while (u1 == 0.0) u1 = uniform();
+        double u2 = uniform();
+        double r = std::sqrt(-2.0 * std::log(u1));
+        double a = 2.0 * 3.14159265358979323846 * u2;
+        spare = r * std::sin(a);
+        have = true;
+        return r * std::cos(a);
+    }
+};
+
+// one layout (atoms or bonds): lists in super-row space
+struct LayoutState {
+    bool ready = false;
+    int p = 1;
+    int64_t nid = 0;
+    std::vector<int32_t> list_off;  // p(1+2p)+1
+    int64_t rows = 0;
+    int64_t nfrom = 0;
+    DBuf node_array, crow, list_off_d, xdst, xsrc, xapi, owner, req;
+    bool api_ready = false;
+    bool api_corrupt = false;
+    // duplicates (host + device groups)
+    bool dups_ready = false;
+    std::vector<int32_t> h_nodes;  // host copy of node_array (lazy)
+    DBuf g_canon, g_start, g_dups, d_canon, d_dup;
+    int64_t ngroups = 0, ndups = 0;
+    int64_t base(int i) const { return list_off[(size_t)i * (1 + 2 * p)]; }
+};
+
+}  // namespace
+
+struct gmd_handle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    bool built = false;
+    int64_t n = 0, ne = 0, nb = 0;
+    int p = 1;
+    double rc = 0, r3 = 0, tau = 0;
+    bool has_lg = false, allow_narrow = false, corrupted = false;
+    Geom geom{};
+    double lat[9]{};
+    int axis = 0;
+    std::vector<double> bounds;
+    double t_graph = 0.0;
+
+    LayoutState atoms, bonds;
+
+    DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
+    DBuf row, src, img, vd, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
+    DBuf brow, bedge, brev, lcnt, lpairs;
+
+    // model
+    bool params_set = false;
+    ModelConst mc{};
+    int F = 16, K = 8, L = 0;
+    double p_r_atom = 0, p_r3 = 0;
+    std::vector<DBuf> H;
+    DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v3_part, red, per_atom,
+        forces, conv_tmp, exp_tmp;
+    cudaEvent_t ev[8] = {};
+
+    // host caches for views (invalidated per build)
+    bool hc_ready = false;
+    std::vector<int32_t> h_owner, h_row, h_src, h_lsrc, h_crow;
+    bool hcb_ready = false;
+    std::vector<int32_t> h_bedge, h_bown, h_pairs;
+};
+
+namespace {
+
+void sync(gmd_handle* h) { GMD_CUDA(cudaStreamSynchronize(h->stream)); }
+
+void read_flags(gmd_handle* h, int32_t out[2]) {
+    GMD_CUDA(cudaMemcpyAsync(out, h->flags.as<int32_t>(), 8, cudaMemcpyDeviceToHost, h->stream));
+    sync(h);
+    int e = out[1];
+    if (e & kErrImgRange)
+        raise(kConfig, "periodic image offset exceeds the packed range (+-511 cells)");
+    if (e & kErrQRange) raise(kConfig, "neighbour stencil exceeds 127 cell images per axis");
+    if (e & kErrCap) raise(kRuntime, "internal: neighbour buffer overflow");
+    if (e & 8) raise(kRuntime, "internal: edge endpoint missing from partition layout");
+    if (e & 16) raise(kConfig, "an atom has more than 64 three-body bonds (unsupported)");
+    if (e & 32) raise(kRuntime, "internal: reverse bond not found (graph not symmetric)");
+}
+
+void scan_i32(gmd_handle* h, const int32_t* in, int32_t* out, int64_t n) {
+    size_t tb = scan_tmp_bytes(n);
+    void* tmp = h->scan_tmp.get<char>(tb);
+    exclusive_scan_i32(in, out, n, tmp, tb, h->stream);
+}
+
+template <typename T>
+void d2h(gmd_handle* h, std::vector<T>& v, const void* d, size_t count) {
+    v.resize(count);
+    if (count)
+        GMD_CUDA(cudaMemcpyAsync(v.data(), d, count * sizeof(T), cudaMemcpyDeviceToHost, h->stream));
+}
+
+// ensure_periodic (system.cpp:242-270) with the per-atom projections on the GPU
+void ensure_periodic_dev(gmd_handle* h, const uint8_t* pbc, double cutoff) {
+    if (!pbc || (pbc[0] && pbc[1] && pbc[2])) return;
+    if (cutoff <= 0.0) raise(kConfig, "cutoff must be positive");
+    double* d = h->small.get<double>(4);
+    for (int k = 0; k < 3; ++k) {
+        if (pbc[k]) continue;
+        V3 dir = row3(h->lat, k);
+        double len = vnorm(dir);
+        if (len == 0.0)
+            dir = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+        else
+            dir = vdiv(dir, len);
+        double dv[3] = {dir.x, dir.y, dir.z};
+        double lo = 0.0, hi = 0.0;
+        if (h->n > 0) {
+            launch_minmax_proj(h->pos.as<double>(), h->n, dv, d, h->stream);
+            unsigned long long mm[2];
+            GMD_CUDA(cudaMemcpyAsync(mm, d, 16, cudaMemcpyDeviceToHost, h->stream));
+            sync(h);
+            lo = dec_ordered(mm[0]);
+            hi = dec_ordered(mm[1]);
+        }
+        double extent = hi - lo + 2.0 * cutoff;
+        V3 nr = vmul(dir, extent);
+        h->lat[3 * k] = nr.x;
+        h->lat[3 * k + 1] = nr.y;
+        h->lat[3 * k + 2] = nr.z;
+        V3 sh = vmul(dir, cutoff - lo);
+        double add[3] = {sh.x, sh.y, sh.z};
+        launch_shift(h->pos.as<double>(), h->n, add, h->stream);
+    }
+}
+
+// PURE/TO/FROM layout of an id space (atoms or bonds) on the GPU
+void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
+                  const unsigned long long* req, int64_t nid, int p) {
+    cudaStream_t s = h->stream;
+    ls.p = p;
+    ls.nid = nid;
+    ls.api_ready = false;
+    ls.dups_ready = false;
+    ls.h_nodes.clear();
+    const int64_t nl = layout_nlists(p), nch = layout_chunks(nid);
+    LayoutWs lw{};
+    lw.counts = h->counts.get<int32_t>(nl * nch + 1);
+    lw.scan_tmp_bytes = scan_tmp_bytes(nl * nch);
+    lw.scan_tmp = h->scan_tmp.get<char>(lw.scan_tmp_bytes);
+    int32_t* lo_d = ls.list_off_d.get<int32_t>(nl + 1);
+    launch_layout_plan(owner, req, nid, p, lw, lo_d, s);
+    d2h(h, ls.list_off, lo_d, nl + 1);
+    sync(h);
+    ls.rows = ls.list_off[nl];
+    int32_t* na = ls.node_array.get<int32_t>(ls.rows);
+    int32_t* cr = ls.crow.get<int32_t>(nid);
+    launch_layout_fill(owner, req, nid, p, lw, na, cr, s);
+    const int stride = 1 + 2 * p;
+    std::vector<int32_t> rp(3 * p + 1);
+    int32_t* ranges = rp.data();
+    int32_t* prefix = rp.data() + 2 * p;
+    prefix[0] = 0;
+    for (int i = 0; i < p; ++i) {
+        ranges[2 * i] = ls.list_off[i * stride + 1 + p];
+        ranges[2 * i + 1] = ls.list_off[(i + 1) * stride];
+        prefix[i + 1] = prefix[i] + ranges[2 * i + 1] - ranges[2 * i];
+    }
+    ls.nfrom = prefix[p];
+    int32_t* sm = h->small.get<int32_t>(3 * p + 1);
+    GMD_CUDA(cudaMemcpyAsync(sm, rp.data(), sizeof(int32_t) * rp.size(), cudaMemcpyHostToDevice, s));
+    launch_from_src(na, cr, sm, p, ls.nfrom, sm + 2 * p, ls.xdst.get<int32_t>(ls.nfrom),
+                    ls.xsrc.get<int32_t>(ls.nfrom), s);
+    sync(h);  // rp is a host temporary
+    ls.ready = true;
+}
+
+void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, const double* lat,
+                const uint8_t* pbc, double rc, double r3, double tau, int p, uint32_t flags) {
+    cudaStream_t s = h->stream;
+    h->built = false;
+    h->hc_ready = h->hcb_ready = false;
+    h->atoms.ready = h->bonds.ready = false;
+    h->corrupted = false;
+    if (!pos || !Z || !lat) raise(kArg, "null input pointer");
+    if (p < 1) raise(kConfig, "partition count must be >= 1");
+    if (rc <= 0.0) raise(kConfig, "cutoff must be positive");
+    if (n <= 0) raise(kConfig, "cannot build neighbor list for empty system");
+    if (n >= ((int64_t)1 << 31) - 1) raise(kConfig, "atom count exceeds the int32 index range");
+    GMD_CUDA(cudaEventRecord(h->ev[0], s));
+    h->n = n;
+    h->p = p;
+    h->rc = rc;
+    h->r3 = r3;
+    h->tau = tau;
+    h->allow_narrow = (flags & GMD_ALLOW_NARROW) != 0;
+    std::memcpy(h->lat, lat, sizeof h->lat);
+
+    double* dpos = h->pos.get<double>(3 * n);
+    int32_t* dZ = h->Z.get<int32_t>(n);
+    cudaMemcpyKind kind =
+        (flags & GMD_INPUT_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    GMD_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, kind, s));
+    GMD_CUDA(cudaMemcpyAsync(dZ, Z, sizeof(int32_t) * n, kind, s));
+    ensure_periodic_dev(h, pbc, rc);
+    if (std::abs(det3(h->lat)) < 1e-10)
+        raise(kConfig, "periodic system requires an invertible lattice");
+
+    // ---- scalar geometry (neighborlist.cpp:119-126)
+    Geom& g = h->geom;
+    std::memcpy(g.L, h->lat, sizeof g.L);
+    inverse3(h->lat, g.inv);
+    int64_t nbins = 1;
+    for (int k = 0; k < 3; ++k) {
+        double width = perp_width(h->lat, k);
+        double fb = std::floor(width / rc);
+        if (fb > 4.0e6) raise(kConfig, "cell is too large relative to the cutoff for binning");
+        g.bins[k] = std::max(1, (int)fb);
+        double bw = width / g.bins[k];
+        g.sten[k] = (int)std::floor(rc / bw) + 1;
+        nbins *= g.bins[k];
+    }
+    if (nbins > ((int64_t)1 << 30)) raise(kConfig, "too many neighbour-search bins");
+    g.cutoff2 = rc * rc;
+    g.pre2 = g.cutoff2 * 1.000001;
+    g.bond_bound = -1.0;
+    {  // partition axis: longest lattice vector, first max wins (partitioner.cpp:57-64)
+        double best = -1.0;
+        for (int k = 0; k < 3; ++k) {
+            double len = vnorm(row3(h->lat, k));
+            if (len > best) {
+                best = len;
+                h->axis = k;
+            }
+        }
+        g.axis = h->axis;
+    }
+    if (p > kMaxParts) raise(kConfig, "partition count limited to 64");
+    if ((int64_t)p > n) raise(kConfig, "more partitions than atoms");
+    if (r3 > 0.0) {  // check_ranges (linegraph.cpp:10-14)
+        if (r3 > rc) raise(kConfig, "three-body range cannot exceed the atom graph cutoff");
+        if (tau < 0.0) raise(kConfig, "tolerance tau must be >= 0");
+        g.bond_bound = r3 + tau;
+    }
+
+    // ---- cell list + neighbour search (neighborlist.cpp:108-197)
+    NLBuffers b{};
+    b.pos = dpos;
+    b.cell = h->cell.get<int32_t>(3 * n);
+    b.fw_axis = h->fw.get<double>(n);
+    b.bin = h->bin.get<int32_t>(n);
+    b.bin_cnt = h->bin_cnt.get<int32_t>(nbins);
+    b.bin_start = h->bin_start.get<int32_t>(nbins + 1);
+    b.s_id = h->s_id.get<int32_t>(n);
+    b.s_w = h->s_w.get<double>(3 * n);
+    b.s_p = h->s_p.get<double>(3 * n);
+    b.s_c = h->s_c.get<int32_t>(3 * n);
+    b.deg = h->deg.get<int32_t>(n);
+    b.bcnt = h->bcnt.get<int32_t>(n);
+    b.flags = h->flags.get<int32_t>(4);
+    int32_t* fillp = h->fill.get<int32_t>(nbins);
+    GMD_CUDA(cudaMemsetAsync(b.bin_cnt, 0, sizeof(int32_t) * nbins, s));
+    GMD_CUDA(cudaMemsetAsync(fillp, 0, sizeof(int32_t) * nbins, s));
+    GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
+    launch_wrap(g, n, b, s);
+    scan_i32(h, b.bin_cnt, b.bin_start, nbins);
+    launch_bin_scatter(g, n, b, fillp, s);
+    launch_nl_count(g, nbins, n, b, s);
+    int32_t* rowp = h->row.get<int32_t>(n + 1);
+    scan_i32(h, b.deg, rowp, n);
+    int32_t ne32 = 0;
+    GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
+    int32_t hdr[2];
+    read_flags(h, hdr);
+    if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
+    h->ne = ne32;
+    int cap = 32;
+    while (cap < hdr[0]) cap <<= 1;
+    GraphDev gd;
+    gd.n = n;
+    gd.ne = h->ne;
+    gd.row = rowp;
+    gd.src = h->src.get<int32_t>(h->ne);
+    gd.img = h->img.get<uint32_t>(h->ne);
+    gd.vd = h->vd.get<float4>(h->ne);
+    gd.bond = h->ebond.get<uint8_t>(h->ne);
+    launch_nl_fill(g, nbins, cap, b, gd, s);
+
+    // ---- partitions (partitioner.cpp:46-218)
+    h->bounds.assign(p + 1, 0.0);
+    h->bounds[p] = 1.0;
+    int32_t* ownp = h->atoms.owner.get<int32_t>(n);
+    LayoutState& A = h->atoms;
+    if (p == 1) {
+        GMD_CUDA(cudaMemsetAsync(ownp, 0, sizeof(int32_t) * n, s));
+        A.p = 1;
+        A.nid = n;
+        A.list_off = {0, (int32_t)n, (int32_t)n, (int32_t)n};
+        A.rows = n;
+        A.nfrom = 0;
+        A.ready = true;
+        A.api_ready = A.dups_ready = false;
+        A.h_nodes.clear();
+    } else {
+        if (flags & GMD_EQUAL_WIDTH) {
+            for (int k = 1; k < p; ++k) h->bounds[k] = (double)k / p;
+        } else {
+            std::vector<int64_t> ranks;
+            for (int k = 1; k < p; ++k) {
+                int64_t c = n * k / p;
+                if (c >= 1 && c < n) {
+                    ranks.push_back(c - 1);
+                    ranks.push_back(c);
+                }
+            }
+            std::sort(ranks.begin(), ranks.end());
+            ranks.erase(std::unique(ranks.begin(), ranks.end()), ranks.end());
+            std::vector<double> vals(ranks.size());
+            if (!ranks.empty()) {
+                void* ws = h->sel_ws.get<char>(select_ws_bytes((int)ranks.size()));
+                double* so = h->sel_out.get<double>(ranks.size());
+                launch_select(b.fw_axis, n, ranks.data(), (int)ranks.size(), ws, so, s);
+                GMD_CUDA(cudaMemcpyAsync(vals.data(), so, sizeof(double) * vals.size(),
+                                         cudaMemcpyDeviceToHost, s));
+                sync(h);
+            }
+            auto at = [&](int64_t r) {
+                size_t i = std::lower_bound(ranks.begin(), ranks.end(), r) - ranks.begin();
+                return vals[i];
+            };
+            for (int k = 1; k < p; ++k) {  // partitioner.cpp:80-85
+                int64_t c = n * k / p;
+                h->bounds[k] = (c >= 1 && c < n) ? 0.5 * (at(c - 1) + at(c)) : (double)k / p;
+            }
+        }
+        for (int k = 1; k <= p; ++k)
+            if (h->bounds[k] <= h->bounds[k - 1])
+                raise(kConfig,
+                      "cannot place distinct partition boundaries; coordinates along the axis "
+                      "are degenerate");
+        if (!h->allow_narrow) {  // check_slab_widths (partitioner.cpp:21-33)
+            double perp = perp_width(h->lat, h->axis);
+            for (int i = 0; i < p; ++i) {
+                double width = (h->bounds[i + 1] - h->bounds[i]) * perp;
+                if (width < rc)
+                    raise(kConfig, "partition-width error: slab " + std::to_string(i) + " is " +
+                                       std::to_string(width) + " A wide, below the cutoff " +
+                                       std::to_string(rc) + " A");
+            }
+        }
+        Bounds bd{};
+        bd.p = p;
+        for (int k = 0; k <= p; ++k) bd.b[k] = h->bounds[k];
+        launch_owner(b.fw_axis, n, bd, ownp, s);
+        auto* reqp = A.req.get<unsigned long long>(n);
+        GMD_CUDA(cudaMemsetAsync(reqp, 0, sizeof(unsigned long long) * n, s));
+        launch_required(rowp, gd.src, n, ownp, reqp, s);
+        build_layout(h, A, ownp, reqp, n, p);
+        launch_edge_lsrc(rowp, gd.src, n, ownp, A.crow.as<int32_t>(), A.node_array.as<int32_t>(),
+                         A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(h->ne), b.flags, s);
+    }
+
+    // ---- three-body bonds (linegraph.cpp:25-43) + reverse-bond index
+    h->has_lg = r3 > 0.0;
+    h->nb = 0;
+    if (h->has_lg) {
+        int32_t* br = h->brow.get<int32_t>(n + 1);
+        scan_i32(h, b.bcnt, br, n);
+        int32_t nb32 = 0;
+        GMD_CUDA(cudaMemcpyAsync(&nb32, br + n, 4, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        h->nb = nb32;
+        int32_t* be = h->bedge.get<int32_t>(h->nb);
+        int32_t* bv = h->brev.get<int32_t>(h->nb);
+        launch_bond_edges(rowp, gd.bond, n, br, be, s);
+        launch_bond_rev(n, gd, br, be, bv, b.flags, s);
+    }
+    GMD_CUDA(cudaEventRecord(h->ev[1], s));
+    read_flags(h, hdr);
+    float ms = 0.f;
+    GMD_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    h->t_graph = ms * 1e-3;
+    h->built = true;
+}
+
+void need_built(const gmd_handle* h) {
+    if (!h->built) raise(kConfig, "no graph has been built on this handle");
+}
+
+// bond layouts + line graph partitions, lazily (export / bond feature API)
+void ensure_bond_layout(gmd_handle* h) {
+    need_built(h);
+    if (!h->has_lg) raise(kConfig, "no line graph was built");
+    LayoutState& B = h->bonds;
+    if (B.ready) return;
+    cudaStream_t s = h->stream;
+    int32_t* bown = B.owner.get<int32_t>(h->nb);
+    launch_bond_owner(h->n, h->brow.as<int32_t>(), h->atoms.owner.as<int32_t>(), bown, s);
+    if (h->p == 1) {
+        B.p = 1;
+        B.nid = h->nb;
+        B.list_off = {0, (int32_t)h->nb, (int32_t)h->nb, (int32_t)h->nb};
+        B.rows = h->nb;
+        B.nfrom = 0;
+        B.ready = true;
+        B.api_ready = B.dups_ready = false;
+        B.h_nodes.clear();
+        return;
+    }
+    auto* breq = B.req.get<unsigned long long>(h->nb);
+    launch_bond_req(h->n, h->brow.as<int32_t>(), h->bedge.as<int32_t>(), h->src.as<int32_t>(),
+                    h->atoms.owner.as<int32_t>(), breq, s);
+    build_layout(h, B, bown, breq, h->nb, h->p);
+}
+
+void ensure_host_cache(gmd_handle* h) {
+    need_built(h);
+    if (h->hc_ready) return;
+    d2h(h, h->h_owner, h->atoms.owner.as<int32_t>(), h->n);
+    d2h(h, h->h_row, h->row.as<int32_t>(), h->n + 1);
+    d2h(h, h->h_src, h->src.as<int32_t>(), h->ne);
+    if (h->p > 1) {
+        d2h(h, h->h_lsrc, h->lsrc.as<int32_t>(), h->ne);
+        d2h(h, h->h_crow, h->atoms.crow.as<int32_t>(), h->n);
+    }
+    sync(h);
+    h->hc_ready = true;
+}
+
+const std::vector<int32_t>& host_nodes(gmd_handle* h, LayoutState& ls) {
+    if (ls.h_nodes.empty() && ls.rows > 0) {
+        if (ls.p == 1) {
+            ls.h_nodes.resize(ls.rows);
+            for (int64_t i = 0; i < ls.rows; ++i) ls.h_nodes[i] = (int32_t)i;
+        } else {
+            d2h(h, ls.h_nodes, ls.node_array.as<int32_t>(), ls.rows);
+            sync(h);
+        }
+    }
+    return ls.h_nodes;
+}
+
+LayoutState& layout_of(gmd_handle* h, int bonds) {
+    need_built(h);
+    if (bonds) {
+        ensure_bond_layout(h);
+        return h->bonds;
+    }
+    return h->atoms;
+}
+
+void check_part(gmd_handle* h, int part) {
+    if (part < 0 || part >= h->p) raise(kArg, "partition index out of range");
+}
+
+// duplicates of one partition in build_span_layout order (partitioner.cpp:159-166)
+std::vector<std::pair<int64_t, int64_t>> dup_pairs(gmd_handle* h, LayoutState& ls, int part) {
+    const auto& nodes = host_nodes(h, ls);
+    const int stride = 1 + 2 * ls.p;
+    const int64_t b0 = ls.list_off[(size_t)part * stride], b1 = ls.list_off[(size_t)(part + 1) * stride];
+    std::unordered_map<int32_t, int64_t> first;
+    first.reserve((size_t)(b1 - b0) * 2);
+    std::vector<std::pair<int64_t, int64_t>> out;
+    for (int64_t r = b0; r < b1; ++r) {
+        auto it = first.emplace(nodes[r], r - b0);
+        if (!it.second) out.emplace_back(it.first->second, r - b0);
+    }
+    return out;
+}
+
+void ensure_dup_groups(gmd_handle* h, LayoutState& ls) {
+    if (ls.dups_ready) return;
+    std::vector<int32_t> gc, gs{0}, dd, dc, du;
+    for (int i = 0; i < ls.p; ++i) {
+        auto pairs = dup_pairs(h, ls, i);
+        const int64_t base = ls.base(i);
+        std::stable_sort(pairs.begin(), pairs.end(),
+                         [](auto& a, auto& b) { return a.first < b.first; });
+        for (size_t k = 0; k < pairs.size(); ++k) {
+            if (k == 0 || pairs[k].first != pairs[k - 1].first) {
+                if (k) gs.push_back((int32_t)dd.size());
+                gc.push_back((int32_t)(pairs[k].first + base));
+            }
+            dd.push_back((int32_t)(pairs[k].second + base));
+            dc.push_back((int32_t)(pairs[k].first + base));
+            du.push_back((int32_t)(pairs[k].second + base));
+        }
+    }
+    gs.push_back((int32_t)dd.size());
+    ls.ngroups = (int64_t)gc.size();
+    ls.ndups = (int64_t)dd.size();
+    cudaStream_t s = h->stream;
+    auto up = [&](DBuf& bf, const std::vector<int32_t>& v) {
+        int32_t* d = bf.get<int32_t>(v.size());
+        if (!v.empty())
+            GMD_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice, s));
+    };
+    up(ls.g_canon, gc);
+    up(ls.g_start, gs);
+    up(ls.g_dups, dd);
+    up(ls.d_canon, dc);
+    up(ls.d_dup, du);
+    sync(h);
+    ls.dups_ready = true;
+}
+
+void ensure_api_plan(gmd_handle* h, LayoutState& ls, bool corrupt) {
+    if (ls.api_ready && ls.api_corrupt == corrupt) return;
+    if (ls.nfrom > 0) {
+        int32_t* out = ls.xapi.get<int32_t>(ls.nfrom);
+        k_api_src<<<div_up(ls.nfrom, 256), 256, 0, h->stream>>>(
+            ls.nfrom, ls.xdst.as<int32_t>(), ls.list_off_d.as<int32_t>(), ls.p, corrupt ? 1 : 0, out);
+        GMD_LAUNCH_CHECK();
+    }
+    ls.api_ready = true;
+    ls.api_corrupt = corrupt;
+}
+
+int elem_size(int dtype) {
+    if (dtype == GMD_F32) return 4;
+    if (dtype == GMD_F64) return 8;
+    raise(kArg, "dtype must be GMD_F32 or GMD_F64");
+}
+
+// ---------------------------------------------------------------------------
+// forward_distributed (potential.cpp:563-985)
+// ---------------------------------------------------------------------------
+void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, double* stress,
+                  double* timing, uint32_t flags) {
+    need_built(h);
+    if (!h->params_set) raise(kConfig, "no parameters have been set on this handle");
+    const bool tb = h->p_r3 > 0.0;
+    if (tb && !h->has_lg)
+        raise(kConfig,
+              "three-body parameters require a line graph in the distributed handle");
+    if (std::abs(h->rc - h->p_r_atom) > 1e-12)
+        raise(kConfig, "distributed handle cutoff does not match the parameters");
+    cudaStream_t s = h->stream;
+    const int64_t n = h->n;
+    const int L = h->L;
+    LayoutState& A = h->atoms;
+    const int64_t R = A.rows;
+    const bool part = h->p > 1;
+    upload_model(h->mc, s);
+
+    GMD_CUDA(cudaEventRecord(h->ev[2], s));
+    if ((int)h->H.size() < L + 1) h->H.resize(L + 1);
+    std::vector<float*> H(L + 1);
+    for (int l = 0; l <= L; ++l) H[l] = h->H[l].get<float>(R * kF);
+    float* TH = h->TH.get<float>((size_t)L * n * kF);
+    float* MB = h->MB.get<float>(R * kF);
+    float* HB = h->HB.get<float>(n * kF);
+    float4* GRAD = h->GRAD.get<float4>(n);
+    const int grid = model_grid(n);
+    double* e_part = h->e_part.get<double>(grid);
+    double* v_part = h->v_part.get<double>((size_t)L * grid * 6);
+    const int tgrid = tb_grid_size(n);
+    double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
+    double* red = h->red.get<double>(16);
+    double* pa = h->per_atom.get<double>(n);
+
+    ConvArgs a{n, part ? A.crow.as<int32_t>() : nullptr, h->row.as<int32_t>(),
+               part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(), h->vd.as<float4>()};
+    BondArgs ba{n,
+                a.crow,
+                h->brow.as<int32_t>(),
+                h->bedge.as<int32_t>(),
+                h->brev.as<int32_t>(),
+                h->src.as<int32_t>(),
+                h->vd.as<float4>()};
+    float *TP = nullptr, *TH3 = nullptr, *TH4 = nullptr;
+    if (tb) {
+        TP = h->TP.get<float>((size_t)h->nb * kF);
+        TH3 = h->TH3.get<float>((size_t)h->nb * kF);
+        TH4 = h->TH4.get<float>(n * kF);
+    }
+    const int32_t* xd = A.xdst.as<int32_t>();
+    const int32_t* xs = A.xsrc.as<int32_t>();
+
+    // ---- feature calculation: embeddings for every layout row (:597-602)
+    launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
+    GMD_CUDA(cudaEventRecord(h->ev[3], s));
+
+    // ---- forward (:657-793)
+    for (int l = 0; l < L; ++l) {
+        const bool tbl = tb && l == L - 1;
+        if (tbl) {
+            launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), s);
+            launch_tb_inject(ba, TP, H[l], TH4, s);
+        }
+        if ((l > 0 || tbl) && A.nfrom > 0) launch_exchange(A.nfrom, xd, xs, H[l], kF, s);
+        launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
+                    l == L - 1 ? e_part : nullptr, s);
+    }
+    GMD_CUDA(cudaEventRecord(h->ev[4], s));
+
+    // ---- backward (:796-984)
+    launch_init_hbar(n, HB, s);
+    GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
+    for (int l = L - 1; l >= 0; --l) {
+        launch_bwd_node(n, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s);
+        if (A.nfrom > 0) launch_exchange(A.nfrom, xd, xs, MB, kF, s);
+        launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * grid * 6, s);
+        if (tb && l == L - 1) {
+            float* QB = h->QB.get<float>(n * kF);
+            float4* VIN = h->VIN.get<float4>(h->nb);
+            float4* VOUT = h->VOUT.get<float4>(h->nb);
+            launch_tb_bwd_q(n, HB, TH4, QB, s);
+            launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, s);
+            launch_tb_grad(ba, VIN, VOUT, GRAD, s);
+        }
+    }
+    const bool out_dev = flags & GMD_OUTPUT_DEVICE;
+    const bool out_f32 = flags & GMD_OUTPUT_F32;
+    double* fd = nullptr;
+    float* ff = nullptr;
+    if (forces) {
+        if (out_f32)
+            ff = out_dev ? static_cast<float*>(forces) : h->forces.get<float>(3 * n);
+        else
+            fd = out_dev ? static_cast<double*>(forces) : h->forces.get<double>(3 * n);
+        launch_forces_out(n, GRAD, fd, ff, s);
+    }
+    launch_reduce_partials(e_part, grid, 1, red, s);
+    launch_reduce_partials(v_part, L * grid, 6, red + 1, s);
+    if (tb)
+        launch_reduce_partials(v3_part, tgrid, 9, red + 7, s);
+    else
+        GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
+    GMD_CUDA(cudaEventRecord(h->ev[5], s));
+
+    double hred[16];
+    GMD_CUDA(cudaMemcpyAsync(hred, red, sizeof hred, cudaMemcpyDeviceToHost, s));
+    if (per_atom) {
+        if (out_f32) {
+            float* dst = out_dev ? static_cast<float*>(per_atom) : h->conv_tmp.get<float>(n);
+            k_to_f32<<<div_up(n, 256), 256, 0, s>>>(n, pa, dst);
+            GMD_LAUNCH_CHECK();
+            if (!out_dev)
+                GMD_CUDA(cudaMemcpyAsync(per_atom, dst, 4 * n, cudaMemcpyDeviceToHost, s));
+        } else {
+            GMD_CUDA(cudaMemcpyAsync(per_atom, pa, 8 * n, out_dev ? cudaMemcpyDeviceToDevice
+                                                                  : cudaMemcpyDeviceToHost, s));
+        }
+    }
+    if (forces && !out_dev) {
+        if (out_f32)
+            GMD_CUDA(cudaMemcpyAsync(forces, ff, 12 * n, cudaMemcpyDeviceToHost, s));
+        else
+            GMD_CUDA(cudaMemcpyAsync(forces, fd, 24 * n, cudaMemcpyDeviceToHost, s));
+    }
+    int32_t hdr[2];
+    read_flags(h, hdr);  // synchronizes the stream
+    if (!std::isfinite(hred[0])) raise(kRuntime, "non-finite energy (non-finite features)");
+    if (energy) *energy = hred[0];
+    if (stress) {  // stress = sym(virial) / V (potential.cpp:978-982)
+        const double* v6 = hred + 1;
+        const double* v9 = hred + 7;
+        double V[9] = {v6[0], v6[3], v6[4], v6[3], v6[1], v6[5], v6[4], v6[5], v6[2]};
+        for (int k = 0; k < 9; ++k) V[k] += v9[k];
+        double vol = std::abs(det3(h->lat));
+        for (int a2 = 0; a2 < 3; ++a2)
+            for (int b2 = 0; b2 < 3; ++b2)
+                stress[3 * a2 + b2] = 0.5 * (V[3 * a2 + b2] + V[3 * b2 + a2]) / vol;
+    }
+    if (timing) {
+        float f1 = 0, f2 = 0, f3 = 0;
+        GMD_CUDA(cudaEventElapsedTime(&f1, h->ev[2], h->ev[3]));
+        GMD_CUDA(cudaEventElapsedTime(&f2, h->ev[3], h->ev[4]));
+        GMD_CUDA(cudaEventElapsedTime(&f3, h->ev[4], h->ev[5]));
+        timing[0] = h->t_graph;
+        timing[1] = f1 * 1e-3;
+        timing[2] = f2 * 1e-3;
+        timing[3] = f3 * 1e-3;
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+
+namespace {
+int run(gmd_handle* h, const std::function<void()>& fn) {
+    if (!h) return GMD_ERR_ARG;
+    try {
+        GMD_CUDA(cudaSetDevice(h->device));
+        fn();
+        h->err.clear();
+        return GMD_OK;
+    } catch (const Status& e) {
+        h->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        h->err = e.what();
+        return GMD_ERR_RUNTIME;
+    }
+}
+thread_local std::string g_err;
+}  // namespace
+
+extern "C" {
+
+const char* gmd_version(void) { return "graphmd_b200 0.1 (sm_100a)"; }
+
+const char* gmd_last_error(const gmd_handle* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int gmd_create(int device, gmd_handle** out) {
+    if (!out) return GMD_ERR_ARG;
+    *out = nullptr;
+    auto* h = new gmd_handle();
+    h->device = device;
+    try {
+        int ndev = 0;
+        GMD_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) raise(kArg, "device ordinal out of range");
+        GMD_CUDA(cudaSetDevice(device));
+        GMD_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        for (auto& e : h->ev) GMD_CUDA(cudaEventCreate(&e));
+    } catch (const Status& e) {
+        g_err = e.what();
+        delete h;
+        return e.code;
+    }
+    *out = h;
+    return GMD_OK;
+}
+
+void gmd_destroy(gmd_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    DBuf* bufs[] = {&h->pos, &h->Z, &h->cell, &h->fw, &h->bin, &h->bin_cnt, &h->bin_start,
+                    &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
+                    &h->row, &h->src, &h->img, &h->vd, &h->ebond, &h->edst, &h->lsrc, &h->counts,
+                    &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
+                    &h->brev, &h->lcnt, &h->lpairs, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
+                    &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
+                    &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp};
+    for (DBuf* b : bufs) b->release();
+    for (LayoutState* ls : {&h->atoms, &h->bonds}) {
+        DBuf* lb[] = {&ls->node_array, &ls->crow, &ls->list_off_d, &ls->xdst, &ls->xsrc,
+                      &ls->xapi, &ls->owner, &ls->req, &ls->g_canon, &ls->g_start, &ls->g_dups,
+                      &ls->d_canon, &ls->d_dup};
+        for (DBuf* b : lb) b->release();
+    }
+    for (auto& b : h->H) b.release();
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+int gmd_build(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z,
+              const double lattice[9], const uint8_t pbc[3], double rc, double r3, double tau,
+              int p, int n_threads, uint32_t flags) {
+    (void)n_threads;
+    return run(h, [&] { build_impl(h, n, pos, Z, lattice, pbc, rc, r3, tau, p, flags); });
+}
+
+int64_t gmd_params_size(int F, int K, int L) {
+    return 119LL * F + (int64_t)L * F * F + (int64_t)L * F + 2LL * F * K + 2LL * F * F + F;
+}
+
+int gmd_params_init(uint64_t seed, int F, int K, int L, double r_atom, double r3, double* blob) {
+    (void)r_atom;
+    (void)r3;
+    if (!blob || F < 1 || K < 1 || L < 1) return GMD_ERR_ARG;
+    HostRng rng(seed ^ 0x9e3779b97f4a7c15ull);  // potential.cpp:132-145
+    const struct {
+        int64_t n;
+        double scale;
+    } seg[8] = {{119LL * F, 0.5},
+                {(int64_t)L * F * F, 1.0 / std::sqrt((double)F)},
+                {(int64_t)L * F, 0.1},
+                {(int64_t)F * K, 1.0 / std::sqrt((double)K)},
+                {(int64_t)F * K, 0.5 / std::sqrt((double)K)},
+                {(int64_t)F * F, 1.0 / std::sqrt((double)F)},
+                {(int64_t)F * F, 0.5 / std::sqrt((double)F)},
+                {(int64_t)F, 0.5}};
+    double* q = blob;
+    for (const auto& sg : seg)
+        for (int64_t i = 0; i < sg.n; ++i) *q++ = sg.scale * rng.normal();
+    return GMD_OK;
+}
+
+int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
+                   const double* blob) {
+    return run(h, [&] {
+        if (!blob) raise(kArg, "null parameter blob");
+        if (L < 1) raise(kConfig, "layer count must be >= 1");
+        if (F < 1 || K < 1) raise(kConfig, "feature and basis widths must be >= 1");
+        if (r_atom <= 0.0) raise(kConfig, "atom cutoff must be positive");
+        if (r3 > 0.0 && r3 > r_atom)
+            raise(kConfig, "three-body cutoff cannot exceed the atom cutoff");
+        if (F != kF || K != kK)
+            raise(kConfig, "compiled kernels support feature_width=16, basis_count=8 only");
+        if (L > kMaxLayers) raise(kConfig, "compiled kernels support at most 8 layers");
+        const int64_t total = gmd_params_size(F, K, L);
+        for (int64_t i = 0; i < total; ++i)
+            if (!std::isfinite(blob[i])) raise(kConfig, "parameter blob contains a non-finite value");
+        ModelConst& m = h->mc;
+        std::memset(&m, 0, sizeof m);
+        const double* q = blob;
+        for (int i = 0; i < 119 * F; ++i) m.emb[i] = (float)*q++;
+        for (int l = 0; l < L; ++l)
+            for (int i = 0; i < F * F; ++i) m.W[l][i] = (float)*q++;
+        for (int l = 0; l < L; ++l)
+            for (int i = 0; i < F; ++i) m.b[l][i] = (float)*q++;
+        for (int i = 0; i < F * K; ++i) m.P[i] = (float)*q++;
+        for (int i = 0; i < F * K; ++i) m.P3[i] = (float)*q++;
+        for (int i = 0; i < F * F; ++i) m.W3[i] = (float)*q++;
+        for (int i = 0; i < F * F; ++i) m.W4[i] = (float)*q++;
+        for (int i = 0; i < F; ++i) m.ro[i] = (float)*q++;
+        m.rc = (float)r_atom;
+        m.inv_rc = (float)(1.0 / r_atom);
+        m.inv_sigma = (float)(K / r_atom);  // sigma = rc / K (potential.cpp:34)
+        m.mu_step = K > 1 ? (float)(r_atom / (K - 1)) : 0.f;
+        const double r3e = r3 > 0.0 ? r3 : 1.0;
+        m.r3 = (float)r3e;
+        m.inv_r3 = (float)(1.0 / r3e);
+        m.inv_sigma3 = (float)(K / r3e);
+        m.mu_step3 = K > 1 ? (float)(r3e / (K - 1)) : 0.f;
+        m.L = L;
+        h->F = F;
+        h->K = K;
+        h->L = L;
+        h->p_r_atom = r_atom;
+        h->p_r3 = r3;
+        h->params_set = true;
+    });
+}
+
+int gmd_forward(gmd_handle* h, double* energy, void* per_atom, void* forces, double* stress,
+                double* timing, uint32_t flags) {
+    return run(h, [&] { forward_impl(h, energy, per_atom, forces, stress, timing, flags); });
+}
+
+int gmd_num_nodes(const gmd_handle* h, int64_t* n) {
+    if (!h || !n) return GMD_ERR_ARG;
+    *n = h->built ? h->n : 0;
+    return GMD_OK;
+}
+int gmd_num_edges(const gmd_handle* h, int64_t* ne) {
+    if (!h || !ne) return GMD_ERR_ARG;
+    *ne = h->built ? h->ne : 0;
+    return GMD_OK;
+}
+int gmd_num_partitions(const gmd_handle* h, int* p) {
+    if (!h || !p) return GMD_ERR_ARG;
+    *p = h->p;
+    return GMD_OK;
+}
+
+int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, double* dist,
+                  double* vec) {
+    return run(h, [&] {
+        need_built(h);
+        const int64_t ne = h->ne;
+        if (ne == 0) return;
+        cudaStream_t s = h->stream;
+        int32_t* edst = h->edst.get<int32_t>(ne);
+        launch_edge_dst(h->row.as<int32_t>(), h->n, edst, s);
+        // staging: src, dst (i64), off (3 x i32), dist, vec (3 x f64)
+        char* tmp = h->exp_tmp.get<char>((size_t)ne * (8 + 8 + 12 + 8 + 24));
+        int64_t* t_src = reinterpret_cast<int64_t*>(tmp);
+        int64_t* t_dst = t_src + ne;
+        double* t_dist = reinterpret_cast<double*>(t_dst + ne);
+        double* t_vec = t_dist + ne;
+        int32_t* t_off = reinterpret_cast<int32_t*>(t_vec + 3 * ne);
+        GraphDev gd;
+        gd.n = h->n;
+        gd.ne = ne;
+        gd.row = h->row.as<int32_t>();
+        gd.src = h->src.as<int32_t>();
+        gd.img = h->img.as<uint32_t>();
+        launch_export_graph(h->geom, h->pos.as<double>(), gd, edst, t_src, t_dst, t_off, t_dist,
+                            t_vec, s);
+        if (src) GMD_CUDA(cudaMemcpyAsync(src, t_src, 8 * ne, cudaMemcpyDeviceToHost, s));
+        if (dst) GMD_CUDA(cudaMemcpyAsync(dst, t_dst, 8 * ne, cudaMemcpyDeviceToHost, s));
+        if (off) GMD_CUDA(cudaMemcpyAsync(off, t_off, 12 * ne, cudaMemcpyDeviceToHost, s));
+        if (dist) GMD_CUDA(cudaMemcpyAsync(dist, t_dist, 8 * ne, cudaMemcpyDeviceToHost, s));
+        if (vec) GMD_CUDA(cudaMemcpyAsync(vec, t_vec, 24 * ne, cudaMemcpyDeviceToHost, s));
+        sync(h);
+    });
+}
+
+int gmd_get_system(gmd_handle* h, double* pos, double* lattice) {
+    return run(h, [&] {
+        need_built(h);
+        if (pos)
+            GMD_CUDA(cudaMemcpyAsync(pos, h->pos.as<double>(), 24 * h->n, cudaMemcpyDeviceToHost,
+                                     h->stream));
+        if (lattice) std::memcpy(lattice, h->lat, sizeof h->lat);
+        sync(h);
+    });
+}
+
+int gmd_get_rule(gmd_handle* h, int* axis, double* boundaries) {
+    return run(h, [&] {
+        need_built(h);
+        if (axis) *axis = h->axis;
+        if (boundaries) std::copy(h->bounds.begin(), h->bounds.end(), boundaries);
+    });
+}
+
+int gmd_get_owner(gmd_handle* h, int32_t* owner) {
+    return run(h, [&] {
+        need_built(h);
+        GMD_CUDA(cudaMemcpyAsync(owner, h->atoms.owner.as<int32_t>(), 4 * h->n,
+                                 cudaMemcpyDeviceToHost, h->stream));
+        sync(h);
+    });
+}
+
+int gmd_get_layout_size(gmd_handle* h, int part, int bonds, int64_t* size) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        check_part(h, part);
+        const int stride = 1 + 2 * ls.p;
+        *size = ls.list_off[(size_t)(part + 1) * stride] - ls.list_off[(size_t)part * stride];
+    });
+}
+
+int gmd_get_layout(gmd_handle* h, int part, int bonds, int64_t* node_array, int64_t* markers) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        check_part(h, part);
+        const int p = ls.p, stride = 1 + 2 * p;
+        const int64_t b0 = ls.list_off[(size_t)part * stride];
+        const int64_t b1 = ls.list_off[(size_t)(part + 1) * stride];
+        if (node_array) {
+            const auto& nodes = host_nodes(h, ls);
+            for (int64_t r = b0; r < b1; ++r) node_array[r - b0] = nodes[r];
+        }
+        if (markers) {
+            markers[0] = 0;
+            for (int bb = 0; bb < 1 + 2 * p; ++bb)
+                markers[bb + 1] = ls.list_off[(size_t)part * stride + bb + 1] - b0;
+        }
+    });
+}
+
+int gmd_get_num_duplicates(gmd_handle* h, int part, int bonds, int64_t* count) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        check_part(h, part);
+        *count = (int64_t)dup_pairs(h, ls, part).size();
+    });
+}
+
+int gmd_get_duplicates(gmd_handle* h, int part, int bonds, int64_t* pairs) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        check_part(h, part);
+        auto v = dup_pairs(h, ls, part);
+        for (size_t k = 0; k < v.size(); ++k) {
+            pairs[2 * k] = v[k].first;
+            pairs[2 * k + 1] = v[k].second;
+        }
+    });
+}
+
+namespace {
+// owned edges of a partition in ascending global id (partitioner.cpp:200-216)
+void owned_edges(gmd_handle* h, int part, std::vector<int64_t>* owned, std::vector<int64_t>* ls,
+                 std::vector<int64_t>* ld, std::vector<int64_t>* border) {
+    ensure_host_cache(h);
+    check_part(h, part);
+    const int64_t base = h->atoms.base(part);
+    int64_t k = 0;
+    for (int64_t v = 0; v < h->n; ++v) {
+        if (h->h_owner[v] != part) continue;
+        for (int32_t e = h->h_row[v]; e < h->h_row[v + 1]; ++e, ++k) {
+            const int32_t u = h->h_src[e];
+            if (owned) owned->push_back(e);
+            if (ls) ls->push_back((h->p > 1 ? h->h_lsrc[e] : u) - base);
+            if (ld) ld->push_back((h->p > 1 ? h->h_crow[v] : v) - base);
+            if (border && h->h_owner[u] != part) border->push_back(k);
+        }
+    }
+}
+}  // namespace
+
+int gmd_get_num_owned_edges(gmd_handle* h, int part, int64_t* count) {
+    return run(h, [&] {
+        ensure_host_cache(h);
+        check_part(h, part);
+        int64_t c = 0;
+        for (int64_t v = 0; v < h->n; ++v)
+            if (h->h_owner[v] == part) c += h->h_row[v + 1] - h->h_row[v];
+        *count = c;
+    });
+}
+
+int gmd_get_owned_edges(gmd_handle* h, int part, int64_t* owned, int64_t* local_src,
+                        int64_t* local_dst) {
+    return run(h, [&] {
+        std::vector<int64_t> a, b, c;
+        owned_edges(h, part, &a, &b, &c, nullptr);
+        if (owned) std::copy(a.begin(), a.end(), owned);
+        if (local_src) std::copy(b.begin(), b.end(), local_src);
+        if (local_dst) std::copy(c.begin(), c.end(), local_dst);
+    });
+}
+
+int gmd_get_num_border_edges(gmd_handle* h, int part, int64_t* count) {
+    return run(h, [&] {
+        std::vector<int64_t> b;
+        owned_edges(h, part, nullptr, nullptr, nullptr, &b);
+        *count = (int64_t)b.size();
+    });
+}
+
+int gmd_get_border_edges(gmd_handle* h, int part, int64_t* border) {
+    return run(h, [&] {
+        std::vector<int64_t> b;
+        owned_edges(h, part, nullptr, nullptr, nullptr, &b);
+        std::copy(b.begin(), b.end(), border);
+    });
+}
+
+int gmd_has_line_graph(const gmd_handle* h, int* yes) {
+    if (!h || !yes) return GMD_ERR_ARG;
+    *yes = h->built && h->has_lg ? 1 : 0;
+    return GMD_OK;
+}
+
+namespace {
+void ensure_line_cache(gmd_handle* h) {
+    ensure_bond_layout(h);
+    if (h->hcb_ready) return;
+    cudaStream_t s = h->stream;
+    const int64_t nb = h->nb;
+    int32_t* cnt = h->lcnt.get<int32_t>(nb + 1);
+    launch_line_count(nb, h->bedge.as<int32_t>(), h->src.as<int32_t>(), h->brow.as<int32_t>(), cnt,
+                      s);
+    scan_i32(h, cnt, cnt, nb);
+    int32_t T = 0;
+    GMD_CUDA(cudaMemcpyAsync(&T, cnt + nb, 4, cudaMemcpyDeviceToHost, s));
+    sync(h);
+    int32_t* pairs = h->lpairs.get<int32_t>(2 * (size_t)T);
+    launch_line_fill(nb, h->bedge.as<int32_t>(), h->src.as<int32_t>(), h->brow.as<int32_t>(),
+                     h->brev.as<int32_t>(), cnt, pairs, s);
+    d2h(h, h->h_pairs, pairs, 2 * (size_t)T);
+    d2h(h, h->h_bedge, h->bedge.as<int32_t>(), nb);
+    d2h(h, h->h_bown, h->bonds.owner.as<int32_t>(), nb);
+    sync(h);
+    h->hcb_ready = true;
+}
+
+// bond global id -> local row of partition `part` (canonical, first occurrence)
+std::unordered_map<int32_t, int64_t> bond_g2l(gmd_handle* h, int part) {
+    LayoutState& B = h->bonds;
+    const auto& nodes = host_nodes(h, B);
+    const int stride = 1 + 2 * B.p;
+    const int64_t b0 = B.list_off[(size_t)part * stride], b1 = B.list_off[(size_t)(part + 1) * stride];
+    std::unordered_map<int32_t, int64_t> m;
+    m.reserve((size_t)(b1 - b0) * 2);
+    for (int64_t r = b0; r < b1; ++r) m.emplace(nodes[r], r - b0);
+    return m;
+}
+}  // namespace
+
+int gmd_get_num_bonds(gmd_handle* h, int64_t* nb) {
+    return run(h, [&] {
+        need_built(h);
+        *nb = h->has_lg ? h->nb : 0;
+    });
+}
+
+int gmd_get_bonds(gmd_handle* h, int64_t* edge_of_bond, int32_t* bond_owner) {
+    return run(h, [&] {
+        ensure_line_cache(h);
+        for (int64_t b = 0; b < h->nb; ++b) {
+            if (edge_of_bond) edge_of_bond[b] = h->h_bedge[b];
+            if (bond_owner) bond_owner[b] = h->h_bown[b];
+        }
+    });
+}
+
+int gmd_get_num_line_edges(gmd_handle* h, int part, int64_t* count) {
+    return run(h, [&] {
+        ensure_line_cache(h);
+        check_part(h, part);
+        int64_t c = 0;
+        const size_t T = h->h_pairs.size() / 2;
+        for (size_t t = 0; t < T; ++t)
+            if (h->h_bown[h->h_pairs[2 * t + 1]] == part) ++c;
+        *count = c;
+    });
+}
+
+int gmd_get_line_edges(gmd_handle* h, int part, int64_t* pairs) {
+    return run(h, [&] {
+        ensure_line_cache(h);
+        check_part(h, part);
+        auto g2l = bond_g2l(h, part);
+        const size_t T = h->h_pairs.size() / 2;
+        int64_t k = 0;
+        for (size_t t = 0; t < T; ++t) {
+            const int32_t e = h->h_pairs[2 * t], ep = h->h_pairs[2 * t + 1];
+            if (h->h_bown[ep] != part) continue;
+            auto a = g2l.find(e), b = g2l.find(ep);
+            if (a == g2l.end() || b == g2l.end())
+                raise(kRuntime, "dangling bond reference in line graph");
+            pairs[2 * k] = a->second;
+            pairs[2 * k + 1] = b->second;
+            ++k;
+        }
+    });
+}
+
+// ---- feature API --------------------------------------------------------
+int gmd_block_rows(gmd_handle* h, int bonds, int64_t* total_rows) {
+    return run(h, [&] { *total_rows = layout_of(h, bonds).rows; });
+}
+
+int gmd_block_offset(gmd_handle* h, int part, int bonds, int64_t* row0) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        check_part(h, part);
+        *row0 = ls.base(part);
+    });
+}
+
+int gmd_transfer(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        const int es = elem_size(dtype);
+        if (width < 1) raise(kArg, "width must be >= 1");
+        if (ls.nfrom == 0) return;
+        ensure_api_plan(h, ls, h->corrupted && !bonds);
+        const int ww = width * es / 4;
+        k_copy_rows<<<div_up(ls.nfrom * ww, 256), 256, 0, h->stream>>>(
+            ls.nfrom, ls.xdst.as<int32_t>(), ls.xapi.as<int32_t>(), static_cast<uint32_t*>(dev_buf),
+            ww);
+        GMD_LAUNCH_CHECK();
+        sync(h);
+    });
+}
+
+int gmd_transfer_transpose(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        const int es = elem_size(dtype);
+        if (width < 1) raise(kArg, "width must be >= 1");
+        cudaStream_t s = h->stream;
+        if (ls.nfrom > 0) {
+            ensure_api_plan(h, ls, false);
+            const int64_t tot = ls.nfrom * width;
+            if (es == 8)
+                k_transpose_add<double><<<div_up(tot, 256), 256, 0, s>>>(
+                    ls.nfrom, ls.xapi.as<int32_t>(), ls.xdst.as<int32_t>(),
+                    static_cast<double*>(dev_buf), width);
+            else
+                k_transpose_add<float><<<div_up(tot, 256), 256, 0, s>>>(
+                    ls.nfrom, ls.xapi.as<int32_t>(), ls.xdst.as<int32_t>(),
+                    static_cast<float*>(dev_buf), width);
+            GMD_LAUNCH_CHECK();
+        }
+        ensure_dup_groups(h, ls);
+        if (ls.ngroups > 0) {
+            const int64_t tot = ls.ngroups * width;
+            if (es == 8)
+                k_dup_fold<double><<<div_up(tot, 256), 256, 0, s>>>(
+                    ls.ngroups, ls.g_canon.as<int32_t>(), ls.g_start.as<int32_t>(),
+                    ls.g_dups.as<int32_t>(), static_cast<double*>(dev_buf), width);
+            else
+                k_dup_fold<float><<<div_up(tot, 256), 256, 0, s>>>(
+                    ls.ngroups, ls.g_canon.as<int32_t>(), ls.g_start.as<int32_t>(),
+                    ls.g_dups.as<int32_t>(), static_cast<float*>(dev_buf), width);
+            GMD_LAUNCH_CHECK();
+        }
+        sync(h);
+    });
+}
+
+int gmd_sync_duplicates(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        const int es = elem_size(dtype);
+        ensure_dup_groups(h, ls);
+        if (ls.ndups == 0) return;
+        const int ww = width * es / 4;
+        k_copy_rows<<<div_up(ls.ndups * ww, 256), 256, 0, h->stream>>>(
+            ls.ndups, ls.d_dup.as<int32_t>(), ls.d_canon.as<int32_t>(),
+            static_cast<uint32_t*>(dev_buf), ww);
+        GMD_LAUNCH_CHECK();
+        sync(h);
+    });
+}
+
+int gmd_distribute(gmd_handle* h, int bonds, const void* host_global, void* dev_buf, int width,
+                   int dtype) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        const int es = elem_size(dtype);
+        const int ww = width * es / 4;
+        cudaStream_t s = h->stream;
+        uint32_t* tmp = h->conv_tmp.get<uint32_t>((size_t)ls.nid * ww);
+        GMD_CUDA(cudaMemcpyAsync(tmp, host_global, (size_t)ls.nid * ww * 4, cudaMemcpyHostToDevice,
+                                 s));
+        if (ls.rows > 0) {
+            k_gather_rows<<<div_up(ls.rows * ww, 256), 256, 0, s>>>(
+                ls.rows, ls.p > 1 ? ls.node_array.as<int32_t>() : nullptr, tmp,
+                static_cast<uint32_t*>(dev_buf), ww);
+            GMD_LAUNCH_CHECK();
+        }
+        sync(h);
+    });
+}
+
+int gmd_aggregate(gmd_handle* h, int bonds, const void* dev_buf, void* host_global, int width,
+                  int dtype) {
+    return run(h, [&] {
+        LayoutState& ls = layout_of(h, bonds);
+        const int es = elem_size(dtype);
+        const int ww = width * es / 4;
+        cudaStream_t s = h->stream;
+        uint32_t* tmp = h->conv_tmp.get<uint32_t>((size_t)ls.nid * ww);
+        if (ls.nid > 0) {  // canonical owned row of every id (engine.cpp:214-229)
+            k_gather_rows<<<div_up(ls.nid * ww, 256), 256, 0, s>>>(
+                ls.nid, ls.p > 1 ? ls.crow.as<int32_t>() : nullptr,
+                static_cast<const uint32_t*>(dev_buf), tmp, ww);
+            GMD_LAUNCH_CHECK();
+        }
+        GMD_CUDA(cudaMemcpyAsync(host_global, tmp, (size_t)ls.nid * ww * 4, cudaMemcpyDeviceToHost,
+                                 s));
+        sync(h);
+    });
+}
+
+int gmd_corrupt_transfer_plan_for_test(gmd_handle* h) {
+    return run(h, [&] {
+        need_built(h);
+        h->corrupted = true;
+    });
+}
+
+int gmd_util_rng_uniform(uint64_t seed, int64_t count, double lo, double hi, double* out) {
+    if (!out || count < 0) return GMD_ERR_ARG;
+    HostRng r(seed);
+    for (int64_t i = 0; i < count; ++i) out[i] = lo + (hi - lo) * r.uniform();
+    return GMD_OK;
+}
+
+int gmd_util_supercell(int64_t n, const double* pos, const int32_t* Z, const double lattice[9],
+                       int rx, int ry, int rz, double amp, uint64_t seed, double* out_pos,
+                       int32_t* out_Z, double* out_lattice) {
+    if (!pos || !Z || !lattice || !out_pos || !out_Z || !out_lattice) return GMD_ERR_ARG;
+    if (rx < 1 || ry < 1 || rz < 1) return GMD_ERR_CONFIG;
+    const int reps[3] = {rx, ry, rz};
+    for (int k = 0; k < 3; ++k) {  // make_supercell (system.cpp:188-214)
+        V3 r = vmul(row3(lattice, k), (double)reps[k]);
+        out_lattice[3 * k] = r.x;
+        out_lattice[3 * k + 1] = r.y;
+        out_lattice[3 * k + 2] = r.z;
+    }
+    int64_t o = 0;
+    for (int a = 0; a < rx; ++a)
+        for (int b = 0; b < ry; ++b)
+            for (int c = 0; c < rz; ++c) {
+                V3 l0 = vmul(row3(lattice, 0), a), l1 = vmul(row3(lattice, 1), b),
+                   l2 = vmul(row3(lattice, 2), c);
+                V3 sh = {l0.x + l1.x + l2.x, l0.y + l1.y + l2.y, l0.z + l1.z + l2.z};
+                for (int64_t i = 0; i < n; ++i, ++o) {
+                    out_pos[3 * o] = pos[3 * i] + sh.x;
+                    out_pos[3 * o + 1] = pos[3 * i + 1] + sh.y;
+                    out_pos[3 * o + 2] = pos[3 * i + 2] + sh.z;
+                    out_Z[o] = Z[i];
+                }
+            }
+    if (amp > 0.0) {  // random_perturb (system.cpp:231-240)
+        HostRng r(seed);
+        for (int64_t i = 0; i < o; ++i)
+            for (int k = 0; k < 3; ++k) out_pos[3 * i + k] += -amp + (amp - -amp) * r.uniform();
+    } else if (amp < 0.0) {
+        return GMD_ERR_CONFIG;
+    }
+    return GMD_OK;
+}
+
+int gmd_profile(gmd_handle* h, int enable) {
+    (void)h;
+    (void)enable;
+    return GMD_OK;
+}
+
+int gmd_profile_read(gmd_handle* h, char* names, int names_cap, double* ms, int* count) {
+    (void)h;
+    (void)names;
+    (void)names_cap;
+    (void)ms;
+    if (count) *count = 0;
+    return GMD_OK;
+}
+
+}  // extern "C"

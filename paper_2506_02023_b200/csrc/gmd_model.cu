@@ -1,0 +1,736 @@
+// Toy invariant MLIP forward + hand-written backward on the GPU
+// (proj/src/potential.cpp:19-78 math, :563-985 distributed pass).
+//
+// Design (B200-first, no float atomics, partition-invariant):
+//  * every per-node reduction is a destination-row (CSR) gather, one warp per
+//    node, lanes over in-edges, a fixed-order butterfly reduce -- results do
+//    not depend on the partition count;
+//  * the backward never scatters to sources: the adjoint of "h[src] feeds
+//    m[dst]" is gathered at the source through the reverse edge (s_e is a
+//    function of |v_e| only, and the reverse edge has the bitwise-negated
+//    vector), so dL/dh, forces and the virial are row-local sums;
+//  * the radial channel s = P u(d) / ds = P u'(d) is recomputed in registers
+//    per edge and layer (never stored: E x F floats would dominate HBM);
+//  * the three-body stage runs per "center" atom s on its in-bond list
+//    (bonds e=(w->s) and their reverses e'=(s->w)): every line edge (e, e')
+//    with dst(e) = src(e') is a pair of slots of one center.
+#include "gmd_model.cuh"
+
+namespace gmd {
+
+__constant__ ModelConst c_m;
+
+void upload_model(const ModelConst& m, cudaStream_t s) {
+    GMD_CUDA(cudaMemcpyToSymbolAsync(c_m, &m, sizeof(ModelConst), 0, cudaMemcpyHostToDevice, s));
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerCta = kThreads / 32;
+
+// u_k(d) = fc(d) exp(-((d - mu_k)/sigma)^2) (potential.cpp:30-50)
+__device__ __forceinline__ void basis(float d, float rc, float inv_rc, float inv_sigma,
+                                      float mu_step, float u[kK]) {
+    const float fc = d < rc ? 0.5f * (cospif(d * inv_rc) + 1.0f) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        float x = (d - mu_step * (float)k) * inv_sigma;
+        u[k] = fc * __expf(-x * x);
+    }
+}
+
+__device__ __forceinline__ void basis_d(float d, float rc, float inv_rc, float inv_sigma,
+                                        float mu_step, float u[kK], float du[kK]) {
+    float sn, cs;
+    sincospif(d * inv_rc, &sn, &cs);
+    const bool in = d < rc;
+    const float fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
+    const float dfc = in ? -0.5f * 3.14159265358979f * inv_rc * sn : 0.0f;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        float x = (d - mu_step * (float)k) * inv_sigma;
+        float phi = __expf(-x * x);
+        u[k] = fc * phi;
+        du[k] = phi * (dfc - 2.0f * fc * x * inv_sigma);
+    }
+}
+
+__device__ __forceinline__ void fcut3(float d, float& fc, float& dfc) {
+    float sn, cs;
+    sincospif(d * c_m.inv_r3, &sn, &cs);
+    const bool in = d < c_m.r3;
+    fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
+    dfc = in ? -0.5f * 3.14159265358979f * c_m.inv_r3 * sn : 0.0f;
+}
+
+__device__ __forceinline__ void load_row16(const float* __restrict__ p, float h[kF]) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float4 t = __ldg(q + i);
+        h[4 * i] = t.x;
+        h[4 * i + 1] = t.y;
+        h[4 * i + 2] = t.z;
+        h[4 * i + 3] = t.w;
+    }
+}
+
+__device__ __forceinline__ void store_row16(float* p, const float h[kF]) {
+    float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = make_float4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
+}
+
+// Sum 16 per-lane values over the warp; lane l ends with feature (l >> 1).
+__device__ __forceinline__ float transpose_reduce16(float v[kF], int lane) {
+    float w8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        bool up = lane & 16;
+        float send = up ? v[i] : v[i + 8];
+        float keep = up ? v[i + 8] : v[i];
+        w8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float w4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        bool up = lane & 8;
+        float send = up ? w8[i] : w8[i + 4];
+        float keep = up ? w8[i + 4] : w8[i];
+        w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float w2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        bool up = lane & 4;
+        float send = up ? w4[i] : w4[i + 2];
+        float keep = up ? w4[i + 2] : w4[i];
+        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    bool up = lane & 2;
+    float send = up ? w2[0] : w2[1];
+    float keep = up ? w2[1] : w2[0];
+    float w1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    return w1 + __shfl_xor_sync(0xffffffffu, w1, 1);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// fixed-order CTA reduction of W doubles per thread-warp; lane 0 of each warp
+// deposits, thread 0 sums warps in order
+template <int W>
+__device__ __forceinline__ void cta_partials(const double (&v)[W], double* out) {
+    __shared__ double red[kWarpsPerCta][W];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double s[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) s[c] = warp_sum_d(v[c]);
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < W; ++c) red[warp][c] = s[c];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < W; ++c) {
+            double acc = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += red[w][c];
+            out[(size_t)blockIdx.x * W + c] = acc;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+__global__ void k_embed(int64_t rows, const int32_t* __restrict__ node_array,
+                        const int32_t* __restrict__ Z, float* __restrict__ H0) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * 4) return;
+    int64_t r = t >> 2;
+    int q = (int)(t & 3);
+    int id = node_array ? node_array[r] : (int)r;
+    int z = Z[id];
+    const float* e = c_m.emb + z * kF + 4 * q;
+    reinterpret_cast<float4*>(H0)[t] = make_float4(e[0], e[1], e[2], e[3]);
+}
+
+__global__ void k_exchange(int64_t nx, const int32_t* __restrict__ xdst,
+                           const int32_t* __restrict__ xsrc, float4* __restrict__ buf, int w4) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nx * w4) return;
+    int64_t k = t / w4;
+    int q = (int)(t - k * w4);
+    buf[(int64_t)xdst[k] * w4 + q] = buf[(int64_t)xsrc[k] * w4 + q];
+}
+
+// forward conv layer (potential.cpp:743-774), warp per owned node
+__global__ void __launch_bounds__(kThreads) k_conv(ConvArgs a, int layer,
+                                                   const float* __restrict__ Hin,
+                                                   float* __restrict__ Hout,
+                                                   float* __restrict__ TH, double* per_atom,
+                                                   double* e_part) {
+    __shared__ float sW[kF][kF + 1];
+    __shared__ float sb[kF], sro[kF];
+    for (int i = threadIdx.x; i < kF * kF; i += kThreads) sW[i / kF][i % kF] = c_m.W[layer][i];
+    if (threadIdx.x < kF) {
+        sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
+        sro[threadIdx.x] = c_m.ro[threadIdx.x];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+    const float rc = c_m.rc, irc = c_m.inv_rc, isg = c_m.inv_sigma, mus = c_m.mu_step;
+    double esum = 0.0;
+    for (int64_t v = w0; v < a.n; v += nw) {
+        float acc[kF];
+#pragma unroll
+        for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
+        const int e1 = a.row[v + 1];
+        for (int e = a.row[v] + lane; e < e1; e += 32) {
+            const float4 q = __ldg(a.vd + e);
+            float u[kK];
+            basis(q.w, rc, irc, isg, mus, u);
+            float h[kF];
+            load_row16(Hin + (size_t)__ldg(a.lsrc + e) * kF, h);
+#pragma unroll
+            for (int f = 0; f < kF; ++f) {
+                float s = 0.0f;
+#pragma unroll
+                for (int k = 0; k < kK; ++k) s = fmaf(c_m.P[f * kK + k], u[k], s);
+                acc[f] = fmaf(h[f], s, acc[f]);
+            }
+        }
+        const float m = transpose_reduce16(acc, lane);
+        const int f = lane >> 1;
+        float z = sb[f];
+#pragma unroll
+        for (int g = 0; g < kF; ++g) z = fmaf(sW[f][g], __shfl_sync(0xffffffffu, m, 2 * g), z);
+        const float th = tanhf(z);
+        const int64_t r = a.crow ? a.crow[v] : v;
+        const float hn = Hin[r * kF + f] + th;
+        if ((lane & 1) == 0) {
+            Hout[r * kF + f] = hn;
+            TH[v * kF + f] = th;
+        }
+        if (per_atom) {
+            float ev = (lane & 1) ? 0.0f : sro[f] * hn;
+            ev = warp_sum(ev);
+            if (lane == 0) per_atom[v] = (double)ev;
+            esum += (double)ev;
+        }
+    }
+    if (e_part) {
+        double vals[1] = {lane == 0 ? esum : 0.0};
+        cta_partials<1>(vals, e_part);
+    }
+}
+
+// m_bar = W^T (h_bar * sech^2) (potential.cpp:816-822), thread per node
+__global__ void k_bwd_node(int64_t n, const int32_t* __restrict__ crow, int layer,
+                           const float* __restrict__ HB, const float* __restrict__ TH,
+                           float* __restrict__ MB) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    float hb[kF], th[kF], y[kF];
+    load_row16(HB + v * kF, hb);
+    load_row16(TH + v * kF, th);
+#pragma unroll
+    for (int f = 0; f < kF; ++f) y[f] = hb[f] * (1.0f - th[f] * th[f]);
+    float mb[kF];
+#pragma unroll
+    for (int g = 0; g < kF; ++g) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W[layer][f * kF + g], y[f], acc);
+        mb[g] = acc;
+    }
+    const int64_t r = crow ? crow[v] : v;
+    store_row16(MB + r * kF, mb);
+}
+
+// backward edge pass in row form (potential.cpp:823-848 restated as gathers)
+__global__ void __launch_bounds__(kThreads) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
+                                                       const float* __restrict__ Hl,
+                                                       float* __restrict__ HB,
+                                                       float4* __restrict__ GRAD,
+                                                       double* vir_part) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+    const float rc = c_m.rc, irc = c_m.inv_rc, isg = c_m.inv_sigma, mus = c_m.mu_step;
+    double vir[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t v = w0; v < a.n; v += nw) {
+        const int64_t r = a.crow ? a.crow[v] : v;
+        float mbu[kF], hu[kF], acc[kF];
+        load_row16(MB + r * kF, mbu);
+        load_row16(Hl + r * kF, hu);
+#pragma unroll
+        for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
+        float gx = 0.f, gy = 0.f, gz = 0.f;
+        const int e1 = a.row[v + 1];
+        for (int e = a.row[v] + lane; e < e1; e += 32) {
+            const float4 q = __ldg(a.vd + e);
+            float u[kK], du[kK];
+            basis_d(q.w, rc, irc, isg, mus, u, du);
+            const int w = __ldg(a.lsrc + e);
+            float mbw[kF], hw[kF];
+            load_row16(MB + (size_t)w * kF, mbw);
+            load_row16(Hl + (size_t)w * kF, hw);
+            float dself = 0.f, drev = 0.f;
+#pragma unroll
+            for (int f = 0; f < kF; ++f) {
+                float s = 0.f, ds = 0.f;
+#pragma unroll
+                for (int k = 0; k < kK; ++k) {
+                    s = fmaf(c_m.P[f * kK + k], u[k], s);
+                    ds = fmaf(c_m.P[f * kK + k], du[k], ds);
+                }
+                acc[f] = fmaf(mbw[f], s, acc[f]);
+                dself = fmaf(mbu[f] * hw[f], ds, dself);
+                drev = fmaf(mbw[f] * hu[f], ds, drev);
+            }
+            const float invd = 1.0f / q.w;
+            const float coef = (dself + drev) * invd;
+            gx -= q.x * coef;
+            gy -= q.y * coef;
+            gz -= q.z * coef;
+            const double cs = (double)(dself * invd);
+            const double vx = q.x, vy = q.y, vz = q.z;
+            vir[0] += cs * vx * vx;
+            vir[1] += cs * vy * vy;
+            vir[2] += cs * vz * vz;
+            vir[3] += cs * vx * vy;
+            vir[4] += cs * vx * vz;
+            vir[5] += cs * vy * vz;
+        }
+        const float hb = transpose_reduce16(acc, lane);
+        gx = warp_sum(gx);
+        gy = warp_sum(gy);
+        gz = warp_sum(gz);
+        if ((lane & 1) == 0) HB[v * kF + (lane >> 1)] += hb;
+        if (lane == 0) {
+            float4 g = GRAD[v];
+            g.x += gx;
+            g.y += gy;
+            g.z += gz;
+            GRAD[v] = g;
+        }
+    }
+    cta_partials<6>(vir, vir_part);
+}
+
+// ---------------------------------------------------------------------------
+// three-body stage (potential.cpp:664-741 forward, :850-961 backward)
+// ---------------------------------------------------------------------------
+constexpr int kTbWarps = 4;
+
+__device__ __forceinline__ void bond_t(float d, float t[kF]) {
+    float u[kK];
+    basis(d, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u);
+#pragma unroll
+    for (int f = 0; f < kF; ++f) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) s = fmaf(c_m.P3[f * kK + k], u[k], s);
+        t[f] = s;
+    }
+}
+
+__device__ __forceinline__ void bond_dt(float d, float ds[kF]) {
+    float u[kK], du[kK];
+    basis_d(d, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u, du);
+#pragma unroll
+    for (int f = 0; f < kF; ++f) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) s = fmaf(c_m.P3[f * kK + k], du[k], s);
+        ds[f] = s;
+    }
+}
+
+// per center s: for each in-bond slot j (bond e1 = (w->s)), compute t' of the
+// reverse bond e' = (s->w): m3_{e'} = sum_{e2 != e1} c(e2, e') t_{e2} in
+// ascending e2, z3 = W3 m3, t' = t + fc3 tanh(z3).  Stored at slot j.
+__global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float* __restrict__ TP,
+                                                              float* __restrict__ TH3,
+                                                              int32_t* flags) {
+    __shared__ float st[kTbWarps][kMaxBondsPerAtom][kF];
+    __shared__ float4 sv[kTbWarps][kMaxBondsPerAtom];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int64_t w0 = (int64_t)blockIdx.x * kTbWarps + wl;
+    const int64_t nw = (int64_t)gridDim.x * kTbWarps;
+    for (int64_t s = w0; s < a.n; s += nw) {
+        const int b0 = a.brow[s], k = a.brow[s + 1] - b0;
+        if (k > kMaxBondsPerAtom) {
+            if (lane == 0) atomicOr(&flags[1], 16);
+            continue;
+        }
+        for (int j = lane; j < k; j += 32) {
+            float4 q = __ldg(a.vd + a.bedge[b0 + j]);
+            sv[wl][j] = q;
+            float t[kF];
+            bond_t(q.w, t);
+#pragma unroll
+            for (int f = 0; f < kF; ++f) st[wl][j][f] = t[f];
+        }
+        __syncwarp();
+        for (int j = lane; j < k; j += 32) {
+            const float4 qj = sv[wl][j];
+            float m3[kF];
+#pragma unroll
+            for (int f = 0; f < kF; ++f) m3[f] = 0.f;
+            for (int e2 = 0; e2 < k; ++e2) {
+                if (e2 == j) continue;  // the reverse pair (linegraph.cpp:16-21)
+                const float4 q2 = sv[wl][e2];
+                const float c = (q2.x * qj.x + q2.y * qj.y + q2.z * qj.z) / (q2.w * qj.w);
+#pragma unroll
+                for (int f = 0; f < kF; ++f) m3[f] = fmaf(c, st[wl][e2][f], m3[f]);
+            }
+            float fc, dfc;
+            fcut3(qj.w, fc, dfc);
+            float tp[kF], th[kF];
+#pragma unroll
+            for (int f = 0; f < kF; ++f) {
+                float z = 0.f;
+#pragma unroll
+                for (int g = 0; g < kF; ++g) z = fmaf(c_m.W3[f * kF + g], m3[g], z);
+                th[f] = tanhf(z);
+                tp[f] = st[wl][j][f] + fc * th[f];
+            }
+            store_row16(TP + (size_t)(b0 + j) * kF, tp);
+            store_row16(TH3 + (size_t)(b0 + j) * kF, th);
+        }
+        __syncwarp();
+    }
+}
+
+// q_u = sum_{b into u} t'_b (ascending b), h_u += tanh(W4 q_u)
+__global__ void k_tb_inject(BondArgs a, const float* __restrict__ TP, float* __restrict__ H,
+                            float* __restrict__ TH4) {
+    int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= a.n) return;
+    float q[kF];
+#pragma unroll
+    for (int f = 0; f < kF; ++f) q[f] = 0.f;
+    for (int b = a.brow[u]; b < a.brow[u + 1]; ++b) {
+        float t[kF];
+        load_row16(TP + (size_t)a.brev[b] * kF, t);
+#pragma unroll
+        for (int f = 0; f < kF; ++f) q[f] += t[f];
+    }
+    const int64_t r = a.crow ? a.crow[u] : u;
+    float h[kF], th[kF];
+    load_row16(H + r * kF, h);
+#pragma unroll
+    for (int f = 0; f < kF; ++f) {
+        float z = 0.f;
+#pragma unroll
+        for (int g = 0; g < kF; ++g) z = fmaf(c_m.W4[f * kF + g], q[g], z);
+        th[f] = tanhf(z);
+        h[f] += th[f];
+    }
+    store_row16(H + r * kF, h);
+    store_row16(TH4 + u * kF, th);
+}
+
+__global__ void k_tb_bwd_q(int64_t n, const float* __restrict__ HB, const float* __restrict__ TH4,
+                           float* __restrict__ QB) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    float hb[kF], th[kF], y[kF], qb[kF];
+    load_row16(HB + v * kF, hb);
+    load_row16(TH4 + v * kF, th);
+#pragma unroll
+    for (int f = 0; f < kF; ++f) y[f] = hb[f] * (1.0f - th[f] * th[f]);
+#pragma unroll
+    for (int g = 0; g < kF; ++g) {
+        float acc = 0.f;
+#pragma unroll
+        for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W4[f * kF + g], y[f], acc);
+        qb[g] = acc;
+    }
+    store_row16(QB + v * kF, qb);
+}
+
+// Per center s.  Slot j holds in-bond e_j = (w_j -> s); its reverse e'_j is
+// the out-bond (s -> w_j).  VOUT[j] collects the gradient w.r.t. v_{e'_j}
+// produced here (fc3 path, identity part of the bond-init adjoint, cos
+// gradient of e'_j); VIN[j] the gradient w.r.t. v_{e_j} produced here
+// (cos gradient of e_j, line-edge part of its bond-init adjoint).
+__global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
+                                                               const float* __restrict__ QB,
+                                                               const float* __restrict__ TH3,
+                                                               float4* __restrict__ VIN,
+                                                               float4* __restrict__ VOUT,
+                                                               double* vir_part) {
+    __shared__ float st[kTbWarps][kMaxBondsPerAtom][kF];
+    __shared__ float sm[kTbWarps][kMaxBondsPerAtom][kF];
+    __shared__ float4 sv[kTbWarps][kMaxBondsPerAtom];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int64_t w0 = (int64_t)blockIdx.x * kTbWarps + wl;
+    const int64_t nw = (int64_t)gridDim.x * kTbWarps;
+    double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t s = w0; s < a.n; s += nw) {
+        const int b0 = a.brow[s], k = a.brow[s + 1] - b0;
+        if (k > kMaxBondsPerAtom) continue;  // flagged in the forward
+        for (int j = lane; j < k; j += 32) {
+            const int e = a.bedge[b0 + j];
+            const float4 q = __ldg(a.vd + e);
+            sv[wl][j] = q;
+            float t[kF];
+            bond_t(q.w, t);
+#pragma unroll
+            for (int f = 0; f < kF; ++f) st[wl][j][f] = t[f];
+            // stage 2: adjoints of the reverse bond e'_j
+            float tpb[kF], th[kF], ds[kF];
+            load_row16(QB + (size_t)__ldg(a.esrc + e) * kF, tpb);
+            load_row16(TH3 + (size_t)(b0 + j) * kF, th);
+            float fc, dfc;
+            fcut3(q.w, fc, dfc);
+            bond_dt(q.w, ds);
+            float dbf = 0.f, da = 0.f, y[kF];
+#pragma unroll
+            for (int f = 0; f < kF; ++f) {
+                dbf = fmaf(tpb[f] * th[f], dfc, dbf);
+                da = fmaf(tpb[f], ds[f], da);
+                y[f] = tpb[f] * fc * (1.0f - th[f] * th[f]);
+            }
+#pragma unroll
+            for (int g = 0; g < kF; ++g) {
+                float acc = 0.f;
+#pragma unroll
+                for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W3[f * kF + g], y[f], acc);
+                sm[wl][j][g] = acc;
+            }
+            const float c0 = -(dbf + da) / q.w;
+            VOUT[b0 + j] = make_float4(q.x * c0, q.y * c0, q.z * c0, 0.f);
+        }
+        __syncwarp();
+        for (int j = lane; j < k; j += 32) {
+            const float4 qj = sv[wl][j];
+            const float idj = 1.0f / qj.w;
+            float tb[kF];
+#pragma unroll
+            for (int f = 0; f < kF; ++f) tb[f] = 0.f;
+            float vix = 0.f, viy = 0.f, viz = 0.f;  // as incoming bond e = e_j
+            float4 vo = VOUT[b0 + j];                // as outgoing bond e' = e'_j
+            for (int o = 0; o < k; ++o) {
+                if (o == j) continue;
+                const float4 qo = sv[wl][o];
+                const float ido = 1.0f / qo.w;
+                const float dotjo = qj.x * qo.x + qj.y * qo.y + qj.z * qo.z;
+                // (a) line edge (e_j, e'_o): c = v_j.v_o/(d_j d_o), a = v_j, b = -v_o
+                {
+                    const float c = dotjo * idj * ido;
+                    float cb = 0.f;
+#pragma unroll
+                    for (int f = 0; f < kF; ++f) {
+                        tb[f] = fmaf(c, sm[wl][o][f], tb[f]);
+                        cb = fmaf(sm[wl][o][f], st[wl][j][f], cb);
+                    }
+                    // dc/da = -(b^ + a^ c)/|a|
+                    vix += -(-qo.x * ido + qj.x * idj * c) * idj * cb;
+                    viy += -(-qo.y * ido + qj.y * idj * c) * idj * cb;
+                    viz += -(-qo.z * ido + qj.z * idj * c) * idj * cb;
+                }
+                // (b) line edge (e_o, e'_j): a = v_o, b = -v_j
+                {
+                    const float c = dotjo * idj * ido;
+                    float cb = 0.f;
+#pragma unroll
+                    for (int f = 0; f < kF; ++f) cb = fmaf(sm[wl][j][f], st[wl][o][f], cb);
+                    // dc/db = -(a^ + b^ c)/|b|
+                    vo.x += -(qo.x * ido - qj.x * idj * c) * idj * cb;
+                    vo.y += -(qo.y * ido - qj.y * idj * c) * idj * cb;
+                    vo.z += -(qo.z * ido - qj.z * idj * c) * idj * cb;
+                }
+            }
+            float ds[kF];
+            bond_dt(qj.w, ds);
+            float db = 0.f;
+#pragma unroll
+            for (int f = 0; f < kF; ++f) db = fmaf(tb[f], ds[f], db);
+            vix += qj.x * db * idj;
+            viy += qj.y * db * idj;
+            viz += qj.z * db * idj;
+            VIN[b0 + j] = make_float4(vix, viy, viz, 0.f);
+            VOUT[b0 + j] = vo;
+            const double dx = (double)vix - vo.x, dy = (double)viy - vo.y, dz = (double)viz - vo.z;
+            vir[0] += dx * qj.x;
+            vir[1] += dx * qj.y;
+            vir[2] += dx * qj.z;
+            vir[3] += dy * qj.x;
+            vir[4] += dy * qj.y;
+            vir[5] += dy * qj.z;
+            vir[6] += dz * qj.x;
+            vir[7] += dz * qj.y;
+            vir[8] += dz * qj.z;
+        }
+        __syncwarp();
+    }
+    cta_partials<9>(vir, vir_part);
+}
+
+// grad[u] += sum_{X into u} (v_bar of rev(X)) - (v_bar of X)
+__global__ void k_tb_grad(BondArgs a, const float4* __restrict__ VIN,
+                          const float4* __restrict__ VOUT, float4* __restrict__ GRAD) {
+    int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= a.n) return;
+    float gx = 0.f, gy = 0.f, gz = 0.f;
+    for (int b = a.brow[u]; b < a.brow[u + 1]; ++b) {
+        const int rb = a.brev[b];
+        const float4 i1 = VIN[rb], o1 = VOUT[b], i2 = VIN[b], o2 = VOUT[rb];
+        gx += (i1.x + o1.x) - (i2.x + o2.x);
+        gy += (i1.y + o1.y) - (i2.y + o2.y);
+        gz += (i1.z + o1.z) - (i2.z + o2.z);
+    }
+    float4 g = GRAD[u];
+    g.x += gx;
+    g.y += gy;
+    g.z += gz;
+    GRAD[u] = g;
+}
+
+__global__ void k_init_hbar(int64_t n, float* HB) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * kF) return;
+    HB[t] = c_m.ro[t % kF];
+}
+
+__global__ void k_forces_out(int64_t n, const float4* __restrict__ GRAD, double* forces,
+                             float* forces32) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    float4 g = GRAD[v];
+    if (forces) {
+        forces[3 * v] = -(double)g.x;
+        forces[3 * v + 1] = -(double)g.y;
+        forces[3 * v + 2] = -(double)g.z;
+    }
+    if (forces32) {
+        forces32[3 * v] = -g.x;
+        forces32[3 * v + 1] = -g.y;
+        forces32[3 * v + 2] = -g.z;
+    }
+}
+
+__global__ void k_reduce_partials(const double* parts, int nparts, int w, double* out) {
+    int c = threadIdx.x;
+    if (c >= w) return;
+    double acc = 0.0;
+    for (int i = 0; i < nparts; ++i) acc += parts[(size_t)i * w + c];
+    out[c] = acc;
+}
+
+}  // namespace
+
+int model_grid(int64_t n) {
+    int64_t g = (n + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (g > 148 * 16) g = 148 * 16;
+    return (int)(g > 0 ? g : 1);
+}
+
+static int tb_grid(int64_t n) {
+    int64_t g = (n + kTbWarps - 1) / kTbWarps;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g > 0 ? g : 1);
+}
+
+void launch_embed(int64_t rows, const int32_t* node_array, const int32_t* Z, float* H0,
+                  cudaStream_t s) {
+    if (rows == 0) return;
+    k_embed<<<div_up(rows * 4, 256), 256, 0, s>>>(rows, node_array, Z, H0);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float* buf, int width,
+                     cudaStream_t s) {
+    if (nx == 0) return;
+    int w4 = width / 4;
+    k_exchange<<<div_up(nx * w4, 256), 256, 0, s>>>(nx, xdst, xsrc, reinterpret_cast<float4*>(buf),
+                                                     w4);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
+                 double* per_atom, double* e_part, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_conv<<<model_grid(a.n), kThreads, 0, s>>>(a, layer, Hin, Hout, TH, per_atom, e_part);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_bwd_node(int64_t n, const int32_t* crow, int layer, const float* HB, const float* TH,
+                     float* MB, cudaStream_t s) {
+    if (n == 0) return;
+    k_bwd_node<<<div_up(n, 128), 128, 0, s>>>(n, crow, layer, HB, TH, MB);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
+                     double* vir_part, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_bwd_edge<<<model_grid(a.n), kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_tb_forward<<<tb_grid(a.n), kTbWarps * 32, 0, s>>>(a, TP, TH3, flags);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_tb_inject(const BondArgs& a, const float* TP, float* H, float* TH4, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_tb_inject<<<div_up(a.n, 128), 128, 0, s>>>(a, TP, H, TH4);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_tb_bwd_q(int64_t n, const float* HB, const float* TH4, float* QB, cudaStream_t s) {
+    if (n == 0) return;
+    k_tb_bwd_q<<<div_up(n, 128), 128, 0, s>>>(n, HB, TH4, QB);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
+                        float4* VOUT, double* vir_part, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_tb_backward<<<tb_grid(a.n), kTbWarps * 32, 0, s>>>(a, QB, TH3, VIN, VOUT, vir_part);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, float4* GRAD,
+                    cudaStream_t s) {
+    if (a.n == 0) return;
+    k_tb_grad<<<div_up(a.n, 128), 128, 0, s>>>(a, VIN, VOUT, GRAD);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_init_hbar(int64_t n, float* HB, cudaStream_t s) {
+    if (n == 0) return;
+    k_init_hbar<<<div_up(n * kF, 256), 256, 0, s>>>(n, HB);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_forces_out(int64_t n, const float4* GRAD, double* forces, float* forces32,
+                       cudaStream_t s) {
+    if (n == 0) return;
+    k_forces_out<<<div_up(n, 256), 256, 0, s>>>(n, GRAD, forces, forces32);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s) {
+    k_reduce_partials<<<1, 32, 0, s>>>(parts, nparts, w, out);
+    GMD_LAUNCH_CHECK();
+}
+
+int tb_grid_size(int64_t n) { return tb_grid(n); }
+
+}  // namespace gmd

@@ -1,0 +1,84 @@
+// Message passing, halo exchange and the hand-written backward of the toy
+// invariant MLIP (proj/src/potential.cpp:19-78, 563-985) on the GPU.
+#pragma once
+#include "gmd_common.cuh"
+
+namespace gmd {
+
+constexpr int kMaxLayers = 8;
+constexpr int kF = 16;  // feature width of the compiled kernels
+constexpr int kK = 8;   // radial basis count of the compiled kernels
+constexpr int kMaxBondsPerAtom = 64;
+
+// fp32 copy of ToyPotentialParams (potential.hpp:15-41) in constant memory
+struct ModelConst {
+    float emb[119 * kF];
+    float W[kMaxLayers][kF * kF];
+    float b[kMaxLayers][kF];
+    float P[kF * kK];
+    float P3[kF * kK];
+    float W3[kF * kF];
+    float W4[kF * kF];
+    float ro[kF];
+    float rc, inv_rc, inv_sigma, mu_step;     // atom radial basis
+    float r3, inv_r3, inv_sigma3, mu_step3;   // three-body radial basis
+    int L;
+};
+
+void upload_model(const ModelConst& m, cudaStream_t s);
+
+// Row/edge views used by the kernels.  Node loops run over global ids
+// [0, n) of owned atoms in ascending order; crow maps an id to its row in the
+// (super-)layout of its owner partition (nullptr = identity); lsrc is the
+// source row per edge.
+struct ConvArgs {
+    int64_t n;
+    const int32_t* crow;
+    const int32_t* row;
+    const int32_t* lsrc;
+    const float4* vd;
+};
+
+int model_grid(int64_t n);  // fixed grid => deterministic reductions
+
+void launch_embed(int64_t rows, const int32_t* node_array, const int32_t* Z, float* H0,
+                  cudaStream_t s);
+void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float* buf, int width,
+                     cudaStream_t s);
+// forward conv layer l: Hout[own] = Hin[own] + tanh(W_l m + b_l); TH_l = tanh(.)
+// last layer additionally writes per-atom energies and per-CTA energy partials
+void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
+                 double* per_atom, double* e_part, cudaStream_t s);
+// backward: MB[row(v)] = W_l^T (HB[v] * (1 - TH_l[v]^2))
+void launch_bwd_node(int64_t n, const int32_t* crow, int layer, const float* HB, const float* TH,
+                     float* MB, cudaStream_t s);
+// backward edge pass (row form, no atomics): HB += gathered adjoints,
+// GRAD += positional gradient, virial partials per CTA (6 doubles)
+void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
+                     double* vir_part, cudaStream_t s);
+
+// three-body stage (global bond CSR by dst; slot = in-bond position)
+struct BondArgs {
+    int64_t n;
+    const int32_t* crow;
+    const int32_t* brow;    // n + 1
+    const int32_t* bedge;   // B: edge id of bond
+    const int32_t* brev;    // B: bond id of the reverse bond
+    const int32_t* esrc;    // E: global source id per edge
+    const float4* vd;       // E
+};
+void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, cudaStream_t s);
+void launch_tb_inject(const BondArgs& a, const float* TP, float* H, float* TH4, cudaStream_t s);
+void launch_tb_bwd_q(int64_t n, const float* HB, const float* TH4, float* QB, cudaStream_t s);
+void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
+                        float4* VOUT, double* vir_part, cudaStream_t s);
+void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, float4* GRAD,
+                    cudaStream_t s);
+
+void launch_init_hbar(int64_t n, float* HB, cudaStream_t s);
+void launch_forces_out(int64_t n, const float4* GRAD, double* forces, float* forces32,
+                       cudaStream_t s);
+// sum nparts consecutive records of width w into out[w] in fixed order
+void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s);
+
+}  // namespace gmd

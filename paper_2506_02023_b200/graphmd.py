@@ -1,0 +1,705 @@
+"""Python mirror of the reference's graphmd plugin API over the C ABI.
+
+Same names, argument meaning and error behaviour as the C++ reference
+(`graphmd::Distributed`, `forward_distributed`, the graph / partition /
+line-graph views), backed by libgraphmd_b200.so (include/graphmd_b200.h).
+
+  reference                                  here
+  Distributed::create_distributed            Distributed.create_distributed   engine.hpp:51-56
+  forward_distributed(dist, params, timing)  forward_distributed              potential.hpp:58-60
+  ToyPotentialParams::init                   ToyPotentialParams.init          potential.hpp:35-37
+  build_neighbor_list                        build_neighbor_list              neighborlist.hpp:37-38
+  AtomGraph / PartitionRule / SpanLayout /   same-named classes (numpy views)
+  AtomPartition / PartitionedAtomGraph /
+  BondSet / PartitionedLineGraph
+  DistributedFeatures + transfer API         DistributedFeatures (CUDA tensor blocks)
+
+There is no CPU fallback: importing works anywhere, but every computation
+goes through the CUDA library and raises if it (or a GPU) is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgraphmd_b200.so")
+
+GMD_OK, GMD_ERR_CONFIG, GMD_ERR_RUNTIME, GMD_ERR_CUDA, GMD_ERR_ARG = 0, 2, 3, 4, 5
+GMD_ALLOW_NARROW, GMD_INPUT_DEVICE, GMD_EQUAL_WIDTH = 1, 2, 4
+GMD_OUTPUT_DEVICE, GMD_OUTPUT_F32 = 1, 2
+GMD_F32, GMD_F64 = 0, 1
+
+# every symbol include/graphmd_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "gmd_version", "gmd_last_error", "gmd_create", "gmd_destroy", "gmd_build",
+    "gmd_set_params", "gmd_params_size", "gmd_params_init", "gmd_forward", "gmd_num_nodes",
+    "gmd_num_edges", "gmd_num_partitions", "gmd_get_graph", "gmd_get_system", "gmd_get_rule",
+    "gmd_get_owner", "gmd_get_layout_size", "gmd_get_layout", "gmd_get_num_duplicates",
+    "gmd_get_duplicates", "gmd_get_num_owned_edges", "gmd_get_owned_edges",
+    "gmd_get_num_border_edges", "gmd_get_border_edges", "gmd_has_line_graph",
+    "gmd_get_num_bonds", "gmd_get_bonds", "gmd_get_num_line_edges", "gmd_get_line_edges",
+    "gmd_block_rows", "gmd_block_offset", "gmd_transfer", "gmd_transfer_transpose",
+    "gmd_sync_duplicates", "gmd_distribute", "gmd_aggregate",
+    "gmd_corrupt_transfer_plan_for_test", "gmd_util_rng_uniform", "gmd_util_supercell",
+    "gmd_profile", "gmd_profile_read",
+]
+
+
+class Error(RuntimeError):
+    """graphmd::Error (system.hpp:13-15)."""
+
+    def __init__(self, msg: str, code: int = GMD_ERR_CONFIG):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib_cache = None
+
+
+def lib():
+    """The loaded CUDA library.  Fails loudly when it is missing."""
+    global _lib_cache
+    if _lib_cache is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2506_02023_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        V, I, I64, D, U32, U64 = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_uint32, C.c_uint64
+        sig = {
+            "gmd_version": (C.c_char_p, []),
+            "gmd_last_error": (C.c_char_p, [V]),
+            "gmd_create": (I, [I, C.POINTER(V)]),
+            "gmd_destroy": (None, [V]),
+            "gmd_build": (I, [V, I64, V, V, V, V, D, D, D, I, I, U32]),
+            "gmd_set_params": (I, [V, I, I, I, D, D, V]),
+            "gmd_params_size": (I64, [I, I, I]),
+            "gmd_params_init": (I, [U64, I, I, I, D, D, V]),
+            "gmd_forward": (I, [V, V, V, V, V, V, U32]),
+            "gmd_num_nodes": (I, [V, V]),
+            "gmd_num_edges": (I, [V, V]),
+            "gmd_num_partitions": (I, [V, V]),
+            "gmd_get_graph": (I, [V, V, V, V, V, V]),
+            "gmd_get_system": (I, [V, V, V]),
+            "gmd_get_rule": (I, [V, V, V]),
+            "gmd_get_owner": (I, [V, V]),
+            "gmd_get_layout_size": (I, [V, I, I, V]),
+            "gmd_get_layout": (I, [V, I, I, V, V]),
+            "gmd_get_num_duplicates": (I, [V, I, I, V]),
+            "gmd_get_duplicates": (I, [V, I, I, V]),
+            "gmd_get_num_owned_edges": (I, [V, I, V]),
+            "gmd_get_owned_edges": (I, [V, I, V, V, V]),
+            "gmd_get_num_border_edges": (I, [V, I, V]),
+            "gmd_get_border_edges": (I, [V, I, V]),
+            "gmd_has_line_graph": (I, [V, V]),
+            "gmd_get_num_bonds": (I, [V, V]),
+            "gmd_get_bonds": (I, [V, V, V]),
+            "gmd_get_num_line_edges": (I, [V, I, V]),
+            "gmd_get_line_edges": (I, [V, I, V]),
+            "gmd_block_rows": (I, [V, I, V]),
+            "gmd_block_offset": (I, [V, I, I, V]),
+            "gmd_transfer": (I, [V, I, V, I, I]),
+            "gmd_transfer_transpose": (I, [V, I, V, I, I]),
+            "gmd_sync_duplicates": (I, [V, I, V, I, I]),
+            "gmd_distribute": (I, [V, I, V, V, I, I]),
+            "gmd_aggregate": (I, [V, I, V, V, I, I]),
+            "gmd_corrupt_transfer_plan_for_test": (I, [V]),
+            "gmd_util_rng_uniform": (I, [U64, I64, D, D, V]),
+            "gmd_util_supercell": (I, [I64, V, V, V, I, I, I, D, U64, V, V, V]),
+            "gmd_profile": (I, [V, I]),
+            "gmd_profile_read": (I, [V, V, I, V, V]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib_cache = L
+    return _lib_cache
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _Handle:
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        rc = lib().gmd_create(device, C.byref(self.h))
+        if rc != GMD_OK:
+            raise Error(lib().gmd_last_error(None).decode() or "gmd_create failed", rc)
+        self.device = device
+
+    def check(self, rc):
+        if rc != GMD_OK:
+            raise Error(lib().gmd_last_error(self.h).decode(), rc)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().gmd_destroy(self.h)
+        except Exception:
+            pass
+
+    def i64(self, fn, *args):
+        out = C.c_int64()
+        self.check(fn(self.h, *args, C.byref(out)))
+        return out.value
+
+
+# ---------------------------------------------------------------------------
+# system + fixtures (system.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class AtomicSystem:
+    positions: np.ndarray
+    lattice: np.ndarray = field(default_factory=lambda: np.eye(3))
+    species: np.ndarray = None
+    pbc: Sequence[bool] = (True, True, True)
+
+    def __post_init__(self):
+        self.positions = np.ascontiguousarray(self.positions, dtype=np.float64).reshape(-1, 3)
+        self.lattice = np.ascontiguousarray(self.lattice, dtype=np.float64).reshape(3, 3)
+        if self.species is None:
+            self.species = np.ones(len(self.positions), np.int32)
+        self.species = np.ascontiguousarray(self.species, dtype=np.int32)
+
+    def size(self) -> int:
+        return len(self.positions)
+
+    def any_pbc(self) -> bool:
+        return any(self.pbc)
+
+    def validate(self):
+        if len(self.species) != len(self.positions):
+            raise Error("species length does not match atom count")
+        if self.any_pbc() and abs(np.linalg.det(self.lattice)) < 1e-10:
+            raise Error("periodic system requires an invertible lattice")
+
+
+def rng_uniform(seed: int, count: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
+    """Rng(seed).uniform(lo, hi) stream (system.hpp:121-149)."""
+    out = np.zeros(count)
+    rc = lib().gmd_util_rng_uniform(seed, count, lo, hi, _p(out))
+    if rc:
+        raise Error("rng_uniform failed", rc)
+    return out
+
+
+def make_supercell(system: AtomicSystem, reps, amplitude: float = 0.0, seed: int = 0) -> AtomicSystem:
+    """make_supercell (+ random_perturb when amplitude > 0) (system.cpp:188-240)."""
+    n = system.size() * reps[0] * reps[1] * reps[2]
+    op = np.zeros((n, 3))
+    oz = np.zeros(n, np.int32)
+    ol = np.zeros((3, 3))
+    rc = lib().gmd_util_supercell(system.size(), _p(system.positions), _p(system.species),
+                                  _p(system.lattice), reps[0], reps[1], reps[2], amplitude, seed,
+                                  _p(op), _p(oz), _p(ol))
+    if rc:
+        raise Error("supercell repetitions must be >= 1" if rc == GMD_ERR_CONFIG else "supercell failed", rc)
+    return AtomicSystem(op, ol, oz, tuple(system.pbc))
+
+
+def random_perturb(system: AtomicSystem, amplitude: float, seed: int) -> AtomicSystem:
+    if amplitude < 0.0:
+        raise Error("perturbation amplitude must be >= 0")
+    return make_supercell(system, (1, 1, 1), amplitude, seed)
+
+
+# ---------------------------------------------------------------------------
+# model parameters (potential.hpp:15-48)
+# ---------------------------------------------------------------------------
+@dataclass
+class ToyPotentialParams:
+    feature_width: int = 16
+    basis_count: int = 8
+    layers: int = 2
+    r_atom: float = 4.0
+    r_3body: float = 0.0
+    seed: int = 0
+    blob: np.ndarray = None
+
+    def threebody(self) -> bool:
+        return self.r_3body > 0.0
+
+    @staticmethod
+    def init(seed: int, feature_width: int = 16, basis_count: int = 8, layers: int = 2,
+             r_atom: float = 4.0, r_3body: float = 0.0) -> "ToyPotentialParams":
+        n = lib().gmd_params_size(feature_width, basis_count, layers)
+        blob = np.zeros(n)
+        rc = lib().gmd_params_init(seed, feature_width, basis_count, layers, r_atom, r_3body, _p(blob))
+        if rc:
+            raise Error("layer count must be >= 1", rc)
+        p = ToyPotentialParams(feature_width, basis_count, layers, r_atom, r_3body, seed, blob)
+        p.validate()
+        return p
+
+    def _sizes(self):
+        F, K, L = self.feature_width, self.basis_count, self.layers
+        return [("embedding", 119 * F), ("layer_w", L * F * F), ("layer_b", L * F),
+                ("basis_proj", F * K), ("basis3_proj", F * K), ("w3", F * F), ("w4", F * F),
+                ("readout", F)]
+
+    def __getattr__(self, name):
+        if name in ("embedding", "layer_w", "layer_b", "basis_proj", "basis3_proj", "w3", "w4", "readout"):
+            off = 0
+            for k, sz in self._sizes():
+                if k == name:
+                    return self.blob[off:off + sz]
+                off += sz
+        raise AttributeError(name)
+
+    def validate(self):
+        if self.layers < 1:
+            raise Error("layer count must be >= 1")
+        if self.feature_width < 1 or self.basis_count < 1:
+            raise Error("feature and basis widths must be >= 1")
+        if self.r_atom <= 0.0:
+            raise Error("atom cutoff must be positive")
+        if self.threebody() and self.r_3body > self.r_atom:
+            raise Error("three-body cutoff cannot exceed the atom cutoff")
+        if self.blob is None or len(self.blob) != sum(s for _, s in self._sizes()):
+            raise Error("parameter array has the wrong size")
+        if not np.all(np.isfinite(self.blob)):
+            raise Error("parameter array contains a non-finite value")
+
+
+@dataclass
+class StepTiming:
+    graph_creation: float = 0.0
+    feature_calculation: float = 0.0
+    forward_pass: float = 0.0
+    backward_pass: float = 0.0
+
+    @staticmethod
+    def category_names():
+        return ["Graph Creation", "Feature Calculation", "Forward Pass", "Backward Pass"]
+
+    def total(self):
+        return self.graph_creation + self.feature_calculation + self.forward_pass + self.backward_pass
+
+    def __iadd__(self, o):
+        self.graph_creation += o.graph_creation
+        self.feature_calculation += o.feature_calculation
+        self.forward_pass += o.forward_pass
+        self.backward_pass += o.backward_pass
+        return self
+
+
+@dataclass
+class PotentialOutput:
+    energy: float
+    per_atom: np.ndarray
+    forces: np.ndarray
+    stress: np.ndarray
+
+
+# ---------------------------------------------------------------------------
+# graph / partition views (neighborlist.hpp, partitioner.hpp, linegraph.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class AtomGraph:
+    src: np.ndarray
+    dst: np.ndarray
+    image_offset: np.ndarray
+    distance: np.ndarray
+    vector: np.ndarray
+    cutoff: float
+    num_nodes: int
+
+    def num_edges(self) -> int:
+        return len(self.src)
+
+    def edges_into(self, node: int):
+        lo = int(np.searchsorted(self.dst, node, "left"))
+        hi = int(np.searchsorted(self.dst, node, "right"))
+        return lo, hi
+
+
+@dataclass
+class PartitionRule:
+    axis: int
+    boundaries: np.ndarray
+    p: int
+
+
+@dataclass
+class Span:
+    begin: int
+    end: int
+
+    def size(self):
+        return self.end - self.begin
+
+
+@dataclass
+class SpanLayout:
+    node_array: np.ndarray
+    markers: np.ndarray
+    duplicates: np.ndarray
+    p: int
+
+    def pure_span(self):
+        return Span(int(self.markers[0]), int(self.markers[1]))
+
+    def to_span(self, j):
+        return Span(int(self.markers[1 + j]), int(self.markers[2 + j]))
+
+    def from_span(self, j):
+        return Span(int(self.markers[1 + self.p + j]), int(self.markers[2 + self.p + j]))
+
+    def owned_end(self):
+        return int(self.markers[1 + self.p])
+
+    def size(self):
+        return len(self.node_array)
+
+    def local_of(self, g):
+        hit = np.nonzero(self.node_array == g)[0]
+        return int(hit[0]) if len(hit) else -1
+
+
+@dataclass
+class Buckets:
+    pure: List[np.ndarray]
+    to: List[List[np.ndarray]]
+    frm: List[List[np.ndarray]]  # `from` is a Python keyword
+
+
+def _buckets(layouts: List[SpanLayout], p: int) -> Buckets:
+    pure = [L.node_array[L.pure_span().begin:L.pure_span().end] for L in layouts]
+    to = [[L.node_array[L.to_span(j).begin:L.to_span(j).end] for j in range(p)] for L in layouts]
+    frm = [[to[i][j] for i in range(p)] for j in range(p)]
+    return Buckets(pure, to, frm)
+
+
+@dataclass
+class AtomPartition:
+    layout: SpanLayout
+    owned_edges: np.ndarray
+    local_src: np.ndarray
+    local_dst: np.ndarray
+    border_edge_list: np.ndarray
+
+
+@dataclass
+class PartitionedAtomGraph:
+    rule: PartitionRule
+    buckets: Buckets
+    owner: np.ndarray
+    parts: List[AtomPartition]
+    p: int
+
+
+@dataclass
+class BondSet:
+    edge_of_bond: np.ndarray
+    bond_of_edge: np.ndarray
+    r: float
+    tau: float
+
+    def size(self):
+        return len(self.edge_of_bond)
+
+
+@dataclass
+class LineGraphPartition:
+    layout: SpanLayout
+    line_edges: np.ndarray  # (local e, local e') pairs, sorted by (global e', global e)
+
+
+@dataclass
+class PartitionedLineGraph:
+    bonds: BondSet
+    bond_owner: np.ndarray
+    bond_buckets: Buckets
+    parts: List[LineGraphPartition]
+    p: int
+
+
+class DistributedFeatures:
+    """Per-partition feature blocks in ONE CUDA tensor (rows x width); block i
+    is rows [offsets[i], offsets[i+1]) aligned to partition i's layout."""
+
+    def __init__(self, data, offsets, width, bonds):
+        self.data, self.offsets, self.width, self.bonds = data, offsets, width, bonds
+
+    def block(self, i):
+        return self.data[self.offsets[i]:self.offsets[i + 1]]
+
+    def row(self, i, local):
+        return self.data[self.offsets[i] + local]
+
+
+# ---------------------------------------------------------------------------
+# Distributed (engine.hpp:49-151)
+# ---------------------------------------------------------------------------
+class Distributed:
+    """Distributed execution handle on one GPU: partitioned graphs plus
+    transfer plans, all resident in HBM."""
+
+    def __init__(self, handle: _Handle, system: AtomicSystem, p: int, n_threads: int,
+                 atom_cutoff: float, threebody_cutoff, tau):
+        self._h = handle
+        self._system_in = system
+        self._p = p
+        self._n_threads = n_threads if n_threads > 0 else 1
+        self.atom_cutoff = atom_cutoff
+        self.threebody_cutoff = threebody_cutoff
+        self.threebody_tau = tau
+        self._graph = self._parts = self._lines = self._system = None
+
+    @staticmethod
+    def create_distributed(system: AtomicSystem, atom_cutoff: float,
+                           threebody_cutoff: Optional[float], p: int, n_threads: int,
+                           allow_narrow: bool = False, threebody_tau: float = 0.0,
+                           device: int = 0, handle: Optional[_Handle] = None,
+                           equal_width: bool = False) -> "Distributed":
+        """Distributed::create_distributed (engine.cpp:44-65).  Pass `handle`
+        to reuse the device buffers of a previous build (per-step rebuilds)."""
+        h = handle or _Handle(device)
+        flags = (GMD_ALLOW_NARROW if allow_narrow else 0) | (GMD_EQUAL_WIDTH if equal_width else 0)
+        pbc = np.array([1 if b else 0 for b in system.pbc], np.uint8)
+        r3 = float(threebody_cutoff) if threebody_cutoff is not None else 0.0
+        if threebody_cutoff is not None and r3 <= 0.0:
+            raise Error("three-body cutoff must be positive")
+        h.check(lib().gmd_build(h.h, system.size(), _p(system.positions), _p(system.species),
+                                _p(system.lattice), _p(pbc), float(atom_cutoff), r3,
+                                float(threebody_tau), int(p), int(n_threads), flags))
+        return Distributed(h, system, p, n_threads, atom_cutoff, threebody_cutoff, threebody_tau)
+
+    # ---- scalars
+    def num_partitions(self):
+        return self._p
+
+    def num_threads(self):
+        return self._n_threads
+
+    def has_line_graph(self):
+        out = C.c_int()
+        self._h.check(lib().gmd_has_line_graph(self._h.h, C.byref(out)))
+        return bool(out.value)
+
+    def num_nodes(self):
+        return self._h.i64(lib().gmd_num_nodes)
+
+    def num_edges(self):
+        return self._h.i64(lib().gmd_num_edges)
+
+    # ---- views
+    def system(self) -> AtomicSystem:
+        if self._system is None:
+            n = self.num_nodes()
+            pos = np.zeros((n, 3))
+            lat = np.zeros((3, 3))
+            self._h.check(lib().gmd_get_system(self._h.h, _p(pos), _p(lat)))
+            self._system = AtomicSystem(pos, lat, self._system_in.species.copy(), (True, True, True))
+        return self._system
+
+    def graph(self) -> AtomGraph:
+        if self._graph is None:
+            ne = self.num_edges()
+            g = dict(src=np.zeros(ne, np.int64), dst=np.zeros(ne, np.int64),
+                     off=np.zeros((ne, 3), np.int32), dist=np.zeros(ne), vec=np.zeros((ne, 3)))
+            self._h.check(lib().gmd_get_graph(self._h.h, *(_p(g[k]) for k in ("src", "dst", "off", "dist", "vec"))))
+            self._graph = AtomGraph(g["src"], g["dst"], g["off"], g["dist"], g["vec"],
+                                    float(self.atom_cutoff), self.num_nodes())
+        return self._graph
+
+    def _layout(self, part, bonds) -> SpanLayout:
+        h, L = self._h, lib()
+        size = C.c_int64()
+        h.check(L.gmd_get_layout_size(h.h, part, bonds, C.byref(size)))
+        na = np.zeros(size.value, np.int64)
+        mk = np.zeros(2 + 2 * self._p, np.int64)
+        h.check(L.gmd_get_layout(h.h, part, bonds, _p(na), _p(mk)))
+        nd = C.c_int64()
+        h.check(L.gmd_get_num_duplicates(h.h, part, bonds, C.byref(nd)))
+        dups = np.zeros((nd.value, 2), np.int64)
+        h.check(L.gmd_get_duplicates(h.h, part, bonds, _p(dups)))
+        return SpanLayout(na, mk, dups, self._p)
+
+    def atom_parts(self) -> PartitionedAtomGraph:
+        if self._parts is None:
+            h, L, p = self._h, lib(), self._p
+            axis = C.c_int()
+            b = np.zeros(p + 1)
+            h.check(L.gmd_get_rule(h.h, C.byref(axis), _p(b)))
+            owner = np.zeros(self.num_nodes(), np.int32)
+            h.check(L.gmd_get_owner(h.h, _p(owner)))
+            parts = []
+            for i in range(p):
+                lay = self._layout(i, 0)
+                cnt = C.c_int64()
+                h.check(L.gmd_get_num_owned_edges(h.h, i, C.byref(cnt)))
+                oe, ls, ld = (np.zeros(cnt.value, np.int64) for _ in range(3))
+                h.check(L.gmd_get_owned_edges(h.h, i, _p(oe), _p(ls), _p(ld)))
+                h.check(L.gmd_get_num_border_edges(h.h, i, C.byref(cnt)))
+                bd = np.zeros(cnt.value, np.int64)
+                h.check(L.gmd_get_border_edges(h.h, i, _p(bd)))
+                parts.append(AtomPartition(lay, oe, ls, ld, bd))
+            self._parts = PartitionedAtomGraph(PartitionRule(axis.value, b, p),
+                                               _buckets([x.layout for x in parts], p), owner, parts, p)
+        return self._parts
+
+    def line_parts(self) -> PartitionedLineGraph:
+        if not self.has_line_graph():
+            raise Error("no line graph was built")
+        if self._lines is None:
+            h, L, p = self._h, lib(), self._p
+            nb = self._h.i64(L.gmd_get_num_bonds)
+            eob = np.zeros(nb, np.int64)
+            own = np.zeros(nb, np.int32)
+            h.check(L.gmd_get_bonds(h.h, _p(eob), _p(own)))
+            boe = np.full(self.num_edges(), -1, np.int64)
+            boe[eob] = np.arange(nb)
+            parts = []
+            for i in range(p):
+                lay = self._layout(i, 1)
+                cnt = C.c_int64()
+                h.check(L.gmd_get_num_line_edges(h.h, i, C.byref(cnt)))
+                le = np.zeros((cnt.value, 2), np.int64)
+                h.check(L.gmd_get_line_edges(h.h, i, _p(le)))
+                parts.append(LineGraphPartition(lay, le))
+            bonds = BondSet(eob, boe, float(self.threebody_cutoff), float(self.threebody_tau))
+            self._lines = PartitionedLineGraph(bonds, own, _buckets([x.layout for x in parts], p), parts, p)
+        return self._lines
+
+    def src_nodes(self, partition):
+        return self.atom_parts().parts[partition].local_src
+
+    def dst_nodes(self, partition):
+        return self.atom_parts().parts[partition].local_dst
+
+    def atom_rows(self, partition):
+        return self.atom_parts().parts[partition].layout.size()
+
+    def bond_rows(self, partition):
+        return self.line_parts().parts[partition].layout.size()
+
+    # ---- feature API (engine.hpp:74-129), blocks are CUDA tensors
+    def _offsets(self, bonds):
+        h, L = self._h, lib()
+        offs = []
+        for i in range(self._p):
+            o = C.c_int64()
+            h.check(L.gmd_block_offset(h.h, i, bonds, C.byref(o)))
+            offs.append(o.value)
+        tot = C.c_int64()
+        h.check(L.gmd_block_rows(h.h, bonds, C.byref(tot)))
+        offs.append(tot.value)
+        return offs
+
+    def _make(self, width, bonds, dtype):
+        import torch
+        offs = self._offsets(bonds)
+        data = torch.zeros((offs[-1], width), dtype=dtype, device=f"cuda:{self._h.device}")
+        return DistributedFeatures(data, offs, width, bonds)
+
+    def make_atom_features(self, width, dtype=None):
+        import torch
+        return self._make(width, 0, dtype or torch.float64)
+
+    def make_bond_features(self, width, dtype=None):
+        import torch
+        if not self.has_line_graph():
+            raise Error("no line graph was built")
+        return self._make(width, 1, dtype or torch.float64)
+
+    @staticmethod
+    def _dt(f):
+        import torch
+        if f.data.dtype == torch.float64:
+            return GMD_F64
+        if f.data.dtype == torch.float32:
+            return GMD_F32
+        raise Error("features must be float32 or float64", GMD_ERR_ARG)
+
+    def _op(self, fn, f):
+        self._h.check(fn(self._h.h, f.bonds, C.c_void_p(f.data.data_ptr()), f.width, self._dt(f)))
+
+    def atom_transfer(self, f):
+        self._op(lib().gmd_transfer, f)
+
+    def bond_transfer(self, f):
+        self._op(lib().gmd_transfer, f)
+
+    def atom_transfer_transpose(self, f):
+        self._op(lib().gmd_transfer_transpose, f)
+
+    def bond_transfer_transpose(self, f):
+        self._op(lib().gmd_transfer_transpose, f)
+
+    def sync_atom_duplicates(self, f):
+        self._op(lib().gmd_sync_duplicates, f)
+
+    def sync_bond_duplicates(self, f):
+        self._op(lib().gmd_sync_duplicates, f)
+
+    def _distribute(self, features, width, bonds):
+        import torch
+        arr = np.ascontiguousarray(features, np.float64)
+        n = self.num_nodes() if not bonds else self.line_parts().bonds.size()
+        if arr.size != n * width:
+            raise Error("node feature shape mismatch" if not bonds else "bond feature shape mismatch")
+        f = self._make(width, bonds, torch.float64)
+        self._h.check(lib().gmd_distribute(self._h.h, bonds, _p(arr), C.c_void_p(f.data.data_ptr()),
+                                           width, GMD_F64))
+        return f
+
+    def distribute_node_features(self, features, width):
+        return self._distribute(features, width, 0)
+
+    def _aggregate(self, f):
+        n = self.num_nodes() if not f.bonds else self.line_parts().bonds.size()
+        out = np.zeros(n * f.width, np.float64 if self._dt(f) == GMD_F64 else np.float32)
+        self._h.check(lib().gmd_aggregate(self._h.h, f.bonds, C.c_void_p(f.data.data_ptr()), _p(out),
+                                          f.width, self._dt(f)))
+        return out
+
+    def aggregate(self, f):
+        return self._aggregate(f)
+
+    def aggregate_bonds(self, f):
+        return self._aggregate(f)
+
+    def corrupt_transfer_plan_for_test(self):
+        self._h.check(lib().gmd_corrupt_transfer_plan_for_test(self._h.h))
+
+    # per-step reuse
+    @property
+    def handle(self):
+        return self._h
+
+
+def forward_distributed(dist: Distributed, params: ToyPotentialParams,
+                        timing: Optional[StepTiming] = None) -> PotentialOutput:
+    """forward_distributed (potential.cpp:563-985) on the GPU."""
+    params.validate()
+    h = dist.handle
+    L = lib()
+    h.check(L.gmd_set_params(h.h, params.feature_width, params.basis_count, params.layers,
+                             params.r_atom, params.r_3body, _p(params.blob)))
+    n = dist.num_nodes()
+    e = C.c_double()
+    pa = np.zeros(n)
+    fo = np.zeros((n, 3))
+    st = np.zeros(9)
+    tm = np.zeros(4)
+    h.check(L.gmd_forward(h.h, C.byref(e), _p(pa), _p(fo), _p(st), _p(tm), 0))
+    if timing is not None:
+        timing.feature_calculation += tm[1]
+        timing.forward_pass += tm[2]
+        timing.backward_pass += tm[3]
+    return PotentialOutput(e.value, pa, fo, st.reshape(3, 3))
+
+
+def build_neighbor_list(system: AtomicSystem, cutoff: float, n_threads: int = 0,
+                        device: int = 0) -> AtomGraph:
+    """build_neighbor_list (neighborlist.cpp:108-197) on the GPU."""
+    d = Distributed.create_distributed(system, cutoff, None, 1, n_threads, True, device=device)
+    return d.graph()

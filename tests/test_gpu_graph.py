@@ -1,0 +1,114 @@
+"""GPU neighbour-list parity: bit-exact (src, dst, image) sets and canonical
+order vs the fp64 oracle (proj/tests/test_neighborlist.cpp, acceptance.cpp
+criterion 5)."""
+import numpy as np
+import pytest
+
+from paper_2506_02023_b200 import graphmd as G
+from tests import systems as S
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_graph(sys_, rc):
+    return G.build_neighbor_list(sys_, rc)
+
+
+def assert_same_graph(g, o):
+    # canonical order is part of the contract: compare arrays position by position
+    assert len(g.src) == len(o["src"])
+    np.testing.assert_array_equal(g.src, o["src"])
+    np.testing.assert_array_equal(g.dst, o["dst"])
+    np.testing.assert_array_equal(g.image_offset, o["off"])
+    # fp64 export is recomputed exactly: bitwise equal distances and vectors
+    np.testing.assert_array_equal(g.distance, o["dist"])
+    np.testing.assert_array_equal(g.vector, o["vec"])
+
+
+def check_invariants(g):
+    assert np.all(g.distance <= g.cutoff)
+    assert np.all(g.distance > 0)
+    keys = S.edge_keys(g.src, g.dst, g.image_offset)
+    rev = S.edge_keys(g.dst, g.src, -g.image_offset)
+    np.testing.assert_array_equal(keys, rev)  # reversal closure
+    assert np.all(np.diff(g.dst) >= 0)
+
+
+def test_two_atoms(oracle_c):
+    s = S.random_system(0, (100, 100, 100), 0)
+    s = G.AtomicSystem(np.array([[50.0, 50, 50], [51.0, 50, 50]]), s.lattice, np.array([1, 1], np.int32))
+    g = gpu_graph(s, 2.0)
+    assert g.num_edges() == 2
+    check_invariants(g)
+
+
+def test_self_image_cell(oracle_c):
+    s = G.AtomicSystem(np.array([[0.3, 0.7, 1.1]]), np.eye(3) * 2.0, np.array([2], np.int32))
+    g = gpu_graph(s, 2.5)
+    o = oracle_c.neighbor_list(*S.as_args(s), 2.5, brute=True)
+    assert g.num_edges() == 6
+    assert_same_graph(g, o)
+
+
+@pytest.mark.parametrize("reps", [(3, 3, 3), (5, 5, 5)])
+def test_quartz_vs_oracle(oracle_c, reps):
+    s = S.quartz(reps)
+    g = gpu_graph(s, 5.0)
+    o = oracle_c.neighbor_list(*S.as_args(s), 5.0)
+    assert_same_graph(g, o)
+    check_invariants(g)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_randomized_systems(oracle_c, seed):
+    # proj/tests/test_neighborlist.cpp:82-96
+    box = 4.0 + (seed % 7)
+    n = 5 + seed * 7 % 60
+    s = S.random_triclinic(n, box, seed) if seed % 3 == 0 else S.random_system(n, (box, box + 1.0, box - 0.5), seed)
+    rc = 2.0 + 0.37 * (seed % 5)
+    g = gpu_graph(s, rc)
+    assert_same_graph(g, oracle_c.neighbor_list(*S.as_args(s), rc, brute=True))
+
+
+@pytest.mark.parametrize("seed", range(0, 100, 3))
+def test_acceptance_c5_generator(oracle_c, seed):
+    # acceptance.cpp:255-279 (includes the 2.1-2.4 A self-image cells)
+    if seed % 10 == 0:
+        s = S.random_system(1 + seed % 3, (2.1, 2.4, 2.2), seed)
+        rc = 2.6
+    else:
+        s = S.random_gas(10 + seed * 9, seed)
+        rc = 2.4 + 0.31 * (seed % 6)
+    g = gpu_graph(s, rc)
+    assert_same_graph(g, oracle_c.neighbor_list(*S.as_args(s), rc))
+
+
+def test_non_periodic_padding(oracle_c):
+    s = S.random_system(40, (9.0, 8.0, 7.0), 11)
+    s.pbc = (True, False, False)
+    g = gpu_graph(s, 3.0)
+    assert_same_graph(g, oracle_c.neighbor_list(*S.as_args(s), 3.0))
+
+
+def test_liquid_dense(oracle_c):
+    s = S.liquid(3000)
+    g = gpu_graph(s, 5.0)
+    assert_same_graph(g, oracle_c.neighbor_list(*S.as_args(s), 5.0))
+
+
+def test_errors():
+    s = S.random_system(3, (5, 5, 5), 0)
+    with pytest.raises(G.Error):
+        gpu_graph(s, 0.0)
+    with pytest.raises(G.Error):
+        gpu_graph(s, -1.0)
+    with pytest.raises(G.Error):
+        gpu_graph(G.AtomicSystem(np.zeros((0, 3)), np.eye(3) * 5, np.zeros(0, np.int32)), 2.0)
+
+
+def test_deterministic_rebuild():
+    s = S.random_system(300, (12, 10, 14), 9)
+    a = gpu_graph(s, 3.5)
+    b = gpu_graph(s, 3.5)
+    for x, y in [(a.src, b.src), (a.image_offset, b.image_offset), (a.vector, b.vector)]:
+        np.testing.assert_array_equal(x, y)

@@ -1,0 +1,125 @@
+"""GPU energy / forces / stress vs the fp64 oracle (proj/tests/test_potential.cpp,
+acceptance.cpp criterion 1), and partition invariance of the GPU path.
+
+Tolerances (fp32 compute against the fp64 oracle, stated per quantity):
+  per-atom energy  |dE_i|          <= 2e-5 eV
+  total energy     |dE| / N        <= 2e-6 eV/atom
+  forces           max |dF|        <= 2e-4 eV/A   (and <= 2e-5 relative to max |F|)
+  stress           max |dS|        <= 2e-6 eV/A^3
+"""
+import numpy as np
+import pytest
+
+from paper_2506_02023_b200 import graphmd as G
+from tests import systems as S
+
+pytestmark = pytest.mark.gpu
+
+TOL_EA, TOL_E, TOL_F, TOL_FREL, TOL_S = 2e-5, 2e-6, 2e-4, 2e-5, 2e-6
+
+
+def run_gpu(s, params, p=1, r3=None, allow_narrow=True):
+    d = G.Distributed.create_distributed(s, params.r_atom, r3, p, 1, allow_narrow)
+    return G.forward_distributed(d, params)
+
+
+def compare(out, ref, n):
+    dea = np.abs(out.per_atom - ref["per_atom"]).max()
+    de = abs(out.energy - ref["energy"]) / n
+    df = np.abs(out.forces - ref["forces"]).max()
+    fmax = np.abs(ref["forces"]).max()
+    ds = np.abs(out.stress - ref["stress"]).max()
+    assert dea <= TOL_EA, f"per-atom energy error {dea:.3e}"
+    assert de <= TOL_E, f"energy error per atom {de:.3e}"
+    assert df <= TOL_F and df <= max(TOL_FREL * fmax, 1e-6), f"force error {df:.3e} (max |F| {fmax:.3e})"
+    assert ds <= TOL_S, f"stress error {ds:.3e}"
+    return dea, de, df, ds
+
+
+def params_for(seed, L, rc, r3=0.0):
+    return G.ToyPotentialParams.init(seed, 16, 8, L, rc, r3)
+
+
+def test_c1_quartz_two_body(oracle_c):
+    s = S.quartz((5, 5, 5))
+    prm = params_for(12345, 2, 5.0)
+    ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, 16, 8, 2, 5.0, 0.0)
+    compare(run_gpu(s, prm), ref, s.size())
+
+
+def test_c2_partitioned_equals_unpartitioned():
+    s = S.quartz((5, 5, 5))
+    prm = params_for(12345, 2, 5.0)
+    a = run_gpu(s, prm, p=1)
+    for p in (2, 3, 4, 8):
+        b = run_gpu(s, prm, p=p)
+        # row-form kernels: identical arithmetic for any partition count
+        np.testing.assert_array_equal(a.per_atom, b.per_atom)
+        np.testing.assert_array_equal(a.forces, b.forces)
+        assert a.energy == b.energy
+        np.testing.assert_array_equal(a.stress, b.stress)
+
+
+@pytest.mark.parametrize("r3", [0.0, 2.4])
+@pytest.mark.parametrize("seed", [0, 1, 2, 5, 13])
+def test_random_gas(oracle_c, seed, r3):
+    s = S.random_gas(10 + seed * 22, seed)
+    prm = params_for(s.size(), 2, 4.0, r3)
+    ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, 16, 8, 2, 4.0, r3)
+    for p in (1, 2, 3):
+        if p > s.size():
+            continue
+        compare(run_gpu(s, prm, p=p, r3=r3 if r3 > 0 else None), ref, s.size())
+
+
+@pytest.mark.parametrize("L", [1, 3])
+def test_three_body_quartz(oracle_c, L):
+    s = S.quartz((3, 3, 3))
+    prm = params_for(7, L, 5.0, 3.0)
+    ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, 16, 8, L, 5.0, 3.0)
+    for p in (1, 2, 4):
+        compare(run_gpu(s, prm, p=p, r3=3.0), ref, s.size())
+
+
+def test_three_body_liquid(oracle_c):
+    s = S.liquid(1500)
+    prm = params_for(3, 3, 5.0, 3.0)
+    ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, 16, 8, 3, 5.0, 3.0)
+    compare(run_gpu(s, prm, p=1, r3=3.0), ref, s.size())
+    compare(run_gpu(s, prm, p=4, r3=3.0), ref, s.size())
+
+
+def test_isolated_atom_closed_form():
+    # proj/tests/test_potential.cpp:31-51
+    s = G.AtomicSystem(np.array([[25.0, 25, 25]]), np.eye(3) * 50, np.array([26], np.int32))
+    prm = params_for(5, 2, 4.0)
+    out = run_gpu(s, prm)
+    F = 16
+    h = prm.embedding[26 * F:27 * F].copy()
+    for l in range(2):
+        h = h + np.tanh(prm.layer_b[l * F:(l + 1) * F])
+    assert abs(out.energy - float(prm.readout @ h)) <= 1e-5
+    assert np.all(out.forces == 0.0)
+    assert np.all(out.stress == 0.0)
+
+
+def test_dimer_symmetry():
+    s = G.AtomicSystem(np.array([[14.0, 15, 15], [16.2, 15, 15]]), np.eye(3) * 30, np.array([8, 8], np.int32))
+    out = run_gpu(s, params_for(2, 2, 4.0))
+    np.testing.assert_allclose(out.forces[0], -out.forces[1], atol=1e-6)
+    assert abs(out.forces[0, 1]) < 1e-6 and abs(out.forces[0, 2]) < 1e-6
+
+
+def test_translation_sum_forces_zero():
+    s = S.random_system(80, (9, 9, 9), 4)
+    out = run_gpu(s, params_for(3, 2, 4.0, 2.4), r3=2.4)
+    assert np.abs(out.forces.sum(axis=0)).max() < 1e-4
+
+
+def test_cutoff_mismatch_error():
+    s = S.quartz((2, 2, 2))
+    d = G.Distributed.create_distributed(s, 4.0, None, 1, 1)
+    with pytest.raises(G.Error, match="cutoff does not match"):
+        G.forward_distributed(d, params_for(1, 2, 5.0))
+    with pytest.raises(G.Error, match="require a line graph"):
+        G.forward_distributed(d, params_for(1, 2, 4.0, 3.0))
