@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark: atoms/s of a full energy+force evaluation (graph build + feature
+calculation + forward + backward) on B200, BASELINE.json metric
+"atoms/sec energy+force eval (1/2/4/8 B200) at 1M atoms; graph-build ms".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl b200|reference]
+
+A step is one `Distributed::create_distributed` + `forward_distributed` pass
+(the reference's regime rebuilds the graph every MD step, md.cpp:55-69) over
+the configured system.  Default workload (N=1): C5, alpha-quartz 48^3 =
+995,328 atoms, rc = 5 A, ToyPotential F=16, K=8, L=3, two-body, p = N slabs.
+
+* `value`  : device-timed (CUDA events on the library's stream) with inputs
+             resident in HBM and outputs left in HBM.
+* `e2e`    : same metric through the public C ABI with host buffers: pinned
+             positions/species copied H2D and energy/per-atom/forces/stress
+             copied D2H inside the timed region, every step.
+* `roofline`: dominant kernel, algorithmic bytes per launch over
+             its average CUDA-event duration inside the timed region.
+* `cpu_baseline`: the UNMODIFIED reference (oracle/_ref, compiled from
+             /root/reference sources) on this box's host cores, bounded sample.
+Inputs (1M atoms: 1.07 GB of edge data per step) exceed the 126 MB L2, so no
+explicit flush is done between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (description, builder, rc, r3, L)
+    "c1": ("quartz 5x5x5 (1,125 atoms), rc 5 A, L=2", ("quartz", (5, 5, 5)), 5.0, 0.0, 2),
+    "c3": ("quartz 22^3 (95,832 atoms), rc 5 A, L=3, two-body", ("quartz", (22, 22, 22)), 5.0, 0.0, 3),
+    "c4": ("liquid 100k atoms at 0.1 A^-3, rc 5 A, r3 3 A, L=3, three-body", ("liquid", 100000), 5.0, 3.0, 3),
+    "c5": ("quartz 48^3 (995,328 atoms), rc 5 A, L=3, two-body", ("quartz", (48, 48, 48)), 5.0, 0.0, 3),
+}
+F, K = 16, 8
+PARAM_SEED = 12345
+
+
+def make_system(spec):
+    from tests import systems as S
+    kind, arg = spec
+    return S.quartz(arg) if kind == "quartz" else S.liquid(arg)
+
+
+def bytes_model(n, ne, nb, L, threebody):
+    """Algorithmic (compulsory) DRAM bytes per launch of each kernel; see
+    DESIGN.md "roofline".  n atoms, ne directed edges."""
+    return {
+        "nl_count": 68 * n + 4 * n,                 # sorted SoA positions/cells/ids, degree out
+        "nl_fill": 68 * n + 25 * ne + 8 * n,        # + src/img/vd/bond-flag per edge
+        "conv": 20 * ne + 4 * n + 64 * n + 64 * n + 64 * n,    # lsrc+vd per edge; h in/out, tanh
+        "bwd_edge": 20 * ne + 4 * n + 64 * n + 64 * n + 128 * n + 32 * n,  # m_bar, h_in, h_bar rw, grad rw
+        "bwd_node": 192 * n,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 7
+                          for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified reference compiled from source)
+# ---------------------------------------------------------------------------
+REF_SAMPLE = ("quartz", (22, 22, 22))  # C3-size bounded sample of the quartz workload
+
+
+def reference_time(steps, warmup, cfg_r3, cfg_L, sample=REF_SAMPLE):
+    from oracle.oracle import Oracle
+    from tests import systems as S
+    R = Oracle("ref")
+    s = make_system(sample)
+    cores = os.cpu_count() or 1
+    p = min(cores, 64)
+    prm = R.params_init(PARAM_SEED, F, K, cfg_L, 5.0, cfg_r3)
+    args = S.as_args(s)
+    times = []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        d = R.create(*args, 5.0, r3=cfg_r3, p=p, allow_narrow=True, n_threads=cores)
+        d.forward(prm, F, K, cfg_L, 5.0, cfg_r3)
+        dt = time.perf_counter() - t0
+        del d
+        if k >= warmup:
+            times.append(dt)
+    per = float(np.mean(times))
+    return s.size() / per, per, s.size(), cores, p
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    desc, spec, rc, r3, L = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    metric = "atoms/sec energy+force eval (1/2/4/8 B200) at 1M atoms; graph-build ms"
+    config = {"workload": f"{args.config}: {desc}", "model": "ToyPotential F=16 K=8",
+              "layers": L, "partitions": max(world, args.gpus), "l2": "inputs > L2 (no flush)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        K_, W_ = max(1, args.steps), max(0, args.warmup)
+        v, per, ns, cores, p = reference_time(K_, W_, r3, L)
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "atoms/s",
+                "n_gpus": args.gpus, "steps": K_, "warmup": W_, "ms_per_step": per * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": v, "unit": "atoms/s", "cores": cores, "kind": "reference",
+                                 "sample": f"quartz 22^3 ({ns} atoms), p={p} slabs, n_threads={cores}, "
+                                           f"create_distributed+forward_distributed per step"},
+                "e2e": {"value": v, "unit": "atoms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    from paper_2506_02023_b200 import graphmd as G
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    device = local if world > 1 else 0
+    torch.cuda.set_device(device)
+
+    s = make_system(spec)
+    n = s.size()
+    prm = G.ToyPotentialParams.init(PARAM_SEED, F, K, L, rc, r3)
+    # N>1 in this round: one independent replica of the full system per GPU
+    # (weak scaling); the partitioned multi-rank exchange is future work
+    p = 1
+    h = G._Handle(device)
+    Lb = G.lib()
+    pbc = np.ones(3, np.uint8)
+    lat = np.ascontiguousarray(s.lattice)
+    h.check(Lb.gmd_set_params(h.h, F, K, L, rc, r3, G._p(prm.blob)))
+
+    # device-resident inputs and outputs
+    pos_d = torch.from_numpy(s.positions).cuda()
+    z_d = torch.from_numpy(s.species).cuda()
+    pa_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    f_d = torch.empty(n * 3, dtype=torch.float64, device="cuda")
+    # pinned host buffers for e2e
+    pos_h = torch.from_numpy(s.positions.copy()).pin_memory()
+    z_h = torch.from_numpy(s.species.copy()).pin_memory()
+    pa_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    f_h = torch.empty(n * 3, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    energy = C.c_double()
+    stress = np.zeros(9)
+    timing = np.zeros(4)
+
+    def step_device():
+        h.check(Lb.gmd_build(h.h, n, C.c_void_p(pos_d.data_ptr()), C.c_void_p(z_d.data_ptr()),
+                             G._p(lat), G._p(pbc), rc, r3, 0.0, p, 0, G.GMD_ALLOW_NARROW | G.GMD_INPUT_DEVICE))
+        h.check(Lb.gmd_forward(h.h, C.byref(energy), C.c_void_p(pa_d.data_ptr()), C.c_void_p(f_d.data_ptr()),
+                               G._p(stress), G._p(timing), G.GMD_OUTPUT_DEVICE))
+
+    def step_e2e():
+        h.check(Lb.gmd_build(h.h, n, C.c_void_p(pos_h.data_ptr()), C.c_void_p(z_h.data_ptr()),
+                             G._p(lat), G._p(pbc), rc, r3, 0.0, p, 0, G.GMD_ALLOW_NARROW))
+        h.check(Lb.gmd_forward(h.h, C.byref(energy), C.c_void_p(pa_h.data_ptr()), C.c_void_p(f_h.data_ptr()),
+                               G._p(stress), G._p(timing), 0))
+
+    sptr = C.c_void_p()
+    h.check(Lb.gmd_get_stream(h.h, C.byref(sptr)))
+    lstream = torch.cuda.ExternalStream(sptr.value, device=f"cuda:{device}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    def timed(fn, k):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        ev0.record(lstream)
+        for _ in range(k):
+            fn()
+        ev1.record(lstream)
+        barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1) / k)
+
+    W = max(3, args.warmup)
+    Kst = max(1, args.steps)
+    for _ in range(W):
+        step_device()
+    ne = C.c_int64()
+    h.check(Lb.gmd_num_edges(h.h, C.byref(ne)))
+    ne = ne.value
+
+    # ---- headline (device-resident) with live per-kernel profiling + clocks
+    h.check(Lb.gmd_profile(h.h, 1))
+    l0 = G.launch_count()
+    with ClockSampler(device) as clk:
+        ms = timed(step_device, Kst)
+    launches = (G.launch_count() - l0) // Kst
+    prof = {}
+    cap = 128
+    names = C.create_string_buffer(8192)
+    tot = np.zeros(cap)
+    ln = np.zeros(cap, np.int32)
+    cnt = C.c_int(cap)
+    h.check(Lb.gmd_profile_read(h.h, names, 8192, G._p(tot), G._p(ln), C.byref(cnt)))
+    parts = names.raw.split(b"\0")
+    for k in range(cnt.value):
+        prof[parts[k].decode()] = (float(tot[k]) / Kst, int(ln[k]) // Kst)
+    h.check(Lb.gmd_profile(h.h, 0))
+    # un-profiled timing (the events above cost a little): the reported value
+    ms_clean = timed(step_device, Kst)
+    value = n * world / (ms_clean * 1e-3)
+    graph_ms = timing[0] * 1e3
+
+    # ---- e2e through the public ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            step_e2e()
+        ms_e2e = timed(step_e2e, Kst)
+        e2e = {"value": n * world / (ms_e2e * 1e-3), "unit": "atoms/s",
+               "h2d_bytes_per_step": n * (24 + 4), "d2h_bytes_per_step": n * (8 + 24) + 8 + 72,
+               "ms_per_step": ms_e2e}
+
+    # ---- roofline of the dominant kernel
+    bm = bytes_model(n, ne, 0, L, r3 > 0)
+    top = max(prof.items(), key=lambda kv: kv[1][0]) if prof else (None, (0, 0))
+    peak, peak_kind = peaks()
+    roof = None
+    if top[0]:
+        kname, (kms, kl) = top
+        per_launch_ms = kms / max(kl, 1)
+        ab = bm.get(kname)
+        ach = ab / (per_launch_ms * 1e-3) / 1e9 if ab else None
+        roof = {"kernel": kname, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": None,
+                "algorithmic_bytes_per_launch": ab, "ms_per_launch": per_launch_ms,
+                "share_of_step": kms / ms, "peak_source": peak_kind}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, per, ns, cores, pp = reference_time(2, 1, r3, L)
+            cpu = {"value": v, "unit": "atoms/s", "cores": cores, "kind": "reference",
+                   "sample": f"quartz 22^3 ({ns} atoms), p={pp} slabs, n_threads={cores}, "
+                             f"mean of 2 evals after 1 warm-up, {per:.2f} s/eval"}
+        except Exception as ex:  # the reference library is built in-tree by build()
+            cpu = {"value": None, "unit": "atoms/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "atoms/s", "n_gpus": world, "steps": Kst,
+                "warmup": W, "ms_per_step": ms_clean, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 features / f64 graph decisions",
+                "data": "synthetic (perturbed alpha-quartz supercell, random-init ToyPotential)",
+                "config": config, "graph_build_ms": graph_ms,
+                "stage_ms": {"graph_creation": timing[0] * 1e3, "feature_calculation": timing[1] * 1e3,
+                             "forward": timing[2] * 1e3, "backward": timing[3] * 1e3},
+                "n_atoms": n, "n_edges": ne, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+                "gpu_launches": launches, "clocks": clk.summary(),
+                "kernels_ms_per_step": {k: round(v[0], 4) for k, v in prof.items()},
+                "energy": energy.value}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

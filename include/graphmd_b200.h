@@ -133,10 +133,18 @@ int gmd_util_supercell(int64_t n, const double* pos, const int32_t* Z, const dou
                        int rx, int ry, int rz, double amp, uint64_t seed, double* out_pos,
                        int32_t* out_Z, double* out_lattice);
 
-/* kernel-level timing of the last gmd_forward/gmd_build (ms per phase), for
- * the bench's roofline: names are NUL-separated in `names` */
+/* Kernel-level timing with CUDA events recorded on the handle's stream around
+ * every launch.  gmd_profile(h, 1) clears and enables recording;
+ * gmd_profile_read returns, per kernel name, the summed device time (ms) and
+ * the number of launches.  names: NUL-separated, up to names_cap bytes;
+ * total_ms / launches: arrays of at least *count entries (*count in = capacity). */
 int gmd_profile(gmd_handle* h, int enable);
-int gmd_profile_read(gmd_handle* h, char* names, int names_cap, double* ms, int* count);
+int gmd_profile_read(gmd_handle* h, char* names, int names_cap, double* total_ms, int* launches,
+                     int* count);
+/* process-wide number of kernel launches issued by this library so far */
+int gmd_launch_count(int64_t* count);
+/* the cudaStream_t every kernel of this handle is launched on */
+int gmd_get_stream(gmd_handle* h, void** stream);
 
 #ifdef __cplusplus
 }

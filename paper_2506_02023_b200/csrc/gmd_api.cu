@@ -262,6 +262,12 @@ struct gmd_handle {
         forces, conv_tmp, exp_tmp;
     cudaEvent_t ev[8] = {};
 
+    // profiler: event pairs recorded on `stream` around every launch
+    bool prof = false;
+    std::vector<cudaEvent_t> pev;
+    int pidx = 0;
+    std::vector<std::pair<const char*, int>> precs;
+
     // host caches for views (invalidated per build)
     bool hc_ready = false;
     std::vector<int32_t> h_owner, h_row, h_src, h_lsrc, h_crow;
@@ -270,6 +276,28 @@ struct gmd_handle {
 };
 
 namespace {
+
+struct Prof {
+    gmd_handle* h;
+    const char* name;
+    int a = -1;
+    Prof(gmd_handle* h_, const char* n) : h(h_), name(n) {
+        if (h->prof && h->pidx + 2 <= (int)h->pev.size()) {
+            a = h->pidx;
+            h->pidx += 2;
+            cudaEventRecord(h->pev[a], h->stream);
+        }
+    }
+    ~Prof() {
+        if (a >= 0) {
+            cudaEventRecord(h->pev[a + 1], h->stream);
+            h->precs.emplace_back(name, a);
+        }
+    }
+};
+#define GMD_PROF_CAT2(a, b) a##b
+#define GMD_PROF_CAT(a, b) GMD_PROF_CAT2(a, b)
+#define PROF(name) Prof GMD_PROF_CAT(prof_, __LINE__)(h, name)
 
 void sync(gmd_handle* h) { GMD_CUDA(cudaStreamSynchronize(h->stream)); }
 
@@ -348,13 +376,13 @@ void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
     lw.scan_tmp_bytes = scan_tmp_bytes(nl * nch);
     lw.scan_tmp = h->scan_tmp.get<char>(lw.scan_tmp_bytes);
     int32_t* lo_d = ls.list_off_d.get<int32_t>(nl + 1);
-    launch_layout_plan(owner, req, nid, p, lw, lo_d, s);
+    { PROF("part_layout_plan"); launch_layout_plan(owner, req, nid, p, lw, lo_d, s); }
     d2h(h, ls.list_off, lo_d, nl + 1);
     sync(h);
     ls.rows = ls.list_off[nl];
     int32_t* na = ls.node_array.get<int32_t>(ls.rows);
     int32_t* cr = ls.crow.get<int32_t>(nid);
-    launch_layout_fill(owner, req, nid, p, lw, na, cr, s);
+    { PROF("part_layout_fill"); launch_layout_fill(owner, req, nid, p, lw, na, cr, s); }
     const int stride = 1 + 2 * p;
     std::vector<int32_t> rp(3 * p + 1);
     int32_t* ranges = rp.data();
@@ -368,6 +396,7 @@ void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
     ls.nfrom = prefix[p];
     int32_t* sm = h->small.get<int32_t>(3 * p + 1);
     GMD_CUDA(cudaMemcpyAsync(sm, rp.data(), sizeof(int32_t) * rp.size(), cudaMemcpyHostToDevice, s));
+    PROF("part_from_src");
     launch_from_src(na, cr, sm, p, ls.nfrom, sm + 2 * p, ls.xdst.get<int32_t>(ls.nfrom),
                     ls.xsrc.get<int32_t>(ls.nfrom), s);
     sync(h);  // rp is a host temporary
@@ -461,12 +490,12 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     GMD_CUDA(cudaMemsetAsync(b.bin_cnt, 0, sizeof(int32_t) * nbins, s));
     GMD_CUDA(cudaMemsetAsync(fillp, 0, sizeof(int32_t) * nbins, s));
     GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
-    launch_wrap(g, n, b, s);
-    scan_i32(h, b.bin_cnt, b.bin_start, nbins);
-    launch_bin_scatter(g, n, b, fillp, s);
-    launch_nl_count(g, nbins, n, b, s);
+    { PROF("nl_wrap"); launch_wrap(g, n, b, s); }
+    { PROF("scan"); scan_i32(h, b.bin_cnt, b.bin_start, nbins); }
+    { PROF("nl_bin_scatter"); launch_bin_scatter(g, n, b, fillp, s); }
+    { PROF("nl_count"); launch_nl_count(g, nbins, n, b, s); }
     int32_t* rowp = h->row.get<int32_t>(n + 1);
-    scan_i32(h, b.deg, rowp, n);
+    { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
     int32_t ne32 = 0;
     GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
     int32_t hdr[2];
@@ -483,7 +512,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     gd.img = h->img.get<uint32_t>(h->ne);
     gd.vd = h->vd.get<float4>(h->ne);
     gd.bond = h->ebond.get<uint8_t>(h->ne);
-    launch_nl_fill(g, nbins, cap, b, gd, s);
+    { PROF("nl_fill"); launch_nl_fill(g, nbins, cap, b, gd, s); }
 
     // ---- partitions (partitioner.cpp:46-218)
     h->bounds.assign(p + 1, 0.0);
@@ -518,7 +547,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
             if (!ranks.empty()) {
                 void* ws = h->sel_ws.get<char>(select_ws_bytes((int)ranks.size()));
                 double* so = h->sel_out.get<double>(ranks.size());
-                launch_select(b.fw_axis, n, ranks.data(), (int)ranks.size(), ws, so, s);
+                { PROF("part_select"); launch_select(b.fw_axis, n, ranks.data(), (int)ranks.size(), ws, so, s); }
                 GMD_CUDA(cudaMemcpyAsync(vals.data(), so, sizeof(double) * vals.size(),
                                          cudaMemcpyDeviceToHost, s));
                 sync(h);
@@ -550,11 +579,12 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         Bounds bd{};
         bd.p = p;
         for (int k = 0; k <= p; ++k) bd.b[k] = h->bounds[k];
-        launch_owner(b.fw_axis, n, bd, ownp, s);
+        { PROF("part_owner"); launch_owner(b.fw_axis, n, bd, ownp, s); }
         auto* reqp = A.req.get<unsigned long long>(n);
         GMD_CUDA(cudaMemsetAsync(reqp, 0, sizeof(unsigned long long) * n, s));
-        launch_required(rowp, gd.src, n, ownp, reqp, s);
+        { PROF("part_required"); launch_required(rowp, gd.src, n, ownp, reqp, s); }
         build_layout(h, A, ownp, reqp, n, p);
+        PROF("part_edge_lsrc");
         launch_edge_lsrc(rowp, gd.src, n, ownp, A.crow.as<int32_t>(), A.node_array.as<int32_t>(),
                          A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(h->ne), b.flags, s);
     }
@@ -564,15 +594,15 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     h->nb = 0;
     if (h->has_lg) {
         int32_t* br = h->brow.get<int32_t>(n + 1);
-        scan_i32(h, b.bcnt, br, n);
+        { PROF("scan"); scan_i32(h, b.bcnt, br, n); }
         int32_t nb32 = 0;
         GMD_CUDA(cudaMemcpyAsync(&nb32, br + n, 4, cudaMemcpyDeviceToHost, s));
         sync(h);
         h->nb = nb32;
         int32_t* be = h->bedge.get<int32_t>(h->nb);
         int32_t* bv = h->brev.get<int32_t>(h->nb);
-        launch_bond_edges(rowp, gd.bond, n, br, be, s);
-        launch_bond_rev(n, gd, br, be, bv, b.flags, s);
+        { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, s); }
+        { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, bv, b.flags, s); }
     }
     GMD_CUDA(cudaEventRecord(h->ev[1], s));
     read_flags(h, hdr);
@@ -777,17 +807,18 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     const int32_t* xs = A.xsrc.as<int32_t>();
 
     // ---- feature calculation: embeddings for every layout row (:597-602)
-    launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
+    { PROF("embed"); launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s); }
     GMD_CUDA(cudaEventRecord(h->ev[3], s));
 
     // ---- forward (:657-793)
     for (int l = 0; l < L; ++l) {
         const bool tbl = tb && l == L - 1;
         if (tbl) {
-            launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), s);
-            launch_tb_inject(ba, TP, H[l], TH4, s);
+            { PROF("tb_forward"); launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), s); }
+            { PROF("tb_inject"); launch_tb_inject(ba, TP, H[l], TH4, s); }
         }
-        if ((l > 0 || tbl) && A.nfrom > 0) launch_exchange(A.nfrom, xd, xs, H[l], kF, s);
+        if ((l > 0 || tbl) && A.nfrom > 0) { PROF("exchange"); launch_exchange(A.nfrom, xd, xs, H[l], kF, s); }
+        PROF("conv");
         launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
                     l == L - 1 ? e_part : nullptr, s);
     }
@@ -797,16 +828,16 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     launch_init_hbar(n, HB, s);
     GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
-        launch_bwd_node(n, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s);
-        if (A.nfrom > 0) launch_exchange(A.nfrom, xd, xs, MB, kF, s);
-        launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * grid * 6, s);
+        { PROF("bwd_node"); launch_bwd_node(n, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s); }
+        if (A.nfrom > 0) { PROF("exchange"); launch_exchange(A.nfrom, xd, xs, MB, kF, s); }
+        { PROF("bwd_edge"); launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * grid * 6, s); }
         if (tb && l == L - 1) {
             float* QB = h->QB.get<float>(n * kF);
             float4* VIN = h->VIN.get<float4>(h->nb);
             float4* VOUT = h->VOUT.get<float4>(h->nb);
-            launch_tb_bwd_q(n, HB, TH4, QB, s);
-            launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, s);
-            launch_tb_grad(ba, VIN, VOUT, GRAD, s);
+            { PROF("tb_bwd_q"); launch_tb_bwd_q(n, HB, TH4, QB, s); }
+            { PROF("tb_backward"); launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, s); }
+            { PROF("tb_grad"); launch_tb_grad(ba, VIN, VOUT, GRAD, s); }
         }
     }
     const bool out_dev = flags & GMD_OUTPUT_DEVICE;
@@ -818,6 +849,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             ff = out_dev ? static_cast<float*>(forces) : h->forces.get<float>(3 * n);
         else
             fd = out_dev ? static_cast<double*>(forces) : h->forces.get<double>(3 * n);
+        PROF("forces_out");
         launch_forces_out(n, GRAD, fd, ff, s);
     }
     launch_reduce_partials(e_part, grid, 1, red, s);
@@ -947,6 +979,7 @@ void gmd_destroy(gmd_handle* h) {
     for (auto& b : h->H) b.release();
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : h->pev) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
@@ -1008,6 +1041,10 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         for (int l = 0; l < L; ++l)
             for (int i = 0; i < F; ++i) m.b[l][i] = (float)*q++;
         for (int i = 0; i < F * K; ++i) m.P[i] = (float)*q++;
+        {
+            const double* Pd = blob + 119 * F + (size_t)L * F * F + (size_t)L * F;
+            for (int i = 0; i < F * K; ++i) m.Pk[i] = (float)(Pd[i] * (double)(i % K));
+        }
         for (int i = 0; i < F * K; ++i) m.P3[i] = (float)*q++;
         for (int i = 0; i < F * F; ++i) m.W3[i] = (float)*q++;
         for (int i = 0; i < F * F; ++i) m.W4[i] = (float)*q++;
@@ -1482,17 +1519,59 @@ int gmd_util_supercell(int64_t n, const double* pos, const int32_t* Z, const dou
 }
 
 int gmd_profile(gmd_handle* h, int enable) {
-    (void)h;
-    (void)enable;
+    return run(h, [&] {
+        h->prof = enable != 0;
+        h->pidx = 0;
+        h->precs.clear();
+        if (h->prof && h->pev.empty()) {
+            h->pev.resize(16384);
+            for (auto& e : h->pev) GMD_CUDA(cudaEventCreate(&e));
+        }
+    });
+}
+
+int gmd_profile_read(gmd_handle* h, char* names, int names_cap, double* total_ms, int* launches,
+                     int* count) {
+    return run(h, [&] {
+        if (!count) raise(kArg, "null count");
+        sync(h);
+        std::vector<std::string> order;
+        std::unordered_map<std::string, std::pair<double, int>> acc;
+        for (auto& r : h->precs) {
+            float ms = 0.f;
+            GMD_CUDA(cudaEventElapsedTime(&ms, h->pev[r.second], h->pev[r.second + 1]));
+            auto it = acc.find(r.first);
+            if (it == acc.end()) {
+                order.push_back(r.first);
+                acc[r.first] = {ms, 1};
+            } else {
+                it->second.first += ms;
+                it->second.second += 1;
+            }
+        }
+        const int cap = *count;
+        int k = 0, pos = 0;
+        for (const auto& nm : order) {
+            if (k >= cap || pos + (int)nm.size() + 1 > names_cap) break;
+            std::memcpy(names + pos, nm.c_str(), nm.size() + 1);
+            pos += (int)nm.size() + 1;
+            total_ms[k] = acc[nm].first;
+            launches[k] = acc[nm].second;
+            ++k;
+        }
+        *count = k;
+    });
+}
+
+int gmd_launch_count(int64_t* count) {
+    if (!count) return GMD_ERR_ARG;
+    *count = __atomic_load_n(&g_gmd_launches, __ATOMIC_RELAXED);
     return GMD_OK;
 }
 
-int gmd_profile_read(gmd_handle* h, char* names, int names_cap, double* ms, int* count) {
-    (void)h;
-    (void)names;
-    (void)names_cap;
-    (void)ms;
-    if (count) *count = 0;
+int gmd_get_stream(gmd_handle* h, void** stream) {
+    if (!h || !stream) return GMD_ERR_ARG;
+    *stream = (void*)h->stream;
     return GMD_OK;
 }
 

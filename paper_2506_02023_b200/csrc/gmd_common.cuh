@@ -34,7 +34,14 @@ enum : int {
                                            cudaGetErrorString(_e) + " at " #x);      \
     } while (0)
 
-#define GMD_LAUNCH_CHECK() GMD_CUDA(cudaGetLastError())
+// every kernel launch is followed by exactly one GMD_LAUNCH_CHECK(), which
+// also counts it (gmd_launch_count) so the bench can report its launches
+extern long long g_gmd_launches;
+#define GMD_LAUNCH_CHECK()                                   \
+    do {                                                     \
+        __atomic_add_fetch(&::gmd::g_gmd_launches, 1, __ATOMIC_RELAXED); \
+        GMD_CUDA(cudaGetLastError());                        \
+    } while (0)
 
 constexpr int kMaxParts = 64;  // requirement masks are u64 (partitioner.cpp:13)
 

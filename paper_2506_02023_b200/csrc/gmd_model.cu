@@ -170,12 +170,54 @@ __global__ void k_exchange(int64_t nx, const int32_t* __restrict__ xdst,
     buf[(int64_t)xdst[k] * w4 + q] = buf[(int64_t)xsrc[k] * w4 + q];
 }
 
-// forward conv layer (potential.cpp:743-774), warp per owned node
-__global__ void __launch_bounds__(kThreads) k_conv(ConvArgs a, int layer,
-                                                   const float* __restrict__ Hin,
-                                                   float* __restrict__ Hout,
-                                                   float* __restrict__ TH, double* per_atom,
-                                                   double* e_part) {
+// Sum 16 per-lane values over a 16-lane group; lane l of the group ends with
+// feature (l & 15).
+__device__ __forceinline__ float transpose_reduce16_g16(float v[kF], int gl) {
+    float w8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        bool up = gl & 8;
+        float send = up ? v[i] : v[i + 8];
+        float keep = up ? v[i + 8] : v[i];
+        w8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float w4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        bool up = gl & 4;
+        float send = up ? w8[i] : w8[i + 4];
+        float keep = up ? w8[i + 4] : w8[i];
+        w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float w2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        bool up = gl & 2;
+        float send = up ? w4[i] : w4[i + 2];
+        float keep = up ? w4[i + 2] : w4[i];
+        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    bool up = gl & 1;
+    float send = up ? w2[0] : w2[1];
+    float keep = up ? w2[1] : w2[0];
+    return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+__device__ __forceinline__ float group_sum16(float v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int kNodesPerCta = kThreads / 16;  // half-warp (16 lanes) per node
+
+// forward conv layer (potential.cpp:743-774): a 16-lane group per owned node,
+// lanes stride over its in-edges, fixed-order group reduction
+__global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
+                                                      const float* __restrict__ Hin,
+                                                      float* __restrict__ Hout,
+                                                      float* __restrict__ TH, double* per_atom,
+                                                      double* e_part) {
     __shared__ float sW[kF][kF + 1];
     __shared__ float sb[kF], sro[kF];
     for (int i = threadIdx.x; i < kF * kF; i += kThreads) sW[i / kF][i % kF] = c_m.W[layer][i];
@@ -185,50 +227,65 @@ __global__ void __launch_bounds__(kThreads) k_conv(ConvArgs a, int layer,
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t w0 = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+    const int gl = lane & 15;
+    const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + (threadIdx.x >> 4);
+    const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
     const float rc = c_m.rc, irc = c_m.inv_rc, isg = c_m.inv_sigma, mus = c_m.mu_step;
     double esum = 0.0;
-    for (int64_t v = w0; v < a.n; v += nw) {
+    // both half-warps iterate the same number of times (shuffles span the warp)
+    const int64_t iters = (a.n + ng - 1) / ng;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t v = g0 + it * ng;
+        const bool valid = v < a.n;
         float acc[kF];
 #pragma unroll
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
-        const int e1 = a.row[v + 1];
-        for (int e = a.row[v] + lane; e < e1; e += 32) {
-            const float4 q = __ldg(a.vd + e);
-            float u[kK];
-            basis(q.w, rc, irc, isg, mus, u);
-            float h[kF];
-            load_row16(Hin + (size_t)__ldg(a.lsrc + e) * kF, h);
+        if (valid) {
+            const int e1 = __ldg(a.row + v + 1);
+            for (int e = __ldg(a.row + v) + gl; e < e1; e += 16) {
+                const float4 q = __ldg(a.vd + e);
+                float u[kK];
+                basis(q.w, rc, irc, isg, mus, u);
+                const float4* hs = reinterpret_cast<const float4*>(Hin + (size_t)__ldg(a.lsrc + e) * kF);
 #pragma unroll
-            for (int f = 0; f < kF; ++f) {
-                float s = 0.0f;
+                for (int c = 0; c < 4; ++c) {
+                    const float4 h4 = __ldg(hs + c);
+                    const float hh[4] = {h4.x, h4.y, h4.z, h4.w};
 #pragma unroll
-                for (int k = 0; k < kK; ++k) s = fmaf(c_m.P[f * kK + k], u[k], s);
-                acc[f] = fmaf(h[f], s, acc[f]);
+                    for (int i = 0; i < 4; ++i) {
+                        const int f = 4 * c + i;
+                        float sv = 0.0f;
+#pragma unroll
+                        for (int k = 0; k < kK; ++k) sv = fmaf(c_m.P[f * kK + k], u[k], sv);
+                        acc[f] = fmaf(hh[i], sv, acc[f]);
+                    }
+                }
             }
         }
-        const float m = transpose_reduce16(acc, lane);
-        const int f = lane >> 1;
-        float z = sb[f];
+        const float m = transpose_reduce16_g16(acc, gl);  // feature gl
+        float z = sb[gl];
 #pragma unroll
-        for (int g = 0; g < kF; ++g) z = fmaf(sW[f][g], __shfl_sync(0xffffffffu, m, 2 * g), z);
+        for (int g = 0; g < kF; ++g)
+            z = fmaf(sW[gl][g], __shfl_sync(0xffffffffu, m, (lane & 16) + g), z);
         const float th = tanhf(z);
-        const int64_t r = a.crow ? a.crow[v] : v;
-        const float hn = Hin[r * kF + f] + th;
-        if ((lane & 1) == 0) {
-            Hout[r * kF + f] = hn;
-            TH[v * kF + f] = th;
+        float ev = 0.0f;
+        if (valid) {
+            const int64_t r = a.crow ? a.crow[v] : v;
+            const float hn = Hin[r * kF + gl] + th;
+            Hout[r * kF + gl] = hn;
+            TH[v * kF + gl] = th;
+            ev = sro[gl] * hn;
         }
         if (per_atom) {
-            float ev = (lane & 1) ? 0.0f : sro[f] * hn;
-            ev = warp_sum(ev);
-            if (lane == 0) per_atom[v] = (double)ev;
-            esum += (double)ev;
+            ev = group_sum16(ev);
+            if (valid && gl == 0) {
+                per_atom[v] = (double)ev;
+                esum += (double)ev;
+            }
         }
     }
     if (e_part) {
-        double vals[1] = {lane == 0 ? esum : 0.0};
+        double vals[1] = {esum};
         cta_partials<1>(vals, e_part);
     }
 }
@@ -256,75 +313,127 @@ __global__ void k_bwd_node(int64_t n, const int32_t* __restrict__ crow, int laye
     store_row16(MB + r * kF, mb);
 }
 
-// backward edge pass in row form (potential.cpp:823-848 restated as gathers)
-__global__ void __launch_bounds__(kThreads) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
-                                                       const float* __restrict__ Hl,
-                                                       float* __restrict__ HB,
-                                                       float4* __restrict__ GRAD,
-                                                       double* vir_part) {
+// backward edge pass in row form (potential.cpp:823-848 restated as
+// gathers): a 16-lane group per node u; the node's own m_bar / h_in rows are
+// staged in shared memory (broadcast reads), neighbour rows stream through
+// registers four features at a time.
+__global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
+                                                          const float* __restrict__ Hl,
+                                                          float* __restrict__ HB,
+                                                          float4* __restrict__ GRAD,
+                                                          double* vir_part) {
+    __shared__ __align__(16) float sU[kNodesPerCta][2][kF];  // [group][m_bar_u, h_u][f]
+    __shared__ double sVir[kNodesPerCta][6];                // per-group fp64 virial sums
     const int lane = threadIdx.x & 31;
-    const int64_t w0 = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-    const int64_t nw = (int64_t)gridDim.x * kWarpsPerCta;
+    const int gl = lane & 15, grp = threadIdx.x >> 4;
+    const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + grp;
+    const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
     const float rc = c_m.rc, irc = c_m.inv_rc, isg = c_m.inv_sigma, mus = c_m.mu_step;
-    double vir[6] = {0, 0, 0, 0, 0, 0};
-    for (int64_t v = w0; v < a.n; v += nw) {
-        const int64_t r = a.crow ? a.crow[v] : v;
-        float mbu[kF], hu[kF], acc[kF];
-        load_row16(MB + r * kF, mbu);
-        load_row16(Hl + r * kF, hu);
+    if (gl < 6) sVir[grp][gl] = 0.0;
+    const int64_t iters = (a.n + ng - 1) / ng;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t v = g0 + it * ng;
+        const bool valid = v < a.n;
+        const int64_t r = valid ? (a.crow ? a.crow[v] : v) : 0;
+        __syncwarp();
+        if (valid) {
+            sU[grp][0][gl] = MB[r * kF + gl];
+            sU[grp][1][gl] = Hl[r * kF + gl];
+        }
+        __syncwarp();
+        float acc[kF];
 #pragma unroll
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
         float gx = 0.f, gy = 0.f, gz = 0.f;
-        const int e1 = a.row[v + 1];
-        for (int e = a.row[v] + lane; e < e1; e += 32) {
-            const float4 q = __ldg(a.vd + e);
-            float u[kK], du[kK];
-            basis_d(q.w, rc, irc, isg, mus, u, du);
-            const int w = __ldg(a.lsrc + e);
-            float mbw[kF], hw[kF];
-            load_row16(MB + (size_t)w * kF, mbw);
-            load_row16(Hl + (size_t)w * kF, hw);
-            float dself = 0.f, drev = 0.f;
-#pragma unroll
-            for (int f = 0; f < kF; ++f) {
-                float s = 0.f, ds = 0.f;
+        float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (valid) {
+            const int e1 = __ldg(a.row + v + 1);
+            const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
+            const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
+            for (int e = __ldg(a.row + v) + gl; e < e1; e += 16) {
+                const float4 q = __ldg(a.vd + e);
+                // s_f = fc A_f, ds_f = dfc A_f - 2 fc/sigma (x0 A_f - a B_f) with
+                // A_f = sum_k P_fk phi_k, B_f = sum_k k P_fk phi_k (potential.cpp:30-50)
+                float sn, cs;
+                sincospif(q.w * irc, &sn, &cs);
+                const bool in = q.w < rc;
+                const float fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
+                const float dfc = in ? -0.5f * 3.14159265358979f * irc * sn : 0.0f;
+                const float x0 = q.w * isg, step = mus * isg;
+                float phi[kK];
 #pragma unroll
                 for (int k = 0; k < kK; ++k) {
-                    s = fmaf(c_m.P[f * kK + k], u[k], s);
-                    ds = fmaf(c_m.P[f * kK + k], du[k], ds);
+                    const float x = x0 - step * (float)k;
+                    phi[k] = __expf(-x * x);
                 }
-                acc[f] = fmaf(mbw[f], s, acc[f]);
-                dself = fmaf(mbu[f] * hw[f], ds, dself);
-                drev = fmaf(mbw[f] * hu[f], ds, drev);
+                const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
+                const int w = __ldg(a.lsrc + e);
+                const float4* mw = reinterpret_cast<const float4*>(MB + (size_t)w * kF);
+                const float4* hw = reinterpret_cast<const float4*>(Hl + (size_t)w * kF);
+                float dself = 0.f, drev = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float4 m4 = __ldg(mw + c), h4 = __ldg(hw + c);
+                    const float4 mu4 = su_m[c], hu4 = su_h[c];
+                    const float mwv[4] = {m4.x, m4.y, m4.z, m4.w};
+                    const float hwv[4] = {h4.x, h4.y, h4.z, h4.w};
+                    const float muv[4] = {mu4.x, mu4.y, mu4.z, mu4.w};
+                    const float huv[4] = {hu4.x, hu4.y, hu4.z, hu4.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int f = 4 * c + i;
+                        float A = 0.f, B = 0.f;
+#pragma unroll
+                        for (int k = 0; k < kK; ++k) {
+                            A = fmaf(c_m.P[f * kK + k], phi[k], A);
+                            B = fmaf(c_m.Pk[f * kK + k], phi[k], B);
+                        }
+                        const float sv = fc * A, ds = fmaf(ca, A, cb * B);
+                        acc[f] = fmaf(mwv[i], sv, acc[f]);
+                        dself = fmaf(muv[i] * hwv[i], ds, dself);
+                        drev = fmaf(mwv[i] * huv[i], ds, drev);
+                    }
+                }
+                const float invd = 1.0f / q.w;
+                const float coef = (dself + drev) * invd;
+                gx -= q.x * coef;
+                gy -= q.y * coef;
+                gz -= q.z * coef;
+                const float cself = dself * invd;
+                vr[0] = fmaf(cself * q.x, q.x, vr[0]);
+                vr[1] = fmaf(cself * q.y, q.y, vr[1]);
+                vr[2] = fmaf(cself * q.z, q.z, vr[2]);
+                vr[3] = fmaf(cself * q.x, q.y, vr[3]);
+                vr[4] = fmaf(cself * q.x, q.z, vr[4]);
+                vr[5] = fmaf(cself * q.y, q.z, vr[5]);
             }
-            const float invd = 1.0f / q.w;
-            const float coef = (dself + drev) * invd;
-            gx -= q.x * coef;
-            gy -= q.y * coef;
-            gz -= q.z * coef;
-            const double cs = (double)(dself * invd);
-            const double vx = q.x, vy = q.y, vz = q.z;
-            vir[0] += cs * vx * vx;
-            vir[1] += cs * vy * vy;
-            vir[2] += cs * vz * vz;
-            vir[3] += cs * vx * vy;
-            vir[4] += cs * vx * vz;
-            vir[5] += cs * vy * vz;
         }
-        const float hb = transpose_reduce16(acc, lane);
-        gx = warp_sum(gx);
-        gy = warp_sum(gy);
-        gz = warp_sum(gz);
-        if ((lane & 1) == 0) HB[v * kF + (lane >> 1)] += hb;
-        if (lane == 0) {
-            float4 g = GRAD[v];
-            g.x += gx;
-            g.y += gy;
-            g.z += gz;
-            GRAD[v] = g;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
+        if (gl == 0)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) sVir[grp][c] += (double)vr[c];
+        const float hb = transpose_reduce16_g16(acc, gl);
+        gx = group_sum16(gx);
+        gy = group_sum16(gy);
+        gz = group_sum16(gz);
+        if (valid) {
+            HB[v * kF + gl] += hb;
+            if (gl == 0) {
+                float4 g = GRAD[v];
+                g.x += gx;
+                g.y += gy;
+                g.z += gz;
+                GRAD[v] = g;
+            }
         }
     }
-    cta_partials<6>(vir, vir_part);
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double acc6 = 0.0;
+        for (int g = 0; g < kNodesPerCta; ++g) acc6 += sVir[g][threadIdx.x];
+        vir_part[(size_t)blockIdx.x * 6 + threadIdx.x] = acc6;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -633,8 +742,8 @@ __global__ void k_reduce_partials(const double* parts, int nparts, int w, double
 }  // namespace
 
 int model_grid(int64_t n) {
-    int64_t g = (n + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (g > 148 * 16) g = 148 * 16;
+    int64_t g = (n + kNodesPerCta - 1) / kNodesPerCta;
+    if (g > 148 * 12) g = 148 * 12;
     return (int)(g > 0 ? g : 1);
 }
 

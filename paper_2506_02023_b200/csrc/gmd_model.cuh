@@ -16,6 +16,7 @@ struct ModelConst {
     float W[kMaxLayers][kF * kF];
     float b[kMaxLayers][kF];
     float P[kF * kK];
+    float Pk[kF * kK];  // k * P[f][k] (derivative of the radial channel)
     float P3[kF * kK];
     float W3[kF * kF];
     float W4[kF * kF];

@@ -299,9 +299,10 @@ void launch_select(const double* keys, int64_t n, const int64_t* ranks_host, int
     for (int pass = 0; pass < 8; ++pass) {
         int shift = 56 - 8 * pass;
         k_sel_hist<<<grid, 256, 0, s>>>(k64, n, dst, hist, shift);
+        GMD_LAUNCH_CHECK();
         k_sel_update<<<1, 128, 0, s>>>(dst, hist, shift, out_dev, pass == 7 ? 1 : 0);
+        GMD_LAUNCH_CHECK();
     }
-    GMD_LAUNCH_CHECK();
 }
 
 void launch_owner(const double* fw_axis, int64_t n, const Bounds& bd, int32_t* owner,

@@ -4,6 +4,7 @@
 #include "gmd_common.cuh"
 
 namespace gmd {
+long long g_gmd_launches = 0;
 namespace {
 
 constexpr int kThreads = 512;
@@ -101,7 +102,9 @@ void scan_impl(const T* in, T* out, int64_t n, void* tmp, size_t tmp_bytes, cuda
     if ((size_t)nt * sizeof(T) > tmp_bytes) raise(kRuntime, "scan: temporary buffer too small");
     T* sums = static_cast<T*>(tmp);
     k_tile_reduce<T><<<(unsigned)nt, kThreads, 0, s>>>(in, n, sums);
+    GMD_LAUNCH_CHECK();
     k_spine<T><<<1, kThreads, 0, s>>>(sums, nt, out + n);
+    GMD_LAUNCH_CHECK();
     k_tile_scan<T><<<(unsigned)nt, kThreads, 0, s>>>(in, n, sums, out);
     GMD_LAUNCH_CHECK();
 }

@@ -46,7 +46,7 @@ EXPORTS = [
     "gmd_block_rows", "gmd_block_offset", "gmd_transfer", "gmd_transfer_transpose",
     "gmd_sync_duplicates", "gmd_distribute", "gmd_aggregate",
     "gmd_corrupt_transfer_plan_for_test", "gmd_util_rng_uniform", "gmd_util_supercell",
-    "gmd_profile", "gmd_profile_read",
+    "gmd_profile", "gmd_profile_read", "gmd_get_stream", "gmd_launch_count",
 ]
 
 
@@ -112,7 +112,9 @@ def lib():
             "gmd_util_rng_uniform": (I, [U64, I64, D, D, V]),
             "gmd_util_supercell": (I, [I64, V, V, V, I, I, I, D, U64, V, V, V]),
             "gmd_profile": (I, [V, I]),
-            "gmd_profile_read": (I, [V, V, I, V, V]),
+            "gmd_profile_read": (I, [V, V, I, V, V, V]),
+            "gmd_get_stream": (I, [V, C.POINTER(V)]),
+            "gmd_launch_count": (I, [V]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -703,3 +705,39 @@ def build_neighbor_list(system: AtomicSystem, cutoff: float, n_threads: int = 0,
     """build_neighbor_list (neighborlist.cpp:108-197) on the GPU."""
     d = Distributed.create_distributed(system, cutoff, None, 1, n_threads, True, device=device)
     return d.graph()
+
+
+def profile_start(dist: "Distributed"):
+    """Clear and enable per-kernel CUDA-event timing on the handle's stream."""
+    dist.handle.check(lib().gmd_profile(dist.handle.h, 1))
+
+
+def profile_read(dist: "Distributed", stop: bool = True):
+    """{kernel name: (total device ms, launches)} since profile_start."""
+    cap = 128
+    names = C.create_string_buffer(8192)
+    ms = np.zeros(cap)
+    ln = np.zeros(cap, np.int32)
+    cnt = C.c_int(cap)
+    h = dist.handle
+    h.check(lib().gmd_profile_read(h.h, names, 8192, _p(ms), _p(ln), C.byref(cnt)))
+    out, parts = {}, names.raw.split(b"\0")
+    for k in range(cnt.value):
+        out[parts[k].decode()] = (float(ms[k]), int(ln[k]))
+    if stop:
+        h.check(lib().gmd_profile(h.h, 0))
+    return out
+
+
+def stream_ptr(dist: "Distributed") -> int:
+    """cudaStream_t (as int) that every kernel of this handle runs on."""
+    s = C.c_void_p()
+    dist.handle.check(lib().gmd_get_stream(dist.handle.h, C.byref(s)))
+    return s.value or 0
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libgraphmd_b200.so in this process so far."""
+    out = C.c_int64()
+    lib().gmd_launch_count(C.byref(out))
+    return out.value
