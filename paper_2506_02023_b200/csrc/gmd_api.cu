@@ -250,7 +250,8 @@ struct gmd_handle {
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
     DBuf row, src, img, vd, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
-    DBuf brow, bedge, brev, lcnt, lpairs;
+    DBuf brow, bedge, brev, lcnt, lpairs, slab;
+    int nl_cap = 0;
 
     // model
     bool params_set = false;
@@ -493,17 +494,52 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     { PROF("nl_wrap"); launch_wrap(g, n, b, s); }
     { PROF("scan"); scan_i32(h, b.bin_cnt, b.bin_start, nbins); }
     { PROF("nl_bin_scatter"); launch_bin_scatter(g, n, b, fillp, s); }
-    { PROF("nl_count"); launch_nl_count(g, nbins, n, b, s); }
+    // fp32 prefilter threshold: keeps every pair the fp64 prefilter keeps.
+    // Coordinates are taken relative to the destination bin origin, so each
+    // component is bounded by B = max_k sum_r |L_rk| (s_r + 1) / bins_r; fp32
+    // rounding moves each component of v by at most delta = 4 B 2^-24.
+    float thr32;
+    {
+        double B = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            double bk = 0.0;
+            for (int r = 0; r < 3; ++r)
+                bk += std::abs(g.L[3 * r + k]) * (double)(g.sten[r] + 1) / g.bins[r];
+            B = std::max(B, bk);
+        }
+        B *= 1.01;
+        const double u = std::ldexp(1.0, -24);
+        const double delta = 4.0 * B * u;
+        const double r = std::sqrt(g.pre2) * (1.0 + 1e-9) + std::sqrt(3.0) * delta;
+        const double thr = r * r * (1.0 + 8.0 * u);
+        thr32 = std::nextafter((float)thr, INFINITY);
+    }
+    int cap = h->nl_cap;
+    if (cap <= 0) {  // first build: density estimate of the mean degree
+        const double mean = (double)n * 4.18879020478639 * rc * rc * rc / std::abs(det3(h->lat));
+        cap = 32;
+        while (cap < 1.3 * mean + 24) cap <<= 1;
+    }
     int32_t* rowp = h->row.get<int32_t>(n + 1);
-    { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
-    int32_t ne32 = 0;
-    GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
     int32_t hdr[2];
-    read_flags(h, hdr);
+    int32_t ne32 = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        auto* slab = h->slab.get<unsigned long long>((size_t)n * cap);
+        { PROF("nl_search"); launch_nl_search(g, thr32, nbins, n, cap, b, slab, s); }
+        { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
+        GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
+        read_flags(h, hdr);
+        if (hdr[0] <= cap) break;
+        while (cap < hdr[0]) cap <<= 1;  // rare: an atom exceeded the slab row
+        GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
+    }
+    {   // next build: size the slab from this one's maximum degree
+        int next = 32;
+        while (next < hdr[0] + hdr[0] / 8 + 4) next <<= 1;
+        h->nl_cap = next;
+    }
     if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
     h->ne = ne32;
-    int cap = 32;
-    while (cap < hdr[0]) cap <<= 1;
     GraphDev gd;
     gd.n = n;
     gd.ne = h->ne;
@@ -512,7 +548,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     gd.img = h->img.get<uint32_t>(h->ne);
     gd.vd = h->vd.get<float4>(h->ne);
     gd.bond = h->ebond.get<uint8_t>(h->ne);
-    { PROF("nl_fill"); launch_nl_fill(g, nbins, cap, b, gd, s); }
+    { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s); }
 
     // ---- partitions (partitioner.cpp:46-218)
     h->bounds.assign(p + 1, 0.0);
@@ -966,7 +1002,7 @@ void gmd_destroy(gmd_handle* h) {
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ebond, &h->edst, &h->lsrc, &h->counts,
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
-                    &h->brev, &h->lcnt, &h->lpairs, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
+                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp};
     for (DBuf* b : bufs) b->release();

@@ -102,224 +102,298 @@ __device__ __forceinline__ uint32_t qcode(int qx, int qy, int qz) {
     return ((uint32_t)(qx + 128) << 16) | ((uint32_t)(qy + 128) << 8) | (uint32_t)(qz + 128);
 }
 
-// One CTA per destination bin.  FILL=false counts edges per destination,
-// FILL=true collects (src, image) keys, sorts them and writes the CSR rows.
-template <bool FILL>
-__global__ void __launch_bounds__(kThreads) k_nl(
-    const Geom g, int64_t nbins, int64_t n, int group, int cap,
+// ---------------------------------------------------------------------------
+// Neighbour search, one CTA per destination bin (neighborlist.cpp:154-194).
+//
+//  1. fp32 prefilter: candidate / destination coordinates relative to the
+//     bin origin, rounded to fp32; a pair is dropped only when
+//     |v32|^2 > thr32, a threshold proven (host side, see nl_thr32) to keep
+//     every pair the reference's fp64 prefilter keeps.
+//  2. survivors are compacted into a per-warp queue and tested 32 at a
+//     time with the reference's exact fp64 expressions (prefilter, then the
+//     raw-position test d2 <= rc^2, d2 != 0) -- no divergence in the fp64 path.
+//  3. hits become (src << 24 | image code) keys in a per-destination shared
+//     buffer; at the end each destination's keys are bitonic-sorted by one
+//     warp (canonical (src, image) order, neighborlist.cpp:21-24) and stored
+//     to a fixed-capacity slab; the emit kernel turns slab rows into CSR.
+// ---------------------------------------------------------------------------
+struct CandW {
+    double c[3][32];  // wrapped_j + shift (fp64, reference expression)
+    double p[3][32];  // raw position of j
+    int nc[3][32];    // q - cell_of[j]
+    int jid[32];
+    unsigned qc[32];
+};
+
+__global__ void __launch_bounds__(kThreads) k_nl_search(
+    const Geom g, float thr32, int64_t nbins, int64_t n, int group, int cap,
     const int32_t* __restrict__ bin_start, const int32_t* __restrict__ s_id,
     const double* __restrict__ s_w, const double* __restrict__ s_p,
-    const int32_t* __restrict__ s_c, const double* __restrict__ pos,
-    const int32_t* __restrict__ cell, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
-    const int32_t* __restrict__ row, int32_t* __restrict__ e_src, uint32_t* __restrict__ e_img,
-    float4* __restrict__ e_vd, uint8_t* __restrict__ e_bond, int32_t* __restrict__ bcnt) {
+    const int32_t* __restrict__ s_c, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
+    unsigned long long* __restrict__ slab) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     NLSmem& S = *reinterpret_cast<NLSmem*>(smem_raw);
-    double* d_w = reinterpret_cast<double*>(smem_raw + sizeof(NLSmem));  // group x 3
-    double* d_p = d_w + 3 * group;                                         // group x 3
-    int* d_c = reinterpret_cast<int*>(d_p + 3 * group);                     // group x 3
-    int* d_id = d_c + 3 * group;                                            // group
-    int* d_cnt = d_id + group;                                              // group
-    unsigned long long* keys =
-        reinterpret_cast<unsigned long long*>(smem_raw + sizeof(NLSmem) +
-                                              (((size_t)group * (48 + 20) + 15) & ~(size_t)15));
+    unsigned char* q = smem_raw + sizeof(NLSmem);
+    CandW* cw = reinterpret_cast<CandW*>(q);
+    q += sizeof(CandW) * kWarps;
+    unsigned short* queue = reinterpret_cast<unsigned short*>(q);  // 64 per warp
+    q += sizeof(unsigned short) * 64 * kWarps;
+    q = reinterpret_cast<unsigned char*>(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    float4* d32 = reinterpret_cast<float4*>(q);
+    q += sizeof(float4) * group;
+    double* d_w = reinterpret_cast<double*>(q);
+    q += sizeof(double) * 3 * group;
+    double* d_p = reinterpret_cast<double*>(q);
+    q += sizeof(double) * 3 * group;
+    int* d_c = reinterpret_cast<int*>(q);
+    q += sizeof(int) * 3 * group;
+    int* d_id = reinterpret_cast<int*>(q);
+    q += sizeof(int) * group;
+    int* d_cnt = reinterpret_cast<int*>(q);
+    q += sizeof(int) * group;
+    q = reinterpret_cast<unsigned char*>(((uintptr_t)q + 15) & ~(uintptr_t)15);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(q);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    CandW& C = cw[warp];
+    unsigned short* Q = queue + 64 * warp;
     const int sx = 2 * g.sten[0] + 1, sy = 2 * g.sten[1] + 1, sz = 2 * g.sten[2] + 1;
     const int ncell = sx * sy * sz;
 
     for (int64_t bb = blockIdx.x; bb < nbins; bb += gridDim.x) {
         const int b0 = bin_start[bb], b1 = bin_start[bb + 1];
-        if (b1 == b0) continue;  // uniform across the CTA
+        if (b1 == b0) continue;
         const int bz = (int)(bb % g.bins[2]);
         const int by = (int)((bb / g.bins[2]) % g.bins[1]);
         const int bx = (int)(bb / ((int64_t)g.bins[2] * g.bins[1]));
+        // bin origin (any common origin works; it only conditions fp32)
+        const d3 org = rowvec_rn(g.L, (double)bx / g.bins[0], (double)by / g.bins[1],
+                                 (double)bz / g.bins[2]);
 
         for (int gbase = b0; gbase < b1; gbase += group) {
             const int nd = min(group, b1 - gbase);
             __syncthreads();
             for (int t = threadIdx.x; t < nd; t += kThreads) {
-                int slot = gbase + t;
+                const int slot = gbase + t;
+                double w3[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    d_w[3 * t + k] = s_w[k * n + slot];
+                    w3[k] = s_w[k * n + slot];
+                    d_w[3 * t + k] = w3[k];
                     d_p[3 * t + k] = s_p[k * n + slot];
                     d_c[3 * t + k] = s_c[k * n + slot];
                 }
+                d32[t] = make_float4((float)(w3[0] - org.x), (float)(w3[1] - org.y),
+                                     (float)(w3[2] - org.z), 0.f);
                 d_id[t] = s_id[slot];
                 d_cnt[t] = 0;
             }
             for (int cbase = 0; cbase < ncell; cbase += kSCap) {
                 const int nc = min(kSCap, ncell - cbase);
                 __syncthreads();
-                // stencil batch table: wrapped bin, image q, shift, candidate prefix
                 for (int ci = threadIdx.x; ci < nc; ci += kThreads) {
-                    int c = cbase + ci;
-                    int dz = c % sz - g.sten[2];
-                    int dy = (c / sz) % sy - g.sten[1];
-                    int dx = c / (sz * sy) - g.sten[0];
-                    int cc[3] = {bx + dx, by + dy, bz + dz};
-                    int q[3], cw[3];
+                    const int c = cbase + ci;
+                    const int dz = c % sz - g.sten[2];
+                    const int dy = (c / sz) % sy - g.sten[1];
+                    const int dx = c / (sz * sy) - g.sten[0];
+                    const int cc[3] = {bx + dx, by + dy, bz + dz};
+                    int qv[3], cwb[3];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {  // neighborlist.cpp:165-170
-                        int nb = g.bins[k];
-                        q[k] = cc[k] >= 0 ? cc[k] / nb : -((-cc[k] + nb - 1) / nb);
-                        cw[k] = cc[k] - q[k] * nb;
-                        S.sc_q[ci][k] = q[k];
+                        const int nb = g.bins[k];
+                        qv[k] = cc[k] >= 0 ? cc[k] / nb : -((-cc[k] + nb - 1) / nb);
+                        cwb[k] = cc[k] - qv[k] * nb;
+                        S.sc_q[ci][k] = qv[k];
                     }
                     // shift = L0*q0 + L1*q1 + L2*q2 (neighborlist.cpp:171-173)
-                    d3 sh = rowvec_rn(g.L, (double)q[0], (double)q[1], (double)q[2]);
+                    const d3 sh = rowvec_rn(g.L, (double)qv[0], (double)qv[1], (double)qv[2]);
                     S.sc_shift[ci][0] = sh.x;
                     S.sc_shift[ci][1] = sh.y;
                     S.sc_shift[ci][2] = sh.z;
-                    int64_t wb = ((int64_t)cw[0] * g.bins[1] + cw[1]) * g.bins[2] + cw[2];
+                    const int64_t wb = ((int64_t)cwb[0] * g.bins[1] + cwb[1]) * g.bins[2] + cwb[2];
                     S.sc_bin[ci] = (int)wb;
                     S.sc_pre[ci + 1] = bin_start[wb + 1] - bin_start[wb];
-                    if (q[0] < -128 || q[0] > 127 || q[1] < -128 || q[1] > 127 || q[2] < -128 ||
-                        q[2] > 127)
+                    if (qv[0] < -128 || qv[0] > 127 || qv[1] < -128 || qv[1] > 127 ||
+                        qv[2] < -128 || qv[2] > 127)
                         atomicOr(&flags[1], kErrQRange);
                 }
                 __syncthreads();
-                if (threadIdx.x == 0) {
-                    int acc = 0;
-                    S.sc_pre[0] = 0;
-                    for (int ci = 0; ci < nc; ++ci) {
-                        acc += S.sc_pre[ci + 1];
-                        S.sc_pre[ci + 1] = acc;
+                if (warp == 0) {  // prefix over the batch's candidate counts
+                    int carry = 0;
+                    for (int base = 0; base < nc; base += 32) {
+                        const int ci = base + lane;
+                        int v = ci < nc ? S.sc_pre[ci + 1] : 0;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            int u = __shfl_up_sync(0xffffffffu, v, o);
+                            if (lane >= o) v += u;
+                        }
+                        if (ci < nc) S.sc_pre[ci + 1] = carry + v;
+                        carry += __shfl_sync(0xffffffffu, v, 31);
                     }
+                    if (lane == 0) S.sc_pre[0] = 0;
                 }
                 __syncthreads();
                 const int total = S.sc_pre[nc];
                 for (int kb = warp * 32; kb < total; kb += kThreads) {
                     const int k = kb + lane;
                     const bool valid = k < total;
-                    double cx = 0, cy = 0, cz = 0, px = 0, py = 0, pz = 0;
-                    int nx = 0, ny = 0, nz = 0, jid = 0;
-                    uint32_t qc = 0;
+                    float c32x = 0.f, c32y = 0.f, c32z = 0.f;
                     if (valid) {
-                        int lo = 0, hi = nc - 1;  // last cell with pre <= k
+                        int lo = 0, hi = nc - 1;  // last stencil cell with pre <= k
                         while (lo < hi) {
-                            int mid = (lo + hi + 1) >> 1;
+                            const int mid = (lo + hi + 1) >> 1;
                             if (S.sc_pre[mid] <= k) lo = mid; else hi = mid - 1;
                         }
                         const int ci = lo;
                         const int slot = bin_start[S.sc_bin[ci]] + (k - S.sc_pre[ci]);
-                        // candidate = wrapped_j + shift (neighborlist.cpp:176)
-                        cx = add_rn(s_w[slot], S.sc_shift[ci][0]);
-                        cy = add_rn(s_w[n + slot], S.sc_shift[ci][1]);
-                        cz = add_rn(s_w[2 * n + slot], S.sc_shift[ci][2]);
-                        px = s_p[slot];
-                        py = s_p[n + slot];
-                        pz = s_p[2 * n + slot];
-                        nx = S.sc_q[ci][0] - s_c[slot];
-                        ny = S.sc_q[ci][1] - s_c[n + slot];
-                        nz = S.sc_q[ci][2] - s_c[2 * n + slot];
-                        jid = s_id[slot];
-                        qc = qcode(S.sc_q[ci][0], S.sc_q[ci][1], S.sc_q[ci][2]);
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            // candidate = wrapped_j + shift (neighborlist.cpp:176)
+                            const double cv = add_rn(s_w[d * n + slot], S.sc_shift[ci][d]);
+                            C.c[d][lane] = cv;
+                            C.p[d][lane] = s_p[d * n + slot];
+                            C.nc[d][lane] = S.sc_q[ci][d] - s_c[d * n + slot];
+                        }
+                        C.jid[lane] = s_id[slot];
+                        C.qc[lane] = qcode(S.sc_q[ci][0], S.sc_q[ci][1], S.sc_q[ci][2]);
+                        c32x = (float)(C.c[0][lane] - org.x);
+                        c32y = (float)(C.c[1][lane] - org.y);
+                        c32z = (float)(C.c[2][lane] - org.z);
                     }
+                    __syncwarp();
+                    int qn = 0;
+                    // exact fp64 tests of `cnt` queued (candidate, destination) pairs
+                    auto drain = [&](int cnt) {
+                        if (lane < cnt) {
+                            const unsigned ent = Q[lane];
+                            const int c = ent & 31, t = ent >> 5;
+                            d3 v = {sub_rn(C.c[0][c], d_w[3 * t]), sub_rn(C.c[1][c], d_w[3 * t + 1]),
+                                    sub_rn(C.c[2][c], d_w[3 * t + 2])};
+                            if (!(dot_rn(v, v) > g.pre2)) {  // neighborlist.cpp:177
+                                const int o0 = C.nc[0][c] + d_c[3 * t];
+                                const int o1 = C.nc[1][c] + d_c[3 * t + 1];
+                                const int o2 = C.nc[2][c] + d_c[3 * t + 2];
+                                const d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
+                                const d3 vr = {add_rn(sub_rn(C.p[0][c], d_p[3 * t]), raw.x),
+                                               add_rn(sub_rn(C.p[1][c], d_p[3 * t + 1]), raw.y),
+                                               add_rn(sub_rn(C.p[2][c], d_p[3 * t + 2]), raw.z)};
+                                const double d2 = dot_rn(vr, vr);
+                                if (!(d2 > g.cutoff2) && d2 != 0.0) {  // :189-190
+                                    const int pos = atomicAdd(&d_cnt[t], 1);
+                                    if (pos < cap)
+                                        keys[(size_t)t * cap + pos] =
+                                            ((unsigned long long)(uint32_t)C.jid[c] << 24) | C.qc[c];
+                                }
+                            }
+                        }
+                    };
                     for (int t = 0; t < nd; ++t) {
-                        bool hit = false;
-                        if (valid) {
-                            // prefilter on wrapped positions (neighborlist.cpp:176-177)
-                            d3 v = {sub_rn(cx, d_w[3 * t]), sub_rn(cy, d_w[3 * t + 1]),
-                                    sub_rn(cz, d_w[3 * t + 2])};
-                            if (!(dot_rn(v, v) > g.pre2)) {
-                                // exact test through raw positions (:178-191)
-                                int o0 = nx + d_c[3 * t], o1 = ny + d_c[3 * t + 1],
-                                    o2 = nz + d_c[3 * t + 2];
-                                d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
-                                d3 vr = {add_rn(sub_rn(px, d_p[3 * t]), raw.x),
-                                         add_rn(sub_rn(py, d_p[3 * t + 1]), raw.y),
-                                         add_rn(sub_rn(pz, d_p[3 * t + 2]), raw.z)};
-                                double d2 = dot_rn(vr, vr);
-                                hit = !(d2 > g.cutoff2) && d2 != 0.0;
-                            }
-                        }
-                        unsigned m = __ballot_sync(0xffffffffu, hit);
-                        if (m == 0) continue;
-                        if (!FILL) {
-                            if (lane == 0) atomicAdd(&d_cnt[t], __popc(m));
-                        } else {
-                            int base = 0;
-                            if (lane == 0) base = atomicAdd(&d_cnt[t], __popc(m));
-                            base = __shfl_sync(0xffffffffu, base, 0);
-                            if (hit) {
-                                int pos_k = base + __popc(m & ((1u << lane) - 1u));
-                                if (pos_k < cap)
-                                    keys[(size_t)t * cap + pos_k] =
-                                        ((unsigned long long)(uint32_t)jid << 24) | qc;
-                                else
-                                    atomicOr(&flags[1], kErrCap);
-                            }
+                        const float4 dd = d32[t];
+                        const float vx = c32x - dd.x, vy = c32y - dd.y, vz = c32z - dd.z;
+                        const bool pass = valid && fmaf(vz, vz, fmaf(vy, vy, vx * vx)) <= thr32;
+                        const unsigned m = __ballot_sync(0xffffffffu, pass);
+                        if (m == 0u) continue;
+                        if (pass) Q[qn + __popc(m & ((1u << lane) - 1u))] = (unsigned short)(lane | (t << 5));
+                        qn += __popc(m);
+                        __syncwarp();
+                        if (qn >= 32) {
+                            drain(32);
+                            __syncwarp();
+                            unsigned short mv = lane < qn - 32 ? Q[32 + lane] : 0;
+                            __syncwarp();
+                            if (lane < qn - 32) Q[lane] = mv;
+                            qn -= 32;
+                            __syncwarp();
                         }
                     }
+                    drain(qn);
+                    __syncwarp();
                 }
             }
             __syncthreads();
-            if (!FILL) {
-                for (int t = threadIdx.x; t < nd; t += kThreads) {
-                    deg[d_id[t]] = d_cnt[t];
-                    atomicMax(&flags[0], d_cnt[t]);
-                }
-            } else {
-                for (int t = warp; t < nd; t += kWarps) {
-                    const int cnt = min(d_cnt[t], cap);
-                    unsigned long long* kk = keys + (size_t)t * cap;
-                    int P = 1;
-                    while (P < cnt) P <<= 1;
-                    for (int k = cnt + lane; k < P; k += 32) kk[k] = ~0ull;
-                    __syncwarp();
-                    for (int sz2 = 2; sz2 <= P; sz2 <<= 1)
-                        for (int j = sz2 >> 1; j > 0; j >>= 1) {
-                            for (int i = lane; i < P; i += 32) {
-                                int ixj = i ^ j;
-                                if (ixj > i) {
-                                    unsigned long long a = kk[i], c2 = kk[ixj];
-                                    bool up = (i & sz2) == 0;
-                                    if ((a > c2) == up) {
-                                        kk[i] = c2;
-                                        kk[ixj] = a;
-                                    }
+            for (int t = warp; t < nd; t += kWarps) {
+                const int full = d_cnt[t];
+                const int cnt = min(full, cap);
+                unsigned long long* kk = keys + (size_t)t * cap;
+                int P = 1;
+                while (P < cnt) P <<= 1;
+                for (int k = cnt + lane; k < P; k += 32) kk[k] = ~0ull;
+                __syncwarp();
+                for (int sz2 = 2; sz2 <= P; sz2 <<= 1)
+                    for (int j = sz2 >> 1; j > 0; j >>= 1) {
+                        for (int i = lane; i < P; i += 32) {
+                            const int ixj = i ^ j;
+                            if (ixj > i) {
+                                const unsigned long long a = kk[i], c2 = kk[ixj];
+                                const bool up = (i & sz2) == 0;
+                                if ((a > c2) == up) {
+                                    kk[i] = c2;
+                                    kk[ixj] = a;
                                 }
                             }
-                            __syncwarp();
                         }
-                    const int did = d_id[t];
-                    const int e0 = row[did];
-                    int nb = 0;
-                    for (int k = lane; k < ((cnt + 31) & ~31); k += 32) {
-                        bool isb = false;
-                        if (k < cnt) {
-                            unsigned long long key = kk[k];
-                            int j = (int)(key >> 24);
-                            int q0 = (int)((key >> 16) & 255) - 128;
-                            int q1 = (int)((key >> 8) & 255) - 128;
-                            int q2 = (int)(key & 255) - 128;
-                            // off = image - cell_of[j] + cell_of[i] (neighborlist.cpp:179-180)
-                            int o0 = q0 - cell[3 * j] + d_c[3 * t];
-                            int o1 = q1 - cell[3 * j + 1] + d_c[3 * t + 1];
-                            int o2 = q2 - cell[3 * j + 2] + d_c[3 * t + 2];
-                            if (!img_in_range(o0) || !img_in_range(o1) || !img_in_range(o2))
-                                atomicOr(&flags[1], kErrImgRange);
-                            d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
-                            d3 vr = {add_rn(sub_rn(pos[3 * j], d_p[3 * t]), raw.x),
-                                     add_rn(sub_rn(pos[3 * j + 1], d_p[3 * t + 1]), raw.y),
-                                     add_rn(sub_rn(pos[3 * j + 2], d_p[3 * t + 2]), raw.z)};
-                            double dd = __dsqrt_rn(dot_rn(vr, vr));
-                            const int e = e0 + k;
-                            e_src[e] = j;
-                            e_img[e] = pack_img(o0, o1, o2);
-                            e_vd[e] = make_float4((float)vr.x, (float)vr.y, (float)vr.z, (float)dd);
-                            isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
-                            e_bond[e] = isb ? 1 : 0;
-                        }
-                        nb += __popc(__ballot_sync(0xffffffffu, isb));
+                        __syncwarp();
                     }
-                    if (lane == 0) bcnt[did] = nb;
+                const int did = d_id[t];
+                unsigned long long* dst = slab + (size_t)did * cap;
+                for (int k = lane; k < cnt; k += 32) dst[k] = kk[k];
+                if (lane == 0) {
+                    deg[did] = full;
+                    atomicMax(&flags[0], full);
                 }
             }
         }
     }
+}
+
+// slab rows -> canonical CSR (neighborlist.cpp:60-85): recompute the exact
+// fp64 vector through the raw positions (:178-191) from (src, image), round
+// to fp32 for the model, mark three-body bonds (linegraph.cpp:34-35).
+__global__ void k_nl_emit(const Geom g, int64_t n, int cap,
+                          const unsigned long long* __restrict__ slab,
+                          const int32_t* __restrict__ row, const double* __restrict__ pos,
+                          const int32_t* __restrict__ cell, int32_t* __restrict__ e_src,
+                          uint32_t* __restrict__ e_img, float4* __restrict__ e_vd,
+                          uint8_t* __restrict__ e_bond, int32_t* __restrict__ bcnt,
+                          int32_t* __restrict__ flags) {
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const int lane = threadIdx.x & 31;
+    const int e0 = row[i], cnt = row[i + 1] - e0;
+    const double pix = pos[3 * i], piy = pos[3 * i + 1], piz = pos[3 * i + 2];
+    const int cix = cell[3 * i], ciy = cell[3 * i + 1], ciz = cell[3 * i + 2];
+    int nb = 0;
+    for (int kb = 0; kb < cnt; kb += 32) {
+        const int k = kb + lane;
+        bool isb = false;
+        if (k < cnt) {
+            const unsigned long long key = slab[(size_t)i * cap + k];
+            const int j = (int)(key >> 24);
+            const int q0 = (int)((key >> 16) & 255) - 128;
+            const int q1 = (int)((key >> 8) & 255) - 128;
+            const int q2 = (int)(key & 255) - 128;
+            // off = image - cell_of[j] + cell_of[i] (neighborlist.cpp:179-180)
+            const int o0 = q0 - cell[3 * j] + cix;
+            const int o1 = q1 - cell[3 * j + 1] + ciy;
+            const int o2 = q2 - cell[3 * j + 2] + ciz;
+            if (!img_in_range(o0) || !img_in_range(o1) || !img_in_range(o2))
+                atomicOr(&flags[1], kErrImgRange);
+            const d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
+            const d3 vr = {add_rn(sub_rn(pos[3 * j], pix), raw.x),
+                           add_rn(sub_rn(pos[3 * j + 1], piy), raw.y),
+                           add_rn(sub_rn(pos[3 * j + 2], piz), raw.z)};
+            const double dd = __dsqrt_rn(dot_rn(vr, vr));
+            const int e = e0 + k;
+            e_src[e] = j;
+            e_img[e] = pack_img(o0, o1, o2);
+            e_vd[e] = make_float4((float)vr.x, (float)vr.y, (float)vr.z, (float)dd);
+            isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
+            e_bond[e] = isb ? 1 : 0;
+        }
+        nb += __popc(__ballot_sync(0xffffffffu, isb));
+    }
+    if (lane == 0) bcnt[i] = nb;
 }
 
 __global__ void k_minmax_proj(const double* __restrict__ pos, int64_t n, double dx, double dy,
@@ -439,9 +513,12 @@ __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
     }
 }
 
-size_t nl_smem(int group, int cap, bool fill) {
-    size_t s = sizeof(NLSmem) + (((size_t)group * (48 + 20) + 15) & ~(size_t)15);
-    if (fill) s += (size_t)group * cap * 8;
+size_t nl_smem(int group, int cap) {
+    size_t s = sizeof(NLSmem) + sizeof(CandW) * kWarps + sizeof(unsigned short) * 64 * kWarps;
+    s = (s + 15) & ~(size_t)15;
+    s += (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
+    s = (s + 15) & ~(size_t)15;
+    s += (size_t)group * cap * 8;
     return s;
 }
 
@@ -463,29 +540,29 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
     GMD_LAUNCH_CHECK();
 }
 
-void launch_nl_count(const Geom& g, int64_t nbins, int64_t n, NLBuffers& b, cudaStream_t s) {
-    const int group = 64;
-    size_t sm = nl_smem(group, 0, false);
-    k_nl<false><<<nl_grid(nbins), kThreads, sm, s>>>(
-        g, nbins, n, group, 0, b.bin_start, b.s_id, b.s_w, b.s_p, b.s_c, b.pos, b.cell, b.deg,
-        b.flags, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
+                      NLBuffers& b, unsigned long long* slab, cudaStream_t s) {
+    int group = 32;
+    while (group > 2 && (size_t)group * cap * 8 > 64 * 1024) group >>= 1;
+    const size_t sm = nl_smem(group, cap);
+    if (sm > 200 * 1024) raise(kRuntime, "neighbour search: per-atom degree too large");
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_nl_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        attr = true;
+    }
+    k_nl_search<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, nbins, n, group, cap, b.bin_start,
+                                                     b.s_id, b.s_w, b.s_p, b.s_c, b.deg, b.flags,
+                                                     slab);
     GMD_LAUNCH_CHECK();
 }
 
-void launch_nl_fill(const Geom& g, int64_t nbins, int cap, NLBuffers& b, GraphDev& gd,
-                    cudaStream_t s) {
-    int group = 32;
-    while (group > 1 && (size_t)group * cap * 8 > 96 * 1024) group >>= 1;
-    size_t sm = nl_smem(group, cap, true);
-    static bool attr_set = false;
-    if (!attr_set) {
-        GMD_CUDA(cudaFuncSetAttribute(k_nl<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-        attr_set = true;
-    }
-    k_nl<true><<<nl_grid(nbins), kThreads, sm, s>>>(
-        g, nbins, gd.n, group, cap, b.bin_start, b.s_id, b.s_w, b.s_p, b.s_c, b.pos, b.cell,
-        b.deg, b.flags, gd.row, gd.src, gd.img, gd.vd, gd.bond, b.bcnt);
+void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long* slab,
+                    NLBuffers& b, GraphDev& gd, cudaStream_t s) {
+    if (n == 0) return;
+    k_nl_emit<<<div_up(n, 8), 256, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src, gd.img,
+                                           gd.vd, gd.bond, b.bcnt, b.flags);
     GMD_LAUNCH_CHECK();
 }
 

@@ -51,9 +51,13 @@ enum : int { kErrImgRange = 1, kErrQRange = 2, kErrCap = 4 };
 
 void launch_wrap(const Geom& g, int64_t n, NLBuffers& b, cudaStream_t s);
 void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, cudaStream_t s);
-void launch_nl_count(const Geom& g, int64_t nbins, int64_t n, NLBuffers& b, cudaStream_t s);
-void launch_nl_fill(const Geom& g, int64_t nbins, int cap, NLBuffers& b, GraphDev& gd,
-                    cudaStream_t s);
+// search: per-destination sorted (src, image) keys into slab[n x cap], true
+// degrees into deg, max degree into flags[0] (slab rows truncated at cap)
+void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
+                      NLBuffers& b, unsigned long long* slab, cudaStream_t s);
+// emit: slab rows -> CSR (row must hold the scanned degrees)
+void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long* slab,
+                    NLBuffers& b, GraphDev& gd, cudaStream_t s);
 void launch_minmax_proj(const double* pos, int64_t n, const double dir[3], double* out2,
                         cudaStream_t s);
 void launch_shift(double* pos, int64_t n, const double add[3], cudaStream_t s);

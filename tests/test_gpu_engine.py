@@ -80,6 +80,12 @@ def test_transpose_is_adjoint(p, bonds):
     g = torch.Generator(device="cuda").manual_seed(p)
     x.data.copy_(torch.randn(x.data.shape, generator=g, device="cuda", dtype=torch.float64))
     y.data.copy_(torch.randn(y.data.shape, generator=g, device="cuda", dtype=torch.float64))
+    # transfer overwrites FROM spans and the transpose folds duplicates, so x
+    # needs zero FROM rows and synced duplicates (test_engine.cpp:101-147)
+    parts = d.line_parts().parts if bonds else d.atom_parts().parts
+    for i, pt in enumerate(parts):
+        x.block(i)[pt.layout.owned_end():] = 0.0
+    (d.sync_bond_duplicates if bonds else d.sync_atom_duplicates)(x)
     tx = mk(3)
     tx.data.copy_(x.data)
     (d.bond_transfer if bonds else d.atom_transfer)(tx)
