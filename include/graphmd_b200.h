@@ -41,9 +41,11 @@ extern "C" {
 #define GMD_OUTPUT_DEVICE 1u  /* output pointers are device pointers */
 #define GMD_OUTPUT_F32 2u     /* per_atom / forces are float instead of double */
 
-/* feature dtypes */
+/* feature dtypes; OR GMD_HOST_MEMORY into dtype when the feature buffer of a
+ * feature-API call is host memory (it is staged through device scratch) */
 #define GMD_F32 0
 #define GMD_F64 1
+#define GMD_HOST_MEMORY 0x100
 
 typedef struct gmd_handle gmd_handle;
 

@@ -1,0 +1,601 @@
+// graphmd_b200/graphmd.hpp -- C++ drop-in for the reference's plugin API.
+//
+// Callers of the reference (md.cpp, graphmd_cli, tests) include this header
+// instead of <graphmd/engine.hpp> + <graphmd/potential.hpp> and link
+// libgraphmd_b200.so; the names, argument meanings and the Error type are the
+// reference's (proj/include/graphmd/{system,neighborlist,partitioner,
+// linegraph,engine,potential}.hpp), the work runs on the GPU through the C ABI
+// in graphmd_b200.h.  Views (graph(), atom_parts(), line_parts()) are
+// materialized from device data on first use.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../graphmd_b200.h"
+
+namespace graphmd {
+
+// ---- errors (system.hpp:13-15) -----------------------------------------
+struct Error : std::runtime_error {
+    explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+
+namespace detail {
+inline void check(const gmd_handle* h, int rc) {
+    if (rc != GMD_OK) throw Error(gmd_last_error(h));
+}
+}  // namespace detail
+
+// ---- geometry (system.hpp:17-94) -----------------------------------------
+struct Vec3 {
+    double x = 0, y = 0, z = 0;
+    Vec3() = default;
+    Vec3(double a, double b, double c) : x(a), y(b), z(c) {}
+    double& operator[](int i) { return i == 0 ? x : i == 1 ? y : z; }
+    double operator[](int i) const { return i == 0 ? x : i == 1 ? y : z; }
+    Vec3 operator+(const Vec3& o) const { return {x + o.x, y + o.y, z + o.z}; }
+    Vec3 operator-(const Vec3& o) const { return {x - o.x, y - o.y, z - o.z}; }
+    Vec3 operator*(double s) const { return {x * s, y * s, z * s}; }
+    Vec3 operator/(double s) const { return {x / s, y / s, z / s}; }
+    Vec3 operator-() const { return {-x, -y, -z}; }
+    Vec3& operator+=(const Vec3& o) { return *this = *this + o; }
+    Vec3& operator-=(const Vec3& o) { return *this = *this - o; }
+    Vec3& operator*=(double s) { return *this = *this * s; }
+    double dot(const Vec3& o) const { return x * o.x + y * o.y + z * o.z; }
+    Vec3 cross(const Vec3& o) const {
+        return {y * o.z - z * o.y, z * o.x - x * o.z, x * o.y - y * o.x};
+    }
+    double norm2() const { return dot(*this); }
+    double norm() const { return std::sqrt(norm2()); }
+};
+inline Vec3 operator*(double s, const Vec3& v) { return v * s; }
+
+struct Mat3 {
+    std::array<Vec3, 3> rows{};
+    Vec3& operator[](int i) { return rows[i]; }
+    const Vec3& operator[](int i) const { return rows[i]; }
+    double det() const { return rows[0].dot(rows[1].cross(rows[2])); }
+    Vec3 rowvec_mul(const Vec3& v) const { return rows[0] * v.x + rows[1] * v.y + rows[2] * v.z; }
+    static Mat3 identity() {
+        Mat3 m;
+        m.rows = {Vec3{1, 0, 0}, Vec3{0, 1, 0}, Vec3{0, 0, 1}};
+        return m;
+    }
+};
+
+struct AtomicSystem {
+    std::vector<Vec3> positions;
+    Mat3 lattice = Mat3::identity();
+    std::vector<int> species;
+    std::array<bool, 3> pbc{true, true, true};
+    std::size_t size() const { return positions.size(); }
+    bool any_pbc() const { return pbc[0] || pbc[1] || pbc[2]; }
+    void validate() const {
+        if (species.size() != positions.size()) throw Error("species length does not match atom count");
+        if (any_pbc() && std::abs(lattice.det()) < 1e-10)
+            throw Error("periodic system requires an invertible lattice");
+    }
+};
+
+// make_supercell + random_perturb on the library's host RNG (system.cpp:188-240)
+inline AtomicSystem make_supercell(const AtomicSystem& s, const std::array<int, 3>& reps,
+                                   double amplitude = 0.0, std::uint64_t seed = 0) {
+    const std::size_t n = s.size(), f = (std::size_t)reps[0] * reps[1] * reps[2];
+    std::vector<double> pos(3 * n), lat(9), opos(3 * n * f), olat(9);
+    std::vector<int32_t> z(s.species.begin(), s.species.end()), oz(n * f);
+    for (std::size_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) pos[3 * i + k] = s.positions[i][k];
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) lat[3 * r + k] = s.lattice[r][k];
+    int rc = gmd_util_supercell((int64_t)n, pos.data(), z.data(), lat.data(), reps[0], reps[1],
+                                reps[2], amplitude, seed, opos.data(), oz.data(), olat.data());
+    if (rc != GMD_OK) throw Error("supercell repetitions must be >= 1");
+    AtomicSystem o;
+    o.pbc = s.pbc;
+    o.positions.resize(n * f);
+    o.species.assign(oz.begin(), oz.end());
+    for (std::size_t i = 0; i < n * f; ++i) o.positions[i] = {opos[3 * i], opos[3 * i + 1], opos[3 * i + 2]};
+    for (int r = 0; r < 3; ++r) o.lattice[r] = {olat[3 * r], olat[3 * r + 1], olat[3 * r + 2]};
+    return o;
+}
+inline AtomicSystem random_perturb(const AtomicSystem& s, double amplitude, std::uint64_t seed) {
+    if (amplitude < 0.0) throw Error("perturbation amplitude must be >= 0");
+    return make_supercell(s, {1, 1, 1}, amplitude, seed);
+}
+
+// ---- graph / partition / line-graph views -----------------------------
+using Offset3 = std::array<int, 3>;
+
+struct AtomGraph {  // neighborlist.hpp:17-33
+    std::vector<std::int64_t> src, dst;
+    std::vector<Offset3> image_offset;
+    std::vector<double> distance;
+    std::vector<Vec3> vector;
+    double cutoff = 0.0;
+    std::int64_t num_nodes = 0;
+    std::size_t num_edges() const { return src.size(); }
+    std::pair<std::size_t, std::size_t> edges_into(std::int64_t node) const {
+        std::size_t lo = 0, hi = dst.size();
+        while (lo < hi) {
+            std::size_t m = (lo + hi) / 2;
+            if (dst[m] < node) lo = m + 1; else hi = m;
+        }
+        std::size_t e = lo;
+        while (e < dst.size() && dst[e] == node) ++e;
+        return {lo, e};
+    }
+};
+
+struct PartitionRule {  // partitioner.hpp:16-20
+    int axis = 0;
+    std::vector<double> boundaries;
+    int p = 1;
+};
+enum class BoundaryMode { kQuantile, kEqualWidth };
+
+struct Buckets {
+    std::vector<std::vector<std::int64_t>> pure;
+    std::vector<std::vector<std::vector<std::int64_t>>> to, from;
+};
+
+struct Span {
+    std::int64_t begin = 0, end = 0;
+    std::int64_t size() const { return end - begin; }
+};
+
+struct SpanLayout {  // partitioner.hpp:45-63 (global_to_local as a sorted probe)
+    std::vector<std::int64_t> node_array;
+    std::vector<std::int64_t> markers;
+    std::vector<std::pair<std::int64_t, std::int64_t>> duplicates;
+    int p = 1;
+    Span pure_span() const { return {markers[0], markers[1]}; }
+    Span to_span(int j) const { return {markers[1 + j], markers[2 + j]}; }
+    Span from_span(int j) const { return {markers[1 + p + j], markers[2 + p + j]}; }
+    std::int64_t owned_end() const { return markers[1 + p]; }
+    std::int64_t size() const { return (std::int64_t)node_array.size(); }
+    std::int64_t local_of(std::int64_t g) const {
+        for (std::size_t r = 0; r < node_array.size(); ++r)
+            if (node_array[r] == g) return (std::int64_t)r;
+        return -1;
+    }
+};
+
+struct AtomPartition {
+    SpanLayout layout;
+    std::vector<std::int64_t> owned_edges, local_src, local_dst, border_edge_list;
+};
+
+struct PartitionedAtomGraph {
+    PartitionRule rule;
+    Buckets buckets;
+    std::vector<int> owner;
+    std::vector<AtomPartition> parts;
+    int p = 1;
+};
+
+struct BondSet {
+    std::vector<std::int64_t> edge_of_bond, bond_of_edge;
+    double r = 0.0, tau = 0.0;
+    std::size_t size() const { return edge_of_bond.size(); }
+};
+
+struct LineGraphPartition {
+    SpanLayout layout;
+    std::vector<std::pair<std::int64_t, std::int64_t>> line_edges;
+};
+
+struct PartitionedLineGraph {
+    BondSet bonds;
+    std::vector<int> bond_owner;
+    Buckets bond_buckets;
+    std::vector<LineGraphPartition> parts;
+    int p = 1;
+};
+
+// ---- engine (engine.hpp:18-151) -----------------------------------------
+struct DistributedFeatures {
+    std::vector<std::vector<double>> blocks;
+    std::int64_t width = 0;
+    double* row(int part, std::int64_t local) { return blocks[part].data() + local * width; }
+    const double* row(int part, std::int64_t local) const { return blocks[part].data() + local * width; }
+};
+
+struct StepTiming {
+    double graph_creation = 0, feature_calculation = 0, forward_pass = 0, backward_pass = 0;
+    static const std::vector<std::string>& category_names() {
+        static const std::vector<std::string> n = {"Graph Creation", "Feature Calculation",
+                                                   "Forward Pass", "Backward Pass"};
+        return n;
+    }
+    double total() const { return graph_creation + feature_calculation + forward_pass + backward_pass; }
+    StepTiming& operator+=(const StepTiming& o) {
+        graph_creation += o.graph_creation;
+        feature_calculation += o.feature_calculation;
+        forward_pass += o.forward_pass;
+        backward_pass += o.backward_pass;
+        return *this;
+    }
+};
+
+class Distributed {
+public:
+    static Distributed create_distributed(const AtomicSystem& system, double atom_cutoff,
+                                          std::optional<double> threebody_cutoff, int p,
+                                          int n_threads, bool allow_narrow = false,
+                                          double threebody_tau = 0.0, int device = 0) {
+        Distributed d;
+        gmd_handle* raw = nullptr;
+        int rc = gmd_create(device, &raw);
+        if (rc != GMD_OK) throw Error(gmd_last_error(nullptr));
+        d.h_.reset(raw, [](gmd_handle* x) { gmd_destroy(x); });
+        d.p_ = p;
+        d.n_threads_ = n_threads > 0 ? n_threads : 1;
+        d.cutoff_ = atom_cutoff;
+        d.r3_ = threebody_cutoff;
+        d.tau_ = threebody_tau;
+        const std::size_t n = system.size();
+        std::vector<double> pos(3 * n), lat(9);
+        std::vector<int32_t> z(system.species.begin(), system.species.end());
+        for (std::size_t i = 0; i < n; ++i)
+            for (int k = 0; k < 3; ++k) pos[3 * i + k] = system.positions[i][k];
+        for (int r = 0; r < 3; ++r)
+            for (int k = 0; k < 3; ++k) lat[3 * r + k] = system.lattice[r][k];
+        uint8_t pbc[3] = {system.pbc[0], system.pbc[1], system.pbc[2]};
+        if (z.size() != n) throw Error("species length does not match atom count");
+        detail::check(d.h_.get(),
+                      gmd_build(d.h_.get(), (int64_t)n, pos.data(), z.data(), lat.data(), pbc,
+                                atom_cutoff, threebody_cutoff ? *threebody_cutoff : 0.0,
+                                threebody_tau, p, n_threads, allow_narrow ? GMD_ALLOW_NARROW : 0u));
+        d.system_ = system;
+        return d;
+    }
+
+    int num_partitions() const { return p_; }
+    int num_threads() const { return n_threads_; }
+    bool has_line_graph() const {
+        int y = 0;
+        gmd_has_line_graph(h_.get(), &y);
+        return y != 0;
+    }
+    gmd_handle* handle() const { return h_.get(); }
+
+    const AtomicSystem& system() const {  // after ensure_periodic
+        if (!sys_ready_) {
+            int64_t n = 0;
+            gmd_num_nodes(h_.get(), &n);
+            std::vector<double> pos(3 * n), lat(9);
+            detail::check(h_.get(), gmd_get_system(h_.get(), pos.data(), lat.data()));
+            AtomicSystem s;
+            s.species = system_.species;
+            s.positions.resize(n);
+            for (int64_t i = 0; i < n; ++i) s.positions[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            for (int r = 0; r < 3; ++r) s.lattice[r] = {lat[3 * r], lat[3 * r + 1], lat[3 * r + 2]};
+            periodic_ = s;
+            sys_ready_ = true;
+        }
+        return periodic_;
+    }
+
+    const AtomGraph& graph() const {
+        if (!graph_) {
+            auto g = std::make_unique<AtomGraph>();
+            int64_t ne = 0, n = 0;
+            gmd_num_edges(h_.get(), &ne);
+            gmd_num_nodes(h_.get(), &n);
+            std::vector<int32_t> off(3 * ne);
+            std::vector<double> vec(3 * ne);
+            g->src.resize(ne);
+            g->dst.resize(ne);
+            g->distance.resize(ne);
+            detail::check(h_.get(), gmd_get_graph(h_.get(), g->src.data(), g->dst.data(), off.data(),
+                                                  g->distance.data(), vec.data()));
+            g->image_offset.resize(ne);
+            g->vector.resize(ne);
+            for (int64_t e = 0; e < ne; ++e) {
+                g->image_offset[e] = {off[3 * e], off[3 * e + 1], off[3 * e + 2]};
+                g->vector[e] = {vec[3 * e], vec[3 * e + 1], vec[3 * e + 2]};
+            }
+            g->cutoff = cutoff_;
+            g->num_nodes = n;
+            graph_ = std::move(g);
+        }
+        return *graph_;
+    }
+
+    const PartitionedAtomGraph& atom_parts() const {
+        if (!parts_) {
+            auto pg = std::make_unique<PartitionedAtomGraph>();
+            pg->p = p_;
+            pg->rule.p = p_;
+            pg->rule.boundaries.resize(p_ + 1);
+            detail::check(h_.get(), gmd_get_rule(h_.get(), &pg->rule.axis, pg->rule.boundaries.data()));
+            int64_t n = 0;
+            gmd_num_nodes(h_.get(), &n);
+            std::vector<int32_t> own(n);
+            detail::check(h_.get(), gmd_get_owner(h_.get(), own.data()));
+            pg->owner.assign(own.begin(), own.end());
+            for (int i = 0; i < p_; ++i) {
+                AtomPartition ap;
+                ap.layout = layout(i, 0);
+                int64_t c = 0;
+                detail::check(h_.get(), gmd_get_num_owned_edges(h_.get(), i, &c));
+                ap.owned_edges.resize(c);
+                ap.local_src.resize(c);
+                ap.local_dst.resize(c);
+                detail::check(h_.get(), gmd_get_owned_edges(h_.get(), i, ap.owned_edges.data(),
+                                                            ap.local_src.data(), ap.local_dst.data()));
+                detail::check(h_.get(), gmd_get_num_border_edges(h_.get(), i, &c));
+                ap.border_edge_list.resize(c);
+                detail::check(h_.get(), gmd_get_border_edges(h_.get(), i, ap.border_edge_list.data()));
+                pg->parts.push_back(std::move(ap));
+            }
+            pg->buckets = buckets_of(pg->parts, [](const AtomPartition& a) -> const SpanLayout& { return a.layout; });
+            parts_ = std::move(pg);
+        }
+        return *parts_;
+    }
+
+    const PartitionedLineGraph& line_parts() const {
+        if (!has_line_graph()) throw Error("no line graph was built");
+        if (!lines_) {
+            auto lg = std::make_unique<PartitionedLineGraph>();
+            lg->p = p_;
+            int64_t nb = 0, ne = 0;
+            detail::check(h_.get(), gmd_get_num_bonds(h_.get(), &nb));
+            gmd_num_edges(h_.get(), &ne);
+            lg->bonds.edge_of_bond.resize(nb);
+            std::vector<int32_t> own(nb);
+            detail::check(h_.get(), gmd_get_bonds(h_.get(), lg->bonds.edge_of_bond.data(), own.data()));
+            lg->bond_owner.assign(own.begin(), own.end());
+            lg->bonds.bond_of_edge.assign(ne, -1);
+            for (int64_t b = 0; b < nb; ++b) lg->bonds.bond_of_edge[lg->bonds.edge_of_bond[b]] = b;
+            lg->bonds.r = r3_ ? *r3_ : 0.0;
+            lg->bonds.tau = tau_;
+            for (int i = 0; i < p_; ++i) {
+                LineGraphPartition part;
+                part.layout = layout(i, 1);
+                int64_t c = 0;
+                detail::check(h_.get(), gmd_get_num_line_edges(h_.get(), i, &c));
+                std::vector<int64_t> pairs(2 * c);
+                detail::check(h_.get(), gmd_get_line_edges(h_.get(), i, pairs.data()));
+                part.line_edges.resize(c);
+                for (int64_t k = 0; k < c; ++k) part.line_edges[k] = {pairs[2 * k], pairs[2 * k + 1]};
+                lg->parts.push_back(std::move(part));
+            }
+            lg->bond_buckets = buckets_of(lg->parts, [](const LineGraphPartition& a) -> const SpanLayout& { return a.layout; });
+            lines_ = std::move(lg);
+        }
+        return *lines_;
+    }
+
+    const std::vector<std::int64_t>& src_nodes(int i) const { return atom_parts().parts[i].local_src; }
+    const std::vector<std::int64_t>& dst_nodes(int i) const { return atom_parts().parts[i].local_dst; }
+    std::int64_t atom_rows(int i) const { return atom_parts().parts[i].layout.size(); }
+    std::int64_t bond_rows(int i) const { return line_parts().parts[i].layout.size(); }
+
+    // ---- features: host blocks, exchanged on the GPU -------------------
+    DistributedFeatures make_atom_features(std::int64_t width) const { return make(width, 0); }
+    DistributedFeatures make_bond_features(std::int64_t width) const {
+        if (!has_line_graph()) throw Error("no line graph was built");
+        return make(width, 1);
+    }
+    DistributedFeatures distribute_node_features(const std::vector<double>& f, std::int64_t width) const {
+        int64_t n = 0;
+        gmd_num_nodes(h_.get(), &n);
+        if ((int64_t)f.size() != n * width) throw Error("node feature shape mismatch");
+        DistributedFeatures out = make(width, 0);
+        std::vector<double> flat(flat_rows(0) * width);
+        detail::check(h_.get(), gmd_distribute(h_.get(), 0, f.data(), flat.data(), (int)width,
+                                               GMD_F64 | GMD_HOST_MEMORY));
+        unflatten(flat, out, 0);
+        return out;
+    }
+    void atom_transfer(DistributedFeatures& f) const { op(gmd_transfer, f, 0); }
+    void bond_transfer(DistributedFeatures& f) const { op(gmd_transfer, f, 1); }
+    void atom_transfer_transpose(DistributedFeatures& f) const { op(gmd_transfer_transpose, f, 0); }
+    void bond_transfer_transpose(DistributedFeatures& f) const { op(gmd_transfer_transpose, f, 1); }
+    void sync_atom_duplicates(DistributedFeatures& f) const { op(gmd_sync_duplicates, f, 0); }
+    void sync_bond_duplicates(DistributedFeatures& f) const { op(gmd_sync_duplicates, f, 1); }
+    std::vector<double> aggregate(const DistributedFeatures& f) const { return agg(f, 0); }
+    std::vector<double> aggregate_bonds(const DistributedFeatures& f) const { return agg(f, 1); }
+    void corrupt_transfer_plan_for_test() { detail::check(h_.get(), gmd_corrupt_transfer_plan_for_test(h_.get())); }
+
+private:
+    std::shared_ptr<gmd_handle> h_;
+    int p_ = 1, n_threads_ = 1;
+    double cutoff_ = 0, tau_ = 0;
+    std::optional<double> r3_;
+    AtomicSystem system_;
+    mutable AtomicSystem periodic_;
+    mutable bool sys_ready_ = false;
+    mutable std::unique_ptr<AtomGraph> graph_;
+    mutable std::unique_ptr<PartitionedAtomGraph> parts_;
+    mutable std::unique_ptr<PartitionedLineGraph> lines_;
+
+    SpanLayout layout(int i, int bonds) const {
+        SpanLayout L;
+        L.p = p_;
+        int64_t sz = 0, nd = 0;
+        detail::check(h_.get(), gmd_get_layout_size(h_.get(), i, bonds, &sz));
+        L.node_array.resize(sz);
+        L.markers.resize(2 + 2 * p_);
+        detail::check(h_.get(), gmd_get_layout(h_.get(), i, bonds, L.node_array.data(), L.markers.data()));
+        detail::check(h_.get(), gmd_get_num_duplicates(h_.get(), i, bonds, &nd));
+        std::vector<int64_t> d(2 * nd);
+        detail::check(h_.get(), gmd_get_duplicates(h_.get(), i, bonds, d.data()));
+        for (int64_t k = 0; k < nd; ++k) L.duplicates.emplace_back(d[2 * k], d[2 * k + 1]);
+        return L;
+    }
+    template <typename P, typename F>
+    Buckets buckets_of(const std::vector<P>& parts, F lay) const {
+        Buckets b;
+        b.pure.resize(p_);
+        b.to.assign(p_, std::vector<std::vector<std::int64_t>>(p_));
+        b.from.assign(p_, std::vector<std::vector<std::int64_t>>(p_));
+        for (int i = 0; i < p_; ++i) {
+            const SpanLayout& L = lay(parts[i]);
+            Span s = L.pure_span();
+            b.pure[i].assign(L.node_array.begin() + s.begin, L.node_array.begin() + s.end);
+            for (int j = 0; j < p_; ++j) {
+                Span t = L.to_span(j);
+                b.to[i][j].assign(L.node_array.begin() + t.begin, L.node_array.begin() + t.end);
+            }
+        }
+        for (int i = 0; i < p_; ++i)
+            for (int j = 0; j < p_; ++j) b.from[j][i] = b.to[i][j];
+        return b;
+    }
+    std::int64_t flat_rows(int bonds) const {
+        int64_t r = 0;
+        detail::check(h_.get(), gmd_block_rows(h_.get(), bonds, &r));
+        return r;
+    }
+    std::int64_t block_offset(int i, int bonds) const {
+        int64_t r = 0;
+        detail::check(h_.get(), gmd_block_offset(h_.get(), i, bonds, &r));
+        return r;
+    }
+    DistributedFeatures make(std::int64_t width, int bonds) const {
+        DistributedFeatures f;
+        f.width = width;
+        f.blocks.resize(p_);
+        for (int i = 0; i < p_; ++i) {
+            std::int64_t rows = (i + 1 < p_ ? block_offset(i + 1, bonds) : flat_rows(bonds)) - block_offset(i, bonds);
+            f.blocks[i].assign(rows * width, 0.0);
+        }
+        return f;
+    }
+    std::vector<double> flatten(const DistributedFeatures& f) const {
+        std::vector<double> flat;
+        for (const auto& b : f.blocks) flat.insert(flat.end(), b.begin(), b.end());
+        return flat;
+    }
+    void unflatten(const std::vector<double>& flat, DistributedFeatures& f, int) const {
+        std::size_t o = 0;
+        for (auto& b : f.blocks) {
+            std::copy(flat.begin() + o, flat.begin() + o + b.size(), b.begin());
+            o += b.size();
+        }
+    }
+    template <typename Fn>
+    void op(Fn fn, DistributedFeatures& f, int bonds) const {
+        if (bonds && !has_line_graph()) throw Error("no line graph was built");
+        std::vector<double> flat = flatten(f);
+        detail::check(h_.get(), fn(h_.get(), bonds, flat.data(), (int)f.width, GMD_F64 | GMD_HOST_MEMORY));
+        unflatten(flat, f, bonds);
+    }
+    std::vector<double> agg(const DistributedFeatures& f, int bonds) const {
+        int64_t n = 0;
+        if (bonds) detail::check(h_.get(), gmd_get_num_bonds(h_.get(), &n));
+        else gmd_num_nodes(h_.get(), &n);
+        std::vector<double> flat = flatten(f), out(n * f.width);
+        detail::check(h_.get(), gmd_aggregate(h_.get(), bonds, flat.data(), out.data(), (int)f.width,
+                                              GMD_F64 | GMD_HOST_MEMORY));
+        return out;
+    }
+};
+
+// ---- model (potential.hpp:15-69) ----------------------------------------
+struct ToyPotentialParams {
+    int feature_width = 16, basis_count = 8, layers = 2;
+    double r_atom = 4.0, r_3body = 0.0;
+    std::uint64_t seed = 0;
+    std::vector<double> embedding, layer_w, layer_b, basis_proj, basis3_proj, w3, w4, readout;
+
+    bool threebody() const { return r_3body > 0.0; }
+    static ToyPotentialParams init(std::uint64_t seed, int F = 16, int K = 8, int L = 2,
+                                   double r_atom = 4.0, double r_3body = 0.0) {
+        ToyPotentialParams p;
+        p.feature_width = F;
+        p.basis_count = K;
+        p.layers = L;
+        p.r_atom = r_atom;
+        p.r_3body = r_3body;
+        p.seed = seed;
+        std::vector<double> blob(gmd_params_size(F, K, L));
+        if (gmd_params_init(seed, F, K, L, r_atom, r_3body, blob.data()) != GMD_OK)
+            throw Error("layer count must be >= 1");
+        p.unpack(blob);
+        p.validate();
+        return p;
+    }
+    std::vector<double> blob() const {
+        std::vector<double> b;
+        for (const auto* v : {&embedding, &layer_w, &layer_b, &basis_proj, &basis3_proj, &w3, &w4, &readout})
+            b.insert(b.end(), v->begin(), v->end());
+        return b;
+    }
+    void validate() const {
+        if (layers < 1) throw Error("layer count must be >= 1");
+        if (feature_width < 1 || basis_count < 1) throw Error("feature and basis widths must be >= 1");
+        if (r_atom <= 0.0) throw Error("atom cutoff must be positive");
+        if (threebody() && r_3body > r_atom) throw Error("three-body cutoff cannot exceed the atom cutoff");
+        if ((int64_t)blob().size() != gmd_params_size(feature_width, basis_count, layers))
+            throw Error("parameter array has the wrong size");
+    }
+
+private:
+    void unpack(const std::vector<double>& b) {
+        const std::size_t F = feature_width, K = basis_count, L = layers;
+        std::size_t o = 0;
+        auto take = [&](std::vector<double>& v, std::size_t n) {
+            v.assign(b.begin() + o, b.begin() + o + n);
+            o += n;
+        };
+        take(embedding, 119 * F);
+        take(layer_w, L * F * F);
+        take(layer_b, L * F);
+        take(basis_proj, F * K);
+        take(basis3_proj, F * K);
+        take(w3, F * F);
+        take(w4, F * F);
+        take(readout, F);
+    }
+};
+
+struct PotentialOutput {
+    double energy = 0.0;
+    std::vector<double> per_atom;
+    std::vector<Vec3> forces;
+    Mat3 stress;
+};
+
+inline PotentialOutput forward_distributed(const Distributed& dist, const ToyPotentialParams& params,
+                                           StepTiming* timing = nullptr) {
+    params.validate();
+    gmd_handle* h = dist.handle();
+    std::vector<double> blob = params.blob();
+    detail::check(h, gmd_set_params(h, params.feature_width, params.basis_count, params.layers,
+                                    params.r_atom, params.r_3body, blob.data()));
+    int64_t n = 0;
+    gmd_num_nodes(h, &n);
+    PotentialOutput out;
+    out.per_atom.resize(n);
+    std::vector<double> f(3 * n);
+    double st[9], tm[4];
+    detail::check(h, gmd_forward(h, &out.energy, out.per_atom.data(), f.data(), st, tm, 0));
+    out.forces.resize(n);
+    for (int64_t i = 0; i < n; ++i) out.forces[i] = {f[3 * i], f[3 * i + 1], f[3 * i + 2]};
+    for (int a = 0; a < 3; ++a) out.stress[a] = {st[3 * a], st[3 * a + 1], st[3 * a + 2]};
+    if (timing) {
+        timing->feature_calculation += tm[1];
+        timing->forward_pass += tm[2];
+        timing->backward_pass += tm[3];
+    }
+    return out;
+}
+
+// neighborlist.hpp:37-38 on the GPU
+inline AtomGraph build_neighbor_list(const AtomicSystem& system, double cutoff, int n_threads = 0) {
+    return Distributed::create_distributed(system, cutoff, std::nullopt, 1, n_threads, true).graph();
+}
+
+}  // namespace graphmd

@@ -250,7 +250,7 @@ struct gmd_handle {
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
     DBuf row, src, img, vd, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
-    DBuf brow, bedge, brev, lcnt, lpairs, slab;
+    DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp;
     int nl_cap = 0;
 
     // model
@@ -735,15 +735,15 @@ std::vector<std::pair<int64_t, int64_t>> dup_pairs(gmd_handle* h, LayoutState& l
 
 void ensure_dup_groups(gmd_handle* h, LayoutState& ls) {
     if (ls.dups_ready) return;
-    std::vector<int32_t> gc, gs{0}, dd, dc, du;
+    std::vector<int32_t> gc, gs, dd, dc, du;
     for (int i = 0; i < ls.p; ++i) {
         auto pairs = dup_pairs(h, ls, i);
         const int64_t base = ls.base(i);
         std::stable_sort(pairs.begin(), pairs.end(),
                          [](auto& a, auto& b) { return a.first < b.first; });
         for (size_t k = 0; k < pairs.size(); ++k) {
-            if (k == 0 || pairs[k].first != pairs[k - 1].first) {
-                if (k) gs.push_back((int32_t)dd.size());
+            if (k == 0 || pairs[k].first != pairs[k - 1].first) {  // new canonical group
+                gs.push_back((int32_t)dd.size());
                 gc.push_back((int32_t)(pairs[k].first + base));
             }
             dd.push_back((int32_t)(pairs[k].second + base));
@@ -781,7 +781,29 @@ void ensure_api_plan(gmd_handle* h, LayoutState& ls, bool corrupt) {
     ls.api_corrupt = corrupt;
 }
 
+// feature-API buffers may be host memory (GMD_HOST_MEMORY): stage them
+struct Staged {
+    gmd_handle* h;
+    void* user;
+    void* dev;
+    size_t bytes;
+    bool host;
+    Staged(gmd_handle* h_, void* buf, size_t b, bool host_, bool copy_in)
+        : h(h_), user(buf), dev(buf), bytes(b), host(host_) {
+        if (host) {
+            dev = h->feat_tmp.get<char>(bytes);
+            if (copy_in && bytes)
+                GMD_CUDA(cudaMemcpyAsync(dev, user, bytes, cudaMemcpyHostToDevice, h->stream));
+        }
+    }
+    void copy_out() {
+        if (host && bytes)
+            GMD_CUDA(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, h->stream));
+    }
+};
+
 int elem_size(int dtype) {
+    dtype &= 0xff;
     if (dtype == GMD_F32) return 4;
     if (dtype == GMD_F64) return 8;
     raise(kArg, "dtype must be GMD_F32 or GMD_F64");
@@ -1002,7 +1024,7 @@ void gmd_destroy(gmd_handle* h) {
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ebond, &h->edst, &h->lsrc, &h->counts,
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
-                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
+                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp};
     for (DBuf* b : bufs) b->release();
@@ -1403,12 +1425,14 @@ int gmd_transfer(gmd_handle* h, int bonds, void* dev_buf, int width, int dtype) 
         const int es = elem_size(dtype);
         if (width < 1) raise(kArg, "width must be >= 1");
         if (ls.nfrom == 0) return;
+        Staged st(h, dev_buf, (size_t)ls.rows * width * es, dtype & GMD_HOST_MEMORY, true);
         ensure_api_plan(h, ls, h->corrupted && !bonds);
         const int ww = width * es / 4;
         k_copy_rows<<<div_up(ls.nfrom * ww, 256), 256, 0, h->stream>>>(
-            ls.nfrom, ls.xdst.as<int32_t>(), ls.xapi.as<int32_t>(), static_cast<uint32_t*>(dev_buf),
+            ls.nfrom, ls.xdst.as<int32_t>(), ls.xapi.as<int32_t>(), static_cast<uint32_t*>(st.dev),
             ww);
         GMD_LAUNCH_CHECK();
+        st.copy_out();
         sync(h);
     });
 }
@@ -1419,6 +1443,8 @@ int gmd_transfer_transpose(gmd_handle* h, int bonds, void* dev_buf, int width, i
         const int es = elem_size(dtype);
         if (width < 1) raise(kArg, "width must be >= 1");
         cudaStream_t s = h->stream;
+        Staged st(h, dev_buf, (size_t)ls.rows * width * es, dtype & GMD_HOST_MEMORY, true);
+        dev_buf = st.dev;
         if (ls.nfrom > 0) {
             ensure_api_plan(h, ls, false);
             const int64_t tot = ls.nfrom * width;
@@ -1445,6 +1471,7 @@ int gmd_transfer_transpose(gmd_handle* h, int bonds, void* dev_buf, int width, i
                     ls.g_dups.as<int32_t>(), static_cast<float*>(dev_buf), width);
             GMD_LAUNCH_CHECK();
         }
+        st.copy_out();
         sync(h);
     });
 }
@@ -1455,11 +1482,13 @@ int gmd_sync_duplicates(gmd_handle* h, int bonds, void* dev_buf, int width, int 
         const int es = elem_size(dtype);
         ensure_dup_groups(h, ls);
         if (ls.ndups == 0) return;
+        Staged st(h, dev_buf, (size_t)ls.rows * width * es, dtype & GMD_HOST_MEMORY, true);
         const int ww = width * es / 4;
         k_copy_rows<<<div_up(ls.ndups * ww, 256), 256, 0, h->stream>>>(
             ls.ndups, ls.d_dup.as<int32_t>(), ls.d_canon.as<int32_t>(),
-            static_cast<uint32_t*>(dev_buf), ww);
+            static_cast<uint32_t*>(st.dev), ww);
         GMD_LAUNCH_CHECK();
+        st.copy_out();
         sync(h);
     });
 }
@@ -1474,12 +1503,14 @@ int gmd_distribute(gmd_handle* h, int bonds, const void* host_global, void* dev_
         uint32_t* tmp = h->conv_tmp.get<uint32_t>((size_t)ls.nid * ww);
         GMD_CUDA(cudaMemcpyAsync(tmp, host_global, (size_t)ls.nid * ww * 4, cudaMemcpyHostToDevice,
                                  s));
+        Staged st(h, dev_buf, (size_t)ls.rows * ww * 4, dtype & GMD_HOST_MEMORY, false);
         if (ls.rows > 0) {
             k_gather_rows<<<div_up(ls.rows * ww, 256), 256, 0, s>>>(
                 ls.rows, ls.p > 1 ? ls.node_array.as<int32_t>() : nullptr, tmp,
-                static_cast<uint32_t*>(dev_buf), ww);
+                static_cast<uint32_t*>(st.dev), ww);
             GMD_LAUNCH_CHECK();
         }
+        st.copy_out();
         sync(h);
     });
 }
@@ -1492,10 +1523,11 @@ int gmd_aggregate(gmd_handle* h, int bonds, const void* dev_buf, void* host_glob
         const int ww = width * es / 4;
         cudaStream_t s = h->stream;
         uint32_t* tmp = h->conv_tmp.get<uint32_t>((size_t)ls.nid * ww);
+        Staged st(h, const_cast<void*>(dev_buf), (size_t)ls.rows * ww * 4, dtype & GMD_HOST_MEMORY, true);
         if (ls.nid > 0) {  // canonical owned row of every id (engine.cpp:214-229)
             k_gather_rows<<<div_up(ls.nid * ww, 256), 256, 0, s>>>(
                 ls.nid, ls.p > 1 ? ls.crow.as<int32_t>() : nullptr,
-                static_cast<const uint32_t*>(dev_buf), tmp, ww);
+                static_cast<const uint32_t*>(st.dev), tmp, ww);
             GMD_LAUNCH_CHECK();
         }
         GMD_CUDA(cudaMemcpyAsync(host_global, tmp, (size_t)ls.nid * ww * 4, cudaMemcpyDeviceToHost,
