@@ -249,7 +249,7 @@ struct gmd_handle {
     LayoutState atoms, bonds;
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
-    DBuf row, src, img, vd, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
+    DBuf row, src, img, vd, ed, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
     DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp;
     int nl_cap = 0;
 
@@ -547,6 +547,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     gd.src = h->src.get<int32_t>(h->ne);
     gd.img = h->img.get<uint32_t>(h->ne);
     gd.vd = h->vd.get<float4>(h->ne);
+    gd.d = h->ed.get<float>(h->ne);
     gd.bond = h->ebond.get<uint8_t>(h->ne);
     { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s); }
 
@@ -847,7 +848,8 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     double* pa = h->per_atom.get<double>(n);
 
     ConvArgs a{n, part ? A.crow.as<int32_t>() : nullptr, h->row.as<int32_t>(),
-               part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(), h->vd.as<float4>()};
+               part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(), h->vd.as<float4>(),
+               h->ed.as<float>()};
     BondArgs ba{n,
                 a.crow,
                 h->brow.as<int32_t>(),
@@ -1022,7 +1024,7 @@ void gmd_destroy(gmd_handle* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     DBuf* bufs[] = {&h->pos, &h->Z, &h->cell, &h->fw, &h->bin, &h->bin_cnt, &h->bin_start,
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
-                    &h->row, &h->src, &h->img, &h->vd, &h->ebond, &h->edst, &h->lsrc, &h->counts,
+                    &h->row, &h->src, &h->img, &h->vd, &h->ed, &h->ebond, &h->edst, &h->lsrc, &h->counts,
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
                     &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
@@ -1111,6 +1113,13 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         m.inv_rc = (float)(1.0 / r_atom);
         m.inv_sigma = (float)(K / r_atom);  // sigma = rc / K (potential.cpp:34)
         m.mu_step = K > 1 ? (float)(r_atom / (K - 1)) : 0.f;
+        {
+            const double sl2e = std::sqrt(1.4426950408889634);  // sqrt(log2 e)
+            m.a2 = (float)(sl2e * K / r_atom);
+            m.pi_rc = (float)(3.14159265358979323846 / r_atom);
+            for (int k = 0; k < K; ++k)
+                m.bx[k] = (float)((K > 1 ? r_atom * k / (K - 1) : 0.0) * sl2e * K / r_atom);
+        }
         const double r3e = r3 > 0.0 ? r3 : 1.0;
         m.r3 = (float)r3e;
         m.inv_r3 = (float)(1.0 / r3e);

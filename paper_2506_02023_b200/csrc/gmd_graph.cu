@@ -355,8 +355,8 @@ __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
                           const int32_t* __restrict__ row, const double* __restrict__ pos,
                           const int32_t* __restrict__ cell, int32_t* __restrict__ e_src,
                           uint32_t* __restrict__ e_img, float4* __restrict__ e_vd,
-                          uint8_t* __restrict__ e_bond, int32_t* __restrict__ bcnt,
-                          int32_t* __restrict__ flags) {
+                          float* __restrict__ e_d, uint8_t* __restrict__ e_bond,
+                          int32_t* __restrict__ bcnt, int32_t* __restrict__ flags) {
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= n) return;
     const int lane = threadIdx.x & 31;
@@ -388,6 +388,7 @@ __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
             e_src[e] = j;
             e_img[e] = pack_img(o0, o1, o2);
             e_vd[e] = make_float4((float)vr.x, (float)vr.y, (float)vr.z, (float)dd);
+            e_d[e] = (float)dd;
             isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
             e_bond[e] = isb ? 1 : 0;
         }
@@ -562,7 +563,7 @@ void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long*
                     NLBuffers& b, GraphDev& gd, cudaStream_t s) {
     if (n == 0) return;
     k_nl_emit<<<div_up(n, 8), 256, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src, gd.img,
-                                           gd.vd, gd.bond, b.bcnt, b.flags);
+                                           gd.vd, gd.d, gd.bond, b.bcnt, b.flags);
     GMD_LAUNCH_CHECK();
 }
 

@@ -26,6 +26,7 @@ struct GraphDev {
     int32_t* src = nullptr;    // ne, global source id
     uint32_t* img = nullptr;   // ne, packed image offset
     float4* vd = nullptr;      // ne, (vx, vy, vz, d) rounded from fp64
+    float* d = nullptr;        // ne, d (the forward pass reads only this)
     uint8_t* bond = nullptr;   // ne, 1 iff d <= r3 + tau (three-body bond)
 };
 

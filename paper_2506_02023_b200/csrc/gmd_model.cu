@@ -64,6 +64,34 @@ __device__ __forceinline__ void fcut3(float d, float& fc, float& dfc) {
     dfc = in ? -0.5f * 3.14159265358979f * c_m.inv_r3 * sn : 0.0f;
 }
 
+// Fast radial basis for the atom channel on the SFU: fc from __cosf on
+// [0, pi], phi_k = ex2(-(d a - b_k)^2) with a = sqrt(log2 e)/sigma and
+// b_k = mu_k a (constants in c_m.bx[]); |error| ~1e-7, far inside the fp32
+// tolerance of the parity tests.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void phi_fast(float d, float phi[kK]) {
+    const float xa = d * c_m.a2;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const float x = xa - c_m.bx[k];
+        phi[k] = ex2_approx(-x * x);
+    }
+}
+__device__ __forceinline__ float fc_fast(float d) {
+    return d < c_m.rc ? 0.5f * __cosf(d * c_m.pi_rc) + 0.5f : 0.0f;
+}
+__device__ __forceinline__ void fc_dfc_fast(float d, float& fc, float& dfc) {
+    float sn, cs;
+    __sincosf(d * c_m.pi_rc, &sn, &cs);
+    const bool in = d < c_m.rc;
+    fc = in ? 0.5f * cs + 0.5f : 0.0f;
+    dfc = in ? -0.5f * c_m.pi_rc * sn : 0.0f;
+}
+
 __device__ __forceinline__ void load_row16(const float* __restrict__ p, float h[kF]) {
     const float4* q = reinterpret_cast<const float4*>(p);
 #pragma unroll
@@ -212,7 +240,28 @@ __device__ __forceinline__ float group_sum16(float v) {
 constexpr int kNodesPerCta = kThreads / 16;  // half-warp (16 lanes) per node
 
 // forward conv layer (potential.cpp:743-774): a 16-lane group per owned node,
-// lanes stride over its in-edges, fixed-order group reduction
+// lanes stride over its in-edges two at a time (both edges' loads in flight
+// before the math), fixed-order group reduction.  Reads 8 B per edge (d and
+// the source row); the radial channel is recomputed in registers.
+__device__ __forceinline__ void conv_edge(float d, const float4* __restrict__ hs, float acc[kF]) {
+    float phi[kK];
+    phi_fast(d, phi);
+    const float fc = fc_fast(d);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float4 h4 = __ldg(hs + c);
+        const float hh[4] = {h4.x * fc, h4.y * fc, h4.z * fc, h4.w * fc};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int f = 4 * c + i;
+            float sv = 0.0f;
+#pragma unroll
+            for (int k = 0; k < kK; ++k) sv = fmaf(c_m.P[f * kK + k], phi[k], sv);
+            acc[f] = fmaf(hh[i], sv, acc[f]);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
                                                       const float* __restrict__ Hin,
                                                       float* __restrict__ Hout,
@@ -230,7 +279,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
     const int gl = lane & 15;
     const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + (threadIdx.x >> 4);
     const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
-    const float rc = c_m.rc, irc = c_m.inv_rc, isg = c_m.inv_sigma, mus = c_m.mu_step;
     double esum = 0.0;
     // both half-warps iterate the same number of times (shuffles span the warp)
     const int64_t iters = (a.n + ng - 1) / ng;
@@ -240,27 +288,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
         float acc[kF];
 #pragma unroll
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
-        if (valid) {
-            const int e1 = __ldg(a.row + v + 1);
-            for (int e = __ldg(a.row + v) + gl; e < e1; e += 16) {
-                const float4 q = __ldg(a.vd + e);
-                float u[kK];
-                basis(q.w, rc, irc, isg, mus, u);
-                const float4* hs = reinterpret_cast<const float4*>(Hin + (size_t)__ldg(a.lsrc + e) * kF);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float4 h4 = __ldg(hs + c);
-                    const float hh[4] = {h4.x, h4.y, h4.z, h4.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int f = 4 * c + i;
-                        float sv = 0.0f;
-#pragma unroll
-                        for (int k = 0; k < kK; ++k) sv = fmaf(c_m.P[f * kK + k], u[k], sv);
-                        acc[f] = fmaf(hh[i], sv, acc[f]);
-                    }
-                }
-            }
+        const int e0 = valid ? __ldg(a.row + v) : 0;
+        const int e1 = valid ? __ldg(a.row + v + 1) : 0;
+        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 32) {
+            const bool ha = e < e1, hb = e + 16 < e1;
+            const float da = ha ? __ldg(a.d + e) : 0.f;
+            const float db = hb ? __ldg(a.d + e + 16) : 0.f;
+            const int ia = ha ? __ldg(a.lsrc + e) : 0;
+            const int ib = hb ? __ldg(a.lsrc + e + 16) : 0;
+            if (ha) conv_edge(da, reinterpret_cast<const float4*>(Hin + (size_t)ia * kF), acc);
+            if (__any_sync(0xffffffffu, hb) && hb)
+                conv_edge(db, reinterpret_cast<const float4*>(Hin + (size_t)ib * kF), acc);
         }
         const float m = transpose_reduce16_g16(acc, gl);  // feature gl
         float z = sb[gl];
@@ -354,18 +392,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
                 const float4 q = __ldg(a.vd + e);
                 // s_f = fc A_f, ds_f = dfc A_f - 2 fc/sigma (x0 A_f - a B_f) with
                 // A_f = sum_k P_fk phi_k, B_f = sum_k k P_fk phi_k (potential.cpp:30-50)
-                float sn, cs;
-                sincospif(q.w * irc, &sn, &cs);
-                const bool in = q.w < rc;
-                const float fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
-                const float dfc = in ? -0.5f * 3.14159265358979f * irc * sn : 0.0f;
-                const float x0 = q.w * isg, step = mus * isg;
+                float fc, dfc;
+                fc_dfc_fast(q.w, fc, dfc);
                 float phi[kK];
-#pragma unroll
-                for (int k = 0; k < kK; ++k) {
-                    const float x = x0 - step * (float)k;
-                    phi[k] = __expf(-x * x);
-                }
+                phi_fast(q.w, phi);
+                const float x0 = q.w * isg, step = mus * isg;
                 const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
                 const int w = __ldg(a.lsrc + e);
                 const float4* mw = reinterpret_cast<const float4*>(MB + (size_t)w * kF);

@@ -22,6 +22,8 @@ struct ModelConst {
     float W4[kF * kF];
     float ro[kF];
     float rc, inv_rc, inv_sigma, mu_step;     // atom radial basis
+    float a2, pi_rc;                          // sqrt(log2 e)/sigma, pi/rc
+    float bx[kK];                             // mu_k sqrt(log2 e)/sigma
     float r3, inv_r3, inv_sigma3, mu_step3;   // three-body radial basis
     int L;
 };
@@ -37,7 +39,8 @@ struct ConvArgs {
     const int32_t* crow;
     const int32_t* row;
     const int32_t* lsrc;
-    const float4* vd;
+    const float4* vd;  // (vx, vy, vz, d) per edge (backward)
+    const float* d;    // d per edge (forward)
 };
 
 int model_grid(int64_t n);  // fixed grid => deterministic reductions
