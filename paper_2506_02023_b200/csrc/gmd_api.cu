@@ -517,8 +517,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     int cap = h->nl_cap;
     if (cap <= 0) {  // first build: density estimate of the mean degree
         const double mean = (double)n * 4.18879020478639 * rc * rc * rc / std::abs(det3(h->lat));
-        cap = 32;
-        while (cap < 1.3 * mean + 24) cap <<= 1;
+        cap = ((int)(1.2 * mean + 16) + 7) & ~7;
     }
     int32_t* rowp = h->row.get<int32_t>(n + 1);
     int32_t hdr[2];
@@ -530,13 +529,11 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
         read_flags(h, hdr);
         if (hdr[0] <= cap) break;
-        while (cap < hdr[0]) cap <<= 1;  // rare: an atom exceeded the slab row
+        cap = (hdr[0] + 7) & ~7;  // rare: an atom exceeded the slab row
         GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
     }
     {   // next build: size the slab from this one's maximum degree
-        int next = 32;
-        while (next < hdr[0] + hdr[0] / 8 + 4) next <<= 1;
-        h->nl_cap = next;
+        h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
     }
     if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
     h->ne = ne32;

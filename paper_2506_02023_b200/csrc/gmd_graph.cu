@@ -125,6 +125,19 @@ struct CandW {
     unsigned qc[32];
 };
 
+constexpr int kWSCap = 32;  // stencil cells per batch (per warp)
+
+struct WarpNL {             // per-warp shared state of the search
+    int sc_bin[kWSCap];
+    int sc_pre[kWSCap + 1];
+    int sc_q[kWSCap][3];
+    double sc_shift[kWSCap][3];
+    CandW cand;
+    unsigned short queue[64];
+};
+
+// Search, one WARP per destination bin (no CTA barriers).  Shared memory per
+// warp: WarpNL + the destination group (<= group atoms) + group x cap keys.
 __global__ void __launch_bounds__(kThreads) k_nl_search(
     const Geom g, float thr32, int64_t nbins, int64_t n, int group, int cap,
     const int32_t* __restrict__ bin_start, const int32_t* __restrict__ s_id,
@@ -132,35 +145,35 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
     const int32_t* __restrict__ s_c, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
     unsigned long long* __restrict__ slab) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    NLSmem& S = *reinterpret_cast<NLSmem*>(smem_raw);
-    unsigned char* q = smem_raw + sizeof(NLSmem);
-    CandW* cw = reinterpret_cast<CandW*>(q);
-    q += sizeof(CandW) * kWarps;
-    unsigned short* queue = reinterpret_cast<unsigned short*>(q);  // 64 per warp
-    q += sizeof(unsigned short) * 64 * kWarps;
-    q = reinterpret_cast<unsigned char*>(((uintptr_t)q + 15) & ~(uintptr_t)15);
-    float4* d32 = reinterpret_cast<float4*>(q);
-    q += sizeof(float4) * group;
-    double* d_w = reinterpret_cast<double*>(q);
-    q += sizeof(double) * 3 * group;
-    double* d_p = reinterpret_cast<double*>(q);
-    q += sizeof(double) * 3 * group;
-    int* d_c = reinterpret_cast<int*>(q);
-    q += sizeof(int) * 3 * group;
-    int* d_id = reinterpret_cast<int*>(q);
-    q += sizeof(int) * group;
-    int* d_cnt = reinterpret_cast<int*>(q);
-    q += sizeof(int) * group;
-    q = reinterpret_cast<unsigned char*>(((uintptr_t)q + 15) & ~(uintptr_t)15);
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(q);
-
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    CandW& C = cw[warp];
-    unsigned short* Q = queue + 64 * warp;
+    // per-warp carve-up by byte offsets (keeps the shared address space)
+    const size_t dst_bytes = (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
+    const size_t per_warp = ((sizeof(WarpNL) + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
+    unsigned char* base = smem_raw + (size_t)warp * per_warp;
+    WarpNL& S = *reinterpret_cast<WarpNL*>(base);
+    CandW& C = S.cand;
+    unsigned short* Q = S.queue;
+    size_t o = sizeof(WarpNL);
+    float4* d32 = reinterpret_cast<float4*>(base + o);
+    o += sizeof(float4) * group;
+    double* d_w = reinterpret_cast<double*>(base + o);
+    o += sizeof(double) * 3 * group;
+    double* d_p = reinterpret_cast<double*>(base + o);
+    o += sizeof(double) * 3 * group;
+    int* d_c = reinterpret_cast<int*>(base + o);
+    o += sizeof(int) * 3 * group;
+    int* d_id = reinterpret_cast<int*>(base + o);
+    o += sizeof(int) * group;
+    int* d_cnt = reinterpret_cast<int*>(base + o);
+    o += sizeof(int) * group;
+    o = (o + 15) & ~(size_t)15;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(base + o);
+
     const int sx = 2 * g.sten[0] + 1, sy = 2 * g.sten[1] + 1, sz = 2 * g.sten[2] + 1;
     const int ncell = sx * sy * sz;
+    const int64_t wg = (int64_t)blockIdx.x * kWarps + warp, nw = (int64_t)gridDim.x * kWarps;
 
-    for (int64_t bb = blockIdx.x; bb < nbins; bb += gridDim.x) {
+    for (int64_t bb = wg; bb < nbins; bb += nw) {
         const int b0 = bin_start[bb], b1 = bin_start[bb + 1];
         if (b1 == b0) continue;
         const int bz = (int)(bb % g.bins[2]);
@@ -169,11 +182,10 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
         // bin origin (any common origin works; it only conditions fp32)
         const d3 org = rowvec_rn(g.L, (double)bx / g.bins[0], (double)by / g.bins[1],
                                  (double)bz / g.bins[2]);
-
         for (int gbase = b0; gbase < b1; gbase += group) {
             const int nd = min(group, b1 - gbase);
-            __syncthreads();
-            for (int t = threadIdx.x; t < nd; t += kThreads) {
+            __syncwarp();
+            for (int t = lane; t < nd; t += 32) {
                 const int slot = gbase + t;
                 double w3[3];
 #pragma unroll
@@ -188,11 +200,12 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                 d_id[t] = s_id[slot];
                 d_cnt[t] = 0;
             }
-            for (int cbase = 0; cbase < ncell; cbase += kSCap) {
-                const int nc = min(kSCap, ncell - cbase);
-                __syncthreads();
-                for (int ci = threadIdx.x; ci < nc; ci += kThreads) {
-                    const int c = cbase + ci;
+            for (int cbase = 0; cbase < ncell; cbase += kWSCap) {
+                const int nc = min(kWSCap, ncell - cbase);
+                __syncwarp();
+                int cntc = 0;
+                if (lane < nc) {
+                    const int c = cbase + lane;
                     const int dz = c % sz - g.sten[2];
                     const int dy = (c / sz) % sy - g.sten[1];
                     const int dx = c / (sz * sy) - g.sten[0];
@@ -203,39 +216,31 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                         const int nb = g.bins[k];
                         qv[k] = cc[k] >= 0 ? cc[k] / nb : -((-cc[k] + nb - 1) / nb);
                         cwb[k] = cc[k] - qv[k] * nb;
-                        S.sc_q[ci][k] = qv[k];
+                        S.sc_q[lane][k] = qv[k];
                     }
                     // shift = L0*q0 + L1*q1 + L2*q2 (neighborlist.cpp:171-173)
                     const d3 sh = rowvec_rn(g.L, (double)qv[0], (double)qv[1], (double)qv[2]);
-                    S.sc_shift[ci][0] = sh.x;
-                    S.sc_shift[ci][1] = sh.y;
-                    S.sc_shift[ci][2] = sh.z;
+                    S.sc_shift[lane][0] = sh.x;
+                    S.sc_shift[lane][1] = sh.y;
+                    S.sc_shift[lane][2] = sh.z;
                     const int64_t wb = ((int64_t)cwb[0] * g.bins[1] + cwb[1]) * g.bins[2] + cwb[2];
-                    S.sc_bin[ci] = (int)wb;
-                    S.sc_pre[ci + 1] = bin_start[wb + 1] - bin_start[wb];
+                    S.sc_bin[lane] = (int)wb;
+                    cntc = bin_start[wb + 1] - bin_start[wb];
                     if (qv[0] < -128 || qv[0] > 127 || qv[1] < -128 || qv[1] > 127 ||
                         qv[2] < -128 || qv[2] > 127)
                         atomicOr(&flags[1], kErrQRange);
                 }
-                __syncthreads();
-                if (warp == 0) {  // prefix over the batch's candidate counts
-                    int carry = 0;
-                    for (int base = 0; base < nc; base += 32) {
-                        const int ci = base + lane;
-                        int v = ci < nc ? S.sc_pre[ci + 1] : 0;
+                int incl = cntc;  // warp scan of candidate counts
 #pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            int u = __shfl_up_sync(0xffffffffu, v, o);
-                            if (lane >= o) v += u;
-                        }
-                        if (ci < nc) S.sc_pre[ci + 1] = carry + v;
-                        carry += __shfl_sync(0xffffffffu, v, 31);
-                    }
-                    if (lane == 0) S.sc_pre[0] = 0;
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += u;
                 }
-                __syncthreads();
-                const int total = S.sc_pre[nc];
-                for (int kb = warp * 32; kb < total; kb += kThreads) {
+                if (lane < nc) S.sc_pre[lane + 1] = incl;
+                if (lane == 0) S.sc_pre[0] = 0;
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                __syncwarp();
+                for (int kb = 0; kb < total; kb += 32) {
                     const int k = kb + lane;
                     const bool valid = k < total;
                     float c32x = 0.f, c32y = 0.f, c32z = 0.f;
@@ -247,19 +252,20 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                         }
                         const int ci = lo;
                         const int slot = bin_start[S.sc_bin[ci]] + (k - S.sc_pre[ci]);
+                        double cv[3];
 #pragma unroll
                         for (int d = 0; d < 3; ++d) {
                             // candidate = wrapped_j + shift (neighborlist.cpp:176)
-                            const double cv = add_rn(s_w[d * n + slot], S.sc_shift[ci][d]);
-                            C.c[d][lane] = cv;
+                            cv[d] = add_rn(s_w[d * n + slot], S.sc_shift[ci][d]);
+                            C.c[d][lane] = cv[d];
                             C.p[d][lane] = s_p[d * n + slot];
                             C.nc[d][lane] = S.sc_q[ci][d] - s_c[d * n + slot];
                         }
                         C.jid[lane] = s_id[slot];
                         C.qc[lane] = qcode(S.sc_q[ci][0], S.sc_q[ci][1], S.sc_q[ci][2]);
-                        c32x = (float)(C.c[0][lane] - org.x);
-                        c32y = (float)(C.c[1][lane] - org.y);
-                        c32z = (float)(C.c[2][lane] - org.z);
+                        c32x = (float)(cv[0] - org.x);
+                        c32y = (float)(cv[1] - org.y);
+                        c32z = (float)(cv[2] - org.z);
                     }
                     __syncwarp();
                     int qn = 0;
@@ -268,8 +274,9 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                         if (lane < cnt) {
                             const unsigned ent = Q[lane];
                             const int c = ent & 31, t = ent >> 5;
-                            d3 v = {sub_rn(C.c[0][c], d_w[3 * t]), sub_rn(C.c[1][c], d_w[3 * t + 1]),
-                                    sub_rn(C.c[2][c], d_w[3 * t + 2])};
+                            const d3 v = {sub_rn(C.c[0][c], d_w[3 * t]),
+                                          sub_rn(C.c[1][c], d_w[3 * t + 1]),
+                                          sub_rn(C.c[2][c], d_w[3 * t + 2])};
                             if (!(dot_rn(v, v) > g.pre2)) {  // neighborlist.cpp:177
                                 const int o0 = C.nc[0][c] + d_c[3 * t];
                                 const int o1 = C.nc[1][c] + d_c[3 * t + 1];
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                         if (qn >= 32) {
                             drain(32);
                             __syncwarp();
-                            unsigned short mv = lane < qn - 32 ? Q[32 + lane] : 0;
+                            const unsigned short mv = lane < qn - 32 ? Q[32 + lane] : 0;
                             __syncwarp();
                             if (lane < qn - 32) Q[lane] = mv;
                             qn -= 32;
@@ -311,35 +318,27 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                     __syncwarp();
                 }
             }
-            __syncthreads();
-            for (int t = warp; t < nd; t += kWarps) {
+            // canonical (src, image) order by rank (keys are unique), then store
+            for (int t = 0; t < nd; ++t) {
                 const int full = d_cnt[t];
                 const int cnt = min(full, cap);
-                unsigned long long* kk = keys + (size_t)t * cap;
-                int P = 1;
-                while (P < cnt) P <<= 1;
-                for (int k = cnt + lane; k < P; k += 32) kk[k] = ~0ull;
-                __syncwarp();
-                for (int sz2 = 2; sz2 <= P; sz2 <<= 1)
-                    for (int j = sz2 >> 1; j > 0; j >>= 1) {
-                        for (int i = lane; i < P; i += 32) {
-                            const int ixj = i ^ j;
-                            if (ixj > i) {
-                                const unsigned long long a = kk[i], c2 = kk[ixj];
-                                const bool up = (i & sz2) == 0;
-                                if ((a > c2) == up) {
-                                    kk[i] = c2;
-                                    kk[ixj] = a;
-                                }
-                            }
-                        }
-                        __syncwarp();
+                const unsigned long long* kk = keys + (size_t)t * cap;
+                unsigned long long* dst = slab + (size_t)d_id[t] * cap;
+                for (int k0 = 0; k0 < cnt; k0 += 64) {
+                    const int ka = k0 + lane, kb2 = k0 + 32 + lane;
+                    const unsigned long long ma = ka < cnt ? kk[ka] : ~0ull;
+                    const unsigned long long mb = kb2 < cnt ? kk[kb2] : ~0ull;
+                    int ra = 0, rb = 0;
+                    for (int i = 0; i < cnt; ++i) {
+                        const unsigned long long x = kk[i];
+                        ra += x < ma;
+                        rb += x < mb;
                     }
-                const int did = d_id[t];
-                unsigned long long* dst = slab + (size_t)did * cap;
-                for (int k = lane; k < cnt; k += 32) dst[k] = kk[k];
+                    if (ka < cnt) dst[ra] = ma;
+                    if (kb2 < cnt) dst[rb] = mb;
+                }
                 if (lane == 0) {
-                    deg[did] = full;
+                    deg[d_id[t]] = full;
                     atomicMax(&flags[0], full);
                 }
             }
@@ -515,16 +514,14 @@ __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
 }
 
 size_t nl_smem(int group, int cap) {
-    size_t s = sizeof(NLSmem) + sizeof(CandW) * kWarps + sizeof(unsigned short) * 64 * kWarps;
-    s = (s + 15) & ~(size_t)15;
-    s += (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
-    s = (s + 15) & ~(size_t)15;
-    s += (size_t)group * cap * 8;
-    return s;
+    const size_t dst_bytes = (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
+    const size_t per_warp = ((sizeof(WarpNL) + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
+    return per_warp * kWarps;
 }
 
 int nl_grid(int64_t nbins) {
-    int64_t g = nbins < 148 * 64 ? nbins : 148 * 64;
+    int64_t g = (nbins + kWarps - 1) / kWarps;
+    if (g > 148 * 32) g = 148 * 32;
     return (int)(g > 0 ? g : 1);
 }
 
@@ -543,8 +540,8 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
 
 void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, cudaStream_t s) {
-    int group = 32;
-    while (group > 2 && (size_t)group * cap * 8 > 64 * 1024) group >>= 1;
+    int group = 16;
+    while (group > 1 && nl_smem(group, cap) > 110 * 1024) group >>= 1;
     const size_t sm = nl_smem(group, cap);
     if (sm > 200 * 1024) raise(kRuntime, "neighbour search: per-atom degree too large");
     static bool attr = false;
