@@ -147,13 +147,14 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp carve-up by byte offsets (keeps the shared address space)
+    const size_t head = (sizeof(WarpNL) + 15) & ~(size_t)15;
     const size_t dst_bytes = (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
-    const size_t per_warp = ((sizeof(WarpNL) + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
+    const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
     unsigned char* base = smem_raw + (size_t)warp * per_warp;
     WarpNL& S = *reinterpret_cast<WarpNL*>(base);
     CandW& C = S.cand;
     unsigned short* Q = S.queue;
-    size_t o = sizeof(WarpNL);
+    size_t o = head;
     float4* d32 = reinterpret_cast<float4*>(base + o);
     o += sizeof(float4) * group;
     double* d_w = reinterpret_cast<double*>(base + o);
@@ -514,8 +515,9 @@ __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
 }
 
 size_t nl_smem(int group, int cap) {
+    const size_t head = (sizeof(WarpNL) + 15) & ~(size_t)15;
     const size_t dst_bytes = (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
-    const size_t per_warp = ((sizeof(WarpNL) + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
+    const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
     return per_warp * kWarps;
 }
 
