@@ -353,8 +353,76 @@ __global__ void k_bwd_node(int64_t n, const int32_t* __restrict__ crow, int laye
 
 // backward edge pass in row form (potential.cpp:823-848 restated as
 // gathers): a 16-lane group per node u; the node's own m_bar / h_in rows are
-// staged in shared memory (broadcast reads), neighbour rows stream through
-// registers four features at a time.
+// staged in shared memory (broadcast reads); each lane takes two in-edges per
+// iteration and issues both edges' neighbour-row loads before any math.
+struct BwdEdgeIn {
+    float4 q;      // (vx, vy, vz, d)
+    float4 m[4];   // m_bar[w]
+    float4 h[4];   // h_in[w]
+};
+
+__device__ __forceinline__ void bwd_load(const ConvArgs& a, const float* __restrict__ MB,
+                                         const float* __restrict__ Hl, int e, BwdEdgeIn& x) {
+    x.q = __ldg(a.vd + e);
+    const int w = __ldg(a.lsrc + e);
+    const float4* mw = reinterpret_cast<const float4*>(MB + (size_t)w * kF);
+    const float4* hw = reinterpret_cast<const float4*>(Hl + (size_t)w * kF);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        x.m[c] = __ldg(mw + c);
+        x.h[c] = __ldg(hw + c);
+    }
+}
+
+__device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
+                                         const float4* su_h, float isg, float mus, float acc[kF],
+                                         float& gx, float& gy, float& gz, float vr[6]) {
+    const float4 q = x.q;
+    // s_f = fc A_f, ds_f = dfc A_f - 2 fc/sigma (x0 A_f - a B_f) with
+    // A_f = sum_k P_fk phi_k, B_f = sum_k k P_fk phi_k (potential.cpp:30-50)
+    float fc, dfc;
+    fc_dfc_fast(q.w, fc, dfc);
+    float phi[kK];
+    phi_fast(q.w, phi);
+    const float x0 = q.w * isg, step = mus * isg;
+    const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
+    float dself = 0.f, drev = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float4 mu4 = su_m[c], hu4 = su_h[c];
+        const float mwv[4] = {x.m[c].x, x.m[c].y, x.m[c].z, x.m[c].w};
+        const float hwv[4] = {x.h[c].x, x.h[c].y, x.h[c].z, x.h[c].w};
+        const float muv[4] = {mu4.x, mu4.y, mu4.z, mu4.w};
+        const float huv[4] = {hu4.x, hu4.y, hu4.z, hu4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int f = 4 * c + i;
+            float A = 0.f, B = 0.f;
+#pragma unroll
+            for (int k = 0; k < kK; ++k) {
+                A = fmaf(c_m.P[f * kK + k], phi[k], A);
+                B = fmaf(c_m.Pk[f * kK + k], phi[k], B);
+            }
+            const float ds = fmaf(ca, A, cb * B);
+            acc[f] = fmaf(mwv[i], fc * A, acc[f]);
+            dself = fmaf(muv[i] * hwv[i], ds, dself);
+            drev = fmaf(mwv[i] * huv[i], ds, drev);
+        }
+    }
+    const float invd = 1.0f / q.w;
+    const float coef = (dself + drev) * invd;
+    gx -= q.x * coef;
+    gy -= q.y * coef;
+    gz -= q.z * coef;
+    const float cself = dself * invd;
+    vr[0] = fmaf(cself * q.x, q.x, vr[0]);
+    vr[1] = fmaf(cself * q.y, q.y, vr[1]);
+    vr[2] = fmaf(cself * q.z, q.z, vr[2]);
+    vr[3] = fmaf(cself * q.x, q.y, vr[3]);
+    vr[4] = fmaf(cself * q.x, q.z, vr[4]);
+    vr[5] = fmaf(cself * q.y, q.z, vr[5]);
+}
+
 __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
                                                           const float* __restrict__ Hl,
                                                           float* __restrict__ HB,
@@ -366,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
     const int gl = lane & 15, grp = threadIdx.x >> 4;
     const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + grp;
     const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
-    const float rc = c_m.rc, irc = c_m.inv_rc, isg = c_m.inv_sigma, mus = c_m.mu_step;
+    const float isg = c_m.inv_sigma, mus = c_m.mu_step;
     if (gl < 6) sVir[grp][gl] = 0.0;
     const int64_t iters = (a.n + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
@@ -384,60 +452,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
         float gx = 0.f, gy = 0.f, gz = 0.f;
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (valid) {
-            const int e1 = __ldg(a.row + v + 1);
-            const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
-            const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
-            for (int e = __ldg(a.row + v) + gl; e < e1; e += 16) {
-                const float4 q = __ldg(a.vd + e);
-                // s_f = fc A_f, ds_f = dfc A_f - 2 fc/sigma (x0 A_f - a B_f) with
-                // A_f = sum_k P_fk phi_k, B_f = sum_k k P_fk phi_k (potential.cpp:30-50)
-                float fc, dfc;
-                fc_dfc_fast(q.w, fc, dfc);
-                float phi[kK];
-                phi_fast(q.w, phi);
-                const float x0 = q.w * isg, step = mus * isg;
-                const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
-                const int w = __ldg(a.lsrc + e);
-                const float4* mw = reinterpret_cast<const float4*>(MB + (size_t)w * kF);
-                const float4* hw = reinterpret_cast<const float4*>(Hl + (size_t)w * kF);
-                float dself = 0.f, drev = 0.f;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float4 m4 = __ldg(mw + c), h4 = __ldg(hw + c);
-                    const float4 mu4 = su_m[c], hu4 = su_h[c];
-                    const float mwv[4] = {m4.x, m4.y, m4.z, m4.w};
-                    const float hwv[4] = {h4.x, h4.y, h4.z, h4.w};
-                    const float muv[4] = {mu4.x, mu4.y, mu4.z, mu4.w};
-                    const float huv[4] = {hu4.x, hu4.y, hu4.z, hu4.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int f = 4 * c + i;
-                        float A = 0.f, B = 0.f;
-#pragma unroll
-                        for (int k = 0; k < kK; ++k) {
-                            A = fmaf(c_m.P[f * kK + k], phi[k], A);
-                            B = fmaf(c_m.Pk[f * kK + k], phi[k], B);
-                        }
-                        const float sv = fc * A, ds = fmaf(ca, A, cb * B);
-                        acc[f] = fmaf(mwv[i], sv, acc[f]);
-                        dself = fmaf(muv[i] * hwv[i], ds, dself);
-                        drev = fmaf(mwv[i] * huv[i], ds, drev);
-                    }
-                }
-                const float invd = 1.0f / q.w;
-                const float coef = (dself + drev) * invd;
-                gx -= q.x * coef;
-                gy -= q.y * coef;
-                gz -= q.z * coef;
-                const float cself = dself * invd;
-                vr[0] = fmaf(cself * q.x, q.x, vr[0]);
-                vr[1] = fmaf(cself * q.y, q.y, vr[1]);
-                vr[2] = fmaf(cself * q.z, q.z, vr[2]);
-                vr[3] = fmaf(cself * q.x, q.y, vr[3]);
-                vr[4] = fmaf(cself * q.x, q.z, vr[4]);
-                vr[5] = fmaf(cself * q.y, q.z, vr[5]);
-            }
+        const int e0 = valid ? __ldg(a.row + v) : 0;
+        const int e1 = valid ? __ldg(a.row + v + 1) : 0;
+        const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
+        const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
+        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 32) {
+            const bool ha = e < e1, hb = e + 16 < e1;
+            BwdEdgeIn xa, xb;
+            if (ha) bwd_load(a, MB, Hl, e, xa);
+            if (hb) bwd_load(a, MB, Hl, e + 16, xb);
+            if (ha) bwd_math(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
+            if (__any_sync(0xffffffffu, hb) && hb)
+                bwd_math(xb, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
         }
 #pragma unroll
         for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
