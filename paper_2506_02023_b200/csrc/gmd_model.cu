@@ -92,6 +92,15 @@ __device__ __forceinline__ void fc_dfc_fast(float d, float& fc, float& dfc) {
     dfc = in ? -0.5f * c_m.pi_rc * sn : 0.0f;
 }
 
+// 256-bit read-only load (LDG.E.ENL2.256 on sm_100a): one instruction per
+// 32-byte sector, so a 64-byte feature row costs two sector accesses.
+__device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                   "=f"(b.w)
+                 : "l"(p));
+}
+
 __device__ __forceinline__ void load_row16(const float* __restrict__ p, float h[kF]) {
     const float4* q = reinterpret_cast<const float4*>(p);
 #pragma unroll
@@ -243,13 +252,16 @@ constexpr int kNodesPerCta = kThreads / 16;  // half-warp (16 lanes) per node
 // lanes stride over its in-edges two at a time (both edges' loads in flight
 // before the math), fixed-order group reduction.  Reads 8 B per edge (d and
 // the source row); the radial channel is recomputed in registers.
-__device__ __forceinline__ void conv_edge(float d, const float4* __restrict__ hs, float acc[kF]) {
+__device__ __forceinline__ void conv_edge(float d, const float* __restrict__ hrow, float acc[kF]) {
+    float4 hv[4];
+    ldg256(hrow, hv[0], hv[1]);
+    ldg256(hrow + 8, hv[2], hv[3]);
     float phi[kK];
     phi_fast(d, phi);
     const float fc = fc_fast(d);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        const float4 h4 = __ldg(hs + c);
+        const float4 h4 = hv[c];
         const float hh[4] = {h4.x * fc, h4.y * fc, h4.z * fc, h4.w * fc};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -296,9 +308,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
             const float db = hb ? __ldg(a.d + e + 16) : 0.f;
             const int ia = ha ? __ldg(a.lsrc + e) : 0;
             const int ib = hb ? __ldg(a.lsrc + e + 16) : 0;
-            if (ha) conv_edge(da, reinterpret_cast<const float4*>(Hin + (size_t)ia * kF), acc);
-            if (__any_sync(0xffffffffu, hb) && hb)
-                conv_edge(db, reinterpret_cast<const float4*>(Hin + (size_t)ib * kF), acc);
+            if (ha) conv_edge(da, Hin + (size_t)ia * kF, acc);
+            if (__any_sync(0xffffffffu, hb) && hb) conv_edge(db, Hin + (size_t)ib * kF, acc);
         }
         const float m = transpose_reduce16_g16(acc, gl);  // feature gl
         float z = sb[gl];
@@ -365,13 +376,12 @@ __device__ __forceinline__ void bwd_load(const ConvArgs& a, const float* __restr
                                          const float* __restrict__ Hl, int e, BwdEdgeIn& x) {
     x.q = __ldg(a.vd + e);
     const int w = __ldg(a.lsrc + e);
-    const float4* mw = reinterpret_cast<const float4*>(MB + (size_t)w * kF);
-    const float4* hw = reinterpret_cast<const float4*>(Hl + (size_t)w * kF);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        x.m[c] = __ldg(mw + c);
-        x.h[c] = __ldg(hw + c);
-    }
+    const float* mw = MB + (size_t)w * kF;
+    const float* hw = Hl + (size_t)w * kF;
+    ldg256(mw, x.m[0], x.m[1]);
+    ldg256(mw + 8, x.m[2], x.m[3]);
+    ldg256(hw, x.h[0], x.h[1]);
+    ldg256(hw + 8, x.h[2], x.h[3]);
 }
 
 __device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
