@@ -129,6 +129,21 @@ int gmd_aggregate(gmd_handle* h, int bonds, const void* dev_buf, void* host_glob
 /* negative-control hook (engine.cpp:296): corrupt one transfer plan entry */
 int gmd_corrupt_transfer_plan_for_test(gmd_handle* h);
 
+/* ---- one rank per GPU ----------------------------------------
+ * Rank r of `world` owns slab r of p = world partitions: gmd_build then builds
+ * only r's rows (positions are replicated inputs), and gmd_forward exchanges
+ * halo rows with the peers every layer.  Outputs (per_atom, forces) are
+ * written for r's atoms only (zeros elsewhere); energy and stress are global.
+ * Transports: NCCL (one process per GPU; rank 0 makes the id, the caller
+ * broadcasts it) or an in-process group of handles (each driven by its own
+ * host thread; device-to-device copies). */
+int gmd_comm_nccl_id(uint8_t id[128]);
+int gmd_comm_init_nccl(gmd_handle* h, int rank, int world, const uint8_t id[128]);
+int gmd_comm_init_local(gmd_handle** handles, int world);
+int gmd_comm_info(const gmd_handle* h, int* rank, int* world);
+int gmd_num_owned(const gmd_handle* h, int64_t* n);
+int gmd_get_owned_ids(gmd_handle* h, int64_t* ids);
+
 /* ---- input synthesis helpers (system.hpp:99-149; host-side) ------------- */
 int gmd_util_rng_uniform(uint64_t seed, int64_t count, double lo, double hi, double* out);
 int gmd_util_supercell(int64_t n, const double* pos, const int32_t* Z, const double lattice[9],

@@ -15,12 +15,15 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
+#include <numeric>
 #include <random>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
 #include "../../include/graphmd_b200.h"
+#include "gmd_comm.cuh"
 #include "gmd_common.cuh"
 #include "gmd_graph.cuh"
 #include "gmd_model.cuh"
@@ -250,7 +253,7 @@ struct gmd_handle {
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
     DBuf row, src, img, vd, ed, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
-    DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp;
+    DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp, flagtmp;
     int nl_cap = 0;
 
     // model
@@ -262,6 +265,12 @@ struct gmd_handle {
     DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v3_part, red, per_atom,
         forces, conv_tmp, exp_tmp;
     cudaEvent_t ev[8] = {};
+
+    // one rank per GPU: transport + this rank's plan
+    std::unique_ptr<Transport> comm;
+    int64_t n_own = 0;
+    DBuf nodes, xsend, sendbuf;
+    std::vector<int64_t> soff, scnt, roff, rcnt;
 
     // profiler: event pairs recorded on `stream` around every launch
     bool prof = false;
@@ -364,7 +373,7 @@ void ensure_periodic_dev(gmd_handle* h, const uint8_t* pbc, double cutoff) {
 
 // PURE/TO/FROM layout of an id space (atoms or bonds) on the GPU
 void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
-                  const unsigned long long* req, int64_t nid, int p) {
+                  const unsigned long long* req, int64_t nid, int p, int only = -1) {
     cudaStream_t s = h->stream;
     ls.p = p;
     ls.nid = nid;
@@ -377,13 +386,13 @@ void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
     lw.scan_tmp_bytes = scan_tmp_bytes(nl * nch);
     lw.scan_tmp = h->scan_tmp.get<char>(lw.scan_tmp_bytes);
     int32_t* lo_d = ls.list_off_d.get<int32_t>(nl + 1);
-    { PROF("part_layout_plan"); launch_layout_plan(owner, req, nid, p, lw, lo_d, s); }
+    { PROF("part_layout_plan"); launch_layout_plan(owner, req, nid, p, lw, lo_d, only, s); }
     d2h(h, ls.list_off, lo_d, nl + 1);
     sync(h);
     ls.rows = ls.list_off[nl];
     int32_t* na = ls.node_array.get<int32_t>(ls.rows);
     int32_t* cr = ls.crow.get<int32_t>(nid);
-    { PROF("part_layout_fill"); launch_layout_fill(owner, req, nid, p, lw, na, cr, s); }
+    { PROF("part_layout_fill"); launch_layout_fill(owner, req, nid, p, lw, na, cr, only, s); }
     const int stride = 1 + 2 * p;
     std::vector<int32_t> rp(3 * p + 1);
     int32_t* ranges = rp.data();
@@ -394,7 +403,7 @@ void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
         ranges[2 * i + 1] = ls.list_off[(i + 1) * stride];
         prefix[i + 1] = prefix[i] + ranges[2 * i + 1] - ranges[2 * i];
     }
-    ls.nfrom = prefix[p];
+    ls.nfrom = only >= 0 ? 0 : prefix[p];  // rank mode exchanges through the transport
     int32_t* sm = h->small.get<int32_t>(3 * p + 1);
     GMD_CUDA(cudaMemcpyAsync(sm, rp.data(), sizeof(int32_t) * rp.size(), cudaMemcpyHostToDevice, s));
     PROF("part_from_src");
@@ -402,6 +411,43 @@ void build_layout(gmd_handle* h, LayoutState& ls, const int32_t* owner,
                     ls.xsrc.get<int32_t>(ls.nfrom), s);
     sync(h);  // rp is a host temporary
     ls.ready = true;
+}
+
+// one rank per GPU: this rank's atoms (ascending), the canonical rows of its
+// TO blocks packed per peer, and the FROM spans peers fill; checked against
+// the peers' plans (engine.cpp:132-133 "transfer plan misalignment")
+void build_rank_plan(gmd_handle* h, const int32_t* ownp, int r) {
+    cudaStream_t s = h->stream;
+    LayoutState& A = h->atoms;
+    const int W = h->p, stride = 1 + 2 * W;
+    const int64_t n = h->n;
+    int32_t* flag = h->flagtmp.get<int32_t>(n + 1);
+    launch_owned_flags(ownp, n, r, flag, s);
+    scan_i32(h, flag, flag, n);
+    int32_t nown = 0;
+    GMD_CUDA(cudaMemcpyAsync(&nown, flag + n, 4, cudaMemcpyDeviceToHost, s));
+    sync(h);
+    h->n_own = nown;
+    launch_owned_compact(ownp, n, r, flag, h->nodes.get<int32_t>(nown), s);
+    const int32_t t0 = A.list_off[(size_t)r * stride + 1], t1 = A.list_off[(size_t)r * stride + 1 + W];
+    launch_send_rows(t0, t1, A.node_array.as<int32_t>(), A.crow.as<int32_t>(),
+                     h->xsend.get<int32_t>(std::max(1, t1 - t0)), s);
+    h->soff.assign(W, 0);
+    h->scnt.assign(W, 0);
+    h->roff.assign(W, 0);
+    h->rcnt.assign(W, 0);
+    for (int j = 0; j < W; ++j) {
+        h->soff[j] = A.list_off[(size_t)r * stride + 1 + j] - t0;
+        h->scnt[j] = A.list_off[(size_t)r * stride + 2 + j] - A.list_off[(size_t)r * stride + 1 + j];
+        h->roff[j] = A.list_off[(size_t)r * stride + 1 + W + j];
+        h->rcnt[j] = A.list_off[(size_t)r * stride + 2 + W + j] - h->roff[j];
+    }
+    std::vector<int64_t> all((size_t)W * W);
+    h->comm->allgather_i64(s, h->scnt.data(), W, all.data());
+    for (int j = 0; j < W; ++j)
+        if (j != r && all[(size_t)j * W + r] != h->rcnt[j])
+            raise(kRuntime, "transfer plan misalignment");
+    sync(h);
 }
 
 void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, const double* lat,
@@ -494,75 +540,21 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     { PROF("nl_wrap"); launch_wrap(g, n, b, s); }
     { PROF("scan"); scan_i32(h, b.bin_cnt, b.bin_start, nbins); }
     { PROF("nl_bin_scatter"); launch_bin_scatter(g, n, b, fillp, s); }
-    // fp32 prefilter threshold: keeps every pair the fp64 prefilter keeps.
-    // Coordinates are taken relative to the destination bin origin, so each
-    // component is bounded by B = max_k sum_r |L_rk| (s_r + 1) / bins_r; fp32
-    // rounding moves each component of v by at most delta = 4 B 2^-24.
-    float thr32;
-    {
-        double B = 0.0;
-        for (int k = 0; k < 3; ++k) {
-            double bk = 0.0;
-            for (int r = 0; r < 3; ++r)
-                bk += std::abs(g.L[3 * r + k]) * (double)(g.sten[r] + 1) / g.bins[r];
-            B = std::max(B, bk);
-        }
-        B *= 1.01;
-        const double u = std::ldexp(1.0, -24);
-        const double delta = 4.0 * B * u;
-        const double r = std::sqrt(g.pre2) * (1.0 + 1e-9) + std::sqrt(3.0) * delta;
-        const double thr = r * r * (1.0 + 8.0 * u);
-        thr32 = std::nextafter((float)thr, INFINITY);
-    }
-    int cap = h->nl_cap;
-    if (cap <= 0) {  // first build: density estimate of the mean degree
-        const double mean = (double)n * 4.18879020478639 * rc * rc * rc / std::abs(det3(h->lat));
-        cap = ((int)(1.2 * mean + 16) + 7) & ~7;
-    }
-    int32_t* rowp = h->row.get<int32_t>(n + 1);
-    int32_t hdr[2];
-    int32_t ne32 = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        auto* slab = h->slab.get<unsigned long long>((size_t)n * cap);
-        { PROF("nl_search"); launch_nl_search(g, thr32, nbins, n, cap, b, slab, s); }
-        { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
-        GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
-        read_flags(h, hdr);
-        if (hdr[0] <= cap) break;
-        cap = (hdr[0] + 7) & ~7;  // rare: an atom exceeded the slab row
-        GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
-    }
-    {   // next build: size the slab from this one's maximum degree
-        h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
-    }
-    if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
-    h->ne = ne32;
-    GraphDev gd;
-    gd.n = n;
-    gd.ne = h->ne;
-    gd.row = rowp;
-    gd.src = h->src.get<int32_t>(h->ne);
-    gd.img = h->img.get<uint32_t>(h->ne);
-    gd.vd = h->vd.get<float4>(h->ne);
-    gd.d = h->ed.get<float>(h->ne);
-    gd.bond = h->ebond.get<uint8_t>(h->ne);
-    { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s); }
-
-    // ---- partitions (partitioner.cpp:46-218)
+    // ---- partition rule and owners (partitioner.cpp:46-108).  Owners only
+    // depend on the wrapped fractional coordinate, so they are known before
+    // the neighbour search -- one rank per GPU then builds only its rows.
+    const bool rank_mode = h->comm && h->comm->world > 1;
+    const int myrank = rank_mode ? h->comm->rank : -1;
+    if (rank_mode && p != h->comm->world)
+        raise(kConfig, "one-rank-per-GPU mode needs p == world size");
+    if (rank_mode && r3 > 0.0)
+        raise(kConfig, "three-body graphs are not supported in one-rank-per-GPU mode yet");
     h->bounds.assign(p + 1, 0.0);
     h->bounds[p] = 1.0;
     int32_t* ownp = h->atoms.owner.get<int32_t>(n);
     LayoutState& A = h->atoms;
     if (p == 1) {
         GMD_CUDA(cudaMemsetAsync(ownp, 0, sizeof(int32_t) * n, s));
-        A.p = 1;
-        A.nid = n;
-        A.list_off = {0, (int32_t)n, (int32_t)n, (int32_t)n};
-        A.rows = n;
-        A.nfrom = 0;
-        A.ready = true;
-        A.api_ready = A.dups_ready = false;
-        A.h_nodes.clear();
     } else {
         if (flags & GMD_EQUAL_WIDTH) {
             for (int k = 1; k < p; ++k) h->bounds[k] = (double)k / p;
@@ -614,13 +606,91 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         bd.p = p;
         for (int k = 0; k <= p; ++k) bd.b[k] = h->bounds[k];
         { PROF("part_owner"); launch_owner(b.fw_axis, n, bd, ownp, s); }
+    }
+    if (rank_mode) GMD_CUDA(cudaMemsetAsync(b.deg, 0, sizeof(int32_t) * n, s));
+
+    // fp32 prefilter threshold: keeps every pair the fp64 prefilter keeps.
+    // Coordinates are taken relative to the destination bin origin, so each
+    // component is bounded by B = max_k sum_r |L_rk| (s_r + 1) / bins_r; fp32
+    // rounding moves each component of v by at most delta = 4 B 2^-24.
+    float thr32;
+    {
+        double B = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            double bk = 0.0;
+            for (int r = 0; r < 3; ++r)
+                bk += std::abs(g.L[3 * r + k]) * (double)(g.sten[r] + 1) / g.bins[r];
+            B = std::max(B, bk);
+        }
+        B *= 1.01;
+        const double u = std::ldexp(1.0, -24);
+        const double delta = 4.0 * B * u;
+        const double r = std::sqrt(g.pre2) * (1.0 + 1e-9) + std::sqrt(3.0) * delta;
+        const double thr = r * r * (1.0 + 8.0 * u);
+        thr32 = std::nextafter((float)thr, INFINITY);
+    }
+    int cap = h->nl_cap;
+    if (cap <= 0) {  // first build: density estimate of the mean degree
+        const double mean = (double)n * 4.18879020478639 * rc * rc * rc / std::abs(det3(h->lat));
+        cap = ((int)(1.2 * mean + 16) + 7) & ~7;
+    }
+    int32_t* rowp = h->row.get<int32_t>(n + 1);
+    int32_t hdr[2];
+    int32_t ne32 = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        auto* slab = h->slab.get<unsigned long long>((size_t)n * cap);
+        { PROF("nl_search"); launch_nl_search(g, thr32, nbins, n, cap, b, slab, ownp, myrank, s); }
+        { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
+        GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
+        read_flags(h, hdr);
+        if (hdr[0] <= cap) break;
+        cap = (hdr[0] + 7) & ~7;  // rare: an atom exceeded the slab row
+        GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
+    }
+    {   // next build: size the slab from this one's maximum degree
+        h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
+    }
+    if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
+    h->ne = ne32;
+    GraphDev gd;
+    gd.n = n;
+    gd.ne = h->ne;
+    gd.row = rowp;
+    gd.src = h->src.get<int32_t>(h->ne);
+    gd.img = h->img.get<uint32_t>(h->ne);
+    gd.vd = h->vd.get<float4>(h->ne);
+    gd.d = h->ed.get<float>(h->ne);
+    gd.bond = h->ebond.get<uint8_t>(h->ne);
+    { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s); }
+
+    // ---- requirement masks, span layouts, local edge ends (partitioner.cpp:110-218)
+    h->n_own = n;
+    if (p == 1) {
+        A.p = 1;
+        A.nid = n;
+        A.list_off = {0, (int32_t)n, (int32_t)n, (int32_t)n};
+        A.rows = n;
+        A.nfrom = 0;
+        A.ready = true;
+        A.api_ready = A.dups_ready = false;
+        A.h_nodes.clear();
+    } else {
         auto* reqp = A.req.get<unsigned long long>(n);
         GMD_CUDA(cudaMemsetAsync(reqp, 0, sizeof(unsigned long long) * n, s));
-        { PROF("part_required"); launch_required(rowp, gd.src, n, ownp, reqp, s); }
-        build_layout(h, A, ownp, reqp, n, p);
-        PROF("part_edge_lsrc");
-        launch_edge_lsrc(rowp, gd.src, n, ownp, A.crow.as<int32_t>(), A.node_array.as<int32_t>(),
-                         A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(h->ne), b.flags, s);
+        if (rank_mode) {
+            PROF("part_required");
+            launch_required_rank(rowp, gd.src, n, ownp, myrank, reqp, s);
+        } else {
+            PROF("part_required");
+            launch_required(rowp, gd.src, n, ownp, reqp, s);
+        }
+        build_layout(h, A, ownp, reqp, n, p, myrank);
+        {
+            PROF("part_edge_lsrc");
+            launch_edge_lsrc(rowp, gd.src, n, ownp, A.crow.as<int32_t>(), A.node_array.as<int32_t>(),
+                             A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(h->ne), b.flags, s);
+        }
+        if (rank_mode) build_rank_plan(h, ownp, myrank);
     }
 
     // ---- three-body bonds (linegraph.cpp:25-43) + reverse-bond index
@@ -821,11 +891,14 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     if (std::abs(h->rc - h->p_r_atom) > 1e-12)
         raise(kConfig, "distributed handle cutoff does not match the parameters");
     cudaStream_t s = h->stream;
-    const int64_t n = h->n;
+    const int64_t n_all = h->n;
+    const bool rank_mode = h->comm && h->comm->world > 1;
+    const int64_t n = rank_mode ? h->n_own : n_all;  // nodes this handle updates
     const int L = h->L;
     LayoutState& A = h->atoms;
     const int64_t R = A.rows;
     const bool part = h->p > 1;
+    if (rank_mode && tb) raise(kConfig, "three-body graphs are not supported in one-rank-per-GPU mode yet");
     upload_model(h->mc, s);
 
     GMD_CUDA(cudaEventRecord(h->ev[2], s));
@@ -842,10 +915,15 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     const int tgrid = tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
-    double* pa = h->per_atom.get<double>(n);
+    double* pa = h->per_atom.get<double>(n_all);
+    if (rank_mode) GMD_CUDA(cudaMemsetAsync(pa, 0, sizeof(double) * n_all, s));
 
-    ConvArgs a{n, part ? A.crow.as<int32_t>() : nullptr, h->row.as<int32_t>(),
-               part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(), h->vd.as<float4>(),
+    ConvArgs a{n,
+               rank_mode ? h->nodes.as<int32_t>() : nullptr,
+               part ? A.crow.as<int32_t>() : nullptr,
+               h->row.as<int32_t>(),
+               part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(),
+               h->vd.as<float4>(),
                h->ed.as<float>()};
     BondArgs ba{n,
                 a.crow,
@@ -862,6 +940,30 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
     const int32_t* xd = A.xdst.as<int32_t>();
     const int32_t* xs = A.xsrc.as<int32_t>();
+    // halo exchange of a row buffer: FROM rows <- owners' canonical rows
+    // (engine.cpp:122-143); one rank per GPU packs its TO rows and goes
+    // through the transport
+    const int64_t nsend = rank_mode ? std::accumulate(h->scnt.begin(), h->scnt.end(), (int64_t)0) : 0;
+    float* sendbuf = rank_mode ? h->sendbuf.get<float>(std::max<int64_t>(1, nsend) * kF) : nullptr;
+    auto exchange = [&](float* buf) {
+        if (rank_mode) {
+            {
+                PROF("halo_pack");
+                if (nsend > 0) {
+                    k_gather_rows<<<div_up(nsend * kF, 256), 256, 0, s>>>(
+                        nsend, h->xsend.as<int32_t>(), reinterpret_cast<const uint32_t*>(buf),
+                        reinterpret_cast<uint32_t*>(sendbuf), kF);
+                    GMD_LAUNCH_CHECK();
+                }
+            }
+            PROF("halo_exchange");
+            h->comm->exchange(s, sendbuf, h->soff.data(), h->scnt.data(), buf, h->roff.data(),
+                              h->rcnt.data(), kF);
+        } else if (A.nfrom > 0) {
+            PROF("exchange");
+            launch_exchange(A.nfrom, xd, xs, buf, kF, s);
+        }
+    };
 
     // ---- feature calculation: embeddings for every layout row (:597-602)
     { PROF("embed"); launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s); }
@@ -874,7 +976,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             { PROF("tb_forward"); launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), s); }
             { PROF("tb_inject"); launch_tb_inject(ba, TP, H[l], TH4, s); }
         }
-        if ((l > 0 || tbl) && A.nfrom > 0) { PROF("exchange"); launch_exchange(A.nfrom, xd, xs, H[l], kF, s); }
+        if (l > 0 || tbl) exchange(H[l]);
         PROF("conv");
         launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
                     l == L - 1 ? e_part : nullptr, s);
@@ -885,8 +987,8 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     launch_init_hbar(n, HB, s);
     GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
-        { PROF("bwd_node"); launch_bwd_node(n, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s); }
-        if (A.nfrom > 0) { PROF("exchange"); launch_exchange(A.nfrom, xd, xs, MB, kF, s); }
+        { PROF("bwd_node"); launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s); }
+        exchange(MB);
         { PROF("bwd_edge"); launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * grid * 6, s); }
         if (tb && l == L - 1) {
             float* QB = h->QB.get<float>(n * kF);
@@ -903,11 +1005,15 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     float* ff = nullptr;
     if (forces) {
         if (out_f32)
-            ff = out_dev ? static_cast<float*>(forces) : h->forces.get<float>(3 * n);
+            ff = out_dev ? static_cast<float*>(forces) : h->forces.get<float>(3 * n_all);
         else
-            fd = out_dev ? static_cast<double*>(forces) : h->forces.get<double>(3 * n);
+            fd = out_dev ? static_cast<double*>(forces) : h->forces.get<double>(3 * n_all);
+        if (rank_mode) {  // only this rank's atoms are written
+            if (ff) GMD_CUDA(cudaMemsetAsync(ff, 0, 12 * n_all, s));
+            if (fd) GMD_CUDA(cudaMemsetAsync(fd, 0, 24 * n_all, s));
+        }
         PROF("forces_out");
-        launch_forces_out(n, GRAD, fd, ff, s);
+        launch_forces_out(n, a.nodes, GRAD, fd, ff, s);
     }
     launch_reduce_partials(e_part, grid, 1, red, s);
     launch_reduce_partials(v_part, L * grid, 6, red + 1, s);
@@ -921,24 +1027,33 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     GMD_CUDA(cudaMemcpyAsync(hred, red, sizeof hred, cudaMemcpyDeviceToHost, s));
     if (per_atom) {
         if (out_f32) {
-            float* dst = out_dev ? static_cast<float*>(per_atom) : h->conv_tmp.get<float>(n);
-            k_to_f32<<<div_up(n, 256), 256, 0, s>>>(n, pa, dst);
+            float* dst = out_dev ? static_cast<float*>(per_atom) : h->conv_tmp.get<float>(n_all);
+            k_to_f32<<<div_up(n_all, 256), 256, 0, s>>>(n_all, pa, dst);
             GMD_LAUNCH_CHECK();
             if (!out_dev)
-                GMD_CUDA(cudaMemcpyAsync(per_atom, dst, 4 * n, cudaMemcpyDeviceToHost, s));
+                GMD_CUDA(cudaMemcpyAsync(per_atom, dst, 4 * n_all, cudaMemcpyDeviceToHost, s));
         } else {
-            GMD_CUDA(cudaMemcpyAsync(per_atom, pa, 8 * n, out_dev ? cudaMemcpyDeviceToDevice
-                                                                  : cudaMemcpyDeviceToHost, s));
+            GMD_CUDA(cudaMemcpyAsync(per_atom, pa, 8 * n_all, out_dev ? cudaMemcpyDeviceToDevice
+                                                                      : cudaMemcpyDeviceToHost, s));
         }
     }
     if (forces && !out_dev) {
         if (out_f32)
-            GMD_CUDA(cudaMemcpyAsync(forces, ff, 12 * n, cudaMemcpyDeviceToHost, s));
+            GMD_CUDA(cudaMemcpyAsync(forces, ff, 12 * n_all, cudaMemcpyDeviceToHost, s));
         else
-            GMD_CUDA(cudaMemcpyAsync(forces, fd, 24 * n, cudaMemcpyDeviceToHost, s));
+            GMD_CUDA(cudaMemcpyAsync(forces, fd, 24 * n_all, cudaMemcpyDeviceToHost, s));
     }
     int32_t hdr[2];
     read_flags(h, hdr);  // synchronizes the stream
+    if (rank_mode) {  // energy + virial: rank-ordered sum of the per-rank sums
+        std::vector<double> all((size_t)h->comm->world * 16);
+        h->comm->allgather_f64(s, hred, 16, all.data());
+        for (int c = 0; c < 16; ++c) {
+            double acc = 0.0;
+            for (int j = 0; j < h->comm->world; ++j) acc += all[(size_t)j * 16 + c];
+            hred[c] = acc;
+        }
+    }
     if (!std::isfinite(hred[0])) raise(kRuntime, "non-finite energy (non-finite features)");
     if (energy) *energy = hred[0];
     if (stress) {  // stress = sym(virial) / V (potential.cpp:978-982)
@@ -1023,7 +1138,7 @@ void gmd_destroy(gmd_handle* h) {
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ed, &h->ebond, &h->edst, &h->lsrc, &h->counts,
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
-                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
+                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->flagtmp, &h->nodes, &h->xsend, &h->sendbuf, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp};
     for (DBuf* b : bufs) b->release();
@@ -1546,6 +1661,63 @@ int gmd_corrupt_transfer_plan_for_test(gmd_handle* h) {
     return run(h, [&] {
         need_built(h);
         h->corrupted = true;
+    });
+}
+
+int gmd_comm_nccl_id(uint8_t id[128]) {
+    if (!id) return GMD_ERR_ARG;
+    std::string err;
+    if (!nccl_unique_id(id, &err)) {
+        g_err = err;
+        return GMD_ERR_CUDA;
+    }
+    return GMD_OK;
+}
+
+int gmd_comm_init_nccl(gmd_handle* h, int rank, int world, const uint8_t id[128]) {
+    return run(h, [&] {
+        if (!id || world < 1 || rank < 0 || rank >= world) raise(kArg, "bad rank/world");
+        h->comm.reset(make_nccl_transport(rank, world, id, h->device));
+        h->built = false;
+    });
+}
+
+int gmd_comm_init_local(gmd_handle** hs, int world) {
+    if (!hs || world < 1) return GMD_ERR_ARG;
+    for (int r = 0; r < world; ++r)
+        if (!hs[r]) return GMD_ERR_ARG;
+    LocalGroup* g = local_group_create(world);
+    for (int r = 0; r < world; ++r) {
+        hs[r]->comm.reset(make_local_transport(g, r));
+        hs[r]->built = false;
+    }
+    return GMD_OK;
+}
+
+int gmd_comm_info(const gmd_handle* h, int* rank, int* world) {
+    if (!h) return GMD_ERR_ARG;
+    if (rank) *rank = h->comm ? h->comm->rank : 0;
+    if (world) *world = h->comm ? h->comm->world : 1;
+    return GMD_OK;
+}
+
+int gmd_num_owned(const gmd_handle* h, int64_t* n) {
+    if (!h || !n) return GMD_ERR_ARG;
+    *n = h->built ? (h->comm && h->comm->world > 1 ? h->n_own : h->n) : 0;
+    return GMD_OK;
+}
+
+int gmd_get_owned_ids(gmd_handle* h, int64_t* ids) {
+    return run(h, [&] {
+        need_built(h);
+        if (h->comm && h->comm->world > 1) {
+            std::vector<int32_t> v;
+            d2h(h, v, h->nodes.as<int32_t>(), h->n_own);
+            sync(h);
+            std::copy(v.begin(), v.end(), ids);
+        } else {
+            for (int64_t i = 0; i < h->n; ++i) ids[i] = i;
+        }
     });
 }
 

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
     const int32_t* __restrict__ bin_start, const int32_t* __restrict__ s_id,
     const double* __restrict__ s_w, const double* __restrict__ s_p,
     const int32_t* __restrict__ s_c, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
-    unsigned long long* __restrict__ slab) {
+    unsigned long long* __restrict__ slab, const int32_t* __restrict__ owner, int only) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp carve-up by byte offsets (keeps the shared address space)
@@ -183,24 +183,37 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
         // bin origin (any common origin works; it only conditions fp32)
         const d3 org = rowvec_rn(g.L, (double)bx / g.bins[0], (double)by / g.bins[1],
                                  (double)bz / g.bins[2]);
-        for (int gbase = b0; gbase < b1; gbase += group) {
-            const int nd = min(group, b1 - gbase);
+        // destination atoms of this bin, in groups of <= `group`; with
+        // only >= 0 (one rank per GPU) just the atoms that rank owns
+        for (int pos = b0; pos < b1;) {
+            int nd = 0;
             __syncwarp();
-            for (int t = lane; t < nd; t += 32) {
-                const int slot = gbase + t;
-                double w3[3];
+            while (nd < group && pos < b1) {
+                const int slot = pos + lane;
+                const bool ok = slot < b1 && (only < 0 || owner[s_id[slot]] == only);
+                const unsigned m = __ballot_sync(0xffffffffu, ok);
+                const int navail = __popc(m), take = min(navail, group - nd);
+                const int rank = __popc(m & ((1u << lane) - 1u));
+                if (ok && rank < take) {
+                    const int t = nd + rank;
+                    double w3[3];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    w3[k] = s_w[k * n + slot];
-                    d_w[3 * t + k] = w3[k];
-                    d_p[3 * t + k] = s_p[k * n + slot];
-                    d_c[3 * t + k] = s_c[k * n + slot];
+                    for (int k = 0; k < 3; ++k) {
+                        w3[k] = s_w[k * n + slot];
+                        d_w[3 * t + k] = w3[k];
+                        d_p[3 * t + k] = s_p[k * n + slot];
+                        d_c[3 * t + k] = s_c[k * n + slot];
+                    }
+                    d32[t] = make_float4((float)(w3[0] - org.x), (float)(w3[1] - org.y),
+                                         (float)(w3[2] - org.z), 0.f);
+                    d_id[t] = s_id[slot];
+                    d_cnt[t] = 0;
                 }
-                d32[t] = make_float4((float)(w3[0] - org.x), (float)(w3[1] - org.y),
-                                     (float)(w3[2] - org.z), 0.f);
-                d_id[t] = s_id[slot];
-                d_cnt[t] = 0;
+                nd += take;
+                pos = take < navail ? pos + (int)__fns(m, 0, take + 1) : pos + 32;
             }
+            __syncwarp();
+            if (nd == 0) break;
             for (int cbase = 0; cbase < ncell; cbase += kWSCap) {
                 const int nc = min(kWSCap, ncell - cbase);
                 __syncwarp();
@@ -541,7 +554,8 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
 }
 
 void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
-                      NLBuffers& b, unsigned long long* slab, cudaStream_t s) {
+                      NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
+                      cudaStream_t s) {
     int group = 16;
     while (group > 1 && nl_smem(group, cap) > 110 * 1024) group >>= 1;
     const size_t sm = nl_smem(group, cap);
@@ -554,7 +568,7 @@ void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int 
     }
     k_nl_search<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, nbins, n, group, cap, b.bin_start,
                                                      b.s_id, b.s_w, b.s_p, b.s_c, b.deg, b.flags,
-                                                     slab);
+                                                     slab, owner, only);
     GMD_LAUNCH_CHECK();
 }
 

@@ -295,8 +295,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
     // both half-warps iterate the same number of times (shuffles span the warp)
     const int64_t iters = (a.n + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t v = g0 + it * ng;
-        const bool valid = v < a.n;
+        const int64_t k = g0 + it * ng;  // local node index
+        const bool valid = k < a.n;
+        const int64_t v = valid ? (a.nodes ? (int64_t)a.nodes[k] : k) : 0;  // global id
         float acc[kF];
 #pragma unroll
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
             const int64_t r = a.crow ? a.crow[v] : v;
             const float hn = Hin[r * kF + gl] + th;
             Hout[r * kF + gl] = hn;
-            TH[v * kF + gl] = th;
+            TH[k * kF + gl] = th;
             ev = sro[gl] * hn;
         }
         if (per_atom) {
@@ -340,14 +341,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
 }
 
 // m_bar = W^T (h_bar * sech^2) (potential.cpp:816-822), thread per node
-__global__ void k_bwd_node(int64_t n, const int32_t* __restrict__ crow, int layer,
+__global__ void k_bwd_node(int64_t n, const int32_t* __restrict__ nodes,
+                           const int32_t* __restrict__ crow, int layer,
                            const float* __restrict__ HB, const float* __restrict__ TH,
                            float* __restrict__ MB) {
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t v = nodes ? (int64_t)nodes[k] : k;
     float hb[kF], th[kF], y[kF];
-    load_row16(HB + v * kF, hb);
-    load_row16(TH + v * kF, th);
+    load_row16(HB + k * kF, hb);
+    load_row16(TH + k * kF, th);
 #pragma unroll
     for (int f = 0; f < kF; ++f) y[f] = hb[f] * (1.0f - th[f] * th[f]);
     float mb[kF];
@@ -448,8 +451,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
     if (gl < 6) sVir[grp][gl] = 0.0;
     const int64_t iters = (a.n + ng - 1) / ng;
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t v = g0 + it * ng;
-        const bool valid = v < a.n;
+        const int64_t k = g0 + it * ng;  // local node index
+        const bool valid = k < a.n;
+        const int64_t v = valid ? (a.nodes ? (int64_t)a.nodes[k] : k) : 0;  // global id
         const int64_t r = valid ? (a.crow ? a.crow[v] : v) : 0;
         __syncwarp();
         if (valid) {
@@ -485,13 +489,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
         gy = group_sum16(gy);
         gz = group_sum16(gz);
         if (valid) {
-            HB[v * kF + gl] += hb;
+            HB[k * kF + gl] += hb;
             if (gl == 0) {
-                float4 g = GRAD[v];
+                float4 g = GRAD[k];
                 g.x += gx;
                 g.y += gy;
                 g.z += gz;
-                GRAD[v] = g;
+                GRAD[k] = g;
             }
         }
     }
@@ -781,11 +785,12 @@ __global__ void k_init_hbar(int64_t n, float* HB) {
     HB[t] = c_m.ro[t % kF];
 }
 
-__global__ void k_forces_out(int64_t n, const float4* __restrict__ GRAD, double* forces,
-                             float* forces32) {
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    float4 g = GRAD[v];
+__global__ void k_forces_out(int64_t n, const int32_t* __restrict__ nodes,
+                             const float4* __restrict__ GRAD, double* forces, float* forces32) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t v = nodes ? (int64_t)nodes[k] : k;
+    float4 g = GRAD[k];
     if (forces) {
         forces[3 * v] = -(double)g.x;
         forces[3 * v + 1] = -(double)g.y;
@@ -843,10 +848,10 @@ void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, fl
     GMD_LAUNCH_CHECK();
 }
 
-void launch_bwd_node(int64_t n, const int32_t* crow, int layer, const float* HB, const float* TH,
-                     float* MB, cudaStream_t s) {
+void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int layer,
+                     const float* HB, const float* TH, float* MB, cudaStream_t s) {
     if (n == 0) return;
-    k_bwd_node<<<div_up(n, 128), 128, 0, s>>>(n, crow, layer, HB, TH, MB);
+    k_bwd_node<<<div_up(n, 128), 128, 0, s>>>(n, nodes, crow, layer, HB, TH, MB);
     GMD_LAUNCH_CHECK();
 }
 
@@ -895,10 +900,10 @@ void launch_init_hbar(int64_t n, float* HB, cudaStream_t s) {
     GMD_LAUNCH_CHECK();
 }
 
-void launch_forces_out(int64_t n, const float4* GRAD, double* forces, float* forces32,
-                       cudaStream_t s) {
+void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, double* forces,
+                       float* forces32, cudaStream_t s) {
     if (n == 0) return;
-    k_forces_out<<<div_up(n, 256), 256, 0, s>>>(n, GRAD, forces, forces32);
+    k_forces_out<<<div_up(n, 256), 256, 0, s>>>(n, nodes, GRAD, forces, forces32);
     GMD_LAUNCH_CHECK();
 }
 

@@ -35,7 +35,8 @@ void upload_model(const ModelConst& m, cudaStream_t s);
 // (super-)layout of its owner partition (nullptr = identity); lsrc is the
 // source row per edge.
 struct ConvArgs {
-    int64_t n;
+    int64_t n;              // number of owned nodes processed
+    const int32_t* nodes;   // their global ids, ascending (nullptr: 0..n-1)
     const int32_t* crow;
     const int32_t* row;
     const int32_t* lsrc;
@@ -54,8 +55,8 @@ void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float
 void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
                  double* per_atom, double* e_part, cudaStream_t s);
 // backward: MB[row(v)] = W_l^T (HB[v] * (1 - TH_l[v]^2))
-void launch_bwd_node(int64_t n, const int32_t* crow, int layer, const float* HB, const float* TH,
-                     float* MB, cudaStream_t s);
+void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int layer,
+                     const float* HB, const float* TH, float* MB, cudaStream_t s);
 // backward edge pass (row form, no atomics): HB += gathered adjoints,
 // GRAD += positional gradient, virial partials per CTA (6 doubles)
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
@@ -80,8 +81,8 @@ void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, fl
                     cudaStream_t s);
 
 void launch_init_hbar(int64_t n, float* HB, cudaStream_t s);
-void launch_forces_out(int64_t n, const float4* GRAD, double* forces, float* forces32,
-                       cudaStream_t s);
+void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, double* forces,
+                       float* forces32, cudaStream_t s);
 // sum nparts consecutive records of width w into out[w] in fixed order
 void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s);
 

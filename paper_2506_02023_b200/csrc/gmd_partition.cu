@@ -130,6 +130,49 @@ __global__ void k_required(const int32_t* __restrict__ row, const int32_t* __res
     }
 }
 
+// One rank per GPU: only the rank's own rows exist.  FROM bits come straight
+// from the rows (an in-edge u -> v of an owned v marks u as required by r,
+// partitioner.cpp:124-134); TO bits of an owned v use the reverse edge (every
+// edge u -> v has the reverse v -> u, neighborlist symmetry).
+__global__ void k_required_rank(const int32_t* __restrict__ row, const int32_t* __restrict__ src,
+                                int64_t n, const int32_t* __restrict__ owner, int r,
+                                unsigned long long* __restrict__ req) {
+    int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (v >= n || owner[v] != r) return;
+    unsigned long long m = 0ull;
+    for (int e = row[v] + (threadIdx.x & 31); e < row[v + 1]; e += 32) {
+        const int u = src[e];
+        const int ou = owner[u];
+        if (ou != r) {
+            atomicOr(&req[u], 1ull << r);
+            m |= 1ull << ou;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+    if ((threadIdx.x & 31) == 0 && m) atomicOr(&req[v], m);
+}
+
+__global__ void k_flag_owned(const int32_t* __restrict__ owner, int64_t n, int r,
+                             int32_t* __restrict__ flag) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) flag[v] = owner[v] == r ? 1 : 0;
+}
+
+__global__ void k_compact_owned(const int32_t* __restrict__ owner, int64_t n, int r,
+                                const int32_t* __restrict__ pos, int32_t* __restrict__ nodes) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n && owner[v] == r) nodes[pos[v]] = (int32_t)v;
+}
+
+// send plan: canonical row of every TO row of partition r (TO region rows
+// [t0, t1) of the super layout)
+__global__ void k_send_rows(int32_t t0, int32_t t1, const int32_t* __restrict__ node_array,
+                            const int32_t* __restrict__ crow, int32_t* __restrict__ xsend) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t0 + k < t1) xsend[k] = crow[node_array[t0 + k]];
+}
+
 // ---------------------------------------------------------------------------
 // stable multi-list compaction (build_span_layout, partitioner.cpp:153-180)
 // ---------------------------------------------------------------------------
@@ -159,9 +202,20 @@ __device__ __forceinline__ int next_list(int o, unsigned long long m, int p, int
     return best;
 }
 
+// memberships restricted to partition `only` (>= 0), i.e. lists
+// [only*stride, (only+1)*stride); only < 0 keeps every partition
+__device__ __forceinline__ int next_list_only(int o, unsigned long long m, int p, int last,
+                                              int only) {
+    const int stride = 1 + 2 * p;
+    int l = next_list(o, m, p, last);
+    if (only >= 0)
+        while (l != 0x7fffffff && l / stride != only) l = next_list(o, m, p, l);
+    return l;
+}
+
 __global__ void k_lay_count(const int32_t* __restrict__ owner,
                             const unsigned long long* __restrict__ req, int64_t nid, int p,
-                            int nlists, int64_t nchunks, int32_t* __restrict__ counts) {
+                            int nlists, int64_t nchunks, int32_t* __restrict__ counts, int only) {
     extern __shared__ int cnt[];
     for (int l = threadIdx.x; l < nlists; l += 32) cnt[l] = 0;
     __syncwarp();
@@ -170,7 +224,8 @@ __global__ void k_lay_count(const int32_t* __restrict__ owner,
     for (int64_t v = b0 + threadIdx.x; v < b1; v += 32) {
         int o = owner[v];
         unsigned long long m = req[v];
-        for (int l = next_list(o, m, p, -1); l != 0x7fffffff; l = next_list(o, m, p, l))
+        for (int l = next_list_only(o, m, p, -1, only); l != 0x7fffffff;
+             l = next_list_only(o, m, p, l, only))
             atomicAdd(&cnt[l], 1);
     }
     __syncwarp();
@@ -180,7 +235,8 @@ __global__ void k_lay_count(const int32_t* __restrict__ owner,
 __global__ void k_lay_scatter(const int32_t* __restrict__ owner,
                               const unsigned long long* __restrict__ req, int64_t nid, int p,
                               int nlists, int64_t nchunks, const int32_t* __restrict__ offs,
-                              int32_t* __restrict__ node_array, int32_t* __restrict__ crow) {
+                              int32_t* __restrict__ node_array, int32_t* __restrict__ crow,
+                              int only) {
     extern __shared__ int run[];
     const int lane = threadIdx.x;
     for (int l = lane; l < nlists; l += 32) run[l] = 0;
@@ -193,7 +249,7 @@ __global__ void k_lay_scatter(const int32_t* __restrict__ owner,
         const bool valid = v < b1;
         int o = valid ? owner[v] : 0;
         unsigned long long m = valid ? req[v] : 0ull;
-        int cur = valid ? next_list(o, m, p, -1) : 0x7fffffff;
+        int cur = valid ? next_list_only(o, m, p, -1, only) : 0x7fffffff;
         const int canon = m == 0ull ? o * stride : o * stride + __ffsll((long long)m);
         while (true) {
             int lmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)cur);
@@ -205,7 +261,7 @@ __global__ void k_lay_scatter(const int32_t* __restrict__ owner,
                 int pos = offs[(int64_t)lmin * nchunks + c] + run[lmin] + rank;
                 node_array[pos] = (int32_t)v;
                 if (lmin == canon) crow[v] = pos;
-                cur = next_list(o, m, p, cur);
+                cur = next_list_only(o, m, p, cur, only);
             }
             __syncwarp();
             if (lane == 0) run[lmin] += __popc(bal);
@@ -321,12 +377,12 @@ int64_t layout_chunks(int64_t nid) { return (nid + kChunk - 1) / kChunk; }
 int64_t layout_nlists(int p) { return (int64_t)p * (1 + 2 * p); }
 
 void launch_layout_plan(const int32_t* owner, const unsigned long long* req, int64_t nid, int p,
-                        LayoutWs& ws, int32_t* list_off, cudaStream_t s) {
+                        LayoutWs& ws, int32_t* list_off, int only, cudaStream_t s) {
     const int nlists = (int)layout_nlists(p);
     const int64_t nch = layout_chunks(nid);
     const size_t sm = (size_t)nlists * 4;
     if (nch > 0) {
-        k_lay_count<<<(unsigned)nch, 32, sm, s>>>(owner, req, nid, p, nlists, nch, ws.counts);
+        k_lay_count<<<(unsigned)nch, 32, sm, s>>>(owner, req, nid, p, nlists, nch, ws.counts, only);
         GMD_LAUNCH_CHECK();
     } else {
         GMD_CUDA(cudaMemsetAsync(ws.counts, 0, sizeof(int32_t) * (nlists + 1), s));
@@ -339,15 +395,40 @@ void launch_layout_plan(const int32_t* owner, const unsigned long long* req, int
 }
 
 void launch_layout_fill(const int32_t* owner, const unsigned long long* req, int64_t nid, int p,
-                        LayoutWs& ws, int32_t* node_array, int32_t* crow, cudaStream_t s) {
+                        LayoutWs& ws, int32_t* node_array, int32_t* crow, int only,
+                        cudaStream_t s) {
     const int nlists = (int)layout_nlists(p);
     const int64_t nch = layout_chunks(nid);
     const size_t sm = (size_t)nlists * 4;
     if (nch > 0) {
         k_lay_scatter<<<(unsigned)nch, 32, sm, s>>>(owner, req, nid, p, nlists, nch, ws.counts,
-                                                     node_array, crow);
+                                                     node_array, crow, only);
         GMD_LAUNCH_CHECK();
     }
+}
+
+void launch_required_rank(const int32_t* row, const int32_t* src, int64_t n, const int32_t* owner,
+                          int r, unsigned long long* req, cudaStream_t s) {
+    k_required_rank<<<div_up(n, 8), 256, 0, s>>>(row, src, n, owner, r, req);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_owned_flags(const int32_t* owner, int64_t n, int r, int32_t* flag, cudaStream_t s) {
+    k_flag_owned<<<div_up(n, 256), 256, 0, s>>>(owner, n, r, flag);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_owned_compact(const int32_t* owner, int64_t n, int r, const int32_t* pos,
+                          int32_t* nodes, cudaStream_t s) {
+    k_compact_owned<<<div_up(n, 256), 256, 0, s>>>(owner, n, r, pos, nodes);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_send_rows(int32_t t0, int32_t t1, const int32_t* node_array, const int32_t* crow,
+                      int32_t* xsend, cudaStream_t s) {
+    if (t1 <= t0) return;
+    k_send_rows<<<div_up(t1 - t0, 256), 256, 0, s>>>(t0, t1, node_array, crow, xsend);
+    GMD_LAUNCH_CHECK();
 }
 
 void launch_from_src(const int32_t* node_array, const int32_t* crow, const int32_t* from_ranges,

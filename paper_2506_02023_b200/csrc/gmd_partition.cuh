@@ -41,10 +41,22 @@ int64_t layout_chunks(int64_t nid);
 int64_t layout_nlists(int p);
 // plan: per-(list, chunk) counts, their scan, and list_off (nlists + 1
 // entries, last = total super rows).  fill: node_array + crow.
+// only >= 0 restricts the layout to partition `only` (one rank per GPU).
 void launch_layout_plan(const int32_t* owner, const unsigned long long* req, int64_t nid, int p,
-                        LayoutWs& ws, int32_t* list_off, cudaStream_t s);
+                        LayoutWs& ws, int32_t* list_off, int only, cudaStream_t s);
 void launch_layout_fill(const int32_t* owner, const unsigned long long* req, int64_t nid, int p,
-                        LayoutWs& ws, int32_t* node_array, int32_t* crow, cudaStream_t s);
+                        LayoutWs& ws, int32_t* node_array, int32_t* crow, int only,
+                        cudaStream_t s);
+
+// one rank per GPU (rank r of p): requirement masks from r's own rows,
+// the ascending list of r's atoms, and the send plan of its TO rows
+void launch_required_rank(const int32_t* row, const int32_t* src, int64_t n, const int32_t* owner,
+                          int r, unsigned long long* req, cudaStream_t s);
+void launch_owned_flags(const int32_t* owner, int64_t n, int r, int32_t* flag, cudaStream_t s);
+void launch_owned_compact(const int32_t* owner, int64_t n, int r, const int32_t* pos,
+                          int32_t* nodes, cudaStream_t s);
+void launch_send_rows(int32_t t0, int32_t t1, const int32_t* node_array, const int32_t* crow,
+                      int32_t* xsend, cudaStream_t s);
 
 // Exchange plan: for every FROM super row, the canonical super row of the
 // same id in its owner partition.  from_ranges[i] = (begin, end) super rows.

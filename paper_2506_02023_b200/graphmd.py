@@ -46,7 +46,8 @@ EXPORTS = [
     "gmd_block_rows", "gmd_block_offset", "gmd_transfer", "gmd_transfer_transpose",
     "gmd_sync_duplicates", "gmd_distribute", "gmd_aggregate",
     "gmd_corrupt_transfer_plan_for_test", "gmd_util_rng_uniform", "gmd_util_supercell",
-    "gmd_profile", "gmd_profile_read", "gmd_get_stream", "gmd_launch_count",
+    "gmd_profile", "gmd_profile_read", "gmd_get_stream", "gmd_launch_count", "gmd_comm_nccl_id",
+    "gmd_comm_init_nccl", "gmd_comm_init_local", "gmd_comm_info", "gmd_num_owned", "gmd_get_owned_ids",
 ]
 
 
@@ -115,6 +116,12 @@ def lib():
             "gmd_profile_read": (I, [V, V, I, V, V, V]),
             "gmd_get_stream": (I, [V, C.POINTER(V)]),
             "gmd_launch_count": (I, [V]),
+            "gmd_comm_nccl_id": (I, [V]),
+            "gmd_comm_init_nccl": (I, [V, I, I, V]),
+            "gmd_comm_init_local": (I, [V, I]),
+            "gmd_comm_info": (I, [V, V, V]),
+            "gmd_num_owned": (I, [V, V]),
+            "gmd_get_owned_ids": (I, [V, V]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -741,3 +748,63 @@ def launch_count() -> int:
     out = C.c_int64()
     lib().gmd_launch_count(C.byref(out))
     return out.value
+
+
+# ---------------------------------------------------------------------------
+# one rank per GPU
+# ---------------------------------------------------------------------------
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId on this process (rank 0); broadcast it to the peers."""
+    buf = (C.c_uint8 * 128)()
+    rc = lib().gmd_comm_nccl_id(buf)
+    if rc:
+        raise Error(lib().gmd_last_error(None).decode() or "ncclGetUniqueId failed", rc)
+    return bytes(buf)
+
+
+def comm_init_nccl(handle: "_Handle", rank: int, world: int, uid: bytes) -> None:
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    handle.check(lib().gmd_comm_init_nccl(handle.h, rank, world, buf))
+
+
+def local_group(world: int, device: int = 0) -> List["_Handle"]:
+    """`world` handles forming one in-process rank group (each rank must be
+    driven from its own thread: build/forward block on the peers)."""
+    hs = [_Handle(device) for _ in range(world)]
+    arr = (C.c_void_p * world)(*[h.h.value for h in hs])
+    rc = lib().gmd_comm_init_local(arr, world)
+    if rc:
+        raise Error("gmd_comm_init_local failed", rc)
+    return hs
+
+
+def owned_ids(dist: "Distributed") -> np.ndarray:
+    """Global ids of the atoms this handle computes (its rank's slab)."""
+    h = dist.handle
+    n = C.c_int64()
+    h.check(lib().gmd_num_owned(h.h, C.byref(n)))
+    out = np.zeros(n.value, np.int64)
+    h.check(lib().gmd_get_owned_ids(h.h, _p(out)))
+    return out
+
+
+def run_ranks(fns):
+    """Run one callable per rank concurrently (ctypes releases the GIL)."""
+    import threading
+    res, errs = [None] * len(fns), [None] * len(fns)
+
+    def body(i):
+        try:
+            res[i] = fns[i]()
+        except BaseException as e:  # noqa: BLE001 - reraised below
+            errs[i] = e
+
+    ts = [threading.Thread(target=body, args=(i,)) for i in range(len(fns))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return res
