@@ -57,13 +57,14 @@ def make_system(spec):
 
 
 def bytes_model(n, ne, nb, L, threebody):
-    """Algorithmic (compulsory) DRAM bytes per launch of each kernel; see
-    DESIGN.md "roofline".  n atoms, ne directed edges."""
+    """Algorithmic (compulsory) DRAM bytes per launch of each kernel (DESIGN.md
+    section 3); n atoms, ne directed edges.  Gathered neighbour rows are not
+    counted (each row is compulsory once, already in the per-node terms)."""
     return {
-        "nl_count": 68 * n + 4 * n,                 # sorted SoA positions/cells/ids, degree out
-        "nl_fill": 68 * n + 25 * ne + 8 * n,        # + src/img/vd/bond-flag per edge
-        "conv": 20 * ne + 4 * n + 64 * n + 64 * n + 64 * n,    # lsrc+vd per edge; h in/out, tanh
-        "bwd_edge": 20 * ne + 4 * n + 64 * n + 64 * n + 128 * n + 32 * n,  # m_bar, h_in, h_bar rw, grad rw
+        "nl_search": 68 * n + 8 * ne,                 # bin-sorted SoA atoms + degree; sorted keys
+        "nl_emit": 37 * ne + 40 * n,                  # keys in; src/img/vd/d/bond out; pos+cell once
+        "conv": 8 * ne + 196 * n,                     # d+src per edge; h_in row, h_out + tanh rows
+        "bwd_edge": 20 * ne + 292 * n,                # vd+src per edge; m_bar, h_in, h_bar rw, grad rw
         "bwd_node": 192 * n,
     }
 
@@ -201,10 +202,7 @@ def main():
     h = G._Handle(device)
     Lb = G.lib()
     if world > 1:
-        uid = G.nccl_unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device=f"cuda:{device}")
-        torch.distributed.broadcast(t, 0)
-        G.comm_init_nccl(h, rank, world, bytes(t.cpu().tolist()))
+        G.init_rank_comm(h, rank, world)
     pbc = np.ones(3, np.uint8)
     lat = np.ascontiguousarray(s.lattice)
     h.check(Lb.gmd_set_params(h.h, F, K, L, rc, r3, G._p(prm.blob)))

@@ -808,3 +808,29 @@ def run_ranks(fns):
         if e is not None:
             raise e
     return res
+
+
+def broadcast_bytes(payload: Optional[bytes], src: int = 0, size: int = 128) -> bytes:
+    """Broadcast `size` bytes from rank `src` over the default torch.distributed
+    group (gloo: CPU tensor, nccl: tensor on the current device)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.zeros(size, dtype=torch.uint8, device=dev)
+    if dist.get_rank() == src:
+        t.copy_(torch.tensor(list(payload), dtype=torch.uint8))
+    dist.broadcast(t, src)
+    return bytes(t.cpu().tolist())
+
+
+def init_rank_comm(handle: "_Handle", rank: int, world: int) -> None:
+    """NCCL halo transport for this process's handle (one process per GPU)."""
+    uid = nccl_unique_id() if rank == 0 else None
+    comm_init_nccl(handle, rank, world, broadcast_bytes(uid, 0))
+
+
+def exchange_plan_consistent(scnt, rcnt, rank: int, all_scnt) -> bool:
+    """The invariant the library checks at build time (engine.cpp:132-133):
+    what rank j sends to `rank` (its TO_j[rank] block) is exactly the FROM
+    span `rank` reserved for j.  all_scnt[j][k] = rows rank j sends to k."""
+    return all(j == rank or int(all_scnt[j][rank]) == int(rcnt[j]) for j in range(len(rcnt)))
