@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -910,8 +911,11 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     float* HB = h->HB.get<float>(n * kF);
     float4* GRAD = h->GRAD.get<float4>(n);
     const int grid = model_grid(n);
+    // tcgen05 backward unless GMD_NO_TC is set (A/B comparisons)
+    static const bool use_tc = std::getenv("GMD_NO_TC") == nullptr;
+    const int vgrid = use_tc ? bwd_tc_grid(n) : grid;
     double* e_part = h->e_part.get<double>(grid);
-    double* v_part = h->v_part.get<double>((size_t)L * grid * 6);
+    double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);
     const int tgrid = tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
@@ -989,7 +993,13 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     for (int l = L - 1; l >= 0; --l) {
         { PROF("bwd_node"); launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s); }
         exchange(MB);
-        { PROF("bwd_edge"); launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * grid * 6, s); }
+        {
+            PROF("bwd_edge");
+            if (use_tc)
+                launch_bwd_edge_tc(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+            else
+                launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+        }
         if (tb && l == L - 1) {
             float* QB = h->QB.get<float>(n * kF);
             float4* VIN = h->VIN.get<float4>(h->nb);
@@ -1016,7 +1026,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         launch_forces_out(n, a.nodes, GRAD, fd, ff, s);
     }
     launch_reduce_partials(e_part, grid, 1, red, s);
-    launch_reduce_partials(v_part, L * grid, 6, red + 1, s);
+    launch_reduce_partials(v_part, L * vgrid, 6, red + 1, s);
     if (tb)
         launch_reduce_partials(v3_part, tgrid, 9, red + 7, s);
     else

@@ -15,6 +15,7 @@
 //    (bonds e=(w->s) and their reverses e'=(s->w)): every line edge (e, e')
 //    with dst(e) = src(e') is a pair of slots of one center.
 #include "gmd_model.cuh"
+#include "gmd_tc.cuh"
 
 namespace gmd {
 
@@ -508,6 +509,233 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
 }
 
 // ---------------------------------------------------------------------------
+// Backward edge pass on the 5th-gen tensor cores (tcgen05 + TMEM).
+//
+// Per 128-edge tile (one edge per thread, thread t <-> TMEM lane t):
+//   phi[e][k] (SFU) -> split into tf32 hi/lo, staged K-major in shared memory;
+//   one thread issues D = phi_hi.Pc_hi + phi_lo.Pc_hi + phi_hi.Pc_lo
+//   (M=128, N=32, K=8, kind::tf32) with Pc = [P ; kP] (32 x 8), so TMEM row e
+//   holds A_f = sum_k P_fk phi_k and B_f = sum_k k P_fk phi_k for all 16 f;
+//   the epilogue (LDTM) forms s_f = fc A_f, ds_f = ca A_f + cb B_f and the
+//   per-edge products of k_bwd_edge; per-node sums run in edge order with a
+//   carry across tile boundaries, so results do not depend on the tiling.
+// CTA c owns a contiguous block of (local) nodes, hence a contiguous edge range.
+// ---------------------------------------------------------------------------
+constexpr int kTM = 128;  // edges per tile = threads = MMA M
+constexpr int kNV = 19;   // per-edge values reduced per node: 16 h_bar, 3 grad
+
+struct BwdTcSmem {
+    float a_hi[kTM * kK], a_lo[kTM * kK];   // phi, K-major interleaved (gmd_tc.cuh)
+    float b_hi[32 * kK], b_lo[32 * kK];     // [P ; kP]
+    float vals[kNV][kTM + 1];
+    int rs[kTM + 1];                        // node starts relative to the tile
+    float carry[kNV];
+    uint64_t mbar;
+    uint32_t tbase;
+};
+
+__device__ __forceinline__ int64_t node_gid(const ConvArgs& a, int64_t k) {
+    return a.nodes ? (int64_t)a.nodes[k] : k;
+}
+
+__global__ void __launch_bounds__(kTM) k_bwd_edge_tc(ConvArgs a, int64_t npc,
+                                                     const float* __restrict__ MB,
+                                                     const float* __restrict__ Hl,
+                                                     float* __restrict__ HB,
+                                                     float4* __restrict__ GRAD, double* vir_part) {
+    extern __shared__ __align__(1024) unsigned char tc_smem[];
+    BwdTcSmem& S = *reinterpret_cast<BwdTcSmem*>(tc_smem);
+    const int tid = threadIdx.x;
+    const int64_t k_lo = (int64_t)blockIdx.x * npc;
+    const int64_t k_hi = min(a.n, k_lo + npc);
+    const float isg = c_m.inv_sigma, mus = c_m.mu_step;
+
+    // B operand [P ; kP] split to tf32 hi/lo (constant for the whole kernel)
+    for (int i = tid; i < 32 * kK; i += kTM) {
+        const int nrow = i / kK, k = i % kK;
+        const float x = nrow < kF ? c_m.P[nrow * kK + k] : c_m.Pk[(nrow - kF) * kK + k];
+        float h, l;
+        tc::split_tf32(x, h, l);
+        S.b_hi[tc::kmajor_off(nrow, k)] = h;
+        S.b_lo[tc::kmajor_off(nrow, k)] = l;
+    }
+    if (tid == 0) {
+        tc::mbar_init(&S.mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (tid < 32) tc::tmem_alloc(&S.tbase, 32);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = S.tbase;
+    const uint32_t idesc = tc::idesc_tf32(kTM, 32);
+    const uint32_t trow = tmem + ((uint32_t)(32 * (tid >> 5)) << 16);
+
+    double vir[6] = {0, 0, 0, 0, 0, 0};
+    int64_t kcur = k_lo;
+    int64_t t0 = k_lo < k_hi ? (int64_t)__ldg(a.row + node_gid(a, k_lo)) : 0;
+    bool have_carry = false;
+    uint32_t phase = 0;
+    while (kcur < k_hi) {
+        const int nk = (int)min((int64_t)kTM, k_hi - kcur);
+        for (int j = tid; j <= nk; j += kTM) {
+            const int64_t kk = kcur + (j < nk ? j : nk - 1);
+            const int64_t vv = node_gid(a, kk);
+            S.rs[j] = (j < nk ? __ldg(a.row + vv) : __ldg(a.row + vv + 1)) - (int)t0;
+        }
+        __syncthreads();
+        const int te = min(kTM, S.rs[nk]);  // edges in this tile
+        if (te <= 0) {                      // nk empty nodes
+            kcur += nk;
+            __syncthreads();
+            continue;
+        }
+        // ---- per-edge operands: gathers first, then phi -> smem
+        const bool valid = tid < te;
+        const int64_t e = t0 + tid;
+        int jn = 0;  // tile-local node of this edge
+        {
+            int lo = 0, hi = nk - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (S.rs[mid] <= tid) lo = mid; else hi = mid - 1;
+            }
+            jn = lo;
+        }
+        float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
+        float4 m4[4], h4[4];
+        if (valid) {
+            q = __ldg(a.vd + e);
+            const int w = __ldg(a.lsrc + e);
+            ldg256(MB + (size_t)w * kF, m4[0], m4[1]);
+            ldg256(MB + (size_t)w * kF + 8, m4[2], m4[3]);
+            ldg256(Hl + (size_t)w * kF, h4[0], h4[1]);
+            ldg256(Hl + (size_t)w * kF + 8, h4[2], h4[3]);
+        }
+        {
+            float phi[kK];
+            phi_fast(q.w, phi);
+#pragma unroll
+            for (int k = 0; k < kK; ++k) {
+                float hv = 0.f, lv = 0.f;
+                if (valid) tc::split_tf32(phi[k], hv, lv);
+                S.a_hi[tc::kmajor_off(tid, k)] = hv;
+                S.a_lo[tc::kmajor_off(tid, k)] = lv;
+            }
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (tid == 0) {
+            tc::mma_tf32(tmem, tc::sdesc(S.a_hi), tc::sdesc(S.b_hi), idesc, false);
+            tc::mma_tf32(tmem, tc::sdesc(S.a_lo), tc::sdesc(S.b_hi), idesc, true);
+            tc::mma_tf32(tmem, tc::sdesc(S.a_hi), tc::sdesc(S.b_lo), idesc, true);
+            tc::commit(&S.mbar);
+        }
+        tc::mbar_wait(&S.mbar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        float AB[32];
+        tc::tmem_ld32(trow, AB);
+        // ---- epilogue for this thread's edge
+        if (valid) {
+            const int64_t vn = node_gid(a, kcur + jn);
+            const int64_t r = a.crow ? a.crow[vn] : vn;
+            float4 u4[4], hu4[4];
+            ldg256(MB + r * kF, u4[0], u4[1]);
+            ldg256(MB + r * kF + 8, u4[2], u4[3]);
+            ldg256(Hl + r * kF, hu4[0], hu4[1]);
+            ldg256(Hl + r * kF + 8, hu4[2], hu4[3]);
+            float fc, dfc;
+            fc_dfc_fast(q.w, fc, dfc);
+            const float x0 = q.w * isg, step = mus * isg;
+            const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
+            float dself = 0.f, drev = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float mw[4] = {m4[c].x, m4[c].y, m4[c].z, m4[c].w};
+                const float hw[4] = {h4[c].x, h4[c].y, h4[c].z, h4[c].w};
+                const float mu[4] = {u4[c].x, u4[c].y, u4[c].z, u4[c].w};
+                const float hu[4] = {hu4[c].x, hu4[c].y, hu4[c].z, hu4[c].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int f = 4 * c + i;
+                    const float A = AB[f], B = AB[kF + f];
+                    const float ds = fmaf(ca, A, cb * B);
+                    S.vals[f][tid] = mw[i] * (fc * A);
+                    dself = fmaf(mu[i] * hw[i], ds, dself);
+                    drev = fmaf(mw[i] * hu[i], ds, drev);
+                }
+            }
+            const float invd = 1.0f / q.w;
+            const float coef = (dself + drev) * invd;
+            S.vals[16][tid] = -q.x * coef;
+            S.vals[17][tid] = -q.y * coef;
+            S.vals[18][tid] = -q.z * coef;
+            const double cself = (double)(dself * invd);
+            vir[0] += cself * q.x * q.x;
+            vir[1] += cself * q.y * q.y;
+            vir[2] += cself * q.z * q.z;
+            vir[3] += cself * q.x * q.y;
+            vir[4] += cself * q.x * q.z;
+            vir[5] += cself * q.y * q.z;
+        }
+        tc::fence_before();
+        __syncthreads();
+        // ---- per-node sums in edge order (carry across tiles), write-out
+        int ndone = 0;  // nodes completed in this tile (a prefix, rs is monotone)
+        {
+            int lo = 0, hi = nk;  // first j with rs[j+1] > te
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (S.rs[mid + 1] <= te) lo = mid + 1; else hi = mid;
+            }
+            ndone = lo;
+        }
+        const int nover = min(nk, ndone + 1);  // nodes with edges in [0, te)
+        for (int pidx = tid; pidx < nover * kNV; pidx += kTM) {
+            const int j = pidx / kNV, c = pidx % kNV;
+            const int lo = max(S.rs[j], 0), hi = min(S.rs[j + 1], te);
+            float sum = (j == 0 && have_carry) ? S.carry[c] : 0.f;
+            for (int ee = lo; ee < hi; ++ee) sum += S.vals[c][ee];
+            if (j < ndone) {
+                const int64_t kk = kcur + j;
+                if (c < kF)
+                    HB[kk * kF + c] += sum;
+                else
+                    reinterpret_cast<float*>(GRAD + kk)[c - kF] += sum;
+            } else {
+                S.carry[c] = sum;
+            }
+        }
+        __syncthreads();
+        have_carry = ndone < nk && S.rs[ndone] < te;
+        t0 += te;
+        kcur += ndone;
+    }
+    // fp64 virial: thread -> warp -> CTA in fixed order -> vir_part[blockIdx.x]
+    __shared__ double wv[kTM / 32][6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        double vsum = vir[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+        if ((tid & 31) == 0) wv[tid >> 5][c] = vsum;
+    }
+    __syncthreads();
+    if (tid < 6) {
+        double acc6 = 0.0;
+        for (int w = 0; w < kTM / 32; ++w) acc6 += wv[w][tid];
+        vir_part[(size_t)blockIdx.x * 6 + tid] = acc6;
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid < 32) tc::tmem_free(tmem, 32);
+}
+
+// ---------------------------------------------------------------------------
 // three-body stage (potential.cpp:664-741 forward, :850-961 backward)
 // ---------------------------------------------------------------------------
 constexpr int kTbWarps = 4;
@@ -859,6 +1087,27 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
                      double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
     k_bwd_edge<<<model_grid(a.n), kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+    GMD_LAUNCH_CHECK();
+}
+
+int bwd_tc_grid(int64_t n) {
+    int64_t g = 148 * 6;
+    if (g > (n + 15) / 16) g = (n + 15) / 16;
+    return (int)(g > 0 ? g : 1);
+}
+
+void launch_bwd_edge_tc(const ConvArgs& a, const float* MB, const float* Hl, float* HB,
+                        float4* GRAD, double* vir_part, cudaStream_t s) {
+    if (a.n == 0) return;
+    const int grid = bwd_tc_grid(a.n);
+    const int64_t npc = (a.n + grid - 1) / grid;
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(BwdTcSmem)));
+        attr = true;
+    }
+    k_bwd_edge_tc<<<grid, kTM, sizeof(BwdTcSmem), s>>>(a, npc, MB, Hl, HB, GRAD, vir_part);
     GMD_LAUNCH_CHECK();
 }
 

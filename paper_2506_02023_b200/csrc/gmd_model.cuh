@@ -62,6 +62,12 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
                      double* vir_part, cudaStream_t s);
 
+// the same pass with the radial contractions on tcgen05 (TMEM accumulator);
+// grid = bwd_tc_grid(n) CTAs, vir_part holds grid x 6 doubles
+int bwd_tc_grid(int64_t n);
+void launch_bwd_edge_tc(const ConvArgs& a, const float* MB, const float* Hl, float* HB,
+                        float4* GRAD, double* vir_part, cudaStream_t s);
+
 // three-body stage (global bond CSR by dst; slot = in-bond position)
 struct BondArgs {
     int64_t n;
