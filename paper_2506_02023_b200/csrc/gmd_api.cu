@@ -911,8 +911,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     float* HB = h->HB.get<float>(n * kF);
     float4* GRAD = h->GRAD.get<float4>(n);
     const int grid = model_grid(n);
-    // tcgen05 backward unless GMD_NO_TC is set (A/B comparisons)
-    static const bool use_tc = std::getenv("GMD_NO_TC") == nullptr;
+    // backward edge pass: FFMA kernel, or the tcgen05 kernel with GMD_BWD_TC=1
+    const char* tc_env = std::getenv("GMD_BWD_TC");
+    const bool use_tc = tc_env && tc_env[0] == '1';
     const int vgrid = use_tc ? bwd_tc_grid(n) : grid;
     double* e_part = h->e_part.get<double>(grid);
     double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);

@@ -511,25 +511,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
 // ---------------------------------------------------------------------------
 // Backward edge pass on the 5th-gen tensor cores (tcgen05 + TMEM).
 //
-// Per 128-edge tile (one edge per thread, thread t <-> TMEM lane t):
-//   phi[e][k] (SFU) -> split into tf32 hi/lo, staged K-major in shared memory;
-//   one thread issues D = phi_hi.Pc_hi + phi_lo.Pc_hi + phi_hi.Pc_lo
-//   (M=128, N=32, K=8, kind::tf32) with Pc = [P ; kP] (32 x 8), so TMEM row e
-//   holds A_f = sum_k P_fk phi_k and B_f = sum_k k P_fk phi_k for all 16 f;
-//   the epilogue (LDTM) forms s_f = fc A_f, ds_f = ca A_f + cb B_f and the
-//   per-edge products of k_bwd_edge; per-node sums run in edge order with a
-//   carry across tile boundaries, so results do not depend on the tiling.
-// CTA c owns a contiguous block of (local) nodes, hence a contiguous edge range.
+// Rows of a 128-row tile are 8 chunks of 16 edge slots; a chunk holds up to 16
+// consecutive in-edges of ONE node (a node of degree d uses ceil(d/16)
+// chunks), so every chunk reduces with a fixed half-warp tree and a node's
+// total is its chunk sums in chunk order -- independent of how nodes are
+// spread over CTAs/tiles (partition- and rank-invariant results).
+// Per tile: phi[slot][k] (SFU) -> tf32 hi/lo, K-major in shared memory; one
+// thread issues D = phi_hi.Pc_hi + phi_lo.Pc_hi + phi_hi.Pc_lo (M=128, N=32,
+// K=8, kind::tf32, Pc = [P ; kP]) into TMEM; the epilogue reads its row
+// (LDTM): A_f = sum_k P_fk phi_k, B_f = sum_k k P_fk phi_k, and forms
+// s_f = fc A_f, ds_f = ca A_f + cb B_f and the products of k_bwd_edge.
 // ---------------------------------------------------------------------------
-constexpr int kTM = 128;  // edges per tile = threads = MMA M
-constexpr int kNV = 19;   // per-edge values reduced per node: 16 h_bar, 3 grad
+constexpr int kTM = 128;  // rows per tile = threads = MMA M
+constexpr int kCH = 16;   // edge slots per chunk
+constexpr int kNCH = kTM / kCH;
+constexpr int kNV = 19;   // per-node values: 16 h_bar, 3 grad
+constexpr int kBwdTcCtas = 5;  // resident CTAs per SM (80 registers)
 
 struct BwdTcSmem {
     float a_hi[kTM * kK], a_lo[kTM * kK];   // phi, K-major interleaved (gmd_tc.cuh)
     float b_hi[32 * kK], b_lo[32 * kK];     // [P ; kP]
-    float vals[kNV][kTM + 1];
-    int rs[kTM + 1];                        // node starts relative to the tile
-    float carry[kNV];
+    float csum[kNCH][kNV + 1];              // chunk sums of this tile
+    int cnode[kNCH];                        // tile-local node index of each chunk (-1: none)
+    int clast[kNCH];                        // chunk is its node's last chunk
+    float run[kNCH + 1][kNV];               // running node sums (carry in slot 0)
+    int chunk_pre[kTM + 1];                 // chunk prefix over the tile's candidate nodes
+    int node_e0[kTM + 1];                   // first edge of each candidate node
+    alignas(16) float own[kNCH][2 * kF];    // MB, H rows of each chunk's node
     uint64_t mbar;
     uint32_t tbase;
 };
@@ -538,19 +546,20 @@ __device__ __forceinline__ int64_t node_gid(const ConvArgs& a, int64_t k) {
     return a.nodes ? (int64_t)a.nodes[k] : k;
 }
 
-__global__ void __launch_bounds__(kTM) k_bwd_edge_tc(ConvArgs a, int64_t npc,
-                                                     const float* __restrict__ MB,
-                                                     const float* __restrict__ Hl,
-                                                     float* __restrict__ HB,
-                                                     float4* __restrict__ GRAD, double* vir_part) {
+__global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int64_t npc,
+                                                        const float* __restrict__ MB,
+                                                        const float* __restrict__ Hl,
+                                                        float* __restrict__ HB,
+                                                        float4* __restrict__ GRAD,
+                                                        double* vir_part) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     BwdTcSmem& S = *reinterpret_cast<BwdTcSmem*>(tc_smem);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ch = tid / kCH, gl = tid % kCH;  // chunk of this thread, lane in chunk
     const int64_t k_lo = (int64_t)blockIdx.x * npc;
     const int64_t k_hi = min(a.n, k_lo + npc);
     const float isg = c_m.inv_sigma, mus = c_m.mu_step;
 
-    // B operand [P ; kP] split to tf32 hi/lo (constant for the whole kernel)
     for (int i = tid; i < 32 * kK; i += kTM) {
         const int nrow = i / kK, k = i % kK;
         const float x = nrow < kF ? c_m.P[nrow * kK + k] : c_m.Pk[(nrow - kF) * kK + k];
@@ -572,35 +581,71 @@ __global__ void __launch_bounds__(kTM) k_bwd_edge_tc(ConvArgs a, int64_t npc,
     const uint32_t trow = tmem + ((uint32_t)(32 * (tid >> 5)) << 16);
 
     double vir[6] = {0, 0, 0, 0, 0, 0};
-    int64_t kcur = k_lo;
-    int64_t t0 = k_lo < k_hi ? (int64_t)__ldg(a.row + node_gid(a, k_lo)) : 0;
-    bool have_carry = false;
+    int64_t kcur = k_lo;  // first node not yet finished
+    int cskip = 0;        // chunks of node kcur already processed
     uint32_t phase = 0;
     while (kcur < k_hi) {
+        // candidate nodes kcur .. kcur+nk-1: first edges and chunk prefix
         const int nk = (int)min((int64_t)kTM, k_hi - kcur);
         for (int j = tid; j <= nk; j += kTM) {
             const int64_t kk = kcur + (j < nk ? j : nk - 1);
             const int64_t vv = node_gid(a, kk);
-            S.rs[j] = (j < nk ? __ldg(a.row + vv) : __ldg(a.row + vv + 1)) - (int)t0;
+            S.node_e0[j] = j < nk ? __ldg(a.row + vv) : __ldg(a.row + vv + 1);
         }
         __syncthreads();
-        const int te = min(kTM, S.rs[nk]);  // edges in this tile
-        if (te <= 0) {                      // nk empty nodes
+        if (tid < 32) {  // chunk prefix (warp scan over nk <= 128 nodes)
+            int carry = 0;
+            for (int base = 0; base < nk; base += 32) {
+                const int j = base + lane;
+                int c = j < nk ? (S.node_e0[j + 1] - S.node_e0[j] + kCH - 1) / kCH : 0;
+                if (j == 0) c -= cskip;
+                int incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                if (j < nk) S.chunk_pre[j + 1] = carry + incl;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (lane == 0) S.chunk_pre[0] = 0;
+        }
+        __syncthreads();
+        const int total_chunks = S.chunk_pre[nk];
+        if (total_chunks == 0) {  // only empty nodes
             kcur += nk;
+            cskip = 0;
             __syncthreads();
             continue;
         }
-        // ---- per-edge operands: gathers first, then phi -> smem
-        const bool valid = tid < te;
-        const int64_t e = t0 + tid;
-        int jn = 0;  // tile-local node of this edge
-        {
-            int lo = 0, hi = nk - 1;
+        const int nch = min(kNCH, total_chunks);
+        // ---- this thread's slot: chunk ch -> node jn, edge
+        int jn = -1, cin = 0;
+        bool valid = false;
+        int64_t e = 0;
+        if (ch < nch) {
+            int lo = 0, hi = nk - 1;  // last j with chunk_pre[j] <= ch
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (S.rs[mid] <= tid) lo = mid; else hi = mid - 1;
+                if (S.chunk_pre[mid] <= ch) lo = mid; else hi = mid - 1;
             }
             jn = lo;
+            cin = ch - S.chunk_pre[jn] + (jn == 0 ? cskip : 0);  // chunk index inside the node
+            const int64_t e0 = S.node_e0[jn] + (int64_t)cin * kCH + gl;
+            valid = e0 < S.node_e0[jn + 1];
+            e = e0;
+        }
+        if (gl == 0) {
+            S.cnode[ch] = ch < nch ? jn : -1;
+            const int nchunks_node = (S.node_e0[jn >= 0 ? jn + 1 : 0] - S.node_e0[jn >= 0 ? jn : 0] + kCH - 1) / kCH;
+            S.clast[ch] = ch < nch && cin == nchunks_node - 1;
+        }
+        if (jn >= 0 && gl < 8) {  // own rows of the chunk's node -> S.own[ch]
+            const int64_t vn = node_gid(a, kcur + jn);
+            const int64_t r = a.crow ? a.crow[vn] : vn;
+            const float* src = (gl < 4 ? MB : Hl) + r * kF + (gl & 3) * 4;
+            *reinterpret_cast<float4*>(&S.own[ch][(gl >> 2) * kF + (gl & 3) * 4]) =
+                __ldg(reinterpret_cast<const float4*>(src));
         }
         float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
         float4 m4[4], h4[4];
@@ -638,41 +683,41 @@ __global__ void __launch_bounds__(kTM) k_bwd_edge_tc(ConvArgs a, int64_t npc,
         tc::fence_after();
         float AB[32];
         tc::tmem_ld32(trow, AB);
-        // ---- epilogue for this thread's edge
+        float acc[kF];
+        float gx = 0.f, gy = 0.f, gz = 0.f;
+#pragma unroll
+        for (int f = 0; f < kF; ++f) acc[f] = 0.f;
         if (valid) {
-            const int64_t vn = node_gid(a, kcur + jn);
-            const int64_t r = a.crow ? a.crow[vn] : vn;
-            float4 u4[4], hu4[4];
-            ldg256(MB + r * kF, u4[0], u4[1]);
-            ldg256(MB + r * kF + 8, u4[2], u4[3]);
-            ldg256(Hl + r * kF, hu4[0], hu4[1]);
-            ldg256(Hl + r * kF + 8, hu4[2], hu4[3]);
             float fc, dfc;
             fc_dfc_fast(q.w, fc, dfc);
             const float x0 = q.w * isg, step = mus * isg;
             const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
             float dself = 0.f, drev = 0.f;
+            const float* ownm = S.own[ch];
+            const float* ownh = S.own[ch] + kF;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float mw[4] = {m4[c].x, m4[c].y, m4[c].z, m4[c].w};
                 const float hw[4] = {h4[c].x, h4[c].y, h4[c].z, h4[c].w};
-                const float mu[4] = {u4[c].x, u4[c].y, u4[c].z, u4[c].w};
-                const float hu[4] = {hu4[c].x, hu4[c].y, hu4[c].z, hu4[c].w};
+                const float4 uu = *reinterpret_cast<const float4*>(ownm + 4 * c);
+                const float4 hh = *reinterpret_cast<const float4*>(ownh + 4 * c);
+                const float mu[4] = {uu.x, uu.y, uu.z, uu.w};
+                const float hu[4] = {hh.x, hh.y, hh.z, hh.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int f = 4 * c + i;
                     const float A = AB[f], B = AB[kF + f];
                     const float ds = fmaf(ca, A, cb * B);
-                    S.vals[f][tid] = mw[i] * (fc * A);
+                    acc[f] = mw[i] * (fc * A);
                     dself = fmaf(mu[i] * hw[i], ds, dself);
                     drev = fmaf(mw[i] * hu[i], ds, drev);
                 }
             }
             const float invd = 1.0f / q.w;
             const float coef = (dself + drev) * invd;
-            S.vals[16][tid] = -q.x * coef;
-            S.vals[17][tid] = -q.y * coef;
-            S.vals[18][tid] = -q.z * coef;
+            gx = -q.x * coef;
+            gy = -q.y * coef;
+            gz = -q.z * coef;
             const double cself = (double)(dself * invd);
             vir[0] += cself * q.x * q.x;
             vir[1] += cself * q.y * q.y;
@@ -681,38 +726,57 @@ __global__ void __launch_bounds__(kTM) k_bwd_edge_tc(ConvArgs a, int64_t npc,
             vir[4] += cself * q.x * q.z;
             vir[5] += cself * q.y * q.z;
         }
+        // ---- chunk sums: fixed half-warp trees
+        const float hsum = transpose_reduce16_g16(acc, gl);  // feature gl
+        gx = group_sum16(gx);
+        gy = group_sum16(gy);
+        gz = group_sum16(gz);
+        S.csum[ch][gl] = hsum;
+        if (gl == 0) {
+            S.csum[ch][16] = gx;
+            S.csum[ch][17] = gy;
+            S.csum[ch][18] = gz;
+        }
         tc::fence_before();
         __syncthreads();
-        // ---- per-node sums in edge order (carry across tiles), write-out
-        int ndone = 0;  // nodes completed in this tile (a prefix, rs is monotone)
-        {
-            int lo = 0, hi = nk;  // first j with rs[j+1] > te
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (S.rs[mid + 1] <= te) lo = mid + 1; else hi = mid;
+        // ---- node totals in chunk order, carried across tiles in run[]
+        if (tid < kNV) {
+            const int c = tid;
+            float runv = S.run[0][c];  // carry of node kcur (valid when cskip > 0)
+            int prev = -1;
+            for (int k2 = 0; k2 < nch; ++k2) {
+                const int j = S.cnode[k2];
+                if (j != prev) {
+                    if (!(j == 0 && cskip > 0)) runv = 0.f;
+                    prev = j;
+                }
+                runv += S.csum[k2][c];
+                if (S.clast[k2]) {
+                    const int64_t kk = kcur + j;
+                    if (c < kF)
+                        HB[kk * kF + c] += runv;
+                    else
+                        reinterpret_cast<float*>(GRAD + kk)[c - kF] += runv;
+                }
             }
-            ndone = lo;
+            S.run[0][c] = runv;  // carry for a node continuing into the next tile
         }
-        const int nover = min(nk, ndone + 1);  // nodes with edges in [0, te)
-        for (int pidx = tid; pidx < nover * kNV; pidx += kTM) {
-            const int j = pidx / kNV, c = pidx % kNV;
-            const int lo = max(S.rs[j], 0), hi = min(S.rs[j + 1], te);
-            float sum = (j == 0 && have_carry) ? S.carry[c] : 0.f;
-            for (int ee = lo; ee < hi; ++ee) sum += S.vals[c][ee];
-            if (j < ndone) {
-                const int64_t kk = kcur + j;
-                if (c < kF)
-                    HB[kk * kF + c] += sum;
-                else
-                    reinterpret_cast<float*>(GRAD + kk)[c - kF] += sum;
+        __syncthreads();
+        // advance: nodes whose last chunk was in this tile are done
+        {
+            const int jl = S.cnode[nch - 1];
+            const bool last_done = S.clast[nch - 1];
+            int chunks_of_jl_here = 0;
+            for (int k2 = 0; k2 < nch; ++k2) chunks_of_jl_here += S.cnode[k2] == jl;
+            if (last_done) {
+                kcur += jl + 1;
+                cskip = 0;
             } else {
-                S.carry[c] = sum;
+                cskip = (jl == 0 ? cskip : 0) + chunks_of_jl_here;
+                kcur += jl;
             }
         }
         __syncthreads();
-        have_carry = ndone < nk && S.rs[ndone] < te;
-        t0 += te;
-        kcur += ndone;
     }
     // fp64 virial: thread -> warp -> CTA in fixed order -> vir_part[blockIdx.x]
     __shared__ double wv[kTM / 32][6];
@@ -721,7 +785,7 @@ __global__ void __launch_bounds__(kTM) k_bwd_edge_tc(ConvArgs a, int64_t npc,
         double vsum = vir[c];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
-        if ((tid & 31) == 0) wv[tid >> 5][c] = vsum;
+        if (lane == 0) wv[tid >> 5][c] = vsum;
     }
     __syncthreads();
     if (tid < 6) {
@@ -1091,7 +1155,7 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
 }
 
 int bwd_tc_grid(int64_t n) {
-    int64_t g = 148 * 6;
+    int64_t g = 148 * kBwdTcCtas;  // one wave
     if (g > (n + 15) / 16) g = (n + 15) / 16;
     return (int)(g > 0 ? g : 1);
 }

@@ -7,6 +7,8 @@ Tolerances (fp32 compute against the fp64 oracle, stated per quantity):
   forces           max |dF|        <= 2e-4 eV/A   (and <= 2e-5 relative to max |F|)
   stress           max |dS|        <= 2e-6 eV/A^3
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -16,6 +18,13 @@ from tests import systems as S
 pytestmark = pytest.mark.gpu
 
 TOL_EA, TOL_E, TOL_F, TOL_FREL, TOL_S = 2e-5, 2e-6, 2e-4, 2e-5, 2e-6
+
+
+@pytest.fixture(params=["ffma", "tcgen05"], autouse=True)
+def bwd_kernel(request, monkeypatch):
+    """Every test runs with both backward edge kernels (GMD_BWD_TC, read per call)."""
+    monkeypatch.setenv("GMD_BWD_TC", "1" if request.param == "tcgen05" else "0")
+    return request.param
 
 
 def run_gpu(s, params, p=1, r3=None, allow_narrow=True):
@@ -123,3 +132,15 @@ def test_cutoff_mismatch_error():
         G.forward_distributed(d, params_for(1, 2, 5.0))
     with pytest.raises(G.Error, match="require a line graph"):
         G.forward_distributed(d, params_for(1, 2, 4.0, 3.0))
+
+
+def test_tc_matches_ffma_backward(monkeypatch):
+    s = S.quartz((4, 4, 4))
+    prm = params_for(11, 3, 5.0)
+    monkeypatch.setenv("GMD_BWD_TC", "0")
+    a = run_gpu(s, prm, p=2)
+    monkeypatch.setenv("GMD_BWD_TC", "1")
+    b = run_gpu(s, prm, p=2)
+    assert a.energy == b.energy  # forward is shared
+    np.testing.assert_allclose(b.forces, a.forces, rtol=0, atol=2e-5 * np.abs(a.forces).max())
+    np.testing.assert_allclose(b.stress, a.stress, rtol=0, atol=1e-7)

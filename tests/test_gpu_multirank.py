@@ -25,9 +25,11 @@ def run_group(s, prm, W):
     return G.run_ranks([rank(r) for r in range(W)])
 
 
+@pytest.mark.parametrize("bwd_tc", ["0", "1"])
 @pytest.mark.parametrize("W", [2, 3, 4])
 @pytest.mark.parametrize("which", ["quartz", "gas"])
-def test_rank_group_equals_single_handle(W, which):
+def test_rank_group_equals_single_handle(W, which, bwd_tc, monkeypatch):
+    monkeypatch.setenv("GMD_BWD_TC", bwd_tc)
     s = S.quartz((4, 4, 4)) if which == "quartz" else S.random_gas(600, 5)
     prm = G.ToyPotentialParams.init(11, 16, 8, 3, 4.0)
     ref_d = G.Distributed.create_distributed(s, 4.0, None, W, 1, True)
