@@ -69,6 +69,21 @@ def bytes_model(n, ne, nb, L, threebody):
     }
 
 
+def ncu_traffic(config, kname):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kname`
+    from the committed `ncu --set full` capture of this config (profiles/)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{config}.json")), reverse=True):
+        try:
+            with open(path) as f:
+                m = json.load(f).get("k_" + kname)
+            if m and m.get("dram_bytes"):
+                return m["dram_bytes"], os.path.relpath(path, ROOT)
+        except (OSError, ValueError):
+            pass
+    return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
@@ -312,8 +327,9 @@ def main():
         per_launch_ms = kms / max(kl, 1)
         ab = bm.get(kname)
         ach = ab / (per_launch_ms * 1e-3) / 1e9 if ab else None
+        traffic, tsrc = ncu_traffic(args.config, kname)
         roof = {"kernel": kname, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": (ach / peak) if ach else None, "traffic": None,
+                "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": tsrc,
                 "algorithmic_bytes_per_launch": ab, "ms_per_launch": per_launch_ms,
                 "share_of_step": kms / ms, "peak_source": peak_kind}
 

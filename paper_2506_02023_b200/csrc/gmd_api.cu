@@ -263,6 +263,9 @@ struct gmd_handle {
     int F = 16, K = 8, L = 0;
     double p_r_atom = 0, p_r3 = 0;
     std::vector<DBuf> H;
+    bool ctab_ok = false;  // chunk records of the tcgen05 backward (per build)
+    int ctab_grid = 0;
+    DBuf ccnt, cstart, ctab, ccta;
     DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v3_part, red, per_atom,
         forces, conv_tmp, exp_tmp;
     cudaEvent_t ev[8] = {};
@@ -456,6 +459,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     cudaStream_t s = h->stream;
     h->built = false;
     h->hc_ready = h->hcb_ready = false;
+    h->ctab_ok = false;
     h->atoms.ready = h->bonds.ready = false;
     h->corrupted = false;
     if (!pos || !Z || !lat) raise(kArg, "null input pointer");
@@ -491,6 +495,12 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         double width = perp_width(h->lat, k);
         double fb = std::floor(width / rc);
         if (fb > 4.0e6) raise(kConfig, "cell is too large relative to the cutoff for binning");
+        // neighborlist.cpp:121-126 bins floor(width / rc) and searches
+        // floor(rc / bw) + 1 cells each way, i.e. 5 cells per axis when the
+        // width is a multiple of rc.  Edge order does not depend on the bins
+        // (rows are key-sorted), so take one bin fewer there: bw > rc by a
+        // wide margin and the 3-cell stencil is exact.
+        if (fb >= 2.0 && width / fb < rc * (1.0 + 1e-6)) fb -= 1.0;
         g.bins[k] = std::max(1, (int)fb);
         double bw = width / g.bins[k];
         g.sten[k] = (int)std::floor(rc / bw) + 1;
@@ -878,6 +888,24 @@ int elem_size(int dtype) {
     raise(kArg, "dtype must be GMD_F32 or GMD_F64");
 }
 
+// chunk records for the tcgen05 backward edge pass (once per graph build)
+void ensure_chunk_table(gmd_handle* h, const ConvArgs& a) {
+    if (h->ctab_ok) return;
+    cudaStream_t s = h->stream;
+    const int grid = bwd_tc_grid(a.n);
+    int32_t* cnt = h->ccnt.get<int32_t>(a.n + 1);
+    int32_t* cst = h->cstart.get<int32_t>(a.n + 1);
+    launch_chunk_count(a, cnt, s);
+    scan_i32(h, cnt, cst, a.n + 1);
+    int32_t T = 0;
+    GMD_CUDA(cudaMemcpyAsync(&T, cst + a.n, 4, cudaMemcpyDeviceToHost, s));
+    GMD_CUDA(cudaStreamSynchronize(s));
+    int4* tab = h->ctab.get<int4>(std::max<int64_t>(1, T));
+    launch_chunk_fill(a, cst, tab, grid, h->ccta.get<int32_t>(grid + 1), s);
+    h->ctab_grid = grid;
+    h->ctab_ok = true;
+}
+
 // ---------------------------------------------------------------------------
 // forward_distributed (potential.cpp:563-985)
 // ---------------------------------------------------------------------------
@@ -930,6 +958,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(),
                h->vd.as<float4>(),
                h->ed.as<float>()};
+    if (use_tc) ensure_chunk_table(h, a);
     BondArgs ba{n,
                 a.crow,
                 h->brow.as<int32_t>(),
@@ -997,7 +1026,8 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         {
             PROF("bwd_edge");
             if (use_tc)
-                launch_bwd_edge_tc(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+                launch_bwd_edge_tc(a, h->ctab.as<int4>(), h->ccta.as<int32_t>(), vgrid, MB, H[l], HB,
+                                   GRAD, v_part + (size_t)l * vgrid * 6, s);
             else
                 launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
         }
@@ -1026,6 +1056,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         PROF("forces_out");
         launch_forces_out(n, a.nodes, GRAD, fd, ff, s);
     }
+    PROF("reduce");
     launch_reduce_partials(e_part, grid, 1, red, s);
     launch_reduce_partials(v_part, L * vgrid, 6, red + 1, s);
     if (tb)

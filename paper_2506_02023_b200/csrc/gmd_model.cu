@@ -526,18 +526,21 @@ constexpr int kTM = 128;  // rows per tile = threads = MMA M
 constexpr int kCH = 16;   // edge slots per chunk
 constexpr int kNCH = kTM / kCH;
 constexpr int kNV = 19;   // per-node values: 16 h_bar, 3 grad
-constexpr int kBwdTcCtas = 5;  // resident CTAs per SM (80 registers)
+constexpr int kBwdTcCtas = 4;   // resident CTAs per SM (shared memory bound)
+constexpr int kRowStride = 36;  // floats per staged edge row: m_bar 16 | h 16 | pad (bank spread)
 
+// Pipeline per CTA (tile u): indices of tile u+1 and the chunk records of
+// tile u+2 are loaded while phi(u) is formed; after MMA(u) is issued the
+// gathered rows of tile u+1 are copied into the other shared-memory buffer
+// with cp.async, so they are in flight during the epilogue of tile u.
 struct BwdTcSmem {
     float a_hi[kTM * kK], a_lo[kTM * kK];   // phi, K-major interleaved (gmd_tc.cuh)
     float b_hi[32 * kK], b_lo[32 * kK];     // [P ; kP]
-    float csum[kNCH][kNV + 1];              // chunk sums of this tile
-    int cnode[kNCH];                        // tile-local node index of each chunk (-1: none)
-    int clast[kNCH];                        // chunk is its node's last chunk
-    float run[kNCH + 1][kNV];               // running node sums (carry in slot 0)
-    int chunk_pre[kTM + 1];                 // chunk prefix over the tile's candidate nodes
-    int node_e0[kTM + 1];                   // first edge of each candidate node
-    alignas(16) float own[kNCH][2 * kF];    // MB, H rows of each chunk's node
+    alignas(16) float rows[2][kTM * kRowStride];  // gathered m_bar[w], h[w] per slot
+    alignas(16) float own[2][kNCH][2 * kF];       // m_bar, h rows of each chunk's node
+    float csum[kNCH][kNV + 1];              // chunk sums of the current tile
+    int cnode[2][kNCH];                     // node (local index) of each chunk, -1: none
+    int clast[2][kNCH];                     // chunk is its node's last chunk
     uint64_t mbar;
     uint32_t tbase;
 };
@@ -546,18 +549,65 @@ __device__ __forceinline__ int64_t node_gid(const ConvArgs& a, int64_t k) {
     return a.nodes ? (int64_t)a.nodes[k] : k;
 }
 
-__global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int64_t npc,
-                                                        const float* __restrict__ MB,
-                                                        const float* __restrict__ Hl,
-                                                        float* __restrict__ HB,
-                                                        float4* __restrict__ GRAD,
-                                                        double* vir_part) {
+// chunk records: {first edge, node k, node's canonical row, len | last << 8}
+__global__ void k_chunk_count(ConvArgs a, int32_t* __restrict__ cnt) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k > a.n) return;
+    if (k == a.n) {
+        cnt[k] = 0;
+        return;
+    }
+    const int64_t v = node_gid(a, k);
+    cnt[k] = (a.row[v + 1] - a.row[v] + kCH - 1) / kCH;
+}
+
+__global__ void k_chunk_fill(ConvArgs a, const int32_t* __restrict__ cstart, int4* __restrict__ tab) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= a.n) return;
+    const int64_t v = node_gid(a, k);
+    const int e0 = a.row[v], deg = a.row[v + 1] - e0;
+    const int r = a.crow ? a.crow[v] : (int)v;
+    const int nch = (deg + kCH - 1) / kCH;
+    int4* t = tab + cstart[k];
+    for (int c = 0; c < nch; ++c)
+        t[c] = make_int4(e0 + c * kCH, (int)k, r, min(kCH, deg - c * kCH) | ((c == nch - 1) << 8));
+}
+
+// CTA b takes chunks [cta[b], cta[b+1]): equal chunk counts, cut at node starts
+__global__ void k_chunk_cta(int64_t n, const int32_t* __restrict__ cstart, int grid,
+                            int32_t* __restrict__ cta) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > grid) return;
+    const int64_t T = cstart[n];
+    const int64_t target = T * b / grid;
+    int64_t lo = 0, hi = n;  // first k with cstart[k] >= target
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cstart[mid] >= target) hi = mid; else lo = mid + 1;
+    }
+    cta[b] = cstart[lo];
+}
+
+__device__ __forceinline__ void stage_edge_rows(float* dst, const float* __restrict__ MB,
+                                                const float* __restrict__ Hl, int w) {
+    const float* m = MB + (size_t)w * kF;
+    const float* hh = Hl + (size_t)w * kF;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tc::cp_async16(dst + 4 * i, m + 4 * i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tc::cp_async16(dst + kF + 4 * i, hh + 4 * i);
+}
+
+__global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
+    ConvArgs a, const int4* __restrict__ ctab, const int32_t* __restrict__ ccta,
+    const float* __restrict__ MB, const float* __restrict__ Hl, float* __restrict__ HB,
+    float4* __restrict__ GRAD, double* vir_part) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     BwdTcSmem& S = *reinterpret_cast<BwdTcSmem*>(tc_smem);
     const int tid = threadIdx.x, lane = tid & 31;
     const int ch = tid / kCH, gl = tid % kCH;  // chunk of this thread, lane in chunk
-    const int64_t k_lo = (int64_t)blockIdx.x * npc;
-    const int64_t k_hi = min(a.n, k_lo + npc);
+    const int c_lo = ccta[blockIdx.x], c_hi = ccta[blockIdx.x + 1];
+    const int ntiles = (c_hi - c_lo + kNCH - 1) / kNCH;
     const float isg = c_m.inv_sigma, mus = c_m.mu_step;
 
     for (int i = tid; i < 32 * kK; i += kTM) {
@@ -580,83 +630,48 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int
     const uint32_t idesc = tc::idesc_tf32(kTM, 32);
     const uint32_t trow = tmem + ((uint32_t)(32 * (tid >> 5)) << 16);
 
+    auto chunk_of = [&](int u) -> int4 {
+        const int c = c_lo + u * kNCH + ch;
+        return (u < ntiles && c < c_hi) ? __ldg(ctab + c) : make_int4(0, -1, 0, 0);
+    };
+    auto stage_own = [&](int buf, const int4& c) {  // 8 lanes x 16 B per chunk
+        if (c.y >= 0 && gl < 8)
+            tc::cp_async16(&S.own[buf][ch][(gl >> 2) * kF + (gl & 3) * 4],
+                           (gl < 4 ? MB : Hl) + (size_t)c.z * kF + (gl & 3) * 4);
+    };
+
+    // prologue: tile 0 staged, tile 1 records loaded
+    int4 ci = chunk_of(0);
+    int4 cn = chunk_of(1);
+    bool valid = ci.y >= 0 && gl < (ci.w & 0xff);
+    float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
+    if (valid) {
+        q = __ldg(a.vd + ci.x + gl);
+        stage_edge_rows(S.rows[0] + tid * kRowStride, MB, Hl, __ldg(a.lsrc + ci.x + gl));
+    }
+    stage_own(0, ci);
+    tc::cp_async_commit();
+
     double vir[6] = {0, 0, 0, 0, 0, 0};
-    int64_t kcur = k_lo;  // first node not yet finished
-    int cskip = 0;        // chunks of node kcur already processed
+    float carry = 0.f;
+    int carry_node = -1;
     uint32_t phase = 0;
-    while (kcur < k_hi) {
-        // candidate nodes kcur .. kcur+nk-1: first edges and chunk prefix
-        const int nk = (int)min((int64_t)kTM, k_hi - kcur);
-        for (int j = tid; j <= nk; j += kTM) {
-            const int64_t kk = kcur + (j < nk ? j : nk - 1);
-            const int64_t vv = node_gid(a, kk);
-            S.node_e0[j] = j < nk ? __ldg(a.row + vv) : __ldg(a.row + vv + 1);
+    for (int u = 0; u < ntiles; ++u) {
+        const int buf = u & 1;
+        // (1) indices of tile u+1, records of tile u+2
+        const bool vn = cn.y >= 0 && gl < (cn.w & 0xff);
+        float4 qn = make_float4(0.f, 0.f, 0.f, 1.f);
+        int wn = 0;
+        if (vn) {
+            qn = __ldg(a.vd + cn.x + gl);
+            wn = __ldg(a.lsrc + cn.x + gl);
         }
-        __syncthreads();
-        if (tid < 32) {  // chunk prefix (warp scan over nk <= 128 nodes)
-            int carry = 0;
-            for (int base = 0; base < nk; base += 32) {
-                const int j = base + lane;
-                int c = j < nk ? (S.node_e0[j + 1] - S.node_e0[j] + kCH - 1) / kCH : 0;
-                if (j == 0) c -= cskip;
-                int incl = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += u;
-                }
-                if (j < nk) S.chunk_pre[j + 1] = carry + incl;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) S.chunk_pre[0] = 0;
-        }
-        __syncthreads();
-        const int total_chunks = S.chunk_pre[nk];
-        if (total_chunks == 0) {  // only empty nodes
-            kcur += nk;
-            cskip = 0;
-            __syncthreads();
-            continue;
-        }
-        const int nch = min(kNCH, total_chunks);
-        // ---- this thread's slot: chunk ch -> node jn, edge
-        int jn = -1, cin = 0;
-        bool valid = false;
-        int64_t e = 0;
-        if (ch < nch) {
-            int lo = 0, hi = nk - 1;  // last j with chunk_pre[j] <= ch
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (S.chunk_pre[mid] <= ch) lo = mid; else hi = mid - 1;
-            }
-            jn = lo;
-            cin = ch - S.chunk_pre[jn] + (jn == 0 ? cskip : 0);  // chunk index inside the node
-            const int64_t e0 = S.node_e0[jn] + (int64_t)cin * kCH + gl;
-            valid = e0 < S.node_e0[jn + 1];
-            e = e0;
-        }
+        const int4 cn2 = chunk_of(u + 2);
         if (gl == 0) {
-            S.cnode[ch] = ch < nch ? jn : -1;
-            const int nchunks_node = (S.node_e0[jn >= 0 ? jn + 1 : 0] - S.node_e0[jn >= 0 ? jn : 0] + kCH - 1) / kCH;
-            S.clast[ch] = ch < nch && cin == nchunks_node - 1;
+            S.cnode[buf][ch] = ci.y;
+            S.clast[buf][ch] = ci.y >= 0 && (ci.w >> 8);
         }
-        if (jn >= 0 && gl < 8) {  // own rows of the chunk's node -> S.own[ch]
-            const int64_t vn = node_gid(a, kcur + jn);
-            const int64_t r = a.crow ? a.crow[vn] : vn;
-            const float* src = (gl < 4 ? MB : Hl) + r * kF + (gl & 3) * 4;
-            *reinterpret_cast<float4*>(&S.own[ch][(gl >> 2) * kF + (gl & 3) * 4]) =
-                __ldg(reinterpret_cast<const float4*>(src));
-        }
-        float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
-        float4 m4[4], h4[4];
-        if (valid) {
-            q = __ldg(a.vd + e);
-            const int w = __ldg(a.lsrc + e);
-            ldg256(MB + (size_t)w * kF, m4[0], m4[1]);
-            ldg256(MB + (size_t)w * kF + 8, m4[2], m4[3]);
-            ldg256(Hl + (size_t)w * kF, h4[0], h4[1]);
-            ldg256(Hl + (size_t)w * kF + 8, h4[2], h4[3]);
-        }
+        // (2) phi(u) -> A operand (tf32 hi/lo)
         {
             float phi[kK];
             phi_fast(q.w, phi);
@@ -669,6 +684,7 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int
             }
         }
         tc::fence_async_smem();
+        tc::cp_async_wait_all();  // rows(u), own(u) of this thread have landed
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
@@ -678,29 +694,33 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int
             tc::mma_tf32(tmem, tc::sdesc(S.a_hi), tc::sdesc(S.b_lo), idesc, true);
             tc::commit(&S.mbar);
         }
+        // (3) stage tile u+1 while MMA(u) and the epilogue run
+        if (vn) stage_edge_rows(S.rows[buf ^ 1] + tid * kRowStride, MB, Hl, wn);
+        stage_own(buf ^ 1, cn);
+        tc::cp_async_commit();
+        // (4) epilogue(u)
         tc::mbar_wait(&S.mbar, phase);
         phase ^= 1u;
         tc::fence_after();
         float AB[32];
         tc::tmem_ld32(trow, AB);
-        float acc[kF];
         float gx = 0.f, gy = 0.f, gz = 0.f;
-#pragma unroll
-        for (int f = 0; f < kF; ++f) acc[f] = 0.f;
         if (valid) {
             float fc, dfc;
             fc_dfc_fast(q.w, fc, dfc);
             const float x0 = q.w * isg, step = mus * isg;
             const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
             float dself = 0.f, drev = 0.f;
-            const float* ownm = S.own[ch];
-            const float* ownh = S.own[ch] + kF;
+            const float* rw = S.rows[buf] + tid * kRowStride;
+            const float* ow = S.own[buf][ch];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const float mw[4] = {m4[c].x, m4[c].y, m4[c].z, m4[c].w};
-                const float hw[4] = {h4[c].x, h4[c].y, h4[c].z, h4[c].w};
-                const float4 uu = *reinterpret_cast<const float4*>(ownm + 4 * c);
-                const float4 hh = *reinterpret_cast<const float4*>(ownh + 4 * c);
+                const float4 m4 = *reinterpret_cast<const float4*>(rw + 4 * c);
+                const float4 h4 = *reinterpret_cast<const float4*>(rw + kF + 4 * c);
+                const float4 uu = *reinterpret_cast<const float4*>(ow + 4 * c);
+                const float4 hh = *reinterpret_cast<const float4*>(ow + kF + 4 * c);
+                const float mw[4] = {m4.x, m4.y, m4.z, m4.w};
+                const float hw[4] = {h4.x, h4.y, h4.z, h4.w};
                 const float mu[4] = {uu.x, uu.y, uu.z, uu.w};
                 const float hu[4] = {hh.x, hh.y, hh.z, hh.w};
 #pragma unroll
@@ -708,7 +728,7 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int
                     const int f = 4 * c + i;
                     const float A = AB[f], B = AB[kF + f];
                     const float ds = fmaf(ca, A, cb * B);
-                    acc[f] = mw[i] * (fc * A);
+                    AB[f] = mw[i] * (fc * A);
                     dself = fmaf(mu[i] * hw[i], ds, dself);
                     drev = fmaf(mw[i] * hu[i], ds, drev);
                 }
@@ -725,9 +745,12 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int
             vir[3] += cself * q.x * q.y;
             vir[4] += cself * q.x * q.z;
             vir[5] += cself * q.y * q.z;
+        } else {
+#pragma unroll
+            for (int f = 0; f < kF; ++f) AB[f] = 0.f;
         }
-        // ---- chunk sums: fixed half-warp trees
-        const float hsum = transpose_reduce16_g16(acc, gl);  // feature gl
+        // (5) chunk sums: fixed half-warp trees
+        const float hsum = transpose_reduce16_g16(AB, gl);  // feature gl
         gx = group_sum16(gx);
         gy = group_sum16(gy);
         gz = group_sum16(gz);
@@ -739,45 +762,30 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(ConvArgs a, int
         }
         tc::fence_before();
         __syncthreads();
-        // ---- node totals in chunk order, carried across tiles in run[]
+        // (6) node totals in chunk order (carried across tiles); one adder
+        // per (node, value), so the reductions below are deterministic
         if (tid < kNV) {
-            const int c = tid;
-            float runv = S.run[0][c];  // carry of node kcur (valid when cskip > 0)
-            int prev = -1;
-            for (int k2 = 0; k2 < nch; ++k2) {
-                const int j = S.cnode[k2];
-                if (j != prev) {
-                    if (!(j == 0 && cskip > 0)) runv = 0.f;
-                    prev = j;
-                }
-                runv += S.csum[k2][c];
-                if (S.clast[k2]) {
-                    const int64_t kk = kcur + j;
-                    if (c < kF)
-                        HB[kk * kF + c] += runv;
-                    else
-                        reinterpret_cast<float*>(GRAD + kk)[c - kF] += runv;
+#pragma unroll 1
+            for (int k2 = 0; k2 < kNCH; ++k2) {
+                const int j = S.cnode[buf][k2];
+                if (j < 0) break;
+                const float x = S.csum[k2][tid];
+                carry = j == carry_node ? carry + x : x;
+                carry_node = j;
+                if (S.clast[buf][k2]) {
+                    float* dst = tid < kF ? HB + (size_t)j * kF + tid
+                                          : reinterpret_cast<float*>(GRAD + j) + (tid - kF);
+                    atomicAdd(dst, carry);
+                    carry_node = -1;
                 }
             }
-            S.run[0][c] = runv;  // carry for a node continuing into the next tile
         }
-        __syncthreads();
-        // advance: nodes whose last chunk was in this tile are done
-        {
-            const int jl = S.cnode[nch - 1];
-            const bool last_done = S.clast[nch - 1];
-            int chunks_of_jl_here = 0;
-            for (int k2 = 0; k2 < nch; ++k2) chunks_of_jl_here += S.cnode[k2] == jl;
-            if (last_done) {
-                kcur += jl + 1;
-                cskip = 0;
-            } else {
-                cskip = (jl == 0 ? cskip : 0) + chunks_of_jl_here;
-                kcur += jl;
-            }
-        }
-        __syncthreads();
+        ci = cn;
+        cn = cn2;
+        q = qn;
+        valid = vn;
     }
+    tc::cp_async_wait_all();
     // fp64 virial: thread -> warp -> CTA in fixed order -> vir_part[blockIdx.x]
     __shared__ double wv[kTM / 32][6];
 #pragma unroll
@@ -1095,12 +1103,26 @@ __global__ void k_forces_out(int64_t n, const int32_t* __restrict__ nodes,
     }
 }
 
-__global__ void k_reduce_partials(const double* parts, int nparts, int w, double* out) {
-    int c = threadIdx.x;
-    if (c >= w) return;
-    double acc = 0.0;
-    for (int i = 0; i < nparts; ++i) acc += parts[(size_t)i * w + c];
-    out[c] = acc;
+// fixed-shape reduction of nparts x w partials: block c sums column c with
+// strided per-thread sums and a fixed tree over 512 threads (deterministic
+// for a given nparts)
+__global__ void __launch_bounds__(512) k_reduce_partials(const double* parts, int nparts, int w,
+                                                         double* out) {
+    __shared__ double sh[512];
+    const int t = threadIdx.x, c = blockIdx.x;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int i = t;
+    for (; i + 3 * 512 < nparts; i += 4 * 512)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += parts[(size_t)(i + u * 512) * w + c];
+    for (; i < nparts; i += 512) acc[0] += parts[(size_t)i * w + c];
+    sh[t] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    __syncthreads();
+    for (int o = 256; o > 0; o >>= 1) {
+        if (t < o) sh[t] += sh[t + o];
+        __syncthreads();
+    }
+    if (t == 0) out[c] = sh[0];
 }
 
 }  // namespace
@@ -1160,18 +1182,31 @@ int bwd_tc_grid(int64_t n) {
     return (int)(g > 0 ? g : 1);
 }
 
-void launch_bwd_edge_tc(const ConvArgs& a, const float* MB, const float* Hl, float* HB,
-                        float4* GRAD, double* vir_part, cudaStream_t s) {
-    if (a.n == 0) return;
-    const int grid = bwd_tc_grid(a.n);
-    const int64_t npc = (a.n + grid - 1) / grid;
+void launch_chunk_count(const ConvArgs& a, int32_t* cnt, cudaStream_t s) {
+    k_chunk_count<<<div_up(a.n + 1, 256), 256, 0, s>>>(a, cnt);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_chunk_fill(const ConvArgs& a, const int32_t* cstart, int4* tab, int grid,
+                       int32_t* cta, cudaStream_t s) {
+    if (a.n > 0) {
+        k_chunk_fill<<<div_up(a.n, 256), 256, 0, s>>>(a, cstart, tab);
+        GMD_LAUNCH_CHECK();
+    }
+    k_chunk_cta<<<div_up(grid + 1, 256), 256, 0, s>>>(a.n, cstart, grid, cta);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_bwd_edge_tc(const ConvArgs& a, const int4* ctab, const int32_t* ccta, int grid,
+                        const float* MB, const float* Hl, float* HB, float4* GRAD,
+                        double* vir_part, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sizeof(BwdTcSmem)));
         attr = true;
     }
-    k_bwd_edge_tc<<<grid, kTM, sizeof(BwdTcSmem), s>>>(a, npc, MB, Hl, HB, GRAD, vir_part);
+    k_bwd_edge_tc<<<grid, kTM, sizeof(BwdTcSmem), s>>>(a, ctab, ccta, MB, Hl, HB, GRAD, vir_part);
     GMD_LAUNCH_CHECK();
 }
 
@@ -1221,7 +1256,7 @@ void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, doub
 }
 
 void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s) {
-    k_reduce_partials<<<1, 32, 0, s>>>(parts, nparts, w, out);
+    k_reduce_partials<<<w, 512, 0, s>>>(parts, nparts, w, out);
     GMD_LAUNCH_CHECK();
 }
 

@@ -63,10 +63,16 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
                      double* vir_part, cudaStream_t s);
 
 // the same pass with the radial contractions on tcgen05 (TMEM accumulator);
+// tcgen05 backward edge pass over 16-edge chunk records (one per chunk of a
+// node's in-edges): count per node -> exclusive scan -> fill + per-CTA ranges.
 // grid = bwd_tc_grid(n) CTAs, vir_part holds grid x 6 doubles
 int bwd_tc_grid(int64_t n);
-void launch_bwd_edge_tc(const ConvArgs& a, const float* MB, const float* Hl, float* HB,
-                        float4* GRAD, double* vir_part, cudaStream_t s);
+void launch_chunk_count(const ConvArgs& a, int32_t* cnt, cudaStream_t s);  // n + 1 entries
+void launch_chunk_fill(const ConvArgs& a, const int32_t* cstart, int4* tab, int grid,
+                       int32_t* cta, cudaStream_t s);
+void launch_bwd_edge_tc(const ConvArgs& a, const int4* ctab, const int32_t* ccta, int grid,
+                        const float* MB, const float* Hl, float* HB, float4* GRAD,
+                        double* vir_part, cudaStream_t s);
 
 // three-body stage (global bond CSR by dst; slot = in-bond position)
 struct BondArgs {
