@@ -14,6 +14,8 @@
 //  * the three-body stage runs per "center" atom s on its in-bond list
 //    (bonds e=(w->s) and their reverses e'=(s->w)): every line edge (e, e')
 //    with dst(e) = src(e') is a pair of slots of one center.
+#include <cstdlib>
+
 #include "gmd_model.cuh"
 #include "gmd_tc.cuh"
 
@@ -437,7 +439,8 @@ __device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
     vr[5] = fmaf(cself * q.y, q.z, vr[5]);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
+template <int CTAS, int INFLIGHT>
+__global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
                                                           const float* __restrict__ Hl,
                                                           float* __restrict__ HB,
                                                           float4* __restrict__ GRAD,
@@ -451,26 +454,41 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
     const float isg = c_m.inv_sigma, mus = c_m.mu_step;
     if (gl < 6) sVir[grp][gl] = 0.0;
     const int64_t iters = (a.n + ng - 1) / ng;
+    // node k + ng's row bounds and own rows are loaded while node k runs
+    int e0n = 0, e1n = 0;
+    float mun = 0.f, hun = 0.f;
+    auto prefetch = [&](int64_t k) {
+        if (k < a.n) {
+            const int64_t v = a.nodes ? (int64_t)a.nodes[k] : k;
+            const int64_t r = a.crow ? a.crow[v] : v;
+            e0n = __ldg(a.row + v);
+            e1n = __ldg(a.row + v + 1);
+            mun = __ldg(MB + r * kF + gl);
+            hun = __ldg(Hl + r * kF + gl);
+        } else {
+            e0n = e1n = 0;
+        }
+    };
+    prefetch(g0);
     for (int64_t it = 0; it < iters; ++it) {
         const int64_t k = g0 + it * ng;  // local node index
         const bool valid = k < a.n;
-        const int64_t v = valid ? (a.nodes ? (int64_t)a.nodes[k] : k) : 0;  // global id
-        const int64_t r = valid ? (a.crow ? a.crow[v] : v) : 0;
+        const int e0 = e0n, e1 = e1n;
         __syncwarp();
         if (valid) {
-            sU[grp][0][gl] = MB[r * kF + gl];
-            sU[grp][1][gl] = Hl[r * kF + gl];
+            sU[grp][0][gl] = mun;
+            sU[grp][1][gl] = hun;
         }
         __syncwarp();
+        prefetch(k + ng);
         float acc[kF];
 #pragma unroll
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
         float gx = 0.f, gy = 0.f, gz = 0.f;
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const int e0 = valid ? __ldg(a.row + v) : 0;
-        const int e1 = valid ? __ldg(a.row + v + 1) : 0;
         const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
         const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
+        if constexpr (INFLIGHT == 2) {
         for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 32) {
             const bool ha = e < e1, hb = e + 16 < e1;
             BwdEdgeIn xa, xb;
@@ -479,6 +497,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
             if (ha) bwd_math(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
             if (__any_sync(0xffffffffu, hb) && hb)
                 bwd_math(xb, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
+        }
+        } else {
+        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
+            if (e < e1) {
+                BwdEdgeIn xa;
+                bwd_load(a, MB, Hl, e, xa);
+                bwd_math(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
+            }
+        }
         }
 #pragma unroll
         for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
@@ -489,14 +516,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
         gx = group_sum16(gx);
         gy = group_sum16(gy);
         gz = group_sum16(gz);
-        if (valid) {
-            HB[k * kF + gl] += hb;
+        if (valid) {  // one adder per element: red.add is the plain read-add-write
+            atomicAdd(HB + k * kF + gl, hb);
             if (gl == 0) {
-                float4 g = GRAD[k];
-                g.x += gx;
-                g.y += gy;
-                g.z += gz;
-                GRAD[k] = g;
+                float* g = reinterpret_cast<float*>(GRAD + k);
+                atomicAdd(g, gx);
+                atomicAdd(g + 1, gy);
+                atomicAdd(g + 2, gz);
             }
         }
     }
@@ -1172,7 +1198,17 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
                      double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
-    k_bwd_edge<<<model_grid(a.n), kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+    static const int variant = [] {
+        const char* v = std::getenv("GMD_BWD_VARIANT");
+        return v ? std::atoi(v) : 0;
+    }();
+    const int g = model_grid(a.n);
+    switch (variant) {
+        case 1: k_bwd_edge<3, 1><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
+        case 2: k_bwd_edge<2, 1><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
+        case 3: k_bwd_edge<3, 2><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
+        default: k_bwd_edge<2, 2><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
+    }
     GMD_LAUNCH_CHECK();
 }
 
