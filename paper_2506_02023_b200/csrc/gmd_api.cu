@@ -40,6 +40,16 @@ void launch_line_count(int64_t nb, const int32_t* bedge, const int32_t* esrc, co
 void launch_line_fill(int64_t nb, const int32_t* bedge, const int32_t* esrc, const int32_t* brow,
                       const int32_t* brev, const int32_t* lpos, int32_t* pairs, cudaStream_t s);
 int tb_grid_size(int64_t n);
+void launch_bond_halo_flag(int64_t nb, const int32_t* bedge, const int32_t* esrc,
+                           const int32_t* owner, int j, int32_t* flag, cudaStream_t s);
+void launch_bond_halo_assign(int64_t nb, const int32_t* bedge, const int32_t* esrc,
+                             const int32_t* owner, int j, const int32_t* pos, int32_t base,
+                             int32_t* brev, cudaStream_t s);
+void launch_bond_send_plan(int64_t n_own, const int32_t* nodes, const int32_t* brow, int64_t nb,
+                           const int32_t* bedge, const int32_t* esrc, const uint32_t* img,
+                           const int32_t* owner, int r, const int32_t* crow, int32_t from0,
+                           int phase, const int32_t* offs, int32_t* cnt_or_fill, int32_t* bcen,
+                           int32_t* xs, int32_t nrows, cudaStream_t s);
 }  // namespace gmd
 
 using namespace gmd;
@@ -275,6 +285,11 @@ struct gmd_handle {
     int64_t n_own = 0;
     DBuf nodes, xsend, sendbuf;
     std::vector<int64_t> soff, scnt, roff, rcnt;
+    // ... and its bond halo plan (three-body): rows nb .. nb + nb_halo of the
+    // per-bond arrays are received, b_* as above in bond rows
+    int64_t nb_halo = 0;
+    DBuf bxsend, bsendbuf, bcen;
+    std::vector<int64_t> b_soff, b_scnt, b_roff, b_rcnt;
 
     // profiler: event pairs recorded on `stream` around every launch
     bool prof = false;
@@ -454,6 +469,72 @@ void build_rank_plan(gmd_handle* h, const int32_t* ownp, int r) {
     sync(h);
 }
 
+// one rank per GPU, three-body: halo bond rows (see gmd_linegraph.cu)
+void build_bond_rank_plan(gmd_handle* h, const int32_t* ownp, int r) {
+    cudaStream_t s = h->stream;
+    LayoutState& A = h->atoms;
+    const int W = h->p, stride = 1 + 2 * W;
+    const int64_t nb = h->nb;
+    const int32_t* be = h->bedge.as<int32_t>();
+    const int32_t* es = h->src.as<int32_t>();
+    int32_t* bv = h->brev.as<int32_t>();
+    h->b_soff.assign(W, 0);
+    h->b_scnt.assign(W, 0);
+    h->b_roff.assign(W, 0);
+    h->b_rcnt.assign(W, 0);
+    // receive rows: per source rank j, bonds (w -> u) with owner(w) = j in (u, row) order
+    int32_t* flag = h->flagtmp.get<int32_t>(nb + 1);
+    int64_t base = nb;
+    for (int j = 0; j < W; ++j) {
+        if (j == r) continue;
+        launch_bond_halo_flag(nb, be, es, ownp, j, flag, s);
+        scan_i32(h, flag, flag, nb + 1);
+        int32_t c = 0;
+        GMD_CUDA(cudaMemcpyAsync(&c, flag + nb, 4, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        launch_bond_halo_assign(nb, be, es, ownp, j, flag, (int32_t)base, bv, s);
+        h->b_roff[j] = base;
+        h->b_rcnt[j] = c;
+        base += c;
+    }
+    h->nb_halo = base - nb;
+    // send rows: per FROM row x (grouped by owner, ascending id), the slots
+    // (x -> w) at centers owned here, in x's canonical row order
+    const int32_t from0 = A.list_off[(size_t)r * stride + 1 + W];
+    const int32_t from1 = A.list_off[(size_t)r * stride + 1 + 2 * W];
+    const int32_t nfr = from1 - from0;
+    int32_t* cnt = h->counts.get<int32_t>(nfr + 1);
+    GMD_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nfr + 1), s));
+    int32_t* bcen = h->bcen.get<int32_t>(std::max<int64_t>(1, nb));
+    const int32_t* crow = A.crow.as<int32_t>();
+    const uint32_t* img = h->img.as<uint32_t>();
+    launch_bond_send_plan(h->n_own, h->nodes.as<int32_t>(), h->brow.as<int32_t>(), nb, be, es, img,
+                          ownp, r, crow, from0, 0, nullptr, cnt, bcen, nullptr, nfr, s);
+    int32_t* offs = h->feat_tmp.get<int32_t>(nfr + 1);
+    scan_i32(h, cnt, offs, nfr + 1);
+    std::vector<int32_t> hoffs;
+    d2h(h, hoffs, offs, nfr + 1);
+    sync(h);
+    const int32_t nsend = hoffs[nfr];
+    int32_t* xs = h->bxsend.get<int32_t>(std::max(1, nsend));
+    GMD_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nfr + 1), s));
+    launch_bond_send_plan(h->n_own, h->nodes.as<int32_t>(), h->brow.as<int32_t>(), nb, be, es, img,
+                          ownp, r, crow, from0, 1, offs, cnt, bcen, xs, nfr, s);
+    for (int j = 0; j < W; ++j) {
+        if (j == r) continue;
+        const int32_t a0 = A.list_off[(size_t)r * stride + 1 + W + j] - from0;
+        const int32_t a1 = A.list_off[(size_t)r * stride + 2 + W + j] - from0;
+        h->b_soff[j] = hoffs[a0];
+        h->b_scnt[j] = hoffs[a1] - hoffs[a0];
+    }
+    std::vector<int64_t> all((size_t)W * W);
+    h->comm->allgather_i64(s, h->b_scnt.data(), W, all.data());
+    for (int j = 0; j < W; ++j)
+        if (j != r && all[(size_t)j * W + r] != h->b_rcnt[j])
+            raise(kRuntime, "bond transfer plan misalignment");
+    sync(h);
+}
+
 void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, const double* lat,
                 const uint8_t* pbc, double rc, double r3, double tau, int p, uint32_t flags) {
     cudaStream_t s = h->stream;
@@ -558,8 +639,6 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     const int myrank = rank_mode ? h->comm->rank : -1;
     if (rank_mode && p != h->comm->world)
         raise(kConfig, "one-rank-per-GPU mode needs p == world size");
-    if (rank_mode && r3 > 0.0)
-        raise(kConfig, "three-body graphs are not supported in one-rank-per-GPU mode yet");
     h->bounds.assign(p + 1, 0.0);
     h->bounds[p] = 1.0;
     int32_t* ownp = h->atoms.owner.get<int32_t>(n);
@@ -717,7 +796,8 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         int32_t* be = h->bedge.get<int32_t>(h->nb);
         int32_t* bv = h->brev.get<int32_t>(h->nb);
         { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, s); }
-        { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, bv, b.flags, s); }
+        { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, bv, b.flags, ownp, myrank, s); }
+        if (rank_mode) build_bond_rank_plan(h, ownp, myrank);
     }
     GMD_CUDA(cudaEventRecord(h->ev[1], s));
     read_flags(h, hdr);
@@ -735,6 +815,8 @@ void need_built(const gmd_handle* h) {
 void ensure_bond_layout(gmd_handle* h) {
     need_built(h);
     if (!h->has_lg) raise(kConfig, "no line graph was built");
+    if (h->comm && h->comm->world > 1)
+        raise(kConfig, "bond partition views are not available in one-rank-per-GPU mode");
     LayoutState& B = h->bonds;
     if (B.ready) return;
     cudaStream_t s = h->stream;
@@ -927,7 +1009,6 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     LayoutState& A = h->atoms;
     const int64_t R = A.rows;
     const bool part = h->p > 1;
-    if (rank_mode && tb) raise(kConfig, "three-body graphs are not supported in one-rank-per-GPU mode yet");
     upload_model(h->mc, s);
 
     GMD_CUDA(cudaEventRecord(h->ev[2], s));
@@ -960,6 +1041,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                h->ed.as<float>()};
     if (use_tc) ensure_chunk_table(h, a);
     BondArgs ba{n,
+                a.nodes,
                 a.crow,
                 h->brow.as<int32_t>(),
                 h->bedge.as<int32_t>(),
@@ -967,9 +1049,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 h->src.as<int32_t>(),
                 h->vd.as<float4>()};
     float *TP = nullptr, *TH3 = nullptr, *TH4 = nullptr;
+    const int64_t nbr = h->nb + (rank_mode ? h->nb_halo : 0);  // bond rows incl. received
     if (tb) {
-        TP = h->TP.get<float>((size_t)h->nb * kF);
-        TH3 = h->TH3.get<float>((size_t)h->nb * kF);
+        TP = h->TP.get<float>((size_t)nbr * kF);
+        TH3 = h->TH3.get<float>((size_t)nbr * kF);
         TH4 = h->TH4.get<float>(n * kF);
     }
     const int32_t* xd = A.xdst.as<int32_t>();
@@ -999,6 +1082,28 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         }
     };
 
+    // bond halo rows (three-body, one rank per GPU): t' and v_bar of the
+    // reverse bonds computed at centers owned by peers
+    const int64_t nbsend =
+        rank_mode && tb ? std::accumulate(h->b_scnt.begin(), h->b_scnt.end(), (int64_t)0) : 0;
+    float* bsend = rank_mode && tb ? h->bsendbuf.get<float>(std::max<int64_t>(1, nbsend) * kF)
+                                   : nullptr;
+    auto bond_exchange = [&](float* buf, int width) {
+        if (!(rank_mode && tb)) return;
+        {
+            PROF("halo_pack");
+            if (nbsend > 0) {
+                k_gather_rows<<<div_up(nbsend * width, 256), 256, 0, s>>>(
+                    nbsend, h->bxsend.as<int32_t>(), reinterpret_cast<const uint32_t*>(buf),
+                    reinterpret_cast<uint32_t*>(bsend), width);
+                GMD_LAUNCH_CHECK();
+            }
+        }
+        PROF("halo_exchange");
+        h->comm->exchange(s, bsend, h->b_soff.data(), h->b_scnt.data(), buf, h->b_roff.data(),
+                          h->b_rcnt.data(), width);
+    };
+
     // ---- feature calculation: embeddings for every layout row (:597-602)
     { PROF("embed"); launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s); }
     GMD_CUDA(cudaEventRecord(h->ev[3], s));
@@ -1008,6 +1113,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         const bool tbl = tb && l == L - 1;
         if (tbl) {
             { PROF("tb_forward"); launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), s); }
+            bond_exchange(TP, kF);
             { PROF("tb_inject"); launch_tb_inject(ba, TP, H[l], TH4, s); }
         }
         if (l > 0 || tbl) exchange(H[l]);
@@ -1032,11 +1138,14 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
         }
         if (tb && l == L - 1) {
-            float* QB = h->QB.get<float>(n * kF);
-            float4* VIN = h->VIN.get<float4>(h->nb);
-            float4* VOUT = h->VOUT.get<float4>(h->nb);
-            { PROF("tb_bwd_q"); launch_tb_bwd_q(n, HB, TH4, QB, s); }
+            float* QB = h->QB.get<float>(R * kF);
+            float4* VIN = h->VIN.get<float4>(nbr);
+            float4* VOUT = h->VOUT.get<float4>(nbr);
+            { PROF("tb_bwd_q"); launch_tb_bwd_q(n, a.nodes, a.crow, HB, TH4, QB, s); }
+            if (rank_mode) exchange(QB);  // q_bar of halo atoms (bond sources)
             { PROF("tb_backward"); launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, s); }
+            bond_exchange(reinterpret_cast<float*>(VIN), 4);
+            bond_exchange(reinterpret_cast<float*>(VOUT), 4);
             { PROF("tb_grad"); launch_tb_grad(ba, VIN, VOUT, GRAD, s); }
         }
     }

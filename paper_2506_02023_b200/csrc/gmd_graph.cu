@@ -496,12 +496,17 @@ __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
                            const int32_t* __restrict__ src, const uint32_t* __restrict__ img,
                            const uint8_t* __restrict__ ebond, const int32_t* __restrict__ brow,
                            const int32_t* __restrict__ bedge, int32_t* __restrict__ brev,
-                           int32_t* __restrict__ flags) {
+                           int32_t* __restrict__ flags, const int32_t* __restrict__ owner,
+                           int only) {
     int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (v >= n) return;
     for (int b = brow[v] + (threadIdx.x & 31); b < brow[v + 1]; b += 32) {
         const int e = bedge[b];
         const int w = src[e];
+        if (only >= 0 && owner[w] != only) {  // reverse bond lives on w's rank:
+            brev[b] = -1;                     // a halo bond row (rank bond plan)
+            continue;
+        }
         int o0, o1, o2;
         unpack_img(img[e], o0, o1, o2);
         const uint32_t want = pack_img(-o0, -o1, -o2);
@@ -617,10 +622,11 @@ void launch_bond_edges(const int32_t* row, const uint8_t* ebond, int64_t n, cons
 }
 
 void launch_bond_rev(int64_t n, const GraphDev& gd, const int32_t* brow, const int32_t* bedge,
-                     int32_t* brev, int32_t* flags, cudaStream_t s) {
+                     int32_t* brev, int32_t* flags, const int32_t* owner, int only,
+                     cudaStream_t s) {
     if (n == 0) return;
     k_bond_rev<<<div_up(n, 8), 256, 0, s>>>(n, gd.row, gd.src, gd.img, gd.bond, brow, bedge, brev,
-                                            flags);
+                                            flags, owner, only);
     GMD_LAUNCH_CHECK();
 }
 

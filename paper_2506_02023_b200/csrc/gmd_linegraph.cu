@@ -65,6 +65,97 @@ __global__ void k_line_fill(int64_t nb, const int32_t* __restrict__ bedge,
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// One rank per GPU: bond halo plan (SURVEY 8e "bond-feature exchange").
+// A bond b = (w -> u) with u owned here and w owned by rank j needs the rows
+// (t', v_bar) its reverse bond (u -> w) gets at center w on rank j.  Receive
+// rows: per j, the bonds b in (u, row) order.  Send rows for rank j: per
+// halo atom x of FROM_r[j] (ascending id), the slots c = (x -> w) at owned
+// centers w, sorted by (w, -image) -- the order of x's row on rank j.
+// ---------------------------------------------------------------------------
+__global__ void k_bond_halo_flag(int64_t nb, const int32_t* __restrict__ bedge,
+                                 const int32_t* __restrict__ esrc,
+                                 const int32_t* __restrict__ owner, int j,
+                                 int32_t* __restrict__ flag) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    flag[b] = b < nb && owner[esrc[bedge[b]]] == j;
+}
+
+__global__ void k_bond_halo_assign(int64_t nb, const int32_t* __restrict__ bedge,
+                                   const int32_t* __restrict__ esrc,
+                                   const int32_t* __restrict__ owner, int j,
+                                   const int32_t* __restrict__ pos, int32_t base,
+                                   int32_t* __restrict__ brev) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    if (owner[esrc[bedge[b]]] == j) brev[b] = base + pos[b];
+}
+
+__global__ void k_bond_center(int64_t n, const int32_t* __restrict__ nodes,
+                              const int32_t* __restrict__ brow, int32_t* __restrict__ bcen) {
+    const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (k >= n) return;
+    const int w = nodes[k];
+    for (int b = brow[w] + (threadIdx.x & 31); b < brow[w + 1]; b += 32) bcen[b] = w;
+}
+
+__global__ void k_bond_send_count(int64_t nb, const int32_t* __restrict__ bedge,
+                                  const int32_t* __restrict__ esrc,
+                                  const int32_t* __restrict__ owner, int r,
+                                  const int32_t* __restrict__ crow, int32_t from0,
+                                  int32_t* __restrict__ cnt) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int x = esrc[bedge[b]];
+    if (owner[x] != r) atomicAdd(&cnt[crow[x] - from0], 1);
+}
+
+__global__ void k_bond_send_fill(int64_t nb, const int32_t* __restrict__ bedge,
+                                 const int32_t* __restrict__ esrc,
+                                 const int32_t* __restrict__ owner, int r,
+                                 const int32_t* __restrict__ crow, int32_t from0,
+                                 const int32_t* __restrict__ offs, int32_t* __restrict__ fill,
+                                 int32_t* __restrict__ xs) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int x = esrc[bedge[b]];
+    if (owner[x] != r) {
+        const int row = crow[x] - from0;
+        xs[offs[row] + atomicAdd(&fill[row], 1)] = (int32_t)b;
+    }
+}
+
+__device__ __forceinline__ unsigned long long send_key(int b, const int32_t* bcen,
+                                                       const int32_t* bedge,
+                                                       const uint32_t* img) {
+    int o0, o1, o2;
+    unpack_img(img[bedge[b]], o0, o1, o2);  // image of (x -> w); rank j sees -o
+    return ((unsigned long long)(uint32_t)bcen[b] << 30) |
+           ((unsigned long long)(512 - o0) << 20) | ((unsigned long long)(512 - o1) << 10) |
+           (unsigned long long)(512 - o2);
+}
+
+__global__ void k_bond_send_sort(int32_t nrows, const int32_t* __restrict__ offs,
+                                 int32_t* __restrict__ xs, const int32_t* __restrict__ bcen,
+                                 const int32_t* __restrict__ bedge,
+                                 const uint32_t* __restrict__ img) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nrows) return;
+    const int a0 = offs[i], a1 = offs[i + 1];
+    for (int t = a0 + 1; t < a1; ++t) {  // insertion sort (<= 64 bonds per atom)
+        const int b = xs[t];
+        const unsigned long long kb = send_key(b, bcen, bedge, img);
+        int u = t - 1;
+        while (u >= a0 && send_key(xs[u], bcen, bedge, img) > kb) {
+            xs[u + 1] = xs[u];
+            --u;
+        }
+        xs[u + 1] = b;
+    }
+}
+
 }  // namespace
 
 void launch_bond_owner(int64_t n, const int32_t* brow, const int32_t* owner, int32_t* bown,
@@ -93,6 +184,48 @@ void launch_line_fill(int64_t nb, const int32_t* bedge, const int32_t* esrc, con
     if (nb == 0) return;
     k_line_fill<<<div_up(nb, 256), 256, 0, s>>>(nb, bedge, esrc, brow, brev, lpos, pairs);
     GMD_LAUNCH_CHECK();
+}
+
+void launch_bond_halo_flag(int64_t nb, const int32_t* bedge, const int32_t* esrc,
+                           const int32_t* owner, int j, int32_t* flag, cudaStream_t s) {
+    k_bond_halo_flag<<<div_up(nb + 1, 256), 256, 0, s>>>(nb, bedge, esrc, owner, j, flag);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_bond_halo_assign(int64_t nb, const int32_t* bedge, const int32_t* esrc,
+                             const int32_t* owner, int j, const int32_t* pos, int32_t base,
+                             int32_t* brev, cudaStream_t s) {
+    if (nb == 0) return;
+    k_bond_halo_assign<<<div_up(nb, 256), 256, 0, s>>>(nb, bedge, esrc, owner, j, pos, base, brev);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_bond_send_plan(int64_t n_own, const int32_t* nodes, const int32_t* brow, int64_t nb,
+                           const int32_t* bedge, const int32_t* esrc, const uint32_t* img,
+                           const int32_t* owner, int r, const int32_t* crow, int32_t from0,
+                           int phase, const int32_t* offs, int32_t* cnt_or_fill, int32_t* bcen,
+                           int32_t* xs, int32_t nrows, cudaStream_t s) {
+    if (phase == 0) {  // count per FROM row
+        if (n_own > 0) {
+            k_bond_center<<<div_up(n_own, 8), 256, 0, s>>>(n_own, nodes, brow, bcen);
+            GMD_LAUNCH_CHECK();
+        }
+        if (nb > 0) {
+            k_bond_send_count<<<div_up(nb, 256), 256, 0, s>>>(nb, bedge, esrc, owner, r, crow,
+                                                              from0, cnt_or_fill);
+            GMD_LAUNCH_CHECK();
+        }
+    } else {  // fill + per-row sort
+        if (nb > 0) {
+            k_bond_send_fill<<<div_up(nb, 256), 256, 0, s>>>(nb, bedge, esrc, owner, r, crow, from0,
+                                                             offs, cnt_or_fill, xs);
+            GMD_LAUNCH_CHECK();
+        }
+        if (nrows > 0) {
+            k_bond_send_sort<<<div_up(nrows, 128), 128, 0, s>>>(nrows, offs, xs, bcen, bedge, img);
+            GMD_LAUNCH_CHECK();
+        }
+    }
 }
 
 }  // namespace gmd

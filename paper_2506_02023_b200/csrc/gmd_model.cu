@@ -873,7 +873,8 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float*
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int64_t w0 = (int64_t)blockIdx.x * kTbWarps + wl;
     const int64_t nw = (int64_t)gridDim.x * kTbWarps;
-    for (int64_t s = w0; s < a.n; s += nw) {
+    for (int64_t ks = w0; ks < a.n; ks += nw) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
         const int b0 = a.brow[s], k = a.brow[s + 1] - b0;
         if (k > kMaxBondsPerAtom) {
             if (lane == 0) atomicOr(&flags[1], 16);
@@ -921,8 +922,9 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float*
 // q_u = sum_{b into u} t'_b (ascending b), h_u += tanh(W4 q_u)
 __global__ void k_tb_inject(BondArgs a, const float* __restrict__ TP, float* __restrict__ H,
                             float* __restrict__ TH4) {
-    int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= a.n) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.n) return;
+    const int64_t u = a.nodes ? (int64_t)a.nodes[k] : k;
     float q[kF];
 #pragma unroll
     for (int f = 0; f < kF; ++f) q[f] = 0.f;
@@ -944,16 +946,18 @@ __global__ void k_tb_inject(BondArgs a, const float* __restrict__ TP, float* __r
         h[f] += th[f];
     }
     store_row16(H + r * kF, h);
-    store_row16(TH4 + u * kF, th);
+    store_row16(TH4 + k * kF, th);
 }
 
-__global__ void k_tb_bwd_q(int64_t n, const float* __restrict__ HB, const float* __restrict__ TH4,
-                           float* __restrict__ QB) {
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
+__global__ void k_tb_bwd_q(int64_t n, const int32_t* __restrict__ nodes,
+                           const int32_t* __restrict__ crow, const float* __restrict__ HB,
+                           const float* __restrict__ TH4, float* __restrict__ QB) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t v = nodes ? (int64_t)nodes[k] : k;
     float hb[kF], th[kF], y[kF], qb[kF];
-    load_row16(HB + v * kF, hb);
-    load_row16(TH4 + v * kF, th);
+    load_row16(HB + k * kF, hb);
+    load_row16(TH4 + k * kF, th);
 #pragma unroll
     for (int f = 0; f < kF; ++f) y[f] = hb[f] * (1.0f - th[f] * th[f]);
 #pragma unroll
@@ -963,7 +967,7 @@ __global__ void k_tb_bwd_q(int64_t n, const float* __restrict__ HB, const float*
         for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W4[f * kF + g], y[f], acc);
         qb[g] = acc;
     }
-    store_row16(QB + v * kF, qb);
+    store_row16(QB + (crow ? (int64_t)crow[v] : v) * kF, qb);
 }
 
 // Per center s.  Slot j holds in-bond e_j = (w_j -> s); its reverse e'_j is
@@ -984,7 +988,8 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
     const int64_t w0 = (int64_t)blockIdx.x * kTbWarps + wl;
     const int64_t nw = (int64_t)gridDim.x * kTbWarps;
     double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t s = w0; s < a.n; s += nw) {
+    for (int64_t ks = w0; ks < a.n; ks += nw) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
         const int b0 = a.brow[s], k = a.brow[s + 1] - b0;
         if (k > kMaxBondsPerAtom) continue;  // flagged in the forward
         for (int j = lane; j < k; j += 32) {
@@ -997,7 +1002,8 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
             for (int f = 0; f < kF; ++f) st[wl][j][f] = t[f];
             // stage 2: adjoints of the reverse bond e'_j
             float tpb[kF], th[kF], ds[kF];
-            load_row16(QB + (size_t)__ldg(a.esrc + e) * kF, tpb);
+            const int x = __ldg(a.esrc + e);
+            load_row16(QB + (size_t)(a.crow ? a.crow[x] : x) * kF, tpb);
             load_row16(TH3 + (size_t)(b0 + j) * kF, th);
             float fc, dfc;
             fcut3(q.w, fc, dfc);
@@ -1088,8 +1094,9 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
 // grad[u] += sum_{X into u} (v_bar of rev(X)) - (v_bar of X)
 __global__ void k_tb_grad(BondArgs a, const float4* __restrict__ VIN,
                           const float4* __restrict__ VOUT, float4* __restrict__ GRAD) {
-    int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= a.n) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.n) return;
+    const int64_t u = a.nodes ? (int64_t)a.nodes[k] : k;
     float gx = 0.f, gy = 0.f, gz = 0.f;
     for (int b = a.brow[u]; b < a.brow[u + 1]; ++b) {
         const int rb = a.brev[b];
@@ -1098,11 +1105,11 @@ __global__ void k_tb_grad(BondArgs a, const float4* __restrict__ VIN,
         gy += (i1.y + o1.y) - (i2.y + o2.y);
         gz += (i1.z + o1.z) - (i2.z + o2.z);
     }
-    float4 g = GRAD[u];
+    float4 g = GRAD[k];
     g.x += gx;
     g.y += gy;
     g.z += gz;
-    GRAD[u] = g;
+    GRAD[k] = g;
 }
 
 __global__ void k_init_hbar(int64_t n, float* HB) {
@@ -1258,9 +1265,10 @@ void launch_tb_inject(const BondArgs& a, const float* TP, float* H, float* TH4, 
     GMD_LAUNCH_CHECK();
 }
 
-void launch_tb_bwd_q(int64_t n, const float* HB, const float* TH4, float* QB, cudaStream_t s) {
+void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const float* HB,
+                     const float* TH4, float* QB, cudaStream_t s) {
     if (n == 0) return;
-    k_tb_bwd_q<<<div_up(n, 128), 128, 0, s>>>(n, HB, TH4, QB);
+    k_tb_bwd_q<<<div_up(n, 128), 128, 0, s>>>(n, nodes, crow, HB, TH4, QB);
     GMD_LAUNCH_CHECK();
 }
 

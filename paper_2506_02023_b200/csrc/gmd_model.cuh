@@ -76,7 +76,8 @@ void launch_bwd_edge_tc(const ConvArgs& a, const int4* ctab, const int32_t* ccta
 
 // three-body stage (global bond CSR by dst; slot = in-bond position)
 struct BondArgs {
-    int64_t n;
+    int64_t n;              // centers this handle updates
+    const int32_t* nodes;   // n: their global ids (one rank per GPU), null = 0..n-1
     const int32_t* crow;
     const int32_t* brow;    // n + 1
     const int32_t* bedge;   // B: edge id of bond
@@ -86,7 +87,8 @@ struct BondArgs {
 };
 void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, cudaStream_t s);
 void launch_tb_inject(const BondArgs& a, const float* TP, float* H, float* TH4, cudaStream_t s);
-void launch_tb_bwd_q(int64_t n, const float* HB, const float* TH4, float* QB, cudaStream_t s);
+void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const float* HB,
+                     const float* TH4, float* QB, cudaStream_t s);  // QB by layout row
 void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
                         float4* VOUT, double* vir_part, cudaStream_t s);
 void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, float4* GRAD,

@@ -260,7 +260,8 @@ __global__ void k_lay_scatter(const int32_t* __restrict__ owner,
                 int rank = __popc(bal & ((1u << lane) - 1u));
                 int pos = offs[(int64_t)lmin * nchunks + c] + run[lmin] + rank;
                 node_array[pos] = (int32_t)v;
-                if (lmin == canon) crow[v] = pos;
+                // one rank per GPU: a halo atom's row is its FROM row here
+                if (lmin == canon || (only >= 0 && o != only)) crow[v] = pos;
                 cur = next_list_only(o, m, p, cur, only);
             }
             __syncwarp();

@@ -12,12 +12,12 @@ from tests import systems as S
 pytestmark = pytest.mark.gpu
 
 
-def run_group(s, prm, W):
+def run_group(s, prm, W, r3=None):
     hs = G.local_group(W)
 
     def rank(r):
         def go():
-            d = G.Distributed.create_distributed(s, prm.r_atom, None, W, 1, True, handle=hs[r])
+            d = G.Distributed.create_distributed(s, prm.r_atom, r3, W, 1, True, handle=hs[r])
             out = G.forward_distributed(d, prm)
             return d, out, G.owned_ids(d)
         return go
@@ -66,3 +66,25 @@ def test_rank_group_rejects_mismatch():
 
     with pytest.raises(G.Error, match="p == world"):
         G.run_ranks([bad(0), bad(1)])
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+@pytest.mark.parametrize("which", ["quartz", "liquid"])
+def test_rank_group_three_body(W, which):
+    """Three-body graphs one rank per GPU: t' / v_bar rows of reverse bonds whose
+    center lives on a peer travel through the bond halo plan; q_bar halo rows
+    through the atom plan.  Owned atoms' energies and forces are bitwise equal
+    to the single-handle result."""
+    s = S.quartz((4, 4, 4)) if which == "quartz" else S.liquid(1200)
+    prm = G.ToyPotentialParams.init(7, 16, 8, 3, 5.0, 3.0)
+    ref_d = G.Distributed.create_distributed(s, 5.0, 3.0, W, 1, True)
+    ref = G.forward_distributed(ref_d, prm)
+    res = run_group(s, prm, W, r3=3.0)
+    seen = np.zeros(s.size(), bool)
+    for d, out, ids in res:
+        seen[ids] = True
+        np.testing.assert_array_equal(out.per_atom[ids], ref.per_atom[ids])
+        np.testing.assert_array_equal(out.forces[ids], ref.forces[ids])
+        assert abs(out.energy - ref.energy) <= 1e-9 * abs(ref.energy)
+        np.testing.assert_allclose(out.stress, ref.stress, atol=1e-12, rtol=1e-9)
+    assert seen.all()
