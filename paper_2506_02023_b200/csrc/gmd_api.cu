@@ -1364,6 +1364,8 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         for (int l = 0; l < L; ++l)
             for (int i = 0; i < F; ++i) m.b[l][i] = (float)*q++;
         for (int i = 0; i < F * K; ++i) m.P[i] = (float)*q++;
+        for (int f = 0; f < F; ++f)
+            for (int k = 0; k < K; ++k) m.PT[k * F + f] = m.P[f * K + k];
         {
             const double* Pd = blob + 119 * F + (size_t)L * F * F + (size_t)L * F;
             for (int i = 0; i < F * K; ++i) m.Pk[i] = (float)(Pd[i] * (double)(i % K));

@@ -439,8 +439,7 @@ __device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
     vr[5] = fmaf(cself * q.y, q.z, vr[5]);
 }
 
-template <int CTAS, int INFLIGHT>
-__global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
+__global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
                                                           const float* __restrict__ Hl,
                                                           float* __restrict__ HB,
                                                           float4* __restrict__ GRAD,
@@ -488,7 +487,6 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge(ConvArgs a, const f
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
         const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
-        if constexpr (INFLIGHT == 2) {
         for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 32) {
             const bool ha = e < e1, hb = e + 16 < e1;
             BwdEdgeIn xa, xb;
@@ -497,15 +495,6 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge(ConvArgs a, const f
             if (ha) bwd_math(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
             if (__any_sync(0xffffffffu, hb) && hb)
                 bwd_math(xb, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
-        }
-        } else {
-        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
-            if (e < e1) {
-                BwdEdgeIn xa;
-                bwd_load(a, MB, Hl, e, xa);
-                bwd_math(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
-            }
-        }
         }
 #pragma unroll
         for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
@@ -523,6 +512,320 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge(ConvArgs a, const f
                 atomicAdd(g, gx);
                 atomicAdd(g + 1, gy);
                 atomicAdd(g + 2, gz);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double acc6 = 0.0;
+        for (int g = 0; g < kNodesPerCta; ++g) acc6 += sVir[g][threadIdx.x];
+        vir_part[(size_t)blockIdx.x * 6 + threadIdx.x] = acc6;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Packed-FP32 (FFMA2) conv and backward edge pass.
+//
+// sm_100a issues FFMA2 / FMUL2: two IEEE fp32 FMAs per instruction with a
+// scalar operand broadcast to both halves and a constant pair from a uniform
+// register (LDCU.128 loads two pairs).  The FMA pipe still does 32 lanes per
+// cycle, so FFMA2 halves issue slots, not FMA cycles; the model kernels were
+// issue-bound (FFMA + LDCU), so packing moves them toward the FMA-pipe bound.
+// Feature pairs (f, f+1) are packed: A_(f,f+1) = sum_k (P[f][k], P[f+1][k]) phi_k
+// uses the k-major copy PT; G_(k,k+1) = sum_f (P[f][k], P[f][k+1]) g_f uses P.
+// Each lane keeps one edge's gathered rows in flight while it computes the
+// previous one (software pipeline across the node's in-edges).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 bcast(float x) { return make_float2(x, x); }
+
+// A[i] = (A_2i, A_2i+1), A_f = sum_k P[f][k] ph[k], summed in ascending k
+__device__ __forceinline__ void radial_pairs(const float ph[kK], float2 A[kF / 2]) {
+    const float2* PT2 = reinterpret_cast<const float2*>(c_m.PT);
+#pragma unroll
+    for (int i = 0; i < kF / 2; ++i) A[i] = f2fma(PT2[i], bcast(ph[0]), make_float2(0.f, 0.f));
+#pragma unroll
+    for (int k = 1; k < kK; ++k)
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) A[i] = f2fma(PT2[k * (kF / 2) + i], bcast(ph[k]), A[i]);
+}
+
+struct ConvIn {
+    float d;
+    float4 h[4];
+};
+
+// gathered row of edge e whose source row w was loaded one step earlier
+__device__ __forceinline__ void conv_load(const ConvArgs& a, const float* __restrict__ Hin, int e,
+                                          int w, ConvIn& x) {
+    x.d = __ldg(a.d + e);
+    const float* hrow = Hin + (size_t)w * kF;
+    ldg256(hrow, x.h[0], x.h[1]);
+    ldg256(hrow + 8, x.h[2], x.h[3]);
+}
+__device__ __forceinline__ int src_of(const ConvArgs& a, int e, int e1) {
+    return e < e1 ? __ldg(a.lsrc + e) : 0;
+}
+
+// same arithmetic, per feature and in the same order, as conv_edge
+__device__ __forceinline__ void conv_math2(const ConvIn& x, float2 acc[kF / 2]) {
+    float phi[kK];
+    phi_fast(x.d, phi);
+    const float fc = fc_fast(x.d);
+    float2 A[kF / 2];
+    radial_pairs(phi, A);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float4 h4 = x.h[c];
+        const float2 h0 = f2mul(make_float2(h4.x, h4.y), bcast(fc));
+        const float2 h1 = f2mul(make_float2(h4.z, h4.w), bcast(fc));
+        acc[2 * c] = f2fma(h0, A[2 * c], acc[2 * c]);
+        acc[2 * c + 1] = f2fma(h1, A[2 * c + 1], acc[2 * c + 1]);
+    }
+}
+
+template <int CTAS>
+__global__ void __launch_bounds__(kThreads, CTAS) k_conv2(ConvArgs a, int layer,
+                                                       const float* __restrict__ Hin,
+                                                       float* __restrict__ Hout,
+                                                       float* __restrict__ TH, double* per_atom,
+                                                       double* e_part) {
+    __shared__ float sW[kF][kF + 1];
+    __shared__ float sb[kF], sro[kF];
+    for (int i = threadIdx.x; i < kF * kF; i += kThreads) sW[i / kF][i % kF] = c_m.W[layer][i];
+    if (threadIdx.x < kF) {
+        sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
+        sro[threadIdx.x] = c_m.ro[threadIdx.x];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & 15;
+    const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + (threadIdx.x >> 4);
+    const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
+    double esum = 0.0;
+    const int64_t iters = (a.n + ng - 1) / ng;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t k = g0 + it * ng;
+        const bool valid = k < a.n;
+        const int64_t v = valid ? (a.nodes ? (int64_t)a.nodes[k] : k) : 0;
+        float2 acc[kF / 2];
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) acc[i] = make_float2(0.f, 0.f);
+        const int e0 = valid ? __ldg(a.row + v) : 0;
+        const int e1 = valid ? __ldg(a.row + v + 1) : 0;
+        // one edge per lane in flight; its source index is read one slot ahead
+        ConvIn x;
+        int w = src_of(a, e0 + gl, e1);
+        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
+            if (e < e1) {
+                conv_load(a, Hin, e, w, x);
+                w = src_of(a, e + 16, e1);
+                conv_math2(x, acc);
+            }
+        }
+        float accf[kF];
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) {
+            accf[2 * i] = acc[i].x;
+            accf[2 * i + 1] = acc[i].y;
+        }
+        const float m = transpose_reduce16_g16(accf, gl);  // feature gl
+        float z = sb[gl];
+#pragma unroll
+        for (int g = 0; g < kF; ++g)
+            z = fmaf(sW[gl][g], __shfl_sync(0xffffffffu, m, (lane & 16) + g), z);
+        const float th = tanhf(z);
+        float ev = 0.0f;
+        if (valid) {
+            const int64_t r = a.crow ? a.crow[v] : v;
+            const float hn = Hin[r * kF + gl] + th;
+            Hout[r * kF + gl] = hn;
+            TH[k * kF + gl] = th;
+            ev = sro[gl] * hn;
+        }
+        if (per_atom) {
+            ev = group_sum16(ev);
+            if (valid && gl == 0) {
+                per_atom[v] = (double)ev;
+                esum += (double)ev;
+            }
+        }
+    }
+    if (e_part) {
+        double vals[1] = {esum};
+        cta_partials<1>(vals, e_part);
+    }
+}
+
+// Backward per edge e = (w -> u) in the "dsum" form (potential.cpp:823-848):
+//   ds_f = sum_k P_fk psi_k,  psi_k = phi_k (ca + cb k)     (u'_k restated)
+//   dbar_e + dbar_rev(e) = sum_f (mbar_u,f h_w,f + h_u,f mbar_w,f) ds_f
+//                        = sum_k psi_k G_k,  G = P^T g  (128 FMA, not 2 x 128)
+// grad_u -= v_e (dbar_e + dbar_rev)/d_e as before; the virial takes half of
+// the pair sum per edge: the reverse edge has the same v (x) v and d, so
+// sum_e dbar_e v v^T / d = 1/2 sum_e (dbar_e + dbar_rev(e)) v v^T / d over any
+// edge set closed under reversal (all edges, or all in-edges of the atoms a
+// rank owns, summed over ranks).
+__device__ __forceinline__ void bwd_load2(const ConvArgs& a, const float* __restrict__ MB,
+                                          const float* __restrict__ Hl, int e, int w, BwdEdgeIn& x) {
+    x.q = __ldg(a.vd + e);
+    const float* mw = MB + (size_t)w * kF;
+    const float* hw = Hl + (size_t)w * kF;
+    ldg256(mw, x.m[0], x.m[1]);
+    ldg256(mw + 8, x.m[2], x.m[3]);
+    ldg256(hw, x.h[0], x.h[1]);
+    ldg256(hw + 8, x.h[2], x.h[3]);
+}
+
+__device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m,
+                                          const float4* su_h, float isg, float mus,
+                                          float2 acc[kF / 2], float& gx, float& gy, float& gz,
+                                          float vr[6]) {
+    const float4 q = x.q;
+    float fc, dfc;
+    fc_dfc_fast(q.w, fc, dfc);
+    float phi[kK];
+    phi_fast(q.w, phi);
+    const float x0 = q.w * isg, step = mus * isg;
+    const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
+    // g_f = mbar_u,f h_w,f + h_u,f mbar_w,f
+    float g[kF];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float4 mu4 = su_m[c], hu4 = su_h[c];
+        const float2 ga = f2fma(make_float2(hu4.x, hu4.y), make_float2(x.m[c].x, x.m[c].y),
+                                f2mul(make_float2(mu4.x, mu4.y), make_float2(x.h[c].x, x.h[c].y)));
+        const float2 gb = f2fma(make_float2(hu4.z, hu4.w), make_float2(x.m[c].z, x.m[c].w),
+                                f2mul(make_float2(mu4.z, mu4.w), make_float2(x.h[c].z, x.h[c].w)));
+        g[4 * c] = ga.x;
+        g[4 * c + 1] = ga.y;
+        g[4 * c + 2] = gb.x;
+        g[4 * c + 3] = gb.y;
+    }
+    // G_(2j, 2j+1) = sum_f (P[f][2j], P[f][2j+1]) g_f
+    const float2* P2 = reinterpret_cast<const float2*>(c_m.P);
+    float2 G[kK / 2];
+#pragma unroll
+    for (int j = 0; j < kK / 2; ++j) G[j] = f2fma(P2[j], bcast(g[0]), make_float2(0.f, 0.f));
+#pragma unroll
+    for (int f = 1; f < kF; ++f)
+#pragma unroll
+        for (int j = 0; j < kK / 2; ++j) G[j] = f2fma(P2[f * (kK / 2) + j], bcast(g[f]), G[j]);
+    // dsum = sum_k phi_k (ca + cb k) G_k
+    float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < kK / 2; ++j) {
+        const float2 ck = f2fma(bcast(cb), make_float2((float)(2 * j), (float)(2 * j + 1)), bcast(ca));
+        s2 = f2fma(f2mul(make_float2(phi[2 * j], phi[2 * j + 1]), ck), G[j], s2);
+    }
+    const float dsum = s2.x + s2.y;
+    // hbar_u += mbar_w (.) s_e, s = fc P phi
+    float php[kK];
+#pragma unroll
+    for (int k = 0; k < kK; ++k) php[k] = fc * phi[k];
+    float2 A[kF / 2];
+    radial_pairs(php, A);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        acc[2 * c] = f2fma(make_float2(x.m[c].x, x.m[c].y), A[2 * c], acc[2 * c]);
+        acc[2 * c + 1] = f2fma(make_float2(x.m[c].z, x.m[c].w), A[2 * c + 1], acc[2 * c + 1]);
+    }
+    const float coef = dsum / q.w;
+    gx = fmaf(-q.x, coef, gx);
+    gy = fmaf(-q.y, coef, gy);
+    gz = fmaf(-q.z, coef, gz);
+    const float ch = 0.5f * coef;
+    vr[0] = fmaf(ch * q.x, q.x, vr[0]);
+    vr[1] = fmaf(ch * q.y, q.y, vr[1]);
+    vr[2] = fmaf(ch * q.z, q.z, vr[2]);
+    vr[3] = fmaf(ch * q.x, q.y, vr[3]);
+    vr[4] = fmaf(ch * q.x, q.z, vr[4]);
+    vr[5] = fmaf(ch * q.y, q.z, vr[5]);
+}
+
+template <int CTAS>
+__global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
+                                                           const float* __restrict__ Hl,
+                                                           float* __restrict__ HB,
+                                                           float4* __restrict__ GRAD,
+                                                           double* vir_part) {
+    __shared__ __align__(16) float sU[kNodesPerCta][2][kF];  // [group][m_bar_u, h_u][f]
+    __shared__ double sVir[kNodesPerCta][6];
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & 15, grp = threadIdx.x >> 4;
+    const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + grp;
+    const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
+    const float isg = c_m.inv_sigma, mus = c_m.mu_step;
+    if (gl < 6) sVir[grp][gl] = 0.0;
+    const int64_t iters = (a.n + ng - 1) / ng;
+    int e0n = 0, e1n = 0;
+    float mun = 0.f, hun = 0.f;
+    BwdEdgeIn xa;
+    int wa = 0;
+    // node k's row bounds, own rows and first source index are loaded while
+    // the previous node finishes
+    auto prefetch = [&](int64_t k) {
+        if (k < a.n) {
+            const int64_t v = a.nodes ? (int64_t)a.nodes[k] : k;
+            const int64_t r = a.crow ? a.crow[v] : v;
+            e0n = __ldg(a.row + v);
+            e1n = __ldg(a.row + v + 1);
+            mun = __ldg(MB + r * kF + gl);
+            hun = __ldg(Hl + r * kF + gl);
+            wa = src_of(a, e0n + gl, e1n);
+        } else {
+            e0n = e1n = 0;
+        }
+    };
+    prefetch(g0);
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t k = g0 + it * ng;
+        const bool valid = k < a.n;
+        const int e0 = e0n, e1 = e1n;
+        __syncwarp();
+        if (valid) {
+            sU[grp][0][gl] = mun;
+            sU[grp][1][gl] = hun;
+        }
+        __syncwarp();
+        float2 acc[kF / 2];
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) acc[i] = make_float2(0.f, 0.f);
+        float gx = 0.f, gy = 0.f, gz = 0.f;
+        float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
+        const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
+        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
+            if (e < e1) {
+                bwd_load2(a, MB, Hl, e, wa, xa);
+                wa = src_of(a, e + 16, e1);
+                bwd_math2(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
+            }
+        }
+        prefetch(k + ng);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
+        if (gl == 0)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) sVir[grp][c] += (double)vr[c];
+        float accf[kF];
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) {
+            accf[2 * i] = acc[i].x;
+            accf[2 * i + 1] = acc[i].y;
+        }
+        const float hb = transpose_reduce16_g16(accf, gl);
+        gx = group_sum16(gx);
+        gy = group_sum16(gy);
+        gz = group_sum16(gz);
+        if (valid) {  // one adder per element: red.add is the plain read-add-write
+            atomicAdd(HB + k * kF + gl, hb);
+            if (gl == 0) {
+                float* gp = reinterpret_cast<float*>(GRAD + k);
+                atomicAdd(gp, gx);
+                atomicAdd(gp + 1, gy);
+                atomicAdd(gp + 2, gz);
             }
         }
     }
@@ -1191,7 +1494,13 @@ void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float
 void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
                  double* per_atom, double* e_part, cudaStream_t s) {
     if (a.n == 0) return;
-    k_conv<<<model_grid(a.n), kThreads, 0, s>>>(a, layer, Hin, Hout, TH, per_atom, e_part);
+    const char* venv = std::getenv("GMD_CONV_VARIANT");  // read per call (tests switch kernels)
+    const int variant = venv ? std::atoi(venv) : 0;
+    const int g = model_grid(a.n);
+    if (variant == 1)  // scalar-FFMA kernel (A/B reference)
+        k_conv<<<g, kThreads, 0, s>>>(a, layer, Hin, Hout, TH, per_atom, e_part);
+    else
+        k_conv2<3><<<g, kThreads, 0, s>>>(a, layer, Hin, Hout, TH, per_atom, e_part);
     GMD_LAUNCH_CHECK();
 }
 
@@ -1205,17 +1514,13 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
                      double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
-    static const int variant = [] {
-        const char* v = std::getenv("GMD_BWD_VARIANT");
-        return v ? std::atoi(v) : 0;
-    }();
+    const char* venv = std::getenv("GMD_BWD_VARIANT");  // read per call (tests switch kernels)
+    const int variant = venv ? std::atoi(venv) : 0;
     const int g = model_grid(a.n);
-    switch (variant) {
-        case 1: k_bwd_edge<3, 1><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
-        case 2: k_bwd_edge<2, 1><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
-        case 3: k_bwd_edge<3, 2><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
-        default: k_bwd_edge<2, 2><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part); break;
-    }
+    if (variant == 1)  // scalar-FFMA kernel (A/B reference)
+        k_bwd_edge<<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+    else
+        k_bwd_edge2<3><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
     GMD_LAUNCH_CHECK();
 }
 

@@ -15,8 +15,9 @@ struct ModelConst {
     float emb[119 * kF];
     float W[kMaxLayers][kF * kF];
     float b[kMaxLayers][kF];
-    float P[kF * kK];
-    float Pk[kF * kK];  // k * P[f][k] (derivative of the radial channel)
+    alignas(16) float P[kF * kK];   // f-major: (P[f][k], P[f][k+1]) pairs
+    alignas(16) float PT[kK * kF];  // k-major: (P[f][k], P[f+1][k]) pairs
+    alignas(16) float Pk[kF * kK];  // k * P[f][k] (derivative of the radial channel)
     float P3[kF * kK];
     float W3[kF * kF];
     float W4[kF * kF];

@@ -116,6 +116,17 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
                  "l"(gmem_src)
                  : "memory");
 }
+// L1-allocating variant (.ca): gathered neighbour rows are reused by nearby
+// destination atoms
+__device__ __forceinline__ void cp_async16_ca(void* smem_dst, const void* gmem_src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)),
+                 "l"(gmem_src)
+                 : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }

@@ -14,16 +14,17 @@ import pytest
 
 from paper_2506_02023_b200 import graphmd as G
 from tests import systems as S
+from tests.conftest import KERNELS, use_kernels
 
 pytestmark = pytest.mark.gpu
 
 TOL_EA, TOL_E, TOL_F, TOL_FREL, TOL_S = 2e-5, 2e-6, 2e-4, 2e-5, 2e-6
 
 
-@pytest.fixture(params=["ffma", "tcgen05"], autouse=True)
-def bwd_kernel(request, monkeypatch):
-    """Every test runs with both backward edge kernels (GMD_BWD_TC, read per call)."""
-    monkeypatch.setenv("GMD_BWD_TC", "1" if request.param == "tcgen05" else "0")
+@pytest.fixture(params=list(KERNELS), autouse=True)
+def kernels(request, monkeypatch):
+    """Every test runs with every kernel family (environment switches read per call)."""
+    use_kernels(monkeypatch, request.param)
     return request.param
 
 
@@ -134,13 +135,18 @@ def test_cutoff_mismatch_error():
         G.forward_distributed(d, params_for(1, 2, 4.0, 3.0))
 
 
-def test_tc_matches_ffma_backward(monkeypatch):
+@pytest.mark.parametrize("other", ["tcgen05", "ffma"])
+def test_kernel_families_agree(monkeypatch, other):
+    """The default packed kernels against the scalar-FFMA and tcgen05 paths."""
     s = S.quartz((4, 4, 4))
     prm = params_for(11, 3, 5.0)
-    monkeypatch.setenv("GMD_BWD_TC", "0")
+    use_kernels(monkeypatch, "ffma2")
     a = run_gpu(s, prm, p=2)
-    monkeypatch.setenv("GMD_BWD_TC", "1")
+    use_kernels(monkeypatch, other)
     b = run_gpu(s, prm, p=2)
-    assert a.energy == b.energy  # forward is shared
+    if other == "tcgen05":
+        assert a.energy == b.energy  # forward is shared
+    else:  # same per-feature operations in the same order
+        np.testing.assert_array_equal(b.per_atom, a.per_atom)
     np.testing.assert_allclose(b.forces, a.forces, rtol=0, atol=2e-5 * np.abs(a.forces).max())
     np.testing.assert_allclose(b.stress, a.stress, rtol=0, atol=1e-6)

@@ -8,6 +8,7 @@ import pytest
 
 from paper_2506_02023_b200 import graphmd as G
 from tests import systems as S
+from tests.conftest import use_kernels
 
 pytestmark = pytest.mark.gpu
 
@@ -25,11 +26,11 @@ def run_group(s, prm, W, r3=None):
     return G.run_ranks([rank(r) for r in range(W)])
 
 
-@pytest.mark.parametrize("bwd_tc", ["0", "1"])
+@pytest.mark.parametrize("kern", ["ffma2", "ffma", "tcgen05"])
 @pytest.mark.parametrize("W", [2, 3, 4])
 @pytest.mark.parametrize("which", ["quartz", "gas"])
-def test_rank_group_equals_single_handle(W, which, bwd_tc, monkeypatch):
-    monkeypatch.setenv("GMD_BWD_TC", bwd_tc)
+def test_rank_group_equals_single_handle(W, which, kern, monkeypatch):
+    use_kernels(monkeypatch, kern)
     s = S.quartz((4, 4, 4)) if which == "quartz" else S.random_gas(600, 5)
     prm = G.ToyPotentialParams.init(11, 16, 8, 3, 4.0)
     ref_d = G.Distributed.create_distributed(s, 4.0, None, W, 1, True)
@@ -69,12 +70,14 @@ def test_rank_group_rejects_mismatch():
 
 
 @pytest.mark.parametrize("W", [2, 3, 4])
+@pytest.mark.parametrize("kern", ["ffma2", "ffma"])
 @pytest.mark.parametrize("which", ["quartz", "liquid"])
-def test_rank_group_three_body(W, which):
+def test_rank_group_three_body(W, which, kern, monkeypatch):
     """Three-body graphs one rank per GPU: t' / v_bar rows of reverse bonds whose
     center lives on a peer travel through the bond halo plan; q_bar halo rows
     through the atom plan.  Owned atoms' energies and forces are bitwise equal
     to the single-handle result."""
+    use_kernels(monkeypatch, kern)
     s = S.quartz((4, 4, 4)) if which == "quartz" else S.liquid(1200)
     prm = G.ToyPotentialParams.init(7, 16, 8, 3, 5.0, 3.0)
     ref_d = G.Distributed.create_distributed(s, 5.0, 3.0, W, 1, True)
