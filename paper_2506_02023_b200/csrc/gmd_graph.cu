@@ -10,6 +10,9 @@
 // in the reference's operand order.  Two passes: count
 // (-> CSR row offsets) and fill (per-destination warp bitonic sort by
 // (src, image) so rows come out in canonical order, neighborlist.cpp:21-24).
+#include <algorithm>
+#include <cstdlib>
+
 #include "gmd_graph.cuh"
 
 namespace gmd {
@@ -122,10 +125,18 @@ struct CandW {
     double p[3][32];  // raw position of j
     int nc[3][32];    // q - cell_of[j]
     int jid[32];
-    unsigned qc[32];
+    unsigned cell[32];  // global stencil-cell index of the candidate
 };
 
 constexpr int kWSCap = 32;  // stencil cells per batch (per warp)
+constexpr int kQCap = 256;  // queued exact tests per round (per warp)
+constexpr int kCodeCap = 128;  // stencil cells whose q code is tabulated
+// Row keys in shared memory are 32-bit: src << cbits | stencil-cell index.  For a
+// fixed src every stencil cell maps to a distinct image, and the image q is
+// monotone in the cell offset per axis, so (src, cell) order is the
+// canonical (src, image) order; the 64-bit slab key (src << 24 | q code) is
+// rebuilt from the cell index on output.
+// The cell field is cbits = ceil(log2(#stencil cells)) wide (launch_nl_search).
 
 struct WarpNL {             // per-warp shared state of the search
     int sc_bin[kWSCap];
@@ -133,8 +144,46 @@ struct WarpNL {             // per-warp shared state of the search
     int sc_q[kWSCap][3];
     double sc_shift[kWSCap][3];
     CandW cand;
-    unsigned short queue[64];
+    unsigned short queue[kQCap];  // (candidate lane, destination) pairs
+    uint32_t code[kCodeCap];      // image q code per stencil cell of the bin
 };
+
+// Warp bitonic sorting networks (ascending) on unique 32-bit keys; padding
+// slots hold ~0 and sort last.
+__device__ __forceinline__ uint32_t cmpx(uint32_t a, uint32_t b, bool keep_min) {
+    return (keep_min == (a < b)) ? a : b;
+}
+__device__ __forceinline__ uint32_t bitonic32(uint32_t k, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, k, stride);
+            const bool asc = (lane & size) == 0, lower = (lane & stride) == 0;
+            k = cmpx(k, o, asc == lower);
+        }
+    return k;
+}
+// 64 keys: element lane in k0, element lane + 32 in k1
+__device__ __forceinline__ void bitonic64(uint32_t& k0, uint32_t& k1, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 64; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride == 32) {  // partner is the other register of this lane
+                const uint32_t lo = min(k0, k1), hi = max(k0, k1);
+                k0 = lo;  // size == 64: ascending
+                k1 = hi;
+            } else {
+                const uint32_t o0 = __shfl_xor_sync(0xffffffffu, k0, stride);
+                const uint32_t o1 = __shfl_xor_sync(0xffffffffu, k1, stride);
+                const bool lower = (lane & stride) == 0;
+                const bool asc0 = (lane & size) == 0, asc1 = ((lane + 32) & size) == 0;
+                k0 = cmpx(k0, o0, asc0 == lower);
+                k1 = cmpx(k1, o1, asc1 == lower);
+            }
+        }
+}
 
 // Search, one WARP per destination bin (no CTA barriers).  Shared memory per
 // warp: WarpNL + the destination group (<= group atoms) + group x cap keys.
@@ -143,13 +192,14 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
     const int32_t* __restrict__ bin_start, const int32_t* __restrict__ s_id,
     const double* __restrict__ s_w, const double* __restrict__ s_p,
     const int32_t* __restrict__ s_c, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
-    unsigned long long* __restrict__ slab, const int32_t* __restrict__ owner, int only) {
+    unsigned long long* __restrict__ slab, const int32_t* __restrict__ owner, int only,
+    int cbits) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp carve-up by byte offsets (keeps the shared address space)
     const size_t head = (sizeof(WarpNL) + 15) & ~(size_t)15;
     const size_t dst_bytes = (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
-    const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
+    const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 4;
     unsigned char* base = smem_raw + (size_t)warp * per_warp;
     WarpNL& S = *reinterpret_cast<WarpNL*>(base);
     CandW& C = S.cand;
@@ -168,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
     int* d_cnt = reinterpret_cast<int*>(base + o);
     o += sizeof(int) * group;
     o = (o + 15) & ~(size_t)15;
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(base + o);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(base + o);
 
     const int sx = 2 * g.sten[0] + 1, sy = 2 * g.sten[1] + 1, sz = 2 * g.sten[2] + 1;
     const int ncell = sx * sy * sz;
@@ -232,6 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                         cwb[k] = cc[k] - qv[k] * nb;
                         S.sc_q[lane][k] = qv[k];
                     }
+                    if (cbase + lane < kCodeCap) S.code[cbase + lane] = qcode(qv[0], qv[1], qv[2]);
                     // shift = L0*q0 + L1*q1 + L2*q2 (neighborlist.cpp:171-173)
                     const d3 sh = rowvec_rn(g.L, (double)qv[0], (double)qv[1], (double)qv[2]);
                     S.sc_shift[lane][0] = sh.x;
@@ -276,80 +327,117 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                             C.nc[d][lane] = S.sc_q[ci][d] - s_c[d * n + slot];
                         }
                         C.jid[lane] = s_id[slot];
-                        C.qc[lane] = qcode(S.sc_q[ci][0], S.sc_q[ci][1], S.sc_q[ci][2]);
+                        C.cell[lane] = (unsigned)(cbase + ci);
                         c32x = (float)(cv[0] - org.x);
                         c32y = (float)(cv[1] - org.y);
                         c32z = (float)(cv[2] - org.z);
                     }
-                    __syncwarp();
-                    int qn = 0;
-                    // exact fp64 tests of `cnt` queued (candidate, destination) pairs
-                    auto drain = [&](int cnt) {
-                        if (lane < cnt) {
-                            const unsigned ent = Q[lane];
-                            const int c = ent & 31, t = ent >> 5;
-                            const d3 v = {sub_rn(C.c[0][c], d_w[3 * t]),
-                                          sub_rn(C.c[1][c], d_w[3 * t + 1]),
-                                          sub_rn(C.c[2][c], d_w[3 * t + 2])};
-                            if (!(dot_rn(v, v) > g.pre2)) {  // neighborlist.cpp:177
-                                const int o0 = C.nc[0][c] + d_c[3 * t];
-                                const int o1 = C.nc[1][c] + d_c[3 * t + 1];
-                                const int o2 = C.nc[2][c] + d_c[3 * t + 2];
-                                const d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
-                                const d3 vr = {add_rn(sub_rn(C.p[0][c], d_p[3 * t]), raw.x),
-                                               add_rn(sub_rn(C.p[1][c], d_p[3 * t + 1]), raw.y),
-                                               add_rn(sub_rn(C.p[2][c], d_p[3 * t + 2]), raw.z)};
-                                const double d2 = dot_rn(vr, vr);
-                                if (!(d2 > g.cutoff2) && d2 != 0.0) {  // :189-190
-                                    const int pos = atomicAdd(&d_cnt[t], 1);
-                                    if (pos < cap)
-                                        keys[(size_t)t * cap + pos] =
-                                            ((unsigned long long)(uint32_t)C.jid[c] << 24) | C.qc[c];
+                    // fp32 prefilter of this lane's candidate against every
+                    // destination of the group -> bitmask of survivors
+                    unsigned mask = 0u;
+                    if (valid) {
+                        for (int t = 0; t < nd; ++t) {
+                            const float4 dd = d32[t];
+                            const float vx = c32x - dd.x, vy = c32y - dd.y, vz = c32z - dd.z;
+                            if (fmaf(vz, vz, fmaf(vy, vy, vx * vx)) <= thr32) mask |= 1u << t;
+                        }
+                    }
+                    // warp-wide compaction of the surviving (candidate, destination)
+                    // pairs, kQCap per round, then exact fp64 tests 32 at a time
+                    // (no divergence in the fp64 path)
+                    while (__any_sync(0xffffffffu, mask != 0u)) {
+                        const int mine = __popc(mask);
+                        int off = mine;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int u = __shfl_up_sync(0xffffffffu, off, o);
+                            if (lane >= o) off += u;
+                        }
+                        const int total = min(__shfl_sync(0xffffffffu, off, 31), kQCap);
+                        off -= mine;
+                        while (mask && off < kQCap) {
+                            const int t = __ffs(mask) - 1;
+                            mask &= mask - 1u;
+                            Q[off++] = (unsigned short)(lane | (t << 5));
+                        }
+                        __syncwarp();
+                        for (int q0 = 0; q0 < total; q0 += 32) {
+                            if (q0 + lane < total) {
+                                const unsigned ent = Q[q0 + lane];
+                                const int c = ent & 31, t = ent >> 5;
+                                const d3 v = {sub_rn(C.c[0][c], d_w[3 * t]),
+                                              sub_rn(C.c[1][c], d_w[3 * t + 1]),
+                                              sub_rn(C.c[2][c], d_w[3 * t + 2])};
+                                if (!(dot_rn(v, v) > g.pre2)) {  // neighborlist.cpp:177
+                                    const int o0 = C.nc[0][c] + d_c[3 * t];
+                                    const int o1 = C.nc[1][c] + d_c[3 * t + 1];
+                                    const int o2 = C.nc[2][c] + d_c[3 * t + 2];
+                                    const d3 raw =
+                                        rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
+                                    const d3 vr = {add_rn(sub_rn(C.p[0][c], d_p[3 * t]), raw.x),
+                                                   add_rn(sub_rn(C.p[1][c], d_p[3 * t + 1]), raw.y),
+                                                   add_rn(sub_rn(C.p[2][c], d_p[3 * t + 2]), raw.z)};
+                                    const double d2 = dot_rn(vr, vr);
+                                    if (!(d2 > g.cutoff2) && d2 != 0.0) {  // :189-190
+                                        const int pos = atomicAdd(&d_cnt[t], 1);
+                                        if (pos < cap)
+                                            keys[(size_t)t * cap + pos] =
+                                                ((uint32_t)C.jid[c] << cbits) | C.cell[c];
+                                    }
                                 }
                             }
                         }
-                    };
-                    for (int t = 0; t < nd; ++t) {
-                        const float4 dd = d32[t];
-                        const float vx = c32x - dd.x, vy = c32y - dd.y, vz = c32z - dd.z;
-                        const bool pass = valid && fmaf(vz, vz, fmaf(vy, vy, vx * vx)) <= thr32;
-                        const unsigned m = __ballot_sync(0xffffffffu, pass);
-                        if (m == 0u) continue;
-                        if (pass) Q[qn + __popc(m & ((1u << lane) - 1u))] = (unsigned short)(lane | (t << 5));
-                        qn += __popc(m);
                         __syncwarp();
-                        if (qn >= 32) {
-                            drain(32);
-                            __syncwarp();
-                            const unsigned short mv = lane < qn - 32 ? Q[32 + lane] : 0;
-                            __syncwarp();
-                            if (lane < qn - 32) Q[lane] = mv;
-                            qn -= 32;
-                            __syncwarp();
-                        }
                     }
-                    drain(qn);
                     __syncwarp();
                 }
             }
-            // canonical (src, image) order by rank (keys are unique), then store
+            // canonical (src, image) order (neighborlist.cpp:21-24): warp bitonic
+            // network for rows of <= 64 keys (keys are unique), rank sort above
+            // slab key of a sorted row entry: src << 24 | code of the image of
+            // its stencil cell (neighborlist.cpp:165-170)
+            auto slab_key = [&](uint32_t k) {
+                const int c = (int)(k & ((1u << cbits) - 1u));
+                if (c < kCodeCap) return ((unsigned long long)(k >> cbits) << 24) | S.code[c];
+                const int cc[3] = {bx + c / (sz * sy) - g.sten[0], by + (c / sz) % sy - g.sten[1],
+                                   bz + c % sz - g.sten[2]};
+                int qv[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const int nb = g.bins[a];
+                    qv[a] = cc[a] >= 0 ? cc[a] / nb : -((-cc[a] + nb - 1) / nb);
+                }
+                return ((unsigned long long)(k >> cbits) << 24) | qcode(qv[0], qv[1], qv[2]);
+            };
             for (int t = 0; t < nd; ++t) {
                 const int full = d_cnt[t];
                 const int cnt = min(full, cap);
-                const unsigned long long* kk = keys + (size_t)t * cap;
+                const uint32_t* kk = keys + (size_t)t * cap;
                 unsigned long long* dst = slab + (size_t)d_id[t] * cap;
-                for (int k0 = 0; k0 < cnt; k0 += 64) {
-                    const int ka = k0 + lane, kb2 = k0 + 32 + lane;
-                    const unsigned long long ma = ka < cnt ? kk[ka] : ~0ull;
-                    const unsigned long long mb = kb2 < cnt ? kk[kb2] : ~0ull;
-                    int ra = 0, rb = 0;
-                    for (int i = 0; i < cnt; ++i) {
-                        const unsigned long long x = kk[i];
-                        ra += x < ma;
-                        rb += x < mb;
+                if (cnt <= 64) {
+                    uint32_t k0 = lane < cnt ? kk[lane] : ~0u;
+                    uint32_t k1 = lane + 32 < cnt ? kk[lane + 32] : ~0u;
+                    if (cnt <= 32) {
+                        k0 = bitonic32(k0, lane);
+                    } else {
+                        bitonic64(k0, k1, lane);
+                        if (lane + 32 < cnt) dst[lane + 32] = slab_key(k1);
                     }
-                    if (ka < cnt) dst[ra] = ma;
-                    if (kb2 < cnt) dst[rb] = mb;
+                    if (lane < cnt) dst[lane] = slab_key(k0);
+                } else {
+                    for (int k0 = 0; k0 < cnt; k0 += 64) {
+                        const int ka = k0 + lane, kb2 = k0 + 32 + lane;
+                        const uint32_t ma = ka < cnt ? kk[ka] : ~0u;
+                        const uint32_t mb = kb2 < cnt ? kk[kb2] : ~0u;
+                        int ra = 0, rb = 0;
+                        for (int i = 0; i < cnt; ++i) {
+                            const uint32_t x = kk[i];
+                            ra += x < ma;
+                            rb += x < mb;
+                        }
+                        if (ka < cnt) dst[ra] = slab_key(ma);
+                        if (kb2 < cnt) dst[rb] = slab_key(mb);
+                    }
                 }
                 if (lane == 0) {
                     deg[d_id[t]] = full;
@@ -535,7 +623,7 @@ __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
 size_t nl_smem(int group, int cap) {
     const size_t head = (sizeof(WarpNL) + 15) & ~(size_t)15;
     const size_t dst_bytes = (size_t)group * (16 + 24 + 24 + 12 + 4 + 4);
-    const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 8;
+    const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 4;
     return per_warp * kWarps;
 }
 
@@ -561,7 +649,14 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
 void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s) {
-    int group = 16;
+    // destinations staged per warp: as many as fit three CTAs per SM (the
+    // search is latency-bound; occupancy beats fewer candidate rescans)
+    static const int gmax = [] {
+        const char* v = std::getenv("GMD_NL_GROUP");
+        return v ? std::max(1, std::min(32, std::atoi(v))) : 16;
+    }();
+    int group = gmax;
+    while (group > 4 && nl_smem(group, cap) > 74 * 1024) --group;
     while (group > 1 && nl_smem(group, cap) > 110 * 1024) group >>= 1;
     const size_t sm = nl_smem(group, cap);
     if (sm > 200 * 1024) raise(kRuntime, "neighbour search: per-atom degree too large");
@@ -571,9 +666,15 @@ void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int 
                                       200 * 1024));
         attr = true;
     }
+    const int64_t ncell = (int64_t)(2 * g.sten[0] + 1) * (2 * g.sten[1] + 1) * (2 * g.sten[2] + 1);
+    int cbits = 1;
+    while (((int64_t)1 << cbits) < ncell) ++cbits;
+    if (cbits > 31 || n > ((int64_t)1 << (32 - cbits)))
+        raise(kConfig, "neighbour search: atom count too large for the " + std::to_string(ncell) +
+                           "-cell stencil (row keys are src << " + std::to_string(cbits) + " | cell)");
     k_nl_search<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, nbins, n, group, cap, b.bin_start,
                                                      b.s_id, b.s_w, b.s_p, b.s_c, b.deg, b.flags,
-                                                     slab, owner, only);
+                                                     slab, owner, only, cbits);
     GMD_LAUNCH_CHECK();
 }
 
