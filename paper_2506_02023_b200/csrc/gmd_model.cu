@@ -1463,9 +1463,16 @@ __global__ void __launch_bounds__(512) k_reduce_partials(const double* parts, in
 
 }  // namespace
 
+// One wave of the 3-CTA/SM model kernels: all resident CTAs sweep the node
+// range together, so the gathered neighbour rows of the active window stay in
+// L2 (C5: 1776 CTAs 7.50 ms/step, 888 7.38, 444 7.26, 296 8.35).
 int model_grid(int64_t n) {
+    static const int cap = [] {
+        const char* v = std::getenv("GMD_MODEL_GRID");
+        return v ? std::atoi(v) : 148 * 3;
+    }();
     int64_t g = (n + kNodesPerCta - 1) / kNodesPerCta;
-    if (g > 148 * 12) g = 148 * 12;
+    if (g > cap) g = cap;
     return (int)(g > 0 ? g : 1);
 }
 
