@@ -69,6 +69,11 @@ def bytes_model(n, ne, nb, L, threebody):
     }
 
 
+# profiler label (gmd_profile) -> CUDA kernel of the default path
+KERNEL_OF = {"bwd_edge": "k_bwd_edge2", "conv": "k_conv2", "nl_search": "k_nl_search",
+             "nl_emit": "k_nl_emit", "bwd_node": "k_bwd_node"}
+
+
 def ncu_traffic(config, kname):
     """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kname`
     from the committed `ncu --set full` capture of this config (profiles/)."""
@@ -76,7 +81,7 @@ def ncu_traffic(config, kname):
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{config}.json")), reverse=True):
         try:
             with open(path) as f:
-                m = json.load(f).get("k_" + kname)
+                m = json.load(f).get(KERNEL_OF.get(kname, "k_" + kname))
             if m and m.get("dram_bytes"):
                 return m["dram_bytes"], os.path.relpath(path, ROOT)
         except (OSError, ValueError):

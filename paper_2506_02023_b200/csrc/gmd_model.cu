@@ -1415,10 +1415,15 @@ __global__ void k_tb_grad(BondArgs a, const float4* __restrict__ VIN,
     GRAD[k] = g;
 }
 
+// h_bar = readout for every node (potential.cpp:808); a row per thread so the
+// constant reads are warp-uniform (broadcast) instead of 16-way divergent
 __global__ void k_init_hbar(int64_t n, float* HB) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n * kF) return;
-    HB[t] = c_m.ro[t % kF];
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    float4* row = reinterpret_cast<float4*>(HB + k * kF);
+#pragma unroll
+    for (int q = 0; q < kF / 4; ++q)
+        row[q] = make_float4(c_m.ro[4 * q], c_m.ro[4 * q + 1], c_m.ro[4 * q + 2], c_m.ro[4 * q + 3]);
 }
 
 __global__ void k_forces_out(int64_t n, const int32_t* __restrict__ nodes,
@@ -1600,7 +1605,7 @@ void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, fl
 
 void launch_init_hbar(int64_t n, float* HB, cudaStream_t s) {
     if (n == 0) return;
-    k_init_hbar<<<div_up(n * kF, 256), 256, 0, s>>>(n, HB);
+    k_init_hbar<<<div_up(n, 256), 256, 0, s>>>(n, HB);
     GMD_LAUNCH_CHECK();
 }
 

@@ -35,6 +35,14 @@ WANT = [
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 
 
+def kernel_name(raw):
+    """'void gmd::<unnamed>::k_conv2<3, 0>(gmd::ConvArgs, ...)' -> 'k_conv2'."""
+    name = raw.split("(")[0]
+    for junk in ("(anonymous namespace)::", "<unnamed>::", "unnamed>::", "gmd::", "void "):
+        name = name.replace(junk, "")
+    return name.split("<")[0].strip()
+
+
 def num(v):
     try:
         return float(v.replace(",", ""))
@@ -50,8 +58,7 @@ def report(path):
     name_i = hdr.index("Kernel Name")
     res = {}
     for r in rows[2:]:
-        name = r[name_i].split("(")[0].replace("(anonymous namespace)::", "")
-        name = name.replace("unnamed>::", "").replace("gmd::", "").strip()
+        name = kernel_name(r[name_i])
         m = {}
         for k, lab in WANT:
             if k in hdr:
@@ -83,7 +90,7 @@ def launches(path):
     for r in csv.DictReader(io.StringIO("".join(lines))):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = r["Kernel Name"].split("(")[0].replace("unnamed>::", "").replace("gmd::", "").strip()
+        name = kernel_name(r["Kernel Name"])
         t = num(r["Metric Value"]) * SCALE.get(r["Metric Unit"], 1)
         c = per.setdefault(name, [0, 0.0])
         c[0] += 1
