@@ -556,16 +556,22 @@ struct ConvIn {
     float4 h[4];
 };
 
-// gathered row of edge e whose source row w was loaded one step earlier
-__device__ __forceinline__ void conv_load(const ConvArgs& a, const float* __restrict__ Hin, int e,
-                                          int w, ConvIn& x) {
-    x.d = __ldg(a.d + e);
+// gathered source row w (its index was read one step earlier)
+__device__ __forceinline__ void conv_load(const float* __restrict__ Hin, int w, ConvIn& x) {
     const float* hrow = Hin + (size_t)w * kF;
     ldg256(hrow, x.h[0], x.h[1]);
     ldg256(hrow + 8, x.h[2], x.h[3]);
 }
+// the per-edge streams (source index, d or (v, d)) are read one slot ahead:
+// they come from DRAM, the gathered rows mostly from L2
 __device__ __forceinline__ int src_of(const ConvArgs& a, int e, int e1) {
     return e < e1 ? __ldg(a.lsrc + e) : 0;
+}
+__device__ __forceinline__ float d_of(const ConvArgs& a, int e, int e1) {
+    return e < e1 ? __ldg(a.d + e) : 0.f;
+}
+__device__ __forceinline__ float4 vd_of(const ConvArgs& a, int e, int e1) {
+    return e < e1 ? __ldg(a.vd + e) : make_float4(0.f, 0.f, 0.f, 1.f);
 }
 
 // same arithmetic, per feature and in the same order, as conv_edge
@@ -605,22 +611,43 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_conv2(ConvArgs a, int layer,
     const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
     double esum = 0.0;
     const int64_t iters = (a.n + ng - 1) / ng;
+    // the next node's bounds and first slot's streams are requested at the
+    // start of the current node
+    int64_t vn = 0;
+    int e0n = 0, e1n = 0, wn = 0;
+    float dn = 0.f;
+    auto prefetch = [&](int64_t k) {
+        if (k < a.n) {
+            vn = a.nodes ? (int64_t)a.nodes[k] : k;
+            e0n = __ldg(a.row + vn);
+            e1n = __ldg(a.row + vn + 1);
+            wn = src_of(a, e0n + gl, e1n);
+            dn = d_of(a, e0n + gl, e1n);
+        } else {
+            vn = 0;
+            e0n = e1n = 0;
+        }
+    };
+    prefetch(g0);
     for (int64_t it = 0; it < iters; ++it) {
         const int64_t k = g0 + it * ng;
         const bool valid = k < a.n;
-        const int64_t v = valid ? (a.nodes ? (int64_t)a.nodes[k] : k) : 0;
+        const int64_t v = vn;
+        const int e0 = e0n, e1 = e1n;
+        int w = wn;
+        float dcur = dn;
+        prefetch(k + ng);
         float2 acc[kF / 2];
 #pragma unroll
         for (int i = 0; i < kF / 2; ++i) acc[i] = make_float2(0.f, 0.f);
-        const int e0 = valid ? __ldg(a.row + v) : 0;
-        const int e1 = valid ? __ldg(a.row + v + 1) : 0;
-        // one edge per lane in flight; its source index is read one slot ahead
+        // one gathered row per lane in flight; index and d one slot ahead
         ConvIn x;
-        int w = src_of(a, e0 + gl, e1);
         for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
             if (e < e1) {
-                conv_load(a, Hin, e, w, x);
+                conv_load(Hin, w, x);
+                x.d = dcur;
                 w = src_of(a, e + 16, e1);
+                dcur = d_of(a, e + 16, e1);
                 conv_math2(x, acc);
             }
         }
@@ -667,9 +694,8 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_conv2(ConvArgs a, int layer,
 // sum_e dbar_e v v^T / d = 1/2 sum_e (dbar_e + dbar_rev(e)) v v^T / d over any
 // edge set closed under reversal (all edges, or all in-edges of the atoms a
 // rank owns, summed over ranks).
-__device__ __forceinline__ void bwd_load2(const ConvArgs& a, const float* __restrict__ MB,
-                                          const float* __restrict__ Hl, int e, int w, BwdEdgeIn& x) {
-    x.q = __ldg(a.vd + e);
+__device__ __forceinline__ void bwd_load2(const float* __restrict__ MB, const float* __restrict__ Hl,
+                                          int w, BwdEdgeIn& x) {
     const float* mw = MB + (size_t)w * kF;
     const float* hw = Hl + (size_t)w * kF;
     ldg256(mw, x.m[0], x.m[1]);
@@ -763,6 +789,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge2(ConvArgs a, const 
     float mun = 0.f, hun = 0.f;
     BwdEdgeIn xa;
     int wa = 0;
+    float4 qa = make_float4(0.f, 0.f, 0.f, 1.f);
     // node k's row bounds, own rows and first source index are loaded while
     // the previous node finishes
     auto prefetch = [&](int64_t k) {
@@ -774,6 +801,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge2(ConvArgs a, const 
             mun = __ldg(MB + r * kF + gl);
             hun = __ldg(Hl + r * kF + gl);
             wa = src_of(a, e0n + gl, e1n);
+            qa = vd_of(a, e0n + gl, e1n);
         } else {
             e0n = e1n = 0;
         }
@@ -798,8 +826,10 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge2(ConvArgs a, const 
         const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
         for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
             if (e < e1) {
-                bwd_load2(a, MB, Hl, e, wa, xa);
+                bwd_load2(MB, Hl, wa, xa);
+                xa.q = qa;
                 wa = src_of(a, e + 16, e1);
+                qa = vd_of(a, e + 16, e1);
                 bwd_math2(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
             }
         }
