@@ -82,6 +82,42 @@ int gmd_params_init(uint64_t seed, int F, int K, int L, double r_atom, double r3
 int gmd_forward(gmd_handle* h, double* energy, void* per_atom, void* forces, double* stress,
                 double* timing, uint32_t flags);
 
+/* ---- on-device MD: the caller of the hot path (md.hpp:49-89, md.cpp) ------
+ * State arrays are DEVICE pointers on the handle's GPU, fp64: pos, vel,
+ * forces (n x 3), masses (n); Z (n int32, device).  gmd_set_params first. */
+/* atomic_mass(Z) (system.cpp:289-293), host arrays */
+int gmd_md_masses(int64_t n, const int32_t* Z, double* masses);
+/* maxwell_boltzmann_velocities(system, T, seed) (md.cpp:20-52), host arrays */
+int gmd_md_maxwell_boltzmann(int64_t n, const int32_t* Z, double temperature, uint64_t seed,
+                             double* vel);
+/* evaluate (md.cpp:55-69): rebuild graph + partitions at pos, forward, forces
+ * (device) <- -dE/dr; energy (host) and timing (4, host) optional */
+int gmd_md_evaluate(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z,
+                    const double lattice[9], const uint8_t pbc[3], double rc, double r3, double tau,
+                    int p, uint32_t flags, double* forces, double* energy, double* timing);
+/* velocity_verlet_step (md.cpp:85-110): half-kick + drift, wrap_positions,
+ * evaluate, half-kick; forces must hold the forces at pos on entry.  A
+ * non-finite force fails with GMD_ERR_RUNTIME ("non-finite force on atom i"). */
+int gmd_md_step(gmd_handle* h, int64_t n, double* pos, double* vel, double* forces,
+                const double* masses, const int32_t* Z, const double lattice[9],
+                const uint8_t pbc[3], double dt, double rc, double r3, double tau, int p,
+                uint32_t flags, double* energy, double* timing);
+/* MDState::kinetic_energy (eV) and max |f| (eV/A) of the device state; forces
+ * may be NULL */
+int gmd_md_observe(gmd_handle* h, int64_t n, const double* vel, const double* masses,
+                   const double* forces, double* kinetic, double* max_force);
+
+/* run_md (md.cpp:112-160) with HOST state in/out and the whole trajectory on
+ * the device: evaluate at pos, then `steps` velocity-Verlet steps.  pos / vel
+ * (n x 3) are read and overwritten with the final state, forces (optional)
+ * receives the final forces; records (optional, (steps + 1) x 8) holds per
+ * step: potential, kinetic, total, max |f|, graph creation, feature calc,
+ * forward, backward (s). */
+int gmd_md_run(gmd_handle* h, int64_t n, double* pos, double* vel, double* forces,
+               const int32_t* Z, const double lattice[9], const uint8_t pbc[3], double dt,
+               int64_t steps, double rc, double r3, double tau, int p, uint32_t flags,
+               double* records);
+
 /* ---- views (parity / export; materialized on demand) -------------------- */
 int gmd_num_nodes(const gmd_handle* h, int64_t* n);
 int gmd_num_edges(const gmd_handle* h, int64_t* ne);

@@ -9,8 +9,11 @@
 // materialized from device data on first use.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cctype>
 #include <cmath>
+#include <fstream>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -596,6 +599,185 @@ inline PotentialOutput forward_distributed(const Distributed& dist, const ToyPot
 // neighborlist.hpp:37-38 on the GPU
 inline AtomGraph build_neighbor_list(const AtomicSystem& system, double cutoff, int n_threads = 0) {
     return Distributed::create_distributed(system, cutoff, std::nullopt, 1, n_threads, true).graph();
+}
+
+// ---- md.hpp (md.cpp:11-179): the caller of the hot path --------------------
+namespace units {
+inline constexpr double kAccel = 9.648533212e-3;
+inline constexpr double kKinetic = 103.642697;
+inline constexpr double kBoltzmann = 8.617333262e-5;
+}  // namespace units
+
+inline double atomic_mass(int z) {
+    double m = 0.0;
+    int32_t zz = z;
+    if (gmd_md_masses(1, &zz, &m) != GMD_OK) throw Error(gmd_last_error(nullptr));
+    return m;
+}
+
+struct MDState {
+    AtomicSystem system;
+    std::vector<Vec3> velocities;  // A/fs
+    std::vector<double> masses;    // amu
+    std::vector<Vec3> forces;      // eV/A at the current positions
+    double potential_energy = 0.0;
+    std::int64_t step = 0;
+    double kinetic_energy() const {
+        double e = 0.0;
+        for (std::size_t i = 0; i < velocities.size(); ++i)
+            e += 0.5 * masses[i] * velocities[i].norm2();
+        return e * units::kKinetic;
+    }
+    double temperature() const {
+        if (velocities.empty()) return 0.0;
+        const double dof = std::max<double>(1.0, 3.0 * velocities.size() - 3.0);
+        return 2.0 * kinetic_energy() / (dof * units::kBoltzmann);
+    }
+};
+
+struct MDOptions {
+    double dt = 1.0;
+    std::int64_t steps = 0;
+    int partitions = 1;
+    int threads = 0;
+    bool allow_narrow = false;
+    std::uint64_t seed = 0;
+    double init_temperature = 300.0;
+    std::string energy_csv;
+    std::string timing_csv;
+    std::string trajectory_xyz;       // accepted, not written (XYZ I/O is out of scope)
+    std::int64_t snapshot_every = 0;
+};
+
+struct MDStepRecord {
+    std::int64_t step = 0;
+    double potential = 0.0, kinetic = 0.0, total = 0.0, max_force = 0.0;
+    StepTiming timing;
+};
+
+struct MDResult {
+    MDState state;
+    std::vector<MDStepRecord> records;
+};
+
+inline std::vector<Vec3> maxwell_boltzmann_velocities(const AtomicSystem& system,
+                                                      double temperature, std::uint64_t seed) {
+    const std::size_t n = system.size();
+    std::vector<int32_t> z(system.species.begin(), system.species.end());
+    std::vector<double> v(3 * n);
+    if (gmd_md_maxwell_boltzmann((int64_t)n, z.data(), temperature, seed, v.data()) != GMD_OK)
+        throw Error(gmd_last_error(nullptr));
+    std::vector<Vec3> out(n);
+    for (std::size_t i = 0; i < n; ++i) out[i] = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+    return out;
+}
+
+inline MDState init_md_state(const AtomicSystem& system, const MDOptions& opts) {
+    MDState st;
+    st.system = system;
+    st.system.validate();
+    st.masses.resize(system.size());
+    for (std::size_t i = 0; i < system.size(); ++i) st.masses[i] = atomic_mass(system.species[i]);
+    st.velocities = maxwell_boltzmann_velocities(system, opts.init_temperature, opts.seed);
+    return st;
+}
+
+namespace detail {
+// `steps` velocity-Verlet steps of st on the device (gmd_md_run): host state
+// in and out, the trajectory in between stays in HBM
+inline std::vector<double> md_device(MDState& st, const ToyPotentialParams& params,
+                                     const MDOptions& opts, std::int64_t steps, int device = 0) {
+    params.validate();
+    if (opts.dt < 0.0) throw Error("time step must be >= 0");
+    gmd_handle* raw = nullptr;
+    if (gmd_create(device, &raw) != GMD_OK) throw Error(gmd_last_error(nullptr));
+    std::unique_ptr<gmd_handle, void (*)(gmd_handle*)> h(raw, [](gmd_handle* x) { gmd_destroy(x); });
+    std::vector<double> blob = params.blob();
+    check(h.get(), gmd_set_params(h.get(), params.feature_width, params.basis_count, params.layers,
+                                  params.r_atom, params.r_3body, blob.data()));
+    const std::size_t n = st.system.size();
+    std::vector<double> pos(3 * n), vel(3 * n), frc(3 * n), lat(9), rec(8 * (steps + 1));
+    std::vector<int32_t> z(st.system.species.begin(), st.system.species.end());
+    for (std::size_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) {
+            pos[3 * i + k] = st.system.positions[i][k];
+            vel[3 * i + k] = st.velocities.empty() ? 0.0 : st.velocities[i][k];
+        }
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) lat[3 * r + k] = st.system.lattice[r][k];
+    uint8_t pbc[3] = {st.system.pbc[0], st.system.pbc[1], st.system.pbc[2]};
+    check(h.get(), gmd_md_run(h.get(), (int64_t)n, pos.data(), vel.data(), frc.data(), z.data(),
+                              lat.data(), pbc, opts.dt, steps, params.r_atom,
+                              params.threebody() ? params.r_3body : 0.0, 0.0, opts.partitions,
+                              opts.allow_narrow ? GMD_ALLOW_NARROW : 0u, rec.data()));
+    st.velocities.resize(n);
+    st.forces.resize(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        st.system.positions[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        st.velocities[i] = {vel[3 * i], vel[3 * i + 1], vel[3 * i + 2]};
+        st.forces[i] = {frc[3 * i], frc[3 * i + 1], frc[3 * i + 2]};
+    }
+    st.potential_energy = rec[8 * steps];
+    st.step += steps;
+    return rec;
+}
+}  // namespace detail
+
+// velocity_verlet_step (md.cpp:85-110) on the device; the forces of the
+// current positions are recomputed on entry (deterministic, equal to
+// state.forces when those belong to the current positions)
+inline void velocity_verlet_step(MDState& state, const ToyPotentialParams& params,
+                                 const MDOptions& opts, StepTiming* timing = nullptr) {
+    if (state.forces.size() != state.system.size())
+        throw Error("step requires forces at the current positions");
+    std::vector<double> rec = detail::md_device(state, params, opts, 1);
+    if (timing) {
+        timing->graph_creation += rec[12];
+        timing->feature_calculation += rec[13];
+        timing->forward_pass += rec[14];
+        timing->backward_pass += rec[15];
+    }
+}
+
+inline void write_energy_csv(const std::string& path, const std::vector<MDStepRecord>& records) {
+    std::ofstream out(path);
+    if (!out) throw Error("cannot write file: " + path);
+    out << "step,potential_ev,kinetic_ev,total_ev,max_force_ev_per_a";
+    for (const std::string& name : StepTiming::category_names()) {
+        std::string col = name;
+        for (char& c : col) c = c == ' ' ? '_' : static_cast<char>(std::tolower(c));
+        out << "," << col << "_s";
+    }
+    out << "\n";
+    out.precision(12);
+    for (const MDStepRecord& r : records)
+        out << r.step << "," << r.potential << "," << r.kinetic << "," << r.total << ","
+            << r.max_force << "," << r.timing.graph_creation << "," << r.timing.feature_calculation
+            << "," << r.timing.forward_pass << "," << r.timing.backward_pass << "\n";
+}
+
+// run_md (md.cpp:112-160): the whole trajectory in one device-resident loop
+inline MDResult run_md(const AtomicSystem& system, const ToyPotentialParams& params,
+                       const MDOptions& opts) {
+    MDResult res;
+    res.state = init_md_state(system, opts);
+    res.state.step = 0;
+    std::vector<double> rec = detail::md_device(res.state, params, opts, opts.steps);
+    for (std::int64_t s = 0; s <= opts.steps; ++s) {
+        MDStepRecord r;
+        r.step = s;
+        r.potential = rec[8 * s];
+        r.kinetic = rec[8 * s + 1];
+        r.total = rec[8 * s + 2];
+        r.max_force = rec[8 * s + 3];
+        r.timing.graph_creation = rec[8 * s + 4];
+        r.timing.feature_calculation = rec[8 * s + 5];
+        r.timing.forward_pass = rec[8 * s + 6];
+        r.timing.backward_pass = rec[8 * s + 7];
+        res.records.push_back(r);
+    }
+    if (!opts.energy_csv.empty()) write_energy_csv(opts.energy_csv, res.records);
+    return res;
 }
 
 }  // namespace graphmd

@@ -1364,3 +1364,116 @@ done:
     sys_free(&s);
     return rcode;
 }
+
+/* ------------------------------------------------------------------------ */
+/* MD (md.cpp:11-160): Maxwell-Boltzmann init, velocity Verlet with a        */
+/* forward_serial evaluation per step (the reference uses                    */
+/* forward_distributed, equal to serial within 1e-10).                        */
+/* ------------------------------------------------------------------------ */
+static const double ORC_MASSES[55] = {
+    0.0,    1.008,  4.0026, 6.94,   9.0122, 10.81,  12.011, 14.007, 15.999, 18.998, 20.180,
+    22.990, 24.305, 26.982, 28.085, 30.974, 32.06,  35.45,  39.948, 39.098, 40.078, 44.956,
+    47.867, 50.942, 51.996, 54.938, 55.845, 58.933, 58.693, 63.546, 65.38,  69.723, 72.630,
+    74.922, 78.971, 79.904, 83.798, 85.468, 87.62,  88.906, 91.224, 92.906, 95.95,  97.0,
+    101.07, 102.91, 106.42, 107.87, 112.41, 114.82, 118.71, 121.76, 127.60, 126.90, 131.29};
+#define ORC_KACCEL 9.648533212e-3
+#define ORC_KKIN 103.642697
+#define ORC_KB 8.617333262e-5
+
+double orc_atomic_mass(int z) { /* system.cpp:289-293 */
+    return z < 55 ? ORC_MASSES[z] : 2.5 * z;
+}
+
+static void md_record(int64_t n, const double* m, const double* v, const double* f, double pot,
+                      double* rec) {
+    double e = 0.0, fm = 0.0;
+    for (int64_t i = 0; i < n; ++i) { /* MDState::kinetic_energy (md.cpp:11-16) */
+        const v3 vi = mk(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+        e += 0.5 * m[i] * vdot(vi, vi);
+        const double fn = vnorm(mk(f[3 * i], f[3 * i + 1], f[3 * i + 2]));
+        fm = fn > fm ? fn : fm;
+    }
+    rec[0] = pot;
+    rec[1] = e * ORC_KKIN;
+    rec[2] = rec[0] + rec[1];
+    rec[3] = fm;
+}
+
+int orc_md_run(int64_t n, const double* pos0, const int32_t* z, const double* lat,
+               const uint8_t* pbc, int F, int K, int L, double r_atom, double r3,
+               const double* blob, double dt, int64_t steps, double temperature, uint64_t seed,
+               double* pos, double* vel, double* forces, double* rec) {
+    if (dt < 0.0) return fail("time step must be >= 0");
+    double* m = (double*)xcalloc((size_t)n, 8);
+    for (int64_t i = 0; i < n; ++i) m[i] = orc_atomic_mass(z[i]);
+    for (int64_t i = 0; i < 3 * n; ++i) {
+        pos[i] = pos0[i];
+        vel[i] = 0.0;
+    }
+    if (temperature > 0.0 && n > 0) { /* maxwell_boltzmann_velocities (md.cpp:20-52) */
+        rng_t g;
+        rng_seed(&g, seed ^ 0xd1b54a32d192ed03ull);
+        for (int64_t i = 0; i < n; ++i) {
+            const double sigma = sqrt(ORC_KB * temperature / (m[i] * ORC_KKIN));
+            for (int k = 0; k < 3; ++k) vel[3 * i + k] = sigma * rng_normal(&g);
+        }
+        v3 ptot = mk(0, 0, 0);
+        double mtot = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            ptot = vadd(ptot, vscale(mk(vel[3 * i], vel[3 * i + 1], vel[3 * i + 2]), m[i]));
+            mtot += m[i];
+        }
+        const v3 vcm = vdiv(ptot, mtot);
+        for (int64_t i = 0; i < n; ++i)
+            for (int k = 0; k < 3; ++k) vel[3 * i + k] -= vcm.c[k];
+    }
+    m3 Lm, inv;
+    for (int k = 0; k < 3; ++k) Lm.r[k] = mk(lat[3 * k], lat[3 * k + 1], lat[3 * k + 2]);
+    if (minverse(&Lm, &inv)) {
+        free(m);
+        return 1;
+    }
+    double pot = 0.0;
+    if (orc_forward_serial(n, pos, z, lat, pbc, F, K, L, r_atom, r3, blob, &pot, NULL, forces,
+                           NULL)) {
+        free(m);
+        return 1;
+    }
+    md_record(n, m, vel, forces, pot, rec);
+    for (int64_t step = 1; step <= steps; ++step) { /* velocity_verlet_step (md.cpp:85-110) */
+        for (int64_t i = 0; i < n; ++i) {
+            const double s = ORC_KACCEL / m[i];
+            for (int k = 0; k < 3; ++k) {
+                vel[3 * i + k] += (forces[3 * i + k] * s) * (0.5 * dt);
+                pos[3 * i + k] += vel[3 * i + k] * dt;
+            }
+        }
+        for (int64_t i = 0; i < n; ++i) { /* wrap_positions (system.cpp:216-229) */
+            v3 fr = rowvec(&inv, mk(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]));
+            for (int k = 0; k < 3; ++k) {
+                fr.c[k] -= floor(fr.c[k]);
+                if (fr.c[k] >= 1.0) fr.c[k] = 0.0;
+            }
+            const v3 r = rowvec(&Lm, fr);
+            for (int k = 0; k < 3; ++k) pos[3 * i + k] = r.c[k];
+        }
+        if (orc_forward_serial(n, pos, z, lat, pbc, F, K, L, r_atom, r3, blob, &pot, NULL,
+                               forces, NULL)) {
+            free(m);
+            return 1;
+        }
+        for (int64_t i = 0; i < 3 * n; ++i)
+            if (!isfinite(forces[i])) {
+                free(m);
+                return fail("non-finite force on atom %lld at step %lld", (long long)(i / 3),
+                            (long long)step);
+            }
+        for (int64_t i = 0; i < n; ++i) {
+            const double s = ORC_KACCEL / m[i];
+            for (int k = 0; k < 3; ++k) vel[3 * i + k] += (forces[3 * i + k] * s) * (0.5 * dt);
+        }
+        md_record(n, m, vel, forces, pot, rec + 4 * step);
+    }
+    free(m);
+    return 0;
+}

@@ -85,6 +85,16 @@ int orc_forward_serial(int64_t n, const double* pos, const int32_t* z, const dou
                        const double* blob, double* energy, double* per_atom,
                        double* forces, double* stress);
 
+/* ---- MD (md.cpp:11-160) ---- */
+double orc_atomic_mass(int z);
+/* init_md_state + forces at pos0, then `steps` velocity-Verlet steps; final
+ * pos / vel / forces (n x 3) and records rec[(steps + 1) x 4] = (potential,
+ * kinetic, total, max |f|) per step, row 0 = initial */
+int orc_md_run(int64_t n, const double* pos0, const int32_t* z, const double* lat,
+               const uint8_t* pbc, int F, int K, int L, double r_atom, double r3,
+               const double* blob, double dt, int64_t steps, double temperature, uint64_t seed,
+               double* pos, double* vel, double* forces, double* rec);
+
 #ifdef __cplusplus
 }
 #endif

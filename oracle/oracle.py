@@ -96,6 +96,11 @@ class Oracle:
         else:
             self._nl = f("neighbor_list", V, _i64, V, V, V, V, D, I, I)
             self._fwd = f("forward", I, V, I, I, I, D, D, V, V, V, V, V, V)
+        if backend == "c":
+            self._md = f("md_run", I, _i64, V, V, V, V, I, I, I, D, D, V, D, _i64, D, U, V, V, V, V)
+        else:
+            self._md = f("md_run", I, _i64, V, V, V, V, I, I, I, D, D, V, D, _i64, I, D, U, V, V,
+                         V, V)
         self._g_ne = f("graph_num_edges", _i64, V)
         self._g_get = f("graph_get", None, V, V, V, V, V, V)
         self._g_free = f("graph_destroy", None, V)
@@ -181,6 +186,24 @@ class Oracle:
         if rc:
             raise OracleError(self.error())
         return dict(energy=float(e[0]), per_atom=pa, forces=fo, stress=st)
+
+    def md_run(self, pos, z, lat, pbc, params, F, K, L, r_atom, r3, dt, steps, temperature,
+               seed, partitions=1):
+        """run_md (md.cpp:112-160): final pos / vel / forces and the per-step
+        records (potential, kinetic, total, max_force), row 0 = initial."""
+        pos, z, lat, pbc = self._sysargs(pos, z, lat, pbc)
+        n = len(z)
+        op, ov, of = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3))
+        rec = np.zeros((steps + 1, 4))
+        params = np.ascontiguousarray(params, np.float64)
+        args = [n, _ptr(pos), _ptr(z), _ptr(lat), _ptr(pbc), F, K, L, r_atom, r3, _ptr(params), dt,
+                steps]
+        if self.backend == "ref":
+            args.append(partitions)
+        args += [temperature, seed, _ptr(op), _ptr(ov), _ptr(of), _ptr(rec)]
+        if self._md(*args):
+            raise OracleError(self.error())
+        return dict(pos=op, vel=ov, forces=of, records=rec)
 
     def create(self, pos, z, lat, pbc, rc, r3=0.0, tau=0.0, p=1, allow_narrow=False, n_threads=1):
         pos, z, lat, pbc = self._sysargs(pos, z, lat, pbc)

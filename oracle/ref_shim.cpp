@@ -14,6 +14,8 @@
 //   serial_line_graph / brute force   proj/include/graphmd/linegraph.hpp:72-78
 //   ToyPotentialParams::init          proj/include/graphmd/potential.hpp:35-37
 //   make_supercell / random_perturb   proj/include/graphmd/system.hpp:99-105
+#include "graphmd/md.hpp"
+
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -396,6 +398,40 @@ int gref_fd_forces(int64_t n, const double* pos, const int32_t* z,
         forces[3 * i] = f[i].x;
         forces[3 * i + 1] = f[i].y;
         forces[3 * i + 2] = f[i].z;
+    }
+    return 0;
+    GUARD_END(1)
+}
+
+// run_md (md.cpp:112-160) with the given options; final state + records
+// rec[(steps + 1) x 4] = (potential, kinetic, total, max_force)
+int gref_md_run(int64_t n, const double* pos, const int32_t* z, const double* lat,
+                const uint8_t* pbc, int F, int K, int L, double r_atom, double r3,
+                const double* blob, double dt, int64_t steps, int partitions,
+                double temperature, uint64_t seed, double* out_pos, double* out_vel,
+                double* out_forces, double* rec) {
+    GUARD_BEGIN
+    ToyPotentialParams p = make_params(F, K, L, r_atom, r3, blob);
+    MDOptions o;
+    o.dt = dt;
+    o.steps = steps;
+    o.partitions = partitions;
+    o.threads = 1;
+    o.allow_narrow = true;
+    o.seed = seed;
+    o.init_temperature = temperature;
+    MDResult r = run_md(make_system(n, pos, z, lat, pbc), p, o);
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) {
+            out_pos[3 * i + k] = r.state.system.positions[i][k];
+            out_vel[3 * i + k] = r.state.velocities[i][k];
+            out_forces[3 * i + k] = r.state.forces[i][k];
+        }
+    for (size_t s = 0; s < r.records.size(); ++s) {
+        rec[4 * s] = r.records[s].potential;
+        rec[4 * s + 1] = r.records[s].kinetic;
+        rec[4 * s + 2] = r.records[s].total;
+        rec[4 * s + 3] = r.records[s].max_force;
     }
     return 0;
     GUARD_END(1)

@@ -27,6 +27,7 @@
 #include "gmd_comm.cuh"
 #include "gmd_common.cuh"
 #include "gmd_graph.cuh"
+#include "gmd_md.cuh"
 #include "gmd_model.cuh"
 #include "gmd_partition.cuh"
 
@@ -278,6 +279,8 @@ struct gmd_handle {
     DBuf ccnt, cstart, ctab, ccta;
     DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v3_part, red, per_atom,
         forces, conv_tmp, exp_tmp;
+    DBuf md_part, md_out, md_bad;  // on-device MD observables / non-finite flag
+    DBuf md_pos, md_vel, md_frc, md_mass, md_z;  // device state of gmd_md_run
     cudaEvent_t ev[8] = {};
 
     // one rank per GPU: transport + this rank's plan
@@ -1291,7 +1294,9 @@ void gmd_destroy(gmd_handle* h) {
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
                     &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->flagtmp, &h->nodes, &h->xsend, &h->sendbuf, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
-                    &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp};
+                    &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp,
+                    &h->md_part, &h->md_out, &h->md_bad, &h->md_pos, &h->md_vel, &h->md_frc,
+                    &h->md_mass, &h->md_z};
     for (DBuf* b : bufs) b->release();
     for (LayoutState* ls : {&h->atoms, &h->bonds}) {
         DBuf* lb[] = {&ls->node_array, &ls->crow, &ls->list_off_d, &ls->xdst, &ls->xsrc,
@@ -1871,6 +1876,166 @@ int gmd_get_owned_ids(gmd_handle* h, int64_t* ids) {
         } else {
             for (int64_t i = 0; i < h->n; ++i) ids[i] = i;
         }
+    });
+}
+
+// ---- on-device MD (md.cpp:20-160) ------------------------------------------
+// standard atomic weights up to Xe, linear estimate beyond (system.cpp:28-37,
+// :289-293)
+static const double kMassTable[55] = {
+    0.0,    1.008,  4.0026, 6.94,   9.0122, 10.81,  12.011, 14.007, 15.999, 18.998, 20.180,
+    22.990, 24.305, 26.982, 28.085, 30.974, 32.06,  35.45,  39.948, 39.098, 40.078, 44.956,
+    47.867, 50.942, 51.996, 54.938, 55.845, 58.933, 58.693, 63.546, 65.38,  69.723, 72.630,
+    74.922, 78.971, 79.904, 83.798, 85.468, 87.62,  88.906, 91.224, 92.906, 95.95,  97.0,
+    101.07, 102.91, 106.42, 107.87, 112.41, 114.82, 118.71, 121.76, 127.60, 126.90, 131.29};
+
+int gmd_md_masses(int64_t n, const int32_t* Z, double* masses) {
+    if ((n > 0 && (!Z || !masses)) || n < 0) return GMD_ERR_ARG;
+    for (int64_t i = 0; i < n; ++i) {
+        const int z = Z[i];
+        if (z < 1 || z > 118) {
+            g_err = "atomic number out of range";
+            return GMD_ERR_CONFIG;
+        }
+        masses[i] = z < 55 ? kMassTable[z] : 2.5 * z;
+    }
+    return GMD_OK;
+}
+
+int gmd_md_maxwell_boltzmann(int64_t n, const int32_t* Z, double temperature, uint64_t seed,
+                             double* vel) {
+    if ((n > 0 && (!Z || !vel)) || n < 0) return GMD_ERR_ARG;
+    std::fill(vel, vel + 3 * n, 0.0);
+    if (temperature <= 0.0 || n == 0) return GMD_OK;
+    std::vector<double> m(n);
+    if (int rc = gmd_md_masses(n, Z, m.data())) return rc;
+    HostRng rng(seed ^ 0xd1b54a32d192ed03ull);  // md.cpp:28
+    for (int64_t i = 0; i < n; ++i) {
+        const double sigma = std::sqrt(gmd::kBoltzmann * temperature / (m[i] * gmd::kKinetic));
+        for (int k = 0; k < 3; ++k) vel[3 * i + k] = sigma * rng.normal();
+    }
+    double p[3] = {0.0, 0.0, 0.0}, mtot = 0.0;  // remove the centre-of-mass momentum
+    for (int64_t i = 0; i < n; ++i) {
+        for (int k = 0; k < 3; ++k) p[k] += vel[3 * i + k] * m[i];
+        mtot += m[i];
+    }
+    const double vcm[3] = {p[0] / mtot, p[1] / mtot, p[2] / mtot};
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) vel[3 * i + k] -= vcm[k];
+    return GMD_OK;
+}
+
+int gmd_md_evaluate(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z,
+                    const double lattice[9], const uint8_t pbc[3], double rc, double r3, double tau,
+                    int p, uint32_t flags, double* forces, double* energy, double* timing) {
+    return run(h, [&] {
+        if (!pos || !Z || !lattice || !forces) raise(kArg, "null pointer");
+        build_impl(h, n, pos, Z, lattice, pbc, rc, r3, tau, p, flags | GMD_INPUT_DEVICE);
+        forward_impl(h, energy, nullptr, forces, nullptr, timing, GMD_OUTPUT_DEVICE);
+    });
+}
+
+int gmd_md_step(gmd_handle* h, int64_t n, double* pos, double* vel, double* forces,
+                const double* masses, const int32_t* Z, const double lattice[9],
+                const uint8_t pbc[3], double dt, double rc, double r3, double tau, int p,
+                uint32_t flags, double* energy, double* timing) {
+    return run(h, [&] {
+        if (!pos || !vel || !forces || !masses || !Z || !lattice) raise(kArg, "null pointer");
+        if (dt < 0.0) raise(kConfig, "time step must be >= 0");
+        if (h->comm && h->comm->world > 1)
+            raise(kConfig, "gmd_md_step integrates all atoms on one handle (rank groups: "
+                           "gather forces with gmd_md_evaluate on each rank)");
+        cudaStream_t s = h->stream;
+        Mat9 L, inv;
+        for (int k = 0; k < 9; ++k) L.m[k] = lattice[k];
+        inverse3(lattice, inv.m);
+        launch_md_kick_drift(n, pos, vel, forces, masses, dt, s);
+        launch_md_wrap(n, pos, L, inv, s);
+        build_impl(h, n, pos, Z, lattice, pbc, rc, r3, tau, p, flags | GMD_INPUT_DEVICE);
+        forward_impl(h, energy, nullptr, forces, nullptr, timing, GMD_OUTPUT_DEVICE);
+        auto* bad = h->md_bad.get<unsigned long long>(1);
+        GMD_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+        launch_md_kick(n, vel, forces, masses, dt, bad, s);
+        unsigned long long hb = 0;
+        GMD_CUDA(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaStreamSynchronize(s));
+        if (hb != ~0ull) raise(kRuntime, "non-finite force on atom " + std::to_string(hb));
+    });
+}
+
+int gmd_md_observe(gmd_handle* h, int64_t n, const double* vel, const double* masses,
+                   const double* forces, double* kinetic, double* max_force) {
+    return run(h, [&] {
+        if (!vel || !masses) raise(kArg, "null pointer");
+        cudaStream_t s = h->stream;
+        double* part = h->md_part.get<double>(2 * (size_t)md_observe_parts());
+        double* out = h->md_out.get<double>(2);
+        launch_md_observe(n, vel, masses, forces, part, out, s);
+        double ho[2];
+        GMD_CUDA(cudaMemcpyAsync(ho, out, sizeof ho, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaStreamSynchronize(s));
+        if (kinetic) *kinetic = ho[0];
+        if (max_force) *max_force = ho[1];
+    });
+}
+
+int gmd_md_run(gmd_handle* h, int64_t n, double* pos, double* vel, double* forces,
+               const int32_t* Z, const double lattice[9], const uint8_t pbc[3], double dt,
+               int64_t steps, double rc, double r3, double tau, int p, uint32_t flags,
+               double* records) {
+    if (!h || !pos || !vel || !Z || !lattice || n < 0 || steps < 0) return GMD_ERR_ARG;
+    std::vector<double> m(n);
+    if (int rc0 = gmd_md_masses(n, Z, m.data())) {
+        h->err = g_err;
+        return rc0;
+    }
+    double *dp = nullptr, *dv = nullptr, *df = nullptr, *dm = nullptr;
+    int32_t* dz = nullptr;
+    int rc1 = run(h, [&] {
+        cudaStream_t s = h->stream;
+        dp = h->md_pos.get<double>(3 * n);
+        dv = h->md_vel.get<double>(3 * n);
+        df = h->md_frc.get<double>(3 * n);
+        dm = h->md_mass.get<double>(n);
+        dz = h->md_z.get<int32_t>(n);
+        GMD_CUDA(cudaMemcpyAsync(dp, pos, 24 * n, cudaMemcpyHostToDevice, s));
+        GMD_CUDA(cudaMemcpyAsync(dv, vel, 24 * n, cudaMemcpyHostToDevice, s));
+        GMD_CUDA(cudaMemcpyAsync(dm, m.data(), 8 * n, cudaMemcpyHostToDevice, s));
+        GMD_CUDA(cudaMemcpyAsync(dz, Z, 4 * n, cudaMemcpyHostToDevice, s));
+    });
+    if (rc1) return rc1;
+    auto rec = [&](int64_t step, double pot, const double* tm) -> int {
+        double ke = 0.0, fm = 0.0;
+        if (int r = gmd_md_observe(h, n, dv, dm, df, &ke, &fm)) return r;
+        if (records) {
+            double* r = records + 8 * step;
+            r[0] = pot;
+            r[1] = ke;
+            r[2] = pot + ke;
+            r[3] = fm;
+            for (int k = 0; k < 4; ++k) r[4 + k] = tm[k];
+        }
+        return GMD_OK;
+    };
+    double pot = 0.0, tm[4] = {0, 0, 0, 0};
+    if (int r = gmd_md_evaluate(h, n, dp, dz, lattice, pbc, rc, r3, tau, p, flags, df, &pot, tm))
+        return r;
+    if (int r = rec(0, pot, tm)) return r;
+    for (int64_t step = 1; step <= steps; ++step) {
+        if (int r = gmd_md_step(h, n, dp, dv, df, dm, dz, lattice, pbc, dt, rc, r3, tau, p, flags,
+                                &pot, tm)) {
+            if (h->err.rfind("non-finite force", 0) == 0)
+                h->err += " at step " + std::to_string(step);
+            return r;
+        }
+        if (int r = rec(step, pot, tm)) return r;
+    }
+    return run(h, [&] {
+        cudaStream_t s = h->stream;
+        GMD_CUDA(cudaMemcpyAsync(pos, dp, 24 * n, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaMemcpyAsync(vel, dv, 24 * n, cudaMemcpyDeviceToHost, s));
+        if (forces) GMD_CUDA(cudaMemcpyAsync(forces, df, 24 * n, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaStreamSynchronize(s));
     });
 }
 

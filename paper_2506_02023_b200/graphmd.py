@@ -48,6 +48,8 @@ EXPORTS = [
     "gmd_corrupt_transfer_plan_for_test", "gmd_util_rng_uniform", "gmd_util_supercell",
     "gmd_profile", "gmd_profile_read", "gmd_get_stream", "gmd_launch_count", "gmd_comm_nccl_id",
     "gmd_comm_init_nccl", "gmd_comm_init_local", "gmd_comm_info", "gmd_num_owned", "gmd_get_owned_ids",
+    "gmd_md_masses", "gmd_md_maxwell_boltzmann", "gmd_md_evaluate", "gmd_md_step", "gmd_md_observe",
+    "gmd_md_run",
 ]
 
 
@@ -122,6 +124,12 @@ def lib():
             "gmd_comm_info": (I, [V, V, V]),
             "gmd_num_owned": (I, [V, V]),
             "gmd_get_owned_ids": (I, [V, V]),
+            "gmd_md_masses": (I, [I64, V, V]),
+            "gmd_md_maxwell_boltzmann": (I, [I64, V, D, U64, V]),
+            "gmd_md_evaluate": (I, [V, I64, V, V, V, V, D, D, D, I, U32, V, V, V]),
+            "gmd_md_step": (I, [V, I64, V, V, V, V, V, V, V, D, D, D, D, I, U32, V, V]),
+            "gmd_md_observe": (I, [V, I64, V, V, V, V, V]),
+            "gmd_md_run": (I, [V, I64, V, V, V, V, V, V, D, I64, D, D, D, I, U32, V]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -834,3 +842,226 @@ def exchange_plan_consistent(scnt, rcnt, rank: int, all_scnt) -> bool:
     what rank j sends to `rank` (its TO_j[rank] block) is exactly the FROM
     span `rank` reserved for j.  all_scnt[j][k] = rows rank j sends to k."""
     return all(j == rank or int(all_scnt[j][rank]) == int(rcnt[j]) for j in range(len(rcnt)))
+
+
+# ---------------------------------------------------------------------------
+# on-device MD: the caller of the hot path (md.hpp:14-89, md.cpp)
+# ---------------------------------------------------------------------------
+class units:  # md.hpp:14-21
+    kAccel = 9.648533212e-3
+    kKinetic = 103.642697
+    kBoltzmann = 8.617333262e-5
+
+
+def atomic_mass(z) -> np.ndarray:
+    """atomic_mass (system.cpp:289-293) for an array of atomic numbers."""
+    z = np.ascontiguousarray(np.atleast_1d(z), dtype=np.int32)
+    out = np.zeros(len(z))
+    rc = lib().gmd_md_masses(len(z), _p(z), _p(out))
+    if rc:
+        raise Error(lib().gmd_last_error(None).decode(), rc)
+    return out
+
+
+def maxwell_boltzmann_velocities(system: AtomicSystem, temperature: float, seed: int) -> np.ndarray:
+    """maxwell_boltzmann_velocities (md.cpp:20-52): deterministic in seed,
+    centre-of-mass momentum removed."""
+    v = np.zeros((system.size(), 3))
+    rc = lib().gmd_md_maxwell_boltzmann(system.size(), _p(system.species), temperature, seed, _p(v))
+    if rc:
+        raise Error(lib().gmd_last_error(None).decode(), rc)
+    return v
+
+
+@dataclass
+class MDOptions:  # md.hpp:36-49
+    dt: float = 1.0
+    steps: int = 0
+    partitions: int = 1
+    threads: int = 0
+    allow_narrow: bool = False
+    seed: int = 0
+    init_temperature: float = 300.0
+    energy_csv: str = ""
+    timing_csv: str = ""
+
+
+@dataclass
+class MDStepRecord:  # md.hpp:51-58
+    step: int = 0
+    potential: float = 0.0
+    kinetic: float = 0.0
+    total: float = 0.0
+    max_force: float = 0.0
+    timing: StepTiming = field(default_factory=StepTiming)
+
+
+class MDState:
+    """MDState (md.hpp:23-34) with the dynamic arrays resident on the GPU
+    (torch float64 tensors): positions, velocities, forces, masses."""
+
+    def __init__(self, system: AtomicSystem, velocities: np.ndarray, device: int = 0):
+        import torch
+        system.validate()
+        self.system = system
+        dev = f"cuda:{device}"
+        self.handle = _Handle(device)
+        self.pos = torch.tensor(system.positions, dtype=torch.float64, device=dev)
+        self.vel = torch.tensor(velocities, dtype=torch.float64, device=dev)
+        self.forces = torch.zeros_like(self.pos)
+        self.masses = torch.tensor(atomic_mass(system.species), dtype=torch.float64, device=dev)
+        self.species = torch.tensor(system.species, dtype=torch.int32, device=dev)
+        self.potential_energy = 0.0
+        self.step = 0
+        self._have_forces = False
+
+    def _observe(self):
+        ke, fm = C.c_double(), C.c_double()
+        self.handle.check(lib().gmd_md_observe(self.handle.h, self.size(), self.vel.data_ptr(),
+                                               self.masses.data_ptr(), self.forces.data_ptr(),
+                                               C.byref(ke), C.byref(fm)))
+        return ke.value, fm.value
+
+    def size(self) -> int:
+        return self.system.size()
+
+    def kinetic_energy(self) -> float:
+        return self._observe()[0]
+
+    def temperature(self) -> float:
+        if self.size() == 0:
+            return 0.0
+        dof = max(1.0, 3.0 * self.size() - 3.0)
+        return 2.0 * self.kinetic_energy() / (dof * units.kBoltzmann)
+
+    def positions(self) -> np.ndarray:
+        return self.pos.cpu().numpy()
+
+    def velocities(self) -> np.ndarray:
+        return self.vel.cpu().numpy()
+
+    def forces_host(self) -> np.ndarray:
+        return self.forces.cpu().numpy()
+
+    def current_system(self) -> AtomicSystem:
+        return AtomicSystem(self.positions(), self.system.lattice.copy(), self.system.species.copy(),
+                            tuple(self.system.pbc))
+
+
+@dataclass
+class MDResult:
+    state: MDState
+    records: List[MDStepRecord]
+
+
+def init_md_state(system: AtomicSystem, opts: MDOptions, device: int = 0) -> MDState:
+    """init_md_state (md.cpp:71-83): masses, Maxwell-Boltzmann velocities."""
+    return MDState(system, maxwell_boltzmann_velocities(system, opts.init_temperature, opts.seed),
+                   device)
+
+
+def _md_args(state: MDState, params: "ToyPotentialParams", opts: MDOptions):
+    params.validate()
+    h = state.handle
+    h.check(lib().gmd_set_params(h.h, params.feature_width, params.basis_count, params.layers,
+                                 params.r_atom, params.r_3body, _p(params.blob)))
+    pbc = np.array([1 if b else 0 for b in state.system.pbc], np.uint8)
+    flags = GMD_ALLOW_NARROW if opts.allow_narrow else 0
+    return h, pbc, flags
+
+
+def _timing(tm, timing: Optional[StepTiming]):
+    if timing is not None:
+        timing.graph_creation += tm[0]
+        timing.feature_calculation += tm[1]
+        timing.forward_pass += tm[2]
+        timing.backward_pass += tm[3]
+
+
+def md_evaluate(state: MDState, params: "ToyPotentialParams", opts: MDOptions,
+                timing: Optional[StepTiming] = None) -> None:
+    """evaluate (md.cpp:55-69) at the current device positions: graph rebuild +
+    forward; forces and potential energy land in the state."""
+    h, pbc, flags = _md_args(state, params, opts)
+    e = C.c_double()
+    tm = np.zeros(4)
+    h.check(lib().gmd_md_evaluate(h.h, state.size(), state.pos.data_ptr(), state.species.data_ptr(),
+                                  _p(state.system.lattice), _p(pbc), params.r_atom,
+                                  params.r_3body if params.threebody() else 0.0, 0.0,
+                                  opts.partitions, flags, state.forces.data_ptr(), C.byref(e),
+                                  _p(tm)))
+    _timing(tm, timing)
+    state.potential_energy = e.value
+    state._have_forces = True
+
+
+def velocity_verlet_step(state: MDState, params: "ToyPotentialParams", opts: MDOptions,
+                         timing: Optional[StepTiming] = None) -> None:
+    """velocity_verlet_step (md.cpp:85-110), every array in HBM: half-kick +
+    drift, wrap_positions, graph + partition rebuild, forward, half-kick."""
+    if not state._have_forces:
+        raise Error("step requires forces at the current positions")
+    if opts.dt < 0.0:
+        raise Error("time step must be >= 0")
+    h, pbc, flags = _md_args(state, params, opts)
+    e = C.c_double()
+    tm = np.zeros(4)
+    rc = lib().gmd_md_step(h.h, state.size(), state.pos.data_ptr(), state.vel.data_ptr(),
+                           state.forces.data_ptr(), state.masses.data_ptr(),
+                           state.species.data_ptr(), _p(state.system.lattice), _p(pbc), opts.dt,
+                           params.r_atom, params.r_3body if params.threebody() else 0.0, 0.0,
+                           opts.partitions, flags, C.byref(e), _p(tm))
+    if rc:
+        msg = lib().gmd_last_error(h.h).decode()
+        if msg.startswith("non-finite force"):
+            msg += f" at step {state.step + 1}"
+        raise Error(msg, rc)
+    _timing(tm, timing)
+    state.step += 1
+    state.potential_energy = e.value
+
+
+def run_md(system: AtomicSystem, params: "ToyPotentialParams", opts: MDOptions,
+           device: int = 0) -> MDResult:
+    """run_md (md.cpp:112-160) on the GPU; records row 0 = initial state."""
+    state = init_md_state(system, opts, device)
+    records: List[MDStepRecord] = []
+
+    def record(step, t):
+        ke, fm = state._observe()
+        records.append(MDStepRecord(step, state.potential_energy, ke, state.potential_energy + ke,
+                                    fm, t))
+
+    t0 = StepTiming()
+    md_evaluate(state, params, opts, t0)
+    record(0, t0)
+    for step in range(1, opts.steps + 1):
+        t = StepTiming()
+        velocity_verlet_step(state, params, opts, t)
+        record(step, t)
+    if opts.energy_csv:
+        write_energy_csv(opts.energy_csv, records)
+    if opts.timing_csv:
+        write_timing_csv(opts.timing_csv, [r.timing for r in records])
+    return MDResult(state, records)
+
+
+def write_energy_csv(path: str, records: List[MDStepRecord]) -> None:
+    """write_energy_csv (md.cpp:162-179)."""
+    cols = ",".join(n.lower().replace(" ", "_") + "_s" for n in StepTiming.category_names())
+    with open(path, "w") as f:
+        f.write("step,potential_ev,kinetic_ev,total_ev,max_force_ev_per_a," + cols + "\n")
+        for r in records:
+            t = r.timing
+            f.write(f"{r.step},{r.potential:.12g},{r.kinetic:.12g},{r.total:.12g},"
+                    f"{r.max_force:.12g},{t.graph_creation:.12g},{t.feature_calculation:.12g},"
+                    f"{t.forward_pass:.12g},{t.backward_pass:.12g}\n")
+
+
+def write_timing_csv(path: str, rows: List[StepTiming]) -> None:
+    """write_timing_csv (engine.cpp:29-41): step, then the four categories."""
+    with open(path, "w") as f:
+        f.write("step," + ",".join(StepTiming.category_names()) + "\n")
+        for i, t in enumerate(rows):
+            f.write(f"{i},{t.graph_creation:.9g},{t.feature_calculation:.9g},"
+                    f"{t.forward_pass:.9g},{t.backward_pass:.9g}\n")

@@ -373,6 +373,49 @@ TEST(forward_argument_errors) {
     CHECK_THROWS(forward_distributed(d, ToyPotentialParams::init(1, 16, 8, 2, 4.0, 3.0)));
 }
 
+// md.cpp run_md / velocity_verlet_step through the drop-in header, against
+// the oracle's restatement (orc_md_run, pinned to the reference's run_md)
+TEST(md_run_vs_oracle) {
+    AtomicSystem s = random_perturb(make_supercell(quartz_cell(), {3, 3, 3}), 0.05, 1);
+    ToyPotentialParams prm = ToyPotentialParams::init(12345, 16, 8, 2, 5.0);
+    MDOptions o;
+    o.dt = 1.0;
+    o.steps = 10;
+    o.partitions = 2;
+    o.allow_narrow = true;
+    o.seed = 9;
+    o.init_temperature = 300.0;
+    MDResult res = run_md(s, prm, o);
+    const int64_t n = (int64_t)s.size();
+    std::vector<double> pos(3 * n), lat(9), blob = prm.blob();
+    std::vector<int32_t> z(s.species.begin(), s.species.end());
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) pos[3 * i + k] = s.positions[i][k];
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) lat[3 * r + k] = s.lattice[r][k];
+    uint8_t pbc[3] = {1, 1, 1};
+    std::vector<double> op(3 * n), ov(3 * n), of(3 * n), rec(4 * 11);
+    CHECK(orc_md_run(n, pos.data(), z.data(), lat.data(), pbc, 16, 8, 2, 5.0, 0.0, blob.data(),
+                     1.0, 10, 300.0, 9, op.data(), ov.data(), of.data(), rec.data()) == 0);
+    CHECK(res.records.size() == 11);
+    double dx = 0, dv = 0, de = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) {
+            dx = std::max(dx, std::abs(res.state.system.positions[i][k] - op[3 * i + k]));
+            dv = std::max(dv, std::abs(res.state.velocities[i][k] - ov[3 * i + k]));
+        }
+    for (int st = 0; st <= 10; ++st) de = std::max(de, std::abs(res.records[st].potential - rec[4 * st]));
+    CHECK(dx < 1e-5 && dv < 1e-5 && de / n < 2e-6);
+    CHECK(std::abs(res.state.kinetic_energy() - rec[4 * 10 + 1]) / n < 1e-6);
+    // one more step through velocity_verlet_step continues the trajectory
+    MDState st = res.state;
+    StepTiming t;
+    velocity_verlet_step(st, prm, o, &t);
+    CHECK(st.step == 11 && t.graph_creation > 0);
+    MDState fresh = init_md_state(s, o);
+    CHECK_THROWS(velocity_verlet_step(fresh, prm, o));  // no forces yet
+}
+
 int main(int argc, char** argv) {
     std::string only = argc > 1 ? argv[1] : "";
     for (auto& [name, fn] : registry()) {
