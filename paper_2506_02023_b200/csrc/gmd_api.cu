@@ -706,7 +706,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     // Coordinates are taken relative to the destination bin origin, so each
     // component is bounded by B = max_k sum_r |L_rk| (s_r + 1) / bins_r; fp32
     // rounding moves each component of v by at most delta = 4 B 2^-24.
-    float thr32;
+    float thr32, acc32, zero32;
     {
         double B = 0.0;
         for (int k = 0; k < 3; ++k) {
@@ -721,6 +721,17 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         const double r = std::sqrt(g.pre2) * (1.0 + 1e-9) + std::sqrt(3.0) * delta;
         const double thr = r * r * (1.0 + 8.0 * u);
         thr32 = std::nextafter((float)thr, INFINITY);
+        // fast-accept band: |v32|^2 <= acc32 puts the true vector within
+        // rc (1 - 1e-9) (|v - v32| <= sqrt(3) delta, fp32 |.|^2 relative error
+        // <= 4u), i.e. inside both fp64 tests with a margin far above fp64
+        // rounding (wrapped vs raw vectors differ by ~1e-12 A); |v32|^2 >
+        // zero32 keeps the true vector away from 0 (d2 != 0).
+        const double ra = std::sqrt(g.cutoff2) * (1.0 - 1e-9) - std::sqrt(3.0) * delta;
+        const double acc = ra > 0.0 ? ra * ra / (1.0 + 8.0 * u) : 0.0;
+        acc32 = std::nextafter((float)acc, 0.0f);
+        const double rz = 2.0 * std::sqrt(3.0) * delta + 1e-6;
+        zero32 = std::nextafter((float)(rz * rz * (1.0 + 8.0 * u)), INFINITY);
+        if (!(acc32 > zero32)) acc32 = -1.0f;  // no fast path: every survivor in fp64
     }
     int cap = h->nl_cap;
     if (cap <= 0) {  // first build: density estimate of the mean degree
@@ -732,7 +743,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     int32_t ne32 = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         auto* slab = h->slab.get<unsigned long long>((size_t)n * cap);
-        { PROF("nl_search"); launch_nl_search(g, thr32, nbins, n, cap, b, slab, ownp, myrank, s); }
+        { PROF("nl_search"); launch_nl_search(g, thr32, acc32, zero32, nbins, n, cap, b, slab, ownp, myrank, s); }
         { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
         GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
         read_flags(h, hdr);

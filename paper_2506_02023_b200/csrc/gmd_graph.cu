@@ -120,16 +120,7 @@ __device__ __forceinline__ uint32_t qcode(int qx, int qy, int qz) {
 //     warp (canonical (src, image) order, neighborlist.cpp:21-24) and stored
 //     to a fixed-capacity slab; the emit kernel turns slab rows into CSR.
 // ---------------------------------------------------------------------------
-struct CandW {
-    double c[3][32];  // wrapped_j + shift (fp64, reference expression)
-    double p[3][32];  // raw position of j
-    int nc[3][32];    // q - cell_of[j]
-    int jid[32];
-    unsigned cell[32];  // global stencil-cell index of the candidate
-};
-
 constexpr int kWSCap = 32;  // stencil cells per batch (per warp)
-constexpr int kQCap = 256;  // queued exact tests per round (per warp)
 constexpr int kCodeCap = 128;  // stencil cells whose q code is tabulated
 // Row keys in shared memory are 32-bit: src << cbits | stencil-cell index.  For a
 // fixed src every stencil cell maps to a distinct image, and the image q is
@@ -143,8 +134,6 @@ struct WarpNL {             // per-warp shared state of the search
     int sc_pre[kWSCap + 1];
     int sc_q[kWSCap][3];
     double sc_shift[kWSCap][3];
-    CandW cand;
-    unsigned short queue[kQCap];  // (candidate lane, destination) pairs
     uint32_t code[kCodeCap];      // image q code per stencil cell of the bin
 };
 
@@ -187,8 +176,9 @@ __device__ __forceinline__ void bitonic64(uint32_t& k0, uint32_t& k1, int lane) 
 
 // Search, one WARP per destination bin (no CTA barriers).  Shared memory per
 // warp: WarpNL + the destination group (<= group atoms) + group x cap keys.
-__global__ void __launch_bounds__(kThreads) k_nl_search(
-    const Geom g, float thr32, int64_t nbins, int64_t n, int group, int cap,
+__global__ void __launch_bounds__(kThreads, 3) k_nl_search(
+    const Geom g, float thr32, float acc32, float zero32, int64_t nbins, int64_t n, int group,
+    int cap,
     const int32_t* __restrict__ bin_start, const int32_t* __restrict__ s_id,
     const double* __restrict__ s_w, const double* __restrict__ s_p,
     const int32_t* __restrict__ s_c, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
@@ -202,8 +192,6 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
     const size_t per_warp = ((head + dst_bytes + 15) & ~(size_t)15) + (size_t)group * cap * 4;
     unsigned char* base = smem_raw + (size_t)warp * per_warp;
     WarpNL& S = *reinterpret_cast<WarpNL*>(base);
-    CandW& C = S.cand;
-    unsigned short* Q = S.queue;
     size_t o = head;
     float4* d32 = reinterpret_cast<float4*>(base + o);
     o += sizeof(float4) * group;
@@ -309,85 +297,68 @@ __global__ void __launch_bounds__(kThreads) k_nl_search(
                     const int k = kb + lane;
                     const bool valid = k < total;
                     float c32x = 0.f, c32y = 0.f, c32z = 0.f;
+                    double cv[3] = {0.0, 0.0, 0.0};
+                    int ci = 0, slot = 0;
+                    uint32_t key = 0u;
                     if (valid) {
                         int lo = 0, hi = nc - 1;  // last stencil cell with pre <= k
                         while (lo < hi) {
                             const int mid = (lo + hi + 1) >> 1;
                             if (S.sc_pre[mid] <= k) lo = mid; else hi = mid - 1;
                         }
-                        const int ci = lo;
-                        const int slot = bin_start[S.sc_bin[ci]] + (k - S.sc_pre[ci]);
-                        double cv[3];
+                        ci = lo;
+                        slot = bin_start[S.sc_bin[ci]] + (k - S.sc_pre[ci]);
 #pragma unroll
-                        for (int d = 0; d < 3; ++d) {
-                            // candidate = wrapped_j + shift (neighborlist.cpp:176)
+                        for (int d = 0; d < 3; ++d)  // wrapped_j + shift (neighborlist.cpp:176)
                             cv[d] = add_rn(s_w[d * n + slot], S.sc_shift[ci][d]);
-                            C.c[d][lane] = cv[d];
-                            C.p[d][lane] = s_p[d * n + slot];
-                            C.nc[d][lane] = S.sc_q[ci][d] - s_c[d * n + slot];
-                        }
-                        C.jid[lane] = s_id[slot];
-                        C.cell[lane] = (unsigned)(cbase + ci);
+                        key = ((uint32_t)s_id[slot] << cbits) | (uint32_t)(cbase + ci);
                         c32x = (float)(cv[0] - org.x);
                         c32y = (float)(cv[1] - org.y);
                         c32z = (float)(cv[2] - org.z);
                     }
-                    // fp32 prefilter of this lane's candidate against every
-                    // destination of the group -> bitmask of survivors
+                    // fp32 test of this lane's candidate against every destination
+                    // of the group: |v32|^2 in (zero32, acc32] is inside both of the
+                    // reference's fp64 tests (and d2 != 0) with a proven margin ->
+                    // accepted here; (acc32, thr32] or <= zero32 is borderline ->
+                    // exact fp64 below; > thr32 is outside the fp64 prefilter.
                     unsigned mask = 0u;
                     if (valid) {
                         for (int t = 0; t < nd; ++t) {
                             const float4 dd = d32[t];
                             const float vx = c32x - dd.x, vy = c32y - dd.y, vz = c32z - dd.z;
-                            if (fmaf(vz, vz, fmaf(vy, vy, vx * vx)) <= thr32) mask |= 1u << t;
-                        }
-                    }
-                    // warp-wide compaction of the surviving (candidate, destination)
-                    // pairs, kQCap per round, then exact fp64 tests 32 at a time
-                    // (no divergence in the fp64 path)
-                    while (__any_sync(0xffffffffu, mask != 0u)) {
-                        const int mine = __popc(mask);
-                        int off = mine;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int u = __shfl_up_sync(0xffffffffu, off, o);
-                            if (lane >= o) off += u;
-                        }
-                        const int total = min(__shfl_sync(0xffffffffu, off, 31), kQCap);
-                        off -= mine;
-                        while (mask && off < kQCap) {
-                            const int t = __ffs(mask) - 1;
-                            mask &= mask - 1u;
-                            Q[off++] = (unsigned short)(lane | (t << 5));
-                        }
-                        __syncwarp();
-                        for (int q0 = 0; q0 < total; q0 += 32) {
-                            if (q0 + lane < total) {
-                                const unsigned ent = Q[q0 + lane];
-                                const int c = ent & 31, t = ent >> 5;
-                                const d3 v = {sub_rn(C.c[0][c], d_w[3 * t]),
-                                              sub_rn(C.c[1][c], d_w[3 * t + 1]),
-                                              sub_rn(C.c[2][c], d_w[3 * t + 2])};
-                                if (!(dot_rn(v, v) > g.pre2)) {  // neighborlist.cpp:177
-                                    const int o0 = C.nc[0][c] + d_c[3 * t];
-                                    const int o1 = C.nc[1][c] + d_c[3 * t + 1];
-                                    const int o2 = C.nc[2][c] + d_c[3 * t + 2];
-                                    const d3 raw =
-                                        rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
-                                    const d3 vr = {add_rn(sub_rn(C.p[0][c], d_p[3 * t]), raw.x),
-                                                   add_rn(sub_rn(C.p[1][c], d_p[3 * t + 1]), raw.y),
-                                                   add_rn(sub_rn(C.p[2][c], d_p[3 * t + 2]), raw.z)};
-                                    const double d2 = dot_rn(vr, vr);
-                                    if (!(d2 > g.cutoff2) && d2 != 0.0) {  // :189-190
-                                        const int pos = atomicAdd(&d_cnt[t], 1);
-                                        if (pos < cap)
-                                            keys[(size_t)t * cap + pos] =
-                                                ((uint32_t)C.jid[c] << cbits) | C.cell[c];
-                                    }
+                            const float d2 = fmaf(vz, vz, fmaf(vy, vy, vx * vx));
+                            if (d2 <= thr32) {
+                                if (d2 <= acc32 && d2 > zero32) {
+                                    const int pos = atomicAdd(&d_cnt[t], 1);
+                                    if (pos < cap) keys[(size_t)t * cap + pos] = key;
+                                } else {
+                                    mask |= 1u << t;
                                 }
                             }
                         }
-                        __syncwarp();
+                    }
+                    // borderline pairs: the reference's exact fp64 expressions
+                    // (rare: a band of relative width ~1e-5 around rc, and
+                    // coincident atoms)
+                    while (mask) {
+                        const int t = __ffs(mask) - 1;
+                        mask &= mask - 1u;
+                        const d3 v = {sub_rn(cv[0], d_w[3 * t]), sub_rn(cv[1], d_w[3 * t + 1]),
+                                      sub_rn(cv[2], d_w[3 * t + 2])};
+                        if (!(dot_rn(v, v) > g.pre2)) {  // neighborlist.cpp:177
+                            const int o0 = S.sc_q[ci][0] - s_c[slot] + d_c[3 * t];
+                            const int o1 = S.sc_q[ci][1] - s_c[n + slot] + d_c[3 * t + 1];
+                            const int o2 = S.sc_q[ci][2] - s_c[2 * n + slot] + d_c[3 * t + 2];
+                            const d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
+                            const d3 vr = {add_rn(sub_rn(s_p[slot], d_p[3 * t]), raw.x),
+                                           add_rn(sub_rn(s_p[n + slot], d_p[3 * t + 1]), raw.y),
+                                           add_rn(sub_rn(s_p[2 * n + slot], d_p[3 * t + 2]), raw.z)};
+                            const double d2 = dot_rn(vr, vr);
+                            if (!(d2 > g.cutoff2) && d2 != 0.0) {  // :189-190
+                                const int pos = atomicAdd(&d_cnt[t], 1);
+                                if (pos < cap) keys[(size_t)t * cap + pos] = key;
+                            }
+                        }
                     }
                     __syncwarp();
                 }
@@ -646,7 +617,8 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
     GMD_LAUNCH_CHECK();
 }
 
-void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
+void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int64_t nbins,
+                      int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s) {
     // destinations staged per warp: as many as fit three CTAs per SM (the
@@ -672,7 +644,8 @@ void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int 
     if (cbits > 31 || n > ((int64_t)1 << (32 - cbits)))
         raise(kConfig, "neighbour search: atom count too large for the " + std::to_string(ncell) +
                            "-cell stencil (row keys are src << " + std::to_string(cbits) + " | cell)");
-    k_nl_search<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, nbins, n, group, cap, b.bin_start,
+    k_nl_search<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, acc32, zero32, nbins, n, group, cap,
+                                                     b.bin_start,
                                                      b.s_id, b.s_w, b.s_p, b.s_c, b.deg, b.flags,
                                                      slab, owner, only, cbits);
     GMD_LAUNCH_CHECK();

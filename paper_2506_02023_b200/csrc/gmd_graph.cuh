@@ -56,7 +56,8 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
 // degrees into deg, max degree into flags[0] (slab rows truncated at cap)
 // only >= 0: rows only for destination atoms with owner[i] == only (the
 // other rows stay empty; deg must be zeroed by the caller)
-void launch_nl_search(const Geom& g, float thr32, int64_t nbins, int64_t n, int cap,
+void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int64_t nbins,
+                      int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s);
 // emit: slab rows -> CSR (row must hold the scanned degrees)

@@ -112,3 +112,24 @@ def test_deterministic_rebuild():
     b = gpu_graph(s, 3.5)
     for x, y in [(a.src, b.src), (a.image_offset, b.image_offset), (a.vector, b.vector)]:
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("rc", [5.0, 3.7])
+def test_cutoff_boundary_and_coincident_pairs(oracle_c, rc):
+    """Pairs straddling the cutoff within the fp32 fast-accept margin and the
+    reference's 1.000001 prefilter band, plus coincident atoms (d2 == 0):
+    these take the exact fp64 path and must match the oracle bit for bit."""
+    fac = [1 - 1e-4, 1 - 1e-6, 1 - 1e-8, 1.0, 1 + 1e-9, 1 + 1e-7, 1 + 4e-7, 1 + 9e-7,
+           1 + 2e-6, 1 + 1e-4]
+    pos = []
+    for i, f in enumerate(fac):  # pairs along x, far apart from each other
+        base = np.array([10.0 + 12.0 * (i % 5), 10.0 + 12.0 * (i // 5), 20.0])
+        pos += [base, base + [rc * f, 0.0, 0.0]]
+    pos += [[40.0, 40.0, 40.0], [40.0, 40.0, 40.0]]  # coincident pair
+    d = rc / np.sqrt(3.0)
+    pos += [[50.0, 50.0, 50.0], [50.0 + d, 50.0 + d, 50.0 + d]]  # |v| == rc in fp64 rounding
+    s = G.AtomicSystem(np.array(pos), np.diag([80.0, 80.0, 80.0]), np.ones(len(pos), np.int32))
+    g = gpu_graph(s, rc)
+    o = oracle_c.neighbor_list(*S.as_args(s), rc)
+    assert_same_graph(g, o)
+    assert len(g.src) > 0
