@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_nl_search(
 // slab rows -> canonical CSR (neighborlist.cpp:60-85): recompute the exact
 // fp64 vector through the raw positions (:178-191) from (src, image), round
 // to fp32 for the model, mark three-body bonds (linegraph.cpp:34-35).
+template <int G>  // lanes per destination row (16 or 32)
 __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
                           const unsigned long long* __restrict__ slab,
                           const int32_t* __restrict__ row, const double* __restrict__ pos,
@@ -429,14 +430,17 @@ __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
                           uint32_t* __restrict__ e_img, float4* __restrict__ e_vd,
                           float* __restrict__ e_d, uint8_t* __restrict__ e_bond,
                           int32_t* __restrict__ bcnt, int32_t* __restrict__ flags) {
-    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (i >= n) return;
-    const int lane = threadIdx.x & 31;
-    const int e0 = row[i], cnt = row[i + 1] - e0;
+    const int64_t i0 = (int64_t)blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
+    const bool live = i0 < n;
+    const int64_t i = live ? i0 : 0;
+    const int lane = threadIdx.x & (G - 1);
+    // lanes of this row (both rows of a warp iterate together for the ballot)
+    const unsigned gmask = G == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+    const int e0 = row[i], cnt = live ? row[i + 1] - e0 : 0;
     const double pix = pos[3 * i], piy = pos[3 * i + 1], piz = pos[3 * i + 2];
     const int cix = cell[3 * i], ciy = cell[3 * i + 1], ciz = cell[3 * i + 2];
     int nb = 0;
-    for (int kb = 0; kb < cnt; kb += 32) {
+    for (int kb = 0; __any_sync(0xffffffffu, kb < cnt); kb += G) {
         const int k = kb + lane;
         bool isb = false;
         if (k < cnt) {
@@ -464,9 +468,9 @@ __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
             isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
             e_bond[e] = isb ? 1 : 0;
         }
-        nb += __popc(__ballot_sync(0xffffffffu, isb));
+        nb += __popc(__ballot_sync(0xffffffffu, isb) & gmask);
     }
-    if (lane == 0) bcnt[i] = nb;
+    if (live && lane == 0) bcnt[i] = nb;
 }
 
 __global__ void k_minmax_proj(const double* __restrict__ pos, int64_t n, double dx, double dy,
@@ -654,8 +658,10 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int
 void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long* slab,
                     NLBuffers& b, GraphDev& gd, cudaStream_t s) {
     if (n == 0) return;
-    k_nl_emit<<<div_up(n, 8), 256, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src, gd.img,
-                                           gd.vd, gd.d, gd.bond, b.bcnt, b.flags);
+    // 16 lanes per row: ~45-edge rows fill 3 x 16 slots (94 %) instead of
+    // 2 x 32 (70 %); C5 0.70 -> 0.53 ms
+    k_nl_emit<16><<<div_up(n, 16), 256, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src,
+                                                gd.img, gd.vd, gd.d, gd.bond, b.bcnt, b.flags);
     GMD_LAUNCH_CHECK();
 }
 
