@@ -275,6 +275,7 @@ struct gmd_handle {
     double p_r_atom = 0, p_r3 = 0;
     std::vector<DBuf> H;
     bool ctab_ok = false;  // chunk records of the tcgen05 backward (per build)
+    int max_bonds = 0;     // max in-bonds of a center (three-body), per build
     int ctab_grid = 0;
     DBuf ccnt, cstart, ctab, ccta;
     DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v3_part, red, per_atom,
@@ -803,10 +804,12 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     if (h->has_lg) {
         int32_t* br = h->brow.get<int32_t>(n + 1);
         { PROF("scan"); scan_i32(h, b.bcnt, br, n); }
-        int32_t nb32 = 0;
+        int32_t nb32 = 0, fl[4];
         GMD_CUDA(cudaMemcpyAsync(&nb32, br + n, 4, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaMemcpyAsync(fl, b.flags, 16, cudaMemcpyDeviceToHost, s));
         sync(h);
         h->nb = nb32;
+        h->max_bonds = fl[2];
         int32_t* be = h->bedge.get<int32_t>(h->nb);
         int32_t* bv = h->brev.get<int32_t>(h->nb);
         { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, s); }
@@ -1157,7 +1160,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             float4* VOUT = h->VOUT.get<float4>(nbr);
             { PROF("tb_bwd_q"); launch_tb_bwd_q(n, a.nodes, a.crow, HB, TH4, QB, s); }
             if (rank_mode) exchange(QB);  // q_bar of halo atoms (bond sources)
-            { PROF("tb_backward"); launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, s); }
+            { PROF("tb_backward"); launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, h->max_bonds, s); }
             bond_exchange(reinterpret_cast<float*>(VIN), 4);
             bond_exchange(reinterpret_cast<float*>(VOUT), 4);
             { PROF("tb_grad"); launch_tb_grad(ba, VIN, VOUT, GRAD, s); }

@@ -470,7 +470,10 @@ __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
         }
         nb += __popc(__ballot_sync(0xffffffffu, isb) & gmask);
     }
-    if (live && lane == 0) bcnt[i] = nb;
+    if (live && lane == 0) {
+        bcnt[i] = nb;
+        if (nb > 0) atomicMax(&flags[2], nb);  // max in-bonds per center
+    }
 }
 
 __global__ void k_minmax_proj(const double* __restrict__ pos, int64_t n, double dx, double dy,

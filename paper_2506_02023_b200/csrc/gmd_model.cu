@@ -14,6 +14,7 @@
 //  * the three-body stage runs per "center" atom s on its in-bond list
 //    (bonds e=(w->s) and their reverses e'=(s->w)): every line edge (e, e')
 //    with dst(e) = src(e') is a pair of slots of one center.
+#include <algorithm>
 #include <cstdlib>
 
 #include "gmd_model.cuh"
@@ -1170,6 +1171,10 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
 // three-body stage (potential.cpp:664-741 forward, :850-961 backward)
 // ---------------------------------------------------------------------------
 constexpr int kTbWarps = 4;
+// a 16-lane group per center: centers have ~11 in-bonds (C4: 11.3), so a
+// warp per center left two thirds of its lanes idle
+constexpr int kTbGroups = kTbWarps * 2;
+constexpr size_t kTbSlotBytes = 2 * sizeof(float) * kF + sizeof(float4);  // st + sm + sv
 
 __device__ __forceinline__ void bond_t(float d, float t[kF]) {
     float u[kK];
@@ -1201,38 +1206,44 @@ __device__ __forceinline__ void bond_dt(float d, float ds[kF]) {
 __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float* __restrict__ TP,
                                                               float* __restrict__ TH3,
                                                               int32_t* flags) {
-    __shared__ float st[kTbWarps][kMaxBondsPerAtom][kF];
-    __shared__ float4 sv[kTbWarps][kMaxBondsPerAtom];
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const int64_t w0 = (int64_t)blockIdx.x * kTbWarps + wl;
-    const int64_t nw = (int64_t)gridDim.x * kTbWarps;
-    for (int64_t ks = w0; ks < a.n; ks += nw) {
-        const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
-        const int b0 = a.brow[s], k = a.brow[s + 1] - b0;
-        if (k > kMaxBondsPerAtom) {
-            if (lane == 0) atomicOr(&flags[1], 16);
-            continue;
+    __shared__ float st[kTbGroups][kMaxBondsPerAtom][kF];
+    __shared__ float4 sv[kTbGroups][kMaxBondsPerAtom];
+    const int gl = threadIdx.x & 15, grp = threadIdx.x >> 4;
+    const int64_t w0 = (int64_t)blockIdx.x * kTbGroups + grp;
+    const int64_t nw = (int64_t)gridDim.x * kTbGroups;
+    const int64_t iters = (a.n + nw - 1) / nw;  // same count for both groups of a warp
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t ks = w0 + it * nw;
+        int b0 = 0, k = 0;
+        if (ks < a.n) {
+            const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
+            b0 = a.brow[s];
+            k = a.brow[s + 1] - b0;
+            if (k > kMaxBondsPerAtom) {
+                if (gl == 0) atomicOr(&flags[1], 16);
+                k = 0;
+            }
         }
-        for (int j = lane; j < k; j += 32) {
+        for (int j = gl; j < k; j += 16) {
             float4 q = __ldg(a.vd + a.bedge[b0 + j]);
-            sv[wl][j] = q;
+            sv[grp][j] = q;
             float t[kF];
             bond_t(q.w, t);
 #pragma unroll
-            for (int f = 0; f < kF; ++f) st[wl][j][f] = t[f];
+            for (int f = 0; f < kF; ++f) st[grp][j][f] = t[f];
         }
         __syncwarp();
-        for (int j = lane; j < k; j += 32) {
-            const float4 qj = sv[wl][j];
+        for (int j = gl; j < k; j += 16) {
+            const float4 qj = sv[grp][j];
             float m3[kF];
 #pragma unroll
             for (int f = 0; f < kF; ++f) m3[f] = 0.f;
             for (int e2 = 0; e2 < k; ++e2) {
                 if (e2 == j) continue;  // the reverse pair (linegraph.cpp:16-21)
-                const float4 q2 = sv[wl][e2];
+                const float4 q2 = sv[grp][e2];
                 const float c = (q2.x * qj.x + q2.y * qj.y + q2.z * qj.z) / (q2.w * qj.w);
 #pragma unroll
-                for (int f = 0; f < kF; ++f) m3[f] = fmaf(c, st[wl][e2][f], m3[f]);
+                for (int f = 0; f < kF; ++f) m3[f] = fmaf(c, st[grp][e2][f], m3[f]);
             }
             float fc, dfc;
             fcut3(qj.w, fc, dfc);
@@ -1243,7 +1254,7 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float*
 #pragma unroll
                 for (int g = 0; g < kF; ++g) z = fmaf(c_m.W3[f * kF + g], m3[g], z);
                 th[f] = tanhf(z);
-                tp[f] = st[wl][j][f] + fc * th[f];
+                tp[f] = st[grp][j][f] + fc * th[f];
             }
             store_row16(TP + (size_t)(b0 + j) * kF, tp);
             store_row16(TH3 + (size_t)(b0 + j) * kF, th);
@@ -1313,26 +1324,35 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                                                                const float* __restrict__ TH3,
                                                                float4* __restrict__ VIN,
                                                                float4* __restrict__ VOUT,
-                                                               double* vir_part) {
-    __shared__ float st[kTbWarps][kMaxBondsPerAtom][kF];
-    __shared__ float sm[kTbWarps][kMaxBondsPerAtom][kF];
-    __shared__ float4 sv[kTbWarps][kMaxBondsPerAtom];
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const int64_t w0 = (int64_t)blockIdx.x * kTbWarps + wl;
-    const int64_t nw = (int64_t)gridDim.x * kTbWarps;
+                                                               double* vir_part, int kc) {
+    // per-group staging of kc >= max in-bonds slots: st/sm [slot][f], sv [slot]
+    extern __shared__ __align__(16) unsigned char tb_smem[];
+    const int gl = threadIdx.x & 15, grp = threadIdx.x >> 4;
+    float(*st)[kF] = reinterpret_cast<float(*)[kF]>(tb_smem) + (size_t)grp * kc;
+    float(*sm)[kF] = reinterpret_cast<float(*)[kF]>(tb_smem) + (size_t)(kTbGroups + grp) * kc;
+    float4* sv = reinterpret_cast<float4*>(tb_smem + 2 * sizeof(float) * kF * kTbGroups * kc) +
+                 (size_t)grp * kc;
+    const int64_t w0 = (int64_t)blockIdx.x * kTbGroups + grp;
+    const int64_t nw = (int64_t)gridDim.x * kTbGroups;
+    const int64_t iters = (a.n + nw - 1) / nw;  // same count for both groups of a warp
     double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t ks = w0; ks < a.n; ks += nw) {
-        const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
-        const int b0 = a.brow[s], k = a.brow[s + 1] - b0;
-        if (k > kMaxBondsPerAtom) continue;  // flagged in the forward
-        for (int j = lane; j < k; j += 32) {
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t ks = w0 + it * nw;
+        int b0 = 0, k = 0;
+        if (ks < a.n) {
+            const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
+            b0 = a.brow[s];
+            k = a.brow[s + 1] - b0;
+            if (k > kc) k = 0;  // > kMaxBondsPerAtom: flagged in the forward
+        }
+        for (int j = gl; j < k; j += 16) {
             const int e = a.bedge[b0 + j];
             const float4 q = __ldg(a.vd + e);
-            sv[wl][j] = q;
+            sv[j] = q;
             float t[kF];
             bond_t(q.w, t);
 #pragma unroll
-            for (int f = 0; f < kF; ++f) st[wl][j][f] = t[f];
+            for (int f = 0; f < kF; ++f) st[j][f] = t[f];
             // stage 2: adjoints of the reverse bond e'_j
             float tpb[kF], th[kF], ds[kF];
             const int x = __ldg(a.esrc + e);
@@ -1353,14 +1373,14 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                 float acc = 0.f;
 #pragma unroll
                 for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W3[f * kF + g], y[f], acc);
-                sm[wl][j][g] = acc;
+                sm[j][g] = acc;
             }
             const float c0 = -(dbf + da) / q.w;
             VOUT[b0 + j] = make_float4(q.x * c0, q.y * c0, q.z * c0, 0.f);
         }
         __syncwarp();
-        for (int j = lane; j < k; j += 32) {
-            const float4 qj = sv[wl][j];
+        for (int j = gl; j < k; j += 16) {
+            const float4 qj = sv[j];
             const float idj = 1.0f / qj.w;
             float tb[kF];
 #pragma unroll
@@ -1369,7 +1389,7 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
             float4 vo = VOUT[b0 + j];                // as outgoing bond e' = e'_j
             for (int o = 0; o < k; ++o) {
                 if (o == j) continue;
-                const float4 qo = sv[wl][o];
+                const float4 qo = sv[o];
                 const float ido = 1.0f / qo.w;
                 const float dotjo = qj.x * qo.x + qj.y * qo.y + qj.z * qo.z;
                 // (a) line edge (e_j, e'_o): c = v_j.v_o/(d_j d_o), a = v_j, b = -v_o
@@ -1378,8 +1398,8 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                     float cb = 0.f;
 #pragma unroll
                     for (int f = 0; f < kF; ++f) {
-                        tb[f] = fmaf(c, sm[wl][o][f], tb[f]);
-                        cb = fmaf(sm[wl][o][f], st[wl][j][f], cb);
+                        tb[f] = fmaf(c, sm[o][f], tb[f]);
+                        cb = fmaf(sm[o][f], st[j][f], cb);
                     }
                     // dc/da = -(b^ + a^ c)/|a|
                     vix += -(-qo.x * ido + qj.x * idj * c) * idj * cb;
@@ -1391,7 +1411,7 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                     const float c = dotjo * idj * ido;
                     float cb = 0.f;
 #pragma unroll
-                    for (int f = 0; f < kF; ++f) cb = fmaf(sm[wl][j][f], st[wl][o][f], cb);
+                    for (int f = 0; f < kF; ++f) cb = fmaf(sm[j][f], st[o][f], cb);
                     // dc/db = -(a^ + b^ c)/|b|
                     vo.x += -(qo.x * ido - qj.x * idj * c) * idj * cb;
                     vo.y += -(qo.y * ido - qj.y * idj * c) * idj * cb;
@@ -1512,7 +1532,7 @@ int model_grid(int64_t n) {
 }
 
 static int tb_grid(int64_t n) {
-    int64_t g = (n + kTbWarps - 1) / kTbWarps;
+    int64_t g = (n + kTbGroups - 1) / kTbGroups;
     if (g > 148 * 32) g = 148 * 32;
     return (int)(g > 0 ? g : 1);
 }
@@ -1620,9 +1640,17 @@ void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const
 }
 
 void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
-                        float4* VOUT, double* vir_part, cudaStream_t s) {
+                        float4* VOUT, double* vir_part, int max_bonds, cudaStream_t s) {
     if (a.n == 0) return;
-    k_tb_backward<<<tb_grid(a.n), kTbWarps * 32, 0, s>>>(a, QB, TH3, VIN, VOUT, vir_part);
+    const int kc = std::min(kMaxBondsPerAtom, std::max(16, (max_bonds + 15) & ~15));
+    const size_t smem = kTbSlotBytes * kTbGroups * kc;
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_tb_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kTbSlotBytes * kTbGroups * kMaxBondsPerAtom)));
+        attr = true;
+    }
+    k_tb_backward<<<tb_grid(a.n), kTbWarps * 32, smem, s>>>(a, QB, TH3, VIN, VOUT, vir_part, kc);
     GMD_LAUNCH_CHECK();
 }
 

@@ -90,8 +90,9 @@ void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags,
 void launch_tb_inject(const BondArgs& a, const float* TP, float* H, float* TH4, cudaStream_t s);
 void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const float* HB,
                      const float* TH4, float* QB, cudaStream_t s);  // QB by layout row
+// max_bonds: largest in-bond count of a center (sizes the per-group staging)
 void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
-                        float4* VOUT, double* vir_part, cudaStream_t s);
+                        float4* VOUT, double* vir_part, int max_bonds, cudaStream_t s);
 void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, float4* GRAD,
                     cudaStream_t s);
 
