@@ -265,7 +265,7 @@ struct gmd_handle {
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
     DBuf row, src, img, vd, ed, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
-    DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp, flagtmp;
+    DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp, flagtmp, ebid;
     int nl_cap = 0;
 
     // model
@@ -812,8 +812,9 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         h->max_bonds = fl[2];
         int32_t* be = h->bedge.get<int32_t>(h->nb);
         int32_t* bv = h->brev.get<int32_t>(h->nb);
-        { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, s); }
-        { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, bv, b.flags, ownp, myrank, s); }
+        int32_t* ebid = h->ebid.get<int32_t>(std::max<int64_t>(1, h->ne));
+        { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, ebid, s); }
+        { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, ebid, bv, b.flags, ownp, myrank, s); }
         if (rank_mode) build_bond_rank_plan(h, ownp, myrank);
     }
     GMD_CUDA(cudaEventRecord(h->ev[1], s));
@@ -1305,7 +1306,7 @@ void gmd_destroy(gmd_handle* h) {
     DBuf* bufs[] = {&h->pos, &h->Z, &h->cell, &h->fw, &h->bin, &h->bin_cnt, &h->bin_start,
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ed, &h->ebond, &h->edst, &h->lsrc, &h->counts,
-                    &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge,
+                    &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge, &h->ebid,
                     &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->flagtmp, &h->nodes, &h->xsend, &h->sendbuf, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp,

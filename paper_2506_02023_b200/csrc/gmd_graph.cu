@@ -542,7 +542,7 @@ __global__ void k_export_graph(const Geom g, const double* __restrict__ pos, int
 // grouped by destination: bedge[brow[v] + k] = k-th bond edge into v
 __global__ void k_bond_edges(const int32_t* __restrict__ row, const uint8_t* __restrict__ ebond,
                              int64_t n, const int32_t* __restrict__ brow,
-                             int32_t* __restrict__ bedge) {
+                             int32_t* __restrict__ bedge, int32_t* __restrict__ ebid) {
     int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (v >= n) return;
     const int lane = threadIdx.x & 31;
@@ -551,7 +551,9 @@ __global__ void k_bond_edges(const int32_t* __restrict__ row, const uint8_t* __r
         int e = eb + lane;
         bool f = e < row[v + 1] && ebond[e];
         unsigned m = __ballot_sync(0xffffffffu, f);
-        if (f) bedge[base + __popc(m & ((1u << lane) - 1u))] = e;
+        const int id = base + __popc(m & ((1u << lane) - 1u));
+        if (f) bedge[id] = e;
+        if (e < row[v + 1]) ebid[e] = f ? id : -1;  // bond id of an edge (bond_of_edge)
         base += __popc(m);
     }
 }
@@ -561,7 +563,8 @@ __global__ void k_bond_edges(const int32_t* __restrict__ row, const uint8_t* __r
 __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
                            const int32_t* __restrict__ src, const uint32_t* __restrict__ img,
                            const uint8_t* __restrict__ ebond, const int32_t* __restrict__ brow,
-                           const int32_t* __restrict__ bedge, int32_t* __restrict__ brev,
+                           const int32_t* __restrict__ bedge, const int32_t* __restrict__ ebid,
+                           int32_t* __restrict__ brev,
                            int32_t* __restrict__ flags, const int32_t* __restrict__ owner,
                            int only) {
     int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -587,13 +590,8 @@ __global__ void k_bond_rev(int64_t n, const int32_t* __restrict__ row,
                 er = x;
                 break;
             }
-        int id = -1;
-        if (er >= 0 && ebond[er]) {
-            id = brow[w];
-            for (int x = row[w]; x < er; ++x) id += ebond[x];
-        } else {
-            atomicOr(&flags[1], 32);
-        }
+        const int id = er >= 0 ? ebid[er] : -1;
+        if (id < 0) atomicOr(&flags[1], 32);
         brev[b] = id;
     }
 }
@@ -698,18 +696,18 @@ void launch_export_graph(const Geom& g, const double* pos, const GraphDev& gd,
 
 
 void launch_bond_edges(const int32_t* row, const uint8_t* ebond, int64_t n, const int32_t* brow,
-                       int32_t* bedge, cudaStream_t s) {
+                       int32_t* bedge, int32_t* ebid, cudaStream_t s) {
     if (n == 0) return;
-    k_bond_edges<<<div_up(n, 8), 256, 0, s>>>(row, ebond, n, brow, bedge);
+    k_bond_edges<<<div_up(n, 8), 256, 0, s>>>(row, ebond, n, brow, bedge, ebid);
     GMD_LAUNCH_CHECK();
 }
 
 void launch_bond_rev(int64_t n, const GraphDev& gd, const int32_t* brow, const int32_t* bedge,
-                     int32_t* brev, int32_t* flags, const int32_t* owner, int only,
-                     cudaStream_t s) {
+                     const int32_t* ebid, int32_t* brev, int32_t* flags, const int32_t* owner,
+                     int only, cudaStream_t s) {
     if (n == 0) return;
-    k_bond_rev<<<div_up(n, 8), 256, 0, s>>>(n, gd.row, gd.src, gd.img, gd.bond, brow, bedge, brev,
-                                            flags, owner, only);
+    k_bond_rev<<<div_up(n, 8), 256, 0, s>>>(n, gd.row, gd.src, gd.img, gd.bond, brow, bedge, ebid,
+                                            brev, flags, owner, only);
     GMD_LAUNCH_CHECK();
 }
 

@@ -76,11 +76,11 @@ void launch_edge_dst(const int32_t* row, int64_t n, int32_t* edst, cudaStream_t 
 // bonds (three-body): bedge[brow[v]..brow[v+1]) = bond edges into v in edge
 // order; brev[b] = bond id of b's reverse bond
 void launch_bond_edges(const int32_t* row, const uint8_t* ebond, int64_t n, const int32_t* brow,
-                       int32_t* bedge, cudaStream_t s);
-// with only >= 0 (one rank per GPU) bonds whose source is owned elsewhere get
-// brev = -1; the rank bond plan points them at halo bond rows
+                       int32_t* bedge, int32_t* ebid, cudaStream_t s);
+// reverse bond per bond (linegraph.cpp:16-21) via binary search in the
+// reverse row + the edge -> bond id map of launch_bond_edges
 void launch_bond_rev(int64_t n, const GraphDev& gd, const int32_t* brow, const int32_t* bedge,
-                     int32_t* brev, int32_t* flags, const int32_t* owner, int only,
-                     cudaStream_t s);
+                     const int32_t* ebid, int32_t* brev, int32_t* flags, const int32_t* owner,
+                     int only, cudaStream_t s);
 
 }  // namespace gmd
