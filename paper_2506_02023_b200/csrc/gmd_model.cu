@@ -1235,15 +1235,22 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float*
         __syncwarp();
         for (int j = gl; j < k; j += 16) {
             const float4 qj = sv[grp][j];
-            float m3[kF];
+            float2 m32[kF / 2];  // feature pairs, packed FP32
 #pragma unroll
-            for (int f = 0; f < kF; ++f) m3[f] = 0.f;
+            for (int i = 0; i < kF / 2; ++i) m32[i] = make_float2(0.f, 0.f);
             for (int e2 = 0; e2 < k; ++e2) {
                 if (e2 == j) continue;  // the reverse pair (linegraph.cpp:16-21)
                 const float4 q2 = sv[grp][e2];
                 const float c = (q2.x * qj.x + q2.y * qj.y + q2.z * qj.z) / (q2.w * qj.w);
+                const float2* t2 = reinterpret_cast<const float2*>(st[grp][e2]);
 #pragma unroll
-                for (int f = 0; f < kF; ++f) m3[f] = fmaf(c, st[grp][e2][f], m3[f]);
+                for (int i = 0; i < kF / 2; ++i) m32[i] = f2fma(bcast(c), t2[i], m32[i]);
+            }
+            float m3[kF];
+#pragma unroll
+            for (int i = 0; i < kF / 2; ++i) {
+                m3[2 * i] = m32[i].x;
+                m3[2 * i + 1] = m32[i].y;
             }
             float fc, dfc;
             fcut3(qj.w, fc, dfc);
@@ -1382,9 +1389,11 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
         for (int j = gl; j < k; j += 16) {
             const float4 qj = sv[j];
             const float idj = 1.0f / qj.w;
-            float tb[kF];
+            float2 tb2[kF / 2];
 #pragma unroll
-            for (int f = 0; f < kF; ++f) tb[f] = 0.f;
+            for (int i = 0; i < kF / 2; ++i) tb2[i] = make_float2(0.f, 0.f);
+            const float2* stj = reinterpret_cast<const float2*>(st[j]);
+            const float2* smj = reinterpret_cast<const float2*>(sm[j]);
             float vix = 0.f, viy = 0.f, viz = 0.f;  // as incoming bond e = e_j
             float4 vo = VOUT[b0 + j];                // as outgoing bond e' = e'_j
             for (int o = 0; o < k; ++o) {
@@ -1395,12 +1404,14 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                 // (a) line edge (e_j, e'_o): c = v_j.v_o/(d_j d_o), a = v_j, b = -v_o
                 {
                     const float c = dotjo * idj * ido;
-                    float cb = 0.f;
+                    const float2* smo = reinterpret_cast<const float2*>(sm[o]);
+                    float2 cb2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int f = 0; f < kF; ++f) {
-                        tb[f] = fmaf(c, sm[o][f], tb[f]);
-                        cb = fmaf(sm[o][f], st[j][f], cb);
+                    for (int i = 0; i < kF / 2; ++i) {
+                        tb2[i] = f2fma(bcast(c), smo[i], tb2[i]);
+                        cb2 = f2fma(smo[i], stj[i], cb2);
                     }
+                    const float cb = cb2.x + cb2.y;
                     // dc/da = -(b^ + a^ c)/|a|
                     vix += -(-qo.x * ido + qj.x * idj * c) * idj * cb;
                     viy += -(-qo.y * ido + qj.y * idj * c) * idj * cb;
@@ -1409,9 +1420,11 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                 // (b) line edge (e_o, e'_j): a = v_o, b = -v_j
                 {
                     const float c = dotjo * idj * ido;
-                    float cb = 0.f;
+                    const float2* sto = reinterpret_cast<const float2*>(st[o]);
+                    float2 cb2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int f = 0; f < kF; ++f) cb = fmaf(sm[j][f], st[o][f], cb);
+                    for (int i = 0; i < kF / 2; ++i) cb2 = f2fma(smj[i], sto[i], cb2);
+                    const float cb = cb2.x + cb2.y;
                     // dc/db = -(a^ + b^ c)/|b|
                     vo.x += -(qo.x * ido - qj.x * idj * c) * idj * cb;
                     vo.y += -(qo.y * ido - qj.y * idj * c) * idj * cb;
@@ -1422,7 +1435,10 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
             bond_dt(qj.w, ds);
             float db = 0.f;
 #pragma unroll
-            for (int f = 0; f < kF; ++f) db = fmaf(tb[f], ds[f], db);
+            for (int i = 0; i < kF / 2; ++i) {
+                db = fmaf(tb2[i].x, ds[2 * i], db);
+                db = fmaf(tb2[i].y, ds[2 * i + 1], db);
+            }
             vix += qj.x * db * idj;
             viy += qj.y * db * idj;
             viz += qj.z * db * idj;
