@@ -283,6 +283,7 @@ struct gmd_handle {
     DBuf md_part, md_out, md_bad;  // on-device MD observables / non-finite flag
     DBuf md_pos, md_vel, md_frc, md_mass, md_z;  // device state of gmd_md_run
     cudaEvent_t ev[8] = {};
+    cudaStream_t side = nullptr;  // D2H of per-atom energies during the backward
 
     // one rank per GPU: transport + this rank's plan
     std::unique_ptr<Transport> comm;
@@ -1140,6 +1141,13 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                     l == L - 1 ? e_part : nullptr, s);
     }
     GMD_CUDA(cudaEventRecord(h->ev[4], s));
+    // per-atom energies are final after the forward: copy them to the host
+    // while the backward runs (e2e use with host buffers)
+    const bool pa_early = per_atom && !(flags & GMD_OUTPUT_DEVICE) && !(flags & GMD_OUTPUT_F32);
+    if (pa_early) {
+        GMD_CUDA(cudaStreamWaitEvent(h->side, h->ev[4], 0));
+        GMD_CUDA(cudaMemcpyAsync(per_atom, pa, 8 * n_all, cudaMemcpyDeviceToHost, h->side));
+    }
 
     // ---- backward (:796-984)
     launch_init_hbar(n, HB, s);
@@ -1201,9 +1209,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             GMD_LAUNCH_CHECK();
             if (!out_dev)
                 GMD_CUDA(cudaMemcpyAsync(per_atom, dst, 4 * n_all, cudaMemcpyDeviceToHost, s));
+        } else if (out_dev) {
+            GMD_CUDA(cudaMemcpyAsync(per_atom, pa, 8 * n_all, cudaMemcpyDeviceToDevice, s));
         } else {
-            GMD_CUDA(cudaMemcpyAsync(per_atom, pa, 8 * n_all, out_dev ? cudaMemcpyDeviceToDevice
-                                                                      : cudaMemcpyDeviceToHost, s));
+            GMD_CUDA(cudaStreamSynchronize(h->side));  // pa_early copy
         }
     }
     if (forces && !out_dev) {
@@ -1289,6 +1298,7 @@ int gmd_create(int device, gmd_handle** out) {
         if (device < 0 || device >= ndev) raise(kArg, "device ordinal out of range");
         GMD_CUDA(cudaSetDevice(device));
         GMD_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        GMD_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         for (auto& e : h->ev) GMD_CUDA(cudaEventCreate(&e));
     } catch (const Status& e) {
         g_err = e.what();
@@ -1324,6 +1334,7 @@ void gmd_destroy(gmd_handle* h) {
         if (e) cudaEventDestroy(e);
     for (auto& e : h->pev) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->side) cudaStreamDestroy(h->side);
     delete h;
 }
 
