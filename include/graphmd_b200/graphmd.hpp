@@ -13,6 +13,8 @@
 #include <array>
 #include <cctype>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <cstdint>
 #include <memory>
@@ -135,6 +137,16 @@ struct AtomGraph {  // neighborlist.hpp:17-33
         while (e < dst.size() && dst[e] == node) ++e;
         return {lo, e};
     }
+    // neighborlist.cpp:97-106
+    void dump_csv(const std::string& path) const {
+        std::ofstream out(path);
+        if (!out) throw Error("cannot write file: " + path);
+        out.precision(17);
+        out << "src,dst,ox,oy,oz,distance\n";
+        for (std::size_t e = 0; e < num_edges(); ++e)
+            out << src[e] << "," << dst[e] << "," << image_offset[e][0] << ","
+                << image_offset[e][1] << "," << image_offset[e][2] << "," << distance[e] << "\n";
+    }
 };
 
 struct PartitionRule {  // partitioner.hpp:16-20
@@ -201,7 +213,71 @@ struct PartitionedLineGraph {
     Buckets bond_buckets;
     std::vector<LineGraphPartition> parts;
     int p = 1;
+    // linegraph.cpp:173-181
+    void dump_csv(const std::string& path) const {
+        std::ofstream out(path);
+        if (!out) throw Error("cannot write file: " + path);
+        out << "partition,bond_e_global,bond_ep_global\n";
+        for (int i = 0; i < p; ++i)
+            for (const auto& [le, lep] : parts[i].line_edges)
+                out << i << "," << parts[i].layout.node_array[le] << ","
+                    << parts[i].layout.node_array[lep] << "\n";
+    }
 };
+
+namespace detail {
+// the reference's JSON layout with dump(2): sorted keys, two-space indent,
+// integer arrays inline, other arrays one element per line
+inline std::string json_ints(const std::vector<std::int64_t>& v) {
+    std::string s = "[";
+    for (std::size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+    return s + "]";
+}
+inline std::string json_lines(const std::vector<std::string>& items, int ind) {
+    if (items.empty()) return "[]";
+    std::string pad(2 * ind, ' '), pad1(2 * ind + 2, ' '), s = "[\n";
+    for (std::size_t i = 0; i < items.size(); ++i) s += pad1 + items[i] + (i + 1 < items.size() ? ",\n" : "\n");
+    return s + pad + "]";
+}
+inline std::string json_double(double x) {  // shortest round-trip, ".0" for integral values
+    char buf[32];
+    for (int prec = 1; prec <= 17; ++prec) {
+        std::snprintf(buf, sizeof buf, "%.*g", prec, x);
+        if (std::strtod(buf, nullptr) == x) break;
+    }
+    std::string s(buf);
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    return s;
+}
+}  // namespace detail
+
+// partitioner.cpp:220-236
+inline std::string partition_plan_to_json(const PartitionedAtomGraph& parts) {
+    using detail::json_ints;
+    using detail::json_lines;
+    auto nested = [](const std::vector<std::vector<std::int64_t>>& v, int ind) {
+        std::vector<std::string> it;
+        for (const auto& x : v) it.push_back(json_ints(x));
+        return json_lines(it, ind);
+    };
+    auto nested2 = [&](const std::vector<std::vector<std::vector<std::int64_t>>>& v) {
+        std::vector<std::string> it;
+        for (const auto& x : v) it.push_back(nested(x, 2));
+        return json_lines(it, 1);
+    };
+    std::vector<std::string> b, pj;
+    for (double x : parts.rule.boundaries) b.push_back(detail::json_double(x));
+    for (const AtomPartition& part : parts.parts)
+        pj.push_back("{\n      \"markers\": " + json_ints(part.layout.markers) +
+                     ",\n      \"node_array\": " + json_ints(part.layout.node_array) +
+                     ",\n      \"owned_edge_count\": " + std::to_string(part.owned_edges.size()) +
+                     "\n    }");
+    return "{\n  \"axis\": " + std::to_string(parts.rule.axis) + ",\n  \"boundaries\": " +
+           json_lines(b, 1) + ",\n  \"from\": " + nested2(parts.buckets.from) +
+           ",\n  \"p\": " + std::to_string(parts.p) + ",\n  \"partitions\": " + json_lines(pj, 1) +
+           ",\n  \"pure\": " + nested(parts.buckets.pure, 1) + ",\n  \"to\": " +
+           nested2(parts.buckets.to) + "\n}";
+}
 
 // ---- engine (engine.hpp:18-151) -----------------------------------------
 struct DistributedFeatures {

@@ -101,6 +101,10 @@ class Oracle:
         else:
             self._md = f("md_run", I, _i64, V, V, V, V, I, I, I, D, D, V, D, _i64, I, D, U, V, V,
                          V, V)
+        if backend == "ref":
+            self._dump_graph = f("dump_graph", I, V, C.c_char_p)
+            self._dump_line = f("dump_line", I, V, C.c_char_p)
+            self._plan_json = f("plan_json", _i64, V, V, _i64)
         self._g_ne = f("graph_num_edges", _i64, V)
         self._g_get = f("graph_get", None, V, V, V, V, V, V)
         self._g_free = f("graph_destroy", None, V)
@@ -219,6 +223,21 @@ class Oracle:
 
 class OracleDist:
     """Snapshot of a create_distributed result as numpy arrays."""
+
+    # the reference's own dump formats (backend "ref" only)
+    def dump_graph(self, path):
+        if self.o._dump_graph(self.h, path.encode()):
+            raise OracleError(self.o.error())
+
+    def dump_line(self, path):
+        if self.o._dump_line(self.h, path.encode()):
+            raise OracleError(self.o.error())
+
+    def plan_json(self) -> str:
+        n = self.o._plan_json(self.h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        self.o._plan_json(self.h, buf, n + 1)
+        return buf.value.decode()
 
     def __init__(self, o: Oracle, h, p):
         self.o, self.h, self.p = o, h, p

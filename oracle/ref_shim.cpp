@@ -437,4 +437,30 @@ int gref_md_run(int64_t n, const double* pos, const int32_t* z, const double* la
     GUARD_END(1)
 }
 
+// the reference's own dump formats (neighborlist.cpp:97-106,
+// linegraph.cpp:173-181, partitioner.cpp:220-236)
+int gref_dump_graph(void* h, const char* path) {
+    GUARD_BEGIN
+    static_cast<Handle*>(h)->dist.graph().dump_csv(path);
+    return 0;
+    GUARD_END(1)
+}
+int gref_dump_line(void* h, const char* path) {
+    GUARD_BEGIN
+    static_cast<Handle*>(h)->dist.line_parts().dump_csv(path);
+    return 0;
+    GUARD_END(1)
+}
+int64_t gref_plan_json(void* h, char* buf, int64_t cap) {
+    std::string js;
+    try {
+        js = partition_plan_to_json(static_cast<Handle*>(h)->dist.atom_parts());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+    if ((int64_t)js.size() < cap) std::memcpy(buf, js.c_str(), js.size() + 1);
+    return (int64_t)js.size();
+}
+
 }  // extern "C"

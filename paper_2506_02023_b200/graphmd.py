@@ -336,6 +336,16 @@ class AtomGraph:
         hi = int(np.searchsorted(self.dst, node, "right"))
         return lo, hi
 
+    def dump_csv(self, path: str) -> None:
+        """AtomGraph::dump_csv (neighborlist.cpp:97-106): src,dst,ox,oy,oz,distance
+        with 17 significant digits."""
+        with open(path, "w") as f:
+            f.write("src,dst,ox,oy,oz,distance\n")
+            off = self.image_offset
+            f.writelines(f"{s},{d},{o[0]},{o[1]},{o[2]},{x:.17g}\n"
+                         for s, d, o, x in zip(self.src.tolist(), self.dst.tolist(), off.tolist(),
+                                               self.distance.tolist()))
+
 
 @dataclass
 class PartitionRule:
@@ -436,6 +446,57 @@ class PartitionedLineGraph:
     bond_buckets: Buckets
     parts: List[LineGraphPartition]
     p: int
+
+    def dump_csv(self, path: str) -> None:
+        """PartitionedLineGraph::dump_csv (linegraph.cpp:173-181): one line edge
+        per row as (partition, global bond e, global bond e')."""
+        with open(path, "w") as f:
+            f.write("partition,bond_e_global,bond_ep_global\n")
+            for i, part in enumerate(self.parts):
+                na = part.layout.node_array
+                le = np.asarray(part.line_edges).reshape(-1, 2)
+                f.writelines(f"{i},{a},{b}\n" for a, b in zip(na[le[:, 0]].tolist(),
+                                                            na[le[:, 1]].tolist()))
+
+
+def partition_plan_to_json(parts: "PartitionedAtomGraph") -> str:
+    """partition_plan_to_json (partitioner.cpp:220-236): the reference's
+    nlohmann dump(2) layout (sorted keys, two-space indent)."""
+    import json
+
+    def lists(x):
+        return [[int(v) for v in np.asarray(a).ravel()] for a in x]
+
+    j = {"p": int(parts.p), "axis": int(parts.rule.axis),
+         "boundaries": [float(b) for b in parts.rule.boundaries],
+         "pure": lists(parts.buckets.pure),
+         "to": [lists(row) for row in parts.buckets.to],
+         "from": [lists(row) for row in parts.buckets.frm],
+         "partitions": [{"node_array": [int(v) for v in pt.layout.node_array],
+                         "markers": [int(v) for v in pt.layout.markers],
+                         "owned_edge_count": int(len(pt.owned_edges))} for pt in parts.parts]}
+    return _json_dump2(j, 0)
+
+
+def _json_dump2(v, ind: int) -> str:
+    """The layout the reference's JSON writer produces with dump(2): sorted
+    keys, two-space indent, arrays of integers on one line, other arrays one
+    element per line."""
+    pad, pad1 = "  " * ind, "  " * (ind + 1)
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        items = [f'{pad1}"{k}": {_json_dump2(v[k], ind + 1)}' for k in sorted(v)]
+        return "{\n" + ",\n".join(items) + "\n" + pad + "}"
+    if isinstance(v, list):
+        if not v:
+            return "[]"
+        if all(isinstance(x, int) and not isinstance(x, bool) for x in v):
+            return "[" + ",".join(str(x) for x in v) + "]"
+        return "[\n" + ",\n".join(pad1 + _json_dump2(x, ind + 1) for x in v) + "\n" + pad + "]"
+    if isinstance(v, float):
+        return repr(v)
+    return str(v)
 
 
 class DistributedFeatures:

@@ -416,7 +416,23 @@ TEST(md_run_vs_oracle) {
     CHECK_THROWS(velocity_verlet_step(fresh, prm, o));  // no forces yet
 }
 
+// dump formats through the header (compared with the reference's own dumps
+// by tests/test_dumps.py): test_cpp_api --dump DIR P
+static int dump_mode(const std::string& dir, int p) {
+    AtomicSystem s = random_perturb(make_supercell(quartz_cell(), {3, 3, 3}), 0.05, 1);
+    Distributed d = Distributed::create_distributed(s, 5.0, 3.0, p, 1, true);
+    d.graph().dump_csv(dir + "/g.csv");
+    d.line_parts().dump_csv(dir + "/l.csv");
+    std::FILE* f = std::fopen((dir + "/plan.json").c_str(), "w");
+    if (!f) return 2;
+    const std::string js = partition_plan_to_json(d.atom_parts());
+    std::fwrite(js.data(), 1, js.size(), f);
+    std::fclose(f);
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 3 && std::string(argv[1]) == "--dump") return dump_mode(argv[2], std::atoi(argv[3]));
     std::string only = argc > 1 ? argv[1] : "";
     for (auto& [name, fn] : registry()) {
         if (!only.empty() && name != only) continue;
