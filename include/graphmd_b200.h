@@ -176,6 +176,17 @@ int gmd_corrupt_transfer_plan_for_test(gmd_handle* h);
 int gmd_comm_nccl_id(uint8_t id[128]);
 int gmd_comm_init_nccl(gmd_handle* h, int rank, int world, const uint8_t id[128]);
 int gmd_comm_init_local(gmd_handle** handles, int world);
+/* CUDA-IPC peer transport for ranks on one node (one process per GPU, or
+ * several processes sharing a GPU): the halo rows of every exchange are
+ * stored straight into the receiving rank's window (P2P over NVLink), with
+ * stream-ordered flag handshakes -- no NCCL, no host round trip.
+ * 1. gmd_comm_ipc_export: allocate this rank's window (slot_rows rows of 16
+ *    floats per peer, double-buffered) and get its 64-byte IPC handle;
+ * 2. all-gather the handles (rank order) over any host channel;
+ * 3. gmd_comm_init_ipc(h, handles[world x 64]) before gmd_build. */
+int gmd_comm_ipc_export(gmd_handle* h, int rank, int world, int64_t slot_rows,
+                        uint8_t handle[64]);
+int gmd_comm_init_ipc(gmd_handle* h, const uint8_t* handles);
 int gmd_comm_info(const gmd_handle* h, int* rank, int* world);
 int gmd_num_owned(const gmd_handle* h, int64_t* n);
 int gmd_get_owned_ids(gmd_handle* h, int64_t* ids);

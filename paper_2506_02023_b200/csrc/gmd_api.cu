@@ -284,6 +284,9 @@ struct gmd_handle {
     DBuf md_pos, md_vel, md_frc, md_mass, md_z;  // device state of gmd_md_run
     cudaEvent_t ev[8] = {};
     cudaStream_t side = nullptr;  // D2H of per-atom energies during the backward
+    void* ipc_window = nullptr;   // exported, not yet attached IPC window
+    int ipc_rank = 0, ipc_world = 1;
+    int64_t ipc_rows = 0;
 
     // one rank per GPU: transport + this rank's plan
     std::unique_ptr<Transport> comm;
@@ -1335,6 +1338,8 @@ void gmd_destroy(gmd_handle* h) {
     for (auto& e : h->pev) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->side) cudaStreamDestroy(h->side);
+    h->comm.reset();
+    if (h->ipc_window) cudaFree(h->ipc_window);
     delete h;
 }
 
@@ -1862,6 +1867,29 @@ int gmd_comm_init_nccl(gmd_handle* h, int rank, int world, const uint8_t id[128]
     return run(h, [&] {
         if (!id || world < 1 || rank < 0 || rank >= world) raise(kArg, "bad rank/world");
         h->comm.reset(make_nccl_transport(rank, world, id, h->device));
+        h->built = false;
+    });
+}
+
+int gmd_comm_ipc_export(gmd_handle* h, int rank, int world, int64_t slot_rows,
+                        uint8_t handle[64]) {
+    return run(h, [&] {
+        if (!handle || world < 1 || rank < 0 || rank >= world || slot_rows < 1)
+            raise(kArg, "bad rank/world/slot_rows");
+        if (h->ipc_window) cudaFree(h->ipc_window);
+        h->ipc_window = ipc_window_create(world, slot_rows, handle);
+        h->ipc_rank = rank;
+        h->ipc_world = world;
+        h->ipc_rows = slot_rows;
+    });
+}
+
+int gmd_comm_init_ipc(gmd_handle* h, const uint8_t* handles) {
+    return run(h, [&] {
+        if (!handles || !h->ipc_window) raise(kArg, "gmd_comm_ipc_export first");
+        h->comm.reset(make_ipc_transport(h->ipc_rank, h->ipc_world, h->device, h->ipc_rows,
+                                         h->ipc_window, handles));
+        h->ipc_window = nullptr;  // owned by the transport now
         h->built = false;
     });
 }

@@ -214,7 +214,238 @@ struct NcclTransport final : Transport {
     }
 };
 
+// ---------------------------------------------------------------------------
+// CUDA-IPC peer transport: every rank exposes one device "window" (flags,
+// all-gather slots, double-buffered halo staging) through cudaIpcMemHandle_t;
+// peers map it and write into it directly -- P2P stores over NVLink on a
+// multi-GPU node, plain device memory when the ranks share a GPU.  Per
+// exchange k (parity k & 1):
+//   send kernel   : wait until peer j consumed my exchange k-2 (ack), then the
+//                   packed rows for j are stored into j's staging[k&1][me]
+//   signal kernel : peer_j.ready[me] = k   (release, system scope)
+//   recv kernel   : wait until ready[j] >= k for every peer, then copy
+//                   staging[k&1][j] -> recv + roff[j] * width
+//   ack kernel    : peer_j.ack[me] = k
+// All four are stream-ordered on the handle's stream; no host round trip.
+// ---------------------------------------------------------------------------
+constexpr int kIpcMaxWorld = 16;
+constexpr size_t kIpcFlags = 4 * 64 * sizeof(long long);   // ready, ack, gready, gack
+constexpr size_t kIpcGather = 64 * 32 * sizeof(double);    // all-gather slots
+constexpr int kIpcGatherMax = 32;
+
+struct IpcWin {  // views of one rank's window
+    long long* ready;
+    long long* ack;
+    long long* gready;
+    long long* gack;
+    double* gather;  // [src][32]
+    float* staging;  // [2][world][slot_rows * 16]
+};
+
+__host__ __device__ inline IpcWin ipc_view(void* base) {
+    char* b = static_cast<char*>(base);
+    IpcWin w;
+    w.ready = reinterpret_cast<long long*>(b);
+    w.ack = w.ready + 64;
+    w.gready = w.ready + 128;
+    w.gack = w.ready + 192;
+    w.gather = reinterpret_cast<double*>(b + kIpcFlags);
+    w.staging = reinterpret_cast<float*>(b + kIpcFlags + kIpcGather);
+    return w;
+}
+
+__device__ __forceinline__ long long ld_acquire(const long long* p) {
+    long long v;
+    asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(long long* p, long long v) {
+    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// block-wide wait until flags[idx[i]] >= v for i < n (thread 0 spins)
+__device__ void wait_flags(long long* const* flags, int n, long long v) {
+    if (threadIdx.x == 0)
+        for (int i = 0; i < n; ++i)
+            while (ld_acquire(flags[i]) < v) __nanosleep(256);
+    __syncthreads();
+}
+
+struct IpcPeers {
+    int n;                          // peers (world - 1)
+    long long* wflag[kIpcMaxWorld];  // flag to wait on, per peer
+    long long* sflag[kIpcMaxWorld];  // flag to set, per peer
+    float* dst[kIpcMaxWorld];
+    const float* src[kIpcMaxWorld];
+    long long cnt[kIpcMaxWorld];     // floats per peer
+};
+
+__global__ void k_ipc_copy(IpcPeers P, long long wait_v) {
+    if (wait_v > 0) wait_flags(P.wflag, P.n, wait_v);
+    for (int j = 0; j < P.n; ++j) {
+        const long long c = P.cnt[j];
+        const float4* src = reinterpret_cast<const float4*>(P.src[j]);
+        float4* dst = reinterpret_cast<float4*>(P.dst[j]);
+        const long long c4 = c >> 2;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c4;
+             i += (long long)gridDim.x * blockDim.x)
+            dst[i] = __ldcg(src + i);
+        for (long long i = (c4 << 2) + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c;
+             i += (long long)gridDim.x * blockDim.x)
+            P.dst[j][i] = __ldcg(P.src[j] + i);
+    }
+    __threadfence_system();
+}
+
+__global__ void k_ipc_signal(IpcPeers P, long long v) {
+    if (threadIdx.x < P.n) st_release(P.sflag[threadIdx.x], v);
+}
+
+struct IpcTransport final : Transport {
+    int device = 0;
+    int64_t slot_rows = 0;
+    void* mine = nullptr;                       // this rank's window (owned)
+    std::vector<void*> peer;                    // mapped windows (peer[rank] = mine)
+    long long epoch = 0, gepoch = 0;
+    explicit IpcTransport(int r, int w, int dev, int64_t rows, void* win) {
+        rank = r;
+        world = w;
+        device = dev;
+        slot_rows = rows;
+        mine = win;
+    }
+    ~IpcTransport() override {
+        for (int j = 0; j < world; ++j)
+            if (j != rank && peer.size() == (size_t)world && peer[j]) cudaIpcCloseMemHandle(peer[j]);
+        if (mine) cudaFree(mine);
+    }
+    const char* name() const override { return "ipc"; }
+
+    float* staging(void* base, int par, int slot) const {
+        return ipc_view(base).staging + ((size_t)par * world + slot) * (size_t)slot_rows * 16;
+    }
+
+    void exchange(cudaStream_t s, const float* send, const int64_t* soff, const int64_t* scnt,
+                  float* recv, const int64_t* roff, const int64_t* rcnt, int width) override {
+        const long long k = ++epoch;
+        const int par = (int)(k & 1);
+        IpcPeers snd{}, sig{}, rcv{}, ack{};
+        for (int j = 0; j < world; ++j) {
+            if (j == rank) continue;
+            if (scnt[j] * width > slot_rows * 16 || rcnt[j] * width > slot_rows * 16)
+                raise(kConfig, "IPC staging too small for the halo (raise staging_rows)");
+            const IpcWin pw = ipc_view(peer[j]), mw = ipc_view(mine);
+            const int i = snd.n;
+            snd.wflag[i] = mw.ack + j;  // j consumed my exchange k-2 (j writes my window)
+            snd.dst[i] = staging(peer[j], par, rank);
+            snd.src[i] = send + soff[j] * width;
+            snd.cnt[i] = scnt[j] * width;
+            sig.sflag[i] = pw.ready + rank;
+            rcv.wflag[i] = mw.ready + j;
+            rcv.dst[i] = recv + roff[j] * width;
+            rcv.src[i] = staging(mine, par, j);
+            rcv.cnt[i] = rcnt[j] * width;
+            ack.sflag[i] = pw.ack + rank;
+            snd.n = sig.n = rcv.n = ack.n = i + 1;
+        }
+        k_ipc_copy<<<148, 256, 0, s>>>(snd, k - 2);
+        GMD_LAUNCH_CHECK();
+        k_ipc_signal<<<1, 32, 0, s>>>(sig, k);
+        GMD_LAUNCH_CHECK();
+        k_ipc_copy<<<148, 256, 0, s>>>(rcv, k);
+        GMD_LAUNCH_CHECK();
+        // ack into each sender's window: it may reuse staging[k & 1][it] at k + 2
+        k_ipc_signal<<<1, 32, 0, s>>>(ack, k);
+        GMD_LAUNCH_CHECK();
+    }
+
+    void gather(cudaStream_t s, const void* in, int n, void* out) {
+        if (n > kIpcGatherMax) raise(kRuntime, "internal: IPC all-gather too large");
+        const long long k = ++gepoch;
+        IpcPeers w{}, sig{};
+        for (int j = 0; j < world; ++j) {
+            if (j == rank) continue;
+            w.wflag[w.n++] = ipc_view(mine).gack + j;  // j read my previous payload
+        }
+        // my payload into every window's slot `rank` (mine included)
+        double* stage = ipc_view(mine).gather + (size_t)rank * 32;
+        GMD_CUDA(cudaMemcpyAsync(stage, in, 8 * n, cudaMemcpyHostToDevice, s));
+        IpcPeers cp{};
+        for (int j = 0; j < world; ++j) {
+            if (j == rank) continue;
+            const int i = cp.n++;
+            cp.wflag[i] = w.wflag[i];
+            cp.dst[i] = reinterpret_cast<float*>(ipc_view(peer[j]).gather + (size_t)rank * 32);
+            cp.src[i] = reinterpret_cast<const float*>(stage);
+            cp.cnt[i] = 2 * n;
+            sig.sflag[sig.n++] = ipc_view(peer[j]).gready + rank;
+        }
+        k_ipc_copy<<<1, 64, 0, s>>>(cp, k - 1);
+        GMD_LAUNCH_CHECK();
+        k_ipc_signal<<<1, 32, 0, s>>>(sig, k);
+        GMD_LAUNCH_CHECK();
+        IpcPeers rd{};
+        for (int j = 0; j < world; ++j)
+            if (j != rank) rd.wflag[rd.n++] = ipc_view(mine).gready + j;
+        k_ipc_copy<<<1, 32, 0, s>>>(rd, k);  // wait only (no copies)
+        GMD_LAUNCH_CHECK();
+        std::vector<double> all((size_t)world * 32);
+        GMD_CUDA(cudaMemcpyAsync(all.data(), ipc_view(mine).gather, 8 * all.size(),
+                                 cudaMemcpyDeviceToHost, s));
+        IpcPeers ak{};
+        for (int j = 0; j < world; ++j)
+            if (j != rank) ak.sflag[ak.n++] = ipc_view(peer[j]).gack + rank;
+        k_ipc_signal<<<1, 32, 0, s>>>(ak, k);
+        GMD_LAUNCH_CHECK();
+        GMD_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < world; ++j)
+            std::memcpy(static_cast<char*>(out) + (size_t)j * 8 * n, all.data() + (size_t)j * 32, 8 * n);
+    }
+    void allgather_f64(cudaStream_t s, const double* in, int n, double* out) override {
+        gather(s, in, n, out);
+    }
+    void allgather_i64(cudaStream_t s, const int64_t* in, int n, int64_t* out) override {
+        gather(s, in, n, out);
+    }
+};
+
 }  // namespace
+
+size_t ipc_window_bytes(int world, int64_t slot_rows) {
+    return kIpcFlags + kIpcGather + sizeof(float) * 2 * (size_t)world * (size_t)slot_rows * 16;
+}
+
+void* ipc_window_create(int world, int64_t slot_rows, unsigned char handle[64]) {
+    if (world < 1 || world > kIpcMaxWorld) raise(kConfig, "IPC transport supports 1..16 ranks");
+    void* w = nullptr;
+    GMD_CUDA(cudaMalloc(&w, ipc_window_bytes(world, slot_rows)));
+    GMD_CUDA(cudaMemset(w, 0, kIpcFlags + kIpcGather));
+    cudaIpcMemHandle_t hd;
+    GMD_CUDA(cudaIpcGetMemHandle(&hd, w));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    std::memcpy(handle, &hd, 64);
+    return w;
+}
+
+Transport* make_ipc_transport(int rank, int world, int device, int64_t slot_rows, void* window,
+                              const unsigned char* handles) {
+    auto* t = new IpcTransport(rank, world, device, slot_rows, window);
+    t->peer.assign(world, nullptr);
+    for (int j = 0; j < world; ++j) {
+        if (j == rank) {
+            t->peer[j] = window;
+            continue;
+        }
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, handles + 64 * (size_t)j, 64);
+        cudaError_t e = cudaIpcOpenMemHandle(&t->peer[j], hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            t->peer[j] = nullptr;
+            delete t;
+            raise(kCuda, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+    }
+    return t;
+}
 
 Transport* make_local_transport(LocalGroup* g, int rank) { return new LocalTransport(g, rank); }
 

@@ -8,6 +8,7 @@
 // no unpack is needed).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "gmd_common.cuh"
@@ -38,5 +39,13 @@ Transport* make_local_transport(LocalGroup* g, int rank);
 // NCCL (libnccl.so.2 loaded at run time; torch's bundled copy when present)
 bool nccl_unique_id(unsigned char id[128], std::string* err);
 Transport* make_nccl_transport(int rank, int world, const unsigned char id[128], int device);
+
+// CUDA-IPC peer transport for ranks on one node (P2P stores over NVLink):
+// ipc_window_create allocates this rank's window and returns its IPC handle;
+// after all ranks exchanged handles, make_ipc_transport maps the peers'.
+size_t ipc_window_bytes(int world, int64_t slot_rows);
+void* ipc_window_create(int world, int64_t slot_rows, unsigned char handle[64]);
+Transport* make_ipc_transport(int rank, int world, int device, int64_t slot_rows, void* window,
+                              const unsigned char* handles /* world x 64 bytes */);
 
 }  // namespace gmd

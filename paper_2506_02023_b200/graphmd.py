@@ -49,7 +49,7 @@ EXPORTS = [
     "gmd_profile", "gmd_profile_read", "gmd_get_stream", "gmd_launch_count", "gmd_comm_nccl_id",
     "gmd_comm_init_nccl", "gmd_comm_init_local", "gmd_comm_info", "gmd_num_owned", "gmd_get_owned_ids",
     "gmd_md_masses", "gmd_md_maxwell_boltzmann", "gmd_md_evaluate", "gmd_md_step", "gmd_md_observe",
-    "gmd_md_run",
+    "gmd_md_run", "gmd_comm_ipc_export", "gmd_comm_init_ipc",
 ]
 
 
@@ -130,6 +130,8 @@ def lib():
             "gmd_md_step": (I, [V, I64, V, V, V, V, V, V, V, D, D, D, D, I, U32, V, V]),
             "gmd_md_observe": (I, [V, I64, V, V, V, V, V]),
             "gmd_md_run": (I, [V, I64, V, V, V, V, V, V, D, I64, D, D, D, I, U32, V]),
+            "gmd_comm_ipc_export": (I, [V, I, I, I64, V]),
+            "gmd_comm_init_ipc": (I, [V, V]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -896,6 +898,24 @@ def init_rank_comm(handle: "_Handle", rank: int, world: int) -> None:
     """NCCL halo transport for this process's handle (one process per GPU)."""
     uid = nccl_unique_id() if rank == 0 else None
     comm_init_nccl(handle, rank, world, broadcast_bytes(uid, 0))
+
+
+def init_rank_comm_ipc(handle: "_Handle", rank: int, world: int, slot_rows: int) -> None:
+    """CUDA-IPC peer transport (ranks on one node): export this rank's window,
+    all-gather the 64-byte handles over the default torch.distributed group
+    (gloo or nccl), attach the peers' windows."""
+    import torch
+    import torch.distributed as dist
+    hd = (C.c_uint8 * 64)()
+    handle.check(lib().gmd_comm_ipc_export(handle.h, rank, world, slot_rows, hd))
+    mine = torch.tensor(list(bytes(hd)), dtype=torch.uint8)
+    if dist.get_backend() == "nccl":
+        mine = mine.cuda()
+    allh = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allh, mine)
+    blob = bytes(b for t in allh for b in t.cpu().tolist())
+    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+    handle.check(lib().gmd_comm_init_ipc(handle.h, buf))
 
 
 def exchange_plan_consistent(scnt, rcnt, rank: int, all_scnt) -> bool:
