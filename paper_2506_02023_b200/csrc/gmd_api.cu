@@ -1194,13 +1194,13 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         PROF("forces_out");
         launch_forces_out(n, a.nodes, GRAD, fd, ff, s);
     }
-    PROF("reduce");
-    launch_reduce_partials(e_part, grid, 1, red, s);
-    launch_reduce_partials(v_part, L * vgrid, 6, red + 1, s);
-    if (tb)
-        launch_reduce_partials(v3_part, tgrid, 9, red + 7, s);
-    else
-        GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
+    {
+        PROF("reduce");
+        const double* ps[3] = {e_part, v_part, v3_part};
+        const int np[3] = {grid, L * vgrid, tgrid}, w[3] = {1, 6, 9};
+        if (!tb) GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
+        launch_reduce_sets(tb ? 3 : 2, ps, np, w, red, s);
+    }
     GMD_CUDA(cudaEventRecord(h->ev[5], s));
 
     double hred[16];

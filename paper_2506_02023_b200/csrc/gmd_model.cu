@@ -1690,6 +1690,51 @@ void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, doub
     GMD_LAUNCH_CHECK();
 }
 
+// up to three partial sets in one launch: block c reduces output column c of
+// the set it falls in (same per-column arithmetic as k_reduce_partials)
+struct ReduceSets {
+    const double* parts[3];
+    int nparts[3], w[3], col0[3];
+    int nsets;
+};
+__global__ void __launch_bounds__(512) k_reduce_sets(ReduceSets R, double* out) {
+    int set = 0;
+    while (set + 1 < R.nsets && (int)blockIdx.x >= R.col0[set + 1]) ++set;
+    const int c = blockIdx.x - R.col0[set], w = R.w[set], np = R.nparts[set];
+    const double* parts = R.parts[set];
+    __shared__ double sh[512];
+    const int t = threadIdx.x;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int i = t;
+    for (; i + 3 * 512 < np; i += 4 * 512)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += parts[(size_t)(i + u * 512) * w + c];
+    for (; i < np; i += 512) acc[0] += parts[(size_t)i * w + c];
+    sh[t] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    __syncthreads();
+    for (int o = 256; o > 0; o >>= 1) {
+        if (t < o) sh[t] += sh[t + o];
+        __syncthreads();
+    }
+    if (t == 0) out[blockIdx.x] = sh[0];
+}
+
+void launch_reduce_sets(int nsets, const double* const* parts, const int* nparts, const int* w,
+                        double* out, cudaStream_t s) {
+    ReduceSets R{};
+    int cols = 0;
+    R.nsets = nsets;
+    for (int k = 0; k < nsets; ++k) {
+        R.parts[k] = parts[k];
+        R.nparts[k] = nparts[k];
+        R.w[k] = w[k];
+        R.col0[k] = cols;
+        cols += w[k];
+    }
+    k_reduce_sets<<<cols, 512, 0, s>>>(R, out);
+    GMD_LAUNCH_CHECK();
+}
+
 void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s) {
     k_reduce_partials<<<w, 512, 0, s>>>(parts, nparts, w, out);
     GMD_LAUNCH_CHECK();

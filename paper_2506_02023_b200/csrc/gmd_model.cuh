@@ -101,5 +101,8 @@ void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, doub
                        float* forces32, cudaStream_t s);
 // sum nparts consecutive records of width w into out[w] in fixed order
 void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s);
+// up to 3 partial sets [nparts[k] x w[k]] into consecutive columns of out
+void launch_reduce_sets(int nsets, const double* const* parts, const int* nparts, const int* w,
+                        double* out, cudaStream_t s);
 
 }  // namespace gmd
