@@ -1045,7 +1045,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     // backward edge pass: FFMA kernel, or the tcgen05 kernel with GMD_BWD_TC=1
     const char* tc_env = std::getenv("GMD_BWD_TC");
     const bool use_tc = tc_env && tc_env[0] == '1';
-    const int vgrid = use_tc ? bwd_tc_grid(n) : grid;
+    const int vgrid = use_tc ? bwd_tc_grid(n) : bwd_edge_grid(n);
     double* e_part = h->e_part.get<double>(grid);
     double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);
     const int tgrid = tb_grid_size(n);

@@ -169,9 +169,9 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // fixed-order CTA reduction of W doubles per thread-warp; lane 0 of each warp
 // deposits, thread 0 sums warps in order
-template <int W>
+template <int W, int NW = kWarpsPerCta>
 __device__ __forceinline__ void cta_partials(const double (&v)[W], double* out) {
-    __shared__ double red[kWarpsPerCta][W];
+    __shared__ double red[NW][W];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double s[W];
 #pragma unroll
@@ -592,15 +592,15 @@ __device__ __forceinline__ void conv_math2(const ConvIn& x, float2 acc[kF / 2]) 
     }
 }
 
-template <int CTAS>
-__global__ void __launch_bounds__(kThreads, CTAS) k_conv2(ConvArgs a, int layer,
+template <int CTAS, int NT = kThreads>
+__global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
                                                        const float* __restrict__ Hin,
                                                        float* __restrict__ Hout,
                                                        float* __restrict__ TH, double* per_atom,
                                                        double* e_part) {
     __shared__ float sW[kF][kF + 1];
     __shared__ float sb[kF], sro[kF];
-    for (int i = threadIdx.x; i < kF * kF; i += kThreads) sW[i / kF][i % kF] = c_m.W[layer][i];
+    for (int i = threadIdx.x; i < kF * kF; i += NT) sW[i / kF][i % kF] = c_m.W[layer][i];
     if (threadIdx.x < kF) {
         sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
         sro[threadIdx.x] = c_m.ro[threadIdx.x];
@@ -608,8 +608,8 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_conv2(ConvArgs a, int layer,
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int gl = lane & 15;
-    const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + (threadIdx.x >> 4);
-    const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
+    const int64_t g0 = (int64_t)blockIdx.x * (NT / 16) + (threadIdx.x >> 4);
+    const int64_t ng = (int64_t)gridDim.x * (NT / 16);
     double esum = 0.0;
     const int64_t iters = (a.n + ng - 1) / ng;
     // the next node's bounds and first slot's streams are requested at the
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_conv2(ConvArgs a, int layer,
     }
     if (e_part) {
         double vals[1] = {esum};
-        cta_partials<1>(vals, e_part);
+        cta_partials<1, NT / 32>(vals, e_part);
     }
 }
 
@@ -771,18 +771,18 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
     vr[5] = fmaf(ch * q.y, q.z, vr[5]);
 }
 
-template <int CTAS>
-__global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
+template <int CTAS, int NT = kThreads>
+__global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
                                                            const float* __restrict__ Hl,
                                                            float* __restrict__ HB,
                                                            float4* __restrict__ GRAD,
                                                            double* vir_part) {
-    __shared__ __align__(16) float sU[kNodesPerCta][2][kF];  // [group][m_bar_u, h_u][f]
-    __shared__ double sVir[kNodesPerCta][6];
+    __shared__ __align__(16) float sU[(NT / 16)][2][kF];  // [group][m_bar_u, h_u][f]
+    __shared__ double sVir[(NT / 16)][6];
     const int lane = threadIdx.x & 31;
     const int gl = lane & 15, grp = threadIdx.x >> 4;
-    const int64_t g0 = (int64_t)blockIdx.x * kNodesPerCta + grp;
-    const int64_t ng = (int64_t)gridDim.x * kNodesPerCta;
+    const int64_t g0 = (int64_t)blockIdx.x * (NT / 16) + grp;
+    const int64_t ng = (int64_t)gridDim.x * (NT / 16);
     const float isg = c_m.inv_sigma, mus = c_m.mu_step;
     if (gl < 6) sVir[grp][gl] = 0.0;
     const int64_t iters = (a.n + ng - 1) / ng;
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_bwd_edge2(ConvArgs a, const 
     __syncthreads();
     if (threadIdx.x < 6) {
         double acc6 = 0.0;
-        for (int g = 0; g < kNodesPerCta; ++g) acc6 += sVir[g][threadIdx.x];
+        for (int g = 0; g < (NT / 16); ++g) acc6 += sVir[g][threadIdx.x];
         vir_part[(size_t)blockIdx.x * 6 + threadIdx.x] = acc6;
     }
 }
@@ -1589,16 +1589,34 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
     GMD_LAUNCH_CHECK();
 }
 
+static int bwd_variant() {
+    const char* venv = std::getenv("GMD_BWD_VARIANT");  // read per call (tests switch kernels)
+    return venv ? std::atoi(venv) : 0;
+}
+
+// The default backward runs 768-thread CTAs, one per SM: the 48 consecutive
+// nodes a CTA works on share most neighbour rows, which then hit in the SM's
+// L1 (C5: 3.13 -> 2.98 ms per step vs 3 x 256-thread CTAs per SM; the
+// forward conv is faster with 256-thread CTAs).
+constexpr int kBwdThreads = 768;
+
+int bwd_edge_grid(int64_t n) {
+    if (bwd_variant() == 1) return model_grid(n);
+    const int64_t per = kBwdThreads / 16;
+    int64_t g = (n + per - 1) / per;
+    if (g > 148) g = 148;
+    return (int)(g > 0 ? g : 1);
+}
+
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
                      double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
-    const char* venv = std::getenv("GMD_BWD_VARIANT");  // read per call (tests switch kernels)
-    const int variant = venv ? std::atoi(venv) : 0;
-    const int g = model_grid(a.n);
+    const int variant = bwd_variant();
+    const int g = bwd_edge_grid(a.n);
     if (variant == 1)  // scalar-FFMA kernel (A/B reference)
         k_bwd_edge<<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
     else
-        k_bwd_edge2<3><<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+        k_bwd_edge2<1, kBwdThreads><<<g, kBwdThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
     GMD_LAUNCH_CHECK();
 }
 

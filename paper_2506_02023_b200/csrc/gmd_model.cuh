@@ -46,6 +46,7 @@ struct ConvArgs {
 };
 
 int model_grid(int64_t n);  // fixed grid => deterministic reductions
+int bwd_edge_grid(int64_t n);  // grid (= virial partial count) of launch_bwd_edge
 
 void launch_embed(int64_t rows, const int32_t* node_array, const int32_t* Z, float* H0,
                   cudaStream_t s);
