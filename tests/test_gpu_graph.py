@@ -133,3 +133,16 @@ def test_cutoff_boundary_and_coincident_pairs(oracle_c, rc):
     o = oracle_c.neighbor_list(*S.as_args(s), rc)
     assert_same_graph(g, o)
     assert len(g.src) > 0
+
+
+@pytest.mark.parametrize("shift", [3, 1 << 19, (1 << 20) + 5, 5_000_000])
+def test_far_images(oracle_c, shift):
+    """Atoms many lattice vectors outside the cell (a common shift plus a few
+    cells between atoms): large cell_of values, small relative images; the
+    graph matches the oracle bit for bit."""
+    s = S.random_system(60, (9.0, 8.0, 10.0), 21)
+    pos = s.positions + shift * s.lattice[0] - (shift // 2) * s.lattice[2]
+    pos[::3] += 3 * s.lattice[1]  # offsets between atoms stay in the packed image range
+    pos[1::7] -= 2 * s.lattice[0]
+    s = G.AtomicSystem(pos, s.lattice, s.species)
+    assert_same_graph(gpu_graph(s, 3.2), oracle_c.neighbor_list(*S.as_args(s), 3.2))
