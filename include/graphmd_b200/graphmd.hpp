@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <memory>
 #include <optional>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -114,6 +115,110 @@ inline AtomicSystem make_supercell(const AtomicSystem& s, const std::array<int, 
 inline AtomicSystem random_perturb(const AtomicSystem& s, double amplitude, std::uint64_t seed) {
     if (amplitude < 0.0) throw Error("perturbation amplitude must be >= 0");
     return make_supercell(s, {1, 1, 1}, amplitude, seed);
+}
+
+// ---- extended-XYZ I/O (system.cpp:95-186, docs/formats.md) ----------------
+namespace detail {
+inline const char* const* element_symbols() {  // index = atomic number, 0 = "X"
+    static const char* const s[119] = {
+        "X",  "H",  "He", "Li", "Be", "B",  "C",  "N",  "O",  "F",  "Ne", "Na", "Mg", "Al", "Si",
+        "P",  "S",  "Cl", "Ar", "K",  "Ca", "Sc", "Ti", "V",  "Cr", "Mn", "Fe", "Co", "Ni", "Cu",
+        "Zn", "Ga", "Ge", "As", "Se", "Br", "Kr", "Rb", "Sr", "Y",  "Zr", "Nb", "Mo", "Tc", "Ru",
+        "Rh", "Pd", "Ag", "Cd", "In", "Sn", "Sb", "Te", "I",  "Xe", "Cs", "Ba", "La", "Ce", "Pr",
+        "Nd", "Pm", "Sm", "Eu", "Gd", "Tb", "Dy", "Ho", "Er", "Tm", "Yb", "Lu", "Hf", "Ta", "W",
+        "Re", "Os", "Ir", "Pt", "Au", "Hg", "Tl", "Pb", "Bi", "Po", "At", "Rn", "Fr", "Ra", "Ac",
+        "Th", "Pa", "U",  "Np", "Pu", "Am", "Cm", "Bk", "Cf", "Es", "Fm", "Md", "No", "Lr", "Rf",
+        "Db", "Sg", "Bh", "Hs", "Mt", "Ds", "Rg", "Cn", "Nh", "Fl", "Mc", "Lv", "Ts", "Og"};
+    return s;
+}
+[[noreturn]] inline void parse_fail(const std::string& path, int line, const std::string& what) {
+    throw Error(path + ":" + std::to_string(line) + ": " + what);
+}
+}  // namespace detail
+
+inline const std::string& z_to_symbol(int z) {
+    static const std::vector<std::string> cache(detail::element_symbols(), detail::element_symbols() + 119);
+    if (z < 1 || z > 118) throw Error("atomic number out of range");
+    return cache[z];
+}
+
+// load_xyz: atom count, comment line with Lattice="..." (and optional
+// pbc="T T F"), then `Symbol x y z` lines
+inline AtomicSystem load_xyz(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw Error("cannot open file: " + path);
+    std::string line;
+    if (!std::getline(in, line)) detail::parse_fail(path, 1, "empty file");
+    std::size_t natoms = 0;
+    try {
+        natoms = std::stoul(line);
+    } catch (...) {
+        detail::parse_fail(path, 1, "expected atom count, got '" + line + "'");
+    }
+    if (!std::getline(in, line)) detail::parse_fail(path, 2, "missing comment line");
+    AtomicSystem sys;
+    const auto lat = line.find("Lattice=\"");
+    const bool have_lattice = lat != std::string::npos;
+    if (have_lattice) {
+        const auto b = lat + 9, e = line.find('"', b);
+        if (e == std::string::npos) detail::parse_fail(path, 2, "unterminated Lattice field");
+        std::istringstream ls(line.substr(b, e - b));
+        double v[9];
+        for (double& x : v)
+            if (!(ls >> x)) detail::parse_fail(path, 2, "Lattice needs 9 numbers");
+        for (int r = 0; r < 3; ++r) sys.lattice[r] = {v[3 * r], v[3 * r + 1], v[3 * r + 2]};
+    }
+    const auto pb = line.find("pbc=\"");
+    if (pb != std::string::npos) {
+        const auto b = pb + 5, e = line.find('"', b);
+        std::istringstream ps(line.substr(b, e == std::string::npos ? std::string::npos : e - b));
+        std::string tok;
+        for (int k = 0; k < 3; ++k) {
+            if (!(ps >> tok)) detail::parse_fail(path, 2, "pbc needs 3 flags");
+            sys.pbc[k] = tok == "T" || tok == "True" || tok == "true" || tok == "1";
+        }
+    }
+    if (!have_lattice) {
+        if (sys.any_pbc()) detail::parse_fail(path, 2, "periodic system requires a Lattice field");
+        sys.lattice = Mat3::identity();
+    }
+    const char* const* sym = detail::element_symbols();
+    for (std::size_t i = 0; i < natoms; ++i) {
+        const int lineno = (int)i + 3;
+        if (!std::getline(in, line)) detail::parse_fail(path, lineno, "unexpected end of file");
+        std::istringstream as(line);
+        std::string s;
+        double x, y, z;
+        if (!(as >> s >> x >> y >> z)) detail::parse_fail(path, lineno, "expected 'symbol x y z'");
+        int zz = 0;
+        for (int k = 1; k <= 118 && !zz; ++k)
+            if (s == sym[k]) zz = k;
+        if (!zz) detail::parse_fail(path, lineno, "unknown element symbol '" + s + "'");
+        sys.species.push_back(zz);
+        sys.positions.push_back({x, y, z});
+    }
+    sys.validate();
+    return sys;
+}
+
+// save_xyz: 17 significant digits (round-trips every double)
+inline void save_xyz(const AtomicSystem& system, const std::string& path,
+                     const std::string& comment_extra = "") {
+    std::ofstream out(path);
+    if (!out) throw Error("cannot write file: " + path);
+    out.precision(17);
+    out << system.size() << "\n";
+    out << "Lattice=\"";
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) out << system.lattice[i][k] << (i == 2 && k == 2 ? "" : " ");
+    out << "\" pbc=\"" << (system.pbc[0] ? "T" : "F") << " " << (system.pbc[1] ? "T" : "F") << " "
+        << (system.pbc[2] ? "T" : "F") << "\"";
+    if (!comment_extra.empty()) out << " " << comment_extra;
+    out << "\n";
+    for (std::size_t i = 0; i < system.size(); ++i) {
+        const Vec3& r = system.positions[i];
+        out << z_to_symbol(system.species[i]) << " " << r.x << " " << r.y << " " << r.z << "\n";
+    }
 }
 
 // ---- graph / partition / line-graph views -----------------------------
@@ -621,7 +726,78 @@ struct ToyPotentialParams {
             throw Error("parameter array has the wrong size");
     }
 
+    // binary parameter files (potential.cpp:178-260): GMPT, u32 version 1,
+    // u32 F K L flags, f64 r_atom r_3body, u64 seed, u64-counted tables
+    void save(const std::string& path) const {
+        validate();
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw Error("cannot write file: " + path);
+        out.write("GMPT", 4);
+        auto put = [&](const auto& v) { out.write(reinterpret_cast<const char*>(&v), sizeof v); };
+        put((std::uint32_t)1);
+        put((std::uint32_t)feature_width);
+        put((std::uint32_t)basis_count);
+        put((std::uint32_t)layers);
+        put((std::uint32_t)(threebody() ? 1u : 0u));
+        put(r_atom);
+        put(r_3body);
+        put(seed);
+        for (const auto* v : {&embedding, &layer_w, &layer_b, &basis_proj, &basis3_proj, &w3, &w4, &readout}) {
+            put((std::uint64_t)v->size());
+            out.write(reinterpret_cast<const char*>(v->data()), (std::streamsize)(v->size() * sizeof(double)));
+        }
+    }
+    static ToyPotentialParams load(const std::string& path) {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw Error("cannot open file: " + path);
+        char magic[4] = {};
+        in.read(magic, 4);
+        if (!in || std::string(magic, 4) != "GMPT") throw Error("bad parameter file magic");
+        auto get = [&](auto& v) { in.read(reinterpret_cast<char*>(&v), sizeof v); };
+        std::uint32_t ver = 0, F = 0, K = 0, L = 0, flags = 0;
+        get(ver);
+        if (!in || ver != 1) throw Error("unsupported parameter file version");
+        ToyPotentialParams p;
+        get(F);
+        get(K);
+        get(L);
+        get(flags);
+        get(p.r_atom);
+        get(p.r_3body);
+        get(p.seed);
+        p.feature_width = (int)F;
+        p.basis_count = (int)K;
+        p.layers = (int)L;
+        for (auto* v : {&p.embedding, &p.layer_w, &p.layer_b, &p.basis_proj, &p.basis3_proj, &p.w3, &p.w4, &p.readout}) {
+            std::uint64_t n = 0;
+            get(n);
+            if (!in) throw Error("truncated parameter file");
+            v->resize((std::size_t)n);
+            in.read(reinterpret_cast<char*>(v->data()), (std::streamsize)(n * sizeof(double)));
+        }
+        if (!in) throw Error("truncated parameter file");
+        p.validate_tables();
+        p.validate();
+        return p;
+    }
+
 private:
+    void validate_tables() const {  // potential.cpp:157-175 messages
+        const std::size_t F = feature_width, K = basis_count, L = layers;
+        auto expect = [](const std::vector<double>& v, std::size_t n, const char* name) {
+            if (v.size() != n) throw Error(std::string("parameter array ") + name + " has the wrong size");
+            for (double x : v)
+                if (!std::isfinite(x)) throw Error(std::string("parameter array ") + name + " contains a non-finite value");
+        };
+        expect(embedding, 119 * F, "embedding");
+        expect(layer_w, L * F * F, "layer_w");
+        expect(layer_b, L * F, "layer_b");
+        expect(basis_proj, F * K, "basis_proj");
+        expect(basis3_proj, F * K, "basis3_proj");
+        expect(w3, F * F, "w3");
+        expect(w4, F * F, "w4");
+        expect(readout, F, "readout");
+    }
     void unpack(const std::vector<double>& b) {
         const std::size_t F = feature_width, K = basis_count, L = layers;
         std::size_t o = 0;
@@ -670,6 +846,17 @@ inline PotentialOutput forward_distributed(const Distributed& dist, const ToyPot
         timing->backward_pass += tm[3];
     }
     return out;
+}
+
+// forward_serial (potential.hpp:51-53): the unpartitioned evaluation, i.e.
+// one partition on one GPU (bitwise equal to every partition count here)
+inline PotentialOutput forward_serial(const AtomicSystem& system, const ToyPotentialParams& params,
+                                      int n_threads = 0, StepTiming* timing = nullptr) {
+    Distributed d = Distributed::create_distributed(
+        system, params.r_atom,
+        params.threebody() ? std::optional<double>(params.r_3body) : std::nullopt, 1, n_threads,
+        true);
+    return forward_distributed(d, params, timing);
 }
 
 // neighborlist.hpp:37-38 on the GPU
@@ -721,8 +908,8 @@ struct MDOptions {
     double init_temperature = 300.0;
     std::string energy_csv;
     std::string timing_csv;
-    std::string trajectory_xyz;       // accepted, not written (XYZ I/O is out of scope)
-    std::int64_t snapshot_every = 0;
+    std::string trajectory_xyz;       // snapshot prefix: PREFIX.<step>.xyz
+    std::int64_t snapshot_every = 0;  // 0 disables
 };
 
 struct MDStepRecord {
@@ -832,16 +1019,36 @@ inline void write_energy_csv(const std::string& path, const std::vector<MDStepRe
             << "," << r.timing.forward_pass << "," << r.timing.backward_pass << "\n";
 }
 
-// run_md (md.cpp:112-160): the whole trajectory in one device-resident loop
+// write_timing_csv (engine.cpp:29-41): step, then the four categories
+inline void write_timing_csv(const std::string& path, const std::vector<StepTiming>& rows) {
+    std::ofstream out(path);
+    if (!out) throw Error("cannot write file: " + path);
+    out << "step";
+    for (const std::string& name : StepTiming::category_names()) out << "," << name;
+    out << "\n";
+    out.precision(9);
+    for (std::size_t i = 0; i < rows.size(); ++i)
+        out << i << "," << rows[i].graph_creation << "," << rows[i].feature_calculation << ","
+            << rows[i].forward_pass << "," << rows[i].backward_pass << "\n";
+}
+
+// run_md (md.cpp:112-160): the trajectory runs device-resident between
+// snapshots (one gmd_md_run per snapshot interval; the forces at a
+// segment's first positions are re-evaluated, bitwise equal to the previous
+// segment's last evaluation, and that duplicate record is dropped)
 inline MDResult run_md(const AtomicSystem& system, const ToyPotentialParams& params,
                        const MDOptions& opts) {
     MDResult res;
     res.state = init_md_state(system, opts);
     res.state.step = 0;
-    std::vector<double> rec = detail::md_device(res.state, params, opts, opts.steps);
-    for (std::int64_t s = 0; s <= opts.steps; ++s) {
+    const bool snap = !opts.trajectory_xyz.empty() && opts.snapshot_every > 0;
+    auto snapshot = [&](std::int64_t step) {
+        if (snap && step % opts.snapshot_every == 0)
+            save_xyz(res.state.system, opts.trajectory_xyz + "." + std::to_string(step) + ".xyz");
+    };
+    auto push = [&](const std::vector<double>& rec, std::int64_t s, std::int64_t step) {
         MDStepRecord r;
-        r.step = s;
+        r.step = step;
         r.potential = rec[8 * s];
         r.kinetic = rec[8 * s + 1];
         r.total = rec[8 * s + 2];
@@ -851,8 +1058,24 @@ inline MDResult run_md(const AtomicSystem& system, const ToyPotentialParams& par
         r.timing.forward_pass = rec[8 * s + 6];
         r.timing.backward_pass = rec[8 * s + 7];
         res.records.push_back(r);
-    }
+    };
+    const std::int64_t seg = snap ? opts.snapshot_every : std::max<std::int64_t>(opts.steps, 0);
+    std::int64_t done = 0;
+    snapshot(0);
+    do {
+        const std::int64_t k = std::min(seg, opts.steps - done);
+        std::vector<double> rec = detail::md_device(res.state, params, opts, k);
+        if (done == 0) push(rec, 0, 0);
+        for (std::int64_t s = 1; s <= k; ++s) push(rec, s, done + s);
+        done += k;
+        if (k > 0) snapshot(done);
+    } while (done < opts.steps);
     if (!opts.energy_csv.empty()) write_energy_csv(opts.energy_csv, res.records);
+    if (!opts.timing_csv.empty()) {
+        std::vector<StepTiming> rows;
+        for (const MDStepRecord& r : res.records) rows.push_back(r.timing);
+        write_timing_csv(opts.timing_csv, rows);
+    }
     return res;
 }
 

@@ -105,6 +105,10 @@ class Oracle:
             self._dump_graph = f("dump_graph", I, V, C.c_char_p)
             self._dump_line = f("dump_line", I, V, C.c_char_p)
             self._plan_json = f("plan_json", _i64, V, V, _i64)
+            self._save_xyz = f("save_xyz", I, _i64, V, V, V, V, C.c_char_p, C.c_char_p)
+            self._load_xyz = f("load_xyz", _i64, C.c_char_p, V, V, V, V)
+            self._psave = f("params_save", I, I, I, I, D, D, U, V, C.c_char_p)
+            self._pload = f("params_load", _i64, C.c_char_p, V, V, V, V, _i64)
         self._g_ne = f("graph_num_edges", _i64, V)
         self._g_get = f("graph_get", None, V, V, V, V, V, V)
         self._g_free = f("graph_destroy", None, V)
@@ -190,6 +194,39 @@ class Oracle:
         if rc:
             raise OracleError(self.error())
         return dict(energy=float(e[0]), per_atom=pa, forces=fo, stress=st)
+
+    def save_xyz(self, pos, z, lat, pbc, path, comment=""):
+        """save_xyz (system.cpp:165-186), backend "ref" only."""
+        pos, z, lat, pbc = self._sysargs(pos, z, lat, pbc)
+        if self._save_xyz(len(z), _ptr(pos), _ptr(z), _ptr(lat), _ptr(pbc), path.encode(),
+                          comment.encode()):
+            raise OracleError(self.error())
+
+    def params_save(self, F, K, L, r_atom, r3, seed, blob, path):
+        """ToyPotentialParams::save (potential.cpp:178-213), backend "ref" only."""
+        blob = np.ascontiguousarray(blob, dtype=np.float64)
+        if self._psave(F, K, L, r_atom, r3, seed, _ptr(blob), path.encode()):
+            raise OracleError(self.error())
+
+    def params_load(self, path):
+        """ToyPotentialParams::load (potential.cpp:215-260): (F, K, L, r_atom, r3, seed, blob)."""
+        hdr, r, seed = np.zeros(3, np.int32), np.zeros(2), np.zeros(1, np.uint64)
+        n = self._pload(path.encode(), _ptr(hdr), _ptr(r), _ptr(seed), None, 0)
+        if n < 0:
+            raise OracleError(self.error())
+        blob = np.zeros(n)
+        self._pload(path.encode(), _ptr(hdr), _ptr(r), _ptr(seed), _ptr(blob), n)
+        return int(hdr[0]), int(hdr[1]), int(hdr[2]), float(r[0]), float(r[1]), int(seed[0]), blob
+
+    def load_xyz(self, path):
+        """load_xyz (system.cpp:95-163), backend "ref" only: (pos, z, lat, pbc)."""
+        n = self._load_xyz(path.encode(), None, None, None, None)
+        if n < 0:
+            raise OracleError(self.error())
+        pos, z = np.zeros((n, 3)), np.zeros(n, np.int32)
+        lat, pbc = np.zeros((3, 3)), np.zeros(3, np.uint8)
+        self._load_xyz(path.encode(), _ptr(pos), _ptr(z), _ptr(lat), _ptr(pbc))
+        return pos, z, lat, pbc.astype(bool)
 
     def md_run(self, pos, z, lat, pbc, params, F, K, L, r_atom, r3, dt, steps, temperature,
                seed, partitions=1):

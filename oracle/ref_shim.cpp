@@ -463,4 +463,67 @@ int64_t gref_plan_json(void* h, char* buf, int64_t cap) {
     return (int64_t)js.size();
 }
 
+// parameter files (potential.cpp:178-260)
+int gref_params_save(int F, int K, int L, double r_atom, double r3, uint64_t seed,
+                     const double* blob, const char* path) {
+    GUARD_BEGIN
+    ToyPotentialParams p = make_params(F, K, L, r_atom, r3, blob);
+    p.seed = seed;
+    p.save(path);
+    return 0;
+    GUARD_END(1)
+}
+// returns the blob length (or -1); hdr = F, K, L; r = r_atom, r_3body
+int64_t gref_params_load(const char* path, int32_t* hdr, double* r, uint64_t* seed, double* blob,
+                         int64_t cap) {
+    try {
+        ToyPotentialParams p = ToyPotentialParams::load(path);
+        std::vector<double> b;
+        for (const auto* v : {&p.embedding, &p.layer_w, &p.layer_b, &p.basis_proj, &p.basis3_proj,
+                              &p.w3, &p.w4, &p.readout})
+            b.insert(b.end(), v->begin(), v->end());
+        hdr[0] = p.feature_width;
+        hdr[1] = p.basis_count;
+        hdr[2] = p.layers;
+        r[0] = p.r_atom;
+        r[1] = p.r_3body;
+        *seed = p.seed;
+        if ((int64_t)b.size() <= cap) std::memcpy(blob, b.data(), b.size() * sizeof(double));
+        return (int64_t)b.size();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// extended-XYZ I/O (system.cpp:95-186)
+int gref_save_xyz(int64_t n, const double* pos, const int32_t* z, const double* lat,
+                  const uint8_t* pbc, const char* path, const char* comment) {
+    GUARD_BEGIN
+    save_xyz(make_system(n, pos, z, lat, pbc), path, comment ? comment : "");
+    return 0;
+    GUARD_END(1)
+}
+// n = atom count or -1 (error text in gref_last_error); when pos != null the
+// system is copied out (pos n x 3, z n, lat 9, pbc 3)
+int64_t gref_load_xyz(const char* path, double* pos, int32_t* z, double* lat, uint8_t* pbc) {
+    try {
+        AtomicSystem s = load_xyz(path);
+        const int64_t n = (int64_t)s.size();
+        if (pos) {
+            for (int64_t i = 0; i < n; ++i) {
+                for (int k = 0; k < 3; ++k) pos[3 * i + k] = s.positions[i][k];
+                z[i] = s.species[i];
+            }
+            for (int r = 0; r < 3; ++r)
+                for (int k = 0; k < 3; ++k) lat[3 * r + k] = s.lattice[r][k];
+            for (int k = 0; k < 3; ++k) pbc[k] = s.pbc[k] ? 1 : 0;
+        }
+        return n;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 }  // extern "C"

@@ -1079,12 +1079,19 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
     const int32_t* xd = A.xdst.as<int32_t>();
     const int32_t* xs = A.xsrc.as<int32_t>();
+    // corrupt_transfer_plan_for_test: the forward atom transfers read the
+    // wrong span, as the reference's transfer_impl does (engine.cpp:136-137)
+    const int32_t* xs_fwd = xs;
+    if (h->corrupted && !rank_mode && A.nfrom > 0) {
+        ensure_api_plan(h, A, true);
+        xs_fwd = A.xapi.as<int32_t>();
+    }
     // halo exchange of a row buffer: FROM rows <- owners' canonical rows
     // (engine.cpp:122-143); one rank per GPU packs its TO rows and goes
     // through the transport
     const int64_t nsend = rank_mode ? std::accumulate(h->scnt.begin(), h->scnt.end(), (int64_t)0) : 0;
     float* sendbuf = rank_mode ? h->sendbuf.get<float>(std::max<int64_t>(1, nsend) * kF) : nullptr;
-    auto exchange = [&](float* buf) {
+    auto exchange = [&](float* buf, bool fwd = false) {
         if (rank_mode) {
             {
                 PROF("halo_pack");
@@ -1100,7 +1107,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                               h->rcnt.data(), kF);
         } else if (A.nfrom > 0) {
             PROF("exchange");
-            launch_exchange(A.nfrom, xd, xs, buf, kF, s);
+            launch_exchange(A.nfrom, xd, fwd ? xs_fwd : xs, buf, kF, s);
         }
     };
 
@@ -1138,7 +1145,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             bond_exchange(TP, kF);
             { PROF("tb_inject"); launch_tb_inject(ba, TP, H[l], TH4, s); }
         }
-        if (l > 0 || tbl) exchange(H[l]);
+        if (l > 0 || tbl) exchange(H[l], true);
         PROF("conv");
         launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
                     l == L - 1 ? e_part : nullptr, s);

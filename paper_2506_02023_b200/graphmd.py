@@ -286,6 +286,61 @@ class ToyPotentialParams:
         if not np.all(np.isfinite(self.blob)):
             raise Error("parameter array contains a non-finite value")
 
+    # binary parameter files (potential.cpp:178-260, docs/formats.md): magic
+    # GMPT, u32 version 1, u32 F K L flags, f64 r_atom r_3body, u64 seed, then
+    # each table as u64 count + raw little-endian doubles
+    def save(self, path: str) -> None:
+        import struct
+        self.validate()
+        try:
+            f = open(path, "wb")
+        except OSError:
+            raise Error(f"cannot write file: {path}")
+        with f:
+            f.write(b"GMPT" + struct.pack("<5I2dQ", 1, self.feature_width, self.basis_count, self.layers,
+                                          1 if self.threebody() else 0, self.r_atom, self.r_3body,
+                                          self.seed))
+            off = 0
+            for _, sz in self._sizes():
+                f.write(struct.pack("<Q", sz) + np.ascontiguousarray(self.blob[off:off + sz], "<f8").tobytes())
+                off += sz
+
+    @staticmethod
+    def load(path: str) -> "ToyPotentialParams":
+        import struct
+        try:
+            f = open(path, "rb")
+        except OSError:
+            raise Error(f"cannot open file: {path}")
+        with f:
+            data = f.read()
+        if data[:4] != b"GMPT":
+            raise Error("bad parameter file magic")
+        if len(data) < 8 or struct.unpack_from("<I", data, 4)[0] != 1:
+            raise Error("unsupported parameter file version")
+        if len(data) < 48:
+            raise Error("truncated parameter file")
+        F, K, L, _flags = struct.unpack_from("<4I", data, 8)
+        r_atom, r3, seed = struct.unpack_from("<2dQ", data, 24)
+        off, tables = 48, []
+        for _ in range(8):
+            if off + 8 > len(data):
+                raise Error("truncated parameter file")
+            n = struct.unpack_from("<Q", data, off)[0]
+            off += 8
+            if off + 8 * n > len(data):
+                raise Error("truncated parameter file")
+            tables.append(np.frombuffer(data, "<f8", n, off).astype(np.float64))
+            off += 8 * n
+        p = ToyPotentialParams(F, K, L, r_atom, r3, seed, np.concatenate(tables))
+        for (name, want), t in zip(p._sizes(), tables):  # per-table messages (potential.cpp:157-175)
+            if len(t) != want:
+                raise Error(f"parameter array {name} has the wrong size")
+            if not np.all(np.isfinite(t)):
+                raise Error(f"parameter array {name} contains a non-finite value")
+        p.validate()
+        return p
+
 
 @dataclass
 class StepTiming:
@@ -926,6 +981,120 @@ def exchange_plan_consistent(scnt, rcnt, rank: int, all_scnt) -> bool:
 
 
 # ---------------------------------------------------------------------------
+# extended-XYZ I/O (system.cpp:95-186, docs/formats.md)
+# ---------------------------------------------------------------------------
+_SYMBOLS = ("X H He Li Be B C N O F Ne Na Mg Al Si P S Cl Ar K Ca Sc Ti V Cr Mn Fe Co Ni Cu Zn "
+            "Ga Ge As Se Br Kr Rb Sr Y Zr Nb Mo Tc Ru Rh Pd Ag Cd In Sn Sb Te I Xe Cs Ba La Ce "
+            "Pr Nd Pm Sm Eu Gd Tb Dy Ho Er Tm Yb Lu Hf Ta W Re Os Ir Pt Au Hg Tl Pb Bi Po At Rn "
+            "Fr Ra Ac Th Pa U Np Pu Am Cm Bk Cf Es Fm Md No Lr Rf Db Sg Bh Hs Mt Ds Rg Cn Nh Fl "
+            "Mc Lv Ts Og").split()
+_Z_OF = {sym: z for z, sym in enumerate(_SYMBOLS) if z > 0}
+
+
+def z_to_symbol(z: int) -> str:
+    if z < 1 or z > 118:
+        raise Error("atomic number out of range")
+    return _SYMBOLS[z]
+
+
+def _parse_fail(path, line, what):
+    raise Error(f"{path}:{line}: {what}")
+
+
+def load_xyz(path: str) -> AtomicSystem:
+    """load_xyz (system.cpp:95-163): count line, comment line with
+    Lattice="..." (and optional pbc="T T F"), then `Symbol x y z` lines."""
+    try:
+        f = open(path)
+    except OSError:
+        raise Error(f"cannot open file: {path}")
+    with f:
+        lines = f.read().split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        _parse_fail(path, 1, "empty file")
+    head = lines[0]
+    try:  # std::stoul: leading whitespace, optional sign, then digits
+        m = __import__("re").match(r"\s*([+-]?\d+)", head)
+        natoms = int(m.group(1))
+        if natoms < 0:
+            natoms %= 1 << 64
+    except (AttributeError, ValueError):
+        _parse_fail(path, 1, f"expected atom count, got '{head}'")
+    if len(lines) < 2:
+        _parse_fail(path, 2, "missing comment line")
+    com = lines[1]
+    lattice = np.eye(3)
+    pbc = [True, True, True]
+    i = com.find('Lattice="')
+    have_lattice = i >= 0
+    if have_lattice:
+        b = i + 9
+        e = com.find('"', b)
+        if e < 0:
+            _parse_fail(path, 2, "unterminated Lattice field")
+        toks = com[b:e].split()
+        vals = []
+        for t in toks[:9]:
+            try:
+                vals.append(float(t))
+            except ValueError:
+                break
+        if len(vals) < 9:
+            _parse_fail(path, 2, "Lattice needs 9 numbers")
+        lattice = np.array(vals).reshape(3, 3)
+    i = com.find('pbc="')
+    if i >= 0:
+        b = i + 5
+        e = com.find('"', b)
+        toks = (com[b:e] if e >= 0 else com[b:]).split()
+        if len(toks) < 3:
+            _parse_fail(path, 2, "pbc needs 3 flags")
+        pbc = [t in ("T", "True", "true", "1") for t in toks[:3]]
+    if not have_lattice:
+        if any(pbc):
+            _parse_fail(path, 2, "periodic system requires a Lattice field")
+        lattice = np.eye(3)
+    pos = np.zeros((natoms, 3))
+    z = np.zeros(natoms, np.int32)
+    for a in range(natoms):
+        ln = a + 3
+        if ln - 1 >= len(lines):
+            _parse_fail(path, ln, "unexpected end of file")
+        t = lines[ln - 1].split()
+        try:
+            sym, x, y, w = t[0], float(t[1]), float(t[2]), float(t[3])
+        except (IndexError, ValueError):
+            _parse_fail(path, ln, "expected 'symbol x y z'")
+        if sym not in _Z_OF:
+            _parse_fail(path, ln, f"unknown element symbol '{sym}'")
+        z[a] = _Z_OF[sym]
+        pos[a] = (x, y, w)
+    s = AtomicSystem(pos, lattice, z, tuple(pbc))
+    s.validate()
+    return s
+
+
+def save_xyz(system: AtomicSystem, path: str, comment_extra: str = "") -> None:
+    """save_xyz (system.cpp:165-186): 17 significant digits."""
+    g = lambda x: format(float(x), ".17g")  # noqa: E731  (= ostream precision 17)
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise Error(f"cannot write file: {path}")
+    with f:
+        f.write(f"{system.size()}\n")
+        f.write('Lattice="' + " ".join(g(v) for v in system.lattice.reshape(-1)) + '" pbc="'
+                + " ".join("T" if b else "F" for b in system.pbc) + '"')
+        if comment_extra:
+            f.write(" " + comment_extra)
+        f.write("\n")
+        for r, zz in zip(system.positions, system.species):
+            f.write(f"{z_to_symbol(int(zz))} {g(r[0])} {g(r[1])} {g(r[2])}\n")
+
+
+# ---------------------------------------------------------------------------
 # on-device MD: the caller of the hot path (md.hpp:14-89, md.cpp)
 # ---------------------------------------------------------------------------
 class units:  # md.hpp:14-21
@@ -965,6 +1134,8 @@ class MDOptions:  # md.hpp:36-49
     init_temperature: float = 300.0
     energy_csv: str = ""
     timing_csv: str = ""
+    trajectory_xyz: str = ""   # snapshot prefix: PREFIX.<step>.xyz
+    snapshot_every: int = 0    # 0 disables
 
 
 @dataclass
@@ -1113,13 +1284,19 @@ def run_md(system: AtomicSystem, params: "ToyPotentialParams", opts: MDOptions,
         records.append(MDStepRecord(step, state.potential_energy, ke, state.potential_energy + ke,
                                     fm, t))
 
+    def snapshot(step):  # md.cpp:131-137
+        if opts.trajectory_xyz and opts.snapshot_every > 0 and step % opts.snapshot_every == 0:
+            save_xyz(state.current_system(), f"{opts.trajectory_xyz}.{step}.xyz")
+
     t0 = StepTiming()
     md_evaluate(state, params, opts, t0)
     record(0, t0)
+    snapshot(0)
     for step in range(1, opts.steps + 1):
         t = StepTiming()
         velocity_verlet_step(state, params, opts, t)
         record(step, t)
+        snapshot(step)
     if opts.energy_csv:
         write_energy_csv(opts.energy_csv, records)
     if opts.timing_csv:

@@ -431,8 +431,32 @@ static int dump_mode(const std::string& dir, int p) {
     return 0;
 }
 
+// parameter files, CPU only (tests/test_cli.py): --params-save PATH SEED L R3
+// writes ToyPotentialParams::init(...).save(PATH); --params-copy IN OUT loads
+// IN and saves it to OUT; errors print "error: <text>" and exit 3
+static int params_mode(int argc, char** argv) {
+    try {
+        const std::string m = argv[1];
+        if (m == "--params-save" && argc > 5) {
+            ToyPotentialParams::init(std::strtoull(argv[3], nullptr, 10), 16, 8, std::atoi(argv[4]), 5.0,
+                                     std::atof(argv[5]))
+                .save(argv[2]);
+            return 0;
+        }
+        if (m == "--params-copy" && argc > 3) {
+            ToyPotentialParams::load(argv[2]).save(argv[3]);
+            return 0;
+        }
+        return 2;
+    } catch (const std::exception& e) {
+        std::printf("error: %s\n", e.what());
+        return 3;
+    }
+}
+
 int main(int argc, char** argv) {
     if (argc > 3 && std::string(argv[1]) == "--dump") return dump_mode(argv[2], std::atoi(argv[3]));
+    if (argc > 1 && std::string(argv[1]).rfind("--params-", 0) == 0) return params_mode(argc, argv);
     std::string only = argc > 1 ? argv[1] : "";
     for (auto& [name, fn] : registry()) {
         if (!only.empty() && name != only) continue;

@@ -146,3 +146,16 @@ def test_partitioned_model_matches_feature_api():
     d.atom_transfer(f)
     for i, pt in enumerate(d.atom_parts().parts):
         np.testing.assert_array_equal(f.block(i).cpu().numpy(), feats[pt.layout.node_array])
+
+
+def test_corrupt_plan_breaks_forward():
+    """The hook also corrupts the forward's atom transfers (engine.cpp:136-137:
+    forward_distributed goes through transfer_impl), so the CLI's audit
+    negative control fails as the reference's does."""
+    s = S.quartz((3, 3, 6))
+    prm = G.ToyPotentialParams.init(12345, 16, 8, 2, 5.0, 0.0)
+    good = G.forward_distributed(G.Distributed.create_distributed(s, 5.0, None, 2, 1), prm)
+    d = G.Distributed.create_distributed(s, 5.0, None, 2, 1)
+    d.corrupt_transfer_plan_for_test()
+    bad = G.forward_distributed(d, prm)
+    assert np.abs(bad.forces - good.forces).max() > 1e-6
