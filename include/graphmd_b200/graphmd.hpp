@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <sstream>
@@ -591,6 +592,67 @@ public:
     std::vector<double> aggregate(const DistributedFeatures& f) const { return agg(f, 0); }
     std::vector<double> aggregate_bonds(const DistributedFeatures& f) const { return agg(f, 1); }
     void corrupt_transfer_plan_for_test() { detail::check(h_.get(), gmd_corrupt_transfer_plan_for_test(h_.get())); }
+
+    // owned-edge feature blocks (engine.cpp:103-120, 248-260): partition i
+    // holds the rows of its owned edges in owned_edges order
+    DistributedFeatures distribute_edge_features(const std::vector<double>& f, std::int64_t width) const {
+        const PartitionedAtomGraph& ap = atom_parts();
+        if (f.size() != graph().num_edges() * (std::size_t)width) throw Error("edge feature shape mismatch");
+        DistributedFeatures out;
+        out.width = width;
+        out.blocks.resize(p_);
+        for (int i = 0; i < p_; ++i) {
+            const auto& owned = ap.parts[i].owned_edges;
+            out.blocks[i].resize(owned.size() * width);
+            for (std::size_t k = 0; k < owned.size(); ++k)
+                std::copy(f.begin() + owned[k] * width, f.begin() + (owned[k] + 1) * width,
+                          out.blocks[i].begin() + k * width);
+        }
+        return out;
+    }
+    std::vector<double> aggregate_edges(const DistributedFeatures& f) const {
+        const PartitionedAtomGraph& ap = atom_parts();
+        std::vector<double> out(graph().num_edges() * f.width, 0.0);
+        for (int i = 0; i < p_; ++i) {
+            const auto& owned = ap.parts[i].owned_edges;
+            for (std::size_t k = 0; k < owned.size(); ++k)
+                std::copy(f.row(i, (std::int64_t)k), f.row(i, (std::int64_t)k) + f.width,
+                          out.begin() + owned[k] * f.width);
+        }
+        return out;
+    }
+
+    using LayerFn = std::function<void(int partition, DistributedFeatures&)>;
+
+    // fn(partition) for every partition; a failure is rethrown with the id of
+    // the first failing partition (engine.cpp:262-284).  Callbacks run in
+    // partition order on the calling thread: the device work they enqueue is
+    // ordered on the handle's stream, so there is no host parallelism to add.
+    void parallel_for_partitions(const std::function<void(int)>& fn) const {
+        std::vector<std::string> errors(p_);
+        bool failed = false;
+        for (int i = 0; i < p_; ++i) {
+            try {
+                fn(i);
+            } catch (const std::exception& e) {
+                errors[i] = e.what();
+                failed = true;
+            }
+        }
+        if (failed)
+            for (int i = 0; i < p_; ++i)
+                if (!errors[i].empty())
+                    throw Error("worker for partition " + std::to_string(i) + " failed: " + errors[i]);
+    }
+
+    // each layer on every partition, then the border exchange (engine.cpp:286-294)
+    void run_layered(const std::vector<LayerFn>& layers, DistributedFeatures& features) const {
+        for (const LayerFn& layer : layers) {
+            parallel_for_partitions([&](int i) { layer(i, features); });
+            sync_atom_duplicates(features);
+            atom_transfer(features);
+        }
+    }
 
 private:
     std::shared_ptr<gmd_handle> h_;

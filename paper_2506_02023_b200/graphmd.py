@@ -556,9 +556,13 @@ def _json_dump2(v, ind: int) -> str:
     return str(v)
 
 
+EDGE_FEATURES = 2  # DistributedFeatures.bonds of owned-edge blocks
+
+
 class DistributedFeatures:
     """Per-partition feature blocks in ONE CUDA tensor (rows x width); block i
-    is rows [offsets[i], offsets[i+1]) aligned to partition i's layout."""
+    is rows [offsets[i], offsets[i+1]) aligned to partition i's layout (atom
+    or bond layout, or its owned edges for edge features)."""
 
     def __init__(self, data, offsets, width, bonds):
         self.data, self.offsets, self.width, self.bonds = data, offsets, width, bonds
@@ -755,6 +759,8 @@ class Distributed:
         raise Error("features must be float32 or float64", GMD_ERR_ARG)
 
     def _op(self, fn, f):
+        if f.bonds == EDGE_FEATURES:
+            raise Error("transfers apply to atom or bond feature blocks", GMD_ERR_ARG)
         self._h.check(fn(self._h.h, f.bonds, C.c_void_p(f.data.data_ptr()), f.width, self._dt(f)))
 
     def atom_transfer(self, f):
@@ -804,6 +810,56 @@ class Distributed:
 
     def corrupt_transfer_plan_for_test(self):
         self._h.check(lib().gmd_corrupt_transfer_plan_for_test(self._h.h))
+
+    # owned-edge feature blocks (engine.cpp:103-120, 248-260): partition i
+    # holds its owned edges' rows in owned_edges order (API plumbing, not the
+    # model path: the gather / scatter run as device index ops)
+    def _edge_order(self):
+        parts = self.atom_parts().parts
+        offs = np.concatenate([[0], np.cumsum([len(x.owned_edges) for x in parts])]).tolist()
+        return np.concatenate([x.owned_edges for x in parts]).astype(np.int64), offs
+
+    def distribute_edge_features(self, features, width):
+        import torch
+        arr = np.ascontiguousarray(features, np.float64)
+        if arr.size != self.num_edges() * width:
+            raise Error("edge feature shape mismatch")
+        order, offs = self._edge_order()
+        dev = f"cuda:{self._h.device}"
+        src = torch.from_numpy(arr.reshape(-1, width)).to(dev)
+        data = src[torch.from_numpy(order).to(dev)].contiguous()
+        return DistributedFeatures(data, offs, width, EDGE_FEATURES)
+
+    def aggregate_edges(self, f):
+        import torch
+        if f.bonds != EDGE_FEATURES:
+            raise Error("aggregate_edges needs edge feature blocks", GMD_ERR_ARG)
+        order, _ = self._edge_order()
+        out = torch.zeros((self.num_edges(), f.width), dtype=f.data.dtype, device=f.data.device)
+        out[torch.from_numpy(order).to(f.data.device)] = f.data
+        return out.reshape(-1).cpu().numpy()
+
+    def parallel_for_partitions(self, fn):
+        """fn(partition) for every partition; the first failing partition's
+        error is re-raised with its id (engine.cpp:262-284).  Callbacks run in
+        partition order: the device work they enqueue is stream-ordered."""
+        errors = [None] * self._p
+        for i in range(self._p):
+            try:
+                fn(i)
+            except Exception as e:  # noqa: BLE001 -- reported with the partition id
+                errors[i] = str(e)
+        for i, e in enumerate(errors):
+            if e is not None:
+                raise Error(f"worker for partition {i} failed: {e}", GMD_ERR_RUNTIME)
+
+    def run_layered(self, layers, features):
+        """Each layer on every partition, then the border exchange
+        (engine.cpp:286-294)."""
+        for layer in layers:
+            self.parallel_for_partitions(lambda i: layer(i, features))
+            self.sync_atom_duplicates(features)
+            self.atom_transfer(features)
 
     # per-step reuse
     @property

@@ -303,6 +303,67 @@ TEST(distribute_aggregate_identity) {
     CHECK(d.aggregate(d.distribute_node_features(feats, 4)) == feats);
 }
 
+// test_engine.cpp:149-203 (run_layered, worker failure) + edge features
+TEST(run_layered_and_worker_failure) {
+    auto run = [&](int p) {
+        Distributed dist = Distributed::create_distributed(chain4(), 1.5, std::nullopt, p, 1, true);
+        std::vector<double> init{1.0, 2.0, 3.0, 4.0};
+        DistributedFeatures f = dist.distribute_node_features(init, 1);
+        std::vector<Distributed::LayerFn> layers;
+        layers.push_back([&dist](int part, DistributedFeatures& feats) {
+            const AtomPartition& ap = dist.atom_parts().parts[part];
+            std::vector<double> sum(dist.atom_rows(part), 0.0);
+            std::vector<int> cnt(dist.atom_rows(part), 0);
+            for (std::size_t e = 0; e < ap.owned_edges.size(); ++e) {
+                sum[ap.local_dst[e]] += *feats.row(part, ap.local_src[e]);
+                cnt[ap.local_dst[e]]++;
+            }
+            for (std::int64_t r = 0; r < ap.layout.owned_end(); ++r)
+                if (ap.layout.local_of(ap.layout.node_array[r]) == r && cnt[r])
+                    *feats.row(part, r) = sum[r] / cnt[r];
+        });
+        dist.run_layered(layers, f);
+        return dist.aggregate(f);
+    };
+    const std::vector<double> serial = run(1);
+    CHECK(serial == (std::vector<double>{2.0, 2.0, 3.0, 3.0}));
+    CHECK(run(2) == serial);
+    Distributed dist = Distributed::create_distributed(chain4(), 1.5, std::nullopt, 2, 1, true);
+    std::vector<double> init{5, 6, 7, 8};
+    DistributedFeatures f = dist.distribute_node_features(init, 1);
+    dist.run_layered(std::vector<Distributed::LayerFn>(3, [](int, DistributedFeatures&) {}), f);
+    CHECK(dist.aggregate(f) == init);
+
+    Distributed d2 = Distributed::create_distributed(random_system(40, {10, 8, 8}, 11), 3.0, std::nullopt, 2, 2, true);
+    bool thrown = false;
+    try {
+        d2.parallel_for_partitions([](int p) {
+            if (p == 1) throw Error("boom");
+        });
+    } catch (const Error& e) {
+        thrown = true;
+        CHECK(std::string(e.what()).find("partition 1") != std::string::npos);
+        CHECK(std::string(e.what()).find("boom") != std::string::npos);
+    }
+    CHECK(thrown);
+
+    // owned-edge features round trip; every edge lands in exactly one block
+    std::vector<double> ef(d2.graph().num_edges() * 3);
+    for (std::size_t i = 0; i < ef.size(); ++i) ef[i] = 0.25 * i - 7.0;
+    DistributedFeatures eb = d2.distribute_edge_features(ef, 3);
+    std::size_t rows = 0;
+    for (int i = 0; i < 2; ++i) rows += eb.blocks[i].size() / 3;
+    CHECK(rows == d2.graph().num_edges());
+    CHECK(d2.aggregate_edges(eb) == ef);
+    bool shape = false;
+    try {
+        d2.distribute_edge_features(std::vector<double>(5), 3);
+    } catch (const Error& e) {
+        shape = std::string(e.what()) == "edge feature shape mismatch";
+    }
+    CHECK(shape);
+}
+
 // ---- potential (test_potential.cpp) ---------------------------------------
 static void compare_to_oracle(const AtomicSystem& s, const ToyPotentialParams& prm, const PotentialOutput& out) {
     Flat f = flat(s);

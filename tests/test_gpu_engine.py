@@ -159,3 +159,59 @@ def test_corrupt_plan_breaks_forward():
     d.corrupt_transfer_plan_for_test()
     bad = G.forward_distributed(d, prm)
     assert np.abs(bad.forces - good.forces).max() > 1e-6
+
+
+def _mean_of_neighbors(d):
+    def layer(part, f):  # test_engine.cpp:158-169
+        ap = d.atom_parts().parts[part]
+        rows = d.atom_rows(part)
+        x = f.block(part)[:, 0].cpu().numpy()
+        s, c = np.zeros(rows), np.zeros(rows, np.int64)
+        np.add.at(s, ap.local_dst, x[ap.local_src])
+        np.add.at(c, ap.local_dst, 1)
+        lay = ap.layout
+        for r in range(lay.owned_end()):
+            if lay.local_of(lay.node_array[r]) == r and c[r]:
+                f.block(part)[r, 0] = s[r] / c[r]
+    return layer
+
+
+def test_run_layered_and_worker_failure():
+    """test_engine.cpp:149-203: mean-of-neighbours on the chain equals the
+    serial result for p = 1, 2; identity layers leave rows untouched; a worker
+    failure names its partition."""
+    def run(p):
+        d = build(S.chain4(), 1.5, p)
+        f = d.distribute_node_features(np.array([1.0, 2.0, 3.0, 4.0]), 1)
+        d.run_layered([_mean_of_neighbors(d)], f)
+        return d.aggregate(f)
+    serial = run(1)
+    np.testing.assert_array_equal(serial, [2.0, 2.0, 3.0, 3.0])
+    np.testing.assert_array_equal(run(2), serial)
+    d = build(S.chain4(), 1.5, 2)
+    f = d.distribute_node_features(np.array([5.0, 6, 7, 8]), 1)
+    d.run_layered([lambda i, x: None] * 3, f)
+    np.testing.assert_array_equal(d.aggregate(f), [5.0, 6, 7, 8])
+    d2 = G.Distributed.create_distributed(S.random_system(40, (10, 8, 8), 11), 3.0, None, 2, 2, True)
+
+    def boom(p):
+        if p == 1:
+            raise G.Error("boom")
+    with pytest.raises(G.Error, match="worker for partition 1 failed: boom"):
+        d2.parallel_for_partitions(boom)
+
+
+def test_edge_features_round_trip():
+    d = G.Distributed.create_distributed(S.random_system(40, (10, 8, 8), 11), 3.0, None, 3, 1, True)
+    ne = d.num_edges()
+    ef = 0.25 * np.arange(ne * 3) - 7.0
+    eb = d.distribute_edge_features(ef, 3)
+    assert eb.data.shape == (ne, 3)
+    ap = d.atom_parts()
+    for i in range(3):  # block i = its owned edges, in order
+        np.testing.assert_array_equal(eb.block(i).cpu().numpy(), ef.reshape(-1, 3)[ap.parts[i].owned_edges])
+    np.testing.assert_array_equal(d.aggregate_edges(eb), ef)
+    with pytest.raises(G.Error, match="edge feature shape mismatch"):
+        d.distribute_edge_features(np.zeros(5), 3)
+    with pytest.raises(G.Error):
+        d.atom_transfer(eb)

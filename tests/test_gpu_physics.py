@@ -1,0 +1,155 @@
+"""Physical invariances of the GPU model and MD (proj/tests/test_potential.cpp
+and test_md.cpp scenarios not covered by the oracle comparisons).
+
+Tolerances are fp32-level, stated per check: the GPU computes features,
+forces and the virial in fp32, so quantities the
+reference conserves exactly in fp64 (total momentum, sum of forces) are
+conserved to fp32 rounding here."""
+import numpy as np
+import pytest
+
+from paper_2506_02023_b200 import graphmd as G
+from tests import systems as S
+
+pytestmark = pytest.mark.gpu
+
+
+def evaluate(s, prm, p=1, r3=None):
+    d = G.Distributed.create_distributed(s, prm.r_atom, r3, p, 1, True)
+    return G.forward_distributed(d, prm)
+
+
+def rotation(seed):
+    rng = np.random.default_rng(seed)
+    q, r = np.linalg.qr(rng.normal(size=(3, 3)))
+    q *= np.sign(np.diag(r))
+    if np.linalg.det(q) < 0:
+        q[:, 0] *= -1
+    return q
+
+
+@pytest.mark.parametrize("r3", [None, 2.6])
+def test_rotation_invariance_and_force_equivariance(r3):
+    """test_potential.cpp "rotation invariance and force equivariance":
+    rotating positions and lattice leaves energies unchanged and rotates the
+    forces (row vectors: F' = F R^T) and the stress (S' = R S R^T)."""
+    s = S.quartz((2, 2, 2))
+    prm = G.ToyPotentialParams.init(21, 16, 8, 2, 4.5, r3 or 0.0)
+    a = evaluate(s, prm, r3=r3)
+    R = rotation(3)
+    t = G.AtomicSystem(s.positions @ R.T, s.lattice @ R.T, s.species)
+    b = evaluate(t, prm, r3=r3)
+    assert abs(a.energy - b.energy) / s.size() < 2e-6
+    np.testing.assert_allclose(b.per_atom, a.per_atom, atol=2e-5)
+    np.testing.assert_allclose(b.forces, a.forces @ R.T, atol=2e-4)
+    np.testing.assert_allclose(b.stress, R @ a.stress @ R.T, atol=2e-6)
+
+
+def test_permutation_equivariance():
+    """test_potential.cpp "permutation equivariance": relabelling atoms
+    permutes per-atom energies and forces; the graph is rebuilt in the new
+    canonical order."""
+    s = S.liquid(600)
+    prm = G.ToyPotentialParams.init(4, 16, 8, 2, 4.0, 2.5)
+    perm = np.random.default_rng(1).permutation(s.size())
+    t = G.AtomicSystem(s.positions[perm], s.lattice, s.species[perm])
+    a, b = evaluate(s, prm, r3=2.5), evaluate(t, prm, r3=2.5)
+    np.testing.assert_allclose(b.per_atom, a.per_atom[perm], atol=2e-5)
+    np.testing.assert_allclose(b.forces, a.forces[perm], atol=2e-4)
+    assert abs(a.energy - b.energy) / s.size() < 2e-6
+
+
+def test_far_separated_atoms_zero_forces_and_stress():
+    """test_potential.cpp "far-separated atoms": no edges, zero forces and
+    stress, energy = sum of isolated-atom energies."""
+    s = G.AtomicSystem(np.array([[1.0, 1, 1], [20, 20, 20], [1, 20, 35]]), np.eye(3) * 50,
+                       np.array([8, 14, 1], np.int32))
+    prm = G.ToyPotentialParams.init(8, 16, 8, 2, 4.0)
+    out = evaluate(s, prm)
+    assert np.all(out.forces == 0.0) and np.all(out.stress == 0.0)
+    singles = [evaluate(G.AtomicSystem(np.array([x]), np.eye(3) * 50, np.array([z], np.int32)), prm).energy
+               for x, z in zip(s.positions, s.species)]
+    assert abs(out.energy - sum(singles)) < 1e-5
+
+
+# ------------------------------------------------------------------ MD
+def quartz_cell(reps, amp, seed):
+    return G.random_perturb(G.make_supercell(S.fixture("quartz"), reps), amp, seed) if amp > 0 \
+        else G.make_supercell(S.fixture("quartz"), reps)
+
+
+def momentum(state):
+    return (state.velocities() * state.masses.cpu().numpy()[:, None]).sum(0)
+
+
+def test_dt_zero_step_leaves_state_unchanged():
+    """test_md.cpp "dt=0 step": positions within the wrap round trip (1e-12),
+    velocities bitwise, step counter advances."""
+    s = quartz_cell((1, 1, 1), 0.05, 3)
+    prm = G.ToyPotentialParams.init(3)
+    opts = G.MDOptions(dt=0.0, seed=7)
+    st = G.init_md_state(s, opts)
+    G.md_evaluate(st, prm, opts)
+    G.velocity_verlet_step(st, prm, G.MDOptions(dt=0.0, seed=7))  # wraps once
+    pos0, vel0, step0 = st.positions(), st.velocities(), st.step
+    G.velocity_verlet_step(st, prm, opts)
+    assert np.abs(st.positions() - pos0).max() <= 1e-12
+    np.testing.assert_array_equal(st.velocities(), vel0)
+    assert st.step == step0 + 1
+
+
+def test_zero_temperature_crystal_stays_put():
+    """test_md.cpp "zero temperature perfect crystal stays put": |dx| <=
+    a_max t^2 / 2 with a_max from the largest initial force."""
+    s = quartz_cell((1, 1, 1), 0.0, 0)
+    prm = G.ToyPotentialParams.init(5)
+    res = G.run_md(s, prm, G.MDOptions(dt=1.0, steps=10, init_temperature=0.0))
+    d = np.linalg.solve(s.lattice.T, (res.state.positions() - s.positions).T).T
+    d -= np.round(d)  # atoms wrapped back into the cell moved by a lattice vector
+    moved = np.linalg.norm(d @ s.lattice, axis=1).max()
+    amax = G.units.kAccel * res.records[0].max_force / 15.999
+    assert moved <= 0.5 * amax * 100.0 + 1e-12
+
+
+def test_energy_conservation_100_steps():
+    """test_md.cpp "energy conservation over 100 steps": |E(t) - E(0)| / N
+    <= 1e-4 eV (three-body potential, dt 0.25 fs)."""
+    s = quartz_cell((2, 1, 1), 0.02, 11)
+    prm = G.ToyPotentialParams.init(7, 16, 8, 2, 4.0, 2.8)
+    res = G.run_md(s, prm, G.MDOptions(dt=0.25, steps=100, init_temperature=0.0, allow_narrow=True))
+    assert len(res.records) == 101
+    e0 = res.records[0].total
+    assert max(abs(r.total - e0) for r in res.records) / s.size() <= 1e-4
+
+
+def test_momentum_conservation():
+    """test_md.cpp "momentum conservation": the reference holds |P| <= 1e-8
+    with fp64 forces; with fp32 forces sum F vanishes to fp32 rounding, so the
+    bound here is 1e-5 amu A/fs after 50 steps (initial |P| < 1e-12)."""
+    s = quartz_cell((2, 1, 1), 0.03, 13)
+    prm = G.ToyPotentialParams.init(9)
+    st = G.init_md_state(s, G.MDOptions(seed=5, init_temperature=250.0))
+    assert np.abs(momentum(st)).max() < 1e-12
+    res = G.run_md(s, prm, G.MDOptions(dt=1.0, steps=50, seed=5, init_temperature=250.0,
+                                      allow_narrow=True))
+    assert np.linalg.norm(momentum(res.state)) <= 1e-5
+
+
+def test_kinetic_energy_and_temperature_identities():
+    s = quartz_cell((1, 1, 1), 0.0, 0)
+    st = G.init_md_state(s, G.MDOptions())
+    st.vel.fill_(0.0)
+    st.vel[:, 0] = 0.01
+    m = G.atomic_mass(s.species)
+    ke = float(np.sum(0.5 * m * 1e-4 * G.units.kKinetic))
+    assert st.kinetic_energy() == pytest.approx(ke, rel=1e-12)
+    dof = 3.0 * s.size() - 3.0
+    assert st.temperature() == pytest.approx(2.0 * ke / (dof * G.units.kBoltzmann), rel=1e-12)
+
+
+def test_energy_csv_steps_zero(tmp_path):
+    """steps = 0 still writes the header and the initial row."""
+    s = quartz_cell((1, 1, 1), 0.05, 1)
+    res = G.run_md(s, G.ToyPotentialParams.init(3), G.MDOptions(steps=0, energy_csv=str(tmp_path / "e.csv")))
+    assert len(res.records) == 1
+    assert len(open(tmp_path / "e.csv").read().splitlines()) == 2
