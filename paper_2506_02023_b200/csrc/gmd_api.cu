@@ -1141,7 +1141,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     for (int l = 0; l < L; ++l) {
         const bool tbl = tb && l == L - 1;
         if (tbl) {
-            { PROF("tb_forward"); launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), s); }
+            { PROF("tb_forward"); launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), h->max_bonds, s); }
             bond_exchange(TP, kF);
             { PROF("tb_inject"); launch_tb_inject(ba, TP, H[l], TH4, s); }
         }
@@ -1416,6 +1416,13 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         for (int i = 0; i < F * K; ++i) m.P3[i] = (float)*q++;
         for (int i = 0; i < F * F; ++i) m.W3[i] = (float)*q++;
         for (int i = 0; i < F * F; ++i) m.W4[i] = (float)*q++;
+        for (int f = 0; f < F; ++f) {
+            for (int k = 0; k < K; ++k) m.P3T[k * F + f] = m.P3[f * K + k];
+            for (int g = 0; g < F; ++g) {
+                m.W3T[g * F + f] = m.W3[f * F + g];
+                m.W4T[g * F + f] = m.W4[f * F + g];
+            }
+        }
         for (int i = 0; i < F; ++i) m.ro[i] = (float)*q++;
         m.rc = (float)r_atom;
         m.inv_rc = (float)(1.0 / r_atom);

@@ -1176,39 +1176,68 @@ constexpr int kTbWarps = 4;
 constexpr int kTbGroups = kTbWarps * 2;
 constexpr size_t kTbSlotBytes = 2 * sizeof(float) * kF + sizeof(float4);  // st + sm + sv
 
+// The three-body contractions run on packed FP32 like the atom channel
+// (FFMA2 over feature pairs, constant pairs from uniform registers); each
+// lane-half performs the scalar kernel's FMAs in the same order, so results
+// are bitwise those of the scalar form.
+// out_f = sum_k M[f][k] x_k (ascending k) from the k-major copy MT
+__device__ __forceinline__ void fk_pairs(const float* MT, const float x[kK], float out[kF]) {
+    const float2* M2 = reinterpret_cast<const float2*>(MT);
+    float2 o[kF / 2];
+#pragma unroll
+    for (int i = 0; i < kF / 2; ++i) o[i] = f2mul(M2[i], bcast(x[0]));
+#pragma unroll
+    for (int k = 1; k < kK; ++k)
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) o[i] = f2fma(M2[k * (kF / 2) + i], bcast(x[k]), o[i]);
+#pragma unroll
+    for (int i = 0; i < kF / 2; ++i) {
+        out[2 * i] = o[i].x;
+        out[2 * i + 1] = o[i].y;
+    }
+}
+// out_g = sum_f A[f][g] y_f (ascending f), A row-major F x F: (A[f][g], A[f][g+1]) pairs
+__device__ __forceinline__ void ff_pairs(const float* A, const float y[kF], float out[kF]) {
+    const float2* A2 = reinterpret_cast<const float2*>(A);
+    float2 o[kF / 2];
+#pragma unroll
+    for (int i = 0; i < kF / 2; ++i) o[i] = f2mul(A2[i], bcast(y[0]));
+#pragma unroll
+    for (int f = 1; f < kF; ++f)
+#pragma unroll
+        for (int i = 0; i < kF / 2; ++i) o[i] = f2fma(A2[f * (kF / 2) + i], bcast(y[f]), o[i]);
+#pragma unroll
+    for (int i = 0; i < kF / 2; ++i) {
+        out[2 * i] = o[i].x;
+        out[2 * i + 1] = o[i].y;
+    }
+}
+
 __device__ __forceinline__ void bond_t(float d, float t[kF]) {
     float u[kK];
     basis(d, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u);
-#pragma unroll
-    for (int f = 0; f < kF; ++f) {
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < kK; ++k) s = fmaf(c_m.P3[f * kK + k], u[k], s);
-        t[f] = s;
-    }
+    fk_pairs(c_m.P3T, u, t);  // t_f = sum_k P3[f][k] u_k
 }
 
 __device__ __forceinline__ void bond_dt(float d, float ds[kF]) {
     float u[kK], du[kK];
     basis_d(d, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u, du);
-#pragma unroll
-    for (int f = 0; f < kF; ++f) {
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < kK; ++k) s = fmaf(c_m.P3[f * kK + k], du[k], s);
-        ds[f] = s;
-    }
+    fk_pairs(c_m.P3T, du, ds);
 }
 
 // per center s: for each in-bond slot j (bond e1 = (w->s)), compute t' of the
 // reverse bond e' = (s->w): m3_{e'} = sum_{e2 != e1} c(e2, e') t_{e2} in
 // ascending e2, z3 = W3 m3, t' = t + fc3 tanh(z3).  Stored at slot j.
+// per-group staging sized by kc >= the build's max in-bonds (dynamic shared
+// memory: C4's 16-slot groups need 10 KB per CTA instead of 40 KB)
 __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float* __restrict__ TP,
                                                               float* __restrict__ TH3,
-                                                              int32_t* flags) {
-    __shared__ float st[kTbGroups][kMaxBondsPerAtom][kF];
-    __shared__ float4 sv[kTbGroups][kMaxBondsPerAtom];
+                                                              int32_t* flags, int kc) {
+    extern __shared__ __align__(16) unsigned char tbf_smem[];
     const int gl = threadIdx.x & 15, grp = threadIdx.x >> 4;
+    float(*st_g)[kF] = reinterpret_cast<float(*)[kF]>(tbf_smem) + (size_t)grp * kc;
+    float4* sv_g = reinterpret_cast<float4*>(tbf_smem + sizeof(float) * kF * kTbGroups * kc) +
+                   (size_t)grp * kc;
     const int64_t w0 = (int64_t)blockIdx.x * kTbGroups + grp;
     const int64_t nw = (int64_t)gridDim.x * kTbGroups;
     const int64_t iters = (a.n + nw - 1) / nw;  // same count for both groups of a warp
@@ -1219,30 +1248,30 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float*
             const int64_t s = a.nodes ? (int64_t)a.nodes[ks] : ks;
             b0 = a.brow[s];
             k = a.brow[s + 1] - b0;
-            if (k > kMaxBondsPerAtom) {
+            if (k > kc) {  // only when k > kMaxBondsPerAtom (kc covers the build's max)
                 if (gl == 0) atomicOr(&flags[1], 16);
                 k = 0;
             }
         }
         for (int j = gl; j < k; j += 16) {
             float4 q = __ldg(a.vd + a.bedge[b0 + j]);
-            sv[grp][j] = q;
+            sv_g[j] = q;
             float t[kF];
             bond_t(q.w, t);
 #pragma unroll
-            for (int f = 0; f < kF; ++f) st[grp][j][f] = t[f];
+            for (int f = 0; f < kF; ++f) st_g[j][f] = t[f];
         }
         __syncwarp();
         for (int j = gl; j < k; j += 16) {
-            const float4 qj = sv[grp][j];
+            const float4 qj = sv_g[j];
             float2 m32[kF / 2];  // feature pairs, packed FP32
 #pragma unroll
             for (int i = 0; i < kF / 2; ++i) m32[i] = make_float2(0.f, 0.f);
             for (int e2 = 0; e2 < k; ++e2) {
                 if (e2 == j) continue;  // the reverse pair (linegraph.cpp:16-21)
-                const float4 q2 = sv[grp][e2];
+                const float4 q2 = sv_g[e2];
                 const float c = (q2.x * qj.x + q2.y * qj.y + q2.z * qj.z) / (q2.w * qj.w);
-                const float2* t2 = reinterpret_cast<const float2*>(st[grp][e2]);
+                const float2* t2 = reinterpret_cast<const float2*>(st_g[e2]);
 #pragma unroll
                 for (int i = 0; i < kF / 2; ++i) m32[i] = f2fma(bcast(c), t2[i], m32[i]);
             }
@@ -1254,14 +1283,12 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_forward(BondArgs a, float*
             }
             float fc, dfc;
             fcut3(qj.w, fc, dfc);
-            float tp[kF], th[kF];
+            float tp[kF], th[kF], z[kF];
+            ff_pairs(c_m.W3T, m3, z);  // z_f = sum_g W3[f][g] m3_g
 #pragma unroll
             for (int f = 0; f < kF; ++f) {
-                float z = 0.f;
-#pragma unroll
-                for (int g = 0; g < kF; ++g) z = fmaf(c_m.W3[f * kF + g], m3[g], z);
-                th[f] = tanhf(z);
-                tp[f] = st[grp][j][f] + fc * th[f];
+                th[f] = tanhf(z[f]);
+                tp[f] = st_g[j][f] + fc * th[f];
             }
             store_row16(TP + (size_t)(b0 + j) * kF, tp);
             store_row16(TH3 + (size_t)(b0 + j) * kF, th);
@@ -1286,14 +1313,12 @@ __global__ void k_tb_inject(BondArgs a, const float* __restrict__ TP, float* __r
         for (int f = 0; f < kF; ++f) q[f] += t[f];
     }
     const int64_t r = a.crow ? a.crow[u] : u;
-    float h[kF], th[kF];
+    float h[kF], th[kF], z[kF];
     load_row16(H + r * kF, h);
+    ff_pairs(c_m.W4T, q, z);  // z_f = sum_g W4[f][g] q_g
 #pragma unroll
     for (int f = 0; f < kF; ++f) {
-        float z = 0.f;
-#pragma unroll
-        for (int g = 0; g < kF; ++g) z = fmaf(c_m.W4[f * kF + g], q[g], z);
-        th[f] = tanhf(z);
+        th[f] = tanhf(z[f]);
         h[f] += th[f];
     }
     store_row16(H + r * kF, h);
@@ -1311,13 +1336,7 @@ __global__ void k_tb_bwd_q(int64_t n, const int32_t* __restrict__ nodes,
     load_row16(TH4 + k * kF, th);
 #pragma unroll
     for (int f = 0; f < kF; ++f) y[f] = hb[f] * (1.0f - th[f] * th[f]);
-#pragma unroll
-    for (int g = 0; g < kF; ++g) {
-        float acc = 0.f;
-#pragma unroll
-        for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W4[f * kF + g], y[f], acc);
-        qb[g] = acc;
-    }
+    ff_pairs(c_m.W4, y, qb);  // qb_g = sum_f W4[f][g] y_f
     store_row16(QB + (crow ? (int64_t)crow[v] : v) * kF, qb);
 }
 
@@ -1326,7 +1345,8 @@ __global__ void k_tb_bwd_q(int64_t n, const int32_t* __restrict__ nodes,
 // produced here (fc3 path, identity part of the bond-init adjoint, cos
 // gradient of e'_j); VIN[j] the gradient w.r.t. v_{e_j} produced here
 // (cos gradient of e_j, line-edge part of its bond-init adjoint).
-__global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
+template <int MINB>
+__global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
                                                                const float* __restrict__ QB,
                                                                const float* __restrict__ TH3,
                                                                float4* __restrict__ VIN,
@@ -1375,13 +1395,10 @@ __global__ void __launch_bounds__(kTbWarps * 32) k_tb_backward(BondArgs a,
                 da = fmaf(tpb[f], ds[f], da);
                 y[f] = tpb[f] * fc * (1.0f - th[f] * th[f]);
             }
+            float w3y[kF];
+            ff_pairs(c_m.W3, y, w3y);  // sum_f W3[f][g] y_f
 #pragma unroll
-            for (int g = 0; g < kF; ++g) {
-                float acc = 0.f;
-#pragma unroll
-                for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W3[f * kF + g], y[f], acc);
-                sm[j][g] = acc;
-            }
+            for (int g = 0; g < kF; ++g) sm[j][g] = w3y[g];
             const float c0 = -(dbf + da) / q.w;
             VOUT[b0 + j] = make_float4(q.x * c0, q.y * c0, q.z * c0, 0.f);
         }
@@ -1654,9 +1671,23 @@ void launch_bwd_edge_tc(const ConvArgs& a, const int4* ctab, const int32_t* ccta
     GMD_LAUNCH_CHECK();
 }
 
-void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, cudaStream_t s) {
+static int tb_slots(int max_bonds) {
+    return std::min(kMaxBondsPerAtom, std::max(16, (max_bonds + 15) & ~15));
+}
+
+void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, int max_bonds,
+                       cudaStream_t s) {
     if (a.n == 0) return;
-    k_tb_forward<<<tb_grid(a.n), kTbWarps * 32, 0, s>>>(a, TP, TH3, flags);
+    const int kc = tb_slots(max_bonds);
+    const size_t smem = (sizeof(float) * kF + sizeof(float4)) * kTbGroups * kc;
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_tb_forward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((sizeof(float) * kF + sizeof(float4)) * kTbGroups *
+                                            kMaxBondsPerAtom)));
+        attr = true;
+    }
+    k_tb_forward<<<tb_grid(a.n), kTbWarps * 32, smem, s>>>(a, TP, TH3, flags, kc);
     GMD_LAUNCH_CHECK();
 }
 
@@ -1676,15 +1707,17 @@ void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const
 void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
                         float4* VOUT, double* vir_part, int max_bonds, cudaStream_t s) {
     if (a.n == 0) return;
-    const int kc = std::min(kMaxBondsPerAtom, std::max(16, (max_bonds + 15) & ~15));
+    const int kc = tb_slots(max_bonds);
     const size_t smem = kTbSlotBytes * kTbGroups * kc;
     static bool attr = false;
     if (!attr) {
-        GMD_CUDA(cudaFuncSetAttribute(k_tb_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GMD_CUDA(cudaFuncSetAttribute(k_tb_backward<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(kTbSlotBytes * kTbGroups * kMaxBondsPerAtom)));
         attr = true;
     }
-    k_tb_backward<<<tb_grid(a.n), kTbWarps * 32, smem, s>>>(a, QB, TH3, VIN, VOUT, vir_part, kc);
+    // 4 CTAs x 128 threads per SM (128 registers, no spills): C4 0.353 ms vs
+    // 0.380 / 0.409 ms for 5 / 6 CTAs (96 / 80 registers with spills)
+    k_tb_backward<4><<<tb_grid(a.n), kTbWarps * 32, smem, s>>>(a, QB, TH3, VIN, VOUT, vir_part, kc);
     GMD_LAUNCH_CHECK();
 }
 

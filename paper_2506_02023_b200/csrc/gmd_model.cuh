@@ -18,9 +18,12 @@ struct ModelConst {
     alignas(16) float P[kF * kK];   // f-major: (P[f][k], P[f][k+1]) pairs
     alignas(16) float PT[kK * kF];  // k-major: (P[f][k], P[f+1][k]) pairs
     alignas(16) float Pk[kF * kK];  // k * P[f][k] (derivative of the radial channel)
-    float P3[kF * kK];
-    float W3[kF * kF];
-    float W4[kF * kF];
+    alignas(16) float P3[kF * kK];
+    alignas(16) float P3T[kK * kF];  // k-major: (P3[f][k], P3[f+1][k]) pairs
+    alignas(16) float W3[kF * kF];   // rows f: (W3[f][g], W3[f][g+1]) pairs
+    alignas(16) float W3T[kF * kF];  // W3T[g][f] = W3[f][g]
+    alignas(16) float W4[kF * kF];
+    alignas(16) float W4T[kF * kF];
     float ro[kF];
     float rc, inv_rc, inv_sigma, mu_step;     // atom radial basis
     float a2, pi_rc;                          // sqrt(log2 e)/sigma, pi/rc
@@ -87,7 +90,9 @@ struct BondArgs {
     const int32_t* esrc;    // E: global source id per edge
     const float4* vd;       // E
 };
-void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, cudaStream_t s);
+// max_bonds: largest in-bond count of a center (sizes the per-group staging)
+void launch_tb_forward(const BondArgs& a, float* TP, float* TH3, int32_t* flags, int max_bonds,
+                       cudaStream_t s);
 void launch_tb_inject(const BondArgs& a, const float* TP, float* H, float* TH4, cudaStream_t s);
 void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const float* HB,
                      const float* TH4, float* QB, cudaStream_t s);  // QB by layout row
