@@ -231,7 +231,16 @@ def main():
     Lb = G.lib()
     if world > 1:
         if args.transport == "ipc":
-            G.init_rank_comm_ipc(h, rank, world, slot_rows=max(4096, 4 * n // world))
+            try:
+                G.init_rank_comm_ipc(h, rank, world, slot_rows=max(4096, 4 * n // world))
+            except G.Error as e:  # all ranks agree (collective-safe init): fall back to NCCL
+                if rank == 0:
+                    print(f"bench: CUDA-IPC transport unavailable ({e}); using NCCL", file=sys.stderr)
+                args.transport = "nccl-fallback"
+                config["parallelism"] = config["parallelism"].replace(
+                    "CUDA-IPC P2P halo exchange", "NCCL halo exchange (CUDA-IPC unavailable)")
+                h = G._Handle(device)
+                G.init_rank_comm(h, rank, world)
         else:
             G.init_rank_comm(h, rank, world)
     pbc = np.ones(3, np.uint8)

@@ -1017,16 +1017,32 @@ def init_rank_comm_ipc(handle: "_Handle", rank: int, world: int, slot_rows: int)
     (gloo or nccl), attach the peers' windows."""
     import torch
     import torch.distributed as dist
+    # collective-safe: every rank takes part in both collectives even when its
+    # own export / attach fails, and all ranks agree on the outcome (so a
+    # caller can fall back to the NCCL transport without a hang)
     hd = (C.c_uint8 * 64)()
-    handle.check(lib().gmd_comm_ipc_export(handle.h, rank, world, slot_rows, hd))
-    mine = torch.tensor(list(bytes(hd)), dtype=torch.uint8)
-    if dist.get_backend() == "nccl":
-        mine = mine.cuda()
+    err = None
+    try:
+        handle.check(lib().gmd_comm_ipc_export(handle.h, rank, world, slot_rows, hd))
+    except Error as e:
+        err = e
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    mine = torch.tensor(list(bytes(hd)), dtype=torch.uint8, device=dev)
     allh = [torch.zeros_like(mine) for _ in range(world)]
     dist.all_gather(allh, mine)
-    blob = bytes(b for t in allh for b in t.cpu().tolist())
-    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
-    handle.check(lib().gmd_comm_init_ipc(handle.h, buf))
+    if err is None:
+        blob = bytes(b for t in allh for b in t.cpu().tolist())
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        try:
+            handle.check(lib().gmd_comm_init_ipc(handle.h, buf))
+        except Error as e:
+            err = e
+    ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if err is not None:
+        raise err
+    if int(ok.item()) == 0:
+        raise Error("CUDA-IPC transport failed on a peer rank", GMD_ERR_RUNTIME)
 
 
 def exchange_plan_consistent(scnt, rcnt, rank: int, all_scnt) -> bool:
