@@ -255,6 +255,7 @@ struct gmd_handle {
     int p = 1;
     double rc = 0, r3 = 0, tau = 0;
     bool has_lg = false, allow_narrow = false, corrupted = false;
+    bool z_pending = false;  // species upload on the side stream (ev[6])
     Geom geom{};
     double lat[9]{};
     int axis = 0;
@@ -543,6 +544,13 @@ void build_bond_rank_plan(gmd_handle* h, const int32_t* ownp, int r) {
     sync(h);
 }
 
+// host copies queued on the side stream never outlive the API call that
+// queued them (also on error paths): the caller may reuse its buffers
+struct DrainSide {
+    cudaStream_t side;
+    ~DrainSide() { cudaStreamSynchronize(side); }
+};
+
 void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, const double* lat,
                 const uint8_t* pbc, double rc, double r3, double tau, int p, uint32_t flags) {
     cudaStream_t s = h->stream;
@@ -570,7 +578,19 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     cudaMemcpyKind kind =
         (flags & GMD_INPUT_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     GMD_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, kind, s));
-    GMD_CUDA(cudaMemcpyAsync(dZ, Z, sizeof(int32_t) * n, kind, s));
+    // species are read first by the forward's embedding: a host upload runs
+    // on the side stream under the graph build (the forward waits on ev[6];
+    // the side stream is drained before gmd_build returns, so the caller may
+    // reuse its buffer afterwards)
+    DrainSide drain{h->side};
+    if (flags & GMD_INPUT_DEVICE) {
+        GMD_CUDA(cudaMemcpyAsync(dZ, Z, sizeof(int32_t) * n, kind, s));
+        h->z_pending = false;
+    } else {
+        GMD_CUDA(cudaMemcpyAsync(dZ, Z, sizeof(int32_t) * n, kind, h->side));
+        GMD_CUDA(cudaEventRecord(h->ev[6], h->side));
+        h->z_pending = true;
+    }
     ensure_periodic_dev(h, pbc, rc);
     if (std::abs(det3(h->lat)) < 1e-10)
         raise(kConfig, "periodic system requires an invertible lattice");
@@ -1024,6 +1044,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     if (std::abs(h->rc - h->p_r_atom) > 1e-12)
         raise(kConfig, "distributed handle cutoff does not match the parameters");
     cudaStream_t s = h->stream;
+    DrainSide drain{h->side};
     const int64_t n_all = h->n;
     const bool rank_mode = h->comm && h->comm->world > 1;
     const int64_t n = rank_mode ? h->n_own : n_all;  // nodes this handle updates
@@ -1046,8 +1067,26 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     const char* tc_env = std::getenv("GMD_BWD_TC");
     const bool use_tc = tc_env && tc_env[0] == '1';
     const int vgrid = use_tc ? bwd_tc_grid(n) : bwd_edge_grid(n);
+    // host forces (e2e): the last layer's edge pass runs in node chunks; a
+    // chunk's forces are final once it finishes (GRAD[v] gathers only v's
+    // in-edges; the three-body terms came at l = L - 1), so they go to the
+    // host on the side stream while the next chunk computes
+    constexpr int kForceChunks = 4;
+    auto pinned = [](const void* p) {  // a pageable copy would block the launching thread
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return at.type == cudaMemoryTypeHost;
+    };
+    const int nchunk = (!rank_mode && forces && !(flags & GMD_OUTPUT_DEVICE) && pinned(forces) &&
+                        !(flags & GMD_OUTPUT_F32) && !use_tc && bwd_edge_ranges() &&
+                        !(tb && L == 1) && bwd_edge_grid(n / kForceChunks) == vgrid)
+                           ? kForceChunks
+                           : 1;
     double* e_part = h->e_part.get<double>(grid);
-    double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);
+    double* v_part = h->v_part.get<double>((size_t)(L + nchunk - 1) * vgrid * 6);
     const int tgrid = tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
@@ -1134,6 +1173,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     };
 
     // ---- feature calculation: embeddings for every layout row (:597-602)
+    if (h->z_pending) {
+        GMD_CUDA(cudaStreamWaitEvent(s, h->ev[6], 0));
+        h->z_pending = false;
+    }
     { PROF("embed"); launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s); }
     GMD_CUDA(cudaEventRecord(h->ev[3], s));
 
@@ -1170,8 +1213,24 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             if (use_tc)
                 launch_bwd_edge_tc(a, h->ctab.as<int4>(), h->ccta.as<int32_t>(), vgrid, MB, H[l], HB,
                                    GRAD, v_part + (size_t)l * vgrid * 6, s);
-            else
+            else if (l > 0 || nchunk == 1)
                 launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+            else {  // l = 0 in node chunks, forces streamed out per chunk
+                double* fd = h->forces.get<double>(3 * n_all);
+                for (int c = 0; c < nchunk; ++c) {
+                    ConvArgs ac = a;
+                    ac.k0 = n * c / nchunk;
+                    ac.n = n * (c + 1) / nchunk;
+                    // virial partials: layer 0's slot, then slots L .. L + nchunk - 2
+                    const int slot = c == 0 ? 0 : L - 1 + c;
+                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part + (size_t)slot * vgrid * 6, s);
+                    launch_forces_out(ac.n - ac.k0, nullptr, GRAD + ac.k0, fd + 3 * ac.k0, nullptr, s);
+                    GMD_CUDA(cudaEventRecord(h->ev[7], s));
+                    GMD_CUDA(cudaStreamWaitEvent(h->side, h->ev[7], 0));
+                    GMD_CUDA(cudaMemcpyAsync(static_cast<double*>(forces) + 3 * ac.k0, fd + 3 * ac.k0,
+                                             24 * (ac.n - ac.k0), cudaMemcpyDeviceToHost, h->side));
+                }
+            }
         }
         if (tb && l == L - 1) {
             float* QB = h->QB.get<float>(R * kF);
@@ -1198,13 +1257,15 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             if (ff) GMD_CUDA(cudaMemsetAsync(ff, 0, 12 * n_all, s));
             if (fd) GMD_CUDA(cudaMemsetAsync(fd, 0, 24 * n_all, s));
         }
-        PROF("forces_out");
-        launch_forces_out(n, a.nodes, GRAD, fd, ff, s);
+        if (nchunk == 1) {  // else written per chunk above
+            PROF("forces_out");
+            launch_forces_out(n, a.nodes, GRAD, fd, ff, s);
+        }
     }
     {
         PROF("reduce");
         const double* ps[3] = {e_part, v_part, v3_part};
-        const int np[3] = {grid, L * vgrid, tgrid}, w[3] = {1, 6, 9};
+        const int np[3] = {grid, (L + nchunk - 1) * vgrid, tgrid}, w[3] = {1, 6, 9};
         if (!tb) GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
         launch_reduce_sets(tb ? 3 : 2, ps, np, w, red, s);
     }
@@ -1225,7 +1286,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             GMD_CUDA(cudaStreamSynchronize(h->side));  // pa_early copy
         }
     }
-    if (forces && !out_dev) {
+    if (forces && !out_dev && nchunk == 1) {
         if (out_f32)
             GMD_CUDA(cudaMemcpyAsync(forces, ff, 12 * n_all, cudaMemcpyDeviceToHost, s));
         else
@@ -1233,6 +1294,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
     int32_t hdr[2];
     read_flags(h, hdr);  // synchronizes the stream
+    if (nchunk > 1) GMD_CUDA(cudaStreamSynchronize(h->side));  // streamed force chunks
     if (rank_mode) {  // energy + virial: rank-ordered sum of the per-rank sums
         std::vector<double> all((size_t)h->comm->world * 16);
         h->comm->allgather_f64(s, hred, 16, all.data());

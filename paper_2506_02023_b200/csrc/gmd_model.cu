@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
     const int64_t ng = (int64_t)gridDim.x * (NT / 16);
     const float isg = c_m.inv_sigma, mus = c_m.mu_step;
     if (gl < 6) sVir[grp][gl] = 0.0;
-    const int64_t iters = (a.n + ng - 1) / ng;
+    const int64_t iters = (a.n - a.k0 + ng - 1) / ng;  // nodes [k0, n)
     int e0n = 0, e1n = 0;
     float mun = 0.f, hun = 0.f;
     BwdEdgeIn xa;
@@ -807,9 +807,9 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
             e0n = e1n = 0;
         }
     };
-    prefetch(g0);
+    prefetch(a.k0 + g0);
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t k = g0 + it * ng;
+        const int64_t k = a.k0 + g0 + it * ng;
         const bool valid = k < a.n;
         const int e0 = e0n, e1 = e1n;
         __syncwarp();
@@ -1629,11 +1629,14 @@ int bwd_edge_grid(int64_t n) {
     return (int)(g > 0 ? g : 1);
 }
 
+bool bwd_edge_ranges() { return bwd_variant() != 1; }
+
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
                      double* vir_part, cudaStream_t s) {
-    if (a.n == 0) return;
+    if (a.n - a.k0 <= 0) return;
     const int variant = bwd_variant();
-    const int g = bwd_edge_grid(a.n);
+    if (variant == 1 && a.k0 != 0) raise(kRuntime, "internal: node ranges need the default kernel");
+    const int g = bwd_edge_grid(a.n - a.k0);
     if (variant == 1)  // scalar-FFMA kernel (A/B reference)
         k_bwd_edge<<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
     else

@@ -46,6 +46,7 @@ struct ConvArgs {
     const int32_t* lsrc;
     const float4* vd;  // (vx, vy, vz, d) per edge (backward)
     const float* d;    // d per edge (forward)
+    int64_t k0 = 0;    // first node processed (launch_bwd_edge: nodes [k0, n))
 };
 
 int model_grid(int64_t n);  // fixed grid => deterministic reductions
@@ -66,6 +67,8 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 // GRAD += positional gradient, virial partials per CTA (6 doubles)
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
                      double* vir_part, cudaStream_t s);
+// the default kernel takes node ranges (a.k0 > 0); grid = bwd_edge_grid(n - k0)
+bool bwd_edge_ranges();
 
 // the same pass with the radial contractions on tcgen05 (TMEM accumulator);
 // tcgen05 backward edge pass over 16-edge chunk records (one per chunk of a

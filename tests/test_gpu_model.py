@@ -150,3 +150,35 @@ def test_kernel_families_agree(monkeypatch, other):
         np.testing.assert_array_equal(b.per_atom, a.per_atom)
     np.testing.assert_allclose(b.forces, a.forces, rtol=0, atol=2e-5 * np.abs(a.forces).max())
     np.testing.assert_allclose(b.stress, a.stress, rtol=0, atol=1e-6)
+
+
+def test_streamed_force_chunks_match_device_output():
+    """Host forces in pinned memory: the last edge pass runs in node chunks and
+    each chunk's forces are copied out while the next computes; forces and
+    per-atom energies are bitwise those of device output, the stress equal up
+    to the regrouped fixed-order virial partials."""
+    import ctypes as C
+    import torch
+    s = S.quartz((15, 15, 15))  # 30,375 atoms: large enough for the chunked pass
+    prm = params_for(3, 3, 5.0)
+    n = s.size()
+    L = G.lib()
+    h = G._Handle(0)
+    h.check(L.gmd_set_params(h.h, 16, 8, 3, 5.0, 0.0, G._p(prm.blob)))
+    pbc = np.ones(3, np.uint8)
+    h.check(L.gmd_build(h.h, n, G._p(s.positions), G._p(s.species), G._p(s.lattice), G._p(pbc), 5.0,
+                        0.0, 0.0, 1, 0, G.GMD_ALLOW_NARROW))
+    e1, e2 = C.c_double(), C.c_double()
+    st1, st2 = np.zeros(9), np.zeros(9)
+    pa_d = torch.empty(n, dtype=torch.float64, device="cuda")
+    f_d = torch.empty(3 * n, dtype=torch.float64, device="cuda")
+    h.check(L.gmd_forward(h.h, C.byref(e1), C.c_void_p(pa_d.data_ptr()), C.c_void_p(f_d.data_ptr()),
+                          G._p(st1), None, G.GMD_OUTPUT_DEVICE))
+    pa_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    f_h = torch.full((3 * n,), np.nan, dtype=torch.float64).pin_memory()
+    h.check(L.gmd_forward(h.h, C.byref(e2), C.c_void_p(pa_h.data_ptr()), C.c_void_p(f_h.data_ptr()),
+                          G._p(st2), None, 0))
+    np.testing.assert_array_equal(f_h.numpy(), f_d.cpu().numpy())
+    np.testing.assert_array_equal(pa_h.numpy(), pa_d.cpu().numpy())
+    assert e1.value == e2.value
+    np.testing.assert_allclose(st2, st1, rtol=1e-12, atol=1e-18)
