@@ -440,11 +440,14 @@ __global__ void k_nl_emit(const Geom g, int64_t n, int cap,
     const double pix = pos[3 * i], piy = pos[3 * i + 1], piz = pos[3 * i + 2];
     const int cix = cell[3 * i], ciy = cell[3 * i + 1], ciz = cell[3 * i + 2];
     int nb = 0;
+    // the next slot's key is requested before this slot's gathers complete
+    unsigned long long knext = lane < cnt ? __ldg(slab + (size_t)i * cap + lane) : 0ull;
     for (int kb = 0; __any_sync(0xffffffffu, kb < cnt); kb += G) {
         const int k = kb + lane;
         bool isb = false;
+        const unsigned long long key = knext;
+        if (k + G < cnt) knext = __ldg(slab + (size_t)i * cap + k + G);
         if (k < cnt) {
-            const unsigned long long key = slab[(size_t)i * cap + k];
             const int j = (int)(key >> 24);
             const int q0 = (int)((key >> 16) & 255) - 128;
             const int q1 = (int)((key >> 8) & 255) - 128;
