@@ -52,6 +52,45 @@ __global__ void k_gather(const float* __restrict__ tab, const int* __restrict__ 
     out[t] = acc;
 }
 
+// each lane still ends with its own two full rows, but every load
+// instruction is shared by a lane pair: in step A the pair reads the two
+// halves of the even lane's row, in step B of the odd lane's row; then each
+// lane swaps the half it holds of its partner's row (8 SHFL per row)
+__global__ void k_pair_swap(const float* __restrict__ tab, const int* __restrict__ idx, int steps,
+                            float* out) {
+    float acc = 0.f;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, half = lane & 1;
+    for (int s = 0; s < steps; ++s) {
+        const int i0 = __ldg(idx + ((t * 2 + s * 977) & 0xfffff));
+        const int i1 = __ldg(idx + ((t * 2 + 1 + s * 977) & 0xfffff));
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int mine = r ? i1 : i0;
+            const int other = __shfl_xor_sync(0xffffffffu, mine, 1);
+            const int ra = half ? other : mine;   // row of the even lane
+            const int rb = half ? mine : other;   // row of the odd lane
+            float4 a0, a1, b0, b1;
+            ld256(tab + (size_t)ra * 16 + 8 * half, a0, a1);  // halves of the even lane's row
+            ld256(tab + (size_t)rb * 16 + 8 * half, b0, b1);  // halves of the odd lane's row
+            // even lane keeps a (its row, half 0) and needs half 0 of... : it
+            // holds half 0 of both rows; it needs half 1 of its row (held by
+            // the odd lane as a) and gives half 0 of the odd row (b).
+            float4 s0 = half ? a0 : b0, s1 = half ? a1 : b1;  // what the partner needs
+            float4 g0, g1;
+            g0.x = __shfl_xor_sync(0xffffffffu, s0.x, 1); g0.y = __shfl_xor_sync(0xffffffffu, s0.y, 1);
+            g0.z = __shfl_xor_sync(0xffffffffu, s0.z, 1); g0.w = __shfl_xor_sync(0xffffffffu, s0.w, 1);
+            g1.x = __shfl_xor_sync(0xffffffffu, s1.x, 1); g1.y = __shfl_xor_sync(0xffffffffu, s1.y, 1);
+            g1.z = __shfl_xor_sync(0xffffffffu, s1.z, 1); g1.w = __shfl_xor_sync(0xffffffffu, s1.w, 1);
+            // own row: even = (a [half 0], g [half 1]); odd = (g [half 0], b [half 1])
+            const float4 h0 = half ? g0 : a0, h1 = half ? g1 : a1;
+            const float4 h2 = half ? b0 : g0, h3 = half ? b1 : g1;
+            acc += h0.x + h1.y + h2.z + h3.w;
+        }
+    }
+    out[t] = acc;
+}
+
 int main() {
     const int rows = 1 << 20;
     float *tab, *out;
@@ -89,6 +128,7 @@ int main() {
             run(k_gather<1>, 1, "lane1 (2 x LDG.256 / row)");
             run(k_gather<2>, 2, "lane2 (LDG.256 / lane) ");
             run(k_gather<4>, 4, "lane4 (LDG.128 / lane) ");
+            run(k_pair_swap, 1, "pair loads + SHFL swap ");
         }
     }
     return 0;
