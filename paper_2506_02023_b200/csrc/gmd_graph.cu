@@ -176,7 +176,8 @@ __device__ __forceinline__ void bitonic64(uint32_t& k0, uint32_t& k1, int lane) 
 
 // Search, one WARP per destination bin (no CTA barriers).  Shared memory per
 // warp: WarpNL + the destination group (<= group atoms) + group x cap keys.
-__global__ void __launch_bounds__(kThreads, 3) k_nl_search(
+template <int CTAS>
+__global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
     const Geom g, float thr32, float acc32, float zero32, int64_t nbins, int64_t n, int group,
     int cap,
     const int32_t* __restrict__ bin_start, const int32_t* __restrict__ s_id,
@@ -629,20 +630,28 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int
                       int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s) {
-    // destinations staged per warp: as many as fit three CTAs per SM (the
-    // search is latency-bound; occupancy beats fewer candidate rescans)
+    // destinations staged per warp (the search is latency-bound; occupancy
+    // beats fewer candidate rescans)
     static const int gmax = [] {
         const char* v = std::getenv("GMD_NL_GROUP");
         return v ? std::max(1, std::min(32, std::atoi(v))) : 16;
     }();
+    // four CTAs per SM (64 registers) when a full destination group still fits
+    // their shared memory (C5: 1.04 -> 0.93 ms); otherwise three with the full
+    // group (C4's deeper rows: a smaller group at 4 CTAs rescans candidates
+    // more often, 0.198 -> 0.214 ms)
+    const int ctas = nl_smem(gmax, cap) <= 55 * 1024 ? 4 : 3;
+    const size_t fit = ctas == 4 ? 55 * 1024 : 74 * 1024;
     int group = gmax;
-    while (group > 4 && nl_smem(group, cap) > 74 * 1024) --group;
+    while (group > 4 && nl_smem(group, cap) > fit) --group;
     while (group > 1 && nl_smem(group, cap) > 110 * 1024) group >>= 1;
     const size_t sm = nl_smem(group, cap);
     if (sm > 200 * 1024) raise(kRuntime, "neighbour search: per-atom degree too large");
     static bool attr = false;
     if (!attr) {
-        GMD_CUDA(cudaFuncSetAttribute(k_nl_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GMD_CUDA(cudaFuncSetAttribute(k_nl_search<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        GMD_CUDA(cudaFuncSetAttribute(k_nl_search<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
         attr = true;
     }
@@ -652,7 +661,8 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int
     if (cbits > 31 || n > ((int64_t)1 << (32 - cbits)))
         raise(kConfig, "neighbour search: atom count too large for the " + std::to_string(ncell) +
                            "-cell stencil (row keys are src << " + std::to_string(cbits) + " | cell)");
-    k_nl_search<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, acc32, zero32, nbins, n, group, cap,
+    auto kern = ctas == 4 ? k_nl_search<4> : k_nl_search<3>;
+    kern<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, acc32, zero32, nbins, n, group, cap,
                                                      b.bin_start,
                                                      b.s_id, b.s_w, b.s_p, b.s_c, b.deg, b.flags,
                                                      slab, owner, only, cbits);
