@@ -423,8 +423,8 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
 // slab rows -> canonical CSR (neighborlist.cpp:60-85): recompute the exact
 // fp64 vector through the raw positions (:178-191) from (src, image), round
 // to fp32 for the model, mark three-body bonds (linegraph.cpp:34-35).
-template <int G>  // lanes per destination row (16 or 32)
-__global__ void k_nl_emit(const Geom g, int64_t n, int cap,
+template <int G, int MINB = 1>  // lanes per destination row (16 or 32)
+__global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, int cap,
                           const unsigned long long* __restrict__ slab,
                           const int32_t* __restrict__ row, const double* __restrict__ pos,
                           const int32_t* __restrict__ cell, int32_t* __restrict__ e_src,
@@ -636,11 +636,13 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int
         const char* v = std::getenv("GMD_NL_GROUP");
         return v ? std::max(1, std::min(32, std::atoi(v))) : 16;
     }();
-    // four CTAs per SM (64 registers) when a full destination group still fits
-    // their shared memory (C5: 1.04 -> 0.93 ms); otherwise three with the full
-    // group (C4's deeper rows: a smaller group at 4 CTAs rescans candidates
-    // more often, 0.198 -> 0.214 ms)
-    const int ctas = nl_smem(gmax, cap) <= 55 * 1024 ? 4 : 3;
+    // four CTAs per SM (64 registers) when a group of >= 12 destinations still
+    // fits their shared memory (C5: 14 destinations, 1.04 -> 0.93 ms);
+    // otherwise three (C4's deeper rows leave 9 at four CTAs: more candidate
+    // rescans, 0.198 -> 0.214 ms)
+    int g4 = gmax;
+    while (g4 > 1 && nl_smem(g4, cap) > 55 * 1024) --g4;
+    const int ctas = g4 >= 12 ? 4 : 3;
     const size_t fit = ctas == 4 ? 55 * 1024 : 74 * 1024;
     int group = gmax;
     while (group > 4 && nl_smem(group, cap) > fit) --group;
@@ -675,7 +677,9 @@ void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long*
     // 16 lanes per row: ~45-edge rows fill 3 x 16 slots (94 %) instead of
     // 2 x 32 (70 %); C5 0.70 -> 0.53 ms
     // 128-thread blocks (C5: 128 0.516 ms, 256 0.527, 512 0.624, 1024 0.656)
-    k_nl_emit<16><<<div_up(n, 8), 128, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src,
+    // 12 CTAs per SM (40 registers): 0.480 -> 0.472 ms at C5 (16 CTAs / 32
+    // registers spill: 0.595 ms)
+    k_nl_emit<16, 12><<<div_up(n, 8), 128, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src,
                                                gd.img, gd.vd, gd.d, gd.bond, b.bcnt, b.flags);
     GMD_LAUNCH_CHECK();
 }
