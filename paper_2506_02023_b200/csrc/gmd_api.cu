@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -272,6 +274,7 @@ struct gmd_handle {
     // model
     bool params_set = false;
     ModelConst mc{};
+    uint64_t mc_ver = 0;  // globally unique id of the current parameter set
     int F = 16, K = 8, L = 0;
     double p_r_atom = 0, p_r3 = 0;
     std::vector<DBuf> H;
@@ -1052,7 +1055,17 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     LayoutState& A = h->atoms;
     const int64_t R = A.rows;
     const bool part = h->p > 1;
-    upload_model(h->mc, s);
+    {   // the __constant__ model copy is per device: upload only when another
+        // parameter set was resident (saves a blocking pageable copy per step)
+        static std::mutex mu;
+        static uint64_t resident[64] = {};
+        std::lock_guard<std::mutex> lock(mu);
+        const int dv = h->device & 63;
+        if (resident[dv] != h->mc_ver) {
+            upload_model(h->mc, s);
+            resident[dv] = h->mc_ver;
+        }
+    }
 
     GMD_CUDA(cudaEventRecord(h->ev[2], s));
     if ((int)h->H.size() < L + 1) h->H.resize(L + 1);
@@ -1509,6 +1522,8 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         h->p_r_atom = r_atom;
         h->p_r3 = r3;
         h->params_set = true;
+        static std::atomic<uint64_t> next_ver{1};
+        h->mc_ver = next_ver++;
     });
 }
 
