@@ -74,16 +74,17 @@ KERNEL_OF = {"bwd_edge": "k_bwd_edge2", "conv": "k_conv2", "nl_search": "k_nl_se
              "nl_emit": "k_nl_emit", "bwd_node": "k_bwd_node"}
 
 
-def ncu_traffic(config, kname):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kname`
-    from the committed `ncu --set full` capture of this config (profiles/)."""
+def ncu_metrics(config, kname):
+    """The committed `ncu --set full` summary of one launch of `kname` for this
+    config (profiles/): dram__bytes_read.sum + dram__bytes_write.sum and the
+    kernel's utilisation figures."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{config}.json")), reverse=True):
         try:
             with open(path) as f:
                 m = json.load(f).get(KERNEL_OF.get(kname, "k_" + kname))
             if m and m.get("dram_bytes"):
-                return m["dram_bytes"], os.path.relpath(path, ROOT)
+                return m, os.path.relpath(path, ROOT)
         except (OSError, ValueError):
             pass
     return None, None
@@ -187,9 +188,10 @@ def main():
     metric = "atoms/sec energy+force eval (1/2/4/8 B200) at 1M atoms; graph-build ms"
     config = {"workload": f"{args.config}: {desc}", "model": "ToyPotential F=16 K=8",
               "layers": L, "partitions": max(world, args.gpus),
-              "parallelism": f"slab-partitioned, {max(world, args.gpus)} rank(s), "
-                             + ("CUDA-IPC P2P halo exchange" if args.transport == "ipc"
-                                else "NCCL halo exchange"),
+              "parallelism": ("1 GPU, one partition (no halo exchange)" if max(world, args.gpus) == 1
+                              else f"slab-partitioned, {max(world, args.gpus)} rank(s), "
+                              + ("CUDA-IPC P2P halo exchange" if args.transport == "ipc"
+                                 else "NCCL halo exchange")),
               "l2": "inputs > L2 (no flush)"}
 
     if args.impl == "reference":
@@ -355,11 +357,16 @@ def main():
         per_launch_ms = kms / max(kl, 1)
         ab = bm.get(kname)
         ach = ab / (per_launch_ms * 1e-3) / 1e9 if ab else None
-        traffic, tsrc = ncu_traffic(args.config, kname)
+        nm, tsrc = ncu_metrics(args.config, kname)
+        traffic = nm["dram_bytes"] if nm else None
         roof = {"kernel": kname, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": tsrc,
                 "algorithmic_bytes_per_launch": ab, "ms_per_launch": per_launch_ms,
                 "share_of_step": kms / ms, "peak_source": peak_kind}
+        if nm:  # what actually limits it: instruction issue and the
+            # memory pipes (for the model kernels, the L1 data pipe serving gathers)
+            roof["limiter"] = {"issue_active_pct": nm.get("issue%"), "mem_pipes_busy_pct": nm.get("mem%"),
+                               "fma_pipe_pct": nm.get("fma%"), "source": tsrc}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
