@@ -28,6 +28,7 @@
 #include "../../include/graphmd_b200.h"
 #include "gmd_comm.cuh"
 #include "gmd_common.cuh"
+#include "gmd_generic.cuh"
 #include "gmd_graph.cuh"
 #include "gmd_md.cuh"
 #include "gmd_model.cuh"
@@ -275,6 +276,9 @@ struct gmd_handle {
     bool params_set = false;
     ModelConst mc{};
     uint64_t mc_ver = 0;  // globally unique id of the current parameter set
+    bool generic = false;  // widths other than the tuned F = 16, K = 8 (gmd_generic.cu)
+    GenModel gm{};
+    DBuf gpar;             // fp32 parameter tables of the generic kernels
     int F = 16, K = 8, L = 0;
     double p_r_atom = 0, p_r3 = 0;
     std::vector<DBuf> H;
@@ -1055,13 +1059,17 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     LayoutState& A = h->atoms;
     const int64_t R = A.rows;
     const bool part = h->p > 1;
+    const bool gen = h->generic;  // widths other than F = 16, K = 8 (gmd_generic.cu)
+    const int F = gen ? h->F : kF;
+    if (gen && tb)
+        raise(kConfig, "three-body parameters need feature_width=16, basis_count=8, <= 8 layers");
     {   // the __constant__ model copy is per device: upload only when another
         // parameter set was resident (saves a blocking pageable copy per step)
         static std::mutex mu;
         static uint64_t resident[64] = {};
         std::lock_guard<std::mutex> lock(mu);
         const int dv = h->device & 63;
-        if (resident[dv] != h->mc_ver) {
+        if (!gen && resident[dv] != h->mc_ver) {
             upload_model(h->mc, s);
             resident[dv] = h->mc_ver;
         }
@@ -1070,16 +1078,16 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     GMD_CUDA(cudaEventRecord(h->ev[2], s));
     if ((int)h->H.size() < L + 1) h->H.resize(L + 1);
     std::vector<float*> H(L + 1);
-    for (int l = 0; l <= L; ++l) H[l] = h->H[l].get<float>(R * kF);
-    float* TH = h->TH.get<float>((size_t)L * n * kF);
-    float* MB = h->MB.get<float>(R * kF);
-    float* HB = h->HB.get<float>(n * kF);
+    for (int l = 0; l <= L; ++l) H[l] = h->H[l].get<float>(R * F);
+    float* TH = h->TH.get<float>((size_t)L * n * F);
+    float* MB = h->MB.get<float>(R * F);
+    float* HB = h->HB.get<float>(n * F);
     float4* GRAD = h->GRAD.get<float4>(n);
     const int grid = model_grid(n);
     // backward edge pass: FFMA kernel, or the tcgen05 kernel with GMD_BWD_TC=1
     const char* tc_env = std::getenv("GMD_BWD_TC");
-    const bool use_tc = tc_env && tc_env[0] == '1';
-    const int vgrid = use_tc ? bwd_tc_grid(n) : bwd_edge_grid(n);
+    const bool use_tc = !gen && tc_env && tc_env[0] == '1';
+    const int vgrid = gen ? gen_grid(n) * 8 : use_tc ? bwd_tc_grid(n) : bwd_edge_grid(n);
     // host forces (e2e): the last layer's edge pass runs in node chunks; a
     // chunk's forces are final once it finishes (GRAD[v] gathers only v's
     // in-edges; the three-body terms came at l = L - 1), so they go to the
@@ -1093,7 +1101,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         }
         return at.type == cudaMemoryTypeHost;
     };
-    const int nchunk = (!rank_mode && forces && !(flags & GMD_OUTPUT_DEVICE) && pinned(forces) &&
+    const int nchunk = (!gen && !rank_mode && forces && !(flags & GMD_OUTPUT_DEVICE) && pinned(forces) &&
                         !(flags & GMD_OUTPUT_F32) && !use_tc && bwd_edge_ranges() &&
                         !(tb && L == 1) && bwd_edge_grid(n / kForceChunks) == vgrid)
                            ? kForceChunks
@@ -1142,24 +1150,30 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     // (engine.cpp:122-143); one rank per GPU packs its TO rows and goes
     // through the transport
     const int64_t nsend = rank_mode ? std::accumulate(h->scnt.begin(), h->scnt.end(), (int64_t)0) : 0;
-    float* sendbuf = rank_mode ? h->sendbuf.get<float>(std::max<int64_t>(1, nsend) * kF) : nullptr;
+    float* sendbuf = rank_mode ? h->sendbuf.get<float>(std::max<int64_t>(1, nsend) * F) : nullptr;
     auto exchange = [&](float* buf, bool fwd = false) {
         if (rank_mode) {
             {
                 PROF("halo_pack");
                 if (nsend > 0) {
-                    k_gather_rows<<<div_up(nsend * kF, 256), 256, 0, s>>>(
+                    k_gather_rows<<<div_up(nsend * F, 256), 256, 0, s>>>(
                         nsend, h->xsend.as<int32_t>(), reinterpret_cast<const uint32_t*>(buf),
-                        reinterpret_cast<uint32_t*>(sendbuf), kF);
+                        reinterpret_cast<uint32_t*>(sendbuf), F);
                     GMD_LAUNCH_CHECK();
                 }
             }
             PROF("halo_exchange");
             h->comm->exchange(s, sendbuf, h->soff.data(), h->scnt.data(), buf, h->roff.data(),
-                              h->rcnt.data(), kF);
+                              h->rcnt.data(), F);
         } else if (A.nfrom > 0) {
             PROF("exchange");
-            launch_exchange(A.nfrom, xd, fwd ? xs_fwd : xs, buf, kF, s);
+            if (gen) {  // any row width: 32-bit words
+                k_copy_rows<<<div_up(A.nfrom * F, 256), 256, 0, s>>>(
+                    A.nfrom, xd, fwd ? xs_fwd : xs, reinterpret_cast<uint32_t*>(buf), F);
+                GMD_LAUNCH_CHECK();
+            } else {
+                launch_exchange(A.nfrom, xd, fwd ? xs_fwd : xs, buf, kF, s);
+            }
         }
     };
 
@@ -1190,7 +1204,13 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         GMD_CUDA(cudaStreamWaitEvent(s, h->ev[6], 0));
         h->z_pending = false;
     }
-    { PROF("embed"); launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s); }
+    {
+        PROF("embed");
+        if (gen)
+            launch_gen_embed(h->gm, R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
+        else
+            launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
+    }
     GMD_CUDA(cudaEventRecord(h->ev[3], s));
 
     // ---- forward (:657-793)
@@ -1203,8 +1223,12 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         }
         if (l > 0 || tbl) exchange(H[l], true);
         PROF("conv");
-        launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
-                    l == L - 1 ? e_part : nullptr, s);
+        if (gen)
+            launch_gen_conv(h->gm, a, l, H[l], H[l + 1], TH + (size_t)l * n * F,
+                            l == L - 1 ? pa : nullptr, s);
+        else
+            launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
+                        l == L - 1 ? e_part : nullptr, s);
     }
     GMD_CUDA(cudaEventRecord(h->ev[4], s));
     // per-atom energies are final after the forward: copy them to the host
@@ -1216,14 +1240,25 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
 
     // ---- backward (:796-984)
-    launch_init_hbar(n, HB, s);
+    if (gen)
+        launch_gen_init_hbar(h->gm, n, HB, s);
+    else
+        launch_init_hbar(n, HB, s);
     GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
-        { PROF("bwd_node"); launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s); }
+        {
+            PROF("bwd_node");
+            if (gen)
+                launch_gen_bwd_node(h->gm, n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * F, MB, s);
+            else
+                launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s);
+        }
         exchange(MB);
         {
             PROF("bwd_edge");
-            if (use_tc)
+            if (gen)
+                launch_gen_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+            else if (use_tc)
                 launch_bwd_edge_tc(a, h->ctab.as<int4>(), h->ccta.as<int32_t>(), vgrid, MB, H[l], HB,
                                    GRAD, v_part + (size_t)l * vgrid * 6, s);
             else if (l > 0 || nchunk == 1)
@@ -1277,8 +1312,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
     {
         PROF("reduce");
-        const double* ps[3] = {e_part, v_part, v3_part};
-        const int np[3] = {grid, (L + nchunk - 1) * vgrid, tgrid}, w[3] = {1, 6, 9};
+        // generic kernels: the energy is the fixed-order sum of the per-atom energies
+        const double* ps[3] = {gen ? pa : e_part, v_part, v3_part};
+        const int np[3] = {gen ? (int)n_all : grid, (L + nchunk - 1) * vgrid, tgrid},
+                  w[3] = {1, 6, 9};
         if (!tb) GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
         launch_reduce_sets(tb ? 3 : 2, ps, np, w, red, s);
     }
@@ -1406,7 +1443,7 @@ void gmd_destroy(gmd_handle* h) {
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp,
                     &h->md_part, &h->md_out, &h->md_bad, &h->md_pos, &h->md_vel, &h->md_frc,
-                    &h->md_mass, &h->md_z};
+                    &h->md_mass, &h->md_z, &h->gpar};
     for (DBuf* b : bufs) b->release();
     for (LayoutState* ls : {&h->atoms, &h->bonds}) {
         DBuf* lb[] = {&ls->node_array, &ls->crow, &ls->list_off_d, &ls->xdst, &ls->xsrc,
@@ -1467,12 +1504,49 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         if (r_atom <= 0.0) raise(kConfig, "atom cutoff must be positive");
         if (r3 > 0.0 && r3 > r_atom)
             raise(kConfig, "three-body cutoff cannot exceed the atom cutoff");
-        if (F != kF || K != kK)
-            raise(kConfig, "compiled kernels support feature_width=16, basis_count=8 only");
-        if (L > kMaxLayers) raise(kConfig, "compiled kernels support at most 8 layers");
         const int64_t total = gmd_params_size(F, K, L);
         for (int64_t i = 0; i < total; ++i)
             if (!std::isfinite(blob[i])) raise(kConfig, "parameter blob contains a non-finite value");
+        h->generic = F != kF || K != kK || L > kMaxLayers;
+        if (h->generic) {  // width-generic kernels: fp32 tables in global memory
+            if (F > kGenMaxF || K > kGenMaxK)
+                raise(kConfig, "feature_width <= 128 and basis_count <= 32 are supported");
+            const size_t nemb = 119 * (size_t)F, nW = (size_t)L * F * F, nb = (size_t)L * F,
+                         nP = (size_t)F * K;
+            std::vector<float> t(nemb + nW + nb + 2 * nP + F);
+            const double* q = blob;
+            size_t o = 0;
+            for (size_t i = 0; i < nemb + nW + nb + nP; ++i) t[o++] = (float)*q++;  // emb, W, b, P
+            const double* Pd = blob + nemb + nW + nb;
+            for (size_t i = 0; i < nP; ++i) t[o++] = (float)(Pd[i] * (double)(i % K));  // k P
+            q += nP + 2 * (size_t)F * F;  // P3, W3, W4 (three-body: tuned widths only)
+            for (int i = 0; i < F; ++i) t[o++] = (float)*q++;  // readout
+            float* d = h->gpar.get<float>(t.size());
+            GMD_CUDA(cudaMemcpy(d, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
+            GenModel& g = h->gm;
+            g.F = F;
+            g.K = K;
+            g.L = L;
+            g.emb = d;
+            g.W = d + nemb;
+            g.b = g.W + nW;
+            g.P = g.b + nb;
+            g.Pk = g.P + nP;
+            g.ro = g.Pk + nP;
+            g.rc = (float)r_atom;
+            g.inv_rc = (float)(1.0 / r_atom);
+            g.inv_sigma = (float)(K / r_atom);  // sigma = rc / K (potential.cpp:34)
+            g.mu_step = K > 1 ? (float)(r_atom / (K - 1)) : 0.f;
+            h->F = F;
+            h->K = K;
+            h->L = L;
+            h->p_r_atom = r_atom;
+            h->p_r3 = r3;
+            h->params_set = true;
+            static std::atomic<uint64_t> gen_ver{1ull << 62};
+            h->mc_ver = gen_ver++;
+            return;
+        }
         ModelConst& m = h->mc;
         std::memset(&m, 0, sizeof m);
         const double* q = blob;

@@ -1,0 +1,39 @@
+// Model kernels for any feature width / basis count (the reference supports
+// arbitrary ToyPotentialParams widths, potential.hpp:15-41).  The tuned
+// kernels (gmd_model.cu) are compiled for F = 16, K = 8 with the parameters
+// in constant memory; these read fp32 parameter tables from global memory,
+// one warp per node with lanes over features (F <= 128) and over basis
+// functions (K <= 32).  Same row-form, atomics-free formulation, so results
+// are partition-invariant; not tuned (the SURVEY configurations use F = 16).
+#pragma once
+#include "gmd_model.cuh"
+
+namespace gmd {
+
+constexpr int kGenMaxF = 128, kGenMaxK = 32;
+
+struct GenModel {
+    int F = 0, K = 0, L = 0;
+    const float* emb = nullptr;  // 119 x F
+    const float* W = nullptr;    // L x F x F (row f: W[f][g])
+    const float* b = nullptr;    // L x F
+    const float* P = nullptr;    // F x K
+    const float* Pk = nullptr;   // F x K: k P[f][k]
+    const float* ro = nullptr;   // F
+    float rc = 0, inv_rc = 0, inv_sigma = 0, mu_step = 0;
+};
+
+int gen_grid(int64_t n);  // CTAs of the warp-per-node kernels (8 warps each)
+void launch_gen_embed(const GenModel& g, int64_t rows, const int32_t* node_array, const int32_t* Z,
+                      float* H0, cudaStream_t s);
+// Hout[own] = Hin[own] + tanh(W_l m + b_l); TH_l; per-atom energies on the last layer
+void launch_gen_conv(const GenModel& g, const ConvArgs& a, int layer, const float* Hin, float* Hout,
+                     float* TH, double* per_atom, cudaStream_t s);
+void launch_gen_init_hbar(const GenModel& g, int64_t n, float* HB, cudaStream_t s);
+void launch_gen_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
+                         int layer, const float* HB, const float* TH, float* MB, cudaStream_t s);
+// vir_part: gen_grid(n) * 8 records of 6 doubles (one per warp)
+void launch_gen_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
+                         float* HB, float4* GRAD, double* vir_part, cudaStream_t s);
+
+}  // namespace gmd
