@@ -45,8 +45,12 @@ CONFIGS = {
     "c3": ("quartz 22^3 (95,832 atoms), rc 5 A, L=3, two-body", ("quartz", (22, 22, 22)), 5.0, 0.0, 3),
     "c4": ("liquid 100k atoms at 0.1 A^-3, rc 5 A, r3 3 A, L=3, three-body", ("liquid", 100000), 5.0, 3.0, 3),
     "c5": ("quartz 48^3 (995,328 atoms), rc 5 A, L=3, two-body", ("quartz", (48, 48, 48)), 5.0, 0.0, 3),
+    # C4 at the "CHGNet width" (width-generic kernels)
+    "c4w": ("liquid 100k atoms at 0.1 A^-3, rc 5 A, r3 3 A, L=3, three-body, F=64",
+            ("liquid", 100000), 5.0, 3.0, 3),
 }
 F, K = 16, 8
+CONFIG_F = {"c4w": 64}  # feature width per config (default F)
 PARAM_SEED = 12345
 
 
@@ -146,7 +150,7 @@ def peaks():
 REF_SAMPLE = ("quartz", (22, 22, 22))  # C3-size bounded sample of the quartz workload
 
 
-def reference_time(steps, warmup, cfg_r3, cfg_L, sample=REF_SAMPLE):
+def reference_time(steps, warmup, cfg_r3, cfg_L, sample=REF_SAMPLE, F=F):
     from oracle.oracle import Oracle
     from tests import systems as S
     R = Oracle("ref")
@@ -182,11 +186,12 @@ def main():
                     help="halo exchange for N>1: CUDA-IPC P2P stores (default) or NCCL send/recv")
     args = ap.parse_args()
     desc, spec, rc, r3, L = CONFIGS[args.config]
+    Fc = CONFIG_F.get(args.config, F)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     metric = "atoms/sec energy+force eval (1/2/4/8 B200) at 1M atoms; graph-build ms"
-    config = {"workload": f"{args.config}: {desc}", "model": "ToyPotential F=16 K=8",
+    config = {"workload": f"{args.config}: {desc}", "model": f"ToyPotential F={CONFIG_F.get(args.config, F)} K={K}",
               "layers": L, "partitions": max(world, args.gpus),
               "parallelism": ("1 GPU, one partition (no halo exchange)" if max(world, args.gpus) == 1
                               else f"slab-partitioned, {max(world, args.gpus)} rank(s), "
@@ -198,7 +203,7 @@ def main():
         if rank != 0:
             return
         K_, W_ = max(1, args.steps), max(0, args.warmup)
-        v, per, ns, cores, p = reference_time(K_, W_, r3, L)
+        v, per, ns, cores, p = reference_time(K_, W_, r3, L, F=Fc)
         line = {"impl": "reference", "metric": metric, "value": v, "unit": "atoms/s",
                 "n_gpus": args.gpus, "steps": K_, "warmup": W_, "ms_per_step": per * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -225,7 +230,7 @@ def main():
 
     s = make_system(spec)
     n = s.size()
-    prm = G.ToyPotentialParams.init(PARAM_SEED, F, K, L, rc, r3)
+    prm = G.ToyPotentialParams.init(PARAM_SEED, Fc, K, L, rc, r3)
     # one slab per GPU (p = world): every rank gets the replicated positions,
     # builds only its slab's rows and exchanges halo rows over NCCL each layer
     p = world
@@ -247,7 +252,7 @@ def main():
             G.init_rank_comm(h, rank, world)
     pbc = np.ones(3, np.uint8)
     lat = np.ascontiguousarray(s.lattice)
-    h.check(Lb.gmd_set_params(h.h, F, K, L, rc, r3, G._p(prm.blob)))
+    h.check(Lb.gmd_set_params(h.h, Fc, K, L, rc, r3, G._p(prm.blob)))
 
     # device-resident inputs and outputs
     pos_d = torch.from_numpy(s.positions).cuda()
@@ -371,7 +376,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, per, ns, cores, pp = reference_time(2, 1, r3, L)
+            v, per, ns, cores, pp = reference_time(2, 1, r3, L, F=Fc)
             cpu = {"value": v, "unit": "atoms/s", "cores": cores, "kind": "reference",
                    "sample": f"quartz 22^3 ({ns} atoms), p={pp} slabs, n_threads={cores}, "
                              f"mean of 2 evals after 1 warm-up, {per:.2f} s/eval"}

@@ -279,6 +279,7 @@ struct gmd_handle {
     bool generic = false;  // widths other than the tuned F = 16, K = 8 (gmd_generic.cu)
     GenModel gm{};
     DBuf gpar;             // fp32 parameter tables of the generic kernels
+    DBuf TT, SMR;          // generic three-body scratch rows (t per bond, m_bar_3 per slot)
     int F = 16, K = 8, L = 0;
     double p_r_atom = 0, p_r3 = 0;
     std::vector<DBuf> H;
@@ -1061,8 +1062,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     const bool part = h->p > 1;
     const bool gen = h->generic;  // widths other than F = 16, K = 8 (gmd_generic.cu)
     const int F = gen ? h->F : kF;
-    if (gen && tb)
-        raise(kConfig, "three-body parameters need feature_width=16, basis_count=8, <= 8 layers");
+
     {   // the __constant__ model copy is per device: upload only when another
         // parameter set was resident (saves a blocking pageable copy per step)
         static std::mutex mu;
@@ -1108,7 +1108,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                            : 1;
     double* e_part = h->e_part.get<double>(grid);
     double* v_part = h->v_part.get<double>((size_t)(L + nchunk - 1) * vgrid * 6);
-    const int tgrid = tb_grid_size(n);
+    const int tgrid = gen ? gen_grid(n) * 8 : tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
     double* pa = h->per_atom.get<double>(n_all);
@@ -1133,9 +1133,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     float *TP = nullptr, *TH3 = nullptr, *TH4 = nullptr;
     const int64_t nbr = h->nb + (rank_mode ? h->nb_halo : 0);  // bond rows incl. received
     if (tb) {
-        TP = h->TP.get<float>((size_t)nbr * kF);
-        TH3 = h->TH3.get<float>((size_t)nbr * kF);
-        TH4 = h->TH4.get<float>(n * kF);
+        TP = h->TP.get<float>((size_t)nbr * F);
+        TH3 = h->TH3.get<float>((size_t)nbr * F);
+        TH4 = h->TH4.get<float>(n * F);
     }
     const int32_t* xd = A.xdst.as<int32_t>();
     const int32_t* xs = A.xsrc.as<int32_t>();
@@ -1181,7 +1181,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     // reverse bonds computed at centers owned by peers
     const int64_t nbsend =
         rank_mode && tb ? std::accumulate(h->b_scnt.begin(), h->b_scnt.end(), (int64_t)0) : 0;
-    float* bsend = rank_mode && tb ? h->bsendbuf.get<float>(std::max<int64_t>(1, nbsend) * kF)
+    float* bsend = rank_mode && tb ? h->bsendbuf.get<float>(std::max<int64_t>(1, nbsend) * F)
                                    : nullptr;
     auto bond_exchange = [&](float* buf, int width) {
         if (!(rank_mode && tb)) return;
@@ -1217,9 +1217,22 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     for (int l = 0; l < L; ++l) {
         const bool tbl = tb && l == L - 1;
         if (tbl) {
-            { PROF("tb_forward"); launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), h->max_bonds, s); }
-            bond_exchange(TP, kF);
-            { PROF("tb_inject"); launch_tb_inject(ba, TP, H[l], TH4, s); }
+            if (gen) {
+                float* TT = h->TT.get<float>((size_t)std::max<int64_t>(1, nbr) * F);
+                { PROF("tb_t"); launch_gen_tb_t(h->gm, ba, nbr, TT, s); }
+                { PROF("tb_forward"); launch_gen_tb_forward(h->gm, ba, TT, TP, TH3, h->flags.as<int32_t>(), s); }
+            } else {
+                PROF("tb_forward");
+                launch_tb_forward(ba, TP, TH3, h->flags.as<int32_t>(), h->max_bonds, s);
+            }
+            bond_exchange(TP, F);
+            {
+                PROF("tb_inject");
+                if (gen)
+                    launch_gen_tb_inject(h->gm, ba, TP, H[l], TH4, s);
+                else
+                    launch_tb_inject(ba, TP, H[l], TH4, s);
+            }
         }
         if (l > 0 || tbl) exchange(H[l], true);
         PROF("conv");
@@ -1281,12 +1294,26 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             }
         }
         if (tb && l == L - 1) {
-            float* QB = h->QB.get<float>(R * kF);
+            float* QB = h->QB.get<float>(R * F);
             float4* VIN = h->VIN.get<float4>(nbr);
             float4* VOUT = h->VOUT.get<float4>(nbr);
-            { PROF("tb_bwd_q"); launch_tb_bwd_q(n, a.nodes, a.crow, HB, TH4, QB, s); }
+            {
+                PROF("tb_bwd_q");
+                if (gen)
+                    launch_gen_tb_bwd_q(h->gm, n, a.nodes, a.crow, HB, TH4, QB, s);
+                else
+                    launch_tb_bwd_q(n, a.nodes, a.crow, HB, TH4, QB, s);
+            }
             if (rank_mode) exchange(QB);  // q_bar of halo atoms (bond sources)
-            { PROF("tb_backward"); launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, h->max_bonds, s); }
+            {
+                PROF("tb_backward");
+                if (gen)
+                    launch_gen_tb_backward(h->gm, ba, QB, TH3, h->TT.as<float>(),
+                                           h->SMR.get<float>((size_t)std::max<int64_t>(1, nbr) * F),
+                                           VIN, VOUT, v3_part, s);
+                else
+                    launch_tb_backward(ba, QB, TH3, VIN, VOUT, v3_part, h->max_bonds, s);
+            }
             bond_exchange(reinterpret_cast<float*>(VIN), 4);
             bond_exchange(reinterpret_cast<float*>(VOUT), 4);
             { PROF("tb_grad"); launch_tb_grad(ba, VIN, VOUT, GRAD, s); }
@@ -1443,7 +1470,7 @@ void gmd_destroy(gmd_handle* h) {
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp,
                     &h->md_part, &h->md_out, &h->md_bad, &h->md_pos, &h->md_vel, &h->md_frc,
-                    &h->md_mass, &h->md_z, &h->gpar};
+                    &h->md_mass, &h->md_z, &h->gpar, &h->TT, &h->SMR};
     for (DBuf* b : bufs) b->release();
     for (LayoutState* ls : {&h->atoms, &h->bonds}) {
         DBuf* lb[] = {&ls->node_array, &ls->crow, &ls->list_off_d, &ls->xdst, &ls->xsrc,
@@ -1511,16 +1538,17 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         if (h->generic) {  // width-generic kernels: fp32 tables in global memory
             if (F > kGenMaxF || K > kGenMaxK)
                 raise(kConfig, "feature_width <= 128 and basis_count <= 32 are supported");
+            // device tables: emb | W | b | P | kP | P3 | W3 | W4 | ro (blob order:
+            // emb W b P P3 W3 W4 ro, potential.hpp:15-41)
             const size_t nemb = 119 * (size_t)F, nW = (size_t)L * F * F, nb = (size_t)L * F,
-                         nP = (size_t)F * K;
-            std::vector<float> t(nemb + nW + nb + 2 * nP + F);
+                         nP = (size_t)F * K, nFF = (size_t)F * F;
+            std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F);
             const double* q = blob;
             size_t o = 0;
             for (size_t i = 0; i < nemb + nW + nb + nP; ++i) t[o++] = (float)*q++;  // emb, W, b, P
             const double* Pd = blob + nemb + nW + nb;
             for (size_t i = 0; i < nP; ++i) t[o++] = (float)(Pd[i] * (double)(i % K));  // k P
-            q += nP + 2 * (size_t)F * F;  // P3, W3, W4 (three-body: tuned widths only)
-            for (int i = 0; i < F; ++i) t[o++] = (float)*q++;  // readout
+            for (size_t i = 0; i < nP + 2 * nFF + F; ++i) t[o++] = (float)*q++;  // P3 W3 W4 ro
             float* d = h->gpar.get<float>(t.size());
             GMD_CUDA(cudaMemcpy(d, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
             GenModel& g = h->gm;
@@ -1532,7 +1560,15 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
             g.b = g.W + nW;
             g.P = g.b + nb;
             g.Pk = g.P + nP;
-            g.ro = g.Pk + nP;
+            g.P3 = g.Pk + nP;
+            g.W3 = g.P3 + nP;
+            g.W4 = g.W3 + nFF;
+            g.ro = g.W4 + nFF;
+            const double r3e = r3 > 0.0 ? r3 : 1.0;
+            g.r3 = (float)r3e;
+            g.inv_r3 = (float)(1.0 / r3e);
+            g.inv_sigma3 = (float)(K / r3e);
+            g.mu_step3 = K > 1 ? (float)(r3e / (K - 1)) : 0.f;
             g.rc = (float)r_atom;
             g.inv_rc = (float)(1.0 / r_atom);
             g.inv_sigma = (float)(K / r_atom);  // sigma = rc / K (potential.cpp:34)

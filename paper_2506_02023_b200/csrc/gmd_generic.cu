@@ -229,6 +229,308 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
     }
 }
 
+// ---- three-body ----------------------------------------------------------
+// lane k (< K) holds the three-body basis value u3_k(d) (with fc3) or phi_k
+__device__ __forceinline__ void gen_fcut3(const GenModel& g, float d, float& fc, float& dfc) {
+    float sn, cs;
+    sincospif(d * g.inv_r3, &sn, &cs);
+    const bool in = d < g.r3;
+    fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
+    dfc = in ? -0.5f * 3.14159265358979f * g.inv_r3 * sn : 0.0f;
+}
+// t_f = sum_k P3[f][k] u3_k(d) into out[j] (features lane + 32 j)
+__device__ __forceinline__ void gen_bond_t(const GenModel& g, float d, int lane, float out[kNJ]) {
+    const int F = g.F, K = g.K, nj = (F + 31) / 32;
+    float fc, dfc;
+    gen_fcut3(g, d, fc, dfc);
+    float u = 0.f;
+    if (lane < K) {
+        const float x = (d - g.mu_step3 * (float)lane) * g.inv_sigma3;
+        u = fc * expf(-x * x);
+    }
+    for (int j = 0; j < kNJ; ++j) out[j] = 0.f;
+    for (int kk = 0; kk < K; ++kk) {
+        const float uk = __shfl_sync(kFull, u, kk);
+        for (int j = 0; j < nj; ++j) {
+            const int f = lane + 32 * j;
+            if (f < F) out[j] = fmaf(g.P3[f * K + kk], uk, out[j]);
+        }
+    }
+}
+// ds_f = sum_k P3[f][k] du3_k(d)
+__device__ __forceinline__ void gen_bond_dt(const GenModel& g, float d, int lane, float out[kNJ]) {
+    const int F = g.F, K = g.K, nj = (F + 31) / 32;
+    float fc, dfc;
+    gen_fcut3(g, d, fc, dfc);
+    float du = 0.f;
+    if (lane < K) {
+        const float x = (d - g.mu_step3 * (float)lane) * g.inv_sigma3;
+        du = expf(-x * x) * (dfc - 2.0f * fc * x * g.inv_sigma3);
+    }
+    for (int j = 0; j < kNJ; ++j) out[j] = 0.f;
+    for (int kk = 0; kk < K; ++kk) {
+        const float uk = __shfl_sync(kFull, du, kk);
+        for (int j = 0; j < nj; ++j) {
+            const int f = lane + 32 * j;
+            if (f < F) out[j] = fmaf(g.P3[f * K + kk], uk, out[j]);
+        }
+    }
+}
+
+// TT[b] = t of bond b for the bonds of every center
+__global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_t(GenModel g, BondArgs a,
+                                                             float* __restrict__ TT) {
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int F = g.F, nj = (F + 31) / 32;
+    for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
+         k += (int64_t)gridDim.x * kGenWarps) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
+        for (int b = a.brow[s]; b < a.brow[s + 1]; ++b) {
+            float t[kNJ];
+            gen_bond_t(g, a.vd[a.bedge[b]].w, lane, t);
+            for (int j = 0; j < nj; ++j) {
+                const int f = lane + 32 * j;
+                if (f < F) TT[(size_t)b * F + f] = t[j];
+            }
+        }
+    }
+}
+
+// per center s, slot j: m3 = sum_{o != j} c(o, j) t_o (ascending o),
+// t' = t_j + fc3(d_j) tanh(W3 m3) -> TP / TH3 slot j
+__global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_forward(GenModel g, BondArgs a,
+                                                                   const float* __restrict__ TT,
+                                                                   float* __restrict__ TP,
+                                                                   float* __restrict__ TH3) {
+    __shared__ float sm[kGenWarps][kGenMaxF];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int F = g.F, nj = (F + 31) / 32;
+    for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
+         k += (int64_t)gridDim.x * kGenWarps) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int b0 = a.brow[s], nbd = a.brow[s + 1] - b0;
+        for (int j = 0; j < nbd; ++j) {
+            const float4 qj = a.vd[a.bedge[b0 + j]];
+            float m3[kNJ] = {0.f, 0.f, 0.f, 0.f};
+            for (int o = 0; o < nbd; ++o) {
+                if (o == j) continue;  // the reverse pair (linegraph.cpp:16-21)
+                const float4 q2 = a.vd[a.bedge[b0 + o]];
+                const float c = (q2.x * qj.x + q2.y * qj.y + q2.z * qj.z) / (q2.w * qj.w);
+                for (int jj = 0; jj < nj; ++jj) {
+                    const int f = lane + 32 * jj;
+                    if (f < F) m3[jj] = fmaf(c, TT[(size_t)(b0 + o) * F + f], m3[jj]);
+                }
+            }
+            for (int jj = 0; jj < nj; ++jj) {
+                const int f = lane + 32 * jj;
+                if (f < F) sm[wq][f] = m3[jj];
+            }
+            __syncwarp();
+            float fc, dfc;
+            gen_fcut3(g, qj.w, fc, dfc);
+            for (int jj = 0; jj < nj; ++jj) {
+                const int f = lane + 32 * jj;
+                if (f < F) {
+                    float z = 0.f;
+                    for (int q = 0; q < F; ++q) z = fmaf(g.W3[(size_t)f * F + q], sm[wq][q], z);
+                    const float th = tanhf(z);
+                    TP[(size_t)(b0 + j) * F + f] = TT[(size_t)(b0 + j) * F + f] + fc * th;
+                    TH3[(size_t)(b0 + j) * F + f] = th;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// q_u = sum_{b into u} t'_rev(b) (ascending b), h_u += tanh(W4 q_u)
+__global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_inject(GenModel g, BondArgs a,
+                                                                  const float* __restrict__ TP,
+                                                                  float* __restrict__ H,
+                                                                  float* __restrict__ TH4) {
+    __shared__ float sq[kGenWarps][kGenMaxF];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int F = g.F, nj = (F + 31) / 32;
+    for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
+         k += (int64_t)gridDim.x * kGenWarps) {
+        const int64_t u = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int64_t r = a.crow ? (int64_t)a.crow[u] : u;
+        float q[kNJ] = {0.f, 0.f, 0.f, 0.f};
+        for (int b = a.brow[u]; b < a.brow[u + 1]; ++b) {
+            const int rb = a.brev[b];
+            for (int jj = 0; jj < nj; ++jj) {
+                const int f = lane + 32 * jj;
+                if (f < F) q[jj] += TP[(size_t)rb * F + f];
+            }
+        }
+        for (int jj = 0; jj < nj; ++jj) {
+            const int f = lane + 32 * jj;
+            if (f < F) sq[wq][f] = q[jj];
+        }
+        __syncwarp();
+        for (int jj = 0; jj < nj; ++jj) {
+            const int f = lane + 32 * jj;
+            if (f < F) {
+                float z = 0.f;
+                for (int q2 = 0; q2 < F; ++q2) z = fmaf(g.W4[(size_t)f * F + q2], sq[wq][q2], z);
+                const float th = tanhf(z);
+                H[(size_t)r * F + f] += th;
+                TH4[(size_t)k * F + f] = th;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// QB[row(v)] = W4^T (HB * (1 - TH4^2))
+__global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_bwd_q(GenModel g, int64_t n,
+                                                                 const int32_t* __restrict__ nodes,
+                                                                 const int32_t* __restrict__ crow,
+                                                                 const float* __restrict__ HB,
+                                                                 const float* __restrict__ TH4,
+                                                                 float* __restrict__ QB) {
+    __shared__ float sy[kGenWarps][kGenMaxF];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int F = g.F, nj = (F + 31) / 32;
+    for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < n;
+         k += (int64_t)gridDim.x * kGenWarps) {
+        const int64_t v = nodes ? (int64_t)nodes[k] : k;
+        const int64_t r = crow ? (int64_t)crow[v] : v;
+        for (int jj = 0; jj < nj; ++jj) {
+            const int f = lane + 32 * jj;
+            if (f < F) {
+                const float th = TH4[(size_t)k * F + f];
+                sy[wq][f] = HB[(size_t)k * F + f] * (1.0f - th * th);
+            }
+        }
+        __syncwarp();
+        for (int jj = 0; jj < nj; ++jj) {
+            const int q = lane + 32 * jj;
+            if (q < F) {
+                float acc = 0.f;
+                for (int f = 0; f < F; ++f) acc = fmaf(g.W4[(size_t)f * F + q], sy[wq][f], acc);
+                QB[(size_t)r * F + q] = acc;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// per center s (the tuned k_tb_backward's adjoint, lanes over features):
+// phase 1 per slot j: adjoints of t'(e'_j) -> m_bar_3 (SMR), VOUT (fc3 and
+// bond-init paths); phase 2: line-edge cosine gradients -> VIN / VOUT
+__global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_backward(
+    GenModel g, BondArgs a, const float* __restrict__ QB, const float* __restrict__ TH3,
+    const float* __restrict__ TT, float* __restrict__ SMR, float4* __restrict__ VIN,
+    float4* __restrict__ VOUT, double* __restrict__ vir_part) {
+    __shared__ float sy[kGenWarps][kGenMaxF];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int F = g.F, nj = (F + 31) / 32;
+    double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
+         k += (int64_t)gridDim.x * kGenWarps) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int b0 = a.brow[s], nbd = a.brow[s + 1] - b0;
+        for (int j = 0; j < nbd; ++j) {  // phase 1
+            const int e = a.bedge[b0 + j];
+            const float4 q = a.vd[e];
+            const int x = a.esrc[e];
+            const int64_t rx = a.crow ? (int64_t)a.crow[x] : x;
+            float fc, dfc, ds[kNJ];
+            gen_fcut3(g, q.w, fc, dfc);
+            gen_bond_dt(g, q.w, lane, ds);
+            float dbf = 0.f, da = 0.f;
+            for (int jj = 0; jj < nj; ++jj) {
+                const int f = lane + 32 * jj;
+                if (f < F) {
+                    const float tpb = QB[(size_t)rx * F + f];
+                    const float th = TH3[(size_t)(b0 + j) * F + f];
+                    dbf = fmaf(tpb * th, dfc, dbf);
+                    da = fmaf(tpb, ds[jj], da);
+                    sy[wq][f] = tpb * fc * (1.0f - th * th);
+                }
+            }
+            dbf = gwarp_sum(dbf);
+            da = gwarp_sum(da);
+            __syncwarp();
+            for (int jj = 0; jj < nj; ++jj) {
+                const int q2 = lane + 32 * jj;
+                if (q2 < F) {
+                    float acc = 0.f;
+                    for (int f = 0; f < F; ++f) acc = fmaf(g.W3[(size_t)f * F + q2], sy[wq][f], acc);
+                    SMR[(size_t)(b0 + j) * F + q2] = acc;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const float c0 = -(dbf + da) / q.w;
+                VOUT[b0 + j] = make_float4(q.x * c0, q.y * c0, q.z * c0, 0.f);
+            }
+        }
+        __syncwarp();
+        for (int j = 0; j < nbd; ++j) {  // phase 2
+            const float4 qj = a.vd[a.bedge[b0 + j]];
+            const float idj = 1.0f / qj.w;
+            float tb[kNJ] = {0.f, 0.f, 0.f, 0.f};
+            float vix = 0.f, viy = 0.f, viz = 0.f;
+            float4 vo = VOUT[b0 + j];
+            for (int o = 0; o < nbd; ++o) {
+                if (o == j) continue;
+                const float4 qo = a.vd[a.bedge[b0 + o]];
+                const float ido = 1.0f / qo.w;
+                const float c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
+                float cb = 0.f, cb2 = 0.f;
+                for (int jj = 0; jj < nj; ++jj) {
+                    const int f = lane + 32 * jj;
+                    if (f < F) {
+                        const float smo = SMR[(size_t)(b0 + o) * F + f];
+                        tb[jj] = fmaf(c, smo, tb[jj]);
+                        cb = fmaf(smo, TT[(size_t)(b0 + j) * F + f], cb);
+                        cb2 = fmaf(SMR[(size_t)(b0 + j) * F + f], TT[(size_t)(b0 + o) * F + f], cb2);
+                    }
+                }
+                cb = gwarp_sum(cb);
+                cb2 = gwarp_sum(cb2);
+                // (a) line edge (e_j, e'_o): dc/da = -(b^ + a^ c)/|a|, a = v_j, b = -v_o
+                vix += -(-qo.x * ido + qj.x * idj * c) * idj * cb;
+                viy += -(-qo.y * ido + qj.y * idj * c) * idj * cb;
+                viz += -(-qo.z * ido + qj.z * idj * c) * idj * cb;
+                // (b) line edge (e_o, e'_j): dc/db = -(a^ + b^ c)/|b|, a = v_o, b = -v_j
+                vo.x += -(qo.x * ido - qj.x * idj * c) * idj * cb2;
+                vo.y += -(qo.y * ido - qj.y * idj * c) * idj * cb2;
+                vo.z += -(qo.z * ido - qj.z * idj * c) * idj * cb2;
+            }
+            float dsj[kNJ];
+            gen_bond_dt(g, qj.w, lane, dsj);
+            float db = 0.f;
+            for (int jj = 0; jj < nj; ++jj) db = fmaf(tb[jj], dsj[jj], db);
+            db = gwarp_sum(db);
+            vix += qj.x * db * idj;
+            viy += qj.y * db * idj;
+            viz += qj.z * db * idj;
+            if (lane == 0) {
+                VIN[b0 + j] = make_float4(vix, viy, viz, 0.f);
+                VOUT[b0 + j] = vo;
+                const double dx = (double)vix - vo.x, dy = (double)viy - vo.y, dz = (double)viz - vo.z;
+                vir[0] += dx * qj.x;
+                vir[1] += dx * qj.y;
+                vir[2] += dx * qj.z;
+                vir[3] += dy * qj.x;
+                vir[4] += dy * qj.y;
+                vir[5] += dy * qj.z;
+                vir[6] += dz * qj.x;
+                vir[7] += dz * qj.y;
+                vir[8] += dz * qj.z;
+            }
+        }
+    }
+    if (lane == 0) {
+        const int64_t rec = (int64_t)blockIdx.x * kGenWarps + wq;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) vir_part[rec * 9 + c] = vir[c];
+    }
+}
+
 }  // namespace
 
 int gen_grid(int64_t n) {
@@ -268,6 +570,46 @@ void launch_gen_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, 
                          float* HB, float4* GRAD, double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
     k_gen_bwd_edge<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, MB, Hl, HB, GRAD, vir_part);
+    GMD_LAUNCH_CHECK();
+}
+
+}  // namespace gmd
+
+namespace gmd {
+
+void launch_gen_tb_t(const GenModel& g, const BondArgs& a, int64_t, float* TT, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_gen_tb_t<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, TT);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_gen_tb_forward(const GenModel& g, const BondArgs& a, const float* TT, float* TP,
+                           float* TH3, int32_t*, cudaStream_t s) {
+    if (a.n == 0) return;
+    k_gen_tb_forward<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, TT, TP, TH3);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_gen_tb_inject(const GenModel& g, const BondArgs& a, const float* TP, float* H, float* TH4,
+                          cudaStream_t s) {
+    if (a.n == 0) return;
+    k_gen_tb_inject<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, TP, H, TH4);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_gen_tb_bwd_q(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
+                         const float* HB, const float* TH4, float* QB, cudaStream_t s) {
+    if (n == 0) return;
+    k_gen_tb_bwd_q<<<gen_grid(n), kGenWarps * 32, 0, s>>>(g, n, nodes, crow, HB, TH4, QB);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_gen_tb_backward(const GenModel& g, const BondArgs& a, const float* QB, const float* TH3,
+                            const float* TT, float* SMR, float4* VIN, float4* VOUT, double* vir_part,
+                            cudaStream_t s) {
+    if (a.n == 0) return;
+    k_gen_tb_backward<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, QB, TH3, TT, SMR, VIN, VOUT,
+                                                               vir_part);
     GMD_LAUNCH_CHECK();
 }
 

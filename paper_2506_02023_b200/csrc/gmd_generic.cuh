@@ -20,7 +20,11 @@ struct GenModel {
     const float* P = nullptr;    // F x K
     const float* Pk = nullptr;   // F x K: k P[f][k]
     const float* ro = nullptr;   // F
+    const float* P3 = nullptr;   // F x K   (three-body)
+    const float* W3 = nullptr;   // F x F
+    const float* W4 = nullptr;   // F x F
     float rc = 0, inv_rc = 0, inv_sigma = 0, mu_step = 0;
+    float r3 = 1, inv_r3 = 1, inv_sigma3 = 0, mu_step3 = 0;
 };
 
 int gen_grid(int64_t n);  // CTAs of the warp-per-node kernels (8 warps each)
@@ -35,5 +39,20 @@ void launch_gen_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, con
 // vir_part: gen_grid(n) * 8 records of 6 doubles (one per warp)
 void launch_gen_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
                          float* HB, float4* GRAD, double* vir_part, cudaStream_t s);
+
+// three-body stage (potential.cpp:664-741, 850-961), same slot conventions
+// as the tuned kernels (TP/TH3 slot j of a center = the reverse bond of its
+// in-bond j); TT / SMR: B x F scratch rows (t of every bond, m_bar_3 per slot)
+void launch_gen_tb_t(const GenModel& g, const BondArgs& a, int64_t nbonds, float* TT, cudaStream_t s);
+void launch_gen_tb_forward(const GenModel& g, const BondArgs& a, const float* TT, float* TP,
+                           float* TH3, int32_t* flags, cudaStream_t s);
+void launch_gen_tb_inject(const GenModel& g, const BondArgs& a, const float* TP, float* H, float* TH4,
+                          cudaStream_t s);
+void launch_gen_tb_bwd_q(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
+                         const float* HB, const float* TH4, float* QB, cudaStream_t s);
+// vir_part: gen_grid(a.n) * 8 records of 9 doubles
+void launch_gen_tb_backward(const GenModel& g, const BondArgs& a, const float* QB, const float* TH3,
+                            const float* TT, float* SMR, float4* VIN, float4* VOUT, double* vir_part,
+                            cudaStream_t s);
 
 }  // namespace gmd
