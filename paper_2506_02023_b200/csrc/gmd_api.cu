@@ -1542,13 +1542,28 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
             // emb W b P P3 W3 W4 ro, potential.hpp:15-41)
             const size_t nemb = 119 * (size_t)F, nW = (size_t)L * F * F, nb = (size_t)L * F,
                          nP = (size_t)F * K, nFF = (size_t)F * F;
-            std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F);
+            std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F + nW + 2 * nFF);
             const double* q = blob;
             size_t o = 0;
             for (size_t i = 0; i < nemb + nW + nb + nP; ++i) t[o++] = (float)*q++;  // emb, W, b, P
             const double* Pd = blob + nemb + nW + nb;
             for (size_t i = 0; i < nP; ++i) t[o++] = (float)(Pd[i] * (double)(i % K));  // k P
             for (size_t i = 0; i < nP + 2 * nFF + F; ++i) t[o++] = (float)*q++;  // P3 W3 W4 ro
+            // transposed W (per layer), W3, W4
+            const float* Wf = t.data() + nemb;
+            const float* W3f = t.data() + nemb + nW + nb + 2 * nP + nP;
+            const float* W4f = W3f + nFF;
+            for (int l = 0; l < L; ++l)
+                for (int f = 0; f < F; ++f)
+                    for (int gg = 0; gg < F; ++gg)
+                        t[o + (size_t)l * nFF + (size_t)gg * F + f] = Wf[(size_t)l * nFF + (size_t)f * F + gg];
+            o += nW;
+            for (int f = 0; f < F; ++f)
+                for (int gg = 0; gg < F; ++gg) {
+                    t[o + (size_t)gg * F + f] = W3f[(size_t)f * F + gg];
+                    t[o + nFF + (size_t)gg * F + f] = W4f[(size_t)f * F + gg];
+                }
+            o += 2 * nFF;
             float* d = h->gpar.get<float>(t.size());
             GMD_CUDA(cudaMemcpy(d, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
             GenModel& g = h->gm;
@@ -1564,6 +1579,9 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
             g.W3 = g.P3 + nP;
             g.W4 = g.W3 + nFF;
             g.ro = g.W4 + nFF;
+            g.WT = g.ro + F;
+            g.W3T = g.WT + nW;
+            g.W4T = g.W3T + nFF;
             const double r3e = r3 > 0.0 ? r3 : 1.0;
             g.r3 = (float)r3e;
             g.inv_r3 = (float)(1.0 / r3e);

@@ -13,6 +13,7 @@ namespace {
 constexpr int kGenWarps = 8;              // warps per CTA, one node per warp
 constexpr int kNJ = kGenMaxF / 32;        // feature slots per lane
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kTbCache = 64;  // bond vectors of a center cached per warp
 
 __device__ __forceinline__ float gwarp_sum(float v) {
 #pragma unroll
@@ -35,54 +36,69 @@ __global__ void k_gen_init_hbar(GenModel g, int64_t n, float* __restrict__ HB) {
     if (t < n * g.F) HB[t] = g.ro[t % g.F];
 }
 
+// Edges in chunks of 32: lane i evaluates edge i's radial basis into shared
+// memory, then the warp (lanes over features) consumes the chunk with
+// independent row loads.  Dynamic shared memory: P (F x K) + per-warp
+// basis rows [32][K + 1] + the m staging row.
 __global__ void __launch_bounds__(kGenWarps * 32) k_gen_conv(GenModel g, ConvArgs a, int layer,
                                                              const float* __restrict__ Hin,
                                                              float* __restrict__ Hout,
                                                              float* __restrict__ TH,
                                                              double* __restrict__ per_atom) {
-    __shared__ float sm[kGenWarps][kGenMaxF];
+    extern __shared__ float gsm[];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    const int F = g.F, K = g.K, nj = (F + 31) / 32;
-    const float* W = g.W + (size_t)layer * F * F;
+    const int F = g.F, K = g.K, nj = (F + 31) / 32, K1 = K + 1;
+    float* sP = gsm;                                         // F x K
+    float* su = sP + F * K + (size_t)wq * (32 * K1 + 32 + kGenMaxF);  // [32][K1]
+    int* sw = reinterpret_cast<int*>(su + 32 * K1);          // [32]
+    float* sm = su + 32 * K1 + 32;                           // [kGenMaxF]
+    for (int t = threadIdx.x; t < F * K; t += blockDim.x) sP[(t % K) * F + t / K] = g.P[t];  // [k][f]
+    __syncthreads();
+    const float* WT = g.WT + (size_t)layer * F * F;
     const float* bl = g.b + (size_t)layer * F;
     for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
          k += (int64_t)gridDim.x * kGenWarps) {
         const int64_t v = a.nodes ? (int64_t)a.nodes[k] : k;
         const int64_t r = a.crow ? (int64_t)a.crow[v] : v;
+        const int e0 = a.row[v], e1 = a.row[v + 1];
         float m[kNJ] = {0.f, 0.f, 0.f, 0.f};
-        for (int e = a.row[v]; e < a.row[v + 1]; ++e) {
-            const float d = a.d[e];
-            const int w = a.lsrc[e];
-            const float fc = d < g.rc ? 0.5f * (cospif(d * g.inv_rc) + 1.0f) : 0.0f;
-            float u = 0.f;
-            if (lane < K) {
-                const float x = (d - g.mu_step * (float)lane) * g.inv_sigma;
-                u = fc * expf(-x * x);
-            }
-            float s[kNJ] = {0.f, 0.f, 0.f, 0.f};
-            for (int kk = 0; kk < K; ++kk) {
-                const float uk = __shfl_sync(kFull, u, kk);
-                for (int j = 0; j < nj; ++j) {
-                    const int f = lane + 32 * j;
-                    if (f < F) s[j] = fmaf(g.P[f * K + kk], uk, s[j]);
+        for (int eb = e0; eb < e1; eb += 32) {
+            const int ne = min(32, e1 - eb);
+            if (lane < ne) {
+                const float d = a.d[eb + lane];
+                sw[lane] = a.lsrc[eb + lane];
+                const float fc = d < g.rc ? 0.5f * (cospif(d * g.inv_rc) + 1.0f) : 0.0f;
+                for (int kk = 0; kk < K; ++kk) {
+                    const float x = (d - g.mu_step * (float)kk) * g.inv_sigma;
+                    su[lane * K1 + kk] = fc * expf(-x * x);
                 }
             }
-            for (int j = 0; j < nj; ++j) {
-                const int f = lane + 32 * j;
-                if (f < F) m[j] = fmaf(Hin[(size_t)w * F + f], s[j], m[j]);
+            __syncwarp();
+            for (int i = 0; i < ne; ++i) {
+                const int w = sw[i];
+                const float* ui = su + i * K1;
+                for (int jj = 0; jj < nj; ++jj) {
+                    const int f = lane + 32 * jj;
+                    if (f < F) {
+                        float s2 = 0.f;
+                        for (int kk = 0; kk < K; ++kk) s2 = fmaf(sP[kk * F + f], ui[kk], s2);
+                        m[jj] = fmaf(Hin[(size_t)w * F + f], s2, m[jj]);
+                    }
+                }
             }
+            __syncwarp();
         }
-        for (int j = 0; j < nj; ++j) {
-            const int f = lane + 32 * j;
-            if (f < F) sm[wq][f] = m[j];
+        for (int jj = 0; jj < nj; ++jj) {
+            const int f = lane + 32 * jj;
+            if (f < F) sm[f] = m[jj];
         }
         __syncwarp();
         float ev = 0.f;
-        for (int j = 0; j < nj; ++j) {
-            const int f = lane + 32 * j;
+        for (int jj = 0; jj < nj; ++jj) {
+            const int f = lane + 32 * jj;
             if (f < F) {
                 float z = bl[f];
-                for (int q = 0; q < F; ++q) z = fmaf(W[(size_t)f * F + q], sm[wq][q], z);
+                for (int q = 0; q < F; ++q) z = fmaf(WT[(size_t)q * F + f], sm[q], z);
                 const float th = tanhf(z);
                 const float hn = Hin[(size_t)r * F + f] + th;
                 Hout[(size_t)r * F + f] = hn;
@@ -133,85 +149,122 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_node(GenModel g, int
     }
 }
 
+// Edges in chunks of 32 as in k_gen_conv: lane i evaluates edge i's basis
+// terms (phi_k, fc, ca, cb) into shared memory; lanes over features then
+// accumulate h_bar and each edge's (dself, drev) partials, which lane i sums
+// for its edge (fixed order) before the gradient and virial terms.
 __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, ConvArgs a,
                                                                  const float* __restrict__ MB,
                                                                  const float* __restrict__ Hl,
                                                                  float* __restrict__ HB,
                                                                  float4* __restrict__ GRAD,
                                                                  double* __restrict__ vir_part) {
+    extern __shared__ float gsm[];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    const int F = g.F, K = g.K, nj = (F + 31) / 32;
+    const int F = g.F, K = g.K, nj = (F + 31) / 32, K1 = K + 1;
+    float* sP = gsm;             // F x K
+    float* sPk = sP + F * K;     // F x K
+    float* base = sPk + F * K + (size_t)wq * (32 * (K1 + 4) + 2 * 32 * 33);
+    float* sph = base;                         // [32][K1] phi
+    float* scf = sph + 32 * K1;                // [32][4]: fc, ca, cb, src (as int)
+    float* pself = scf + 32 * 4;               // [32 edges][33]
+    float* prev = pself + 32 * 33;             // [32 edges][33]
+    for (int t = threadIdx.x; t < F * K; t += blockDim.x) {  // [k][f]
+        sP[(t % K) * F + t / K] = g.P[t];
+        sPk[(t % K) * F + t / K] = g.Pk[t];
+    }
+    __syncthreads();
     const float isg = g.inv_sigma, mus = g.mu_step;
     double wvir[6] = {0, 0, 0, 0, 0, 0};
     for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
          k += (int64_t)gridDim.x * kGenWarps) {
         const int64_t v = a.nodes ? (int64_t)a.nodes[k] : k;
         const int64_t ru = a.crow ? (int64_t)a.crow[v] : v;
+        const int e0 = a.row[v], e1 = a.row[v + 1];
         float mu[kNJ], hu[kNJ], hb[kNJ] = {0.f, 0.f, 0.f, 0.f};
-        for (int j = 0; j < kNJ; ++j) {
-            const int f = lane + 32 * j;
-            mu[j] = j < nj && f < F ? MB[(size_t)ru * F + f] : 0.f;
-            hu[j] = j < nj && f < F ? Hl[(size_t)ru * F + f] : 0.f;
+        for (int jj = 0; jj < kNJ; ++jj) {
+            const int f = lane + 32 * jj;
+            mu[jj] = jj < nj && f < F ? MB[(size_t)ru * F + f] : 0.f;
+            hu[jj] = jj < nj && f < F ? Hl[(size_t)ru * F + f] : 0.f;
         }
         float gx = 0.f, gy = 0.f, gz = 0.f;
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int e = a.row[v]; e < a.row[v + 1]; ++e) {
-            const float4 q = a.vd[e];
-            const int w = a.lsrc[e];
-            const float d = q.w;
-            float sn, cs;
-            sincospif(d * g.inv_rc, &sn, &cs);
-            const bool in = d < g.rc;
-            const float fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
-            const float dfc = in ? -0.5f * 3.14159265358979f * g.inv_rc * sn : 0.0f;
-            float ph = 0.f;
-            if (lane < K) {
-                const float x = (d - mus * (float)lane) * isg;
-                ph = expf(-x * x);
+        for (int eb = e0; eb < e1; eb += 32) {
+            const int ne = min(32, e1 - eb);
+            float4 qi = make_float4(0.f, 0.f, 0.f, 1.f);
+            if (lane < ne) {
+                qi = a.vd[eb + lane];
+                const float d = qi.w;
+                float sn, cs;
+                sincospif(d * g.inv_rc, &sn, &cs);
+                const bool in = d < g.rc;
+                const float fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
+                const float dfc = in ? -0.5f * 3.14159265358979f * g.inv_rc * sn : 0.0f;
+                const float x0 = d * isg, step = mus * isg;
+                scf[lane * 4 + 0] = fc;
+                scf[lane * 4 + 1] = dfc - 2.0f * fc * isg * x0;
+                scf[lane * 4 + 2] = 2.0f * fc * isg * step;
+                scf[lane * 4 + 3] = __int_as_float(a.lsrc[eb + lane]);
+                for (int kk = 0; kk < K; ++kk) {
+                    const float x = (d - mus * (float)kk) * isg;
+                    sph[lane * K1 + kk] = expf(-x * x);
+                }
             }
-            const float x0 = d * isg, step = mus * isg;
-            const float ca = dfc - 2.0f * fc * isg * x0, cb = 2.0f * fc * isg * step;
-            float A[kNJ] = {0.f, 0.f, 0.f, 0.f}, B[kNJ] = {0.f, 0.f, 0.f, 0.f};
-            for (int kk = 0; kk < K; ++kk) {
-                const float pk = __shfl_sync(kFull, ph, kk);
-                for (int j = 0; j < nj; ++j) {
-                    const int f = lane + 32 * j;
+            __syncwarp();
+            for (int i = 0; i < ne; ++i) {
+                const float fc = scf[i * 4], ca = scf[i * 4 + 1], cb = scf[i * 4 + 2];
+                const int w = __float_as_int(scf[i * 4 + 3]);
+                const float* ph = sph + i * K1;
+                float ds_self = 0.f, ds_rev = 0.f;
+                for (int jj = 0; jj < nj; ++jj) {
+                    const int f = lane + 32 * jj;
                     if (f < F) {
-                        A[j] = fmaf(g.P[f * K + kk], pk, A[j]);
-                        B[j] = fmaf(g.Pk[f * K + kk], pk, B[j]);
+                        float A = 0.f, B = 0.f;
+                        for (int kk = 0; kk < K; ++kk) {
+                            A = fmaf(sP[kk * F + f], ph[kk], A);
+                            B = fmaf(sPk[kk * F + f], ph[kk], B);
+                        }
+                        const float mw = MB[(size_t)w * F + f], hw = Hl[(size_t)w * F + f];
+                        const float ds = fmaf(ca, A, cb * B);
+                        hb[jj] = fmaf(mw, fc * A, hb[jj]);
+                        ds_self = fmaf(mu[jj] * hw, ds, ds_self);
+                        ds_rev = fmaf(mw * hu[jj], ds, ds_rev);
                     }
                 }
+                pself[i * 33 + lane] = ds_self;
+                prev[i * 33 + lane] = ds_rev;
             }
-            float dself = 0.f, drev = 0.f;
-            for (int j = 0; j < nj; ++j) {
-                const int f = lane + 32 * j;
-                if (f < F) {
-                    const float mw = MB[(size_t)w * F + f], hw = Hl[(size_t)w * F + f];
-                    const float ds = fmaf(ca, A[j], cb * B[j]);
-                    hb[j] = fmaf(mw, fc * A[j], hb[j]);
-                    dself = fmaf(mu[j] * hw, ds, dself);
-                    drev = fmaf(mw * hu[j], ds, drev);
+            __syncwarp();
+            if (lane < ne) {  // edge `lane`: its partials over the 32 feature lanes, in order
+                float dself = 0.f, drev = 0.f;
+                for (int l = 0; l < 32; ++l) {
+                    dself += pself[lane * 33 + l];
+                    drev += prev[lane * 33 + l];
                 }
+                const float invd = 1.0f / qi.w;
+                const float coef = (dself + drev) * invd;
+                gx -= qi.x * coef;
+                gy -= qi.y * coef;
+                gz -= qi.z * coef;
+                const float cself = dself * invd;
+                vr[0] = fmaf(cself * qi.x, qi.x, vr[0]);
+                vr[1] = fmaf(cself * qi.y, qi.y, vr[1]);
+                vr[2] = fmaf(cself * qi.z, qi.z, vr[2]);
+                vr[3] = fmaf(cself * qi.x, qi.y, vr[3]);
+                vr[4] = fmaf(cself * qi.x, qi.z, vr[4]);
+                vr[5] = fmaf(cself * qi.y, qi.z, vr[5]);
             }
-            dself = gwarp_sum(dself);
-            drev = gwarp_sum(drev);
-            const float invd = 1.0f / d;
-            const float coef = (dself + drev) * invd;
-            gx -= q.x * coef;
-            gy -= q.y * coef;
-            gz -= q.z * coef;
-            const float cself = dself * invd;
-            vr[0] = fmaf(cself * q.x, q.x, vr[0]);
-            vr[1] = fmaf(cself * q.y, q.y, vr[1]);
-            vr[2] = fmaf(cself * q.z, q.z, vr[2]);
-            vr[3] = fmaf(cself * q.x, q.y, vr[3]);
-            vr[4] = fmaf(cself * q.x, q.z, vr[4]);
-            vr[5] = fmaf(cself * q.y, q.z, vr[5]);
+            __syncwarp();
         }
-        for (int j = 0; j < nj; ++j) {  // one writer per element
-            const int f = lane + 32 * j;
-            if (f < F) HB[(size_t)k * F + f] += hb[j];
+        for (int jj = 0; jj < nj; ++jj) {  // one writer per element
+            const int f = lane + 32 * jj;
+            if (f < F) HB[(size_t)k * F + f] += hb[jj];
         }
+        gx = gwarp_sum(gx);
+        gy = gwarp_sum(gy);
+        gz = gwarp_sum(gz);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
         if (lane == 0) {
             float4 gr = GRAD[k];
             gr.x += gx;
@@ -303,18 +356,22 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_forward(GenModel g, B
                                                                    float* __restrict__ TP,
                                                                    float* __restrict__ TH3) {
     __shared__ float sm[kGenWarps][kGenMaxF];
+    __shared__ float4 sq[kGenWarps][kTbCache];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int F = g.F, nj = (F + 31) / 32;
     for (int64_t k = (int64_t)blockIdx.x * kGenWarps + wq; k < a.n;
          k += (int64_t)gridDim.x * kGenWarps) {
         const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
         const int b0 = a.brow[s], nbd = a.brow[s + 1] - b0;
+        for (int o = lane; o < nbd && o < kTbCache; o += 32) sq[wq][o] = a.vd[a.bedge[b0 + o]];
+        __syncwarp();
+        auto qof = [&](int o) { return o < kTbCache ? sq[wq][o] : a.vd[a.bedge[b0 + o]]; };
         for (int j = 0; j < nbd; ++j) {
-            const float4 qj = a.vd[a.bedge[b0 + j]];
+            const float4 qj = qof(j);
             float m3[kNJ] = {0.f, 0.f, 0.f, 0.f};
             for (int o = 0; o < nbd; ++o) {
                 if (o == j) continue;  // the reverse pair (linegraph.cpp:16-21)
-                const float4 q2 = a.vd[a.bedge[b0 + o]];
+                const float4 q2 = qof(o);
                 const float c = (q2.x * qj.x + q2.y * qj.y + q2.z * qj.z) / (q2.w * qj.w);
                 for (int jj = 0; jj < nj; ++jj) {
                     const int f = lane + 32 * jj;
@@ -332,7 +389,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_forward(GenModel g, B
                 const int f = lane + 32 * jj;
                 if (f < F) {
                     float z = 0.f;
-                    for (int q = 0; q < F; ++q) z = fmaf(g.W3[(size_t)f * F + q], sm[wq][q], z);
+                    for (int q = 0; q < F; ++q) z = fmaf(g.W3T[(size_t)q * F + f], sm[wq][q], z);
                     const float th = tanhf(z);
                     TP[(size_t)(b0 + j) * F + f] = TT[(size_t)(b0 + j) * F + f] + fc * th;
                     TH3[(size_t)(b0 + j) * F + f] = th;
@@ -340,6 +397,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_forward(GenModel g, B
             }
             __syncwarp();
         }
+        __syncwarp();
     }
 }
 
@@ -372,7 +430,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_inject(GenModel g, Bo
             const int f = lane + 32 * jj;
             if (f < F) {
                 float z = 0.f;
-                for (int q2 = 0; q2 < F; ++q2) z = fmaf(g.W4[(size_t)f * F + q2], sq[wq][q2], z);
+                for (int q2 = 0; q2 < F; ++q2) z = fmaf(g.W4T[(size_t)q2 * F + f], sq[wq][q2], z);
                 const float th = tanhf(z);
                 H[(size_t)r * F + f] += th;
                 TH4[(size_t)k * F + f] = th;
@@ -424,6 +482,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_backward(
     const float* __restrict__ TT, float* __restrict__ SMR, float4* __restrict__ VIN,
     float4* __restrict__ VOUT, double* __restrict__ vir_part) {
     __shared__ float sy[kGenWarps][kGenMaxF];
+    __shared__ float4 sq[kGenWarps][kTbCache];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int F = g.F, nj = (F + 31) / 32;
     double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -431,6 +490,10 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_backward(
          k += (int64_t)gridDim.x * kGenWarps) {
         const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
         const int b0 = a.brow[s], nbd = a.brow[s + 1] - b0;
+        __syncwarp();
+        for (int o = lane; o < nbd && o < kTbCache; o += 32) sq[wq][o] = a.vd[a.bedge[b0 + o]];
+        __syncwarp();
+        auto qof = [&](int o) { return o < kTbCache ? sq[wq][o] : a.vd[a.bedge[b0 + o]]; };
         for (int j = 0; j < nbd; ++j) {  // phase 1
             const int e = a.bedge[b0 + j];
             const float4 q = a.vd[e];
@@ -469,14 +532,14 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_backward(
         }
         __syncwarp();
         for (int j = 0; j < nbd; ++j) {  // phase 2
-            const float4 qj = a.vd[a.bedge[b0 + j]];
+            const float4 qj = qof(j);
             const float idj = 1.0f / qj.w;
             float tb[kNJ] = {0.f, 0.f, 0.f, 0.f};
             float vix = 0.f, viy = 0.f, viz = 0.f;
             float4 vo = VOUT[b0 + j];
             for (int o = 0; o < nbd; ++o) {
                 if (o == j) continue;
-                const float4 qo = a.vd[a.bedge[b0 + o]];
+                const float4 qo = qof(o);
                 const float ido = 1.0f / qo.w;
                 const float c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
                 float cb = 0.f, cb2 = 0.f;
@@ -549,7 +612,10 @@ void launch_gen_embed(const GenModel& g, int64_t rows, const int32_t* node_array
 void launch_gen_conv(const GenModel& g, const ConvArgs& a, int layer, const float* Hin, float* Hout,
                      float* TH, double* per_atom, cudaStream_t s) {
     if (a.n == 0) return;
-    k_gen_conv<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, layer, Hin, Hout, TH, per_atom);
+    const int K1 = g.K + 1;
+    const size_t smem = sizeof(float) * ((size_t)g.F * g.K + kGenWarps * (32 * K1 + 32 + kGenMaxF));
+    GMD_CUDA(cudaFuncSetAttribute(k_gen_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_gen_conv<<<gen_grid(a.n), kGenWarps * 32, smem, s>>>(g, a, layer, Hin, Hout, TH, per_atom);
     GMD_LAUNCH_CHECK();
 }
 
@@ -569,7 +635,12 @@ void launch_gen_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, con
 void launch_gen_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
                          float* HB, float4* GRAD, double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
-    k_gen_bwd_edge<<<gen_grid(a.n), kGenWarps * 32, 0, s>>>(g, a, MB, Hl, HB, GRAD, vir_part);
+    const int K1 = g.K + 1;
+    const size_t smem =
+        sizeof(float) * (2 * (size_t)g.F * g.K + kGenWarps * (32 * (K1 + 4) + 2 * 32 * 33));
+    GMD_CUDA(cudaFuncSetAttribute(k_gen_bwd_edge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    k_gen_bwd_edge<<<gen_grid(a.n), kGenWarps * 32, smem, s>>>(g, a, MB, Hl, HB, GRAD, vir_part);
     GMD_LAUNCH_CHECK();
 }
 

@@ -23,6 +23,10 @@ struct GenModel {
     const float* P3 = nullptr;   // F x K   (three-body)
     const float* W3 = nullptr;   // F x F
     const float* W4 = nullptr;   // F x F
+    // transposed copies, so lanes over f read consecutive addresses
+    const float* WT = nullptr;   // L x F x F: WT[l][g][f] = W[l][f][g]
+    const float* W3T = nullptr;
+    const float* W4T = nullptr;
     float rc = 0, inv_rc = 0, inv_sigma = 0, mu_step = 0;
     float r3 = 1, inv_r3 = 1, inv_sigma3 = 0, mu_step3 = 0;
 };
