@@ -1253,10 +1253,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
 
     // ---- backward (:796-984)
-    if (gen)
-        launch_gen_init_hbar(h->gm, n, HB, s);
-    else
-        launch_init_hbar(n, HB, s);
+    if (gen) launch_gen_init_hbar(h->gm, n, HB, s);  // (tuned: fused into the first bwd_node)
     GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
         {
@@ -1264,7 +1261,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             if (gen)
                 launch_gen_bwd_node(h->gm, n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * F, MB, s);
             else
-                launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, s);
+                launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, l == L - 1, s);
         }
         exchange(MB);
         {

@@ -345,15 +345,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
 }
 
 // m_bar = W^T (h_bar * sech^2) (potential.cpp:816-822), thread per node
+// init: the first backward layer, where h_bar is still the readout for every
+// node (potential.cpp:808): use it directly and write it as HB's initial value
 __global__ void k_bwd_node(int64_t n, const int32_t* __restrict__ nodes,
                            const int32_t* __restrict__ crow, int layer,
-                           const float* __restrict__ HB, const float* __restrict__ TH,
-                           float* __restrict__ MB) {
+                           float* __restrict__ HB, const float* __restrict__ TH,
+                           float* __restrict__ MB, bool init) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int64_t v = nodes ? (int64_t)nodes[k] : k;
     float hb[kF], th[kF], y[kF];
-    load_row16(HB + k * kF, hb);
+    if (init) {
+#pragma unroll
+        for (int f = 0; f < kF; ++f) hb[f] = c_m.ro[f];
+        store_row16(HB + k * kF, hb);
+    } else {
+        load_row16(HB + k * kF, hb);
+    }
     load_row16(TH + k * kF, th);
 #pragma unroll
     for (int f = 0; f < kF; ++f) y[f] = hb[f] * (1.0f - th[f] * th[f]);
@@ -1605,9 +1613,9 @@ void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, fl
 }
 
 void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int layer,
-                     const float* HB, const float* TH, float* MB, cudaStream_t s) {
+                     float* HB, const float* TH, float* MB, bool init, cudaStream_t s) {
     if (n == 0) return;
-    k_bwd_node<<<div_up(n, 128), 128, 0, s>>>(n, nodes, crow, layer, HB, TH, MB);
+    k_bwd_node<<<div_up(n, 128), 128, 0, s>>>(n, nodes, crow, layer, HB, TH, MB, init);
     GMD_LAUNCH_CHECK();
 }
 

@@ -60,9 +60,10 @@ void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float
 // last layer additionally writes per-atom energies and per-CTA energy partials
 void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
                  double* per_atom, double* e_part, cudaStream_t s);
-// backward: MB[row(v)] = W_l^T (HB[v] * (1 - TH_l[v]^2))
+// backward: MB[row(v)] = W_l^T (HB[v] * (1 - TH_l[v]^2)); init: HB := readout
+// first (the first backward layer, replacing launch_init_hbar)
 void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int layer,
-                     const float* HB, const float* TH, float* MB, cudaStream_t s);
+                     float* HB, const float* TH, float* MB, bool init, cudaStream_t s);
 // backward edge pass (row form, no atomics): HB += gathered adjoints,
 // GRAD += positional gradient, virial partials per CTA (6 doubles)
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
