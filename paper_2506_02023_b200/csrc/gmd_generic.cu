@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_conv(GenModel g, ConvArg
                 const float d = a.d[eb + lane];
                 sw[lane] = a.lsrc[eb + lane];
                 const float fc = d < g.rc ? 0.5f * (cospif(d * g.inv_rc) + 1.0f) : 0.0f;
+#pragma unroll 4
                 for (int kk = 0; kk < K; ++kk) {
                     const float x = (d - g.mu_step * (float)kk) * g.inv_sigma;
                     su[lane * K1 + kk] = fc * expf(-x * x);
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_conv(GenModel g, ConvArg
                     const int f = lane + 32 * jj;
                     if (f < F) {
                         float s2 = 0.f;
+#pragma unroll 4
                         for (int kk = 0; kk < K; ++kk) s2 = fmaf(sP[kk * F + f], ui[kk], s2);
                         m[jj] = fmaf(Hin[(size_t)w * F + f], s2, m[jj]);
                     }
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_conv(GenModel g, ConvArg
             const int f = lane + 32 * jj;
             if (f < F) {
                 float z = bl[f];
+#pragma unroll 4
                 for (int q = 0; q < F; ++q) z = fmaf(WT[(size_t)q * F + f], sm[q], z);
                 const float th = tanhf(z);
                 const float hn = Hin[(size_t)r * F + f] + th;
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_node(GenModel g, int
             const int q = lane + 32 * j;
             if (q < F) {
                 float acc = 0.f;
+#pragma unroll 4
                 for (int f = 0; f < F; ++f) acc = fmaf(W[(size_t)f * F + q], sy[wq][f], acc);
                 MB[(size_t)r * F + q] = acc;
             }
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
                 scf[lane * 4 + 1] = dfc - 2.0f * fc * isg * x0;
                 scf[lane * 4 + 2] = 2.0f * fc * isg * step;
                 scf[lane * 4 + 3] = __int_as_float(a.lsrc[eb + lane]);
+#pragma unroll 4
                 for (int kk = 0; kk < K; ++kk) {
                     const float x = (d - mus * (float)kk) * isg;
                     sph[lane * K1 + kk] = expf(-x * x);
@@ -220,6 +225,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
                     const int f = lane + 32 * jj;
                     if (f < F) {
                         float A = 0.f, B = 0.f;
+#pragma unroll 4
                         for (int kk = 0; kk < K; ++kk) {
                             A = fmaf(sP[kk * F + f], ph[kk], A);
                             B = fmaf(sPk[kk * F + f], ph[kk], B);
@@ -302,6 +308,7 @@ __device__ __forceinline__ void gen_bond_t(const GenModel& g, float d, int lane,
         u = fc * expf(-x * x);
     }
     for (int j = 0; j < kNJ; ++j) out[j] = 0.f;
+#pragma unroll 4
     for (int kk = 0; kk < K; ++kk) {
         const float uk = __shfl_sync(kFull, u, kk);
         for (int j = 0; j < nj; ++j) {
@@ -321,6 +328,7 @@ __device__ __forceinline__ void gen_bond_dt(const GenModel& g, float d, int lane
         du = expf(-x * x) * (dfc - 2.0f * fc * x * g.inv_sigma3);
     }
     for (int j = 0; j < kNJ; ++j) out[j] = 0.f;
+#pragma unroll 4
     for (int kk = 0; kk < K; ++kk) {
         const float uk = __shfl_sync(kFull, du, kk);
         for (int j = 0; j < nj; ++j) {
@@ -389,6 +397,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_forward(GenModel g, B
                 const int f = lane + 32 * jj;
                 if (f < F) {
                     float z = 0.f;
+#pragma unroll 4
                     for (int q = 0; q < F; ++q) z = fmaf(g.W3T[(size_t)q * F + f], sm[wq][q], z);
                     const float th = tanhf(z);
                     TP[(size_t)(b0 + j) * F + f] = TT[(size_t)(b0 + j) * F + f] + fc * th;
@@ -430,6 +439,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_inject(GenModel g, Bo
             const int f = lane + 32 * jj;
             if (f < F) {
                 float z = 0.f;
+#pragma unroll 4
                 for (int q2 = 0; q2 < F; ++q2) z = fmaf(g.W4T[(size_t)q2 * F + f], sq[wq][q2], z);
                 const float th = tanhf(z);
                 H[(size_t)r * F + f] += th;
@@ -466,6 +476,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_bwd_q(GenModel g, int
             const int q = lane + 32 * jj;
             if (q < F) {
                 float acc = 0.f;
+#pragma unroll 4
                 for (int f = 0; f < F; ++f) acc = fmaf(g.W4[(size_t)f * F + q], sy[wq][f], acc);
                 QB[(size_t)r * F + q] = acc;
             }
@@ -520,6 +531,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_tb_backward(
                 const int q2 = lane + 32 * jj;
                 if (q2 < F) {
                     float acc = 0.f;
+#pragma unroll 4
                     for (int f = 0; f < F; ++f) acc = fmaf(g.W3[(size_t)f * F + q2], sy[wq][f], acc);
                     SMR[(size_t)(b0 + j) * F + q2] = acc;
                 }
