@@ -1539,7 +1539,7 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
             // emb W b P P3 W3 W4 ro, potential.hpp:15-41)
             const size_t nemb = 119 * (size_t)F, nW = (size_t)L * F * F, nb = (size_t)L * F,
                          nP = (size_t)F * K, nFF = (size_t)F * F;
-            std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F + nW + 2 * nFF);
+            std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F + nW + 2 * nFF + nP);
             const double* q = blob;
             size_t o = 0;
             for (size_t i = 0; i < nemb + nW + nb + nP; ++i) t[o++] = (float)*q++;  // emb, W, b, P
@@ -1561,6 +1561,10 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
                     t[o + nFF + (size_t)gg * F + f] = W4f[(size_t)f * F + gg];
                 }
             o += 2 * nFF;
+            const float* P3f = t.data() + nemb + nW + nb + 2 * nP;
+            for (int f = 0; f < F; ++f)
+                for (int kk = 0; kk < K; ++kk) t[o + (size_t)kk * F + f] = P3f[(size_t)f * K + kk];
+            o += nP;
             float* d = h->gpar.get<float>(t.size());
             GMD_CUDA(cudaMemcpy(d, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
             GenModel& g = h->gm;
@@ -1579,6 +1583,7 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
             g.WT = g.ro + F;
             g.W3T = g.WT + nW;
             g.W4T = g.W3T + nFF;
+            g.P3T = g.W4T + nFF;
             const double r3e = r3 > 0.0 ? r3 : 1.0;
             g.r3 = (float)r3e;
             g.inv_r3 = (float)(1.0 / r3e);

@@ -313,7 +313,7 @@ __device__ __forceinline__ void gen_bond_t(const GenModel& g, float d, int lane,
         const float uk = __shfl_sync(kFull, u, kk);
         for (int j = 0; j < nj; ++j) {
             const int f = lane + 32 * j;
-            if (f < F) out[j] = fmaf(g.P3[f * K + kk], uk, out[j]);
+            if (f < F) out[j] = fmaf(g.P3T[kk * F + f], uk, out[j]);
         }
     }
 }
@@ -333,7 +333,7 @@ __device__ __forceinline__ void gen_bond_dt(const GenModel& g, float d, int lane
         const float uk = __shfl_sync(kFull, du, kk);
         for (int j = 0; j < nj; ++j) {
             const int f = lane + 32 * j;
-            if (f < F) out[j] = fmaf(g.P3[f * K + kk], uk, out[j]);
+            if (f < F) out[j] = fmaf(g.P3T[kk * F + f], uk, out[j]);
         }
     }
 }

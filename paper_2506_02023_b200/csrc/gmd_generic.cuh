@@ -27,6 +27,7 @@ struct GenModel {
     const float* WT = nullptr;   // L x F x F: WT[l][g][f] = W[l][f][g]
     const float* W3T = nullptr;
     const float* W4T = nullptr;
+    const float* P3T = nullptr;  // K x F: P3T[k][f] = P3[f][k]
     float rc = 0, inv_rc = 0, inv_sigma = 0, mu_step = 0;
     float r3 = 1, inv_r3 = 1, inv_sigma3 = 0, mu_step3 = 0;
 };
