@@ -271,6 +271,8 @@ struct gmd_handle {
     DBuf row, src, img, vd, ed, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
     DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp, flagtmp, ebid;
     int nl_cap = 0;
+    int emit_cap = 0;     // slab row capacity of the current build
+    bool img_ok = false;  // per-edge packed images written (else derived on export)
 
     // model
     bool params_set = false;
@@ -794,7 +796,12 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     gd.ne = h->ne;
     gd.row = rowp;
     gd.src = h->src.get<int32_t>(h->ne);
-    gd.img = h->img.get<uint32_t>(h->ne);
+    // packed image offsets: the three-body stage needs them; otherwise they
+    // are only read by the graph export, which re-derives them from the slab
+    // (4 B per edge not written per step)
+    h->emit_cap = cap;
+    h->img_ok = r3 > 0.0;
+    gd.img = h->img_ok ? h->img.get<uint32_t>(h->ne) : nullptr;
     gd.vd = h->vd.get<float4>(h->ne);
     gd.d = h->ed.get<float>(h->ne);
     gd.bond = h->ebond.get<uint8_t>(h->ne);
@@ -1694,6 +1701,24 @@ int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, doubl
         double* t_dist = reinterpret_cast<double*>(t_dst + ne);
         double* t_vec = t_dist + ne;
         int32_t* t_off = reinterpret_cast<int32_t*>(t_vec + 3 * ne);
+        if (!h->img_ok) {  // re-run the (deterministic) emit once with image output
+            NLBuffers b{};
+            b.pos = h->pos.as<double>();
+            b.cell = h->cell.as<int32_t>();
+            b.bcnt = h->bcnt.as<int32_t>();
+            b.flags = h->flags.as<int32_t>();
+            GraphDev ge;
+            ge.n = h->n;
+            ge.ne = ne;
+            ge.row = h->row.as<int32_t>();
+            ge.src = h->src.as<int32_t>();
+            ge.img = h->img.get<uint32_t>(std::max<int64_t>(1, ne));
+            ge.vd = h->vd.as<float4>();
+            ge.d = h->ed.as<float>();
+            ge.bond = h->ebond.as<uint8_t>();
+            launch_nl_emit(h->geom, h->n, h->emit_cap, h->slab.as<unsigned long long>(), b, ge, s);
+            h->img_ok = true;
+        }
         GraphDev gd;
         gd.n = h->n;
         gd.ne = ne;

@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, 
             const double dd = __dsqrt_rn(dot_rn(vr, vr));
             const int e = e0 + k;
             e_src[e] = j;
-            e_img[e] = pack_img(o0, o1, o2);
+            if (e_img) e_img[e] = pack_img(o0, o1, o2);  // null: not needed by this build
             e_vd[e] = make_float4((float)vr.x, (float)vr.y, (float)vr.z, (float)dd);
             e_d[e] = (float)dd;
             isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
