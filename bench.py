@@ -66,7 +66,8 @@ def bytes_model(n, ne, nb, L, threebody):
     counted (each row is compulsory once, already in the per-node terms)."""
     return {
         "nl_search": 68 * n + 8 * ne,                 # bin-sorted SoA atoms + degree; sorted keys
-        "nl_emit": 37 * ne + 40 * n,                  # keys in; src/img/vd/d/bond out; pos+cell once
+        # keys in; src/vd/d out (+ img/bond with three-body); pos+cell once
+        "nl_emit": (37 if threebody else 32) * ne + 40 * n,
         "conv": 8 * ne + 196 * n,                     # d+src per edge; h_in row, h_out + tanh rows
         "bwd_edge": 20 * ne + 292 * n,                # vd+src per edge; m_bar, h_in, h_bar rw, grad rw
         "bwd_node": 192 * n,

@@ -804,7 +804,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     gd.img = h->img_ok ? h->img.get<uint32_t>(h->ne) : nullptr;
     gd.vd = h->vd.get<float4>(h->ne);
     gd.d = h->ed.get<float>(h->ne);
-    gd.bond = h->ebond.get<uint8_t>(h->ne);
+    gd.bond = r3 > 0.0 ? h->ebond.get<uint8_t>(h->ne) : nullptr;  // three-body bonds only
     { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s); }
 
     // ---- requirement masks, span layouts, local edge ends (partitioner.cpp:110-218)
@@ -1715,7 +1715,7 @@ int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, doubl
             ge.img = h->img.get<uint32_t>(std::max<int64_t>(1, ne));
             ge.vd = h->vd.as<float4>();
             ge.d = h->ed.as<float>();
-            ge.bond = h->ebond.as<uint8_t>();
+            ge.bond = h->has_lg ? h->ebond.as<uint8_t>() : nullptr;
             launch_nl_emit(h->geom, h->n, h->emit_cap, h->slab.as<unsigned long long>(), b, ge, s);
             h->img_ok = true;
         }

@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, 
             e_vd[e] = make_float4((float)vr.x, (float)vr.y, (float)vr.z, (float)dd);
             e_d[e] = (float)dd;
             isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
-            e_bond[e] = isb ? 1 : 0;
+            if (e_bond) e_bond[e] = isb ? 1 : 0;
         }
         nb += __popc(__ballot_sync(0xffffffffu, isb) & gmask);
     }
