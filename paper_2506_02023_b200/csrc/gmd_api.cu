@@ -289,8 +289,8 @@ struct gmd_handle {
     int max_bonds = 0;     // max in-bonds of a center (three-body), per build
     int ctab_grid = 0;
     DBuf ccnt, cstart, ctab, ccta;
-    DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v3_part, red, per_atom,
-        forces, conv_tmp, exp_tmp;
+    DBuf TH, MB, HB, GRAD, TP, TH3, TH4, QB, VIN, VOUT, e_part, v_part, v_grp, v3_part, red, per_atom,
+        forces, conv_tmp, exp_tmp, nonfin;
     DBuf md_part, md_out, md_bad;  // on-device MD observables / non-finite flag
     DBuf md_pos, md_vel, md_frc, md_mass, md_z;  // device state of gmd_md_run
     cudaEvent_t ev[8] = {};
@@ -741,7 +741,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     // Coordinates are taken relative to the destination bin origin, so each
     // component is bounded by B = max_k sum_r |L_rk| (s_r + 1) / bins_r; fp32
     // rounding moves each component of v by at most delta = 4 B 2^-24.
-    float thr32, acc32, zero32;
+    float thr32, acc32, zero32, pos_gate;
     {
         double B = 0.0;
         for (int k = 0; k < 3; ++k) {
@@ -767,6 +767,21 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         const double rz = 2.0 * std::sqrt(3.0) * delta + 1e-6;
         zero32 = std::nextafter((float)(rz * rz * (1.0 + 8.0 * u)), INFINITY);
         if (!(acc32 > zero32)) acc32 = -1.0f;  // no fast path: every survivor in fp64
+        // The band's margin (rc * 1e-9) must dwarf the fp64 disagreement between
+        // the wrapped vector (fractional -> floor -> lattice) and the reference's
+        // raw one ((p_j - p_i) + off L).  Both are a few dozen roundings of
+        // magnitudes <= kappa (M + S), M = max |input coordinate| (k_wrap, on
+        // the device), S = sum |L|, kappa = conditioning of the fractional map:
+        // fast accept is kept only while 64 u64 kappa (M + S) <= rc 1e-9 / 2.
+        double S = 0.0, imax = 0.0;
+        for (int k = 0; k < 9; ++k) {
+            S += std::abs(g.L[k]);
+            imax = std::max(imax, std::abs(g.inv[k]));
+        }
+        const double kappa = 3.0 * S * imax + 1.0;
+        const double mgate = 0.5e-9 * std::sqrt(g.cutoff2) / (64.0 * std::ldexp(1.0, -53) * kappa) - S;
+        pos_gate = mgate > 0.0 ? std::nextafter((float)mgate, 0.0f) : -1.0f;
+        if (!(pos_gate > 0.0f)) acc32 = -1.0f;
     }
     int cap = h->nl_cap;
     if (cap <= 0) {  // first build: density estimate of the mean degree
@@ -778,13 +793,13 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     int32_t ne32 = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         auto* slab = h->slab.get<unsigned long long>((size_t)n * cap);
-        { PROF("nl_search"); launch_nl_search(g, thr32, acc32, zero32, nbins, n, cap, b, slab, ownp, myrank, s); }
+        { PROF("nl_search"); launch_nl_search(g, thr32, acc32, zero32, pos_gate, nbins, n, cap, b, slab, ownp, myrank, s); }
         { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
         GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
         read_flags(h, hdr);
         if (hdr[0] <= cap) break;
         cap = (hdr[0] + 7) & ~7;  // rare: an atom exceeded the slab row
-        GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
+        GMD_CUDA(cudaMemsetAsync(b.flags, 0, 8, s));  // keeps k_wrap's flags[3]
     }
     {   // next build: size the slab from this one's maximum degree
         h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
@@ -1114,7 +1129,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                            ? kForceChunks
                            : 1;
     double* e_part = h->e_part.get<double>(grid);
-    double* v_part = h->v_part.get<double>((size_t)(L + nchunk - 1) * vgrid * 6);
+    double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);
     const int tgrid = gen ? gen_grid(n) * 8 : tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
@@ -1129,6 +1144,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                h->vd.as<float4>(),
                h->ed.as<float>()};
     if (use_tc) ensure_chunk_table(h, a);
+    // per-layer non-finite feature check (potential.cpp:107-115, :772)
+    auto* nonfin = h->nonfin.get<unsigned long long>(1);
+    GMD_CUDA(cudaMemsetAsync(nonfin, 0xff, 8, s));
+    a.nonfinite = nonfin;
     BondArgs ba{n,
                 a.nodes,
                 a.crow,
@@ -1282,13 +1301,16 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
             else {  // l = 0 in node chunks, forces streamed out per chunk
                 double* fd = h->forces.get<double>(3 * n_all);
+                // chunk starts on multiples of the grid's node stride and one
+                // carried per-group virial: bitwise the unchunked launch
+                const int64_t stride = bwd_edge_stride(vgrid);
+                double* vg = h->v_grp.get<double>((size_t)stride * 6);
                 for (int c = 0; c < nchunk; ++c) {
                     ConvArgs ac = a;
-                    ac.k0 = n * c / nchunk;
-                    ac.n = n * (c + 1) / nchunk;
-                    // virial partials: layer 0's slot, then slots L .. L + nchunk - 2
-                    const int slot = c == 0 ? 0 : L - 1 + c;
-                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part + (size_t)slot * vgrid * 6, s);
+                    ac.k0 = (n * c / nchunk) / stride * stride;
+                    ac.n = c + 1 == nchunk ? n : (n * (c + 1) / nchunk) / stride * stride;
+                    if (ac.n <= ac.k0) continue;
+                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part, s, vg, vgrid);
                     launch_forces_out(ac.n - ac.k0, nullptr, GRAD + ac.k0, fd + 3 * ac.k0, nullptr, s);
                     GMD_CUDA(cudaEventRecord(h->ev[7], s));
                     GMD_CUDA(cudaStreamWaitEvent(h->side, h->ev[7], 0));
@@ -1345,7 +1367,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         PROF("reduce");
         // generic kernels: the energy is the fixed-order sum of the per-atom energies
         const double* ps[3] = {gen ? pa : e_part, v_part, v3_part};
-        const int np[3] = {gen ? (int)n_all : grid, (L + nchunk - 1) * vgrid, tgrid},
+        const int np[3] = {gen ? (int)n_all : grid, L * vgrid, tgrid},
                   w[3] = {1, 6, 9};
         if (!tb) GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
         launch_reduce_sets(tb ? 3 : 2, ps, np, w, red, s);
@@ -1373,18 +1395,60 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         else
             GMD_CUDA(cudaMemcpyAsync(forces, fd, 24 * n_all, cudaMemcpyDeviceToHost, s));
     }
+    unsigned long long nfkey = ~0ull;
+    GMD_CUDA(cudaMemcpyAsync(&nfkey, nonfin, 8, cudaMemcpyDeviceToHost, s));
     int32_t hdr[2];
     read_flags(h, hdr);  // synchronizes the stream
     if (nchunk > 1) GMD_CUDA(cudaStreamSynchronize(h->side));  // streamed force chunks
-    if (rank_mode) {  // energy + virial: rank-ordered sum of the per-rank sums
-        std::vector<double> all((size_t)h->comm->world * 16);
-        h->comm->allgather_f64(s, hred, 16, all.data());
-        for (int c = 0; c < 16; ++c) {
-            double acc = 0.0;
-            for (int j = 0; j < h->comm->world; ++j) acc += all[(size_t)j * 16 + c];
-            hred[c] = acc;
+    // first non-finite feature: (layer, partition, layout row) -> global atom id
+    int64_t nf_layer = -1, nf_part = -1, nf_atom = -1;
+    if (nfkey != ~0ull) {
+        nf_layer = (int64_t)(nfkey >> 40);
+        const int64_t row = (int64_t)(nfkey & ((1ull << 40) - 1));
+        nf_atom = row;
+        if (part) {
+            int32_t gid = 0;
+            GMD_CUDA(cudaMemcpy(&gid, A.node_array.as<int32_t>() + row, 4, cudaMemcpyDeviceToHost));
+            nf_atom = gid;
+        }
+        if (rank_mode) {
+            nf_part = h->comm->rank;
+        } else if (part) {
+            int32_t ow = 0;
+            GMD_CUDA(cudaMemcpy(&ow, h->atoms.owner.as<int32_t>() + nf_atom, 4, cudaMemcpyDeviceToHost));
+            nf_part = ow;
+        } else {
+            nf_part = 0;
         }
     }
+    if (rank_mode) {  // energy + virial: rank-ordered sum of the per-rank sums
+        constexpr int kW = 19;  // 16 sums + first non-finite (layer, partition, atom)
+        double mine[kW];
+        std::copy(hred, hred + 16, mine);
+        mine[16] = (double)nf_layer;
+        mine[17] = (double)nf_part;
+        mine[18] = (double)nf_atom;
+        std::vector<double> all((size_t)h->comm->world * kW);
+        h->comm->allgather_f64(s, mine, kW, all.data());
+        for (int c = 0; c < 16; ++c) {
+            double acc = 0.0;
+            for (int j = 0; j < h->comm->world; ++j) acc += all[(size_t)j * kW + c];
+            hred[c] = acc;
+        }
+        nf_layer = -1;  // every rank reports the same offender: lowest layer, then rank
+        for (int j = 0; j < h->comm->world; ++j) {
+            const double* o = all.data() + (size_t)j * kW;
+            if (o[16] >= 0 && (nf_layer < 0 || o[16] < nf_layer)) {
+                nf_layer = (int64_t)o[16];
+                nf_part = (int64_t)o[17];
+                nf_atom = (int64_t)o[18];
+            }
+        }
+    }
+    if (nf_layer >= 0)  // parallel_for_partitions' wrapper (engine.cpp:278-283)
+        raise(kRuntime, "worker for partition " + std::to_string(nf_part) +
+                            " failed: non-finite feature at layer " + std::to_string(nf_layer) +
+                            ", atom " + std::to_string(nf_atom));
     if (!std::isfinite(hred[0])) raise(kRuntime, "non-finite energy (non-finite features)");
     if (energy) *energy = hred[0];
     if (stress) {  // stress = sym(virial) / V (potential.cpp:978-982)
@@ -1536,8 +1600,22 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
         if (r3 > 0.0 && r3 > r_atom)
             raise(kConfig, "three-body cutoff cannot exceed the atom cutoff");
         const int64_t total = gmd_params_size(F, K, L);
-        for (int64_t i = 0; i < total; ++i)
-            if (!std::isfinite(blob[i])) raise(kConfig, "parameter blob contains a non-finite value");
+        {   // ToyPotentialParams::validate (potential.cpp:150-176), blob order
+            const int64_t f = F, k = K, l = L;
+            const std::pair<const char*, int64_t> arrays[] = {
+                {"embedding", 119 * f}, {"layer_w", l * f * f}, {"layer_b", l * f},
+                {"basis_proj", f * k}, {"basis3_proj", f * k}, {"w3", f * f}, {"w4", f * f},
+                {"readout", f}};
+            int64_t off = 0;
+            for (const auto& a : arrays) {
+                for (int64_t i = 0; i < a.second; ++i)
+                    if (!std::isfinite(blob[off + i]))
+                        raise(kConfig, std::string("parameter array ") + a.first +
+                                           " contains a non-finite value");
+                off += a.second;
+            }
+            if (off != total) raise(kRuntime, "internal: parameter blob layout");
+        }
         h->generic = F != kF || K != kK || L > kMaxLayers;
         if (h->generic) {  // width-generic kernels: fp32 tables in global memory
             if (F > kGenMaxF || K > kGenMaxK)

@@ -24,9 +24,10 @@ struct LocalGroup {
     std::vector<std::vector<int64_t>> soff, scnt;
     std::vector<std::vector<double>> dbuf;
     std::vector<std::vector<int64_t>> ibuf;
+    std::vector<int> bad;  // per rank: this exchange failed its plan check
 
     explicit LocalGroup(int w)
-        : world(w), refs(w), send(w), soff(w), scnt(w), dbuf(w), ibuf(w) {}
+        : world(w), refs(w), send(w), soff(w), scnt(w), dbuf(w), ibuf(w), bad(w, 0) {}
 
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
@@ -70,14 +71,28 @@ struct LocalTransport final : Transport {
         g->soff[rank].assign(soff, soff + world);
         g->scnt[rank].assign(scnt, scnt + world);
         g->barrier();
+        // a plan mismatch is recorded, not thrown here: every rank must still
+        // reach the second barrier, then all of them raise together (a rank
+        // leaving early would leave its peers blocked in barrier())
+        bool bad = false;
         for (int j = 0; j < world; ++j) {
             if (j == rank || rcnt[j] == 0) continue;
-            if (g->scnt[j][rank] != rcnt[j]) raise(kRuntime, "transfer plan misalignment");
+            if (g->scnt[j][rank] != rcnt[j]) {
+                bad = true;
+                continue;
+            }
             GMD_CUDA(cudaMemcpyAsync(recv + roff[j] * width, g->send[j] + g->soff[j][rank] * width,
                                      sizeof(float) * rcnt[j] * width, cudaMemcpyDefault, s));
         }
         GMD_CUDA(cudaStreamSynchronize(s));
+        // each rank writes only its own slot, and only after the first barrier
+        // of an exchange, so the reads below never race with the next exchange
+        g->bad[rank] = bad;
         g->barrier();  // peers are done reading this rank's send buffer
+        if (bad) raise(kRuntime, "transfer plan misalignment");
+        for (int j = 0; j < world; ++j)
+            if (g->bad[j])
+                raise(kRuntime, "transfer plan misalignment (detected by rank " + std::to_string(j) + ")");
     }
 
     void allgather_f64(cudaStream_t, const double* in, int n, double* out) override {

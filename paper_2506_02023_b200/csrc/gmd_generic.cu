@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_conv(GenModel g, ConvArg
                 const float th = tanhf(z);
                 const float hn = Hin[(size_t)r * F + f] + th;
                 Hout[(size_t)r * F + f] = hn;
+                note_nonfinite(a, layer, r, hn);
                 TH[(size_t)k * F + f] = th;
                 ev = fmaf(g.ro[f], hn, ev);
             }

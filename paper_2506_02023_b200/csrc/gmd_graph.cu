@@ -52,8 +52,19 @@ __device__ __forceinline__ int64_t bin_of(const Geom& g, const double fw[3], int
 
 __global__ void k_wrap(const Geom g, int64_t n, const double* __restrict__ pos,
                        int32_t* __restrict__ cell, double* __restrict__ fw_axis,
-                       int32_t* __restrict__ bin, int32_t* __restrict__ bin_cnt) {
+                       int32_t* __restrict__ bin, int32_t* __restrict__ bin_cnt,
+                       int32_t* __restrict__ flags) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // max |coordinate| over the input (rounded up to fp32) -> flags[3]: the
+    // search's fast-accept band is only sound while the wrapped and raw
+    // vectors agree far below its rc * 1e-9 margin (launch_nl_search)
+    float m = 0.f;
+    if (i < n)
+        m = fmaxf(fmaxf(__double2float_ru(fabs(pos[3 * i])), __double2float_ru(fabs(pos[3 * i + 1]))),
+                  __double2float_ru(fabs(pos[3 * i + 2])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(&flags[3], __float_as_int(m));
     if (i >= n) return;
     int c[3], b[3];
     double fw[3];
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
     const double* __restrict__ s_w, const double* __restrict__ s_p,
     const int32_t* __restrict__ s_c, int32_t* __restrict__ deg, int32_t* __restrict__ flags,
     unsigned long long* __restrict__ slab, const int32_t* __restrict__ owner, int only,
-    int cbits) {
+    int cbits, float pos_gate) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp carve-up by byte offsets (keeps the shared address space)
@@ -209,6 +220,9 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
     o = (o + 15) & ~(size_t)15;
     uint32_t* keys = reinterpret_cast<uint32_t*>(base + o);
 
+    // fast accept only while every |coordinate| <= pos_gate (k_wrap's max in
+    // flags[3]; NaN bit patterns compare above the gate)
+    if (!(__int_as_float(flags[3]) <= pos_gate)) acc32 = -1.0f;
     const int sx = 2 * g.sten[0] + 1, sy = 2 * g.sten[1] + 1, sz = 2 * g.sten[2] + 1;
     const int ncell = sx * sy * sz;
     const int64_t wg = (int64_t)blockIdx.x * kWarps + warp, nw = (int64_t)gridDim.x * kWarps;
@@ -616,7 +630,8 @@ int nl_grid(int64_t nbins) {
 }  // namespace
 
 void launch_wrap(const Geom& g, int64_t n, NLBuffers& b, cudaStream_t s) {
-    k_wrap<<<div_up(n, 256), 256, 0, s>>>(g, n, b.pos, b.cell, b.fw_axis, b.bin, b.bin_cnt);
+    k_wrap<<<div_up(n, 256), 256, 0, s>>>(g, n, b.pos, b.cell, b.fw_axis, b.bin, b.bin_cnt,
+                                          b.flags);
     GMD_LAUNCH_CHECK();
 }
 
@@ -626,8 +641,8 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
     GMD_LAUNCH_CHECK();
 }
 
-void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int64_t nbins,
-                      int64_t n, int cap,
+void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, float pos_gate,
+                      int64_t nbins, int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s) {
     // destinations staged per warp (the search is latency-bound; occupancy
@@ -667,7 +682,7 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int
     kern<<<nl_grid(nbins), kThreads, sm, s>>>(g, thr32, acc32, zero32, nbins, n, group, cap,
                                                      b.bin_start,
                                                      b.s_id, b.s_w, b.s_p, b.s_c, b.deg, b.flags,
-                                                     slab, owner, only, cbits);
+                                                     slab, owner, only, cbits, pos_gate);
     GMD_LAUNCH_CHECK();
 }
 

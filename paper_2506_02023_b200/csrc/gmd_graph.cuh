@@ -45,7 +45,8 @@ struct NLBuffers {
     int32_t* s_c;        // 3 x n SoA: cell_of
     int32_t* deg;        // n (per-dst degree)
     int32_t* bcnt;       // n (per-dst bond count)
-    int32_t* flags;      // [0] max degree, [1] error bits
+    int32_t* flags;      // [0] max degree, [1] error bits, [2] max in-bonds,
+                         // [3] max |input coordinate| (fp32 bits, k_wrap)
 };
 
 enum : int { kErrImgRange = 1, kErrQRange = 2, kErrCap = 4 };
@@ -56,8 +57,11 @@ void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, c
 // degrees into deg, max degree into flags[0] (slab rows truncated at cap)
 // only >= 0: rows only for destination atoms with owner[i] == only (the
 // other rows stay empty; deg must be zeroed by the caller)
-void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, int64_t nbins,
-                      int64_t n, int cap,
+// pos_gate: the fast-accept band is disabled on the device when any input
+// coordinate exceeds it (wrapped vs raw vectors could then differ by more
+// than the band's margin)
+void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, float pos_gate,
+                      int64_t nbins, int64_t n, int cap,
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s);
 // emit: slab rows -> CSR (row must hold the scanned degrees)

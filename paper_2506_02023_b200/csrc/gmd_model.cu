@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
             const int64_t r = a.crow ? a.crow[v] : v;
             const float hn = Hin[r * kF + gl] + th;
             Hout[r * kF + gl] = hn;
+            note_nonfinite(a, layer, r, hn);
             TH[k * kF + gl] = th;
             ev = sro[gl] * hn;
         }
@@ -677,6 +678,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
             const int64_t r = a.crow ? a.crow[v] : v;
             const float hn = Hin[r * kF + gl] + th;
             Hout[r * kF + gl] = hn;
+            note_nonfinite(a, layer, r, hn);
             TH[k * kF + gl] = th;
             ev = sro[gl] * hn;
         }
@@ -784,7 +786,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
                                                            const float* __restrict__ Hl,
                                                            float* __restrict__ HB,
                                                            float4* __restrict__ GRAD,
-                                                           double* vir_part) {
+                                                           double* vir_part, double* vir_grp) {
     __shared__ __align__(16) float sU[(NT / 16)][2][kF];  // [group][m_bar_u, h_u][f]
     __shared__ double sVir[(NT / 16)][6];
     const int lane = threadIdx.x & 31;
@@ -792,7 +794,10 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
     const int64_t g0 = (int64_t)blockIdx.x * (NT / 16) + grp;
     const int64_t ng = (int64_t)gridDim.x * (NT / 16);
     const float isg = c_m.inv_sigma, mus = c_m.mu_step;
-    if (gl < 6) sVir[grp][gl] = 0.0;
+    // vir_grp (node-chunked launches, k0 a multiple of ng): every group's
+    // running virial sum carries over from the previous chunk, so the fp64
+    // accumulation order is exactly the unchunked launch's
+    if (gl < 6) sVir[grp][gl] = (vir_grp && a.k0 > 0) ? vir_grp[(size_t)g0 * 6 + gl] : 0.0;
     const int64_t iters = (a.n - a.k0 + ng - 1) / ng;  // nodes [k0, n)
     int e0n = 0, e1n = 0;
     float mun = 0.f, hun = 0.f;
@@ -868,6 +873,8 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
             }
         }
     }
+    __syncwarp();
+    if (vir_grp && gl < 6) vir_grp[(size_t)g0 * 6 + gl] = sVir[grp][gl];
     __syncthreads();
     if (threadIdx.x < 6) {
         double acc6 = 0.0;
@@ -1640,16 +1647,19 @@ int bwd_edge_grid(int64_t n) {
 
 bool bwd_edge_ranges() { return bwd_variant() != 1; }
 
+int64_t bwd_edge_stride(int grid) { return (int64_t)grid * (kBwdThreads / 16); }
+
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
-                     double* vir_part, cudaStream_t s) {
+                     double* vir_part, cudaStream_t s, double* vir_grp, int grid) {
     if (a.n - a.k0 <= 0) return;
     const int variant = bwd_variant();
     if (variant == 1 && a.k0 != 0) raise(kRuntime, "internal: node ranges need the default kernel");
-    const int g = bwd_edge_grid(a.n - a.k0);
+    const int g = grid > 0 ? grid : bwd_edge_grid(a.n - a.k0);
     if (variant == 1)  // scalar-FFMA kernel (A/B reference)
         k_bwd_edge<<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
     else
-        k_bwd_edge2<1, kBwdThreads><<<g, kBwdThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+        k_bwd_edge2<1, kBwdThreads><<<g, kBwdThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
+                                                              vir_grp);
     GMD_LAUNCH_CHECK();
 }
 

@@ -47,7 +47,16 @@ struct ConvArgs {
     const float4* vd;  // (vx, vy, vz, d) per edge (backward)
     const float* d;    // d per edge (forward)
     int64_t k0 = 0;    // first node processed (launch_bwd_edge: nodes [k0, n))
+    // conv kernels: first non-finite feature, atomicMin of (layer << 40 | row)
+    // with row the node's layout row (crow) -- the reference's check_finite
+    // order (potential.cpp:107-115; partitions ascending, layout order)
+    unsigned long long* nonfinite = nullptr;
 };
+
+__device__ __forceinline__ void note_nonfinite(const ConvArgs& a, int layer, int64_t row, float h) {
+    if (a.nonfinite && !isfinite(h))
+        atomicMin(a.nonfinite, ((unsigned long long)layer << 40) | (unsigned long long)row);
+}
 
 int model_grid(int64_t n);  // fixed grid => deterministic reductions
 int bwd_edge_grid(int64_t n);  // grid (= virial partial count) of launch_bwd_edge
@@ -66,10 +75,17 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
                      float* HB, const float* TH, float* MB, bool init, cudaStream_t s);
 // backward edge pass (row form, no atomics): HB += gathered adjoints,
 // GRAD += positional gradient, virial partials per CTA (6 doubles)
+// vir_grp / grid: node-chunked launches (default kernel only) pass a fixed
+// grid and a carry buffer of grid * bwd_edge_stride(grid) / ... per-group
+// virial sums; with chunk starts k0 that are multiples of
+// bwd_edge_stride(grid) every node meets the same CTA group in the same order
+// as in one launch, so the virial (and everything else) is bitwise the same
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
-                     double* vir_part, cudaStream_t s);
+                     double* vir_part, cudaStream_t s, double* vir_grp = nullptr, int grid = 0);
 // the default kernel takes node ranges (a.k0 > 0); grid = bwd_edge_grid(n - k0)
 bool bwd_edge_ranges();
+// nodes per sweep of the default kernel's grid (node k -> group k mod stride)
+int64_t bwd_edge_stride(int grid);
 
 // the same pass with the radial contractions on tcgen05 (TMEM accumulator);
 // tcgen05 backward edge pass over 16-edge chunk records (one per chunk of a

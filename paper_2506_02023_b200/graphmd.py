@@ -283,8 +283,11 @@ class ToyPotentialParams:
             raise Error("three-body cutoff cannot exceed the atom cutoff")
         if self.blob is None or len(self.blob) != sum(s for _, s in self._sizes()):
             raise Error("parameter array has the wrong size")
-        if not np.all(np.isfinite(self.blob)):
-            raise Error("parameter array contains a non-finite value")
+        off = 0
+        for name, sz in self._sizes():  # potential.cpp:157-175, in table order
+            if not np.all(np.isfinite(self.blob[off:off + sz])):
+                raise Error(f"parameter array {name} contains a non-finite value")
+            off += sz
 
     # binary parameter files (potential.cpp:178-260, docs/formats.md): magic
     # GMPT, u32 version 1, u32 F K L flags, f64 r_atom r_3body, u64 seed, then

@@ -8,6 +8,14 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# fp32-vs-fp64 tolerances of every GPU-vs-oracle comparison: SURVEY §8(c)'s
+# proposal, calibrated in tests/test_gpu_scale.py::test_tolerance_calibration
+# (the fp64 reference's own sensitivity to fp32-rounded positions at C3):
+#   per-atom energy |dE_i| <= 1e-5 eV; total |dE|/N <= 1e-6 eV/atom;
+#   forces max |dF| <= 1e-4 eV/A and <= 1e-5 x max |F|; stress <= 1e-6 eV/A^3
+TOL_EA, TOL_E, TOL_F, TOL_FREL, TOL_S = 1e-5, 1e-6, 1e-4, 1e-5, 1e-6
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: longer-running parity sweeps")

@@ -4,13 +4,14 @@ ToyPotentialParams widths, potential.hpp:15-41): the width-generic kernels
 
 Two-body and three-body (SURVEY §8d's F = 64 "CHGNet-width" variant).
 Tolerances as tests/test_gpu_model.py (fp32 compute against fp64): per-atom
-energy 2e-5 eV, total energy 2e-6 eV/atom, forces 2e-4 eV/A, stress 2e-6 eV/A^3
+energy 1e-5 eV, total energy 1e-6 eV/atom, forces 1e-4 eV/A, stress 1e-6 eV/A^3
 -- scaled by sqrt(F / 16) for wider features (longer fp32 sums)."""
 import numpy as np
 import pytest
 
 from paper_2506_02023_b200 import graphmd as G
 from tests import systems as S
+from tests.conftest import TOL_E, TOL_EA, TOL_F, TOL_FREL, TOL_S
 
 pytestmark = pytest.mark.gpu
 
@@ -30,11 +31,11 @@ def test_generic_widths_vs_oracle(oracle_c, F, K, L, r3):
     ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, F, K, L, 5.0, r3)
     out = run(s, prm)
     sc = max(1.0, np.sqrt(F / 16.0)) * max(1.0, L / 3.0)
-    assert np.abs(out.per_atom - ref["per_atom"]).max() <= 2e-5 * sc
-    assert abs(out.energy - ref["energy"]) / s.size() <= 2e-6 * sc
+    assert np.abs(out.per_atom - ref["per_atom"]).max() <= TOL_EA * sc
+    assert abs(out.energy - ref["energy"]) / s.size() <= TOL_E * sc
     fmax = np.abs(ref["forces"]).max()
-    assert np.abs(out.forces - ref["forces"]).max() <= max(2e-4, 2e-5 * fmax) * sc
-    assert np.abs(out.stress - ref["stress"]).max() <= 2e-6 * sc
+    assert np.abs(out.forces - ref["forces"]).max() <= min(TOL_F, max(TOL_FREL * fmax, 1e-6)) * sc
+    assert np.abs(out.stress - ref["stress"]).max() <= TOL_S * sc
 
 
 @pytest.mark.parametrize("F,K,r3", [(32, 8, 0.0), (12, 6, 0.0), (64, 8, 3.0)])

@@ -146,3 +146,24 @@ def test_far_images(oracle_c, shift):
     pos[1::7] -= 2 * s.lattice[0]
     s = G.AtomicSystem(pos, s.lattice, s.species)
     assert_same_graph(gpu_graph(s, 3.2), oracle_c.neighbor_list(*S.as_args(s), 3.2))
+
+
+@pytest.mark.parametrize("shift", [0, 1 << 12, 1 << 16, 5_000_000])
+def test_far_pairs_at_cutoff(oracle_c, shift):
+    """Pairs at rc (1 +- 1e-11 .. 1e-8) placed `shift` cells out: there the
+    wrapped and raw fp64 vectors disagree by up to ~1e-8 A, so the fp32 fast
+    accept must switch itself off (k_wrap's max |coordinate| vs the host's
+    gate) and every survivor take the reference's raw-position test."""
+    rc = 5.0
+    rng = np.random.default_rng(shift + 1)
+    fac = 1.0 + np.concatenate([-np.logspace(-11, -8, 12), np.logspace(-11, -8, 12)])
+    lat = np.diag([80.0, 80.0, 80.0])
+    pos = []
+    for i, f in enumerate(fac):
+        base = np.array([6.0 + 13.0 * (i % 5), 6.0 + 13.0 * ((i // 5) % 5), 6.0 + 13.0 * (i // 25)])
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        pos += [base, base + rc * f * u]
+    pos = np.array(pos) + shift * lat[0] - (shift // 3) * lat[2]
+    s = G.AtomicSystem(pos, lat, np.ones(len(pos), np.int32))
+    assert_same_graph(gpu_graph(s, rc), oracle_c.neighbor_list(*S.as_args(s), rc))

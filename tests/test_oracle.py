@@ -168,3 +168,35 @@ def test_errors(oracle_c):
     big = S.random_system(200, (40, 10, 10), 3)
     with pytest.raises(OracleError, match="partition-width error"):
         oracle_c.create(*S.as_args(big), 3.0, p=16)
+
+
+def test_bench_ref_systems(oracle_ref):
+    """bench.py's reference arm builds its systems through the reference
+    (never mapping the product library); they are bitwise the test builders."""
+    import bench
+    from tests import systems as S
+    for spec, mk in [(("quartz", (6, 5, 4)), lambda: S.quartz((6, 5, 4))),
+                     (("liquid", 3000), lambda: S.liquid(3000))]:
+        pos, z, lat, _ = bench.ref_system(spec, oracle_ref)
+        s = mk()
+        np.testing.assert_array_equal(pos, s.positions)
+        np.testing.assert_array_equal(z, s.species)
+        np.testing.assert_array_equal(lat, s.lattice)
+
+
+def test_bench_reference_arm_maps_no_product_library():
+    import json
+    import subprocess
+    import sys
+    from oracle.oracle import available
+    if not available("ref"):
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--config", "c1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["native_libs"] == ["oracle/_ref/libgraphmd_ref.so"]
+    assert line["config"]["workload"].startswith("c1")
