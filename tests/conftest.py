@@ -8,12 +8,15 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
-# fp32-vs-fp64 tolerances of every GPU-vs-oracle comparison: SURVEY §8(c)'s
-# proposal, calibrated in tests/test_gpu_scale.py::test_tolerance_calibration
-# (the fp64 reference's own sensitivity to fp32-rounded positions at C3):
-#   per-atom energy |dE_i| <= 1e-5 eV; total |dE|/N <= 1e-6 eV/atom;
-#   forces max |dF| <= 1e-4 eV/A and <= 1e-5 x max |F|; stress <= 1e-6 eV/A^3
-TOL_EA, TOL_E, TOL_F, TOL_FREL, TOL_S = 1e-5, 1e-6, 1e-4, 1e-5, 1e-6
+# fp32-vs-fp64 tolerances of every GPU-vs-oracle comparison, calibrated in
+# tests/test_gpu_scale.py::test_tolerance_calibration: the fp64 reference run
+# on fp32-ROUNDED positions moves per-atom energies by 1.5e-5 eV at C3, above
+# SURVEY §8(c)'s proposed 1e-5, so the proposal is widened 2x to sit at that
+# floor (the GPU keeps fp64 positions and lands well inside it: 3e-6 eV):
+#   per-atom energy |dE_i| <= 2e-5 eV; total |dE|/N <= 2e-6 eV/atom;
+#   forces max |dF| <= 2e-4 eV/A and <= 2e-5 x max |F|; stress <= 2e-6 eV/A^3
+TOL_EA, TOL_E, TOL_F, TOL_FREL, TOL_S = 2e-5, 2e-6, 2e-4, 2e-5, 2e-6
+SURVEY_TOL = dict(dE_i=1e-5, dE_N=1e-6, dF=1e-4, dS=1e-6)  # SURVEY §8(c) proposal
 
 
 def pytest_configure(config):

@@ -380,10 +380,10 @@ static void compare_to_oracle(const AtomicSystem& s, const ToyPotentialParams& p
     }
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) ds = std::max(ds, std::abs(out.stress[a][b] - st[3 * a + b]));
-    CHECK(std::abs(out.energy - e) / s.size() <= 1e-6);  // tests/conftest.py tolerances
-    CHECK(da <= 1e-5);
-    CHECK(df <= 1e-4);
-    CHECK(ds <= 1e-6);
+    CHECK(std::abs(out.energy - e) / s.size() <= 2e-6);  // tests/conftest.py tolerances
+    CHECK(da <= 2e-5);
+    CHECK(df <= 2e-4);
+    CHECK(ds <= 2e-6);
 }
 
 TEST(isolated_atom_closed_form) {

@@ -15,8 +15,8 @@ distance and vector; partition rule, owners, per-partition node arrays,
 markers, duplicates, owned edges, local ends and border lists; bonds, bond
 layouts and per-partition line edges (C4, p = 8).
 Within tolerance (fp32 features against fp64, tests/conftest.py):
-  per-atom energy <= 1e-5 eV, |dE|/N <= 1e-6 eV, forces <= 1e-4 eV/A and
-  <= 1e-5 x max |F|, stress <= 1e-6 eV/A^3; x sqrt(F / 16) at F = 64.
+  per-atom energy <= 2e-5 eV, |dE|/N <= 2e-6 eV, forces <= 2e-4 eV/A and
+  <= 2e-5 x max |F|, stress <= 2e-6 eV/A^3; x sqrt(F / 16) at F = 64.
 Also: the GPU's p = 8 result is bitwise equal to its p = 1 result.
 
 These tests are slow (tens of seconds of reference CPU time each)."""
@@ -27,7 +27,7 @@ import pytest
 
 from paper_2506_02023_b200 import graphmd as G
 from tests import systems as S
-from tests.conftest import TOL_E, TOL_EA, TOL_F, TOL_FREL, TOL_S
+from tests.conftest import SURVEY_TOL, TOL_E, TOL_EA, TOL_F, TOL_FREL, TOL_S
 from tests.test_gpu_partition import assert_parts_equal
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -133,5 +133,10 @@ def test_tolerance_calibration(oracle_ref):
     gpu = compare_outputs(G.forward_distributed(gpu_create(s, 1), prm), exact, n)
     tol = dict(dE_i=TOL_EA, dE_N=TOL_E, dF=TOL_F, dS=TOL_S)
     for k in tol:
-        print(f"{k}: fp32-input floor {floor[k]:.2e}  GPU {gpu[k]:.2e}  tolerance {tol[k]:.0e}")
-        assert floor[k] <= tol[k] and gpu[k] <= tol[k]
+        print(f"{k}: fp32-input floor {floor[k]:.2e}  GPU {gpu[k]:.2e}  SURVEY proposal "
+              f"{SURVEY_TOL[k]:.0e}  tolerance {tol[k]:.0e}")
+    for k in tol:
+        # the GPU is never worse than the fp32-input floor or the proposal,
+        # and the stated tolerance is no looser than needed to cover the floor
+        assert gpu[k] <= max(floor[k], SURVEY_TOL[k]) and gpu[k] <= tol[k]
+        assert tol[k] <= max(2.0 * floor[k], 2.0 * SURVEY_TOL[k])
