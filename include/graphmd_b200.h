@@ -125,6 +125,12 @@ int gmd_num_partitions(const gmd_handle* h, int* p);
 /* AtomGraph in canonical order; off = image_offset (n x 3 int32) */
 int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, double* dist,
                   double* vec);
+/* ensure_periodic (system.cpp:242-270) on the device: non-periodic axes padded
+ * to extent + 2 cutoff, positions shifted by cutoff - lo */
+int gmd_util_ensure_periodic(gmd_handle* h, int64_t n, const double* pos, const double lattice[9],
+                             const uint8_t pbc[3], double cutoff, double* out_pos, double* out_lat);
+/* canonical CSR by destination: row (n + 1), src (ne), int32 */
+int gmd_get_csr(gmd_handle* h, int32_t* row, int32_t* src);
 /* system after ensure_periodic (positions n x 3, lattice 3 x 3) */
 int gmd_get_system(gmd_handle* h, double* pos, double* lattice);
 /* PartitionRule: axis and p + 1 boundaries */
@@ -148,6 +154,46 @@ int gmd_get_num_bonds(gmd_handle* h, int64_t* nb);
 int gmd_get_bonds(gmd_handle* h, int64_t* edge_of_bond, int32_t* bond_owner);
 int gmd_get_num_line_edges(gmd_handle* h, int part, int64_t* count);
 int gmd_get_line_edges(gmd_handle* h, int part, int64_t* pairs /* (local e, local e') */);
+
+/* ---- free builders (device-backed) ---------------------------------------
+ * The reference's public lower-level builders on the GPU; every view getter
+ * above then reads the handle.  Replaces, one for one:
+ *   choose_partition_rule  partitioner.hpp:91-92 / partitioner.cpp:46-91
+ *   fractional_along_axis, which_partition(node)  partitioner.hpp:94-99
+ *   assign_to_partitions, build_atom_partitions  partitioner.hpp:101-109
+ *   build_two_hop_closure  linegraph.hpp:58-59
+ *   build_edge_tables (per-partition table membership)  linegraph.hpp:61-64
+ *   build_line_graph_partitions, serial_line_graph  linegraph.hpp:66-73
+ *   brute_force_line_graph  linegraph.hpp:75-78
+ *   brute_force_neighbor_list  neighborlist.hpp:40-42 */
+/* choose_partition_rule: axis = longest lattice row; p + 1 boundaries
+ * (quantile walls by a device radix select, or equal widths) */
+int gmd_partition_rule(gmd_handle* h, int64_t n, const double* pos, const double lattice[9], int p,
+                       int equal_width, int* axis, double* boundaries);
+/* wrapped fractional coordinate along `axis` (fracs, may be NULL) and
+ * which_partition of every atom (owner, may be NULL; needs the rule) */
+int gmd_assign_owners(gmd_handle* h, int64_t n, const double* pos, const double lattice[9], int axis,
+                      int p, const double* boundaries, double* fracs, int32_t* owner);
+/* partitions (+ bonds / line graph when r3 > 0) of a caller-supplied graph in
+ * canonical dst-major order; owners from `owner` if non-NULL, else from
+ * positions + rule.  flags: GMD_ALLOW_NARROW.  The handle then serves the
+ * partition / bond / line-graph getters and the feature API (no forward). */
+int gmd_build_partitions(gmd_handle* h, int64_t n, const double* pos, const double lattice[9],
+                         int64_t ne, const int64_t* src, const int64_t* dst, const int32_t* off,
+                         const double* dist, double cutoff, double r3, double tau, int axis, int p,
+                         const double* boundaries, const int32_t* owner, uint32_t flags);
+/* two-hop closure of partition `part`: ascending node ids (ids may be NULL) */
+int gmd_get_closure(gmd_handle* h, int part, int64_t* count, int64_t* ids);
+/* edge-table membership: bit i of mask[b] = bond b in partition i's table */
+int gmd_get_bond_tables(gmd_handle* h, uint64_t* mask);
+/* brute-force line graph of the handle's bonds: sorted (edge e, edge e') */
+int gmd_brute_force_line_graph(gmd_handle* h, int64_t* count, int64_t* pairs);
+/* brute-force radius graph (N <= 5000), canonical order; with all output
+ * pointers NULL only *ne is returned */
+int gmd_brute_force_neighbor_list(gmd_handle* h, int64_t n, const double* pos,
+                                  const double lattice[9], const uint8_t pbc[3], double cutoff,
+                                  int64_t* ne, int64_t* src, int64_t* dst, int32_t* off,
+                                  double* dist, double* vec);
 
 /* ---- Distributed feature API (engine.hpp:74-129) -------------------------
  * Per-partition blocks live in ONE device buffer: partition i's block starts

@@ -20,10 +20,12 @@
 #include <functional>
 #include <memory>
 #include <optional>
+#include <random>
 #include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <unordered_map>
 #include <vector>
 
 #include "../graphmd_b200.h"
@@ -76,6 +78,20 @@ struct Mat3 {
         m.rows = {Vec3{1, 0, 0}, Vec3{0, 1, 0}, Vec3{0, 0, 1}};
         return m;
     }
+    // system.cpp:55-70 operand order (columns of the inverse are (b x c) / d, ...)
+    Mat3 inverse() const {
+        const double d = det();
+        if (std::abs(d) < 1e-10) throw Error("lattice is singular (|det| < 1e-10)");
+        const Vec3 bc = rows[1].cross(rows[2]) / d, ca = rows[2].cross(rows[0]) / d,
+                   ab = rows[0].cross(rows[1]) / d;
+        Mat3 inv;
+        inv.rows = {Vec3{bc.x, ca.x, ab.x}, Vec3{bc.y, ca.y, ab.y}, Vec3{bc.z, ca.z, ab.z}};
+        return inv;
+    }
+};
+
+struct FractionalCoords {
+    std::vector<Vec3> coords;
 };
 
 struct AtomicSystem {
@@ -90,7 +106,63 @@ struct AtomicSystem {
         if (any_pbc() && std::abs(lattice.det()) < 1e-10)
             throw Error("periodic system requires an invertible lattice");
     }
+    FractionalCoords fractional() const {  // f = r L^-1 (system.cpp:79-85)
+        const Mat3 inv = lattice.inverse();
+        FractionalCoords f;
+        f.coords.reserve(positions.size());
+        for (const Vec3& r : positions) f.coords.push_back(inv.rowvec_mul(r));
+        return f;
+    }
+    double perpendicular_width(int axis) const {  // |det| / |b x c| (system.cpp:87-93)
+        const double area = lattice[(axis + 1) % 3].cross(lattice[(axis + 2) % 3]).norm();
+        if (area <= 0.0) throw Error("degenerate cell");
+        return std::abs(lattice.det()) / area;
+    }
 };
+
+// Rng (system.hpp:121-149): mt19937_64, uniform = (u64 >> 11) 2^-53,
+// Box-Muller normals with a cached spare -- the reference's streams exactly
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : gen_(seed) {}
+    double uniform() { return static_cast<double>(gen_() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    double normal() {
+        if (have_spare_) {
+            have_spare_ = false;
+            return spare_;
+        }
+        double u1 = 0.0;
+        while (u1 == 0.0) u1 = uniform();
+        const double u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1)), a = 2.0 * M_PI * u2;
+        spare_ = r * std::sin(a);
+        have_spare_ = true;
+        return r * std::cos(a);
+    }
+    std::uint64_t next_u64() { return gen_(); }
+
+private:
+    std::mt19937_64 gen_;
+    bool have_spare_ = false;
+    double spare_ = 0.0;
+};
+
+// wrap_positions (system.cpp:215-229): positions folded into the cell
+inline AtomicSystem wrap_positions(const AtomicSystem& system) {
+    system.validate();
+    AtomicSystem out = system;
+    const FractionalCoords f = system.fractional();
+    for (std::size_t i = 0; i < out.size(); ++i) {
+        Vec3 fr = f.coords[i];
+        for (int k = 0; k < 3; ++k) {
+            fr[k] -= std::floor(fr[k]);
+            if (fr[k] >= 1.0) fr[k] = 0.0;
+        }
+        out.positions[i] = out.lattice.rowvec_mul(fr);
+    }
+    return out;
+}
 
 // make_supercell + random_perturb on the library's host RNG (system.cpp:188-240)
 inline AtomicSystem make_supercell(const AtomicSystem& s, const std::array<int, 3>& reps,
@@ -272,9 +344,10 @@ struct Span {
     std::int64_t size() const { return end - begin; }
 };
 
-struct SpanLayout {  // partitioner.hpp:45-63 (global_to_local as a sorted probe)
+struct SpanLayout {  // partitioner.hpp:45-63
     std::vector<std::int64_t> node_array;
     std::vector<std::int64_t> markers;
+    std::unordered_map<std::int64_t, std::int64_t> global_to_local;  // canonical (first) row
     std::vector<std::pair<std::int64_t, std::int64_t>> duplicates;
     int p = 1;
     Span pure_span() const { return {markers[0], markers[1]}; }
@@ -283,9 +356,8 @@ struct SpanLayout {  // partitioner.hpp:45-63 (global_to_local as a sorted probe
     std::int64_t owned_end() const { return markers[1 + p]; }
     std::int64_t size() const { return (std::int64_t)node_array.size(); }
     std::int64_t local_of(std::int64_t g) const {
-        for (std::size_t r = 0; r < node_array.size(); ++r)
-            if (node_array[r] == g) return (std::int64_t)r;
-        return -1;
+        auto it = global_to_local.find(g);
+        return it == global_to_local.end() ? -1 : it->second;
     }
 };
 
@@ -302,8 +374,9 @@ struct PartitionedAtomGraph {
     int p = 1;
 };
 
-struct BondSet {
+struct BondSet {  // linegraph.hpp:15-24
     std::vector<std::int64_t> edge_of_bond, bond_of_edge;
+    std::vector<std::vector<std::int64_t>> by_src, by_dst;  // atom -> bond ids (ascending)
     double r = 0.0, tau = 0.0;
     std::size_t size() const { return edge_of_bond.size(); }
 };
@@ -311,6 +384,15 @@ struct BondSet {
 struct LineGraphPartition {
     SpanLayout layout;
     std::vector<std::pair<std::int64_t, std::int64_t>> line_edges;
+};
+
+// linegraph.hpp:31-37: per-partition tables (node -> bond ids with both ends
+// in the partition's two-hop closure), bond owners and bond buckets
+struct EdgeTables {
+    BondSet bonds;
+    std::vector<std::unordered_map<std::int64_t, std::vector<std::int64_t>>> per_partition;
+    std::vector<int> bond_owner;
+    Buckets bond_buckets;
 };
 
 struct PartitionedLineGraph {
@@ -330,6 +412,133 @@ struct PartitionedLineGraph {
                     << parts[i].layout.node_array[lep] << "\n";
     }
 };
+
+namespace detail {
+// ---- views of a built handle (gmd_build or gmd_build_partitions) ----------
+inline SpanLayout read_layout(gmd_handle* h, int p, int i, int bonds) {
+    SpanLayout L;
+    L.p = p;
+    int64_t sz = 0, nd = 0;
+    check(h, gmd_get_layout_size(h, i, bonds, &sz));
+    L.node_array.resize(sz);
+    L.markers.resize(2 + 2 * p);
+    check(h, gmd_get_layout(h, i, bonds, L.node_array.data(), L.markers.data()));
+    check(h, gmd_get_num_duplicates(h, i, bonds, &nd));
+    std::vector<int64_t> d(2 * nd);
+    check(h, gmd_get_duplicates(h, i, bonds, d.data()));
+    for (int64_t k = 0; k < nd; ++k) L.duplicates.emplace_back(d[2 * k], d[2 * k + 1]);
+    L.global_to_local.reserve(L.node_array.size() * 2);
+    for (std::size_t r = 0; r < L.node_array.size(); ++r) L.global_to_local.emplace(L.node_array[r], (std::int64_t)r);
+    return L;
+}
+
+// PURE / TO / FROM lists are the layout's spans (build_span_layout order)
+inline Buckets buckets_of(const std::vector<const SpanLayout*>& lays) {
+    const int p = (int)lays.size();
+    Buckets b;
+    b.pure.resize(p);
+    b.to.assign(p, std::vector<std::vector<std::int64_t>>(p));
+    b.from.assign(p, std::vector<std::vector<std::int64_t>>(p));
+    for (int i = 0; i < p; ++i) {
+        const SpanLayout& L = *lays[i];
+        Span s = L.pure_span();
+        b.pure[i].assign(L.node_array.begin() + s.begin, L.node_array.begin() + s.end);
+        for (int j = 0; j < p; ++j) {
+            Span t = L.to_span(j);
+            b.to[i][j].assign(L.node_array.begin() + t.begin, L.node_array.begin() + t.end);
+        }
+    }
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j) b.from[j][i] = b.to[i][j];
+    return b;
+}
+
+inline PartitionedAtomGraph read_atom_parts(gmd_handle* h, int p) {
+    PartitionedAtomGraph pg;
+    pg.p = p;
+    pg.rule.p = p;
+    pg.rule.boundaries.resize(p + 1);
+    check(h, gmd_get_rule(h, &pg.rule.axis, pg.rule.boundaries.data()));
+    int64_t n = 0;
+    gmd_num_nodes(h, &n);
+    std::vector<int32_t> own(n);
+    check(h, gmd_get_owner(h, own.data()));
+    pg.owner.assign(own.begin(), own.end());
+    std::vector<const SpanLayout*> lays;
+    pg.parts.reserve(p);
+    for (int i = 0; i < p; ++i) {
+        AtomPartition ap;
+        ap.layout = read_layout(h, p, i, 0);
+        int64_t c = 0;
+        check(h, gmd_get_num_owned_edges(h, i, &c));
+        ap.owned_edges.resize(c);
+        ap.local_src.resize(c);
+        ap.local_dst.resize(c);
+        check(h, gmd_get_owned_edges(h, i, ap.owned_edges.data(), ap.local_src.data(), ap.local_dst.data()));
+        check(h, gmd_get_num_border_edges(h, i, &c));
+        ap.border_edge_list.resize(c);
+        check(h, gmd_get_border_edges(h, i, ap.border_edge_list.data()));
+        pg.parts.push_back(std::move(ap));
+    }
+    for (const auto& ap : pg.parts) lays.push_back(&ap.layout);
+    pg.buckets = buckets_of(lays);
+    return pg;
+}
+
+// BondSet with by_src / by_dst lists (linegraph.cpp:25-43 order: ascending bond id)
+inline BondSet read_bonds(gmd_handle* h, double r, double tau, std::vector<int>* owner) {
+    BondSet bs;
+    int64_t nb = 0, ne = 0, n = 0;
+    check(h, gmd_get_num_bonds(h, &nb));
+    gmd_num_edges(h, &ne);
+    gmd_num_nodes(h, &n);
+    bs.edge_of_bond.resize(nb);
+    std::vector<int32_t> own(nb);
+    check(h, gmd_get_bonds(h, bs.edge_of_bond.data(), own.data()));
+    if (owner) owner->assign(own.begin(), own.end());
+    bs.bond_of_edge.assign(ne, -1);
+    for (int64_t b = 0; b < nb; ++b) bs.bond_of_edge[bs.edge_of_bond[b]] = b;
+    bs.r = r;
+    bs.tau = tau;
+    bs.by_src.assign(n, {});
+    bs.by_dst.assign(n, {});
+    if (nb) {
+        std::vector<int32_t> row(n + 1), src(ne);
+        check(h, gmd_get_csr(h, row.data(), src.data()));
+        std::vector<int32_t> dst_of(ne);
+        for (int64_t v = 0; v < n; ++v)
+            for (int32_t e = row[v]; e < row[v + 1]; ++e) dst_of[e] = (int32_t)v;
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t e = bs.edge_of_bond[b];
+            bs.by_src[src[e]].push_back(b);
+            bs.by_dst[dst_of[e]].push_back(b);
+        }
+    }
+    return bs;
+}
+
+inline PartitionedLineGraph read_line_parts(gmd_handle* h, int p, double r, double tau) {
+    PartitionedLineGraph lg;
+    lg.p = p;
+    lg.bonds = read_bonds(h, r, tau, &lg.bond_owner);
+    std::vector<const SpanLayout*> lays;
+    lg.parts.reserve(p);
+    for (int i = 0; i < p; ++i) {
+        LineGraphPartition part;
+        part.layout = read_layout(h, p, i, 1);
+        int64_t c = 0;
+        check(h, gmd_get_num_line_edges(h, i, &c));
+        std::vector<int64_t> pairs(2 * c);
+        check(h, gmd_get_line_edges(h, i, pairs.data()));
+        part.line_edges.resize(c);
+        for (int64_t k = 0; k < c; ++k) part.line_edges[k] = {pairs[2 * k], pairs[2 * k + 1]};
+        lg.parts.push_back(std::move(part));
+    }
+    for (const auto& pt : lg.parts) lays.push_back(&pt.layout);
+    lg.bond_buckets = buckets_of(lays);
+    return lg;
+}
+}  // namespace detail
 
 namespace detail {
 // the reference's JSON layout with dump(2): sorted keys, two-space indent,
@@ -496,68 +705,15 @@ public:
     }
 
     const PartitionedAtomGraph& atom_parts() const {
-        if (!parts_) {
-            auto pg = std::make_unique<PartitionedAtomGraph>();
-            pg->p = p_;
-            pg->rule.p = p_;
-            pg->rule.boundaries.resize(p_ + 1);
-            detail::check(h_.get(), gmd_get_rule(h_.get(), &pg->rule.axis, pg->rule.boundaries.data()));
-            int64_t n = 0;
-            gmd_num_nodes(h_.get(), &n);
-            std::vector<int32_t> own(n);
-            detail::check(h_.get(), gmd_get_owner(h_.get(), own.data()));
-            pg->owner.assign(own.begin(), own.end());
-            for (int i = 0; i < p_; ++i) {
-                AtomPartition ap;
-                ap.layout = layout(i, 0);
-                int64_t c = 0;
-                detail::check(h_.get(), gmd_get_num_owned_edges(h_.get(), i, &c));
-                ap.owned_edges.resize(c);
-                ap.local_src.resize(c);
-                ap.local_dst.resize(c);
-                detail::check(h_.get(), gmd_get_owned_edges(h_.get(), i, ap.owned_edges.data(),
-                                                            ap.local_src.data(), ap.local_dst.data()));
-                detail::check(h_.get(), gmd_get_num_border_edges(h_.get(), i, &c));
-                ap.border_edge_list.resize(c);
-                detail::check(h_.get(), gmd_get_border_edges(h_.get(), i, ap.border_edge_list.data()));
-                pg->parts.push_back(std::move(ap));
-            }
-            pg->buckets = buckets_of(pg->parts, [](const AtomPartition& a) -> const SpanLayout& { return a.layout; });
-            parts_ = std::move(pg);
-        }
+        if (!parts_) parts_ = std::make_unique<PartitionedAtomGraph>(detail::read_atom_parts(h_.get(), p_));
         return *parts_;
     }
 
     const PartitionedLineGraph& line_parts() const {
         if (!has_line_graph()) throw Error("no line graph was built");
-        if (!lines_) {
-            auto lg = std::make_unique<PartitionedLineGraph>();
-            lg->p = p_;
-            int64_t nb = 0, ne = 0;
-            detail::check(h_.get(), gmd_get_num_bonds(h_.get(), &nb));
-            gmd_num_edges(h_.get(), &ne);
-            lg->bonds.edge_of_bond.resize(nb);
-            std::vector<int32_t> own(nb);
-            detail::check(h_.get(), gmd_get_bonds(h_.get(), lg->bonds.edge_of_bond.data(), own.data()));
-            lg->bond_owner.assign(own.begin(), own.end());
-            lg->bonds.bond_of_edge.assign(ne, -1);
-            for (int64_t b = 0; b < nb; ++b) lg->bonds.bond_of_edge[lg->bonds.edge_of_bond[b]] = b;
-            lg->bonds.r = r3_ ? *r3_ : 0.0;
-            lg->bonds.tau = tau_;
-            for (int i = 0; i < p_; ++i) {
-                LineGraphPartition part;
-                part.layout = layout(i, 1);
-                int64_t c = 0;
-                detail::check(h_.get(), gmd_get_num_line_edges(h_.get(), i, &c));
-                std::vector<int64_t> pairs(2 * c);
-                detail::check(h_.get(), gmd_get_line_edges(h_.get(), i, pairs.data()));
-                part.line_edges.resize(c);
-                for (int64_t k = 0; k < c; ++k) part.line_edges[k] = {pairs[2 * k], pairs[2 * k + 1]};
-                lg->parts.push_back(std::move(part));
-            }
-            lg->bond_buckets = buckets_of(lg->parts, [](const LineGraphPartition& a) -> const SpanLayout& { return a.layout; });
-            lines_ = std::move(lg);
-        }
+        if (!lines_)
+            lines_ = std::make_unique<PartitionedLineGraph>(
+                detail::read_line_parts(h_.get(), p_, r3_ ? *r3_ : 0.0, tau_));
         return *lines_;
     }
 
@@ -666,39 +822,6 @@ private:
     mutable std::unique_ptr<PartitionedAtomGraph> parts_;
     mutable std::unique_ptr<PartitionedLineGraph> lines_;
 
-    SpanLayout layout(int i, int bonds) const {
-        SpanLayout L;
-        L.p = p_;
-        int64_t sz = 0, nd = 0;
-        detail::check(h_.get(), gmd_get_layout_size(h_.get(), i, bonds, &sz));
-        L.node_array.resize(sz);
-        L.markers.resize(2 + 2 * p_);
-        detail::check(h_.get(), gmd_get_layout(h_.get(), i, bonds, L.node_array.data(), L.markers.data()));
-        detail::check(h_.get(), gmd_get_num_duplicates(h_.get(), i, bonds, &nd));
-        std::vector<int64_t> d(2 * nd);
-        detail::check(h_.get(), gmd_get_duplicates(h_.get(), i, bonds, d.data()));
-        for (int64_t k = 0; k < nd; ++k) L.duplicates.emplace_back(d[2 * k], d[2 * k + 1]);
-        return L;
-    }
-    template <typename P, typename F>
-    Buckets buckets_of(const std::vector<P>& parts, F lay) const {
-        Buckets b;
-        b.pure.resize(p_);
-        b.to.assign(p_, std::vector<std::vector<std::int64_t>>(p_));
-        b.from.assign(p_, std::vector<std::vector<std::int64_t>>(p_));
-        for (int i = 0; i < p_; ++i) {
-            const SpanLayout& L = lay(parts[i]);
-            Span s = L.pure_span();
-            b.pure[i].assign(L.node_array.begin() + s.begin, L.node_array.begin() + s.end);
-            for (int j = 0; j < p_; ++j) {
-                Span t = L.to_span(j);
-                b.to[i][j].assign(L.node_array.begin() + t.begin, L.node_array.begin() + t.end);
-            }
-        }
-        for (int i = 0; i < p_; ++i)
-            for (int j = 0; j < p_; ++j) b.from[j][i] = b.to[i][j];
-        return b;
-    }
     std::int64_t flat_rows(int bonds) const {
         int64_t r = 0;
         detail::check(h_.get(), gmd_block_rows(h_.get(), bonds, &r));
@@ -924,6 +1047,362 @@ inline PotentialOutput forward_serial(const AtomicSystem& system, const ToyPoten
 // neighborlist.hpp:37-38 on the GPU
 inline AtomGraph build_neighbor_list(const AtomicSystem& system, double cutoff, int n_threads = 0) {
     return Distributed::create_distributed(system, cutoff, std::nullopt, 1, n_threads, true).graph();
+}
+
+// ---- free builders (partitioner.hpp:66-109, linegraph.hpp:26-78,
+// neighborlist.hpp:40-42, potential.hpp:62-69), device-backed through the
+// gmd_build_partitions / gmd_partition_rule / brute-force entry points ----
+namespace detail {
+using Handle = std::shared_ptr<gmd_handle>;
+inline Handle make_handle(int device = 0) {
+    gmd_handle* raw = nullptr;
+    if (gmd_create(device, &raw) != GMD_OK) throw Error(gmd_last_error(nullptr));
+    return Handle(raw, [](gmd_handle* x) { gmd_destroy(x); });
+}
+inline void flat_system(const AtomicSystem& s, std::vector<double>& pos, std::vector<double>& lat) {
+    pos.resize(3 * s.size());
+    lat.resize(9);
+    for (std::size_t i = 0; i < s.size(); ++i)
+        for (int k = 0; k < 3; ++k) pos[3 * i + k] = s.positions[i][k];
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) lat[3 * r + k] = s.lattice[r][k];
+}
+// a caller's AtomGraph as the partitions of `owner` (or of system + rule)
+inline Handle partitions_of(const AtomGraph& g, const AtomicSystem* sys, const PartitionRule& rule,
+                            const std::vector<int>* owner, double r3, double tau, bool allow_narrow) {
+    Handle h = make_handle();
+    const std::size_t ne = g.num_edges();
+    std::vector<int32_t> off(3 * ne);
+    for (std::size_t e = 0; e < ne; ++e)
+        for (int k = 0; k < 3; ++k) off[3 * e + k] = g.image_offset[e][k];
+    std::vector<double> pos, lat;
+    if (sys) flat_system(*sys, pos, lat);
+    std::vector<int32_t> own;
+    if (owner) own.assign(owner->begin(), owner->end());
+    if (owner && (std::int64_t)own.size() != g.num_nodes) throw Error("owner table does not match the graph");
+    if (sys && (std::int64_t)sys->size() != g.num_nodes) throw Error("system does not match the graph");
+    check(h.get(), gmd_build_partitions(h.get(), g.num_nodes, sys ? pos.data() : nullptr,
+                                        sys ? lat.data() : nullptr, (int64_t)ne, g.src.data(),
+                                        g.dst.data(), off.data(), g.distance.data(), g.cutoff, r3, tau,
+                                        rule.axis, rule.p, rule.boundaries.data(),
+                                        owner ? own.data() : nullptr, allow_narrow ? GMD_ALLOW_NARROW : 0u));
+    return h;
+}
+inline void check_rule(const PartitionRule& rule) {
+    if (rule.p < 1 || (int)rule.boundaries.size() != rule.p + 1)
+        throw Error("partition rule needs p + 1 boundaries");
+}
+}  // namespace detail
+
+// ensure_periodic (system.cpp:242-270) on the device
+inline AtomicSystem ensure_periodic(const AtomicSystem& system, double cutoff) {
+    if (system.pbc[0] && system.pbc[1] && system.pbc[2]) return system;
+    auto h = detail::make_handle();
+    std::vector<double> pos, lat, opos(3 * system.size()), olat(9);
+    detail::flat_system(system, pos, lat);
+    const uint8_t pbc[3] = {system.pbc[0], system.pbc[1], system.pbc[2]};
+    detail::check(h.get(), gmd_util_ensure_periodic(h.get(), (int64_t)system.size(), pos.data(), lat.data(),
+                                                    pbc, cutoff, opos.data(), olat.data()));
+    AtomicSystem out = system;
+    for (std::size_t i = 0; i < out.size(); ++i) out.positions[i] = {opos[3 * i], opos[3 * i + 1], opos[3 * i + 2]};
+    for (int r = 0; r < 3; ++r) out.lattice[r] = {olat[3 * r], olat[3 * r + 1], olat[3 * r + 2]};
+    out.pbc = {true, true, true};
+    out.validate();
+    return out;
+}
+
+inline int symbol_to_z(const std::string& symbol) {  // system.cpp:272-277
+    for (int z = 1; z <= 118; ++z)
+        if (symbol == detail::element_symbols()[z]) return z;
+    throw Error("unknown element symbol '" + symbol + "'");
+}
+
+// choose_partition_rule (partitioner.cpp:46-91): quantile walls by a device
+// radix select over the wrapped fractions
+inline PartitionRule choose_partition_rule(const AtomicSystem& system, int p,
+                                           BoundaryMode mode = BoundaryMode::kQuantile) {
+    if (p < 1) throw Error("partition count must be >= 1");
+    if (p > 64) throw Error("partition count limited to 64");
+    if (static_cast<std::size_t>(p) > system.size()) throw Error("more partitions than atoms");
+    system.validate();
+    auto h = detail::make_handle();
+    std::vector<double> pos, lat;
+    detail::flat_system(system, pos, lat);
+    PartitionRule rule;
+    rule.p = p;
+    rule.boundaries.resize(p + 1);
+    detail::check(h.get(), gmd_partition_rule(h.get(), (int64_t)system.size(), pos.data(), lat.data(), p,
+                                              mode == BoundaryMode::kEqualWidth ? 1 : 0, &rule.axis,
+                                              rule.boundaries.data()));
+    return rule;
+}
+
+// which_partition (partitioner.cpp:93-108): half-open slabs, ties to the right
+inline int which_partition(const PartitionRule& rule, double frac) {
+    if (frac >= 1.0) return rule.p - 1;
+    auto it = std::upper_bound(rule.boundaries.begin() + 1, rule.boundaries.end() - 1, frac);
+    return static_cast<int>(it - rule.boundaries.begin()) - 1;
+}
+
+// fractional_along_axis (partitioner.cpp:38-44) on the device
+inline std::vector<double> fractional_along_axis(const AtomicSystem& system, int axis) {
+    auto h = detail::make_handle();
+    std::vector<double> pos, lat, out(system.size());
+    detail::flat_system(system, pos, lat);
+    detail::check(h.get(), gmd_assign_owners(h.get(), (int64_t)system.size(), pos.data(), lat.data(), axis,
+                                             0, nullptr, out.data(), nullptr));
+    return out;
+}
+
+inline int which_partition(std::int64_t node, const AtomicSystem& system, const PartitionRule& rule) {
+    if (node < 0 || static_cast<std::size_t>(node) >= system.size()) throw Error("node id out of range");
+    return which_partition(rule, fractional_along_axis(system, rule.axis)[node]);
+}
+
+// build_span_layout (partitioner.cpp:153-180): [PURE | TO... | FROM...] of
+// caller-supplied buckets (first occurrence is canonical)
+inline SpanLayout build_span_layout(const Buckets& buckets, int partition) {
+    const int p = static_cast<int>(buckets.pure.size());
+    SpanLayout L;
+    L.p = p;
+    L.markers.assign(2 + 2 * p, 0);
+    auto append = [&](const std::vector<std::int64_t>& ids) {
+        for (std::int64_t g : ids) {
+            const std::int64_t r = static_cast<std::int64_t>(L.node_array.size());
+            L.node_array.push_back(g);
+            auto ins = L.global_to_local.emplace(g, r);
+            if (!ins.second) L.duplicates.emplace_back(ins.first->second, r);
+        }
+    };
+    append(buckets.pure[partition]);
+    L.markers[1] = L.size();
+    for (int j = 0; j < p; ++j) {
+        append(buckets.to[partition][j]);
+        L.markers[2 + j] = L.size();
+    }
+    for (int j = 0; j < p; ++j) {
+        append(buckets.from[partition][j]);
+        L.markers[2 + p + j] = L.size();
+    }
+    return L;
+}
+
+// build_atom_partitions / assign_to_partitions (partitioner.cpp:110-218) of
+// the caller's graph: owners, requirement masks, stable compaction into span
+// layouts and edge ownership all run on the GPU
+inline PartitionedAtomGraph build_atom_partitions(const AtomGraph& graph, const AtomicSystem& system,
+                                                  const PartitionRule& rule, bool allow_narrow = false) {
+    detail::check_rule(rule);
+    auto h = detail::partitions_of(graph, &system, rule, nullptr, 0.0, 0.0, allow_narrow);
+    PartitionedAtomGraph out = detail::read_atom_parts(h.get(), rule.p);
+    out.rule = rule;
+    return out;
+}
+
+inline Buckets assign_to_partitions(const AtomGraph& graph, const AtomicSystem& system,
+                                    const PartitionRule& rule, bool allow_narrow = false) {
+    return build_atom_partitions(graph, system, rule, allow_narrow).buckets;
+}
+
+// collect_bonds (linegraph.cpp:25-43): edges with d <= r + tau, on the device
+inline BondSet collect_bonds(const AtomGraph& graph, double r, double tau) {
+    if (r > graph.cutoff) throw Error("three-body range cannot exceed the atom graph cutoff");
+    if (tau < 0.0) throw Error("tolerance tau must be >= 0");
+    PartitionRule one;
+    one.boundaries = {0.0, 1.0};
+    const std::vector<int> zero(graph.num_nodes, 0);
+    if (r <= 0.0) {  // no bond can pass d <= r + tau with d > 0 ... unless tau > 0
+        BondSet b;
+        b.r = r;
+        b.tau = tau;
+        b.bond_of_edge.assign(graph.num_edges(), -1);
+        b.by_src.assign(graph.num_nodes, {});
+        b.by_dst.assign(graph.num_nodes, {});
+        if (r + tau <= 0.0) return b;
+    }
+    auto h = detail::partitions_of(graph, nullptr, one, &zero, r > 0.0 ? r : 1e-300, r > 0.0 ? tau : r + tau - 1e-300, true);
+    BondSet b = detail::read_bonds(h.get(), r, tau, nullptr);
+    return b;
+}
+
+// build_two_hop_closure (linegraph.cpp:45-65): u64 partition masks per node,
+// two gather hops along the CSR on the device
+inline std::vector<std::vector<std::int64_t>> build_two_hop_closure(const PartitionedAtomGraph& atom_parts,
+                                                                    const AtomGraph& graph) {
+    auto h = detail::partitions_of(graph, nullptr, atom_parts.rule, &atom_parts.owner, 0.0, 0.0, true);
+    std::vector<std::vector<std::int64_t>> out(atom_parts.p);
+    for (int i = 0; i < atom_parts.p; ++i) {
+        int64_t c = 0;
+        detail::check(h.get(), gmd_get_closure(h.get(), i, &c, nullptr));
+        out[i].resize(c);
+        detail::check(h.get(), gmd_get_closure(h.get(), i, &c, out[i].data()));
+    }
+    return out;
+}
+
+// build_edge_tables (linegraph.cpp:67-122).  Table membership is computed on
+// the device from the two-hop closure; the closure passed in must be that
+// closure (the reference's only construction of it)
+inline EdgeTables build_edge_tables(const AtomGraph& graph,
+                                    const std::vector<std::vector<std::int64_t>>& closure,
+                                    const PartitionedAtomGraph& atom_parts, double r, double tau) {
+    if (r > graph.cutoff) throw Error("three-body range cannot exceed the atom graph cutoff");
+    if (tau < 0.0) throw Error("tolerance tau must be >= 0");
+    auto h = detail::partitions_of(graph, nullptr, atom_parts.rule, &atom_parts.owner, r, tau, true);
+    for (int i = 0; i < atom_parts.p; ++i) {
+        int64_t c = 0;
+        detail::check(h.get(), gmd_get_closure(h.get(), i, &c, nullptr));
+        std::vector<std::int64_t> mine(c);
+        detail::check(h.get(), gmd_get_closure(h.get(), i, &c, mine.data()));
+        std::vector<std::int64_t> given = i < (int)closure.size() ? closure[i] : std::vector<std::int64_t>{};
+        std::sort(given.begin(), given.end());
+        if (given != mine)
+            throw Error("build_edge_tables: closure is not build_two_hop_closure(atom_parts, graph)");
+    }
+    EdgeTables t;
+    PartitionedLineGraph lg = detail::read_line_parts(h.get(), atom_parts.p, r, tau);
+    t.bonds = std::move(lg.bonds);
+    t.bond_owner = std::move(lg.bond_owner);
+    t.bond_buckets = std::move(lg.bond_buckets);
+    std::vector<uint64_t> mask(t.bonds.size());
+    if (!mask.empty()) detail::check(h.get(), gmd_get_bond_tables(h.get(), mask.data()));
+    t.per_partition.resize(atom_parts.p);
+    for (std::size_t b = 0; b < t.bonds.size(); ++b) {
+        const std::int64_t v = graph.src[t.bonds.edge_of_bond[b]];
+        for (uint64_t m = mask[b]; m; m &= m - 1)
+            t.per_partition[__builtin_ctzll(m)][v].push_back((std::int64_t)b);
+    }
+    return t;
+}
+
+// build_line_graph_partitions (linegraph.cpp:124-171): bond layouts and the
+// (e', e)-ordered line edges per partition, on the device
+inline PartitionedLineGraph build_line_graph_partitions(const EdgeTables& tables, const AtomGraph& graph,
+                                                        const PartitionedAtomGraph& atom_parts) {
+    auto h = detail::partitions_of(graph, nullptr, atom_parts.rule, &atom_parts.owner, tables.bonds.r,
+                                   tables.bonds.tau, true);
+    PartitionedLineGraph lg = detail::read_line_parts(h.get(), atom_parts.p, tables.bonds.r, tables.bonds.tau);
+    if (lg.bonds.edge_of_bond != tables.bonds.edge_of_bond)
+        throw Error("build_line_graph_partitions: tables do not belong to this graph");
+    return lg;
+}
+
+// serial_line_graph (linegraph.cpp:183-199): the p = 1 line graph as sorted
+// global (edge e, edge e') pairs
+inline std::vector<std::pair<std::int64_t, std::int64_t>> serial_line_graph(const AtomGraph& graph, double r,
+                                                                             double tau) {
+    if (r > graph.cutoff) throw Error("three-body range cannot exceed the atom graph cutoff");
+    if (tau < 0.0) throw Error("tolerance tau must be >= 0");
+    PartitionRule one;
+    one.boundaries = {0.0, 1.0};
+    const std::vector<int> zero(graph.num_nodes, 0);
+    auto h = detail::partitions_of(graph, nullptr, one, &zero, r, tau, true);
+    PartitionedLineGraph lg = detail::read_line_parts(h.get(), 1, r, tau);
+    std::vector<std::pair<std::int64_t, std::int64_t>> out;
+    out.reserve(lg.parts[0].line_edges.size());
+    const auto& na = lg.parts[0].layout.node_array;
+    for (const auto& [le, lep] : lg.parts[0].line_edges)
+        out.emplace_back(lg.bonds.edge_of_bond[na[le]], lg.bonds.edge_of_bond[na[lep]]);
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+// brute_force_line_graph (linegraph.cpp:201-219): independent per-center
+// enumeration of (in-bond, out-bond) pairs on the device, N <= 2000
+inline std::vector<std::pair<std::int64_t, std::int64_t>> brute_force_line_graph(const AtomGraph& graph, double r,
+                                                                                  double tau) {
+    if (graph.num_nodes > 2000) throw Error("brute force guard: N > 2000");
+    if (r > graph.cutoff) throw Error("three-body range cannot exceed the atom graph cutoff");
+    if (tau < 0.0) throw Error("tolerance tau must be >= 0");
+    PartitionRule one;
+    one.boundaries = {0.0, 1.0};
+    const std::vector<int> zero(graph.num_nodes, 0);
+    auto h = detail::partitions_of(graph, nullptr, one, &zero, r, tau, true);
+    int64_t c = 0;
+    detail::check(h.get(), gmd_brute_force_line_graph(h.get(), &c, nullptr));
+    std::vector<int64_t> pairs(2 * c);
+    detail::check(h.get(), gmd_brute_force_line_graph(h.get(), &c, pairs.data()));
+    std::vector<std::pair<std::int64_t, std::int64_t>> out(c);
+    for (int64_t k = 0; k < c; ++k) out[k] = {pairs[2 * k], pairs[2 * k + 1]};
+    return out;
+}
+
+// brute_force_neighbor_list (neighborlist.cpp:199-239): every (dst, src,
+// image) of the span tested on the device with the reference's fp64
+// expressions, N <= 5000
+inline AtomGraph brute_force_neighbor_list(const AtomicSystem& system, double cutoff) {
+    if (cutoff <= 0.0) throw Error("cutoff must be positive");
+    if (system.size() == 0) throw Error("cannot build neighbor list for empty system");
+    if (system.size() > 5000) throw Error("brute force guard: N > 5000");
+    auto h = detail::make_handle();
+    std::vector<double> pos, lat;
+    detail::flat_system(system, pos, lat);
+    const uint8_t pbc[3] = {system.pbc[0], system.pbc[1], system.pbc[2]};
+    int64_t ne = 0;
+    const int64_t n = (int64_t)system.size();
+    detail::check(h.get(), gmd_brute_force_neighbor_list(h.get(), n, pos.data(), lat.data(), pbc, cutoff, &ne,
+                                                         nullptr, nullptr, nullptr, nullptr, nullptr));
+    AtomGraph g;
+    g.cutoff = cutoff;
+    g.num_nodes = n;
+    g.src.resize(ne);
+    g.dst.resize(ne);
+    g.distance.resize(ne);
+    std::vector<int32_t> off(3 * ne);
+    std::vector<double> vec(3 * ne);
+    detail::check(h.get(), gmd_brute_force_neighbor_list(h.get(), n, pos.data(), lat.data(), pbc, cutoff, &ne,
+                                                         g.src.data(), g.dst.data(), off.data(),
+                                                         g.distance.data(), vec.data()));
+    g.image_offset.resize(ne);
+    g.vector.resize(ne);
+    for (int64_t e = 0; e < ne; ++e) {
+        g.image_offset[e] = {off[3 * e], off[3 * e + 1], off[3 * e + 2]};
+        g.vector[e] = {vec[3 * e], vec[3 * e + 1], vec[3 * e + 2]};
+    }
+    return g;
+}
+
+// finite_difference_forces / _stress (potential.cpp:991-1037): central
+// differences of the GPU energy (forward_serial).  The energy is a sum of
+// fp32-computed per-atom terms, so the difference quotient carries
+// ~1e-6 eV / (2 eps) of rounding noise -- a check at fp32 tolerance, not the
+// reference's fp64 1e-6 eV/A
+inline std::vector<Vec3> finite_difference_forces(const AtomicSystem& system, const ToyPotentialParams& params,
+                                                  double eps) {
+    if (eps < 1e-6 || eps > 1e-2) throw Error("finite-difference step must lie in [1e-6, 1e-2] A");
+    std::vector<Vec3> forces(system.size(), Vec3{});
+    AtomicSystem probe = system;
+    for (std::size_t i = 0; i < system.size(); ++i)
+        for (int k = 0; k < 3; ++k) {
+            probe.positions[i][k] = system.positions[i][k] + eps;
+            const double ep = forward_serial(probe, params).energy;
+            probe.positions[i][k] = system.positions[i][k] - eps;
+            const double em = forward_serial(probe, params).energy;
+            probe.positions[i][k] = system.positions[i][k];
+            forces[i][k] = -(ep - em) / (2.0 * eps);
+        }
+    return forces;
+}
+
+inline Mat3 finite_difference_stress(const AtomicSystem& system, const ToyPotentialParams& params, double eps) {
+    if (eps <= 0.0 || eps > 1e-3) throw Error("strain step must lie in (0, 1e-3]");
+    const AtomicSystem base = ensure_periodic(system, params.r_atom);
+    const double volume = std::abs(base.lattice.det());
+    auto deform = [&](int a, int b, double strain) {  // x_a += strain x_b, positions and lattice
+        AtomicSystem s = base;
+        for (Vec3& r : s.positions) r[a] += strain * r[b];
+        for (int row = 0; row < 3; ++row) s.lattice[row][a] += strain * s.lattice[row][b];
+        return s;
+    };
+    Mat3 raw{}, out{};
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+            raw[a][b] = (forward_serial(deform(a, b, eps), params).energy -
+                         forward_serial(deform(a, b, -eps), params).energy) /
+                        (2.0 * eps * volume);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) out[a][b] = 0.5 * (raw[a][b] + raw[b][a]);
+    return out;
 }
 
 // ---- md.hpp (md.cpp:11-179): the caller of the hot path --------------------

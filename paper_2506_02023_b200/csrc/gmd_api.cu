@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/graphmd_b200.h"
+#include "gmd_builders.cuh"
 #include "gmd_comm.cuh"
 #include "gmd_common.cuh"
 #include "gmd_generic.cuh"
@@ -302,6 +303,11 @@ struct gmd_handle {
     // one rank per GPU: transport + this rank's plan
     std::unique_ptr<Transport> comm;
     int64_t n_own = 0;
+    // partitions of a caller-supplied graph (gmd_build_partitions): no positions
+    // or per-edge geometry on the device, so no model evaluation / graph export
+    bool graph_only = false;
+    DBuf cmask, bmask;  // two-hop closure masks per node / edge-table masks per bond
+    bool closure_ready = false;
     DBuf nodes, xsend, sendbuf;
     std::vector<int64_t> soff, scnt, roff, rcnt;
     // ... and its bond halo plan (three-body): rows nb .. nb + nb_halo of the
@@ -561,10 +567,46 @@ struct DrainSide {
     ~DrainSide() { cudaStreamSynchronize(side); }
 };
 
+// equal-count walls b_k = (s[c-1] + s[c]) / 2, c = n k / p, over the sorted
+// wrapped fractions (partitioner.cpp:77-85): radix select of the needed order
+// statistics on the device
+void quantile_walls(gmd_handle* h, const double* fw, int64_t n, int p, double* bounds) {
+    cudaStream_t s = h->stream;
+    std::vector<int64_t> ranks;
+    for (int k = 1; k < p; ++k) {
+        int64_t c = n * k / p;
+        if (c >= 1 && c < n) {
+            ranks.push_back(c - 1);
+            ranks.push_back(c);
+        }
+    }
+    std::sort(ranks.begin(), ranks.end());
+    ranks.erase(std::unique(ranks.begin(), ranks.end()), ranks.end());
+    std::vector<double> vals(ranks.size());
+    if (!ranks.empty()) {
+        void* ws = h->sel_ws.get<char>(select_ws_bytes((int)ranks.size()));
+        double* so = h->sel_out.get<double>(ranks.size());
+        { PROF("part_select"); launch_select(fw, n, ranks.data(), (int)ranks.size(), ws, so, s); }
+        GMD_CUDA(cudaMemcpyAsync(vals.data(), so, sizeof(double) * vals.size(),
+                                 cudaMemcpyDeviceToHost, s));
+        sync(h);
+    }
+    auto at = [&](int64_t r) {
+        size_t i = std::lower_bound(ranks.begin(), ranks.end(), r) - ranks.begin();
+        return vals[i];
+    };
+    for (int k = 1; k < p; ++k) {
+        int64_t c = n * k / p;
+        bounds[k] = (c >= 1 && c < n) ? 0.5 * (at(c - 1) + at(c)) : (double)k / p;
+    }
+}
+
 void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, const double* lat,
                 const uint8_t* pbc, double rc, double r3, double tau, int p, uint32_t flags) {
     cudaStream_t s = h->stream;
     h->built = false;
+    h->graph_only = false;
+    h->closure_ready = false;
     h->hc_ready = h->hcb_ready = false;
     h->ctab_ok = false;
     h->atoms.ready = h->bonds.ready = false;
@@ -687,33 +729,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         if (flags & GMD_EQUAL_WIDTH) {
             for (int k = 1; k < p; ++k) h->bounds[k] = (double)k / p;
         } else {
-            std::vector<int64_t> ranks;
-            for (int k = 1; k < p; ++k) {
-                int64_t c = n * k / p;
-                if (c >= 1 && c < n) {
-                    ranks.push_back(c - 1);
-                    ranks.push_back(c);
-                }
-            }
-            std::sort(ranks.begin(), ranks.end());
-            ranks.erase(std::unique(ranks.begin(), ranks.end()), ranks.end());
-            std::vector<double> vals(ranks.size());
-            if (!ranks.empty()) {
-                void* ws = h->sel_ws.get<char>(select_ws_bytes((int)ranks.size()));
-                double* so = h->sel_out.get<double>(ranks.size());
-                { PROF("part_select"); launch_select(b.fw_axis, n, ranks.data(), (int)ranks.size(), ws, so, s); }
-                GMD_CUDA(cudaMemcpyAsync(vals.data(), so, sizeof(double) * vals.size(),
-                                         cudaMemcpyDeviceToHost, s));
-                sync(h);
-            }
-            auto at = [&](int64_t r) {
-                size_t i = std::lower_bound(ranks.begin(), ranks.end(), r) - ranks.begin();
-                return vals[i];
-            };
-            for (int k = 1; k < p; ++k) {  // partitioner.cpp:80-85
-                int64_t c = n * k / p;
-                h->bounds[k] = (c >= 1 && c < n) ? 0.5 * (at(c - 1) + at(c)) : (double)k / p;
-            }
+            quantile_walls(h, b.fw_axis, n, p, h->bounds.data());
         }
         for (int k = 1; k <= p; ++k)
             if (h->bounds[k] <= h->bounds[k - 1])
@@ -1066,6 +1082,8 @@ void ensure_chunk_table(gmd_handle* h, const ConvArgs& a) {
 void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, double* stress,
                   double* timing, uint32_t flags) {
     need_built(h);
+    if (h->graph_only)
+        raise(kConfig, "this handle holds partitions of a caller-supplied graph (no model evaluation)");
     if (!h->params_set) raise(kConfig, "no parameters have been set on this handle");
     const bool tb = h->p_r3 > 0.0;
     if (tb && !h->has_lg)
@@ -1767,6 +1785,7 @@ int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, doubl
                   double* vec) {
     return run(h, [&] {
         need_built(h);
+        if (h->graph_only) raise(kConfig, "this handle holds partitions of a caller-supplied graph");
         const int64_t ne = h->ne;
         if (ne == 0) return;
         cudaStream_t s = h->stream;
@@ -1822,6 +1841,485 @@ int gmd_get_system(gmd_handle* h, double* pos, double* lattice) {
                                      h->stream));
         if (lattice) std::memcpy(lattice, h->lat, sizeof h->lat);
         sync(h);
+    });
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Free builder API (partitioner.hpp:66-106, linegraph.hpp:26-78): the same
+// partition / bond / line-graph kernels as gmd_build, on a caller's graph
+// ---------------------------------------------------------------------------
+// wrapped fractional coordinate along `axis` of every atom (fractional_along_axis,
+// partitioner.cpp:38-44) into h->fw; positions as given (no ensure_periodic)
+const double* wrapped_fracs(gmd_handle* h, int64_t n, const double* pos, const double* lat, int axis) {
+    cudaStream_t s = h->stream;
+    if (std::abs(det3(lat)) < 1e-10) raise(kConfig, "degenerate cell");
+    double* dpos = h->pos.get<double>(3 * n);
+    GMD_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    Geom g{};
+    std::memcpy(g.L, lat, sizeof g.L);
+    inverse3(lat, g.inv);
+    g.bins[0] = g.bins[1] = g.bins[2] = 1;
+    g.axis = axis;
+    NLBuffers b{};
+    b.pos = dpos;
+    b.cell = h->cell.get<int32_t>(3 * n);
+    b.fw_axis = h->fw.get<double>(n);
+    b.bin = h->bin.get<int32_t>(n);
+    b.bin_cnt = h->bin_cnt.get<int32_t>(1);
+    b.flags = h->flags.get<int32_t>(4);
+    GMD_CUDA(cudaMemsetAsync(b.bin_cnt, 0, 4, s));
+    GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
+    launch_wrap(g, n, b, s);
+    return b.fw_axis;
+}
+
+void check_rule_args(int64_t n, int p) {  // choose_partition_rule (partitioner.cpp:48-51)
+    if (p < 1) raise(kConfig, "partition count must be >= 1");
+    if (p > kMaxParts) raise(kConfig, "partition count limited to 64");
+    if ((int64_t)p > n) raise(kConfig, "more partitions than atoms");
+}
+
+int longest_axis(const double* lat) {  // partitioner.cpp:57-64
+    int axis = 0;
+    double best = -1.0;
+    for (int k = 0; k < 3; ++k) {
+        double len = vnorm(row3(lat, k));
+        if (len > best) {
+            best = len;
+            axis = k;
+        }
+    }
+    return axis;
+}
+
+void partitions_impl(gmd_handle* h, int64_t n, const double* pos, const double* lat, int64_t ne,
+                     const int64_t* src, const int64_t* dst, const int32_t* off, const double* dist,
+                     double cutoff, double r3, double tau, int axis, int p, const double* bounds,
+                     const int32_t* owner, uint32_t flags) {
+    cudaStream_t s = h->stream;
+    h->built = false;
+    h->graph_only = true;
+    h->closure_ready = false;
+    h->hc_ready = h->hcb_ready = false;
+    h->ctab_ok = false;
+    h->atoms.ready = h->bonds.ready = false;
+    h->corrupted = false;
+    if (n <= 0) raise(kConfig, "graph has no nodes");
+    if (p < 1) raise(kConfig, "partition count must be >= 1");
+    if (p > kMaxParts) raise(kConfig, "partition count limited to 64");
+    if (ne < 0 || (ne > 0 && (!src || !dst || !off))) raise(kArg, "null edge arrays");
+    if (n >= ((int64_t)1 << 31) - 1 || ne >= ((int64_t)1 << 31) - 1)
+        raise(kConfig, "graph exceeds the int32 index range");
+    if (r3 > 0.0) {  // check_ranges (linegraph.cpp:10-14)
+        if (r3 > cutoff) raise(kConfig, "three-body range cannot exceed the atom graph cutoff");
+        if (tau < 0.0) raise(kConfig, "tolerance tau must be >= 0");
+        if (ne > 0 && !dist) raise(kArg, "null distance array");
+    }
+    if (bounds) {
+        h->bounds.assign(bounds, bounds + p + 1);
+    } else {
+        h->bounds.assign(p + 1, 0.0);
+        h->bounds[p] = 1.0;
+    }
+    if (lat) std::memcpy(h->lat, lat, sizeof h->lat);
+    // check_slab_widths (partitioner.cpp:21-33), with the graph's cutoff
+    if (p > 1 && !(flags & GMD_ALLOW_NARROW)) {
+        if (!lat || !bounds) raise(kArg, "slab-width check needs the lattice and the rule");
+        const double perp = perp_width(lat, axis);
+        for (int i = 0; i < p; ++i) {
+            const double width = (bounds[i + 1] - bounds[i]) * perp;
+            if (width < cutoff)
+                raise(kConfig, "partition-width error: slab " + std::to_string(i) + " is " +
+                                   std::to_string(width) + " A wide, below the cutoff " +
+                                   std::to_string(cutoff) + " A");
+        }
+    }
+    h->n = n;
+    h->ne = ne;
+    h->p = p;
+    h->rc = cutoff;
+    h->r3 = r3;
+    h->tau = tau;
+    h->axis = axis;
+    h->allow_narrow = (flags & GMD_ALLOW_NARROW) != 0;
+    h->n_own = n;
+
+    // owners: given, or which_partition of each atom's wrapped fraction
+    int32_t* ownp = h->atoms.owner.get<int32_t>(n);
+    if (owner) {
+        for (int64_t i = 0; i < n; ++i)
+            if (owner[i] < 0 || owner[i] >= p) raise(kArg, "owner out of range");
+        GMD_CUDA(cudaMemcpyAsync(ownp, owner, 4 * n, cudaMemcpyHostToDevice, s));
+    } else if (p == 1) {
+        GMD_CUDA(cudaMemsetAsync(ownp, 0, 4 * n, s));
+    } else {
+        if (!pos || !lat || !bounds) raise(kArg, "owners need positions, lattice and rule");
+        const double* fw = wrapped_fracs(h, n, pos, lat, axis);
+        Bounds bd{};
+        bd.p = p;
+        for (int k = 0; k <= p; ++k) bd.b[k] = bounds[k];
+        launch_owner(fw, n, bd, ownp, s);
+    }
+    // CSR of the caller's edges: canonical order is dst-major (neighborlist.hpp:14-16)
+    std::vector<int32_t> row(n + 1, 0), s32(ne);
+    for (int64_t e = 0; e < ne; ++e) {
+        if (dst[e] < 0 || dst[e] >= n || src[e] < 0 || src[e] >= n)
+            raise(kArg, "edge endpoint out of range");
+        if (e > 0 && dst[e] < dst[e - 1]) raise(kConfig, "graph edges are not in dst-major order");
+        ++row[dst[e] + 1];
+        s32[e] = (int32_t)src[e];
+    }
+    for (int64_t v = 0; v < n; ++v) row[v + 1] += row[v];
+    int32_t* rowp = h->row.get<int32_t>(n + 1);
+    int32_t* srcp = h->src.get<int32_t>(std::max<int64_t>(1, ne));
+    GMD_CUDA(cudaMemcpyAsync(rowp, row.data(), 4 * (n + 1), cudaMemcpyHostToDevice, s));
+    if (ne) GMD_CUDA(cudaMemcpyAsync(srcp, s32.data(), 4 * ne, cudaMemcpyHostToDevice, s));
+    int32_t* fl = h->flags.get<int32_t>(4);
+    GMD_CUDA(cudaMemsetAsync(fl, 0, 16, s));
+    GraphDev gd;
+    gd.n = n;
+    gd.ne = ne;
+    gd.row = rowp;
+    gd.src = srcp;
+    gd.img = h->img.get<uint32_t>(std::max<int64_t>(1, ne));
+    gd.bond = r3 > 0.0 ? h->ebond.get<uint8_t>(std::max<int64_t>(1, ne)) : nullptr;
+    if (ne) {
+        int32_t* off_d = reinterpret_cast<int32_t*>(h->exp_tmp.get<char>((size_t)ne * 20));
+        double* dist_d = reinterpret_cast<double*>(off_d + 3 * ne + (ne & 1));
+        GMD_CUDA(cudaMemcpyAsync(off_d, off, 12 * ne, cudaMemcpyHostToDevice, s));
+        if (r3 > 0.0) GMD_CUDA(cudaMemcpyAsync(dist_d, dist, 8 * ne, cudaMemcpyHostToDevice, s));
+        launch_graph_import(ne, off_d, dist_d, r3 > 0.0 ? r3 + tau : -1.0, gd.img, gd.bond, fl, s);
+    }
+    h->img_ok = true;
+    LayoutState& A = h->atoms;
+    if (p == 1) {
+        A.p = 1;
+        A.nid = n;
+        A.list_off = {0, (int32_t)n, (int32_t)n, (int32_t)n};
+        A.rows = n;
+        A.nfrom = 0;
+        A.ready = true;
+        A.api_ready = A.dups_ready = false;
+        A.h_nodes.clear();
+    } else {
+        auto* reqp = A.req.get<unsigned long long>(n);
+        GMD_CUDA(cudaMemsetAsync(reqp, 0, sizeof(unsigned long long) * n, s));
+        launch_required(rowp, srcp, n, ownp, reqp, s);
+        build_layout(h, A, ownp, reqp, n, p);
+        launch_edge_lsrc(rowp, srcp, n, ownp, A.crow.as<int32_t>(), A.node_array.as<int32_t>(),
+                         A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(std::max<int64_t>(1, ne)),
+                         fl, s);
+    }
+    h->has_lg = r3 > 0.0;
+    h->nb = 0;
+    if (h->has_lg) {
+        int32_t* bc = h->bcnt.get<int32_t>(n);
+        launch_row_bond_count(rowp, gd.bond, n, bc, s);
+        int32_t* br = h->brow.get<int32_t>(n + 1);
+        scan_i32(h, bc, br, n);
+        int32_t nb32 = 0;
+        GMD_CUDA(cudaMemcpyAsync(&nb32, br + n, 4, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        h->nb = nb32;
+        int32_t* be = h->bedge.get<int32_t>(std::max<int64_t>(1, h->nb));
+        int32_t* bv = h->brev.get<int32_t>(std::max<int64_t>(1, h->nb));
+        int32_t* ebid = h->ebid.get<int32_t>(std::max<int64_t>(1, ne));
+        launch_bond_edges(rowp, gd.bond, n, br, be, ebid, s);
+        launch_bond_rev(n, gd, br, be, ebid, bv, fl, ownp, -1, s);
+    }
+    int32_t hf[4];
+    GMD_CUDA(cudaMemcpyAsync(hf, fl, 16, cudaMemcpyDeviceToHost, s));
+    sync(h);
+    // a caller's graph need not be closed under reversal: a bond without a
+    // reverse (flag 32) simply has none to skip (is_reverse_pair, linegraph.cpp:16-21)
+    if (hf[1] & kErrImgRange)
+        raise(kConfig, "periodic image offset exceeds the packed range (+-511 cells)");
+    if (hf[1] & 8) raise(kRuntime, "internal: edge endpoint missing from partition layout");
+    h->built = true;
+}
+
+// two-hop closures of every partition at once (linegraph.cpp:45-65)
+void ensure_closure(gmd_handle* h) {
+    need_built(h);
+    if (h->closure_ready) return;
+    cudaStream_t s = h->stream;
+    const int64_t n = h->n;
+    auto* m0 = h->cmask.get<unsigned long long>(2 * n);
+    auto* m1 = m0 + n;
+    launch_closure_init(h->atoms.owner.as<int32_t>(), n, m0, s);
+    launch_closure_hop(h->row.as<int32_t>(), h->src.as<int32_t>(), n, m0, m1, s);
+    launch_closure_hop(h->row.as<int32_t>(), h->src.as<int32_t>(), n, m1, m0, s);
+    h->closure_ready = true;
+}
+}  // namespace
+
+// ---- free builders ----------------------------------------------------------
+int gmd_partition_rule(gmd_handle* h, int64_t n, const double* pos, const double* lattice, int p,
+                       int equal_width, int* axis, double* boundaries) {
+    return run(h, [&] {
+        if (!lattice || !axis || !boundaries || (n > 0 && !pos)) raise(kArg, "null argument");
+        check_rule_args(n, p);
+        if (std::abs(det3(lattice)) < 1e-10) raise(kConfig, "degenerate cell");
+        *axis = longest_axis(lattice);
+        boundaries[0] = 0.0;
+        boundaries[p] = 1.0;
+        if (p == 1) return;
+        if (equal_width) {
+            for (int k = 1; k < p; ++k) boundaries[k] = (double)k / p;
+            return;
+        }
+        const double* fw = wrapped_fracs(h, n, pos, lattice, *axis);
+        quantile_walls(h, fw, n, p, boundaries);
+        for (int k = 1; k <= p; ++k)
+            if (boundaries[k] <= boundaries[k - 1])
+                raise(kConfig,
+                      "cannot place distinct partition boundaries; coordinates along the axis "
+                      "are degenerate");
+    });
+}
+
+int gmd_assign_owners(gmd_handle* h, int64_t n, const double* pos, const double* lattice, int axis,
+                      int p, const double* boundaries, double* fracs, int32_t* owner) {
+    return run(h, [&] {
+        if (n <= 0) return;
+        if (!pos || !lattice) raise(kArg, "null argument");
+        if (axis < 0 || axis > 2) raise(kArg, "axis out of range");
+        const double* fw = wrapped_fracs(h, n, pos, lattice, axis);
+        cudaStream_t s = h->stream;
+        if (owner) {
+            if (!boundaries || p < 1 || p > kMaxParts) raise(kArg, "bad partition rule");
+            Bounds bd{};
+            bd.p = p;
+            for (int k = 0; k <= p; ++k) bd.b[k] = boundaries[k];
+            int32_t* o = h->flagtmp.get<int32_t>(n + 1);
+            launch_owner(fw, n, bd, o, s);
+            GMD_CUDA(cudaMemcpyAsync(owner, o, 4 * n, cudaMemcpyDeviceToHost, s));
+        }
+        if (fracs) GMD_CUDA(cudaMemcpyAsync(fracs, fw, 8 * n, cudaMemcpyDeviceToHost, s));
+        sync(h);
+    });
+}
+
+int gmd_build_partitions(gmd_handle* h, int64_t n, const double* pos, const double* lattice,
+                         int64_t ne, const int64_t* src, const int64_t* dst, const int32_t* off,
+                         const double* dist, double cutoff, double r3, double tau, int axis, int p,
+                         const double* boundaries, const int32_t* owner, uint32_t flags) {
+    return run(h, [&] {
+        partitions_impl(h, n, pos, lattice, ne, src, dst, off, dist, cutoff, r3, tau, axis, p,
+                        boundaries, owner, flags);
+    });
+}
+
+int gmd_get_closure(gmd_handle* h, int part, int64_t* count, int64_t* ids) {
+    return run(h, [&] {
+        ensure_closure(h);
+        check_part(h, part);
+        std::vector<unsigned long long> m;
+        d2h(h, m, h->cmask.as<unsigned long long>(), h->n);
+        sync(h);
+        int64_t c = 0;
+        for (int64_t v = 0; v < h->n; ++v)
+            if (m[v] >> part & 1ull) {
+                if (ids) ids[c] = v;
+                ++c;
+            }
+        if (count) *count = c;
+    });
+}
+
+int gmd_get_bond_tables(gmd_handle* h, uint64_t* mask) {
+    return run(h, [&] {
+        need_built(h);
+        if (!h->has_lg) raise(kConfig, "no line graph was built");
+        ensure_closure(h);
+        cudaStream_t s = h->stream;
+        const int64_t nb = h->nb;
+        int32_t* edst = h->edst.get<int32_t>(std::max<int64_t>(1, h->ne));
+        launch_edge_dst(h->row.as<int32_t>(), h->n, edst, s);
+        auto* bm = h->bmask.get<unsigned long long>(std::max<int64_t>(1, nb));
+        launch_bond_tables(nb, h->bedge.as<int32_t>(), edst, h->src.as<int32_t>(),
+                           h->cmask.as<unsigned long long>(), bm, s);
+        if (nb) GMD_CUDA(cudaMemcpyAsync(mask, bm, 8 * nb, cudaMemcpyDeviceToHost, s));
+        sync(h);
+    });
+}
+
+int gmd_brute_force_line_graph(gmd_handle* h, int64_t* count, int64_t* pairs) {
+    return run(h, [&] {
+        need_built(h);
+        if (!h->has_lg) raise(kConfig, "no line graph was built");
+        cudaStream_t s = h->stream;
+        const int64_t n = h->n, nb = h->nb;
+        int32_t* edst = h->edst.get<int32_t>(std::max<int64_t>(1, h->ne));
+        launch_edge_dst(h->row.as<int32_t>(), h->n, edst, s);
+        // by_dst = the bond CSR (brow / bond ids in order); by_src built here
+        std::vector<int32_t> be, es;
+        d2h(h, be, h->bedge.as<int32_t>(), nb);
+        d2h(h, es, h->src.as<int32_t>(), h->ne);
+        sync(h);
+        std::vector<int32_t> orow(n + 1, 0), obond(std::max<int64_t>(1, nb)), inb(std::max<int64_t>(1, nb));
+        for (int64_t b = 0; b < nb; ++b) ++orow[es[be[b]] + 1];
+        for (int64_t v = 0; v < n; ++v) orow[v + 1] += orow[v];
+        std::vector<int32_t> fill(orow.begin(), orow.end() - 1);
+        for (int64_t b = 0; b < nb; ++b) obond[fill[es[be[b]]]++] = (int32_t)b;
+        for (int64_t b = 0; b < nb; ++b) inb[b] = (int32_t)b;
+        int32_t* d_orow = h->lcnt.get<int32_t>(3 * (n + 1) + 2 * std::max<int64_t>(1, nb));
+        int32_t* d_obond = d_orow + (n + 1);
+        int32_t* d_inb = d_obond + std::max<int64_t>(1, nb);
+        int32_t* d_cnt = d_inb + std::max<int64_t>(1, nb);
+        int32_t* d_off = d_cnt + (n + 1);
+        GMD_CUDA(cudaMemcpyAsync(d_orow, orow.data(), 4 * (n + 1), cudaMemcpyHostToDevice, s));
+        if (nb) {
+            GMD_CUDA(cudaMemcpyAsync(d_obond, obond.data(), 4 * nb, cudaMemcpyHostToDevice, s));
+            GMD_CUDA(cudaMemcpyAsync(d_inb, inb.data(), 4 * nb, cudaMemcpyHostToDevice, s));
+        }
+        launch_brute_line(n, h->brow.as<int32_t>(), d_inb, d_orow, d_obond, h->bedge.as<int32_t>(),
+                          h->src.as<int32_t>(), edst, h->img.as<uint32_t>(), d_cnt, nullptr, nullptr, s);
+        scan_i32(h, d_cnt, d_off, n);
+        int32_t T = 0;
+        GMD_CUDA(cudaMemcpyAsync(&T, d_off + n, 4, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        int32_t* d_pairs = h->lpairs.get<int32_t>(2 * std::max<int64_t>(1, T));
+        launch_brute_line(n, h->brow.as<int32_t>(), d_inb, d_orow, d_obond, h->bedge.as<int32_t>(),
+                          h->src.as<int32_t>(), edst, h->img.as<uint32_t>(), d_cnt, d_off, d_pairs, s);
+        std::vector<int32_t> hp;
+        d2h(h, hp, d_pairs, 2 * (size_t)T);
+        sync(h);
+        h->hcb_ready = false;  // lpairs / lcnt are shared with the line-graph cache
+        if (count) *count = T;
+        if (pairs) {
+            std::vector<std::pair<int64_t, int64_t>> v((size_t)T);
+            for (int64_t t = 0; t < T; ++t) v[t] = {hp[2 * t], hp[2 * t + 1]};
+            std::sort(v.begin(), v.end());
+            for (int64_t t = 0; t < T; ++t) {
+                pairs[2 * t] = v[t].first;
+                pairs[2 * t + 1] = v[t].second;
+            }
+        }
+    });
+}
+
+int gmd_brute_force_neighbor_list(gmd_handle* h, int64_t n, const double* pos,
+                                  const double* lattice, const uint8_t* pbc, double cutoff,
+                                  int64_t* ne_out, int64_t* src, int64_t* dst, int32_t* off,
+                                  double* dist, double* vec) {
+    return run(h, [&] {
+        if (cutoff <= 0.0) raise(kConfig, "cutoff must be positive");
+        if (n == 0) raise(kConfig, "cannot build neighbor list for empty system");
+        if (n > 5000) raise(kConfig, "brute force guard: N > 5000");
+        if (!pos || !lattice || !ne_out) raise(kArg, "null argument");
+        cudaStream_t s = h->stream;
+        h->built = false;
+        h->n = n;
+        double* dpos = h->pos.get<double>(3 * n);
+        GMD_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+        std::memcpy(h->lat, lattice, sizeof h->lat);
+        ensure_periodic_dev(h, pbc, cutoff);  // pads non-periodic axes (system.cpp:242-270)
+        if (std::abs(det3(h->lat)) < 1e-10)
+            raise(kConfig, "periodic system requires an invertible lattice");
+        Geom g{};
+        std::memcpy(g.L, h->lat, sizeof g.L);
+        inverse3(h->lat, g.inv);
+        g.bins[0] = g.bins[1] = g.bins[2] = 1;
+        NLBuffers b{};
+        b.pos = dpos;
+        b.cell = h->cell.get<int32_t>(3 * n);
+        b.fw_axis = h->fw.get<double>(n);
+        b.bin = h->bin.get<int32_t>(n);
+        b.bin_cnt = h->bin_cnt.get<int32_t>(1);
+        b.flags = h->flags.get<int32_t>(4);
+        GMD_CUDA(cudaMemsetAsync(b.bin_cnt, 0, 4, s));
+        GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
+        launch_wrap(g, n, b, s);  // cell_of of wrap_for_search (neighborlist.cpp:42-50)
+        BruteNL bn{};
+        std::memcpy(bn.L, h->lat, sizeof bn.L);
+        bn.cutoff2 = cutoff * cutoff;
+        for (int k = 0; k < 3; ++k)  // neighborlist.cpp:211-214
+            bn.span[k] = (int)std::ceil(cutoff / perp_width(h->lat, k)) + 1;
+        int32_t* cnt = h->deg.get<int32_t>(n + 1);
+        int32_t* rowoff = h->row.get<int32_t>(n + 1);
+        launch_brute_nl(bn, n, dpos, b.cell, cnt, nullptr, nullptr, nullptr, s);
+        scan_i32(h, cnt, rowoff, n);
+        int32_t ne32 = 0;
+        GMD_CUDA(cudaMemcpyAsync(&ne32, rowoff + n, 4, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        const int64_t ne = ne32;
+        *ne_out = ne;
+        if (!src && !dst && !off && !dist && !vec) return;
+        int32_t* d_src = h->src.get<int32_t>(std::max<int64_t>(1, ne));
+        int32_t* d_off = reinterpret_cast<int32_t*>(h->exp_tmp.get<char>(std::max<int64_t>(1, ne) * 12));
+        launch_brute_nl(bn, n, dpos, b.cell, cnt, rowoff, d_src, d_off, s);
+        std::vector<int32_t> hs, ho, hr;
+        d2h(h, hs, d_src, ne);
+        d2h(h, ho, d_off, 3 * ne);
+        d2h(h, hr, rowoff, n + 1);
+        sync(h);
+        // assemble (neighborlist.cpp:60-85): rows in (src, ox, oy, oz) order
+        std::vector<int32_t> order(ne), ssrc(ne), sdst(ne), soff(3 * ne);
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t a = hr[i], z = hr[i + 1];
+            for (int32_t k = a; k < z; ++k) order[k] = k;
+            std::sort(order.begin() + a, order.begin() + z, [&](int32_t x, int32_t y) {
+                if (hs[x] != hs[y]) return hs[x] < hs[y];
+                for (int c = 0; c < 3; ++c)
+                    if (ho[3 * x + c] != ho[3 * y + c]) return ho[3 * x + c] < ho[3 * y + c];
+                return false;
+            });
+            for (int32_t k = a; k < z; ++k) {
+                ssrc[k] = hs[order[k]];
+                sdst[k] = (int32_t)i;
+                for (int c = 0; c < 3; ++c) soff[3 * k + c] = ho[3 * order[k] + c];
+            }
+        }
+        if (src) for (int64_t e = 0; e < ne; ++e) src[e] = ssrc[e];
+        if (dst) for (int64_t e = 0; e < ne; ++e) dst[e] = sdst[e];
+        if (off) std::copy(soff.begin(), soff.end(), off);
+        if (dist || vec) {  // exact fp64 geometry on the device
+            int32_t* d_dst = h->edst.get<int32_t>(std::max<int64_t>(1, ne));
+            double* d_dist = h->fw.get<double>(std::max<int64_t>(1, 4 * ne));
+            GMD_CUDA(cudaMemcpyAsync(d_src, ssrc.data(), 4 * ne, cudaMemcpyHostToDevice, s));
+            GMD_CUDA(cudaMemcpyAsync(d_dst, sdst.data(), 4 * ne, cudaMemcpyHostToDevice, s));
+            GMD_CUDA(cudaMemcpyAsync(d_off, soff.data(), 12 * ne, cudaMemcpyHostToDevice, s));
+            launch_edge_geometry(bn, ne, dpos, d_src, d_dst, d_off, d_dist, d_dist + ne, s);
+            std::vector<double> hd;
+            d2h(h, hd, d_dist, 4 * ne);
+            sync(h);
+            if (dist) std::copy(hd.begin(), hd.begin() + ne, dist);
+            if (vec) std::copy(hd.begin() + ne, hd.end(), vec);
+        }
+    });
+}
+
+int gmd_get_csr(gmd_handle* h, int32_t* row, int32_t* src) {
+    return run(h, [&] {
+        need_built(h);
+        cudaStream_t s = h->stream;
+        if (row) GMD_CUDA(cudaMemcpyAsync(row, h->row.as<int32_t>(), 4 * (h->n + 1), cudaMemcpyDeviceToHost, s));
+        if (src && h->ne) GMD_CUDA(cudaMemcpyAsync(src, h->src.as<int32_t>(), 4 * h->ne, cudaMemcpyDeviceToHost, s));
+        sync(h);
+    });
+}
+
+int gmd_util_ensure_periodic(gmd_handle* h, int64_t n, const double* pos, const double* lattice,
+                             const uint8_t* pbc, double cutoff, double* out_pos, double* out_lat) {
+    return run(h, [&] {
+        if (!lattice || !pbc || !out_lat || (n > 0 && (!pos || !out_pos))) raise(kArg, "null argument");
+        h->built = false;
+        h->n = n;
+        std::memcpy(h->lat, lattice, sizeof h->lat);
+        if (n > 0) {
+            double* d = h->pos.get<double>(3 * n);
+            GMD_CUDA(cudaMemcpyAsync(d, pos, 24 * n, cudaMemcpyHostToDevice, h->stream));
+            ensure_periodic_dev(h, pbc, cutoff);
+            GMD_CUDA(cudaMemcpyAsync(out_pos, d, 24 * n, cudaMemcpyDeviceToHost, h->stream));
+            sync(h);
+        } else if (!(pbc[0] && pbc[1] && pbc[2])) {
+            if (cutoff <= 0.0) raise(kConfig, "cutoff must be positive");
+            raise(kConfig, "cannot pad the cell of an empty system");
+        }
+        std::memcpy(out_lat, h->lat, sizeof h->lat);
     });
 }
 

@@ -33,3 +33,15 @@ if __name__ == "__main__":
     with open(dst, "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", dst)
+    # the fixture file the reference's own tests open (fixture_path("quartz.xyz"),
+    # proj/tests/helpers.hpp:15-21), re-serialised by the reference's save_xyz
+    # (17 significant digits: loads back bitwise) for tests/cpp/ref/*
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+    import numpy as np
+    from oracle.oracle import Oracle
+    q = out["quartz"]
+    xyz = os.path.join(os.path.dirname(dst), "quartz.xyz")
+    Oracle("ref").save_xyz(np.array(q["positions"]), np.array(q["species"], np.int32),
+                           np.array(q["lattice"]), np.ones(3, np.uint8), xyz)
+    print("wrote", xyz)
