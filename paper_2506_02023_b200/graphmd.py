@@ -50,6 +50,10 @@ EXPORTS = [
     "gmd_comm_init_nccl", "gmd_comm_init_local", "gmd_comm_info", "gmd_num_owned", "gmd_get_owned_ids",
     "gmd_md_masses", "gmd_md_maxwell_boltzmann", "gmd_md_evaluate", "gmd_md_step", "gmd_md_observe",
     "gmd_md_run", "gmd_comm_ipc_export", "gmd_comm_init_ipc",
+    # free builder API (partitioner.hpp / linegraph.hpp / neighborlist.hpp)
+    "gmd_partition_rule", "gmd_assign_owners", "gmd_build_partitions", "gmd_get_closure",
+    "gmd_get_bond_tables", "gmd_brute_force_line_graph", "gmd_brute_force_neighbor_list",
+    "gmd_get_csr", "gmd_util_ensure_periodic",
 ]
 
 
@@ -132,6 +136,15 @@ def lib():
             "gmd_md_run": (I, [V, I64, V, V, V, V, V, V, D, I64, D, D, D, I, U32, V]),
             "gmd_comm_ipc_export": (I, [V, I, I, I64, V]),
             "gmd_comm_init_ipc": (I, [V, V]),
+            "gmd_partition_rule": (I, [V, I64, V, V, I, I, V, V]),
+            "gmd_assign_owners": (I, [V, I64, V, V, I, I, V, V, V]),
+            "gmd_build_partitions": (I, [V, I64, V, V, I64, V, V, V, V, D, D, D, I, I, V, V, U32]),
+            "gmd_get_closure": (I, [V, I, V, V]),
+            "gmd_get_bond_tables": (I, [V, V]),
+            "gmd_brute_force_line_graph": (I, [V, V, V]),
+            "gmd_brute_force_neighbor_list": (I, [V, I64, V, V, V, D, V, V, V, V, V, V]),
+            "gmd_get_csr": (I, [V, V, V]),
+            "gmd_util_ensure_periodic": (I, [V, I64, V, V, V, D, V, V]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -15,6 +15,7 @@ from tests import systems as S
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
+CPP = os.path.join(HERE, "cpp", "test_cpp_api")
 
 
 @pytest.fixture
