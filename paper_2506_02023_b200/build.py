@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgraphmd_b200.so")
 OBJ = os.path.join(HERE, "build_obj")
 SOURCES = ["gmd_scan.cu", "gmd_graph.cu", "gmd_partition.cu", "gmd_linegraph.cu",
-           "gmd_model.cu", "gmd_generic.cu", "gmd_comm.cu", "gmd_md.cu", "gmd_builders.cu",
+           "gmd_model.cu", "gmd_generic.cu", "gmd_wide.cu", "gmd_comm.cu", "gmd_md.cu", "gmd_builders.cu",
            "gmd_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

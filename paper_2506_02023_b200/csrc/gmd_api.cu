@@ -34,6 +34,7 @@
 #include "gmd_md.cuh"
 #include "gmd_model.cuh"
 #include "gmd_partition.cuh"
+#include "gmd_wide.cuh"
 
 namespace gmd {
 void launch_bond_owner(int64_t n, const int32_t* brow, const int32_t* owner, int32_t* bown,
@@ -1102,6 +1103,15 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     const bool part = h->p > 1;
     const bool gen = h->generic;  // widths other than F = 16, K = 8 (gmd_generic.cu)
     const int F = gen ? h->F : kF;
+    // F = 64, K = 8: the feature-major / tcgen05 kernels of gmd_wide.cu
+    // (GMD_WIDE=0 selects the width-generic kernels instead)
+    const char* wide_env = std::getenv("GMD_WIDE");
+    const bool wide = gen && wide_model(h->gm) && !(wide_env && wide_env[0] == '0');
+    // tuned widths, but a center with more in-bonds than the tuned three-body
+    // kernels stage: the three-body stage runs on the width-generic kernels
+    // (any in-bond count, linegraph.cpp:144-160)
+    const bool tbg = tb && !gen && h->max_bonds > kMaxBondsPerAtom;
+    const bool tgen = gen || tbg;  // generic three-body kernels
 
     {   // the __constant__ model copy is per device: upload only when another
         // parameter set was resident (saves a blocking pageable copy per step)
@@ -1127,7 +1137,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     // backward edge pass: FFMA kernel, or the tcgen05 kernel with GMD_BWD_TC=1
     const char* tc_env = std::getenv("GMD_BWD_TC");
     const bool use_tc = !gen && tc_env && tc_env[0] == '1';
-    const int vgrid = gen ? gen_grid(n) * 8 : use_tc ? bwd_tc_grid(n) : bwd_edge_grid(n);
+    const int vgrid = wide ? wide_bwd_grid(n) : gen ? gen_grid(n) * 8 : use_tc ? bwd_tc_grid(n) : bwd_edge_grid(n);
     // host forces (e2e): the last layer's edge pass runs in node chunks; a
     // chunk's forces are final once it finishes (GRAD[v] gathers only v's
     // in-edges; the three-body terms came at l = L - 1), so they go to the
@@ -1148,7 +1158,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                            : 1;
     double* e_part = h->e_part.get<double>(grid);
     double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);
-    const int tgrid = gen ? gen_grid(n) * 8 : tb_grid_size(n);
+    const int tgrid = wide ? wide_tb_grid(n) : tgen ? gen_grid(n) * 8 : tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
     double* pa = h->per_atom.get<double>(n_all);
@@ -1261,7 +1271,11 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     for (int l = 0; l < L; ++l) {
         const bool tbl = tb && l == L - 1;
         if (tbl) {
-            if (gen) {
+            if (wide) {
+                float* TT = h->TT.get<float>((size_t)std::max<int64_t>(1, nbr) * F);
+                { PROF("tb_t"); launch_wide_tb_t(h->gm, ba, TT, s); }
+                { PROF("tb_forward"); launch_wide_tb_forward(h->gm, ba, TT, TP, TH3, s); }
+            } else if (tgen) {
                 float* TT = h->TT.get<float>((size_t)std::max<int64_t>(1, nbr) * F);
                 { PROF("tb_t"); launch_gen_tb_t(h->gm, ba, nbr, TT, s); }
                 { PROF("tb_forward"); launch_gen_tb_forward(h->gm, ba, TT, TP, TH3, h->flags.as<int32_t>(), s); }
@@ -1272,7 +1286,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             bond_exchange(TP, F);
             {
                 PROF("tb_inject");
-                if (gen)
+                if (wide)
+                    launch_wide_tb_inject(h->gm, ba, TP, H[l], TH4, s);
+                else if (tgen)
                     launch_gen_tb_inject(h->gm, ba, TP, H[l], TH4, s);
                 else
                     launch_tb_inject(ba, TP, H[l], TH4, s);
@@ -1280,7 +1296,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         }
         if (l > 0 || tbl) exchange(H[l], true);
         PROF("conv");
-        if (gen)
+        if (wide)
+            launch_wide_conv(h->gm, a, l, H[l], H[l + 1], TH + (size_t)l * n * F,
+                             l == L - 1 ? pa : nullptr, s);
+        else if (gen)
             launch_gen_conv(h->gm, a, l, H[l], H[l + 1], TH + (size_t)l * n * F,
                             l == L - 1 ? pa : nullptr, s);
         else
@@ -1297,12 +1316,15 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     }
 
     // ---- backward (:796-984)
-    if (gen) launch_gen_init_hbar(h->gm, n, HB, s);  // (tuned: fused into the first bwd_node)
+    if (gen && !wide) launch_gen_init_hbar(h->gm, n, HB, s);  // (tuned, wide: fused into the first bwd_node)
     GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
         {
             PROF("bwd_node");
-            if (gen)
+            if (wide)
+                launch_wide_bwd_node(h->gm, n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * F, MB,
+                                     l == L - 1, s);
+            else if (gen)
                 launch_gen_bwd_node(h->gm, n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * F, MB, s);
             else
                 launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, l == L - 1, s);
@@ -1310,7 +1332,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         exchange(MB);
         {
             PROF("bwd_edge");
-            if (gen)
+            if (wide)
+                launch_wide_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+            else if (gen)
                 launch_gen_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
             else if (use_tc)
                 launch_bwd_edge_tc(a, h->ctab.as<int4>(), h->ccta.as<int32_t>(), vgrid, MB, H[l], HB,
@@ -1343,7 +1367,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             float4* VOUT = h->VOUT.get<float4>(nbr);
             {
                 PROF("tb_bwd_q");
-                if (gen)
+                if (wide)
+                    launch_wide_tb_bwd_q(h->gm, n, a.nodes, a.crow, HB, TH4, QB, s);
+                else if (tgen)
                     launch_gen_tb_bwd_q(h->gm, n, a.nodes, a.crow, HB, TH4, QB, s);
                 else
                     launch_tb_bwd_q(n, a.nodes, a.crow, HB, TH4, QB, s);
@@ -1351,7 +1377,11 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             if (rank_mode) exchange(QB);  // q_bar of halo atoms (bond sources)
             {
                 PROF("tb_backward");
-                if (gen)
+                if (wide)
+                    launch_wide_tb_backward(h->gm, ba, QB, TH3, h->TT.as<float>(),
+                                            h->SMR.get<float>((size_t)std::max<int64_t>(1, nbr) * F),
+                                            VIN, VOUT, v3_part, s);
+                else if (tgen)
                     launch_gen_tb_backward(h->gm, ba, QB, TH3, h->TT.as<float>(),
                                            h->SMR.get<float>((size_t)std::max<int64_t>(1, nbr) * F),
                                            VIN, VOUT, v3_part, s);
@@ -1608,6 +1638,68 @@ int gmd_params_init(uint64_t seed, int F, int K, int L, double r_atom, double r3
     return GMD_OK;
 }
 
+namespace {
+void build_gen_tables(gmd_handle* h, int F, int K, int L, double r_atom, double r3, const double* blob) {
+    const size_t nemb = 119 * (size_t)F, nW = (size_t)L * F * F, nb = (size_t)L * F,
+                 nP = (size_t)F * K, nFF = (size_t)F * F;
+    std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F + nW + 2 * nFF + nP);
+    const double* q = blob;
+    size_t o = 0;
+    for (size_t i = 0; i < nemb + nW + nb + nP; ++i) t[o++] = (float)*q++;  // emb, W, b, P
+    const double* Pd = blob + nemb + nW + nb;
+    for (size_t i = 0; i < nP; ++i) t[o++] = (float)(Pd[i] * (double)(i % K));  // k P
+    for (size_t i = 0; i < nP + 2 * nFF + F; ++i) t[o++] = (float)*q++;  // P3 W3 W4 ro
+    // transposed W (per layer), W3, W4
+    const float* Wf = t.data() + nemb;
+    const float* W3f = t.data() + nemb + nW + nb + 2 * nP + nP;
+    const float* W4f = W3f + nFF;
+    for (int l = 0; l < L; ++l)
+        for (int f = 0; f < F; ++f)
+            for (int gg = 0; gg < F; ++gg)
+                t[o + (size_t)l * nFF + (size_t)gg * F + f] = Wf[(size_t)l * nFF + (size_t)f * F + gg];
+    o += nW;
+    for (int f = 0; f < F; ++f)
+        for (int gg = 0; gg < F; ++gg) {
+            t[o + (size_t)gg * F + f] = W3f[(size_t)f * F + gg];
+            t[o + nFF + (size_t)gg * F + f] = W4f[(size_t)f * F + gg];
+        }
+    o += 2 * nFF;
+    const float* P3f = t.data() + nemb + nW + nb + 2 * nP;
+    for (int f = 0; f < F; ++f)
+        for (int kk = 0; kk < K; ++kk) t[o + (size_t)kk * F + f] = P3f[(size_t)f * K + kk];
+    o += nP;
+    float* d = h->gpar.get<float>(t.size());
+    GMD_CUDA(cudaMemcpy(d, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
+    GenModel& g = h->gm;
+    g.F = F;
+    g.K = K;
+    g.L = L;
+    g.emb = d;
+    g.W = d + nemb;
+    g.b = g.W + nW;
+    g.P = g.b + nb;
+    g.Pk = g.P + nP;
+    g.P3 = g.Pk + nP;
+    g.W3 = g.P3 + nP;
+    g.W4 = g.W3 + nFF;
+    g.ro = g.W4 + nFF;
+    g.WT = g.ro + F;
+    g.W3T = g.WT + nW;
+    g.W4T = g.W3T + nFF;
+    g.P3T = g.W4T + nFF;
+    const double r3e = r3 > 0.0 ? r3 : 1.0;
+    g.r3 = (float)r3e;
+    g.inv_r3 = (float)(1.0 / r3e);
+    g.inv_sigma3 = (float)(K / r3e);
+    g.mu_step3 = K > 1 ? (float)(r3e / (K - 1)) : 0.f;
+    g.rc = (float)r_atom;
+    g.inv_rc = (float)(1.0 / r_atom);
+    g.inv_sigma = (float)(K / r_atom);  // sigma = rc / K (potential.cpp:34)
+    g.mu_step = K > 1 ? (float)(r_atom / (K - 1)) : 0.f;
+}
+
+}  // namespace
+
 int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
                    const double* blob) {
     return run(h, [&] {
@@ -1635,67 +1727,13 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
             if (off != total) raise(kRuntime, "internal: parameter blob layout");
         }
         h->generic = F != kF || K != kK || L > kMaxLayers;
-        if (h->generic) {  // width-generic kernels: fp32 tables in global memory
-            if (F > kGenMaxF || K > kGenMaxK)
-                raise(kConfig, "feature_width <= 128 and basis_count <= 32 are supported");
-            // device tables: emb | W | b | P | kP | P3 | W3 | W4 | ro (blob order:
-            // emb W b P P3 W3 W4 ro, potential.hpp:15-41)
-            const size_t nemb = 119 * (size_t)F, nW = (size_t)L * F * F, nb = (size_t)L * F,
-                         nP = (size_t)F * K, nFF = (size_t)F * F;
-            std::vector<float> t(nemb + nW + nb + 3 * nP + 2 * nFF + F + nW + 2 * nFF + nP);
-            const double* q = blob;
-            size_t o = 0;
-            for (size_t i = 0; i < nemb + nW + nb + nP; ++i) t[o++] = (float)*q++;  // emb, W, b, P
-            const double* Pd = blob + nemb + nW + nb;
-            for (size_t i = 0; i < nP; ++i) t[o++] = (float)(Pd[i] * (double)(i % K));  // k P
-            for (size_t i = 0; i < nP + 2 * nFF + F; ++i) t[o++] = (float)*q++;  // P3 W3 W4 ro
-            // transposed W (per layer), W3, W4
-            const float* Wf = t.data() + nemb;
-            const float* W3f = t.data() + nemb + nW + nb + 2 * nP + nP;
-            const float* W4f = W3f + nFF;
-            for (int l = 0; l < L; ++l)
-                for (int f = 0; f < F; ++f)
-                    for (int gg = 0; gg < F; ++gg)
-                        t[o + (size_t)l * nFF + (size_t)gg * F + f] = Wf[(size_t)l * nFF + (size_t)f * F + gg];
-            o += nW;
-            for (int f = 0; f < F; ++f)
-                for (int gg = 0; gg < F; ++gg) {
-                    t[o + (size_t)gg * F + f] = W3f[(size_t)f * F + gg];
-                    t[o + nFF + (size_t)gg * F + f] = W4f[(size_t)f * F + gg];
-                }
-            o += 2 * nFF;
-            const float* P3f = t.data() + nemb + nW + nb + 2 * nP;
-            for (int f = 0; f < F; ++f)
-                for (int kk = 0; kk < K; ++kk) t[o + (size_t)kk * F + f] = P3f[(size_t)f * K + kk];
-            o += nP;
-            float* d = h->gpar.get<float>(t.size());
-            GMD_CUDA(cudaMemcpy(d, t.data(), sizeof(float) * t.size(), cudaMemcpyHostToDevice));
-            GenModel& g = h->gm;
-            g.F = F;
-            g.K = K;
-            g.L = L;
-            g.emb = d;
-            g.W = d + nemb;
-            g.b = g.W + nW;
-            g.P = g.b + nb;
-            g.Pk = g.P + nP;
-            g.P3 = g.Pk + nP;
-            g.W3 = g.P3 + nP;
-            g.W4 = g.W3 + nFF;
-            g.ro = g.W4 + nFF;
-            g.WT = g.ro + F;
-            g.W3T = g.WT + nW;
-            g.W4T = g.W3T + nFF;
-            g.P3T = g.W4T + nFF;
-            const double r3e = r3 > 0.0 ? r3 : 1.0;
-            g.r3 = (float)r3e;
-            g.inv_r3 = (float)(1.0 / r3e);
-            g.inv_sigma3 = (float)(K / r3e);
-            g.mu_step3 = K > 1 ? (float)(r3e / (K - 1)) : 0.f;
-            g.rc = (float)r_atom;
-            g.inv_rc = (float)(1.0 / r_atom);
-            g.inv_sigma = (float)(K / r_atom);  // sigma = rc / K (potential.cpp:34)
-            g.mu_step = K > 1 ? (float)(r_atom / (K - 1)) : 0.f;
+        if (h->generic && (F > kGenMaxF || K > kGenMaxK))
+            raise(kConfig, "feature_width <= 128 and basis_count <= 32 are supported");
+        // fp32 tables of the width-generic kernels: the whole model for other
+        // widths; for F = 16, K = 8 the three-body fallback for centers with
+        // more in-bonds than the tuned kernels stage (kMaxBondsPerAtom)
+        build_gen_tables(h, F, K, L, r_atom, r3, blob);
+        if (h->generic) {
             h->F = F;
             h->K = K;
             h->L = L;

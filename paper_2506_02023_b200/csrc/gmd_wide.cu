@@ -1,0 +1,1244 @@
+// F = 64, K = 8 model kernels (see gmd_wide.cuh).  Formulas as
+// gmd_generic.cu / proj/src/potential.cpp:19-78 (radial basis), 743-774
+// (conv), 816-848 (backward):
+//   u_k(d) = fc(d) exp(-((d - mu_k)/sigma)^2),  s_f = sum_k P_fk u_k
+//   m_u    = sum_{e=(w->u)} s_e (.) h_w,  h_u' = h_u + tanh(W m_u + b)
+//   backward ("dsum" form, gmd_model.cu): per in-edge e = (w -> u)
+//     hbar_u += mbar_w (.) s_e
+//     dsum_e  = sum_k psi_k G_k,  G = X P,  X_f = mbar_u,f h_w,f + h_u,f mbar_w,f,
+//               psi_k = phi_k (ca + cb k)
+//     grad_u -= v_e dsum_e / d_e,  virial += 1/2 dsum_e / d_e v_e (x) v_e
+#include "gmd_tc.cuh"
+#include "gmd_wide.cuh"
+
+namespace gmd {
+namespace {
+
+constexpr int F = kWideF, K = kWideK;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
+
+__device__ __forceinline__ float ex2a(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+struct Basis {  // per-call scalars of the atom-channel radial basis
+    float a2;   // sqrt(log2 e) / sigma
+    float mu2;  // mu_step * a2
+    float rc, pi_rc, isg, mus;
+};
+
+__host__ Basis make_basis(const GenModel& g) {
+    Basis b;
+    b.a2 = 1.2011224087864498f * g.inv_sigma;  // sqrt(log2(e)) / sigma
+    b.mu2 = g.mu_step * b.a2;
+    b.rc = g.rc;
+    b.pi_rc = 3.14159265358979f * g.inv_rc;
+    b.isg = g.inv_sigma;
+    b.mus = g.mu_step;
+    return b;
+}
+
+// phi_k = exp(-((d - mu_k)/sigma)^2) = 2^(-(d a2 - k mu2)^2)
+__device__ __forceinline__ void phi8(const Basis& b, float d, float phi[K]) {
+    const float xa = d * b.a2;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float x = xa - (float)k * b.mu2;
+        phi[k] = ex2a(-x * x);
+    }
+}
+
+__device__ __forceinline__ float gwarp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// forward conv: one warp per node, lane l holds features 2l, 2l+1
+// ---------------------------------------------------------------------------
+constexpr int kConvWarps = 8;
+
+struct ConvSmem {
+    float2 WT[F][F / 2];           // WT[q][l] = (W[2l][q], W[2l+1][q])
+    float4 u[kConvWarps][32][2];   // fc * phi_0..7 of the chunk's edges
+    int src[kConvWarps][32];
+    float4 m[kConvWarps][F / 4];   // the node's m row (broadcast reads)
+};
+
+__global__ void __launch_bounds__(kConvWarps * 32) k_wide_conv(GenModel g, Basis bs, ConvArgs a,
+                                                               int layer, const float* __restrict__ Hin,
+                                                               float* __restrict__ Hout,
+                                                               float* __restrict__ TH,
+                                                               double* __restrict__ per_atom) {
+    __shared__ __align__(16) ConvSmem S;
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const float* W = g.W + (size_t)layer * F * F;  // W[f][q]
+    for (int t = threadIdx.x; t < F * F / 2; t += blockDim.x) {
+        const int q = t / (F / 2), l = t % (F / 2);
+        S.WT[q][l] = make_float2(W[(2 * l) * F + q], W[(2 * l + 1) * F + q]);
+    }
+    float2 P2[K];  // (P[2l][k], P[2l+1][k])
+#pragma unroll
+    for (int k = 0; k < K; ++k) P2[k] = make_float2(g.P[(2 * lane) * K + k], g.P[(2 * lane + 1) * K + k]);
+    const float2 b2 = make_float2(g.b[layer * F + 2 * lane], g.b[layer * F + 2 * lane + 1]);
+    const float2 ro2 = make_float2(g.ro[2 * lane], g.ro[2 * lane + 1]);
+    __syncthreads();
+    for (int64_t k = (int64_t)blockIdx.x * kConvWarps + wq; k < a.n;
+         k += (int64_t)gridDim.x * kConvWarps) {
+        const int64_t v = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int64_t r = a.crow ? (int64_t)a.crow[v] : v;
+        const int e0 = a.row[v], e1 = a.row[v + 1];
+        float2 m = make_float2(0.f, 0.f);
+        for (int eb = e0; eb < e1; eb += 32) {
+            const int ne = min(32, e1 - eb);
+            if (lane < ne) {
+                const float d = a.d[eb + lane];
+                float phi[K];
+                phi8(bs, d, phi);
+                const float fc = d < bs.rc ? 0.5f * __cosf(d * bs.pi_rc) + 0.5f : 0.0f;
+                S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
+                S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+                S.src[wq][lane] = a.lsrc[eb + lane];
+            }
+            __syncwarp();
+            int i = 0;
+            for (; i + 4 <= ne; i += 4) {  // four gathered rows in flight
+                float2 h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    h[j] = __ldg(reinterpret_cast<const float2*>(Hin + (size_t)S.src[wq][i + j] * F) + lane);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 ua = S.u[wq][i + j][0], ub = S.u[wq][i + j][1];
+                    float2 sv = f2mul(P2[0], bc2(ua.x));
+                    sv = f2fma(P2[1], bc2(ua.y), sv);
+                    sv = f2fma(P2[2], bc2(ua.z), sv);
+                    sv = f2fma(P2[3], bc2(ua.w), sv);
+                    sv = f2fma(P2[4], bc2(ub.x), sv);
+                    sv = f2fma(P2[5], bc2(ub.y), sv);
+                    sv = f2fma(P2[6], bc2(ub.z), sv);
+                    sv = f2fma(P2[7], bc2(ub.w), sv);
+                    m = f2fma(h[j], sv, m);
+                }
+            }
+            for (; i < ne; ++i) {
+                const float2 h = __ldg(reinterpret_cast<const float2*>(Hin + (size_t)S.src[wq][i] * F) + lane);
+                const float4 ua = S.u[wq][i][0], ub = S.u[wq][i][1];
+                float2 sv = f2mul(P2[0], bc2(ua.x));
+                sv = f2fma(P2[1], bc2(ua.y), sv);
+                sv = f2fma(P2[2], bc2(ua.z), sv);
+                sv = f2fma(P2[3], bc2(ua.w), sv);
+                sv = f2fma(P2[4], bc2(ub.x), sv);
+                sv = f2fma(P2[5], bc2(ub.y), sv);
+                sv = f2fma(P2[6], bc2(ub.z), sv);
+                sv = f2fma(P2[7], bc2(ub.w), sv);
+                m = f2fma(h, sv, m);
+            }
+            __syncwarp();
+        }
+        // z = W m + b: m broadcast from shared memory, W column pair per lane
+        reinterpret_cast<float2*>(S.m[wq])[lane] = m;
+        __syncwarp();
+        float2 z = b2;
+#pragma unroll 4
+        for (int q4 = 0; q4 < F / 4; ++q4) {
+            const float4 mm = S.m[wq][q4];
+            z = f2fma(S.WT[4 * q4][lane], bc2(mm.x), z);
+            z = f2fma(S.WT[4 * q4 + 1][lane], bc2(mm.y), z);
+            z = f2fma(S.WT[4 * q4 + 2][lane], bc2(mm.z), z);
+            z = f2fma(S.WT[4 * q4 + 3][lane], bc2(mm.w), z);
+        }
+        __syncwarp();
+        const float2 th = make_float2(tanhf(z.x), tanhf(z.y));
+        const float2 hin = reinterpret_cast<const float2*>(Hin + (size_t)r * F)[lane];
+        const float2 hn = make_float2(hin.x + th.x, hin.y + th.y);
+        reinterpret_cast<float2*>(Hout + (size_t)r * F)[lane] = hn;
+        note_nonfinite(a, layer, r, hn.x);
+        note_nonfinite(a, layer, r, hn.y);
+        reinterpret_cast<float2*>(TH + (size_t)k * F)[lane] = th;
+        if (per_atom) {
+            const float ev = gwarp_sum(fmaf(ro2.x, hn.x, ro2.y * hn.y));
+            if (lane == 0) per_atom[v] = (double)ev;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// backward node pass: MB[row] = W^T (HB (.) (1 - th^2)), lane = feature pair
+// ---------------------------------------------------------------------------
+// (also the three-body q_bar = W4^T (HB (.) (1 - TH4^2)) with W = W4)
+__global__ void __launch_bounds__(kConvWarps * 32) k_wide_bwd_node(GenModel g, int64_t n,
+                                                                   const int32_t* __restrict__ nodes,
+                                                                   const int32_t* __restrict__ crow,
+                                                                   const float* __restrict__ W,
+                                                                   float* __restrict__ HB,
+                                                                   const float* __restrict__ TH,
+                                                                   float* __restrict__ MB, int init) {
+    __shared__ __align__(16) float2 sW[F][F / 2];  // sW[f][l] = (W[f][2l], W[f][2l+1])
+    __shared__ __align__(16) float4 sy[kConvWarps][F / 4];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < F * F / 2; t += blockDim.x)
+        sW[t / (F / 2)][t % (F / 2)] = reinterpret_cast<const float2*>(W)[t];
+    const float2 ro2 = make_float2(g.ro[2 * lane], g.ro[2 * lane + 1]);
+    __syncthreads();
+    for (int64_t k = (int64_t)blockIdx.x * kConvWarps + wq; k < n; k += (int64_t)gridDim.x * kConvWarps) {
+        const int64_t v = nodes ? (int64_t)nodes[k] : k;
+        const int64_t r = crow ? (int64_t)crow[v] : v;
+        float2 hb;
+        if (init) {  // h_bar starts as the readout (potential.cpp:800-806)
+            hb = ro2;
+            reinterpret_cast<float2*>(HB + (size_t)k * F)[lane] = hb;
+        } else {
+            hb = reinterpret_cast<const float2*>(HB + (size_t)k * F)[lane];
+        }
+        const float2 th = reinterpret_cast<const float2*>(TH + (size_t)k * F)[lane];
+        const float2 y = make_float2(hb.x * (1.0f - th.x * th.x), hb.y * (1.0f - th.y * th.y));
+        reinterpret_cast<float2*>(sy[wq])[lane] = y;
+        __syncwarp();
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int f4 = 0; f4 < F / 4; ++f4) {
+            const float4 yy = sy[wq][f4];
+            acc = f2fma(sW[4 * f4][lane], bc2(yy.x), acc);
+            acc = f2fma(sW[4 * f4 + 1][lane], bc2(yy.y), acc);
+            acc = f2fma(sW[4 * f4 + 2][lane], bc2(yy.z), acc);
+            acc = f2fma(sW[4 * f4 + 3][lane], bc2(yy.w), acc);
+        }
+        __syncwarp();
+        reinterpret_cast<float2*>(MB + (size_t)r * F)[lane] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// backward edge pass with the K = 64 contraction on tcgen05
+// ---------------------------------------------------------------------------
+constexpr int kBW = 8;            // warps per CTA: 8 x 16 edge slots = MMA M = 128
+constexpr int kSlots = 16;        // edge slots per warp and step (warps w and w + 4 share a TMEM lane quarter)
+constexpr int kXLbo = 144;        // bytes between K-adjacent core matrices (16 B pad: conflict-free stores)
+constexpr int kXSbo = 16 * kXLbo; // bytes between 8-row groups (64 K = 16 core matrices)
+constexpr int kXBytes = 16 * kXSbo;  // 128 rows
+constexpr int kPLbo = 128, kPSbo = 16 * kPLbo;
+constexpr int kPBytes = 2 * kPSbo;   // N = 16 rows (P^T in rows 0..7, zeros in 8..15)
+constexpr int kNcols = 16;           // MMA N (TMEM columns used)
+
+struct BwdSmem {
+    unsigned char x_hi[kXBytes];
+    unsigned char x_lo[kXBytes];
+    unsigned char p_hi[kPBytes];
+    unsigned char p_lo[kPBytes];
+    float4 u[kBW][kSlots][2];  // fc * phi of the chunk's edges
+    int src[kBW][kSlots];
+    uint64_t mbar;
+    uint32_t tbase;
+};
+
+__device__ __forceinline__ int xoff(int r, int k) {  // byte offset of (row r, K index k)
+    return (r >> 3) * kXSbo + (k >> 2) * kXLbo + (r & 7) * 16 + (k & 3) * 4;
+}
+__device__ __forceinline__ int poff(int r, int k) {
+    return (r >> 3) * kPSbo + (k >> 2) * kPLbo + (r & 7) * 16 + (k & 3) * 4;
+}
+
+// shared-memory descriptor, K-major, no swizzle, explicit offsets
+__device__ __forceinline__ uint64_t sdesc2(const void* base, uint32_t lbo, uint32_t sbo) {
+    const uint64_t addr = tc::smem_u32(base);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void split2(float2 x, float2& hi, float2& lo) {
+    tc::split_tf32(x.x, hi.x, lo.x);
+    tc::split_tf32(x.y, hi.y, lo.y);
+}
+
+__global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis bs, ConvArgs a,
+                                                              const float* __restrict__ MB,
+                                                              const float* __restrict__ Hl,
+                                                              float* __restrict__ HB,
+                                                              float4* __restrict__ GRAD,
+                                                              double* __restrict__ vir_part) {
+    extern __shared__ __align__(1024) unsigned char wsm[];
+    BwdSmem& S = *reinterpret_cast<BwdSmem*>(wsm);
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    // B operand: B[n][f] = P[f][n] (n < 8), 0 (n >= 8); tf32 hi / lo
+    for (int t = tid; t < kNcols * F; t += blockDim.x) {
+        const int nn = t / F, f = t % F;
+        const float x = nn < K ? g.P[f * K + nn] : 0.0f;
+        float hv, lv;
+        tc::split_tf32(x, hv, lv);
+        *reinterpret_cast<float*>(S.p_hi + poff(nn, f)) = hv;
+        *reinterpret_cast<float*>(S.p_lo + poff(nn, f)) = lv;
+    }
+    if (tid == 0) {
+        tc::mbar_init(&S.mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (wq == 0) tc::tmem_alloc(&S.tbase, 32);
+    float2 P2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) P2[k] = make_float2(g.P[(2 * lane) * K + k], g.P[(2 * lane + 1) * K + k]);
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = S.tbase;
+    const uint32_t idesc = tc::idesc_tf32(128, kNcols);
+    // rows of warp w: lane quarter w % 4, slots 16 (w / 4) .. 16 (w / 4) + 15
+    const int row0 = 32 * (wq & 3) + kSlots * (wq >> 2);
+    const uint32_t trow = tmem + ((uint32_t)(32 * (wq & 3)) << 16);
+
+    // this warp's node sequence; all warps step together (one MMA per step)
+    const int64_t gw = (int64_t)blockIdx.x * kBW + wq, nw = (int64_t)gridDim.x * kBW;
+    const int64_t my_nodes = gw < a.n ? (a.n - 1 - gw) / nw + 1 : 0;
+    // steps of this CTA = max over its warps of sum of ceil(deg / 32): the
+    // first warp of the CTA has the most nodes; count chunks per warp and
+    // agree on the maximum through shared memory
+    __shared__ int steps_w[kBW];
+    int my_steps = 0;
+    for (int64_t j = lane; j < my_nodes; j += 32) {
+        const int64_t kk = gw + j * nw;
+        const int64_t vv = a.nodes ? (int64_t)a.nodes[kk] : kk;
+        const int deg = a.row[vv + 1] - a.row[vv];
+        my_steps += deg > 0 ? (deg + kSlots - 1) / kSlots : 1;  // empty rows still finalize
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_steps += __shfl_xor_sync(kFull, my_steps, o);
+    if (lane == 0) steps_w[wq] = my_steps;
+    __syncthreads();
+    int steps = 0;
+    for (int w = 0; w < kBW; ++w) steps = max(steps, steps_w[w]);
+
+    double vir[6] = {0, 0, 0, 0, 0, 0};
+    int64_t jn = 0;            // index of the current node in this warp's sequence
+    int64_t k = -1, v = 0;     // current node (-1: none yet)
+    int pos = 0, e1 = 0;
+    float2 mu = make_float2(0.f, 0.f), hu = mu, hb = mu;
+    float gx = 0.f, gy = 0.f, gz = 0.f;
+    float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint32_t phase = 0;
+    auto finish = [&]() {  // node k complete: one writer per element
+        if (k < 0) return;
+        float2* hbp = reinterpret_cast<float2*>(HB + (size_t)k * F) + lane;
+        const float2 old = *hbp;
+        *hbp = make_float2(old.x + hb.x, old.y + hb.y);
+        const float sx = gwarp_sum(gx), sy = gwarp_sum(gy), sz = gwarp_sum(gz);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
+        if (lane == 0) {
+            float4 gr = GRAD[k];
+            gr.x += sx;
+            gr.y += sy;
+            gr.z += sz;
+            GRAD[k] = gr;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) vir[c] += (double)vr[c];
+        }
+    };
+    for (int step = 0; step < steps; ++step) {
+        // (1) next node when the current one is done
+        if (pos >= e1) {
+            finish();
+            k = -1;
+            if (jn < my_nodes) {
+                k = gw + jn * nw;
+                ++jn;
+                v = a.nodes ? (int64_t)a.nodes[k] : k;
+                const int64_t r = a.crow ? (int64_t)a.crow[v] : v;
+                pos = a.row[v];
+                e1 = a.row[v + 1];
+                mu = reinterpret_cast<const float2*>(MB + (size_t)r * F)[lane];
+                hu = reinterpret_cast<const float2*>(Hl + (size_t)r * F)[lane];
+                hb = make_float2(0.f, 0.f);
+                gx = gy = gz = 0.f;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) vr[c] = 0.f;
+            } else {
+                pos = e1 = 0;
+            }
+        }
+        const int ne = k >= 0 ? min(kSlots, e1 - pos) : 0;
+        // (2) per-edge scalars, lane = edge slot
+        float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
+        float psi[K];
+        if (lane < ne) {
+            q = __ldg(a.vd + pos + lane);
+            const float d = q.w;
+            float phi[K];
+            phi8(bs, d, phi);
+            float sn, cs;
+            __sincosf(d * bs.pi_rc, &sn, &cs);
+            const bool in = d < bs.rc;
+            const float fc = in ? 0.5f * cs + 0.5f : 0.0f;
+            const float dfc = in ? -0.5f * bs.pi_rc * sn : 0.0f;
+            const float x0 = d * bs.isg, stp = bs.mus * bs.isg;
+            const float ca = dfc - 2.0f * fc * bs.isg * x0, cb = 2.0f * fc * bs.isg * stp;
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) psi[kk] = phi[kk] * fmaf(cb, (float)kk, ca);
+            S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
+            S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+            S.src[wq][lane] = a.lsrc[pos + lane];
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < K; ++kk) psi[kk] = 0.f;
+        }
+        __syncwarp();
+        // (3) feature lanes: hbar, and X rows (tf32 hi / lo) of the A operand;
+        // eight edges' rows in flight
+        for (int i0 = 0; i0 < ne; i0 += 8) {
+            float2 mw[8], hw[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (i0 + j < ne) {
+                    const int w = S.src[wq][i0 + j];
+                    mw[j] = __ldg(reinterpret_cast<const float2*>(MB + (size_t)w * F) + lane);
+                    hw[j] = __ldg(reinterpret_cast<const float2*>(Hl + (size_t)w * F) + lane);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = i0 + j;
+                if (i < ne) {
+                    const float4 ua = S.u[wq][i][0], ub = S.u[wq][i][1];
+                    float2 sv = f2mul(P2[0], bc2(ua.x));
+                    sv = f2fma(P2[1], bc2(ua.y), sv);
+                    sv = f2fma(P2[2], bc2(ua.z), sv);
+                    sv = f2fma(P2[3], bc2(ua.w), sv);
+                    sv = f2fma(P2[4], bc2(ub.x), sv);
+                    sv = f2fma(P2[5], bc2(ub.y), sv);
+                    sv = f2fma(P2[6], bc2(ub.z), sv);
+                    sv = f2fma(P2[7], bc2(ub.w), sv);
+                    hb = f2fma(mw[j], sv, hb);
+                    const float2 x = f2fma(hu, mw[j], f2mul(mu, hw[j]));
+                    float2 xh, xl;
+                    split2(x, xh, xl);
+                    const int off = xoff(row0 + i, 2 * lane);
+                    *reinterpret_cast<float2*>(S.x_hi + off) = xh;
+                    *reinterpret_cast<float2*>(S.x_lo + off) = xl;
+                }
+            }
+        }
+        // (4) G = X P on the tensor cores (3xTF32), one thread issues
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (tid == 0) {
+#pragma unroll
+            for (int ks = 0; ks < F / 8; ++ks) {
+                const uint64_t ah = sdesc2(S.x_hi + ks * 2 * kXLbo, kXLbo, kXSbo);
+                const uint64_t al = sdesc2(S.x_lo + ks * 2 * kXLbo, kXLbo, kXSbo);
+                const uint64_t bh = sdesc2(S.p_hi + ks * 2 * kPLbo, kPLbo, kPSbo);
+                const uint64_t bl = sdesc2(S.p_lo + ks * 2 * kPLbo, kPLbo, kPSbo);
+                tc::mma_tf32(tmem, ah, bh, idesc, ks > 0);
+                tc::mma_tf32(tmem, al, bh, idesc, true);
+                tc::mma_tf32(tmem, ah, bl, idesc, true);
+            }
+            tc::commit(&S.mbar);
+        }
+        tc::mbar_wait(&S.mbar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        // (5) edge lanes: dsum, gradient, virial (the lane that computed the
+        // slot's scalars reads the slot's TMEM row)
+        float G[8];
+        tmem_ld8(trow, G);
+        {
+            float Gs[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) Gs[kk] = __shfl_sync(kFull, G[kk], (lane + kSlots * (wq >> 2)) & 31);
+            if (lane < ne) {
+                float dsum = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) dsum = fmaf(psi[kk], Gs[kk], dsum);
+                const float coef = dsum / q.w;
+                gx = fmaf(-q.x, coef, gx);
+                gy = fmaf(-q.y, coef, gy);
+                gz = fmaf(-q.z, coef, gz);
+                const float ch = 0.5f * coef;
+                vr[0] = fmaf(ch * q.x, q.x, vr[0]);
+                vr[1] = fmaf(ch * q.y, q.y, vr[1]);
+                vr[2] = fmaf(ch * q.z, q.z, vr[2]);
+                vr[3] = fmaf(ch * q.x, q.y, vr[3]);
+                vr[4] = fmaf(ch * q.x, q.z, vr[4]);
+                vr[5] = fmaf(ch * q.y, q.z, vr[5]);
+            }
+        }
+        pos += ne;
+        tc::fence_before();
+        __syncthreads();  // every warp has read its TMEM rows before the next MMA
+        tc::fence_after();
+    }
+    if (pos >= e1) finish();
+    // fp64 virial: warp records in fixed order -> CTA record
+    __shared__ double wv[kBW][6];
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) wv[wq][c] = vir[c];
+    tc::fence_before();
+    __syncthreads();
+    if (tid < 6) {
+        double acc = 0.0;
+        for (int w = 0; w < kBW; ++w) acc += wv[w][tid];
+        vir_part[(size_t)blockIdx.x * 6 + tid] = acc;
+    }
+    if (wq == 0) tc::tmem_free(tmem, 32);
+}
+
+
+// ---------------------------------------------------------------------------
+// three-body stage (potential.cpp:664-741, 850-961), the generic kernels'
+// slot conventions: slot j of center s = in-bond b0 + j (x_j -> s); TP / TH3 /
+// SMR slot j belong to its reverse, the out-bond (s -> x_j)
+// ---------------------------------------------------------------------------
+struct Basis3 {
+    float r3, pi_r3, isg3, mus3;
+};
+__host__ Basis3 make_basis3(const GenModel& g) {
+    return Basis3{g.r3, 3.14159265358979f * g.inv_r3, g.inv_sigma3, g.mu_step3};
+}
+__device__ __forceinline__ void fcut3w(const Basis3& b, float d, float& fc, float& dfc) {
+    float sn, cs;
+    sincospif(d / b.r3, &sn, &cs);
+    const bool in = d < b.r3;
+    fc = in ? 0.5f * (cs + 1.0f) : 0.0f;
+    dfc = in ? -0.5f * b.pi_r3 * sn : 0.0f;
+}
+// u3_k (with fc3) or its derivative du3_k, k = 0..7 (uniform across the warp)
+__device__ __forceinline__ void u3w(const Basis3& b, float d, float u[K], bool deriv) {
+    float fc, dfc;
+    fcut3w(b, d, fc, dfc);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float x = (d - b.mus3 * (float)k) * b.isg3;
+        const float e = expf(-x * x);
+        u[k] = deriv ? e * (dfc - 2.0f * fc * x * b.isg3) : fc * e;
+    }
+}
+// the same, lane k < 8 evaluating u3_k and broadcasting it (warp-uniform d)
+__device__ __forceinline__ void u3l(const Basis3& b, float d, int lane, float u[K], bool deriv) {
+    float fc, dfc;
+    fcut3w(b, d, fc, dfc);
+    float mine = 0.f;
+    if (lane < K) {
+        const float x = (d - b.mus3 * (float)lane) * b.isg3;
+        const float e = expf(-x * x);
+        mine = deriv ? e * (dfc - 2.0f * fc * x * b.isg3) : fc * e;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) u[k] = __shfl_sync(kFull, mine, k);
+}
+__device__ __forceinline__ float2 p3dot(const float2 P32[K], const float u[K]) {
+    float2 t = f2mul(P32[0], bc2(u[0]));
+#pragma unroll
+    for (int k = 1; k < K; ++k) t = f2fma(P32[k], bc2(u[k]), t);
+    return t;
+}
+
+// TT[b] = P3 u3(d_b) for the in-bonds of every center
+__global__ void __launch_bounds__(kConvWarps * 32) k_wide_tb_t(GenModel g, Basis3 b3, BondArgs a,
+                                                               float* __restrict__ TT) {
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    float2 P32[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) P32[k] = make_float2(g.P3[(2 * lane) * K + k], g.P3[(2 * lane + 1) * K + k]);
+    for (int64_t k = (int64_t)blockIdx.x * kConvWarps + wq; k < a.n; k += (int64_t)gridDim.x * kConvWarps) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
+        for (int b = a.brow[s]; b < a.brow[s + 1]; ++b) {
+            float u[K];
+            u3l(b3, a.vd[a.bedge[b]].w, lane, u, false);
+            reinterpret_cast<float2*>(TT + (size_t)b * F)[lane] = p3dot(P32, u);
+        }
+    }
+}
+
+// q_u = sum_{b into u} t'_rev(b) (ascending b), h_u += tanh(W4 q_u), TH4
+__global__ void __launch_bounds__(kConvWarps * 32) k_wide_tb_inject(GenModel g, BondArgs a,
+                                                                    const float* __restrict__ TP,
+                                                                    float* __restrict__ H,
+                                                                    float* __restrict__ TH4) {
+    __shared__ __align__(16) float2 sWT[F][F / 2];  // (W4[2l][q], W4[2l+1][q])
+    __shared__ __align__(16) float4 sq[kConvWarps][F / 4];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < F * F / 2; t += blockDim.x) {
+        const int q = t / (F / 2), l = t % (F / 2);
+        sWT[q][l] = make_float2(g.W4[(2 * l) * F + q], g.W4[(2 * l + 1) * F + q]);
+    }
+    __syncthreads();
+    for (int64_t k = (int64_t)blockIdx.x * kConvWarps + wq; k < a.n; k += (int64_t)gridDim.x * kConvWarps) {
+        const int64_t u = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int64_t r = a.crow ? (int64_t)a.crow[u] : u;
+        float2 q = make_float2(0.f, 0.f);
+        for (int b = a.brow[u]; b < a.brow[u + 1]; ++b) {
+            const float2 t = reinterpret_cast<const float2*>(TP + (size_t)a.brev[b] * F)[lane];
+            q.x += t.x;
+            q.y += t.y;
+        }
+        reinterpret_cast<float2*>(sq[wq])[lane] = q;
+        __syncwarp();
+        float2 z = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int q4 = 0; q4 < F / 4; ++q4) {
+            const float4 mm = sq[wq][q4];
+            z = f2fma(sWT[4 * q4][lane], bc2(mm.x), z);
+            z = f2fma(sWT[4 * q4 + 1][lane], bc2(mm.y), z);
+            z = f2fma(sWT[4 * q4 + 2][lane], bc2(mm.z), z);
+            z = f2fma(sWT[4 * q4 + 3][lane], bc2(mm.w), z);
+        }
+        __syncwarp();
+        const float2 th = make_float2(tanhf(z.x), tanhf(z.y));
+        float2* hp = reinterpret_cast<float2*>(H + (size_t)r * F) + lane;
+        const float2 h0 = *hp;
+        *hp = make_float2(h0.x + th.x, h0.y + th.y);
+        reinterpret_cast<float2*>(TH4 + (size_t)k * F)[lane] = th;
+    }
+}
+
+// per-bond dense contraction Y = X W^T (N = K = 64) on tcgen05: each warp
+// stages <= 16 slot rows per step (X in tf32 hi / lo); one thread issues
+// the CTA's 24 MMAs; the row's owner lane then reads its 64 outputs
+constexpr int kTW = 8;           // warps per CTA
+constexpr int kWBytes = 8 * kPSbo;  // 64 rows (N) x 64 K, dense (LBO 128, SBO 2048)
+
+struct TbSmem {
+    unsigned char x_hi[kXBytes];
+    unsigned char x_lo[kXBytes];
+    unsigned char w_hi[kWBytes];
+    unsigned char w_lo[kWBytes];
+    int slot_b[kTW][kSlots];    // bond row of each slot
+    float4 sq[kTW][32];         // bond vectors of the current center (first 32)
+    int steps_w[kTW];
+    uint64_t mbar;
+    uint32_t tbase;
+};
+
+// B operand: B[n][k] = Wsrc[n * ldn + k * ldk] (tf32 hi / lo)
+__device__ __forceinline__ void stage_w(TbSmem& S, const float* Wsrc, int ldn, int ldk) {
+    for (int t = threadIdx.x; t < F * F; t += blockDim.x) {
+        const int nn = t / F, kk = t % F;
+        float hv, lv;
+        tc::split_tf32(Wsrc[nn * ldn + kk * ldk], hv, lv);
+        *reinterpret_cast<float*>(S.w_hi + poff(nn, kk)) = hv;
+        *reinterpret_cast<float*>(S.w_lo + poff(nn, kk)) = lv;
+    }
+}
+
+__device__ __forceinline__ void tb_mma(TbSmem& S, uint32_t tmem, uint32_t& phase) {
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = tc::idesc_tf32(128, F);
+#pragma unroll
+        for (int ks = 0; ks < F / 8; ++ks) {
+            const uint64_t ah = sdesc2(S.x_hi + ks * 2 * kXLbo, kXLbo, kXSbo);
+            const uint64_t al = sdesc2(S.x_lo + ks * 2 * kXLbo, kXLbo, kXSbo);
+            const uint64_t bh = sdesc2(S.w_hi + ks * 2 * kPLbo, kPLbo, kPSbo);
+            const uint64_t bl = sdesc2(S.w_lo + ks * 2 * kPLbo, kPLbo, kPSbo);
+            tc::mma_tf32(tmem, ah, bh, idesc, ks > 0);
+            tc::mma_tf32(tmem, al, bh, idesc, true);
+            tc::mma_tf32(tmem, ah, bl, idesc, true);
+        }
+        tc::commit(&S.mbar);
+    }
+    tc::mbar_wait(&S.mbar, phase);
+    phase ^= 1u;
+    tc::fence_after();
+}
+
+__device__ __forceinline__ void stage_row(TbSmem& S, int row, int lane, float2 x) {
+    float2 xh, xl;
+    split2(x, xh, xl);
+    const int off = xoff(row, 2 * lane);
+    *reinterpret_cast<float2*>(S.x_hi + off) = xh;
+    *reinterpret_cast<float2*>(S.x_lo + off) = xl;
+}
+
+// the 64 outputs of this lane's TMEM row
+__device__ __forceinline__ void tmem_row64(uint32_t trow, float z[F]) {
+    tc::tmem_ld32(trow, z);
+    tc::tmem_ld32(trow + 32, z + 32);
+}
+
+// CTA-wide step count: every step packs 16 slots of a warp's consecutive
+// centers, so a warp needs ceil(sum_centers n / 16) steps; max over warps
+// (packed = false: every step holds slots of one center, sum of ceil(n / 16))
+__device__ __forceinline__ int tb_steps(const BondArgs& a, int64_t gw, int64_t nw, int64_t my, int lane,
+                                        int wq, int* steps_w, bool packed = true) {
+    int st = 0;
+    for (int64_t j = lane; j < my; j += 32) {
+        const int64_t kk = gw + j * nw;
+        const int64_t s = a.nodes ? (int64_t)a.nodes[kk] : kk;
+        const int nbj = a.brow[s + 1] - a.brow[s];
+        st += packed ? nbj : (nbj + kSlots - 1) / kSlots;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) st += __shfl_xor_sync(kFull, st, o);
+    if (lane == 0) steps_w[wq] = packed ? (st + kSlots - 1) / kSlots : st;
+    __syncthreads();
+    int steps = 0;
+    for (int w = 0; w < kTW; ++w) steps = max(steps, steps_w[w]);
+    return steps;
+}
+
+// forward: per out-slot j of center s, m3 = sum_{o != j} c(o, j) t_o
+// (ascending o, c = v_o . v_j / (d_o d_j)); z3 = W3 m3 on tcgen05;
+// TP = t_j + fc3(d_j) tanh(z3), TH3 = tanh(z3)
+__global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Basis3 b3, BondArgs a,
+                                                                 const float* __restrict__ TT,
+                                                                 float* __restrict__ TP,
+                                                                 float* __restrict__ TH3) {
+    extern __shared__ __align__(1024) unsigned char wsm[];
+    TbSmem& S = *reinterpret_cast<TbSmem*>(wsm);
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    stage_w(S, g.W3, F, 1);  // B[n][k] = W3[n][k]: z_n = sum_k W3[n][k] m_k
+    if (tid == 0) {
+        tc::mbar_init(&S.mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (wq == 0) tc::tmem_alloc(&S.tbase, F);
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = S.tbase;
+    const int row0 = 32 * (wq & 3) + kSlots * (wq >> 2);
+    const uint32_t trow = tmem + ((uint32_t)(32 * (wq & 3)) << 16);
+    const bool owner = (lane >> 4) == (wq >> 2);
+    const int oslot = lane & 15;
+    const int64_t gw = (int64_t)blockIdx.x * kTW + wq, nw = (int64_t)gridDim.x * kTW;
+    const int64_t my = gw < a.n ? (a.n - 1 - gw) / nw + 1 : 0;
+    const int steps = tb_steps(a, gw, nw, my, lane, wq, S.steps_w, false);
+
+    uint32_t phase = 0;
+    int64_t jn = 0;
+    int b0 = 0, nb = 0, jpos = 0;  // current center: bonds [b0, b0 + nb), next slot jpos
+    for (int step = 0; step < steps; ++step) {
+        while (jpos >= nb && jn < my) {  // next center with bonds
+            const int64_t kk = gw + jn * nw;
+            ++jn;
+            const int64_t s = a.nodes ? (int64_t)a.nodes[kk] : kk;
+            b0 = a.brow[s];
+            nb = a.brow[s + 1] - b0;
+            jpos = 0;
+            __syncwarp();
+            for (int o = lane; o < nb && o < 32; o += 32) S.sq[wq][o] = a.vd[a.bedge[b0 + o]];
+            __syncwarp();
+        }
+        // slots jpos .. jpos + ns - 1 of this center; o outer so each t_o row
+        // is read once per step, m3 of the step's slots in registers
+        const int ns = jpos < nb ? min(kSlots, nb - jpos) : 0;
+        auto qof = [&](int o) { return o < 32 ? S.sq[wq][o] : a.vd[a.bedge[b0 + o]]; };
+        float4 qmine = make_float4(0.f, 0.f, 0.f, 1.f);  // lane i < ns: slot i's bond vector
+        if (lane < ns) qmine = qof(jpos + lane);
+        float2 m3[kSlots];
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i) m3[i] = make_float2(0.f, 0.f);
+        for (int o = 0; o < nb && ns > 0; ++o) {
+            const float2 tv = __ldg(reinterpret_cast<const float2*>(TT + (size_t)(b0 + o) * F) + lane);
+            const float4 qo = qof(o);
+            // c(o, j) = v_o . v_j / (d_o d_j), lane i for slot i (0 for o == j)
+            const float cm = (lane < ns && jpos + lane != o)
+                                 ? (qo.x * qmine.x + qo.y * qmine.y + qo.z * qmine.z) / (qo.w * qmine.w)
+                                 : 0.f;
+#pragma unroll
+            for (int i = 0; i < kSlots; ++i) {
+                const float ci = __shfl_sync(kFull, cm, i);
+                if (i < ns && jpos + i != o) m3[i] = f2fma(bc2(ci), tv, m3[i]);  // ascending o
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i)
+            if (i < ns) stage_row(S, row0 + i, lane, m3[i]);
+        if (lane < ns) S.slot_b[wq][lane] = b0 + jpos + lane;
+        jpos += ns;
+        __syncwarp();
+        tb_mma(S, tmem, phase);
+        float z[F];
+        tmem_row64(trow, z);
+        if (owner && oslot < ns) {
+            const int b = S.slot_b[wq][oslot];
+            const float d = a.vd[a.bedge[b]].w;
+            float fc, dfc;
+            fcut3w(b3, d, fc, dfc);
+            const float4* tt = reinterpret_cast<const float4*>(TT + (size_t)b * F);
+            float4* tp = reinterpret_cast<float4*>(TP + (size_t)b * F);
+            float4* t3 = reinterpret_cast<float4*>(TH3 + (size_t)b * F);
+#pragma unroll
+            for (int c4 = 0; c4 < F / 4; ++c4) {
+                const float4 t = tt[c4];
+                const float4 th = make_float4(tanhf(z[4 * c4]), tanhf(z[4 * c4 + 1]), tanhf(z[4 * c4 + 2]),
+                                              tanhf(z[4 * c4 + 3]));
+                t3[c4] = th;
+                tp[c4] = make_float4(t.x + fc * th.x, t.y + fc * th.y, t.z + fc * th.z, t.w + fc * th.w);
+            }
+        }
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (wq == 0) tc::tmem_free(tmem, F);
+}
+
+// backward phase 1 per slot j (out-bond e'_j = (s -> x_j)): tbar' = q_bar[x_j];
+// VOUT = v_j (-(dbf + da) / d_j) with dbf = tbar' . th3 fc3', da = tbar' . (P3 u3');
+// m_bar_3 = W3^T (tbar' (.) fc3 (1 - th3^2)) on tcgen05 -> SMR
+__global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis3 b3, BondArgs a,
+                                                               const float* __restrict__ QB,
+                                                               const float* __restrict__ TH3,
+                                                               float* __restrict__ SMR,
+                                                               float4* __restrict__ VOUT) {
+    extern __shared__ __align__(1024) unsigned char wsm[];
+    TbSmem& S = *reinterpret_cast<TbSmem*>(wsm);
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    stage_w(S, g.W3, 1, F);  // B[n][k] = W3[k][n]: mbar_n = sum_k W3[k][n] y_k
+    if (tid == 0) {
+        tc::mbar_init(&S.mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (wq == 0) tc::tmem_alloc(&S.tbase, F);
+    float2 P32[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) P32[k] = make_float2(g.P3[(2 * lane) * K + k], g.P3[(2 * lane + 1) * K + k]);
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = S.tbase;
+    const int row0 = 32 * (wq & 3) + kSlots * (wq >> 2);
+    const uint32_t trow = tmem + ((uint32_t)(32 * (wq & 3)) << 16);
+    const bool owner = (lane >> 4) == (wq >> 2);
+    const int oslot = lane & 15;
+    const int64_t gw = (int64_t)blockIdx.x * kTW + wq, nw = (int64_t)gridDim.x * kTW;
+    const int64_t my = gw < a.n ? (a.n - 1 - gw) / nw + 1 : 0;
+    const int steps = tb_steps(a, gw, nw, my, lane, wq, S.steps_w);
+
+    uint32_t phase = 0;
+    int64_t jn = 0;
+    int b0 = 0, nb = 0, jpos = 0;
+    for (int step = 0; step < steps; ++step) {
+        // this step's slots (consecutive bonds of consecutive centers): lane i
+        // takes slot i's bond and loads its indices, all slots in parallel
+        int ns = 0, myb = -1;
+        while (ns < kSlots) {
+            if (jpos >= nb) {
+                if (jn >= my) break;
+                const int64_t kk = gw + jn * nw;
+                ++jn;
+                const int64_t s = a.nodes ? (int64_t)a.nodes[kk] : kk;
+                b0 = a.brow[s];
+                nb = a.brow[s + 1] - b0;
+                jpos = 0;
+                continue;
+            }
+            const int take = min(kSlots - ns, nb - jpos);
+            if (lane >= ns && lane < ns + take) myb = b0 + jpos + (lane - ns);
+            ns += take;
+            jpos += take;
+        }
+        float4 qm = make_float4(0.f, 0.f, 0.f, 1.f);
+        int rxm = 0;
+        if (myb >= 0) {
+            const int e = a.bedge[myb];
+            qm = a.vd[e];
+            const int x = a.esrc[e];
+            rxm = a.crow ? a.crow[x] : x;
+        }
+        for (int i0 = 0; i0 < ns; i0 += 4) {
+            float2 tpb[4], th[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {  // four slots' rows in flight
+                const int i = i0 + jj;
+                const int rx = __shfl_sync(kFull, rxm, i & 31), b = __shfl_sync(kFull, myb, i & 31);
+                if (i < ns) {
+                    tpb[jj] = __ldg(reinterpret_cast<const float2*>(QB + (size_t)rx * F) + lane);
+                    th[jj] = reinterpret_cast<const float2*>(TH3 + (size_t)b * F)[lane];
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int i = i0 + jj;
+                const float qx = __shfl_sync(kFull, qm.x, i & 31), qy = __shfl_sync(kFull, qm.y, i & 31),
+                            qz = __shfl_sync(kFull, qm.z, i & 31), qw = __shfl_sync(kFull, qm.w, i & 31);
+                const int b = __shfl_sync(kFull, myb, i & 31);
+                if (i >= ns) continue;
+                float fc, dfc, du[K];
+                fcut3w(b3, qw, fc, dfc);
+                u3l(b3, qw, lane, du, true);
+                const float2 ds = p3dot(P32, du);
+                float dbf = fmaf(tpb[jj].x * th[jj].x, dfc, (tpb[jj].y * th[jj].y) * dfc);
+                float da = fmaf(tpb[jj].x, ds.x, tpb[jj].y * ds.y);
+                dbf = gwarp_sum(dbf);
+                da = gwarp_sum(da);
+                const float2 y = make_float2(tpb[jj].x * fc * (1.0f - th[jj].x * th[jj].x),
+                                             tpb[jj].y * fc * (1.0f - th[jj].y * th[jj].y));
+                stage_row(S, row0 + i, lane, y);
+                if (lane == 0) {
+                    S.slot_b[wq][i] = b;
+                    const float c0 = -(dbf + da) / qw;
+                    VOUT[b] = make_float4(qx * c0, qy * c0, qz * c0, 0.f);
+                }
+            }
+        }
+        __syncwarp();
+        tb_mma(S, tmem, phase);
+        float z[F];
+        tmem_row64(trow, z);
+        if (owner && oslot < ns) {
+            float4* sm = reinterpret_cast<float4*>(SMR + (size_t)S.slot_b[wq][oslot] * F);
+#pragma unroll
+            for (int c4 = 0; c4 < F / 4; ++c4)
+                sm[c4] = make_float4(z[4 * c4], z[4 * c4 + 1], z[4 * c4 + 2], z[4 * c4 + 3]);
+        }
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (wq == 0) tc::tmem_free(tmem, F);
+}
+
+// backward phase 2 per center s, slot j: the line edges through s.
+//   (a) (e_j, e'_o): tbar_j += c m_bar_3,o; cb = m_bar_3,o . t_j;
+//       VIN_j += -(-v_o/d_o + v_j c / d_j) / d_j cb
+//   (b) (e_o, e'_j): cb2 = m_bar_3,j . t_o; VOUT_j += -(v_o/d_o - v_j c/d_j)/d_j cb2
+//   then VIN_j += v_j db / d_j with db = tbar_j . ds_j, ds_j = P3 u3'(d_j)
+//   virial (VIN - VOUT) (x) v_j.
+// Centers with <= kB2Max bonds (the common case): the center's m_bar_3, t and
+// ds rows are staged in shared memory (row stride 68 floats: 16-byte loads of
+// 8 rows hit distinct banks); C[o][j] = m_bar_3,o . t_j and
+// D[o][j] = m_bar_3,o . ds_j are computed once with lanes over (o, j)
+// (db_j = sum_o c_oj D[o][j]); then lane j sums its pairs over ascending o
+// with no cross-lane reductions.  Larger centers: lanes over o per slot j,
+// rows from global memory.
+constexpr int kB2Warps = 4;
+constexpr int kB2Max = 16;
+constexpr int kRS = F + 4;  // staged row stride (floats)
+
+struct __align__(16) Back2Smem {
+    float rows[kB2Warps][3][kB2Max * kRS];  // m_bar_3 | t | ds rows of the center
+    float C[kB2Warps][kB2Max * kB2Max];
+    float D[kB2Warps][kB2Max * kB2Max];
+    float4 sq[kB2Warps][64];
+};
+
+__device__ __forceinline__ float dot64s(const float* x, const float* y) {
+    const float4* a4 = reinterpret_cast<const float4*>(x);
+    const float4* b4 = reinterpret_cast<const float4*>(y);
+    float acc = 0.f;
+#pragma unroll 4
+    for (int c4 = 0; c4 < F / 4; ++c4) {
+        const float4 u = a4[c4], w = b4[c4];
+        acc = fmaf(u.w, w.w, fmaf(u.z, w.z, fmaf(u.y, w.y, fmaf(u.x, w.x, acc))));
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kB2Warps * 32) k_wide_tb_back2(GenModel g, Basis3 b3, BondArgs a,
+                                                                 const float* __restrict__ TT,
+                                                                 const float* __restrict__ SMR,
+                                                                 float4* __restrict__ VIN,
+                                                                 float4* __restrict__ VOUT,
+                                                                 double* __restrict__ vir_part) {
+    extern __shared__ __align__(16) unsigned char b2sm[];
+    Back2Smem& S = *reinterpret_cast<Back2Smem*>(b2sm);
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    float* smr_s = S.rows[wq][0];
+    float* tt_s = S.rows[wq][1];
+    float* ds_s = S.rows[wq][2];
+    float* Cm = S.C[wq];
+    float* Dm = S.D[wq];
+    float2 P32[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) P32[k] = make_float2(g.P3[(2 * lane) * K + k], g.P3[(2 * lane + 1) * K + k]);
+    double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    auto add_vir = [&](float vix, float viy, float viz, float4 vo, float4 qj) {
+        const double dx = (double)vix - vo.x, dy = (double)viy - vo.y, dz = (double)viz - vo.z;
+        vir[0] += dx * qj.x;
+        vir[1] += dx * qj.y;
+        vir[2] += dx * qj.z;
+        vir[3] += dy * qj.x;
+        vir[4] += dy * qj.y;
+        vir[5] += dy * qj.z;
+        vir[6] += dz * qj.x;
+        vir[7] += dz * qj.y;
+        vir[8] += dz * qj.z;
+    };
+    for (int64_t k = (int64_t)blockIdx.x * kB2Warps + wq; k < a.n; k += (int64_t)gridDim.x * kB2Warps) {
+        const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int b0 = a.brow[s], nb = a.brow[s + 1] - b0;
+        if (nb == 0) continue;
+        __syncwarp();
+        for (int o = lane; o < nb && o < 64; o += 32) S.sq[wq][o] = a.vd[a.bedge[b0 + o]];
+        __syncwarp();
+        auto qof = [&](int o) { return o < 64 ? S.sq[wq][o] : a.vd[a.bedge[b0 + o]]; };
+        if (nb <= kB2Max) {
+            for (int o = 0; o < nb; ++o) {  // coalesced row loads; ds_o = P3 u3'(d_o)
+                const float2 m2 = reinterpret_cast<const float2*>(SMR + (size_t)(b0 + o) * F)[lane];
+                const float2 t2 = reinterpret_cast<const float2*>(TT + (size_t)(b0 + o) * F)[lane];
+                float du[K];
+                u3l(b3, S.sq[wq][o].w, lane, du, true);
+                const float2 d2 = p3dot(P32, du);
+                *reinterpret_cast<float2*>(smr_s + o * kRS + 2 * lane) = m2;
+                *reinterpret_cast<float2*>(tt_s + o * kRS + 2 * lane) = t2;
+                *reinterpret_cast<float2*>(ds_s + o * kRS + 2 * lane) = d2;
+            }
+            __syncwarp();
+            for (int pq = lane; pq < nb * nb; pq += 32) {
+                const int o = pq / nb, j = pq - o * nb;
+                Cm[o * kB2Max + j] = dot64s(smr_s + o * kRS, tt_s + j * kRS);
+                Dm[o * kB2Max + j] = dot64s(smr_s + o * kRS, ds_s + j * kRS);
+            }
+            __syncwarp();
+            if (lane < nb) {
+                const int j = lane;
+                const float4 qj = S.sq[wq][j];
+                const float idj = 1.0f / qj.w;
+                float vi[3] = {0.f, 0.f, 0.f}, vo3[3] = {0.f, 0.f, 0.f}, db = 0.f;
+                const float qw[3] = {qj.x, qj.y, qj.z};
+                for (int o = 0; o < nb; ++o) {
+                    if (o == j) continue;
+                    const float4 qo = S.sq[wq][o];
+                    const float ido = 1.0f / qo.w;
+                    const float c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
+                    const float cb = Cm[o * kB2Max + j], cb2 = Cm[j * kB2Max + o];
+                    db = fmaf(c, Dm[o * kB2Max + j], db);
+                    const float qv[3] = {qo.x, qo.y, qo.z};
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        vi[d] += -(-qv[d] * ido + qw[d] * idj * c) * idj * cb;
+                        vo3[d] += -(qv[d] * ido - qw[d] * idj * c) * idj * cb2;
+                    }
+                }
+                const float vix = vi[0] + qj.x * db * idj, viy = vi[1] + qj.y * db * idj,
+                            viz = vi[2] + qj.z * db * idj;
+                float4 vo = VOUT[b0 + j];
+                vo.x += vo3[0];
+                vo.y += vo3[1];
+                vo.z += vo3[2];
+                VIN[b0 + j] = make_float4(vix, viy, viz, 0.f);
+                VOUT[b0 + j] = vo;
+                add_vir(vix, viy, viz, vo, qj);
+            }
+            continue;
+        }
+        // large centers: lanes over o per slot j, rows from global memory
+        auto gram = [&](const float* x, const float* y) {
+            const float4* x4 = reinterpret_cast<const float4*>(x);
+            const float4* y4 = reinterpret_cast<const float4*>(y);
+            float acc = 0.f;
+            for (int c4 = 0; c4 < F / 4; ++c4) {
+                const float4 u = __ldg(x4 + c4), w = __ldg(y4 + c4);
+                acc = fmaf(u.w, w.w, fmaf(u.z, w.z, fmaf(u.y, w.y, fmaf(u.x, w.x, acc))));
+            }
+            return acc;
+        };
+        for (int j = 0; j < nb; ++j) {
+            const float4 qj = qof(j);
+            const float idj = 1.0f / qj.w;
+            float2 tb = make_float2(0.f, 0.f);
+            float Vi[3] = {0.f, 0.f, 0.f}, Vo[3] = {0.f, 0.f, 0.f};
+            for (int ob = 0; ob < nb; ob += 32) {
+                const int o = ob + lane;
+                float c = 0.f, pi[3] = {0.f, 0.f, 0.f}, po[3] = {0.f, 0.f, 0.f};
+                if (o < nb && o != j) {
+                    const float4 qo = qof(o);
+                    const float ido = 1.0f / qo.w;
+                    c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
+                    const float cb = gram(SMR + (size_t)(b0 + o) * F, TT + (size_t)(b0 + j) * F);
+                    const float cb2 = gram(SMR + (size_t)(b0 + j) * F, TT + (size_t)(b0 + o) * F);
+                    const float qv[3] = {qo.x, qo.y, qo.z}, qw[3] = {qj.x, qj.y, qj.z};
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        pi[d] = -(-qv[d] * ido + qw[d] * idj * c) * idj * cb;
+                        po[d] = -(qv[d] * ido - qw[d] * idj * c) * idj * cb2;
+                    }
+                }
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    Vi[d] += gwarp_sum(pi[d]);
+                    Vo[d] += gwarp_sum(po[d]);
+                }
+                const int oe = min(32, nb - ob);
+                for (int t = 0; t < oe; ++t) {  // tbar_j += c(o, j) m_bar_3,o, ascending o
+                    const float ct = __shfl_sync(kFull, c, t);
+                    if (ob + t == j) continue;
+                    const float2 sm2 = __ldg(reinterpret_cast<const float2*>(SMR + (size_t)(b0 + ob + t) * F) + lane);
+                    tb = f2fma(bc2(ct), sm2, tb);
+                }
+            }
+            float du[K];
+            u3l(b3, qj.w, lane, du, true);
+            const float2 dsj = p3dot(P32, du);
+            const float db = gwarp_sum(fmaf(tb.x, dsj.x, tb.y * dsj.y));
+            const float vix = Vi[0] + qj.x * db * idj, viy = Vi[1] + qj.y * db * idj,
+                        viz = Vi[2] + qj.z * db * idj;
+            if (lane == 0) {
+                float4 vo = VOUT[b0 + j];
+                vo.x += Vo[0];
+                vo.y += Vo[1];
+                vo.z += Vo[2];
+                VIN[b0 + j] = make_float4(vix, viy, viz, 0.f);
+                VOUT[b0 + j] = vo;
+                add_vir(vix, viy, viz, vo, qj);
+            }
+        }
+    }
+    // per-warp virial: lanes' partials summed in lane order by lane 0
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+        double acc = 0.0;
+        for (int l = 0; l < 32; ++l) acc += __shfl_sync(kFull, vir[c], l);
+        if (lane == 0) vir_part[((int64_t)blockIdx.x * kB2Warps + wq) * 9 + c] = acc;
+    }
+}
+
+}  // namespace
+
+int wide_conv_grid(int64_t n) {
+    int64_t g = (n + kConvWarps - 1) / kConvWarps;
+    if (g > 148 * 8) g = 148 * 8;
+    return (int)(g > 0 ? g : 1);
+}
+
+int wide_bwd_grid(int64_t n) {  // two CTAs per SM (shared memory), one wave
+    int64_t g = (n + kBW - 1) / kBW;
+    if (g > 148 * 2) g = 148 * 2;
+    return (int)(g > 0 ? g : 1);
+}
+
+void launch_wide_conv(const GenModel& g, const ConvArgs& a, int layer, const float* Hin, float* Hout,
+                      float* TH, double* per_atom, cudaStream_t s) {
+    if (a.n <= 0) return;
+    k_wide_conv<<<wide_conv_grid(a.n), kConvWarps * 32, 0, s>>>(g, make_basis(g), a, layer, Hin, Hout,
+                                                                TH, per_atom);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_wide_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
+                          int layer, float* HB, const float* TH, float* MB, bool init, cudaStream_t s) {
+    if (n <= 0) return;
+    k_wide_bwd_node<<<wide_conv_grid(n), kConvWarps * 32, 0, s>>>(g, n, nodes, crow,
+                                                                  g.W + (size_t)layer * F * F, HB, TH,
+                                                                  MB, init ? 1 : 0);
+    GMD_LAUNCH_CHECK();
+}
+
+static int back2_grid(int64_t n) {  // three CTAs of 4 warps per SM (shared memory), one wave
+    int64_t gr = (n + kB2Warps - 1) / kB2Warps;
+    if (gr > 148 * 3) gr = 148 * 3;
+    return (int)(gr > 0 ? gr : 1);
+}
+
+int wide_tb_grid(int64_t n) {  // records of launch_wide_tb_backward's virial (9 doubles each)
+    return back2_grid(n) * kB2Warps;
+}
+
+void launch_wide_tb_t(const GenModel& g, const BondArgs& a, float* TT, cudaStream_t s) {
+    if (a.n <= 0) return;
+    k_wide_tb_t<<<wide_conv_grid(a.n), kConvWarps * 32, 0, s>>>(g, make_basis3(g), a, TT);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_wide_tb_inject(const GenModel& g, const BondArgs& a, const float* TP, float* H, float* TH4,
+                           cudaStream_t s) {
+    if (a.n <= 0) return;
+    k_wide_tb_inject<<<wide_conv_grid(a.n), kConvWarps * 32, 0, s>>>(g, a, TP, H, TH4);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_wide_tb_bwd_q(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
+                          const float* HB, const float* TH4, float* QB, cudaStream_t s) {
+    if (n <= 0) return;
+    k_wide_bwd_node<<<wide_conv_grid(n), kConvWarps * 32, 0, s>>>(g, n, nodes, crow, g.W4,
+                                                                  const_cast<float*>(HB), TH4, QB, 0);
+    GMD_LAUNCH_CHECK();
+}
+
+static int tb_tc_grid(int64_t n) {  // two CTAs per SM (shared memory), one wave
+    int64_t gr = (n + kTW - 1) / kTW;
+    if (gr > 148 * 2) gr = 148 * 2;
+    return (int)(gr > 0 ? gr : 1);
+}
+
+void launch_wide_tb_forward(const GenModel& g, const BondArgs& a, const float* TT, float* TP, float* TH3,
+                            cudaStream_t s) {
+    if (a.n <= 0) return;
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_wide_tb_forward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(TbSmem)));
+        attr = true;
+    }
+    k_wide_tb_forward<<<tb_tc_grid(a.n), kTW * 32, sizeof(TbSmem), s>>>(g, make_basis3(g), a, TT, TP, TH3);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_wide_tb_backward(const GenModel& g, const BondArgs& a, const float* QB, const float* TH3,
+                             const float* TT, float* SMR, float4* VIN, float4* VOUT, double* vir_part,
+                             cudaStream_t s) {
+    const int vg = wide_tb_grid(a.n);
+    if (a.n <= 0) {
+        GMD_CUDA(cudaMemsetAsync(vir_part, 0, sizeof(double) * 9 * vg, s));
+        return;
+    }
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_wide_tb_back1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(TbSmem)));
+        attr = true;
+    }
+    k_wide_tb_back1<<<tb_tc_grid(a.n), kTW * 32, sizeof(TbSmem), s>>>(g, make_basis3(g), a, QB, TH3, SMR,
+                                                                       VOUT);
+    GMD_LAUNCH_CHECK();
+    static bool attr2 = false;
+    if (!attr2) {
+        GMD_CUDA(cudaFuncSetAttribute(k_wide_tb_back2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(Back2Smem)));
+        attr2 = true;
+    }
+    k_wide_tb_back2<<<back2_grid(a.n), kB2Warps * 32, sizeof(Back2Smem), s>>>(g, make_basis3(g), a, TT, SMR,
+                                                                             VIN, VOUT, vir_part);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
+                          float* HB, float4* GRAD, double* vir_part, cudaStream_t s) {
+    const int grid = wide_bwd_grid(a.n);
+    if (a.n <= 0) {
+        GMD_CUDA(cudaMemsetAsync(vir_part, 0, sizeof(double) * 6 * grid, s));
+        return;
+    }
+    static bool attr = false;
+    if (!attr) {
+        GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(BwdSmem) + 1024));
+        attr = true;
+    }
+    k_wide_bwd_edge<<<grid, kBW * 32, sizeof(BwdSmem) + 1024, s>>>(g, make_basis(g), a, MB, Hl, HB, GRAD,
+                                                                     vir_part);
+    GMD_LAUNCH_CHECK();
+}
+
+}  // namespace gmd

@@ -140,3 +140,15 @@ def test_tolerance_calibration(oracle_ref):
         # and the stated tolerance is no looser than needed to cover the floor
         assert gpu[k] <= max(floor[k], SURVEY_TOL[k]) and gpu[k] <= tol[k]
         assert tol[k] <= max(2.0 * floor[k], 2.0 * SURVEY_TOL[k])
+
+
+def test_liquid_threebody_at_rc(oracle_ref):
+    """r3 = rc on the C4 liquid: ~52 bonds per center on average and centers
+    with more than 64 in-bonds (the tuned kernels' staging width), which then
+    run the three-body stage on the width-generic kernels; the reference
+    enumerates triplets for any bond count (linegraph.cpp:144-160)."""
+    s = S.liquid(5000)
+    d1 = gpu_create(s, 1, RC)
+    bonds_per_center = np.bincount(d1.graph().dst[d1.line_parts().bonds.edge_of_bond], minlength=s.size())
+    assert bonds_per_center.max() > 64
+    run_config(oracle_ref, s, RC, Fs=(16, 64))
