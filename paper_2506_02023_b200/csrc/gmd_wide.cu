@@ -486,9 +486,9 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
             }
         }
         pos += ne;
-        tc::fence_before();
-        __syncthreads();  // every warp has read its TMEM rows before the next MMA
-        tc::fence_after();
+        // no barrier here: the next MMA is issued after the next step's
+        // barrier, which every warp reaches only after this epilogue's TMEM
+        // reads (fenced before that barrier); X is free once the MMA committed
     }
     if (pos >= e1) finish();
     // fp64 virial: warp records in fixed order -> CTA record
@@ -644,13 +644,13 @@ __device__ __forceinline__ void stage_w(TbSmem& S, const float* Wsrc, int ldn, i
     }
 }
 
-__device__ __forceinline__ void tb_mma(TbSmem& S, uint32_t tmem, uint32_t& phase) {
+__device__ __forceinline__ void tb_mma(TbSmem& S, uint32_t tmem, uint32_t& phase, int N = F) {
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (threadIdx.x == 0) {
-        const uint32_t idesc = tc::idesc_tf32(128, F);
+        const uint32_t idesc = tc::idesc_tf32(128, N);
 #pragma unroll
         for (int ks = 0; ks < F / 8; ++ks) {
             const uint64_t ah = sdesc2(S.x_hi + ks * 2 * kXLbo, kXLbo, kXSbo);
@@ -756,17 +756,25 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Bas
         float2 m3[kSlots];
 #pragma unroll
         for (int i = 0; i < kSlots; ++i) m3[i] = make_float2(0.f, 0.f);
-        for (int o = 0; o < nb && ns > 0; ++o) {
-            const float2 tv = __ldg(reinterpret_cast<const float2*>(TT + (size_t)(b0 + o) * F) + lane);
-            const float4 qo = qof(o);
-            // c(o, j) = v_o . v_j / (d_o d_j), lane i for slot i (0 for o == j)
-            const float cm = (lane < ns && jpos + lane != o)
-                                 ? (qo.x * qmine.x + qo.y * qmine.y + qo.z * qmine.z) / (qo.w * qmine.w)
-                                 : 0.f;
+        for (int o0 = 0; o0 < nb && ns > 0; o0 += 4) {
+            float2 tv[4];
 #pragma unroll
-            for (int i = 0; i < kSlots; ++i) {
-                const float ci = __shfl_sync(kFull, cm, i);
-                if (i < ns && jpos + i != o) m3[i] = f2fma(bc2(ci), tv, m3[i]);  // ascending o
+            for (int jj = 0; jj < 4; ++jj)  // four t rows in flight
+                if (o0 + jj < nb) tv[jj] = __ldg(reinterpret_cast<const float2*>(TT + (size_t)(b0 + o0 + jj) * F) + lane);
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int o = o0 + jj;
+                if (o >= nb) break;
+                const float4 qo = qof(o);
+                // c(o, j) = v_o . v_j / (d_o d_j), lane i for slot i (0 for o == j)
+                const float cm = (lane < ns && jpos + lane != o)
+                                     ? (qo.x * qmine.x + qo.y * qmine.y + qo.z * qmine.z) / (qo.w * qmine.w)
+                                     : 0.f;
+#pragma unroll
+                for (int i = 0; i < kSlots; ++i) {
+                    const float ci = __shfl_sync(kFull, cm, i);
+                    if (i < ns && jpos + i != o) m3[i] = f2fma(bc2(ci), tv[jj], m3[i]);  // ascending o
+                }
             }
         }
 #pragma unroll
@@ -795,30 +803,43 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Bas
                 tp[c4] = make_float4(t.x + fc * th.x, t.y + fc * th.y, t.z + fc * th.z, t.w + fc * th.w);
             }
         }
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
     }
+    tc::fence_before();
+    __syncthreads();
     if (wq == 0) tc::tmem_free(tmem, F);
 }
 
 // backward phase 1 per slot j (out-bond e'_j = (s -> x_j)): tbar' = q_bar[x_j];
 // VOUT = v_j (-(dbf + da) / d_j) with dbf = tbar' . th3 fc3', da = tbar' . (P3 u3');
-// m_bar_3 = W3^T (tbar' (.) fc3 (1 - th3^2)) on tcgen05 -> SMR
+// y = tbar' (.) fc3 (1 - th3^2), m_bar_3 = W3^T y.  Phase 2 only needs
+// m_bar_3 through its products with t_o = P3 u3(d_o) and ds_o = P3 u3'(d_o),
+// i.e. through E = P3^T m_bar_3 = (W3 P3)^T y (8 values per bond): one
+// tcgen05 contraction Y (W3 P3) (M = 128 slots, N = 16 with 8 zero columns,
+// K = 64) writes E instead of the 64-wide m_bar_3 rows
 __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis3 b3, BondArgs a,
                                                                const float* __restrict__ QB,
                                                                const float* __restrict__ TH3,
-                                                               float* __restrict__ SMR,
+                                                               float* __restrict__ EB,
                                                                float4* __restrict__ VOUT) {
     extern __shared__ __align__(1024) unsigned char wsm[];
     TbSmem& S = *reinterpret_cast<TbSmem*>(wsm);
     const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
-    stage_w(S, g.W3, 1, F);  // B[n][k] = W3[k][n]: mbar_n = sum_k W3[k][n] y_k
+    // B[n][f] = sum_q W3[f][q] P3[q][n] (n < 8), 0 (n = 8..15)
+    for (int t = tid; t < 16 * F; t += blockDim.x) {
+        const int nn = t / F, f = t % F;
+        float x = 0.f;
+        if (nn < K)
+            for (int q = 0; q < F; ++q) x = fmaf(g.W3[f * F + q], g.P3[q * K + nn], x);
+        float hv, lv;
+        tc::split_tf32(x, hv, lv);
+        *reinterpret_cast<float*>(S.w_hi + poff(nn, f)) = hv;
+        *reinterpret_cast<float*>(S.w_lo + poff(nn, f)) = lv;
+    }
     if (tid == 0) {
         tc::mbar_init(&S.mbar, 1);
         tc::fence_mbar_init();
     }
-    if (wq == 0) tc::tmem_alloc(&S.tbase, F);
+    if (wq == 0) tc::tmem_alloc(&S.tbase, 32);
     float2 P32[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) P32[k] = make_float2(g.P3[(2 * lane) * K + k], g.P3[(2 * lane + 1) * K + k]);
@@ -903,20 +924,18 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
             }
         }
         __syncwarp();
-        tb_mma(S, tmem, phase);
-        float z[F];
-        tmem_row64(trow, z);
+        tb_mma(S, tmem, phase, 16);
+        float ev[8];
+        tmem_ld8(trow, ev);
         if (owner && oslot < ns) {
-            float4* sm = reinterpret_cast<float4*>(SMR + (size_t)S.slot_b[wq][oslot] * F);
-#pragma unroll
-            for (int c4 = 0; c4 < F / 4; ++c4)
-                sm[c4] = make_float4(z[4 * c4], z[4 * c4 + 1], z[4 * c4 + 2], z[4 * c4 + 3]);
+            float4* ep = reinterpret_cast<float4*>(EB + (size_t)S.slot_b[wq][oslot] * K);
+            ep[0] = make_float4(ev[0], ev[1], ev[2], ev[3]);
+            ep[1] = make_float4(ev[4], ev[5], ev[6], ev[7]);
         }
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
     }
-    if (wq == 0) tc::tmem_free(tmem, F);
+    tc::fence_before();
+    __syncthreads();
+    if (wq == 0) tc::tmem_free(tmem, 32);
 }
 
 // backward phase 2 per center s, slot j: the line edges through s.
@@ -925,112 +944,100 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
 //   (b) (e_o, e'_j): cb2 = m_bar_3,j . t_o; VOUT_j += -(v_o/d_o - v_j c/d_j)/d_j cb2
 //   then VIN_j += v_j db / d_j with db = tbar_j . ds_j, ds_j = P3 u3'(d_j)
 //   virial (VIN - VOUT) (x) v_j.
-// Centers with <= kB2Max bonds (the common case): the center's m_bar_3, t and
-// ds rows are staged in shared memory (row stride 68 floats: 16-byte loads of
-// 8 rows hit distinct banks); C[o][j] = m_bar_3,o . t_j and
-// D[o][j] = m_bar_3,o . ds_j are computed once with lanes over (o, j)
-// (db_j = sum_o c_oj D[o][j]); then lane j sums its pairs over ascending o
-// with no cross-lane reductions.  Larger centers: lanes over o per slot j,
-// rows from global memory.
-constexpr int kB2Warps = 4;
-constexpr int kB2Max = 16;
-constexpr int kRS = F + 4;  // staged row stride (floats)
+// With t = P3 u3 and E = P3^T m_bar_3 (from back1): cb = E_o . u3_j,
+// cb2 = E_j . u3_o, db = sum_o c_oj E_o . u3'_j -- 8-wide products.  The
+// center's per-bond E, u3, u3' and v are staged in shared memory (lane o),
+// then lane j sums its pairs over ascending o (no cross-lane reductions).
+constexpr int kB2Warps = 8;
+constexpr int kB2Max = 64;  // bonds per center staged; larger centers stage in windows
 
 struct __align__(16) Back2Smem {
-    float rows[kB2Warps][3][kB2Max * kRS];  // m_bar_3 | t | ds rows of the center
-    float C[kB2Warps][kB2Max * kB2Max];
-    float D[kB2Warps][kB2Max * kB2Max];
-    float4 sq[kB2Warps][64];
+    float4 q[kB2Warps][kB2Max];
+    float4 e[kB2Warps][kB2Max][2];
+    float4 u[kB2Warps][kB2Max][2];
 };
 
-__device__ __forceinline__ float dot64s(const float* x, const float* y) {
-    const float4* a4 = reinterpret_cast<const float4*>(x);
-    const float4* b4 = reinterpret_cast<const float4*>(y);
-    float acc = 0.f;
-#pragma unroll 4
-    for (int c4 = 0; c4 < F / 4; ++c4) {
-        const float4 u = a4[c4], w = b4[c4];
-        acc = fmaf(u.w, w.w, fmaf(u.z, w.z, fmaf(u.y, w.y, fmaf(u.x, w.x, acc))));
+__device__ __forceinline__ float dot8(float4 a0, float4 a1, const float b[K]) {
+    return fmaf(a1.w, b[7], fmaf(a1.z, b[6], fmaf(a1.y, b[5], fmaf(a1.x, b[4],
+           fmaf(a0.w, b[3], fmaf(a0.z, b[2], fmaf(a0.y, b[1], a0.x * b[0])))))));
+}
+
+__device__ __forceinline__ void u3both(const Basis3& b, float d, float u[K], float du[K]) {
+    float fc, dfc;
+    fcut3w(b, d, fc, dfc);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float x = (d - b.mus3 * (float)k) * b.isg3;
+        const float e = expf(-x * x);
+        u[k] = fc * e;
+        du[k] = e * (dfc - 2.0f * fc * x * b.isg3);
     }
-    return acc;
 }
 
 __global__ void __launch_bounds__(kB2Warps * 32) k_wide_tb_back2(GenModel g, Basis3 b3, BondArgs a,
-                                                                 const float* __restrict__ TT,
-                                                                 const float* __restrict__ SMR,
+                                                                 const float* __restrict__ EB,
                                                                  float4* __restrict__ VIN,
                                                                  float4* __restrict__ VOUT,
                                                                  double* __restrict__ vir_part) {
     extern __shared__ __align__(16) unsigned char b2sm[];
     Back2Smem& S = *reinterpret_cast<Back2Smem*>(b2sm);
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    float* smr_s = S.rows[wq][0];
-    float* tt_s = S.rows[wq][1];
-    float* ds_s = S.rows[wq][2];
-    float* Cm = S.C[wq];
-    float* Dm = S.D[wq];
-    float2 P32[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) P32[k] = make_float2(g.P3[(2 * lane) * K + k], g.P3[(2 * lane + 1) * K + k]);
     double vir[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    auto add_vir = [&](float vix, float viy, float viz, float4 vo, float4 qj) {
-        const double dx = (double)vix - vo.x, dy = (double)viy - vo.y, dz = (double)viz - vo.z;
-        vir[0] += dx * qj.x;
-        vir[1] += dx * qj.y;
-        vir[2] += dx * qj.z;
-        vir[3] += dy * qj.x;
-        vir[4] += dy * qj.y;
-        vir[5] += dy * qj.z;
-        vir[6] += dz * qj.x;
-        vir[7] += dz * qj.y;
-        vir[8] += dz * qj.z;
-    };
     for (int64_t k = (int64_t)blockIdx.x * kB2Warps + wq; k < a.n; k += (int64_t)gridDim.x * kB2Warps) {
         const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
         const int b0 = a.brow[s], nb = a.brow[s + 1] - b0;
-        if (nb == 0) continue;
-        __syncwarp();
-        for (int o = lane; o < nb && o < 64; o += 32) S.sq[wq][o] = a.vd[a.bedge[b0 + o]];
-        __syncwarp();
-        auto qof = [&](int o) { return o < 64 ? S.sq[wq][o] : a.vd[a.bedge[b0 + o]]; };
-        if (nb <= kB2Max) {
-            for (int o = 0; o < nb; ++o) {  // coalesced row loads; ds_o = P3 u3'(d_o)
-                const float2 m2 = reinterpret_cast<const float2*>(SMR + (size_t)(b0 + o) * F)[lane];
-                const float2 t2 = reinterpret_cast<const float2*>(TT + (size_t)(b0 + o) * F)[lane];
-                float du[K];
-                u3l(b3, S.sq[wq][o].w, lane, du, true);
-                const float2 d2 = p3dot(P32, du);
-                *reinterpret_cast<float2*>(smr_s + o * kRS + 2 * lane) = m2;
-                *reinterpret_cast<float2*>(tt_s + o * kRS + 2 * lane) = t2;
-                *reinterpret_cast<float2*>(ds_s + o * kRS + 2 * lane) = d2;
-            }
-            __syncwarp();
-            for (int pq = lane; pq < nb * nb; pq += 32) {
-                const int o = pq / nb, j = pq - o * nb;
-                Cm[o * kB2Max + j] = dot64s(smr_s + o * kRS, tt_s + j * kRS);
-                Dm[o * kB2Max + j] = dot64s(smr_s + o * kRS, ds_s + j * kRS);
-            }
-            __syncwarp();
-            if (lane < nb) {
-                const int j = lane;
-                const float4 qj = S.sq[wq][j];
-                const float idj = 1.0f / qj.w;
-                float vi[3] = {0.f, 0.f, 0.f}, vo3[3] = {0.f, 0.f, 0.f}, db = 0.f;
-                const float qw[3] = {qj.x, qj.y, qj.z};
-                for (int o = 0; o < nb; ++o) {
-                    if (o == j) continue;
-                    const float4 qo = S.sq[wq][o];
-                    const float ido = 1.0f / qo.w;
-                    const float c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
-                    const float cb = Cm[o * kB2Max + j], cb2 = Cm[j * kB2Max + o];
-                    db = fmaf(c, Dm[o * kB2Max + j], db);
-                    const float qv[3] = {qo.x, qo.y, qo.z};
+        for (int jb = 0; jb < nb; jb += 32) {  // slots j = jb + lane
+            const int j = jb + lane;
+            float4 qj = make_float4(0.f, 0.f, 0.f, 1.f), ej0 = make_float4(0.f, 0.f, 0.f, 0.f), ej1 = ej0;
+            float uj[K], duj[K];
+            if (j < nb) {
+                qj = a.vd[a.bedge[b0 + j]];
+                ej0 = reinterpret_cast<const float4*>(EB + (size_t)(b0 + j) * K)[0];
+                ej1 = reinterpret_cast<const float4*>(EB + (size_t)(b0 + j) * K)[1];
+                u3both(b3, qj.w, uj, duj);
+            } else {
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        vi[d] += -(-qv[d] * ido + qw[d] * idj * c) * idj * cb;
-                        vo3[d] += -(qv[d] * ido - qw[d] * idj * c) * idj * cb2;
+                for (int kk = 0; kk < K; ++kk) uj[kk] = duj[kk] = 0.f;
+            }
+            const float idj = 1.0f / qj.w;
+            float vi[3] = {0.f, 0.f, 0.f}, vo3[3] = {0.f, 0.f, 0.f}, db = 0.f;
+            for (int ob = 0; ob < nb; ob += kB2Max) {  // window of staged bonds o
+                const int on = min(kB2Max, nb - ob);
+                __syncwarp();
+                for (int o = lane; o < on; o += 32) {
+                    const float4 qo = a.vd[a.bedge[b0 + ob + o]];
+                    S.q[wq][o] = qo;
+                    S.e[wq][o][0] = reinterpret_cast<const float4*>(EB + (size_t)(b0 + ob + o) * K)[0];
+                    S.e[wq][o][1] = reinterpret_cast<const float4*>(EB + (size_t)(b0 + ob + o) * K)[1];
+                    float uo[K], duo[K];
+                    u3both(b3, qo.w, uo, duo);
+                    S.u[wq][o][0] = make_float4(uo[0], uo[1], uo[2], uo[3]);
+                    S.u[wq][o][1] = make_float4(uo[4], uo[5], uo[6], uo[7]);
+                }
+                __syncwarp();
+                if (j < nb) {
+                    for (int oo = 0; oo < on; ++oo) {
+                        const int o = ob + oo;
+                        if (o == j) continue;  // the reverse pair
+                        const float4 qo = S.q[wq][oo];
+                        const float ido = 1.0f / qo.w;
+                        const float c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
+                        const float4 eo0 = S.e[wq][oo][0], eo1 = S.e[wq][oo][1];
+                        const float4 uo0 = S.u[wq][oo][0], uo1 = S.u[wq][oo][1];
+                        const float uo[K] = {uo0.x, uo0.y, uo0.z, uo0.w, uo1.x, uo1.y, uo1.z, uo1.w};
+                        const float cb = dot8(eo0, eo1, uj);    // m_bar_3,o . t_j
+                        const float cb2 = dot8(ej0, ej1, uo);   // m_bar_3,j . t_o
+                        db = fmaf(c, dot8(eo0, eo1, duj), db);  // c (m_bar_3,o . ds_j)
+                        const float qv[3] = {qo.x, qo.y, qo.z}, qw[3] = {qj.x, qj.y, qj.z};
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            vi[d] += -(-qv[d] * ido + qw[d] * idj * c) * idj * cb;
+                            vo3[d] += -(qv[d] * ido - qw[d] * idj * c) * idj * cb2;
+                        }
                     }
                 }
+            }
+            if (j < nb) {
                 const float vix = vi[0] + qj.x * db * idj, viy = vi[1] + qj.y * db * idj,
                             viz = vi[2] + qj.z * db * idj;
                 float4 vo = VOUT[b0 + j];
@@ -1039,73 +1046,20 @@ __global__ void __launch_bounds__(kB2Warps * 32) k_wide_tb_back2(GenModel g, Bas
                 vo.z += vo3[2];
                 VIN[b0 + j] = make_float4(vix, viy, viz, 0.f);
                 VOUT[b0 + j] = vo;
-                add_vir(vix, viy, viz, vo, qj);
-            }
-            continue;
-        }
-        // large centers: lanes over o per slot j, rows from global memory
-        auto gram = [&](const float* x, const float* y) {
-            const float4* x4 = reinterpret_cast<const float4*>(x);
-            const float4* y4 = reinterpret_cast<const float4*>(y);
-            float acc = 0.f;
-            for (int c4 = 0; c4 < F / 4; ++c4) {
-                const float4 u = __ldg(x4 + c4), w = __ldg(y4 + c4);
-                acc = fmaf(u.w, w.w, fmaf(u.z, w.z, fmaf(u.y, w.y, fmaf(u.x, w.x, acc))));
-            }
-            return acc;
-        };
-        for (int j = 0; j < nb; ++j) {
-            const float4 qj = qof(j);
-            const float idj = 1.0f / qj.w;
-            float2 tb = make_float2(0.f, 0.f);
-            float Vi[3] = {0.f, 0.f, 0.f}, Vo[3] = {0.f, 0.f, 0.f};
-            for (int ob = 0; ob < nb; ob += 32) {
-                const int o = ob + lane;
-                float c = 0.f, pi[3] = {0.f, 0.f, 0.f}, po[3] = {0.f, 0.f, 0.f};
-                if (o < nb && o != j) {
-                    const float4 qo = qof(o);
-                    const float ido = 1.0f / qo.w;
-                    c = (qj.x * qo.x + qj.y * qo.y + qj.z * qo.z) * idj * ido;
-                    const float cb = gram(SMR + (size_t)(b0 + o) * F, TT + (size_t)(b0 + j) * F);
-                    const float cb2 = gram(SMR + (size_t)(b0 + j) * F, TT + (size_t)(b0 + o) * F);
-                    const float qv[3] = {qo.x, qo.y, qo.z}, qw[3] = {qj.x, qj.y, qj.z};
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        pi[d] = -(-qv[d] * ido + qw[d] * idj * c) * idj * cb;
-                        po[d] = -(qv[d] * ido - qw[d] * idj * c) * idj * cb2;
-                    }
-                }
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    Vi[d] += gwarp_sum(pi[d]);
-                    Vo[d] += gwarp_sum(po[d]);
-                }
-                const int oe = min(32, nb - ob);
-                for (int t = 0; t < oe; ++t) {  // tbar_j += c(o, j) m_bar_3,o, ascending o
-                    const float ct = __shfl_sync(kFull, c, t);
-                    if (ob + t == j) continue;
-                    const float2 sm2 = __ldg(reinterpret_cast<const float2*>(SMR + (size_t)(b0 + ob + t) * F) + lane);
-                    tb = f2fma(bc2(ct), sm2, tb);
-                }
-            }
-            float du[K];
-            u3l(b3, qj.w, lane, du, true);
-            const float2 dsj = p3dot(P32, du);
-            const float db = gwarp_sum(fmaf(tb.x, dsj.x, tb.y * dsj.y));
-            const float vix = Vi[0] + qj.x * db * idj, viy = Vi[1] + qj.y * db * idj,
-                        viz = Vi[2] + qj.z * db * idj;
-            if (lane == 0) {
-                float4 vo = VOUT[b0 + j];
-                vo.x += Vo[0];
-                vo.y += Vo[1];
-                vo.z += Vo[2];
-                VIN[b0 + j] = make_float4(vix, viy, viz, 0.f);
-                VOUT[b0 + j] = vo;
-                add_vir(vix, viy, viz, vo, qj);
+                const double dx = (double)vix - vo.x, dy = (double)viy - vo.y, dz = (double)viz - vo.z;
+                vir[0] += dx * qj.x;
+                vir[1] += dx * qj.y;
+                vir[2] += dx * qj.z;
+                vir[3] += dy * qj.x;
+                vir[4] += dy * qj.y;
+                vir[5] += dy * qj.z;
+                vir[6] += dz * qj.x;
+                vir[7] += dz * qj.y;
+                vir[8] += dz * qj.z;
             }
         }
     }
-    // per-warp virial: lanes' partials summed in lane order by lane 0
+    // per-warp virial: lanes' partials summed in lane order
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
         double acc = 0.0;
@@ -1145,9 +1099,9 @@ void launch_wide_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, co
     GMD_LAUNCH_CHECK();
 }
 
-static int back2_grid(int64_t n) {  // three CTAs of 4 warps per SM (shared memory), one wave
+static int back2_grid(int64_t n) {  // four CTAs of 8 warps per SM, one wave
     int64_t gr = (n + kB2Warps - 1) / kB2Warps;
-    if (gr > 148 * 3) gr = 148 * 3;
+    if (gr > 148 * 4) gr = 148 * 4;
     return (int)(gr > 0 ? gr : 1);
 }
 
@@ -1209,7 +1163,8 @@ void launch_wide_tb_backward(const GenModel& g, const BondArgs& a, const float* 
                                       (int)sizeof(TbSmem)));
         attr = true;
     }
-    k_wide_tb_back1<<<tb_tc_grid(a.n), kTW * 32, sizeof(TbSmem), s>>>(g, make_basis3(g), a, QB, TH3, SMR,
+    float* EB = SMR;  // back1 writes E = P3^T m_bar_3 (8 floats per bond) in the scratch rows
+    k_wide_tb_back1<<<tb_tc_grid(a.n), kTW * 32, sizeof(TbSmem), s>>>(g, make_basis3(g), a, QB, TH3, EB,
                                                                        VOUT);
     GMD_LAUNCH_CHECK();
     static bool attr2 = false;
@@ -1218,8 +1173,9 @@ void launch_wide_tb_backward(const GenModel& g, const BondArgs& a, const float* 
                                       (int)sizeof(Back2Smem)));
         attr2 = true;
     }
-    k_wide_tb_back2<<<back2_grid(a.n), kB2Warps * 32, sizeof(Back2Smem), s>>>(g, make_basis3(g), a, TT, SMR,
-                                                                             VIN, VOUT, vir_part);
+    (void)TT;
+    k_wide_tb_back2<<<back2_grid(a.n), kB2Warps * 32, sizeof(Back2Smem), s>>>(g, make_basis3(g), a, EB, VIN,
+                                                                             VOUT, vir_part);
     GMD_LAUNCH_CHECK();
 }
 
