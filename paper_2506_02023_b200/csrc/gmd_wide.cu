@@ -8,6 +8,8 @@
 //     dsum_e  = sum_k psi_k G_k,  G = X P,  X_f = mbar_u,f h_w,f + h_u,f mbar_w,f,
 //               psi_k = phi_k (ca + cb k)
 //     grad_u -= v_e dsum_e / d_e,  virial += 1/2 dsum_e / d_e v_e (x) v_e
+#include <cstdlib>
+
 #include "gmd_tc.cuh"
 #include "gmd_wide.cuh"
 
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(kConvWarps * 32) k_wide_bwd_node(GenModel g, i
 // ---------------------------------------------------------------------------
 constexpr int kBW = 8;            // warps per CTA: 8 x 16 edge slots = MMA M = 128
 constexpr int kSlots = 16;        // edge slots per warp and step (warps w and w + 4 share a TMEM lane quarter)
+
 constexpr int kXLbo = 144;        // bytes between K-adjacent core matrices (16 B pad: conflict-free stores)
 constexpr int kXSbo = 16 * kXLbo; // bytes between 8-row groups (64 K = 16 core matrices)
 constexpr int kXBytes = 16 * kXSbo;  // 128 rows
@@ -233,8 +236,12 @@ struct BwdSmem {
     unsigned char x_lo[kXBytes];
     unsigned char p_hi[kPBytes];
     unsigned char p_lo[kPBytes];
-    float4 u[kBW][kSlots][2];  // fc * phi of the chunk's edges
-    int src[kBW][kSlots];
+    // per-step edge records, double-buffered: step u + 1's are loaded while
+    // the tensor cores run step u
+    float4 u[2][kBW][kSlots][2];    // fc * phi of the chunk's edges
+    float4 psi[2][kBW][kSlots][2];  // psi_k of the chunk's edges (epilogue)
+    float4 q[2][kBW][kSlots];       // (v, d) of the chunk's edges (epilogue)
+    int src[2][kBW][kSlots];
     uint64_t mbar;
     uint32_t tbase;
 };
@@ -273,6 +280,7 @@ __device__ __forceinline__ void split2(float2 x, float2& hi, float2& lo) {
     tc::split_tf32(x.y, hi.y, lo.y);
 }
 
+template <int kBatch>  // gathered edges in flight per warp
 __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis bs, ConvArgs a,
                                                               const float* __restrict__ MB,
                                                               const float* __restrict__ Hl,
@@ -331,59 +339,38 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
     for (int w = 0; w < kBW; ++w) steps = max(steps, steps_w[w]);
 
     double vir[6] = {0, 0, 0, 0, 0, 0};
-    int64_t jn = 0;            // index of the current node in this warp's sequence
-    int64_t k = -1, v = 0;     // current node (-1: none yet)
-    int pos = 0, e1 = 0;
-    float2 mu = make_float2(0.f, 0.f), hu = mu, hb = mu;
-    float gx = 0.f, gy = 0.f, gz = 0.f;
-    float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    uint32_t phase = 0;
-    auto finish = [&]() {  // node k complete: one writer per element
-        if (k < 0) return;
-        float2* hbp = reinterpret_cast<float2*>(HB + (size_t)k * F) + lane;
-        const float2 old = *hbp;
-        *hbp = make_float2(old.x + hb.x, old.y + hb.y);
-        const float sx = gwarp_sum(gx), sy = gwarp_sum(gy), sz = gwarp_sum(gz);
-#pragma unroll
-        for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
-        if (lane == 0) {
-            float4 gr = GRAD[k];
-            gr.x += sx;
-            gr.y += sy;
-            gr.z += sz;
-            GRAD[k] = gr;
-#pragma unroll
-            for (int c = 0; c < 6; ++c) vir[c] += (double)vr[c];
-        }
+    // schedule: steps of <= 16 edges of one node, in this warp's node order
+    struct Step {
+        int64_t k, r;
+        int pos, ne;
+        bool first, last;
     };
-    for (int step = 0; step < steps; ++step) {
-        // (1) next node when the current one is done
-        if (pos >= e1) {
-            finish();
-            k = -1;
-            if (jn < my_nodes) {
-                k = gw + jn * nw;
-                ++jn;
-                v = a.nodes ? (int64_t)a.nodes[k] : k;
-                const int64_t r = a.crow ? (int64_t)a.crow[v] : v;
-                pos = a.row[v];
-                e1 = a.row[v + 1];
-                mu = reinterpret_cast<const float2*>(MB + (size_t)r * F)[lane];
-                hu = reinterpret_cast<const float2*>(Hl + (size_t)r * F)[lane];
-                hb = make_float2(0.f, 0.f);
-                gx = gy = gz = 0.f;
-#pragma unroll
-                for (int c = 0; c < 6; ++c) vr[c] = 0.f;
-            } else {
-                pos = e1 = 0;
-            }
+    int64_t jn = 0, sk = -1, sr = 0;
+    int spos = 0, se1 = 0;
+    auto schedule = [&]() {
+        Step st{-1, 0, 0, 0, false, false};
+        if (spos >= se1) {
+            if (jn >= my_nodes) return st;
+            sk = gw + jn * nw;
+            ++jn;
+            const int64_t sv = a.nodes ? (int64_t)a.nodes[sk] : sk;
+            sr = a.crow ? (int64_t)a.crow[sv] : sv;
+            spos = a.row[sv];
+            se1 = a.row[sv + 1];
+            st.first = true;
         }
-        const int ne = k >= 0 ? min(kSlots, e1 - pos) : 0;
-        // (2) per-edge scalars, lane = edge slot
-        float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
-        float psi[K];
-        if (lane < ne) {
-            q = __ldg(a.vd + pos + lane);
+        st.k = sk;
+        st.r = sr;
+        st.pos = spos;
+        st.ne = min(kSlots, se1 - spos);
+        spos += st.ne;
+        st.last = spos >= se1;
+        return st;
+    };
+    // per-edge scalars of a step into buffer b, lane = edge slot
+    auto load_step = [&](int b, const Step& st) {
+        if (lane < st.ne) {
+            const float4 q = __ldg(a.vd + st.pos + lane);
             const float d = q.w;
             float phi[K];
             phi8(bs, d, phi);
@@ -394,33 +381,47 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
             const float dfc = in ? -0.5f * bs.pi_rc * sn : 0.0f;
             const float x0 = d * bs.isg, stp = bs.mus * bs.isg;
             const float ca = dfc - 2.0f * fc * bs.isg * x0, cb = 2.0f * fc * bs.isg * stp;
+            float psi[K];
 #pragma unroll
             for (int kk = 0; kk < K; ++kk) psi[kk] = phi[kk] * fmaf(cb, (float)kk, ca);
-            S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
-            S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
-            S.src[wq][lane] = a.lsrc[pos + lane];
-        } else {
-#pragma unroll
-            for (int kk = 0; kk < K; ++kk) psi[kk] = 0.f;
+            S.psi[b][wq][lane][0] = make_float4(psi[0], psi[1], psi[2], psi[3]);
+            S.psi[b][wq][lane][1] = make_float4(psi[4], psi[5], psi[6], psi[7]);
+            S.q[b][wq][lane] = q;
+            S.u[b][wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
+            S.u[b][wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+            S.src[b][wq][lane] = a.lsrc[st.pos + lane];
         }
+    };
+    float2 mu = make_float2(0.f, 0.f), hu = mu, hb = mu, mun = mu, hun = mu;
+    float gx = 0.f, gy = 0.f, gz = 0.f;
+    float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    uint32_t phase = 0;
+    Step cur = schedule();
+    load_step(0, cur);
+    if (cur.first) {
+        mu = reinterpret_cast<const float2*>(MB + (size_t)cur.r * F)[lane];
+        hu = reinterpret_cast<const float2*>(Hl + (size_t)cur.r * F)[lane];
+    }
+    for (int step = 0; step < steps; ++step) {
+        const int bsel = step & 1;
+        const int ne = cur.ne;
         __syncwarp();
-        // (3) feature lanes: hbar, and X rows (tf32 hi / lo) of the A operand;
-        // eight edges' rows in flight
-        for (int i0 = 0; i0 < ne; i0 += 8) {
-            float2 mw[8], hw[8];
+        // (1) feature lanes: hbar, and X rows (tf32 hi / lo) of the A operand
+        for (int i0 = 0; i0 < ne; i0 += kBatch) {
+            float2 mw[kBatch], hw[kBatch];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kBatch; ++j) {
                 if (i0 + j < ne) {
-                    const int w = S.src[wq][i0 + j];
+                    const int w = S.src[bsel][wq][i0 + j];
                     mw[j] = __ldg(reinterpret_cast<const float2*>(MB + (size_t)w * F) + lane);
                     hw[j] = __ldg(reinterpret_cast<const float2*>(Hl + (size_t)w * F) + lane);
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < kBatch; ++j) {
                 const int i = i0 + j;
                 if (i < ne) {
-                    const float4 ua = S.u[wq][i][0], ub = S.u[wq][i][1];
+                    const float4 ua = S.u[bsel][wq][i][0], ub = S.u[bsel][wq][i][1];
                     float2 sv = f2mul(P2[0], bc2(ua.x));
                     sv = f2fma(P2[1], bc2(ua.y), sv);
                     sv = f2fma(P2[2], bc2(ua.z), sv);
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
                 }
             }
         }
-        // (4) G = X P on the tensor cores (3xTF32), one thread issues
+        // (2) G = X P on the tensor cores (3xTF32), one thread issues
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
@@ -457,10 +458,17 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
             }
             tc::commit(&S.mbar);
         }
+        // (3) the next step's records and own rows load under the MMA
+        const Step nxt = schedule();
+        load_step(bsel ^ 1, nxt);
+        if (nxt.first) {
+            mun = reinterpret_cast<const float2*>(MB + (size_t)nxt.r * F)[lane];
+            hun = reinterpret_cast<const float2*>(Hl + (size_t)nxt.r * F)[lane];
+        }
         tc::mbar_wait(&S.mbar, phase);
         phase ^= 1u;
         tc::fence_after();
-        // (5) edge lanes: dsum, gradient, virial (the lane that computed the
+        // (4) edge lanes: dsum, gradient, virial (the lane that computed the
         // slot's scalars reads the slot's TMEM row)
         float G[8];
         tmem_ld8(trow, G);
@@ -469,6 +477,9 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) Gs[kk] = __shfl_sync(kFull, G[kk], (lane + kSlots * (wq >> 2)) & 31);
             if (lane < ne) {
+                const float4 q = S.q[bsel][wq][lane];
+                const float4 p0 = S.psi[bsel][wq][lane][0], p1 = S.psi[bsel][wq][lane][1];
+                const float psi[K] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
                 float dsum = 0.f;
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) dsum = fmaf(psi[kk], Gs[kk], dsum);
@@ -485,12 +496,37 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
                 vr[5] = fmaf(ch * q.y, q.z, vr[5]);
             }
         }
-        pos += ne;
+        // (5) node complete: one writer per element
+        if (cur.last) {
+            float2* hbp = reinterpret_cast<float2*>(HB + (size_t)cur.k * F) + lane;
+            const float2 old = *hbp;
+            *hbp = make_float2(old.x + hb.x, old.y + hb.y);
+            const float sx = gwarp_sum(gx), sy = gwarp_sum(gy), sz = gwarp_sum(gz);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
+            if (lane == 0) {
+                float4 gr = GRAD[cur.k];
+                gr.x += sx;
+                gr.y += sy;
+                gr.z += sz;
+                GRAD[cur.k] = gr;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) vir[c] += (double)vr[c];
+            }
+            hb = make_float2(0.f, 0.f);
+            gx = gy = gz = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) vr[c] = 0.f;
+        }
+        if (nxt.first) {
+            mu = mun;
+            hu = hun;
+        }
+        cur = nxt;
         // no barrier here: the next MMA is issued after the next step's
         // barrier, which every warp reaches only after this epilogue's TMEM
         // reads (fenced before that barrier); X is free once the MMA committed
     }
-    if (pos >= e1) finish();
     // fp64 virial: warp records in fixed order -> CTA record
     __shared__ double wv[kBW][6];
     if (lane == 0)
@@ -565,10 +601,15 @@ __global__ void __launch_bounds__(kConvWarps * 32) k_wide_tb_t(GenModel g, Basis
     for (int k = 0; k < K; ++k) P32[k] = make_float2(g.P3[(2 * lane) * K + k], g.P3[(2 * lane + 1) * K + k]);
     for (int64_t k = (int64_t)blockIdx.x * kConvWarps + wq; k < a.n; k += (int64_t)gridDim.x * kConvWarps) {
         const int64_t s = a.nodes ? (int64_t)a.nodes[k] : k;
-        for (int b = a.brow[s]; b < a.brow[s + 1]; ++b) {
-            float u[K];
-            u3l(b3, a.vd[a.bedge[b]].w, lane, u, false);
-            reinterpret_cast<float2*>(TT + (size_t)b * F)[lane] = p3dot(P32, u);
+        const int b0 = a.brow[s], b1 = a.brow[s + 1];
+        for (int bb = b0; bb < b1; bb += 32) {  // lane i loads bond bb + i's distance
+            const float dl = bb + lane < b1 ? a.vd[a.bedge[bb + lane]].w : 1.0f;
+            const int nbb = min(32, b1 - bb);
+            for (int i = 0; i < nbb; ++i) {
+                float u[K];
+                u3l(b3, __shfl_sync(kFull, dl, i), lane, u, false);
+                reinterpret_cast<float2*>(TT + (size_t)(bb + i) * F)[lane] = p3dot(P32, u);
+            }
         }
     }
 }
@@ -1186,14 +1227,22 @@ void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB,
         GMD_CUDA(cudaMemsetAsync(vir_part, 0, sizeof(double) * 6 * grid, s));
         return;
     }
+    // edges whose neighbour rows are in flight per warp (A/B: GMD_WIDE_BATCH =
+    // 8 | 12; 16 spills at the two-CTA register budget)
+    static const int batch = [] {
+        const char* v = std::getenv("GMD_WIDE_BATCH");
+        return v && std::atoi(v) == 12 ? 12 : 8;
+    }();
     static bool attr = false;
     if (!attr) {
-        GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(BwdSmem) + 1024));
+        GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sizeof(BwdSmem) + 1024));
         attr = true;
     }
-    k_wide_bwd_edge<<<grid, kBW * 32, sizeof(BwdSmem) + 1024, s>>>(g, make_basis(g), a, MB, Hl, HB, GRAD,
-                                                                     vir_part);
+    auto kern = batch == 8 ? k_wide_bwd_edge<8> : k_wide_bwd_edge<12>;
+    kern<<<grid, kBW * 32, sizeof(BwdSmem) + 1024, s>>>(g, make_basis(g), a, MB, Hl, HB, GRAD, vir_part);
     GMD_LAUNCH_CHECK();
 }
 
