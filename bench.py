@@ -60,23 +60,31 @@ def make_system(spec):
     return S.quartz(arg) if kind == "quartz" else S.liquid(arg)
 
 
-def bytes_model(n, ne, nb, L, threebody):
+def bytes_model(n, ne, nb, L, threebody, F=16):
     """Algorithmic (compulsory) DRAM bytes per launch of each kernel (DESIGN.md
-    section 3); n atoms, ne directed edges.  Gathered neighbour rows are not
-    counted (each row is compulsory once, already in the per-node terms)."""
-    return {
+    section 3); n atoms, ne directed edges, nb three-body bonds, feature
+    width F.  Gathered neighbour rows are not counted (each row is
+    compulsory once, already in the per-node terms)."""
+    r = 4 * F  # one feature row
+    m = {
         "nl_search": 68 * n + 8 * ne,                 # bin-sorted SoA atoms + degree; sorted keys
         # keys in; src/vd/d out (+ img/bond with three-body); pos+cell once
         "nl_emit": (37 if threebody else 32) * ne + 40 * n,
-        "conv": 8 * ne + 196 * n,                     # d+src per edge; h_in row, h_out + tanh rows
-        "bwd_edge": 20 * ne + 292 * n,                # vd+src per edge; m_bar, h_in, h_bar rw, grad rw
-        "bwd_node": 192 * n,
+        "conv": 8 * ne + (3 * r + 4) * n,             # d+src per edge; h_in row, h_out + tanh rows
+        "bwd_edge": 20 * ne + (4 * r + 36) * n,       # vd+src per edge; m_bar, h_in, h_bar rw, grad rw
+        "bwd_node": 3 * r * n,
     }
+    if threebody and nb:  # F = 64 three-body passes: per-bond rows
+        m["tb_forward"] = nb * (2 * r + r + 20)       # t read, t' + tanh rows written, bond record
+        m["tb_backward"] = nb * (r + r + 64) + n * r  # q_bar, tanh rows, E + VIN / VOUT
+    return m
 
 
 # profiler label (gmd_profile) -> CUDA kernel of the default path
 KERNEL_OF = {"bwd_edge": "k_bwd_edge2", "conv": "k_conv2", "nl_search": "k_nl_search",
              "nl_emit": "k_nl_emit", "bwd_node": "k_bwd_node"}
+KERNEL_OF_WIDE = {"bwd_edge": "k_wide_bwd_edge", "conv": "k_wide_conv", "bwd_node": "k_wide_bwd_node",
+                  "tb_forward": "k_wide_tb_forward", "tb_backward": "k_wide_tb_back2"}
 
 
 def ncu_metrics(config, kname):
@@ -87,7 +95,8 @@ def ncu_metrics(config, kname):
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{config}.json")), reverse=True):
         try:
             with open(path) as f:
-                m = json.load(f).get(KERNEL_OF.get(kname, "k_" + kname))
+                kof = KERNEL_OF_WIDE if config.startswith("c4w") else KERNEL_OF
+                m = json.load(f).get(kof.get(kname, "k_" + kname))
             if m and m.get("dram_bytes"):
                 return m, os.path.relpath(path, ROOT)
         except (OSError, ValueError):
@@ -423,7 +432,9 @@ def main():
                "ms_per_step": ms_e2e}
 
     # ---- roofline of the dominant kernel
-    bm = bytes_model(n, ne, 0, L, r3 > 0)
+    nbonds = C.c_int64()
+    h.check(Lb.gmd_get_num_bonds(h.h, C.byref(nbonds)))
+    bm = bytes_model(n, ne, nbonds.value, L, r3 > 0, Fc)
     # dominant compute kernel (the transport's waits are not a kernel roofline)
     kern = {k: v for k, v in prof.items() if k in bm}
     top = max(kern.items(), key=lambda kv: kv[1][0]) if kern else (None, (0, 0))
