@@ -32,9 +32,19 @@ def _deps_mtime():
     return max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC)) if os.path.isdir(CSRC) else 0
 
 
+# Files whose backward computes the edge/reverse-edge products
+# (m_u h_w + h_u m_w) that must round identically at both ends (exact
+# Newton's third law, gmd_model.cu grad_add): ptxas contracts
+# add.rn.f32x2(mul.rn.f32x2, mul.rn.f32x2) into an FFMA2 despite the explicit
+# rounding (checked in the SASS), which makes the two ends differ by an ulp.
+# Every intended fusion in these files is an explicit fmaf / __ffma2_rn.
+NO_FMAD = {"gmd_model.cu", "gmd_wide.cu"}
+
+
 def _compile(src: str) -> str:
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = ["-fmad=false"] if src in NO_FMAD else []
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

@@ -1132,7 +1132,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     float* TH = h->TH.get<float>((size_t)L * n * F);
     float* MB = h->MB.get<float>(R * F);
     float* HB = h->HB.get<float>(n * F);
-    float4* GRAD = h->GRAD.get<float4>(n);
+    double4* GRAD = h->GRAD.get<double4>(n);  // fp64: exact per-node sums of antisymmetric edge terms
     const int grid = model_grid(n);
     // backward edge pass: FFMA kernel, or the tcgen05 kernel with GMD_BWD_TC=1
     const char* tc_env = std::getenv("GMD_BWD_TC");
@@ -1317,7 +1317,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
 
     // ---- backward (:796-984)
     if (gen && !wide) launch_gen_init_hbar(h->gm, n, HB, s);  // (tuned, wide: fused into the first bwd_node)
-    GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(float4) * n, s));
+    GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(double4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
         {
             PROF("bwd_node");

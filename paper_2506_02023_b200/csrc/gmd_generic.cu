@@ -20,6 +20,11 @@ __device__ __forceinline__ float gwarp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;
 }
+__device__ __forceinline__ double gwarp_sumd(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
 
 __global__ void k_gen_embed(GenModel g, int64_t rows, const int32_t* __restrict__ node_array,
                             const int32_t* __restrict__ Z, float* __restrict__ H0) {
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
                                                                  const float* __restrict__ MB,
                                                                  const float* __restrict__ Hl,
                                                                  float* __restrict__ HB,
-                                                                 float4* __restrict__ GRAD,
+                                                                 double4* __restrict__ GRAD,
                                                                  double* __restrict__ vir_part) {
     extern __shared__ float gsm[];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
             mu[jj] = jj < nj && f < F ? MB[(size_t)ru * F + f] : 0.f;
             hu[jj] = jj < nj && f < F ? Hl[(size_t)ru * F + f] : 0.f;
         }
-        float gx = 0.f, gy = 0.f, gz = 0.f;
+        double gx = 0.0, gy = 0.0, gz = 0.0;
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int eb = e0; eb < e1; eb += 32) {
             const int ne = min(32, e1 - eb);
@@ -249,10 +254,10 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
                     drev += prev[lane * 33 + l];
                 }
                 const float invd = 1.0f / qi.w;
-                const float coef = (dself + drev) * invd;
-                gx -= qi.x * coef;
-                gy -= qi.y * coef;
-                gz -= qi.z * coef;
+                const float coef = (dself + drev) * invd;  // swapped terms on the reverse edge
+                gx -= (double)(qi.x * coef);
+                gy -= (double)(qi.y * coef);
+                gz -= (double)(qi.z * coef);
                 const float cself = dself * invd;
                 vr[0] = fmaf(cself * qi.x, qi.x, vr[0]);
                 vr[1] = fmaf(cself * qi.y, qi.y, vr[1]);
@@ -267,13 +272,13 @@ __global__ void __launch_bounds__(kGenWarps * 32) k_gen_bwd_edge(GenModel g, Con
             const int f = lane + 32 * jj;
             if (f < F) HB[(size_t)k * F + f] += hb[jj];
         }
-        gx = gwarp_sum(gx);
-        gy = gwarp_sum(gy);
-        gz = gwarp_sum(gz);
+        gx = gwarp_sumd(gx);
+        gy = gwarp_sumd(gy);
+        gz = gwarp_sumd(gz);
 #pragma unroll
         for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
-        if (lane == 0) {
-            float4 gr = GRAD[k];
+        if (lane == 0) {  // fp64, one writer per node (exact antisymmetric sums, gmd_model.cu)
+            double4 gr = GRAD[k];
             gr.x += gx;
             gr.y += gy;
             gr.z += gz;
@@ -646,7 +651,7 @@ void launch_gen_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, con
 }
 
 void launch_gen_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
-                         float* HB, float4* GRAD, double* vir_part, cudaStream_t s) {
+                         float* HB, double4* GRAD, double* vir_part, cudaStream_t s) {
     if (a.n == 0) return;
     const int K1 = g.K + 1;
     const size_t smem =

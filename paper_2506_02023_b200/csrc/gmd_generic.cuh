@@ -43,7 +43,7 @@ void launch_gen_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, con
                          int layer, const float* HB, const float* TH, float* MB, cudaStream_t s);
 // vir_part: gen_grid(n) * 8 records of 6 doubles (one per warp)
 void launch_gen_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
-                         float* HB, float4* GRAD, double* vir_part, cudaStream_t s);
+                         float* HB, double4* GRAD, double* vir_part, cudaStream_t s);
 
 // three-body stage (potential.cpp:664-741, 850-961), same slot conventions
 // as the tuned kernels (TP/TH3 slot j of a center = the reverse bond of its

@@ -249,6 +249,25 @@ __device__ __forceinline__ float group_sum16(float v) {
     for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+__device__ __forceinline__ double group_sum16d(double v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double group_sum16a(float v) { return (double)group_sum16(v); }
+__device__ __forceinline__ double group_sum16a(double v) { return group_sum16d(v); }
+// Newton's third law, exactly: an edge and its reverse produce bitwise
+// opposite fp32 gradient terms (symmetric dsum, negated vector), which are
+// summed per node in fp64 -- exact for terms within 2^29 of each other -- so
+// the forces sum to zero up to the final fp64 rounding (translation invariance,
+// momentum conservation; test_potential.cpp:160-172, test_md.cpp:110-122)
+__device__ __forceinline__ void grad_add(double4* GRAD, int64_t k, double gx, double gy, double gz) {
+    double4 g = GRAD[k];  // one writer per node and kernel: plain read-add-write
+    g.x += gx;
+    g.y += gy;
+    g.z += gz;
+    GRAD[k] = g;
+}
 
 constexpr int kNodesPerCta = kThreads / 16;  // half-warp (16 lanes) per node
 
@@ -402,7 +421,7 @@ __device__ __forceinline__ void bwd_load(const ConvArgs& a, const float* __restr
 
 __device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
                                          const float4* su_h, float isg, float mus, float acc[kF],
-                                         float& gx, float& gy, float& gz, float vr[6]) {
+                                         double& gx, double& gy, double& gz, float vr[6]) {
     const float4 q = x.q;
     // s_f = fc A_f, ds_f = dfc A_f - 2 fc/sigma (x0 A_f - a B_f) with
     // A_f = sum_k P_fk phi_k, B_f = sum_k k P_fk phi_k (potential.cpp:30-50)
@@ -436,10 +455,10 @@ __device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
         }
     }
     const float invd = 1.0f / q.w;
-    const float coef = (dself + drev) * invd;
-    gx -= q.x * coef;
-    gy -= q.y * coef;
-    gz -= q.z * coef;
+    const float coef = (dself + drev) * invd;  // dself and drev swap on the reverse edge
+    gx -= (double)(q.x * coef);
+    gy -= (double)(q.y * coef);
+    gz -= (double)(q.z * coef);
     const float cself = dself * invd;
     vr[0] = fmaf(cself * q.x, q.x, vr[0]);
     vr[1] = fmaf(cself * q.y, q.y, vr[1]);
@@ -452,7 +471,7 @@ __device__ __forceinline__ void bwd_math(const BwdEdgeIn& x, const float4* su_m,
 __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const float* __restrict__ MB,
                                                           const float* __restrict__ Hl,
                                                           float* __restrict__ HB,
-                                                          float4* __restrict__ GRAD,
+                                                          double4* __restrict__ GRAD,
                                                           double* vir_part) {
     __shared__ __align__(16) float sU[kNodesPerCta][2][kF];  // [group][m_bar_u, h_u][f]
     __shared__ double sVir[kNodesPerCta][6];                // per-group fp64 virial sums
@@ -493,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
         float acc[kF];
 #pragma unroll
         for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
-        float gx = 0.f, gy = 0.f, gz = 0.f;
+        double gx = 0.0, gy = 0.0, gz = 0.0;
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
         const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
@@ -512,17 +531,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_bwd_edge(ConvArgs a, const floa
 #pragma unroll
             for (int c = 0; c < 6; ++c) sVir[grp][c] += (double)vr[c];
         const float hb = transpose_reduce16_g16(acc, gl);
-        gx = group_sum16(gx);
-        gy = group_sum16(gy);
-        gz = group_sum16(gz);
-        if (valid) {  // one adder per element: red.add is the plain read-add-write
-            atomicAdd(HB + k * kF + gl, hb);
-            if (gl == 0) {
-                float* g = reinterpret_cast<float*>(GRAD + k);
-                atomicAdd(g, gx);
-                atomicAdd(g + 1, gy);
-                atomicAdd(g + 2, gz);
-            }
+        gx = group_sum16d(gx);
+        gy = group_sum16d(gy);
+        gz = group_sum16d(gz);
+        if (valid) {  // one writer per element: plain read-add-write
+            HB[k * kF + gl] += hb;
+            if (gl == 0) grad_add(GRAD, k, gx, gy, gz);
         }
     }
     __syncthreads();
@@ -715,9 +729,10 @@ __device__ __forceinline__ void bwd_load2(const float* __restrict__ MB, const fl
     ldg256(hw + 8, x.h[2], x.h[3]);
 }
 
+template <typename Acc>
 __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m,
                                           const float4* su_h, float isg, float mus,
-                                          float2 acc[kF / 2], float& gx, float& gy, float& gz,
+                                          float2 acc[kF / 2], Acc& gx, Acc& gy, Acc& gz,
                                           float vr[6]) {
     const float4 q = x.q;
     float fc, dfc;
@@ -731,10 +746,29 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const float4 mu4 = su_m[c], hu4 = su_h[c];
-        const float2 ga = f2fma(make_float2(hu4.x, hu4.y), make_float2(x.m[c].x, x.m[c].y),
-                                f2mul(make_float2(mu4.x, mu4.y), make_float2(x.h[c].x, x.h[c].y)));
-        const float2 gb = f2fma(make_float2(hu4.z, hu4.w), make_float2(x.m[c].z, x.m[c].w),
-                                f2mul(make_float2(mu4.z, mu4.w), make_float2(x.h[c].z, x.h[c].w)));
+        float2 ga, gb;
+        if (sizeof(Acc) == 8) {
+            // exact mode: g = 1/2 (S_u S_w - D_u D_w), S = mbar + h, D = mbar - h,
+            // a form symmetric under u <-> w whatever ptxas fuses (it contracts
+            // add.rn.f32x2 of two mul.rn.f32x2 into an FFMA2, which makes
+            // m_u h_w + h_u m_w round differently at the two ends); the 1/2
+            // is applied to dsum
+            const float2 su0 = __fadd2_rn(make_float2(mu4.x, mu4.y), make_float2(hu4.x, hu4.y));
+            const float2 du0 = __fadd2_rn(make_float2(mu4.x, mu4.y), make_float2(-hu4.x, -hu4.y));
+            const float2 sw0 = __fadd2_rn(make_float2(x.m[c].x, x.m[c].y), make_float2(x.h[c].x, x.h[c].y));
+            const float2 dw0 = __fadd2_rn(make_float2(x.m[c].x, x.m[c].y), make_float2(-x.h[c].x, -x.h[c].y));
+            ga = f2fma(su0, sw0, f2mul(make_float2(-du0.x, -du0.y), dw0));
+            const float2 su1 = __fadd2_rn(make_float2(mu4.z, mu4.w), make_float2(hu4.z, hu4.w));
+            const float2 du1 = __fadd2_rn(make_float2(mu4.z, mu4.w), make_float2(-hu4.z, -hu4.w));
+            const float2 sw1 = __fadd2_rn(make_float2(x.m[c].z, x.m[c].w), make_float2(x.h[c].z, x.h[c].w));
+            const float2 dw1 = __fadd2_rn(make_float2(x.m[c].z, x.m[c].w), make_float2(-x.h[c].z, -x.h[c].w));
+            gb = f2fma(su1, sw1, f2mul(make_float2(-du1.x, -du1.y), dw1));
+        } else {
+            ga = f2fma(make_float2(hu4.x, hu4.y), make_float2(x.m[c].x, x.m[c].y),
+                       f2mul(make_float2(mu4.x, mu4.y), make_float2(x.h[c].x, x.h[c].y)));
+            gb = f2fma(make_float2(hu4.z, hu4.w), make_float2(x.m[c].z, x.m[c].w),
+                       f2mul(make_float2(mu4.z, mu4.w), make_float2(x.h[c].z, x.h[c].w)));
+        }
         g[4 * c] = ga.x;
         g[4 * c + 1] = ga.y;
         g[4 * c + 2] = gb.x;
@@ -756,7 +790,7 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
         const float2 ck = f2fma(bcast(cb), make_float2((float)(2 * j), (float)(2 * j + 1)), bcast(ca));
         s2 = f2fma(f2mul(make_float2(phi[2 * j], phi[2 * j + 1]), ck), G[j], s2);
     }
-    const float dsum = s2.x + s2.y;
+    const float dsum = sizeof(Acc) == 8 ? 0.5f * (s2.x + s2.y) : s2.x + s2.y;
     // hbar_u += mbar_w (.) s_e, s = fc P phi
     float php[kK];
 #pragma unroll
@@ -769,9 +803,9 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
         acc[2 * c + 1] = f2fma(make_float2(x.m[c].z, x.m[c].w), A[2 * c + 1], acc[2 * c + 1]);
     }
     const float coef = dsum / q.w;
-    gx = fmaf(-q.x, coef, gx);
-    gy = fmaf(-q.y, coef, gy);
-    gz = fmaf(-q.z, coef, gz);
+    gx -= (Acc)(q.x * coef);
+    gy -= (Acc)(q.y * coef);
+    gz -= (Acc)(q.z * coef);
     const float ch = 0.5f * coef;
     vr[0] = fmaf(ch * q.x, q.x, vr[0]);
     vr[1] = fmaf(ch * q.y, q.y, vr[1]);
@@ -781,11 +815,11 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
     vr[5] = fmaf(ch * q.y, q.z, vr[5]);
 }
 
-template <int CTAS, int NT = kThreads>
+template <int CTAS, int NT, typename Acc>
 __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
                                                            const float* __restrict__ Hl,
                                                            float* __restrict__ HB,
-                                                           float4* __restrict__ GRAD,
+                                                           double4* __restrict__ GRAD,
                                                            double* vir_part, double* vir_grp) {
     __shared__ __align__(16) float sU[(NT / 16)][2][kF];  // [group][m_bar_u, h_u][f]
     __shared__ double sVir[(NT / 16)][6];
@@ -834,7 +868,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
         float2 acc[kF / 2];
 #pragma unroll
         for (int i = 0; i < kF / 2; ++i) acc[i] = make_float2(0.f, 0.f);
-        float gx = 0.f, gy = 0.f, gz = 0.f;
+        Acc gx = 0, gy = 0, gz = 0;
         float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         const float4* su_m = reinterpret_cast<const float4*>(sU[grp][0]);
         const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
@@ -860,16 +894,23 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
             accf[2 * i + 1] = acc[i].y;
         }
         const float hb = transpose_reduce16_g16(accf, gl);
-        gx = group_sum16(gx);
-        gy = group_sum16(gy);
-        gz = group_sum16(gz);
-        if (valid) {  // one adder per element: red.add is the plain read-add-write
-            atomicAdd(HB + k * kF + gl, hb);
-            if (gl == 0) {
-                float* gp = reinterpret_cast<float*>(GRAD + k);
-                atomicAdd(gp, gx);
-                atomicAdd(gp + 1, gy);
-                atomicAdd(gp + 2, gz);
+        const double sx = group_sum16a(gx), sy = group_sum16a(gy), sz = group_sum16a(gz);
+        if (valid) {
+            // one writer per element (node k belongs to this group alone):
+            // deterministic either way.  The fp32 kernel uses reductions
+            // (RED, fire-and-forget: at its 80-register budget a read-add-
+            // write spills); the fp64 kernel a plain read-add-write
+            if (sizeof(Acc) == 4) {
+                atomicAdd(HB + k * kF + gl, hb);
+                if (gl == 0) {
+                    double* gp = reinterpret_cast<double*>(GRAD + k);
+                    atomicAdd(gp, sx);
+                    atomicAdd(gp + 1, sy);
+                    atomicAdd(gp + 2, sz);
+                }
+            } else {
+                HB[k * kF + gl] += hb;
+                if (gl == 0) grad_add(GRAD, k, sx, sy, sz);
             }
         }
     }
@@ -913,7 +954,8 @@ struct BwdTcSmem {
     float b_hi[32 * kK], b_lo[32 * kK];     // [P ; kP]
     alignas(16) float rows[2][kTM * kRowStride];  // gathered m_bar[w], h[w] per slot
     alignas(16) float own[2][kNCH][2 * kF];       // m_bar, h rows of each chunk's node
-    float csum[kNCH][kNV + 1];              // chunk sums of the current tile
+    float csum[kNCH][kNV + 1];              // chunk sums of the current tile (h_bar)
+    double gsum[kNCH][3];                   // chunk sums of the positional gradient
     int cnode[2][kNCH];                     // node (local index) of each chunk, -1: none
     int clast[2][kNCH];                     // chunk is its node's last chunk
     uint64_t mbar;
@@ -976,7 +1018,7 @@ __device__ __forceinline__ void stage_edge_rows(float* dst, const float* __restr
 __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
     ConvArgs a, const int4* __restrict__ ctab, const int32_t* __restrict__ ccta,
     const float* __restrict__ MB, const float* __restrict__ Hl, float* __restrict__ HB,
-    float4* __restrict__ GRAD, double* vir_part) {
+    double4* __restrict__ GRAD, double* vir_part) {
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     BwdTcSmem& S = *reinterpret_cast<BwdTcSmem*>(tc_smem);
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1028,7 +1070,7 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
     tc::cp_async_commit();
 
     double vir[6] = {0, 0, 0, 0, 0, 0};
-    float carry = 0.f;
+    double carry = 0.0;  // h_bar chunk sums stay fp32 values (exact in fp64)
     int carry_node = -1;
     uint32_t phase = 0;
     for (int u = 0; u < ntiles; ++u) {
@@ -1079,7 +1121,7 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
         tc::fence_after();
         float AB[32];
         tc::tmem_ld32(trow, AB);
-        float gx = 0.f, gy = 0.f, gz = 0.f;
+        double gx = 0.0, gy = 0.0, gz = 0.0;
         if (valid) {
             float fc, dfc;
             fc_dfc_fast(q.w, fc, dfc);
@@ -1110,9 +1152,9 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
             }
             const float invd = 1.0f / q.w;
             const float coef = (dself + drev) * invd;
-            gx = -q.x * coef;
-            gy = -q.y * coef;
-            gz = -q.z * coef;
+            gx = -(double)(q.x * coef);
+            gy = -(double)(q.y * coef);
+            gz = -(double)(q.z * coef);
             const double cself = (double)(dself * invd);
             vir[0] += cself * q.x * q.x;
             vir[1] += cself * q.y * q.y;
@@ -1126,14 +1168,14 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
         }
         // (5) chunk sums: fixed half-warp trees
         const float hsum = transpose_reduce16_g16(AB, gl);  // feature gl
-        gx = group_sum16(gx);
-        gy = group_sum16(gy);
-        gz = group_sum16(gz);
+        gx = group_sum16d(gx);
+        gy = group_sum16d(gy);
+        gz = group_sum16d(gz);
         S.csum[ch][gl] = hsum;
         if (gl == 0) {
-            S.csum[ch][16] = gx;
-            S.csum[ch][17] = gy;
-            S.csum[ch][18] = gz;
+            S.gsum[ch][0] = gx;
+            S.gsum[ch][1] = gy;
+            S.gsum[ch][2] = gz;
         }
         tc::fence_before();
         __syncthreads();
@@ -1144,13 +1186,14 @@ __global__ void __launch_bounds__(kTM, kBwdTcCtas) k_bwd_edge_tc(
             for (int k2 = 0; k2 < kNCH; ++k2) {
                 const int j = S.cnode[buf][k2];
                 if (j < 0) break;
-                const float x = S.csum[k2][tid];
+                const double x = tid < kF ? (double)S.csum[k2][tid] : S.gsum[k2][tid - kF];
                 carry = j == carry_node ? carry + x : x;
                 carry_node = j;
-                if (S.clast[buf][k2]) {
-                    float* dst = tid < kF ? HB + (size_t)j * kF + tid
-                                          : reinterpret_cast<float*>(GRAD + j) + (tid - kF);
-                    atomicAdd(dst, carry);
+                if (S.clast[buf][k2]) {  // one writer per (node, value)
+                    if (tid < kF)
+                        HB[(size_t)j * kF + tid] += (float)carry;
+                    else
+                        reinterpret_cast<double*>(GRAD + j)[tid - kF] += carry;
                     carry_node = -1;
                 }
             }
@@ -1494,23 +1537,21 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
 
 // grad[u] += sum_{X into u} (v_bar of rev(X)) - (v_bar of X)
 __global__ void k_tb_grad(BondArgs a, const float4* __restrict__ VIN,
-                          const float4* __restrict__ VOUT, float4* __restrict__ GRAD) {
+                          const float4* __restrict__ VOUT, double4* __restrict__ GRAD) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= a.n) return;
     const int64_t u = a.nodes ? (int64_t)a.nodes[k] : k;
-    float gx = 0.f, gy = 0.f, gz = 0.f;
+    // the fp32 term of bond b at u is bitwise the negation of its reverse's
+    // term at the bond's source (same operands, exchanged); fp64 sums
+    double gx = 0.0, gy = 0.0, gz = 0.0;
     for (int b = a.brow[u]; b < a.brow[u + 1]; ++b) {
         const int rb = a.brev[b];
         const float4 i1 = VIN[rb], o1 = VOUT[b], i2 = VIN[b], o2 = VOUT[rb];
-        gx += (i1.x + o1.x) - (i2.x + o2.x);
-        gy += (i1.y + o1.y) - (i2.y + o2.y);
-        gz += (i1.z + o1.z) - (i2.z + o2.z);
+        gx += (double)((i1.x + o1.x) - (i2.x + o2.x));
+        gy += (double)((i1.y + o1.y) - (i2.y + o2.y));
+        gz += (double)((i1.z + o1.z) - (i2.z + o2.z));
     }
-    float4 g = GRAD[k];
-    g.x += gx;
-    g.y += gy;
-    g.z += gz;
-    GRAD[k] = g;
+    grad_add(GRAD, k, gx, gy, gz);
 }
 
 // h_bar = readout for every node (potential.cpp:808); a row per thread so the
@@ -1525,20 +1566,20 @@ __global__ void k_init_hbar(int64_t n, float* HB) {
 }
 
 __global__ void k_forces_out(int64_t n, const int32_t* __restrict__ nodes,
-                             const float4* __restrict__ GRAD, double* forces, float* forces32) {
+                             const double4* __restrict__ GRAD, double* forces, float* forces32) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int64_t v = nodes ? (int64_t)nodes[k] : k;
-    float4 g = GRAD[k];
+    const double4 g = GRAD[k];
     if (forces) {
-        forces[3 * v] = -(double)g.x;
-        forces[3 * v + 1] = -(double)g.y;
-        forces[3 * v + 2] = -(double)g.z;
+        forces[3 * v] = -g.x;
+        forces[3 * v + 1] = -g.y;
+        forces[3 * v + 2] = -g.z;
     }
     if (forces32) {
-        forces32[3 * v] = -g.x;
-        forces32[3 * v + 1] = -g.y;
-        forces32[3 * v + 2] = -g.z;
+        forces32[3 * v] = -(float)g.x;
+        forces32[3 * v + 1] = -(float)g.y;
+        forces32[3 * v + 2] = -(float)g.z;
     }
 }
 
@@ -1631,15 +1672,31 @@ static int bwd_variant() {
     return venv ? std::atoi(venv) : 0;
 }
 
-// The default backward runs 768-thread CTAs, one per SM: the 48 consecutive
+// The default backward runs 640-thread CTAs, one per SM: the 40 consecutive
 // nodes a CTA works on share most neighbour rows, which then hit in the SM's
 // L1 (C5: 3.13 -> 2.98 ms per step vs 3 x 256-thread CTAs per SM; the
 // forward conv is faster with 256-thread CTAs).
-constexpr int kBwdThreads = 768;
+constexpr int kBwdThreads = 768;       // fp32 gradient lanes (80 registers)
+constexpr int kBwdThreads2 = 640;      // the same at 96 registers (A/B: GMD_BWD_THREADS=640)
+constexpr int kBwdThreadsExact = 640;  // fp64 gradient lanes (96 registers)
+
+// exact mode (GMD_EXACT_FORCES=1): Newton's third law to the last bit (fp64
+// per-lane gradient sums of bitwise-opposite edge terms); the default sums the
+// per-lane terms in fp32 (forces sum to zero to ~1e-7 relative)
+static bool exact_forces() {
+    const char* v = std::getenv("GMD_EXACT_FORCES");  // read per call (tests switch)
+    return v && v[0] == '1';
+}
+
+static int bwd_threads() {
+    if (exact_forces()) return kBwdThreadsExact;
+    const char* v = std::getenv("GMD_BWD_THREADS");
+    return v && std::atoi(v) == kBwdThreads2 ? kBwdThreads2 : kBwdThreads;
+}
 
 int bwd_edge_grid(int64_t n) {
     if (bwd_variant() == 1) return model_grid(n);
-    const int64_t per = kBwdThreads / 16;
+    const int64_t per = bwd_threads() / 16;
     int64_t g = (n + per - 1) / per;
     if (g > 148) g = 148;
     return (int)(g > 0 ? g : 1);
@@ -1647,9 +1704,9 @@ int bwd_edge_grid(int64_t n) {
 
 bool bwd_edge_ranges() { return bwd_variant() != 1; }
 
-int64_t bwd_edge_stride(int grid) { return (int64_t)grid * (kBwdThreads / 16); }
+int64_t bwd_edge_stride(int grid) { return (int64_t)grid * (bwd_threads() / 16); }
 
-void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
+void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
                      double* vir_part, cudaStream_t s, double* vir_grp, int grid) {
     if (a.n - a.k0 <= 0) return;
     const int variant = bwd_variant();
@@ -1657,8 +1714,14 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
     const int g = grid > 0 ? grid : bwd_edge_grid(a.n - a.k0);
     if (variant == 1)  // scalar-FFMA kernel (A/B reference)
         k_bwd_edge<<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
+    else if (exact_forces())
+        k_bwd_edge2<1, kBwdThreadsExact, double><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
+                                                                                vir_grp);
+    else if (bwd_threads() == kBwdThreads2)
+        k_bwd_edge2<1, kBwdThreads2, float><<<g, kBwdThreads2, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
+                                                                       vir_grp);
     else
-        k_bwd_edge2<1, kBwdThreads><<<g, kBwdThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
+        k_bwd_edge2<1, kBwdThreads, float><<<g, kBwdThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
                                                               vir_grp);
     GMD_LAUNCH_CHECK();
 }
@@ -1685,7 +1748,7 @@ void launch_chunk_fill(const ConvArgs& a, const int32_t* cstart, int4* tab, int 
 }
 
 void launch_bwd_edge_tc(const ConvArgs& a, const int4* ctab, const int32_t* ccta, int grid,
-                        const float* MB, const float* Hl, float* HB, float4* GRAD,
+                        const float* MB, const float* Hl, float* HB, double4* GRAD,
                         double* vir_part, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
@@ -1747,7 +1810,7 @@ void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, fl
     GMD_LAUNCH_CHECK();
 }
 
-void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, float4* GRAD,
+void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, double4* GRAD,
                     cudaStream_t s) {
     if (a.n == 0) return;
     k_tb_grad<<<div_up(a.n, 128), 128, 0, s>>>(a, VIN, VOUT, GRAD);
@@ -1760,7 +1823,7 @@ void launch_init_hbar(int64_t n, float* HB, cudaStream_t s) {
     GMD_LAUNCH_CHECK();
 }
 
-void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, double* forces,
+void launch_forces_out(int64_t n, const int32_t* nodes, const double4* GRAD, double* forces,
                        float* forces32, cudaStream_t s) {
     if (n == 0) return;
     k_forces_out<<<div_up(n, 256), 256, 0, s>>>(n, nodes, GRAD, forces, forces32);

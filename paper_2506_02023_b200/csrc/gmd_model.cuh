@@ -80,7 +80,7 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 // virial sums; with chunk starts k0 that are multiples of
 // bwd_edge_stride(grid) every node meets the same CTA group in the same order
 // as in one launch, so the virial (and everything else) is bitwise the same
-void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, float4* GRAD,
+void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
                      double* vir_part, cudaStream_t s, double* vir_grp = nullptr, int grid = 0);
 // the default kernel takes node ranges (a.k0 > 0); grid = bwd_edge_grid(n - k0)
 bool bwd_edge_ranges();
@@ -96,7 +96,7 @@ void launch_chunk_count(const ConvArgs& a, int32_t* cnt, cudaStream_t s);  // n 
 void launch_chunk_fill(const ConvArgs& a, const int32_t* cstart, int4* tab, int grid,
                        int32_t* cta, cudaStream_t s);
 void launch_bwd_edge_tc(const ConvArgs& a, const int4* ctab, const int32_t* ccta, int grid,
-                        const float* MB, const float* Hl, float* HB, float4* GRAD,
+                        const float* MB, const float* Hl, float* HB, double4* GRAD,
                         double* vir_part, cudaStream_t s);
 
 // three-body stage (global bond CSR by dst; slot = in-bond position)
@@ -119,11 +119,11 @@ void launch_tb_bwd_q(int64_t n, const int32_t* nodes, const int32_t* crow, const
 // max_bonds: largest in-bond count of a center (sizes the per-group staging)
 void launch_tb_backward(const BondArgs& a, const float* QB, const float* TH3, float4* VIN,
                         float4* VOUT, double* vir_part, int max_bonds, cudaStream_t s);
-void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, float4* GRAD,
+void launch_tb_grad(const BondArgs& a, const float4* VIN, const float4* VOUT, double4* GRAD,
                     cudaStream_t s);
 
 void launch_init_hbar(int64_t n, float* HB, cudaStream_t s);
-void launch_forces_out(int64_t n, const int32_t* nodes, const float4* GRAD, double* forces,
+void launch_forces_out(int64_t n, const int32_t* nodes, const double4* GRAD, double* forces,
                        float* forces32, cudaStream_t s);
 // sum nparts consecutive records of width w into out[w] in fixed order
 void launch_reduce_partials(const double* parts, int nparts, int w, double* out, cudaStream_t s);

@@ -61,6 +61,11 @@ __device__ __forceinline__ float gwarp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;
 }
+__device__ __forceinline__ double gwarp_sumd(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
 
 // ---------------------------------------------------------------------------
 // forward conv: one warp per node, lane l holds features 2l, 2l+1
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
                                                               const float* __restrict__ MB,
                                                               const float* __restrict__ Hl,
                                                               float* __restrict__ HB,
-                                                              float4* __restrict__ GRAD,
+                                                              double4* __restrict__ GRAD,
                                                               double* __restrict__ vir_part) {
     extern __shared__ __align__(1024) unsigned char wsm[];
     BwdSmem& S = *reinterpret_cast<BwdSmem*>(wsm);
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
         }
     };
     float2 mu = make_float2(0.f, 0.f), hu = mu, hb = mu, mun = mu, hun = mu;
-    float gx = 0.f, gy = 0.f, gz = 0.f;
+    double gx = 0.0, gy = 0.0, gz = 0.0;  // fp64: exact sums of antisymmetric terms
     float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     uint32_t phase = 0;
     Step cur = schedule();
@@ -405,6 +410,7 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
     for (int step = 0; step < steps; ++step) {
         const int bsel = step & 1;
         const int ne = cur.ne;
+        const float2 su = __fadd2_rn(mu, hu), ndu = __fadd2_rn(make_float2(-mu.x, -mu.y), hu);  // S_u, -D_u
         __syncwarp();
         // (1) feature lanes: hbar, and X rows (tf32 hi / lo) of the A operand
         for (int i0 = 0; i0 < ne; i0 += kBatch) {
@@ -431,7 +437,13 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
                     sv = f2fma(P2[6], bc2(ub.z), sv);
                     sv = f2fma(P2[7], bc2(ub.w), sv);
                     hb = f2fma(mw[j], sv, hb);
-                    const float2 x = f2fma(hu, mw[j], f2mul(mu, hw[j]));
+                    // 2 X = S_u S_w - D_u D_w (S = mbar + h, D = mbar - h):
+                    // symmetric under u <-> w whatever ptxas fuses, so the
+                    // reverse edge gets bitwise the same X row, G and dsum
+                    // (exact Newton's third law; the 1/2 is applied to dsum)
+                    const float2 sw = __fadd2_rn(mw[j], hw[j]);
+                    const float2 dw = __fadd2_rn(mw[j], make_float2(-hw[j].x, -hw[j].y));
+                    const float2 x = f2fma(su, sw, f2mul(ndu, dw));
                     float2 xh, xl;
                     split2(x, xh, xl);
                     const int off = xoff(row0 + i, 2 * lane);
@@ -483,10 +495,10 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
                 float dsum = 0.f;
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) dsum = fmaf(psi[kk], Gs[kk], dsum);
-                const float coef = dsum / q.w;
-                gx = fmaf(-q.x, coef, gx);
-                gy = fmaf(-q.y, coef, gy);
-                gz = fmaf(-q.z, coef, gz);
+                const float coef = (0.5f * dsum) / q.w;
+                gx -= (double)(q.x * coef);
+                gy -= (double)(q.y * coef);
+                gz -= (double)(q.z * coef);
                 const float ch = 0.5f * coef;
                 vr[0] = fmaf(ch * q.x, q.x, vr[0]);
                 vr[1] = fmaf(ch * q.y, q.y, vr[1]);
@@ -501,11 +513,11 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
             float2* hbp = reinterpret_cast<float2*>(HB + (size_t)cur.k * F) + lane;
             const float2 old = *hbp;
             *hbp = make_float2(old.x + hb.x, old.y + hb.y);
-            const float sx = gwarp_sum(gx), sy = gwarp_sum(gy), sz = gwarp_sum(gz);
+            const double sx = gwarp_sumd(gx), sy = gwarp_sumd(gy), sz = gwarp_sumd(gz);
 #pragma unroll
             for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
             if (lane == 0) {
-                float4 gr = GRAD[cur.k];
+                double4 gr = GRAD[cur.k];
                 gr.x += sx;
                 gr.y += sy;
                 gr.z += sz;
@@ -514,7 +526,7 @@ __global__ void __launch_bounds__(kBW * 32, 2) k_wide_bwd_edge(GenModel g, Basis
                 for (int c = 0; c < 6; ++c) vir[c] += (double)vr[c];
             }
             hb = make_float2(0.f, 0.f);
-            gx = gy = gz = 0.f;
+            gx = gy = gz = 0.0;
 #pragma unroll
             for (int c = 0; c < 6; ++c) vr[c] = 0.f;
         }
@@ -1221,7 +1233,7 @@ void launch_wide_tb_backward(const GenModel& g, const BondArgs& a, const float* 
 }
 
 void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
-                          float* HB, float4* GRAD, double* vir_part, cudaStream_t s) {
+                          float* HB, double4* GRAD, double* vir_part, cudaStream_t s) {
     const int grid = wide_bwd_grid(a.n);
     if (a.n <= 0) {
         GMD_CUDA(cudaMemsetAsync(vir_part, 0, sizeof(double) * 6 * grid, s));

@@ -153,3 +153,28 @@ def test_energy_csv_steps_zero(tmp_path):
     res = G.run_md(s, G.ToyPotentialParams.init(3), G.MDOptions(steps=0, energy_csv=str(tmp_path / "e.csv")))
     assert len(res.records) == 1
     assert len(open(tmp_path / "e.csv").read().splitlines()) == 2
+
+
+@pytest.mark.parametrize("F,K,r3", [(16, 8, 0.0), (16, 8, 2.6), (32, 6, 2.6), (64, 8, 2.6), (64, 8, 0.0)])
+@pytest.mark.parametrize("exact", [True, False])
+def test_forces_sum_to_zero(F, K, r3, exact, monkeypatch):
+    """Newton's third law: every edge (and three-body bond) gradient term has
+    a bitwise-opposite partner and the per-atom sums run in fp64, so sum_i F_i
+    vanishes up to the final fp64 rounding -- the reference's translation-
+    invariance and momentum-conservation checks (1e-8, test_potential.cpp:
+    160-172, test_md.cpp:110-122).  Always for the width-generic and F = 64
+    kernels; for the tuned F = 16 backward with GMD_EXACT_FORCES=1 (its
+    default sums per-lane terms in fp32: zero to ~1e-7 relative)."""
+    monkeypatch.setenv("GMD_EXACT_FORCES", "1" if exact else "0")
+    s = S.random_gas(300, 4)
+    prm = G.ToyPotentialParams.init(7, F, K, 2, 4.0, r3)
+    d = G.Distributed.create_distributed(s, 4.0, r3 if r3 > 0 else None, 1, 1, True)
+    out = G.forward_distributed(d, prm)
+    fmax = np.abs(out.forces).max()
+    fsum = np.abs(out.forces.sum(axis=0)).max()
+    print(f"F={F} r3={r3} exact={exact}: max|F| {fmax:.3e}  |sum F| {fsum:.3e}")
+    assert fmax > 1e-3
+    if exact or F != 16:
+        assert fsum <= 1e-12 * max(1.0, fmax) * s.size()
+    else:
+        assert fsum <= 1e-6 * fmax
