@@ -247,6 +247,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partitions", type=int, default=0,
+                    help="one GPU only: p slab partitions in one process (exchanges are device "
+                         "copies) -- measures the partition machinery; default p = #GPUs")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="halo exchange for N>1: CUDA-IPC P2P stores (default) or NCCL send/recv")
     args = ap.parse_args()
@@ -314,6 +317,12 @@ def main():
     # one slab per GPU (p = world): every rank gets the replicated positions,
     # builds only its slab's rows and exchanges halo rows over NCCL each layer
     p = world
+    if args.partitions > 1:
+        if world > 1:
+            raise SystemExit("bench: --partitions is a one-GPU option")
+        p = args.partitions
+        config["partitions"] = p
+        config["parallelism"] = f"1 GPU, {p} slab partitions in one process (device-copy halo exchange)"
     h = G._Handle(device)
     Lb = G.lib()
     if world > 1:
@@ -349,15 +358,19 @@ def main():
     stress = np.zeros(9)
     timing = np.zeros(4)
 
+    # p > 1 partitions in one process with three-body terms: the line-graph
+    # partitions are built inside the timed build, as create_distributed does
+    bflags = G.GMD_ALLOW_NARROW | (G.GMD_LINE_PARTS if (p > 1 and world == 1 and r3 > 0) else 0)
+
     def step_device():
         h.check(Lb.gmd_build(h.h, n, C.c_void_p(pos_d.data_ptr()), C.c_void_p(z_d.data_ptr()),
-                             G._p(lat), G._p(pbc), rc, r3, 0.0, p, 0, G.GMD_ALLOW_NARROW | G.GMD_INPUT_DEVICE))
+                             G._p(lat), G._p(pbc), rc, r3, 0.0, p, 0, bflags | G.GMD_INPUT_DEVICE))
         h.check(Lb.gmd_forward(h.h, C.byref(energy), C.c_void_p(pa_d.data_ptr()), C.c_void_p(f_d.data_ptr()),
                                G._p(stress), G._p(timing), G.GMD_OUTPUT_DEVICE))
 
     def step_e2e():
         h.check(Lb.gmd_build(h.h, n, C.c_void_p(pos_h.data_ptr()), C.c_void_p(z_h.data_ptr()),
-                             G._p(lat), G._p(pbc), rc, r3, 0.0, p, 0, G.GMD_ALLOW_NARROW))
+                             G._p(lat), G._p(pbc), rc, r3, 0.0, p, 0, bflags))
         h.check(Lb.gmd_forward(h.h, C.byref(energy), C.c_void_p(pa_h.data_ptr()), C.c_void_p(f_h.data_ptr()),
                                G._p(stress), G._p(timing), 0))
 

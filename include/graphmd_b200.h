@@ -36,6 +36,9 @@ extern "C" {
 #define GMD_ALLOW_NARROW 1u   /* allow slabs narrower than the cutoff (partitioner.cpp:21-33) */
 #define GMD_INPUT_DEVICE 2u   /* pos/Z are device pointers on the handle's GPU */
 #define GMD_EQUAL_WIDTH 4u    /* BoundaryMode::kEqualWidth (partitioner.hpp:22-25) */
+#define GMD_LINE_PARTS 8u     /* build the per-partition line-graph edges inside gmd_build, as
+                                 create_distributed does (engine.cpp:57-62); the model does not
+                                 need them, the views build them on first use otherwise */
 
 /* gmd_forward flags */
 #define GMD_OUTPUT_DEVICE 1u  /* output pointers are device pointers */

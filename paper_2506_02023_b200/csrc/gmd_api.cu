@@ -327,6 +327,8 @@ struct gmd_handle {
     bool hc_ready = false;
     std::vector<int32_t> h_owner, h_row, h_src, h_lsrc, h_crow;
     bool hcb_ready = false;
+    bool line_dev_ready = false;  // line edges built on the device (lcnt / lpairs)
+    int64_t nline = 0;
     std::vector<int32_t> h_bedge, h_bown, h_pairs;
 };
 
@@ -602,6 +604,29 @@ void quantile_walls(gmd_handle* h, const double* fw, int64_t n, int p, double* b
     }
 }
 
+void ensure_bond_layout(gmd_handle* h);
+
+// line edges (e', e) of every partition on the device (linegraph.cpp:124-171,
+// count -> scan -> fill in (e', e) order); lcnt / lpairs
+void build_line_edges_dev(gmd_handle* h) {
+    ensure_bond_layout(h);
+    if (h->line_dev_ready) return;
+    cudaStream_t s = h->stream;
+    const int64_t nb = h->nb;
+    int32_t* cnt = h->lcnt.get<int32_t>(nb + 1);
+    launch_line_count(nb, h->bedge.as<int32_t>(), h->src.as<int32_t>(), h->brow.as<int32_t>(), cnt,
+                      s);
+    scan_i32(h, cnt, cnt, nb);
+    int32_t T = 0;
+    GMD_CUDA(cudaMemcpyAsync(&T, cnt + nb, 4, cudaMemcpyDeviceToHost, s));
+    sync(h);
+    h->nline = T;
+    int32_t* pairs = h->lpairs.get<int32_t>(2 * (size_t)T);
+    launch_line_fill(nb, h->bedge.as<int32_t>(), h->src.as<int32_t>(), h->brow.as<int32_t>(),
+                     h->brev.as<int32_t>(), cnt, pairs, s);
+    h->line_dev_ready = true;
+}
+
 void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, const double* lat,
                 const uint8_t* pbc, double rc, double r3, double tau, int p, uint32_t flags) {
     cudaStream_t s = h->stream;
@@ -609,6 +634,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     h->graph_only = false;
     h->closure_ready = false;
     h->hc_ready = h->hcb_ready = false;
+    h->line_dev_ready = false;
     h->ctab_ok = false;
     h->atoms.ready = h->bonds.ready = false;
     h->corrupted = false;
@@ -888,12 +914,16 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, ebid, bv, b.flags, ownp, myrank, s); }
         if (rank_mode) build_bond_rank_plan(h, ownp, myrank);
     }
+    h->built = true;
+    // create_distributed builds the line-graph partitions eagerly
+    // (engine.cpp:57-62); the model never reads them (it works per center on
+    // the global bonds), so they are built here only on request
+    if ((flags & GMD_LINE_PARTS) && h->has_lg && !rank_mode) build_line_edges_dev(h);
     GMD_CUDA(cudaEventRecord(h->ev[1], s));
     read_flags(h, hdr);
     float ms = 0.f;
     GMD_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
     h->t_graph = ms * 1e-3;
-    h->built = true;
 }
 
 void need_built(const gmd_handle* h) {
@@ -1941,6 +1971,7 @@ void partitions_impl(gmd_handle* h, int64_t n, const double* pos, const double* 
     h->graph_only = true;
     h->closure_ready = false;
     h->hc_ready = h->hcb_ready = false;
+    h->line_dev_ready = false;
     h->ctab_ok = false;
     h->atoms.ready = h->bonds.ready = false;
     h->corrupted = false;
@@ -2226,6 +2257,7 @@ int gmd_brute_force_line_graph(gmd_handle* h, int64_t* count, int64_t* pairs) {
         d2h(h, hp, d_pairs, 2 * (size_t)T);
         sync(h);
         h->hcb_ready = false;  // lpairs / lcnt are shared with the line-graph cache
+        h->line_dev_ready = false;
         if (count) *count = T;
         if (pairs) {
             std::vector<std::pair<int64_t, int64_t>> v((size_t)T);
@@ -2493,21 +2525,10 @@ int gmd_has_line_graph(const gmd_handle* h, int* yes) {
 
 namespace {
 void ensure_line_cache(gmd_handle* h) {
-    ensure_bond_layout(h);
+    build_line_edges_dev(h);
     if (h->hcb_ready) return;
-    cudaStream_t s = h->stream;
     const int64_t nb = h->nb;
-    int32_t* cnt = h->lcnt.get<int32_t>(nb + 1);
-    launch_line_count(nb, h->bedge.as<int32_t>(), h->src.as<int32_t>(), h->brow.as<int32_t>(), cnt,
-                      s);
-    scan_i32(h, cnt, cnt, nb);
-    int32_t T = 0;
-    GMD_CUDA(cudaMemcpyAsync(&T, cnt + nb, 4, cudaMemcpyDeviceToHost, s));
-    sync(h);
-    int32_t* pairs = h->lpairs.get<int32_t>(2 * (size_t)T);
-    launch_line_fill(nb, h->bedge.as<int32_t>(), h->src.as<int32_t>(), h->brow.as<int32_t>(),
-                     h->brev.as<int32_t>(), cnt, pairs, s);
-    d2h(h, h->h_pairs, pairs, 2 * (size_t)T);
+    d2h(h, h->h_pairs, h->lpairs.as<int32_t>(), 2 * (size_t)h->nline);
     d2h(h, h->h_bedge, h->bedge.as<int32_t>(), nb);
     d2h(h, h->h_bown, h->bonds.owner.as<int32_t>(), nb);
     sync(h);

@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(_HERE, "libgraphmd_b200.so")
 
 GMD_OK, GMD_ERR_CONFIG, GMD_ERR_RUNTIME, GMD_ERR_CUDA, GMD_ERR_ARG = 0, 2, 3, 4, 5
 GMD_ALLOW_NARROW, GMD_INPUT_DEVICE, GMD_EQUAL_WIDTH = 1, 2, 4
+GMD_LINE_PARTS = 8  # build the per-partition line-graph edges inside gmd_build
 GMD_OUTPUT_DEVICE, GMD_OUTPUT_F32 = 1, 2
 GMD_F32, GMD_F64 = 0, 1
 
