@@ -1236,7 +1236,11 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     const int64_t nsend = rank_mode ? std::accumulate(h->scnt.begin(), h->scnt.end(), (int64_t)0) : 0;
     float* sendbuf = rank_mode ? h->sendbuf.get<float>(std::max<int64_t>(1, nsend) * F) : nullptr;
     auto exchange = [&](float* buf, bool fwd = false) {
-        if (rank_mode) {
+        if (rank_mode && h->comm->fused_gather()) {
+            PROF("halo_exchange");  // gather + P2P store + flags in the transport's kernels
+            h->comm->exchange_gather(s, buf, h->xsend.as<int32_t>(), h->soff.data(), h->scnt.data(), buf,
+                                     h->roff.data(), h->rcnt.data(), F);
+        } else if (rank_mode) {
             {
                 PROF("halo_pack");
                 if (nsend > 0) {
@@ -1269,6 +1273,12 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                                    : nullptr;
     auto bond_exchange = [&](float* buf, int width) {
         if (!(rank_mode && tb)) return;
+        if (h->comm->fused_gather()) {
+            PROF("halo_exchange");
+            h->comm->exchange_gather(s, buf, h->bxsend.as<int32_t>(), h->b_soff.data(), h->b_scnt.data(),
+                                     buf, h->b_roff.data(), h->b_rcnt.data(), width);
+            return;
+        }
         {
             PROF("halo_pack");
             if (nbsend > 0) {

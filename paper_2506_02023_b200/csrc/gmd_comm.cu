@@ -1,6 +1,7 @@
 // Halo-exchange transports (see gmd_comm.cuh).
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -315,6 +316,41 @@ __global__ void k_ipc_signal(IpcPeers P, long long v) {
     if (threadIdx.x < P.n) st_release(P.sflag[threadIdx.x], v);
 }
 
+// one fused launch per direction: the last block to finish (fenced
+// counter) publishes the flags, so pack + send + signal and receive + ack are
+// one kernel each instead of five launches per exchange
+struct IpcRows {
+    int n;
+    long long* wflag[kIpcMaxWorld];
+    long long* sflag[kIpcMaxWorld];
+    uint32_t* dst[kIpcMaxWorld];
+    const uint32_t* src[kIpcMaxWorld];   // base of the rows
+    const int32_t* idx[kIpcMaxWorld];    // row indices into src (nullptr: contiguous)
+    long long rows[kIpcMaxWorld];
+};
+
+__global__ void k_ipc_rows(IpcRows P, int wwords, long long wait_v, long long sig_v,
+                           unsigned int* done) {
+    if (wait_v > 0) wait_flags(P.wflag, P.n, wait_v);
+    for (int j = 0; j < P.n; ++j) {
+        const long long tot = P.rows[j] * wwords;
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+             t += (long long)gridDim.x * blockDim.x) {
+            const long long r = t / wwords;
+            const int c = (int)(t - r * wwords);
+            const long long sr = P.idx[j] ? (long long)P.idx[j][r] : r;
+            P.dst[j][t] = __ldcg(P.src[j] + sr * wwords + c);
+        }
+    }
+    __threadfence_system();  // this block's stores before its arrival
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
+        __threadfence_system();
+        *done = 0u;  // next launch on this stream starts from zero
+        for (int j = 0; j < P.n; ++j) st_release(P.sflag[j], sig_v);
+    }
+}
+
 struct IpcTransport final : Transport {
     int device = 0;
     int64_t slot_rows = 0;
@@ -328,10 +364,54 @@ struct IpcTransport final : Transport {
         slot_rows = rows;
         mine = win;
     }
+    unsigned int* done = nullptr;               // arrival counters of k_ipc_rows (2)
     ~IpcTransport() override {
         for (int j = 0; j < world; ++j)
             if (j != rank && peer.size() == (size_t)world && peer[j]) cudaIpcCloseMemHandle(peer[j]);
         if (mine) cudaFree(mine);
+        if (done) cudaFree(done);
+    }
+    bool fused_gather() const override { return true; }
+
+    // send: rows sidx[soff[j] ..] of src -> peer j's staging, then ready;
+    // receive: my staging -> recv + roff[j], then ack (2 launches)
+    void exchange_gather(cudaStream_t s, const float* src, const int32_t* sidx, const int64_t* soff,
+                         const int64_t* scnt, float* recv, const int64_t* roff, const int64_t* rcnt,
+                         int width) override {
+        if (!done) {
+            GMD_CUDA(cudaMalloc(&done, 2 * sizeof(unsigned int)));
+            GMD_CUDA(cudaMemsetAsync(done, 0, 2 * sizeof(unsigned int), s));
+        }
+        const long long k = ++epoch;
+        const int par = (int)(k & 1);
+        IpcRows snd{}, rcv{};
+        long long maxrows = 0;
+        for (int j = 0; j < world; ++j) {
+            if (j == rank) continue;
+            if (scnt[j] * width > slot_rows * 16 || rcnt[j] * width > slot_rows * 16)
+                raise(kConfig, "IPC staging too small for the halo (raise staging_rows)");
+            const IpcWin pw = ipc_view(peer[j]), mw = ipc_view(mine);
+            const int i = snd.n;
+            snd.wflag[i] = mw.ack + j;  // j consumed my exchange k-2 (j writes my window)
+            snd.sflag[i] = pw.ready + rank;
+            snd.dst[i] = reinterpret_cast<uint32_t*>(staging(peer[j], par, rank));
+            snd.src[i] = reinterpret_cast<const uint32_t*>(src);
+            snd.idx[i] = sidx + soff[j];
+            snd.rows[i] = scnt[j];
+            rcv.wflag[i] = mw.ready + j;
+            rcv.sflag[i] = pw.ack + rank;  // j may reuse staging[k & 1][it] at k + 2
+            rcv.dst[i] = reinterpret_cast<uint32_t*>(recv + roff[j] * width);
+            rcv.src[i] = reinterpret_cast<const uint32_t*>(staging(mine, par, j));
+            rcv.idx[i] = nullptr;
+            rcv.rows[i] = rcnt[j];
+            maxrows = std::max<long long>(maxrows, std::max<long long>(scnt[j], rcnt[j]));
+            snd.n = rcv.n = i + 1;
+        }
+        const int grid = (int)std::max<long long>(1, std::min<long long>(148, (maxrows * width + 255) / 256));
+        k_ipc_rows<<<grid, 256, 0, s>>>(snd, width, k - 2, k, done);
+        GMD_LAUNCH_CHECK();
+        k_ipc_rows<<<grid, 256, 0, s>>>(rcv, width, k, k, done + 1);
+        GMD_LAUNCH_CHECK();
     }
     const char* name() const override { return "ipc"; }
 

@@ -24,6 +24,16 @@ struct Transport {
     virtual void exchange(cudaStream_t s, const float* send, const int64_t* soff,
                           const int64_t* scnt, float* recv, const int64_t* roff,
                           const int64_t* rcnt, int width) = 0;
+    // the same exchange with the send rows gathered by the transport from
+    // src rows sidx[soff[j] ..) (no separate packing pass); transports that
+    // cannot fuse it pack into `scratch` and call exchange
+    virtual bool fused_gather() const { return false; }
+    virtual void exchange_gather(cudaStream_t s, const float* src, const int32_t* sidx,
+                                 const int64_t* soff, const int64_t* scnt, float* recv,
+                                 const int64_t* roff, const int64_t* rcnt, int width) {
+        (void)s, (void)src, (void)sidx, (void)soff, (void)scnt, (void)recv, (void)roff, (void)rcnt,
+            (void)width;
+    }
     // rank-ordered all-gathers of small host vectors (out: world * n)
     virtual void allgather_f64(cudaStream_t s, const double* in, int n, double* out) = 0;
     virtual void allgather_i64(cudaStream_t s, const int64_t* in, int n, int64_t* out) = 0;
