@@ -239,6 +239,9 @@ int gmd_comm_init_ipc(gmd_handle* h, const uint8_t* handles);
 int gmd_comm_info(const gmd_handle* h, int* rank, int* world);
 int gmd_num_owned(const gmd_handle* h, int64_t* n);
 int gmd_get_owned_ids(gmd_handle* h, int64_t* ids);
+/* owned atoms with no in-edge from a peer's atom: their layer updates run
+ * while the halo exchange is in flight (GMD_OVERLAP=0 disables the split) */
+int gmd_num_interior(const gmd_handle* h, int64_t* n);
 
 /* ---- input synthesis helpers (system.hpp:99-149; host-side) ------------- */
 int gmd_util_rng_uniform(uint64_t seed, int64_t count, double lo, double hi, double* out);

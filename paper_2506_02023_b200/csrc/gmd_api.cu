@@ -310,6 +310,9 @@ struct gmd_handle {
     DBuf cmask, bmask;  // two-hop closure masks per node / edge-table masks per bond
     bool closure_ready = false;
     DBuf nodes, xsend, sendbuf;
+    // the same atoms as evaluated: interior (no halo in-edge) first, then border
+    DBuf nodes_x;
+    int64_t n_int = 0;
     std::vector<int64_t> soff, scnt, roff, rcnt;
     // ... and its bond halo plan (three-body): rows nb .. nb + nb_halo of the
     // per-bond arrays are received, b_* as above in bond rows
@@ -476,6 +479,18 @@ void build_rank_plan(gmd_handle* h, const int32_t* ownp, int r) {
     sync(h);
     h->n_own = nown;
     launch_owned_compact(ownp, n, r, flag, h->nodes.get<int32_t>(nown), s);
+    {  // interior atoms first: their layer updates overlap the halo exchange
+        int32_t* pos = h->counts.get<int32_t>(nown + 1);
+        launch_flag_interior(nown, h->nodes.as<int32_t>(), h->row.as<int32_t>(), h->src.as<int32_t>(),
+                             ownp, r, pos, s);
+        scan_i32(h, pos, pos, nown);
+        launch_split_nodes(nown, h->nodes.as<int32_t>(), pos, h->nodes_x.get<int32_t>(std::max(1, nown)),
+                           s);
+        int32_t ni = 0;
+        GMD_CUDA(cudaMemcpyAsync(&ni, pos + nown, 4, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        h->n_int = ni;
+    }
     const int32_t t0 = A.list_off[(size_t)r * stride + 1], t1 = A.list_off[(size_t)r * stride + 1 + W];
     launch_send_rows(t0, t1, A.node_array.as<int32_t>(), A.crow.as<int32_t>(),
                      h->xsend.get<int32_t>(std::max(1, t1 - t0)), s);
@@ -1186,8 +1201,19 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                         !(tb && L == 1) && bwd_edge_grid(n / kForceChunks) == vgrid)
                            ? kForceChunks
                            : 1;
-    double* e_part = h->e_part.get<double>(grid);
-    double* v_part = h->v_part.get<double>((size_t)L * vgrid * 6);
+    // one rank per GPU: interior atoms (h->nodes_x[0, n_int)) compute while
+    // the halo rows are in flight, the border atoms after they landed; the
+    // two launches have their own energy / virial partial slots
+    const char* ov_env = std::getenv("GMD_OVERLAP");
+    const bool overlap = rank_mode && !use_tc && h->n_int > 0 && h->n_int < n &&
+                         !(ov_env && ov_env[0] == '0');
+    const int halves = overlap ? 2 : 1;
+    double* e_part = h->e_part.get<double>((size_t)grid * halves);
+    double* v_part = h->v_part.get<double>((size_t)L * halves * vgrid * 6);
+    if (overlap) {
+        GMD_CUDA(cudaMemsetAsync(e_part, 0, sizeof(double) * grid * halves, s));
+        GMD_CUDA(cudaMemsetAsync(v_part, 0, sizeof(double) * L * halves * vgrid * 6, s));
+    }
     const int tgrid = wide ? wide_tb_grid(n) : tgen ? gen_grid(n) * 8 : tb_grid_size(n);
     double* v3_part = h->v3_part.get<double>((size_t)tgrid * 9);
     double* red = h->red.get<double>(16);
@@ -1195,7 +1221,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     if (rank_mode) GMD_CUDA(cudaMemsetAsync(pa, 0, sizeof(double) * n_all, s));
 
     ConvArgs a{n,
-               rank_mode ? h->nodes.as<int32_t>() : nullptr,
+               rank_mode ? h->nodes_x.as<int32_t>() : nullptr,
                part ? A.crow.as<int32_t>() : nullptr,
                h->row.as<int32_t>(),
                part ? h->lsrc.as<int32_t>() : h->src.as<int32_t>(),
@@ -1262,6 +1288,23 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             } else {
                 launch_exchange(A.nfrom, xd, fwd ? xs_fwd : xs, buf, kF, s);
             }
+        }
+    };
+
+    // split exchange (overlap): sends now, receives at exchange_end
+    auto exchange_begin = [&](float* buf) {
+        if (h->comm->fused_gather()) {
+            PROF("halo_send");
+            h->comm->exchange_gather_begin(s, buf, h->xsend.as<int32_t>(), h->soff.data(), h->scnt.data(),
+                                           buf, h->roff.data(), h->rcnt.data(), F);
+        } else {
+            exchange(buf);
+        }
+    };
+    auto exchange_end = [&]() {
+        if (h->comm->fused_gather()) {
+            PROF("halo_recv");
+            h->comm->exchange_gather_end(s);
         }
     };
 
@@ -1334,17 +1377,33 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                     launch_tb_inject(ba, TP, H[l], TH4, s);
             }
         }
-        if (l > 0 || tbl) exchange(H[l], true);
-        PROF("conv");
-        if (wide)
-            launch_wide_conv(h->gm, a, l, H[l], H[l + 1], TH + (size_t)l * n * F,
-                             l == L - 1 ? pa : nullptr, s);
-        else if (gen)
-            launch_gen_conv(h->gm, a, l, H[l], H[l + 1], TH + (size_t)l * n * F,
-                            l == L - 1 ? pa : nullptr, s);
-        else
-            launch_conv(a, l, H[l], H[l + 1], TH + (size_t)l * n * kF, l == L - 1 ? pa : nullptr,
-                        l == L - 1 ? e_part : nullptr, s);
+        // nodes [k0, k1) of the evaluation order; energy partials in half `hf`
+        auto conv = [&](int64_t k0, int64_t k1, int hf) {
+            if (k1 <= k0) return;
+            PROF("conv");
+            ConvArgs ar = a;
+            ar.n = k1 - k0;
+            if (ar.nodes) ar.nodes += k0;
+            float* th = TH + ((size_t)l * n + k0) * F;
+            double* pl = l == L - 1 ? pa : nullptr;
+            if (wide)
+                launch_wide_conv(h->gm, ar, l, H[l], H[l + 1], th, pl, s);
+            else if (gen)
+                launch_gen_conv(h->gm, ar, l, H[l], H[l + 1], th, pl, s);
+            else
+                launch_conv(ar, l, H[l], H[l + 1], th, pl, l == L - 1 ? e_part + (size_t)hf * grid : nullptr,
+                            s);
+        };
+        const bool halo = l > 0 || tbl;
+        if (halo && overlap) {
+            exchange_begin(H[l]);
+            conv(0, h->n_int, 0);
+            exchange_end();
+            conv(h->n_int, n, 1);
+        } else {
+            if (halo) exchange(H[l], true);
+            conv(0, n, 0);
+        }
     }
     GMD_CUDA(cudaEventRecord(h->ev[4], s));
     // per-atom energies are final after the forward: copy them to the host
@@ -1369,8 +1428,27 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             else
                 launch_bwd_node(n, a.nodes, a.crow, l, HB, TH + (size_t)l * n * kF, MB, l == L - 1, s);
         }
-        exchange(MB);
-        {
+        if (overlap) {
+            auto edge = [&](int64_t k0, int64_t k1, int hf) {
+                if (k1 <= k0) return;
+                PROF("bwd_edge");
+                ConvArgs ar = a;
+                ar.n = k1 - k0;
+                ar.nodes += k0;
+                double* vp = v_part + ((size_t)l * 2 + hf) * vgrid * 6;
+                if (wide)
+                    launch_wide_bwd_edge(h->gm, ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
+                else if (gen)
+                    launch_gen_bwd_edge(h->gm, ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
+                else
+                    launch_bwd_edge(ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
+            };
+            exchange_begin(MB);
+            edge(0, h->n_int, 0);
+            exchange_end();
+            edge(h->n_int, n, 1);
+        } else {
+            exchange(MB);
             PROF("bwd_edge");
             if (wide)
                 launch_wide_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
@@ -1455,7 +1533,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         PROF("reduce");
         // generic kernels: the energy is the fixed-order sum of the per-atom energies
         const double* ps[3] = {gen ? pa : e_part, v_part, v3_part};
-        const int np[3] = {gen ? (int)n_all : grid, L * vgrid, tgrid},
+        const int np[3] = {gen ? (int)n_all : grid * halves, L * halves * vgrid, tgrid},
                   w[3] = {1, 6, 9};
         if (!tb) GMD_CUDA(cudaMemsetAsync(red + 7, 0, 9 * sizeof(double), s));
         launch_reduce_sets(tb ? 3 : 2, ps, np, w, red, s);
@@ -1622,7 +1700,7 @@ void gmd_destroy(gmd_handle* h) {
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ed, &h->ebond, &h->edst, &h->lsrc, &h->counts,
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge, &h->ebid,
-                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->flagtmp, &h->nodes, &h->xsend, &h->sendbuf, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
+                    &h->brev, &h->lcnt, &h->lpairs, &h->slab, &h->feat_tmp, &h->flagtmp, &h->nodes, &h->nodes_x, &h->xsend, &h->sendbuf, &h->TH, &h->MB, &h->HB, &h->GRAD, &h->TP,
                     &h->TH3, &h->TH4, &h->QB, &h->VIN, &h->VOUT, &h->e_part, &h->v_part,
                     &h->v3_part, &h->red, &h->per_atom, &h->forces, &h->conv_tmp, &h->exp_tmp,
                     &h->md_part, &h->md_out, &h->md_bad, &h->md_pos, &h->md_vel, &h->md_frc,
@@ -2807,6 +2885,12 @@ int gmd_comm_info(const gmd_handle* h, int* rank, int* world) {
 int gmd_num_owned(const gmd_handle* h, int64_t* n) {
     if (!h || !n) return GMD_ERR_ARG;
     *n = h->built ? (h->comm && h->comm->world > 1 ? h->n_own : h->n) : 0;
+    return GMD_OK;
+}
+
+int gmd_num_interior(const gmd_handle* h, int64_t* n) {
+    if (!h || !n) return GMD_ERR_ARG;
+    *n = h->built && h->comm && h->comm->world > 1 ? h->n_int : 0;
     return GMD_OK;
 }
 

@@ -378,6 +378,16 @@ struct IpcTransport final : Transport {
     void exchange_gather(cudaStream_t s, const float* src, const int32_t* sidx, const int64_t* soff,
                          const int64_t* scnt, float* recv, const int64_t* roff, const int64_t* rcnt,
                          int width) override {
+        exchange_gather_begin(s, src, sidx, soff, scnt, recv, roff, rcnt, width);
+        exchange_gather_end(s);
+    }
+    IpcRows pending{};  // receive half of the exchange begun last
+    long long pending_k = 0;
+    int pending_w = 0, pending_grid = 0;
+    void exchange_gather_begin(cudaStream_t s, const float* src, const int32_t* sidx,
+                               const int64_t* soff, const int64_t* scnt, float* recv,
+                               const int64_t* roff, const int64_t* rcnt, int width) override {
+        if (pending_k) raise(kRuntime, "internal: IPC exchange begun twice");
         if (!done) {
             GMD_CUDA(cudaMalloc(&done, 2 * sizeof(unsigned int)));
             GMD_CUDA(cudaMemsetAsync(done, 0, 2 * sizeof(unsigned int), s));
@@ -410,7 +420,15 @@ struct IpcTransport final : Transport {
         const int grid = (int)std::max<long long>(1, std::min<long long>(148, (maxrows * width + 255) / 256));
         k_ipc_rows<<<grid, 256, 0, s>>>(snd, width, k - 2, k, done);
         GMD_LAUNCH_CHECK();
-        k_ipc_rows<<<grid, 256, 0, s>>>(rcv, width, k, k, done + 1);
+        pending = rcv;
+        pending_k = k;
+        pending_w = width;
+        pending_grid = grid;
+    }
+    void exchange_gather_end(cudaStream_t s) override {
+        if (!pending_k) raise(kRuntime, "internal: IPC exchange not begun");
+        k_ipc_rows<<<pending_grid, 256, 0, s>>>(pending, pending_w, pending_k, pending_k, done + 1);
+        pending_k = 0;
         GMD_LAUNCH_CHECK();
     }
     const char* name() const override { return "ipc"; }

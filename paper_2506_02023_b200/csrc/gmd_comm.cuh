@@ -34,6 +34,16 @@ struct Transport {
         (void)s, (void)src, (void)sidx, (void)soff, (void)scnt, (void)recv, (void)roff, (void)rcnt,
             (void)width;
     }
+    // split form of exchange_gather: begin issues the sends, end completes the
+    // receives; stream work between them that does not touch recv's halo rows
+    // (interior atoms) overlaps the transfer.  Transports without a split do
+    // the whole exchange in begin.
+    virtual void exchange_gather_begin(cudaStream_t s, const float* src, const int32_t* sidx,
+                                       const int64_t* soff, const int64_t* scnt, float* recv,
+                                       const int64_t* roff, const int64_t* rcnt, int width) {
+        exchange_gather(s, src, sidx, soff, scnt, recv, roff, rcnt, width);
+    }
+    virtual void exchange_gather_end(cudaStream_t s) { (void)s; }
     // rank-ordered all-gathers of small host vectors (out: world * n)
     virtual void allgather_f64(cudaStream_t s, const double* in, int n, double* out) = 0;
     virtual void allgather_i64(cudaStream_t s, const int64_t* in, int n, int64_t* out) = 0;

@@ -165,6 +165,28 @@ __global__ void k_compact_owned(const int32_t* __restrict__ owner, int64_t n, in
     if (v < n && owner[v] == r) nodes[pos[v]] = (int32_t)v;
 }
 
+// interior atoms of rank r: every in-edge source owned by r, so their
+// layer update reads no halo row and can run while the halo is in flight
+__global__ void k_flag_interior(int64_t n_own, const int32_t* __restrict__ nodes,
+                                const int32_t* __restrict__ row, const int32_t* __restrict__ src,
+                                const int32_t* __restrict__ owner, int r, int32_t* __restrict__ flag) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_own) return;
+    const int v = nodes[k];
+    int in = 1;
+    for (int e = row[v]; e < row[v + 1] && in; ++e) in = owner[src[e]] == r;
+    flag[k] = in;
+}
+
+// stable split: interior atoms first, then the border atoms, ascending in each
+__global__ void k_split_nodes(int64_t n_own, const int32_t* __restrict__ nodes,
+                              const int32_t* __restrict__ pos, int32_t* __restrict__ out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_own) return;
+    const int64_t n_int = pos[n_own];
+    out[pos[k + 1] > pos[k] ? pos[k] : n_int + k - pos[k]] = nodes[k];
+}
+
 // send plan: canonical row of every TO row of partition r (TO region rows
 // [t0, t1) of the super layout)
 __global__ void k_send_rows(int32_t t0, int32_t t1, const int32_t* __restrict__ node_array,
@@ -422,6 +444,20 @@ void launch_owned_flags(const int32_t* owner, int64_t n, int r, int32_t* flag, c
 void launch_owned_compact(const int32_t* owner, int64_t n, int r, const int32_t* pos,
                           int32_t* nodes, cudaStream_t s) {
     k_compact_owned<<<div_up(n, 256), 256, 0, s>>>(owner, n, r, pos, nodes);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_flag_interior(int64_t n_own, const int32_t* nodes, const int32_t* row, const int32_t* src,
+                          const int32_t* owner, int r, int32_t* flag, cudaStream_t s) {
+    if (n_own <= 0) return;
+    k_flag_interior<<<div_up(n_own, 256), 256, 0, s>>>(n_own, nodes, row, src, owner, r, flag);
+    GMD_LAUNCH_CHECK();
+}
+
+void launch_split_nodes(int64_t n_own, const int32_t* nodes, const int32_t* pos, int32_t* out,
+                        cudaStream_t s) {
+    if (n_own <= 0) return;
+    k_split_nodes<<<div_up(n_own, 256), 256, 0, s>>>(n_own, nodes, pos, out);
     GMD_LAUNCH_CHECK();
 }
 

@@ -55,6 +55,12 @@ void launch_required_rank(const int32_t* row, const int32_t* src, int64_t n, con
 void launch_owned_flags(const int32_t* owner, int64_t n, int r, int32_t* flag, cudaStream_t s);
 void launch_owned_compact(const int32_t* owner, int64_t n, int r, const int32_t* pos,
                           int32_t* nodes, cudaStream_t s);
+// interior / border split of r's atoms (flag[k] = 1: no in-edge from a peer's
+// atom; out = interior ascending, then border ascending; pos = scan of flag)
+void launch_flag_interior(int64_t n_own, const int32_t* nodes, const int32_t* row, const int32_t* src,
+                          const int32_t* owner, int r, int32_t* flag, cudaStream_t s);
+void launch_split_nodes(int64_t n_own, const int32_t* nodes, const int32_t* pos, int32_t* out,
+                        cudaStream_t s);
 void launch_send_rows(int32_t t0, int32_t t1, const int32_t* node_array, const int32_t* crow,
                       int32_t* xsend, cudaStream_t s);
 

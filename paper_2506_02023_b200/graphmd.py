@@ -48,7 +48,7 @@ EXPORTS = [
     "gmd_sync_duplicates", "gmd_distribute", "gmd_aggregate",
     "gmd_corrupt_transfer_plan_for_test", "gmd_util_rng_uniform", "gmd_util_supercell",
     "gmd_profile", "gmd_profile_read", "gmd_get_stream", "gmd_launch_count", "gmd_comm_nccl_id",
-    "gmd_comm_init_nccl", "gmd_comm_init_local", "gmd_comm_info", "gmd_num_owned", "gmd_get_owned_ids",
+    "gmd_comm_init_nccl", "gmd_comm_init_local", "gmd_comm_info", "gmd_num_owned", "gmd_get_owned_ids", "gmd_num_interior",
     "gmd_md_masses", "gmd_md_maxwell_boltzmann", "gmd_md_evaluate", "gmd_md_step", "gmd_md_observe",
     "gmd_md_run", "gmd_comm_ipc_export", "gmd_comm_init_ipc",
     # free builder API (partitioner.hpp / linegraph.hpp / neighborlist.hpp)
@@ -128,6 +128,7 @@ def lib():
             "gmd_comm_init_local": (I, [V, I]),
             "gmd_comm_info": (I, [V, V, V]),
             "gmd_num_owned": (I, [V, V]),
+            "gmd_num_interior": (I, [V, V]),
             "gmd_get_owned_ids": (I, [V, V]),
             "gmd_md_masses": (I, [I64, V, V]),
             "gmd_md_maxwell_boltzmann": (I, [I64, V, D, U64, V]),
@@ -975,6 +976,13 @@ def local_group(world: int, device: int = 0) -> List["_Handle"]:
     if rc:
         raise Error("gmd_comm_init_local failed", rc)
     return hs
+
+
+def num_interior(dist: "Distributed") -> int:
+    """Owned atoms whose in-edges all come from owned atoms (rank mode)."""
+    n = C.c_int64()
+    dist.handle.check(lib().gmd_num_interior(dist.handle.h, C.byref(n)))
+    return n.value
 
 
 def owned_ids(dist: "Distributed") -> np.ndarray:

@@ -91,3 +91,28 @@ def test_rank_group_three_body(W, which, kern, monkeypatch):
         assert abs(out.energy - ref.energy) <= 1e-9 * abs(ref.energy)
         np.testing.assert_allclose(out.stress, ref.stress, atol=1e-12, rtol=1e-9)
     assert seen.all()
+
+
+@pytest.mark.parametrize("W", [2, 3])
+@pytest.mark.parametrize("F,K", [(16, 8), (24, 6), (64, 8)])
+@pytest.mark.parametrize("r3", [None, 3.0])
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_rank_group_interior_overlap(W, F, K, r3, overlap, monkeypatch):
+    """Slabs thick enough to have interior atoms (no in-edge from a peer):
+    those compute while the halo is in flight, the border atoms after it
+    landed, in two launches per layer.  Per-atom energies and forces stay
+    bitwise equal to the single handle, with and without the split."""
+    monkeypatch.setenv("GMD_OVERLAP", overlap)
+    s = S.quartz((8, 4, 4))
+    prm = G.ToyPotentialParams.init(5, F, K, 3, 5.0, r3 or 0.0)
+    ref = G.forward_distributed(G.Distributed.create_distributed(s, 5.0, r3, W, 1, True), prm)
+    res = run_group(s, prm, W, r3=r3)
+    seen = np.zeros(s.size(), bool)
+    for d, out, ids in res:
+        seen[ids] = True
+        assert 0 < G.num_interior(d) < len(ids)
+        np.testing.assert_array_equal(out.per_atom[ids], ref.per_atom[ids])
+        np.testing.assert_array_equal(out.forces[ids], ref.forces[ids])
+        assert abs(out.energy - ref.energy) <= 1e-9 * abs(ref.energy)
+        np.testing.assert_allclose(out.stress, ref.stress, atol=1e-12, rtol=1e-9)
+    assert seen.all()

@@ -24,16 +24,21 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, which, r3, outdir):
+def _system(which):
+    from tests import systems as S
+
+    return {"quartz": lambda: S.quartz((4, 4, 4)), "liquid": lambda: S.liquid(1200),
+            "slab": lambda: S.quartz((8, 4, 4))}[which]()
+
+
+def _worker(rank, world, port, which, r3, F, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2506_02023_b200 import graphmd as G
-        from tests import systems as S
-
-        s = S.quartz((4, 4, 4)) if which == "quartz" else S.liquid(1200)
-        prm = G.ToyPotentialParams.init(7, 16, 8, 3, 5.0, r3)
+        s = _system(which)
+        prm = G.ToyPotentialParams.init(7, F, 8, 3, 5.0, r3)
         h = G._Handle(0)
         G.init_rank_comm_ipc(h, rank, world, slot_rows=4 * s.size())
         d = G.Distributed.create_distributed(s, 5.0, r3 if r3 > 0 else None, world, 1, True,
@@ -42,24 +47,26 @@ def _worker(rank, world, port, which, r3, outdir):
         ids = G.owned_ids(d)
         # a second evaluation reuses the windows (exchange epochs > 2)
         out2 = G.forward_distributed(d, prm)
-        np.savez(os.path.join(outdir, f"r{rank}.npz"), ids=ids, pa=out.per_atom[ids],
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), ids=ids, nint=G.num_interior(d), pa=out.per_atom[ids],
                  f=out.forces[ids], e=out.energy, st=out.stress, pa2=out2.per_atom[ids])
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("which,r3", [("quartz", 0.0), ("liquid", 3.0)])
-def test_ipc_rank_processes_equal_single_handle(tmp_path, world, which, r3):
+@pytest.mark.parametrize("which,r3,F", [("quartz", 0.0, 16), ("liquid", 3.0, 16), ("slab", 0.0, 16),
+                                        ("slab", 3.0, 16), ("slab", 3.0, 64)])
+def test_ipc_rank_processes_equal_single_handle(tmp_path, world, which, r3, F):
+    """("slab": thick slabs with interior atoms, whose layer updates run
+    between the send and the receive kernel of each exchange.)"""
     from paper_2506_02023_b200 import graphmd as G
-    from tests import systems as S
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     os.environ["PYTHONPATH"] = root + os.pathsep + os.environ.get("PYTHONPATH", "")
-    mp.start_processes(_worker, args=(world, _free_port(), which, r3, str(tmp_path)),
+    mp.start_processes(_worker, args=(world, _free_port(), which, r3, F, str(tmp_path)),
                        nprocs=world, join=True, start_method="spawn")
-    s = S.quartz((4, 4, 4)) if which == "quartz" else S.liquid(1200)
-    prm = G.ToyPotentialParams.init(7, 16, 8, 3, 5.0, r3)
+    s = _system(which)
+    prm = G.ToyPotentialParams.init(7, F, 8, 3, 5.0, r3)
     ref = G.forward_distributed(
         G.Distributed.create_distributed(s, 5.0, r3 if r3 > 0 else None, world, 1, True), prm)
     seen = np.zeros(s.size(), bool)
@@ -68,6 +75,8 @@ def test_ipc_rank_processes_equal_single_handle(tmp_path, world, which, r3):
         ids = z["ids"]
         assert not seen[ids].any()
         seen[ids] = True
+        if which == "slab":
+            assert 0 < int(z["nint"]) < len(ids)
         np.testing.assert_array_equal(z["pa"], ref.per_atom[ids])
         np.testing.assert_array_equal(z["pa2"], ref.per_atom[ids])
         np.testing.assert_array_equal(z["f"], ref.forces[ids])
