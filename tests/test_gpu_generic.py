@@ -92,3 +92,27 @@ def test_generic_rank_group_equals_single_handle(r3):
         assert abs(out.energy - ref.energy) <= 1e-9 * abs(ref.energy)
         np.testing.assert_allclose(out.stress, ref.stress, atol=1e-12, rtol=1e-9)
     assert seen.all()
+
+
+@pytest.mark.parametrize("variant", [{"GMD_WIDE_FF": "16"}, {"GMD_WIDE_TC": "1"}])
+def test_wide_backward_families_agree(monkeypatch, oracle_c, variant):
+    """F = 64 backward edge pass: the default packed-FP32 kernel (32-edge
+    chunks, transposed warp reduction) against its 16-edge-chunk form and the
+    tcgen05 form (G = X P, 3xTF32 in TMEM); all three are checked against the
+    oracle and keep exact Newton's third law (test_gpu_physics bound)."""
+    s = S.liquid(1500)
+    prm = G.ToyPotentialParams.init(9, 64, 8, 2, 5.0, 3.0)
+    ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, 64, 8, 2, 5.0, 3.0)
+    for k in ("GMD_WIDE_FF", "GMD_WIDE_TC"):
+        monkeypatch.delenv(k, raising=False)
+    a = run(s, prm)
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    b = run(s, prm, 2)
+    assert a.energy == b.energy  # the forward is shared
+    fmax = np.abs(ref["forces"]).max()
+    for out in (a, b):
+        assert np.abs(out.forces - ref["forces"]).max() <= max(4e-4, 4e-5 * fmax)
+        assert np.abs(out.stress - ref["stress"]).max() <= 4e-6
+        assert np.abs(out.forces.sum(axis=0)).max() <= 1e-12 * fmax * s.size()
+    np.testing.assert_allclose(b.forces, a.forces, rtol=0, atol=2e-5 * fmax)
