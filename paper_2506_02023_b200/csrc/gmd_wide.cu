@@ -9,6 +9,7 @@
 //               psi_k = phi_k (ca + cb k)
 //     grad_u -= v_e dsum_e / d_e,  virial += 1/2 dsum_e / d_e v_e (x) v_e
 #include <cstdlib>
+#include <string>
 
 #include "gmd_tc.cuh"
 #include "gmd_wide.cuh"
@@ -737,6 +738,170 @@ __global__ void __launch_bounds__(kFW * 32, MINB) k_wide_bwd_edge_ff(GenModel g,
     }
 }
 
+// Same pass with the per-edge partials in shared memory instead of
+// registers: lane l stores its share of X . s' for slot i at part[i][l]
+// (one conflict-free row per edge), and lane j then sums row j over
+// l = 0..31 in order (8 LDS.128) -- the same order for every edge, so the
+// exactness argument above holds; 32 registers fewer (three CTAs per SM).
+// Slots are padded to a multiple of BATCH with u = psi = 0 and a valid row,
+// whose terms are exact zeros: no per-slot branches in the feature loop.
+constexpr int kPartLd = 36;  // row stride (floats): 16-byte reads conflict-free
+
+struct BwdSmSmem {
+    float4 u[kFW][32][2];
+    float4 psi[kFW][32][2];
+    int src[kFW][32];
+    float part[kFW][32][kPartLd];
+};
+
+template <int BATCH, int MINB>
+__global__ void __launch_bounds__(kFW * 32, MINB) k_wide_bwd_edge_sm(GenModel g, Basis bs, ConvArgs a,
+                                                                     const float* __restrict__ MB,
+                                                                     const float* __restrict__ Hl,
+                                                                     float* __restrict__ HB,
+                                                                     double4* __restrict__ GRAD,
+                                                                     double* __restrict__ vir_part) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    BwdSmSmem& S = *reinterpret_cast<BwdSmSmem*>(smraw);
+    __shared__ double wv[kFW][6];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    float2 P2[K];  // (P[2l][k], P[2l+1][k])
+#pragma unroll
+    for (int k = 0; k < K; ++k) P2[k] = make_float2(g.P[(2 * lane) * K + k], g.P[(2 * lane + 1) * K + k]);
+    if (lane < 6) wv[wq][lane] = 0.0;  // per-warp fp64 virial (lane 0 accumulates)
+    __syncwarp();
+    float* prow = &S.part[wq][0][lane];
+    for (int64_t k = (int64_t)blockIdx.x * kFW + wq; k < a.n; k += (int64_t)gridDim.x * kFW) {
+        const int64_t v = a.nodes ? (int64_t)a.nodes[k] : k;
+        const int64_t r = a.crow ? (int64_t)a.crow[v] : v;
+        const int e0 = a.row[v], e1 = a.row[v + 1];
+        const float2 mu = reinterpret_cast<const float2*>(MB + (size_t)r * F)[lane];
+        const float2 hu = reinterpret_cast<const float2*>(Hl + (size_t)r * F)[lane];
+        const float2 su = __fadd2_rn(mu, hu), ndu = __fadd2_rn(make_float2(-mu.x, -mu.y), hu);  // S_u, -D_u
+        float2 hb = make_float2(0.f, 0.f);
+        double gx = 0.0, gy = 0.0, gz = 0.0;  // fp64: exact sums of antisymmetric terms
+        float vr[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int eb = e0; eb < e1; eb += 32) {
+            const int ne = min(32, e1 - eb);
+            const int nep = (ne + BATCH - 1) / BATCH * BATCH;
+            // (1) edge lanes: radial scalars of the chunk (padding: zeros)
+            float4 q = make_float4(0.f, 0.f, 0.f, 1.f);
+            if (lane < ne) {
+                q = __ldg(a.vd + eb + lane);
+                const float d = q.w;
+                float phi[K];
+                phi8(bs, d, phi);
+                float sn, cs;
+                __sincosf(d * bs.pi_rc, &sn, &cs);
+                const bool in = d < bs.rc;
+                const float fc = in ? 0.5f * cs + 0.5f : 0.0f;
+                const float dfc = in ? -0.5f * bs.pi_rc * sn : 0.0f;
+                const float x0 = d * bs.isg, stp = bs.mus * bs.isg;
+                const float ca = dfc - 2.0f * fc * bs.isg * x0, cb = 2.0f * fc * bs.isg * stp;
+                float psi[K];
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) psi[kk] = phi[kk] * fmaf(cb, (float)kk, ca);
+                S.psi[wq][lane][0] = make_float4(psi[0], psi[1], psi[2], psi[3]);
+                S.psi[wq][lane][1] = make_float4(psi[4], psi[5], psi[6], psi[7]);
+                S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
+                S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+                S.src[wq][lane] = a.lsrc[eb + lane];
+            } else if (lane < nep) {
+                const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                S.psi[wq][lane][0] = S.psi[wq][lane][1] = S.u[wq][lane][0] = S.u[wq][lane][1] = z4;
+                S.src[wq][lane] = (int)r;
+            }
+            __syncwarp();
+            // (2) feature lanes: h_bar and this lane's share of X . s' per edge
+            for (int i0 = 0; i0 < nep; i0 += BATCH) {
+                float2 mw[BATCH], hw[BATCH];
+#pragma unroll
+                for (int j = 0; j < BATCH; ++j) {
+                    const int w = S.src[wq][i0 + j];
+                    mw[j] = __ldg(reinterpret_cast<const float2*>(MB + (size_t)w * F) + lane);
+                    hw[j] = __ldg(reinterpret_cast<const float2*>(Hl + (size_t)w * F) + lane);
+                }
+#pragma unroll
+                for (int j = 0; j < BATCH; ++j) {
+                    const int i = i0 + j;
+                    const float4 ua = S.u[wq][i][0], ub = S.u[wq][i][1];
+                    float2 sv = f2mul(P2[0], bc2(ua.x));
+                    sv = f2fma(P2[1], bc2(ua.y), sv);
+                    sv = f2fma(P2[2], bc2(ua.z), sv);
+                    sv = f2fma(P2[3], bc2(ua.w), sv);
+                    sv = f2fma(P2[4], bc2(ub.x), sv);
+                    sv = f2fma(P2[5], bc2(ub.y), sv);
+                    sv = f2fma(P2[6], bc2(ub.z), sv);
+                    sv = f2fma(P2[7], bc2(ub.w), sv);
+                    hb = f2fma(mw[j], sv, hb);
+                    const float4 pa = S.psi[wq][i][0], pb = S.psi[wq][i][1];
+                    float2 sp = f2mul(P2[0], bc2(pa.x));
+                    sp = f2fma(P2[1], bc2(pa.y), sp);
+                    sp = f2fma(P2[2], bc2(pa.z), sp);
+                    sp = f2fma(P2[3], bc2(pa.w), sp);
+                    sp = f2fma(P2[4], bc2(pb.x), sp);
+                    sp = f2fma(P2[5], bc2(pb.y), sp);
+                    sp = f2fma(P2[6], bc2(pb.z), sp);
+                    sp = f2fma(P2[7], bc2(pb.w), sp);
+                    // 2 X = S_u S_w - D_u D_w: symmetric under u <-> w
+                    const float2 sw = __fadd2_rn(mw[j], hw[j]);
+                    const float2 dw = __fadd2_rn(mw[j], make_float2(-hw[j].x, -hw[j].y));
+                    const float2 x = f2fma(su, sw, f2mul(ndu, dw));
+                    const float2 xs = f2mul(x, sp);
+                    prow[i * kPartLd] = __fadd_rn(xs.x, xs.y);
+                }
+            }
+            __syncwarp();
+            // (3) lane j: dsum of edge j (row j summed over lanes in order),
+            // gradient and virial
+            if (lane < ne) {
+                const float4* pr = reinterpret_cast<const float4*>(&S.part[wq][lane][0]);
+                float dsum = 0.f;
+#pragma unroll
+                for (int c4 = 0; c4 < 8; ++c4) {
+                    const float4 p4 = pr[c4];
+                    dsum = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(dsum, p4.x), p4.y), p4.z), p4.w);
+                }
+                const float coef = (0.5f * dsum) / q.w;
+                gx -= (double)(q.x * coef);
+                gy -= (double)(q.y * coef);
+                gz -= (double)(q.z * coef);
+                const float ch = 0.5f * coef;
+                vr[0] = fmaf(ch * q.x, q.x, vr[0]);
+                vr[1] = fmaf(ch * q.y, q.y, vr[1]);
+                vr[2] = fmaf(ch * q.z, q.z, vr[2]);
+                vr[3] = fmaf(ch * q.x, q.y, vr[3]);
+                vr[4] = fmaf(ch * q.x, q.z, vr[4]);
+                vr[5] = fmaf(ch * q.y, q.z, vr[5]);
+            }
+            __syncwarp();
+        }
+        // node complete: one writer per element
+        float2* hbp = reinterpret_cast<float2*>(HB + (size_t)k * F) + lane;
+        const float2 old = *hbp;
+        *hbp = make_float2(old.x + hb.x, old.y + hb.y);
+        const double sx = gwarp_sumd(gx), sy = gwarp_sumd(gy), sz = gwarp_sumd(gz);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
+        if (lane == 0) {
+            double4 gr = GRAD[k];
+            gr.x += sx;
+            gr.y += sy;
+            gr.z += sz;
+            GRAD[k] = gr;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) wv[wq][c] += (double)vr[c];
+        }
+    }
+    // fp64 virial: warp records in fixed order -> CTA record
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double acc = 0.0;
+        for (int w = 0; w < kFW; ++w) acc += wv[w][threadIdx.x];
+        vir_part[(size_t)blockIdx.x * 6 + threadIdx.x] = acc;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // three-body stage (potential.cpp:664-741, 850-961), the generic kernels'
 // slot conventions: slot j of center s = in-bond b0 + j (x_j -> s); TP / TH3 /
@@ -1311,19 +1476,28 @@ int wide_conv_grid(int64_t n) {
     return (int)(g > 0 ? g : 1);
 }
 
-// backward edge kernel: 0 = packed FP32, 32-edge chunks (default); 1 = 16-edge
-// chunks (GMD_WIDE_FF=16); 2 = G = X P on tcgen05 (GMD_WIDE_TC=1)
-// (read per call: tests switch kernel families)
+// backward edge kernel (GMD_WIDE_BWD, read per call: tests switch families):
+// "sm" (default) partials in shared memory, 4 rows in flight, 3 CTAs per SM;
+// "sm8" 8 rows in flight, 2 CTAs; "ff" / "ff16" register partials with the
+// transposed butterfly, 32 / 16-edge chunks; "tc" G = X P on tcgen05 (also
+// GMD_WIDE_TC=1)
+enum { kBwdSm4, kBwdSm8, kBwdFf32, kBwdFf16, kBwdTc };
 static int bwd_variant() {
     const char* tc = std::getenv("GMD_WIDE_TC");
-    if (tc && std::atoi(tc) == 1) return 2;
-    const char* ff = std::getenv("GMD_WIDE_FF");
-    return ff && std::atoi(ff) == 16 ? 1 : 0;
+    if (tc && std::atoi(tc) == 1) return kBwdTc;
+    const char* v = std::getenv("GMD_WIDE_BWD");
+    if (!v) return kBwdSm4;
+    const std::string s(v);
+    return s == "sm8" ? kBwdSm8 : s == "ff" ? kBwdFf32 : s == "ff16" ? kBwdFf16 : s == "tc" ? kBwdTc : kBwdSm4;
+}
+static int bwd_ctas_per_sm() {
+    const int v = bwd_variant();
+    return v == kBwdSm4 || v == kBwdFf16 ? 3 : 2;
 }
 
-int wide_bwd_grid(int64_t n) {  // one wave: 2 CTAs per SM (3 for 16-edge chunks)
+int wide_bwd_grid(int64_t n) {  // one wave
     int64_t g = (n + kBW - 1) / kBW;
-    const int64_t cap = 148 * (bwd_variant() == 1 ? 3 : 2);
+    const int64_t cap = 148 * bwd_ctas_per_sm();
     if (g > cap) g = cap;
     return (int)(g > 0 ? g : 1);
 }
@@ -1446,11 +1620,24 @@ void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB,
                                       (int)sizeof(BwdSmem) + 1024));
         attr = true;
     }
-    if (bwd_variant() != 2) {  // packed FP32 + transposed reduction
-        if (bwd_variant() == 1)
-            k_wide_bwd_edge_ff<16, 3><<<grid, kFW * 32, 0, s>>>(g, make_basis(g), a, MB, Hl, HB, GRAD, vir_part);
+    const int var = bwd_variant();
+    if (var != kBwdTc) {
+        const Basis bs = make_basis(g);
+        const size_t sm = sizeof(BwdSmSmem);
+        static bool attr_sm = false;
+        if (!attr_sm) {
+            GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge_sm<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge_sm<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr_sm = true;
+        }
+        if (var == kBwdSm4)
+            k_wide_bwd_edge_sm<4, 3><<<grid, kFW * 32, sm, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);
+        else if (var == kBwdSm8)
+            k_wide_bwd_edge_sm<8, 2><<<grid, kFW * 32, sm, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);
+        else if (var == kBwdFf16)
+            k_wide_bwd_edge_ff<16, 3><<<grid, kFW * 32, 0, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);
         else
-            k_wide_bwd_edge_ff<32, 2><<<grid, kFW * 32, 0, s>>>(g, make_basis(g), a, MB, Hl, HB, GRAD, vir_part);
+            k_wide_bwd_edge_ff<32, 2><<<grid, kFW * 32, 0, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);
         GMD_LAUNCH_CHECK();
         return;
     }

@@ -94,20 +94,20 @@ def test_generic_rank_group_equals_single_handle(r3):
     assert seen.all()
 
 
-@pytest.mark.parametrize("variant", [{"GMD_WIDE_FF": "16"}, {"GMD_WIDE_TC": "1"}])
+@pytest.mark.parametrize("variant", ["sm8", "ff", "ff16", "tc"])
 def test_wide_backward_families_agree(monkeypatch, oracle_c, variant):
-    """F = 64 backward edge pass: the default packed-FP32 kernel (32-edge
-    chunks, transposed warp reduction) against its 16-edge-chunk form and the
-    tcgen05 form (G = X P, 3xTF32 in TMEM); all three are checked against the
+    """F = 64 backward edge pass: the default packed-FP32 kernel (partials in
+    shared memory) against its other forms (8 rows in flight; register
+    partials with a transposed butterfly over 32 / 16-edge chunks; G = X P on
+    tcgen05, 3xTF32 in TMEM); every form is checked against the
     oracle and keep exact Newton's third law (test_gpu_physics bound)."""
     s = S.liquid(1500)
     prm = G.ToyPotentialParams.init(9, 64, 8, 2, 5.0, 3.0)
     ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, 64, 8, 2, 5.0, 3.0)
-    for k in ("GMD_WIDE_FF", "GMD_WIDE_TC"):
+    for k in ("GMD_WIDE_BWD", "GMD_WIDE_TC"):
         monkeypatch.delenv(k, raising=False)
     a = run(s, prm)
-    for k, v in variant.items():
-        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("GMD_WIDE_BWD", variant)
     b = run(s, prm, 2)
     assert a.energy == b.energy  # the forward is shared
     fmax = np.abs(ref["forces"]).max()
