@@ -1019,19 +1019,27 @@ __global__ void __launch_bounds__(kConvWarps * 32) k_wide_tb_inject(GenModel g, 
 // stages <= 16 slot rows per step (X in tf32 hi / lo); one thread issues
 // the CTA's 24 MMAs; the row's owner lane then reads its 64 outputs
 constexpr int kTW = 8;           // warps per CTA
+constexpr int kZLd = 68;         // z row stride (floats) in the epilogue: conflict-free 16-byte stores
+static_assert(kSlots * kZLd * 4 <= 2 * kXSbo && 32 * kSlots * 4 <= 2 * kXSbo, "per-warp scratch");
 constexpr int kWBytes = 8 * kPSbo;  // 64 rows (N) x 64 K, dense (LBO 128, SBO 2048)
 
-struct TbSmem {
+struct TbSmem {  // two CTAs per SM: keep 2 x (sizeof + 1 KB) <= 228 KB
     unsigned char x_hi[kXBytes];
     unsigned char x_lo[kXBytes];
     unsigned char w_hi[kWBytes];
     unsigned char w_lo[kWBytes];
     int slot_b[kTW][kSlots];    // bond row of each slot
-    float4 sq[kTW][32];         // bond vectors of the current center (first 32)
+    union {
+        float4 sq[kTW][32];         // forward: bond vectors of the current center (first 32)
+        float4 du[kTW][kSlots][2];  // back1: du3_k of the step's slots
+    };
+    float2 fcd[kTW][kSlots];        // back1: (fc3, fc3') of the step's slots
     int steps_w[kTW];
     uint64_t mbar;
     uint32_t tbase;
 };
+
+static_assert(2 * (sizeof(TbSmem) + 1024) <= 228 * 1024, "three-body kernels: two CTAs per SM");
 
 // B operand: B[n][k] = Wsrc[n * ldn + k * ldk] (tf32 hi / lo)
 __device__ __forceinline__ void stage_w(TbSmem& S, const float* Wsrc, int ldn, int ldk) {
@@ -1148,35 +1156,53 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Bas
             __syncwarp();
         }
         // slots jpos .. jpos + ns - 1 of this center; o outer so each t_o row
-        // is read once per step, m3 of the step's slots in registers
+        // is read once per step, m3 of the step's slots in registers.  The
+        // warp's own A-operand rows are free here (the previous MMA has
+        // completed): they hold the step's cosine table C[o][i] (x_hi) and
+        // the epilogue's z rows (x_lo)
         const int ns = jpos < nb ? min(kSlots, nb - jpos) : 0;
         auto qof = [&](int o) { return o < 32 ? S.sq[wq][o] : a.vd[a.bedge[b0 + o]]; };
-        float4 qmine = make_float4(0.f, 0.f, 0.f, 1.f);  // lane i < ns: slot i's bond vector
-        if (lane < ns) qmine = qof(jpos + lane);
+        float* Cm = reinterpret_cast<float*>(S.x_hi + (row0 >> 3) * kXSbo);  // [32][16]
+        float* Zs = reinterpret_cast<float*>(S.x_lo + (row0 >> 3) * kXSbo);  // [16][kZLd]
         float2 m3[kSlots];
 #pragma unroll
         for (int i = 0; i < kSlots; ++i) m3[i] = make_float2(0.f, 0.f);
-        for (int o0 = 0; o0 < nb && ns > 0; o0 += 4) {
-            float2 tv[4];
+        for (int oc = 0; oc < nb && ns > 0; oc += 32) {
+            const int no = min(32, nb - oc);
+            __syncwarp();
+            // c(o, j) = v_o . v_j / (d_o d_j); 0 for o == j and unused slots
+            for (int t = lane; t < no * kSlots; t += 32) {
+                const int o = oc + (t >> 4), i = t & (kSlots - 1);
+                float c = 0.f;
+                if (i < ns && jpos + i != o) {
+                    const float4 qo = qof(o), qj = qof(jpos + i);
+                    c = (qo.x * qj.x + qo.y * qj.y + qo.z * qj.z) / (qo.w * qj.w);
+                }
+                Cm[t] = c;
+            }
+            __syncwarp();
+            for (int o0 = 0; o0 < no; o0 += 4) {
+                float2 tv[4];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj)  // four t rows in flight
-                if (o0 + jj < nb) tv[jj] = __ldg(reinterpret_cast<const float2*>(TT + (size_t)(b0 + o0 + jj) * F) + lane);
+                for (int jj = 0; jj < 4; ++jj)  // four t rows in flight
+                    if (o0 + jj < no)
+                        tv[jj] = __ldg(reinterpret_cast<const float2*>(TT + (size_t)(b0 + oc + o0 + jj) * F) + lane);
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int o = o0 + jj;
-                if (o >= nb) break;
-                const float4 qo = qof(o);
-                // c(o, j) = v_o . v_j / (d_o d_j), lane i for slot i (0 for o == j)
-                const float cm = (lane < ns && jpos + lane != o)
-                                     ? (qo.x * qmine.x + qo.y * qmine.y + qo.z * qmine.z) / (qo.w * qmine.w)
-                                     : 0.f;
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (o0 + jj >= no) break;
+                    const float4* cr = reinterpret_cast<const float4*>(Cm + (o0 + jj) * kSlots);
 #pragma unroll
-                for (int i = 0; i < kSlots; ++i) {
-                    const float ci = __shfl_sync(kFull, cm, i);
-                    if (i < ns && jpos + i != o) m3[i] = f2fma(bc2(ci), tv[jj], m3[i]);  // ascending o
+                    for (int i4 = 0; i4 < kSlots / 4; ++i4) {  // ascending o; + 0 t_j on the diagonal
+                        const float4 c4 = cr[i4];
+                        m3[4 * i4] = f2fma(bc2(c4.x), tv[jj], m3[4 * i4]);
+                        m3[4 * i4 + 1] = f2fma(bc2(c4.y), tv[jj], m3[4 * i4 + 1]);
+                        m3[4 * i4 + 2] = f2fma(bc2(c4.z), tv[jj], m3[4 * i4 + 2]);
+                        m3[4 * i4 + 3] = f2fma(bc2(c4.w), tv[jj], m3[4 * i4 + 3]);
+                    }
                 }
             }
         }
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < kSlots; ++i)
             if (i < ns) stage_row(S, row0 + i, lane, m3[i]);
@@ -1184,25 +1210,32 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Bas
         jpos += ns;
         __syncwarp();
         tb_mma(S, tmem, phase);
-        float z[F];
-        tmem_row64(trow, z);
-        if (owner && oslot < ns) {
-            const int b = S.slot_b[wq][oslot];
-            const float d = a.vd[a.bedge[b]].w;
-            float fc, dfc;
-            fcut3w(b3, d, fc, dfc);
-            const float4* tt = reinterpret_cast<const float4*>(TT + (size_t)b * F);
-            float4* tp = reinterpret_cast<float4*>(TP + (size_t)b * F);
-            float4* t3 = reinterpret_cast<float4*>(TH3 + (size_t)b * F);
+        {   // z rows (TMEM lane = slot) -> shared memory -> feature lanes
+            float z[F];
+            tmem_row64(trow, z);
+            if (owner && oslot < ns) {
+                float4* zr = reinterpret_cast<float4*>(Zs + oslot * kZLd);
 #pragma unroll
-            for (int c4 = 0; c4 < F / 4; ++c4) {
-                const float4 t = tt[c4];
-                const float4 th = make_float4(tanhf(z[4 * c4]), tanhf(z[4 * c4 + 1]), tanhf(z[4 * c4 + 2]),
-                                              tanhf(z[4 * c4 + 3]));
-                t3[c4] = th;
-                tp[c4] = make_float4(t.x + fc * th.x, t.y + fc * th.y, t.z + fc * th.z, t.w + fc * th.w);
+                for (int c4 = 0; c4 < F / 4; ++c4)
+                    zr[c4] = make_float4(z[4 * c4], z[4 * c4 + 1], z[4 * c4 + 2], z[4 * c4 + 3]);
             }
         }
+        float fcm = 0.f;
+        if (lane < ns) {
+            float dfc;
+            fcut3w(b3, a.vd[a.bedge[S.slot_b[wq][lane]]].w, fcm, dfc);
+        }
+        __syncwarp();
+        for (int i = 0; i < ns; ++i) {
+            const int b = S.slot_b[wq][i];
+            const float fc = __shfl_sync(kFull, fcm, i);
+            const float2 zz = *reinterpret_cast<const float2*>(Zs + i * kZLd + 2 * lane);
+            const float2 th = make_float2(tanhf(zz.x), tanhf(zz.y));
+            const float2 t = __ldg(reinterpret_cast<const float2*>(TT + (size_t)b * F) + lane);
+            reinterpret_cast<float2*>(TH3 + (size_t)b * F)[lane] = th;
+            reinterpret_cast<float2*>(TP + (size_t)b * F)[lane] = make_float2(t.x + fc * th.x, t.y + fc * th.y);
+        }
+        __syncwarp();
     }
     tc::fence_before();
     __syncthreads();
@@ -1279,6 +1312,7 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
             ns += take;
             jpos += take;
         }
+        // lane i: slot i's bond, its radial scalars into shared memory
         float4 qm = make_float4(0.f, 0.f, 0.f, 1.f);
         int rxm = 0;
         if (myb >= 0) {
@@ -1286,41 +1320,58 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
             qm = a.vd[e];
             const int x = a.esrc[e];
             rxm = a.crow ? a.crow[x] : x;
+            float fc, dfc, du[K];
+            fcut3w(b3, qm.w, fc, dfc);
+            u3w(b3, qm.w, du, true);
+            S.du[wq][lane][0] = make_float4(du[0], du[1], du[2], du[3]);
+            S.du[wq][lane][1] = make_float4(du[4], du[5], du[6], du[7]);
+            S.fcd[wq][lane] = make_float2(fc, dfc);
+            S.slot_b[wq][lane] = myb;
         }
-        for (int i0 = 0; i0 < ns; i0 += 4) {
-            float2 tpb[4], th[4];
+        __syncwarp();
+        // feature lanes: y rows (A operand) and this lane's share of
+        // dbf + da per slot; one transposed reduction for the 16 slots
+        float part[kSlots];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {  // four slots' rows in flight
-                const int i = i0 + jj;
-                const int rx = __shfl_sync(kFull, rxm, i & 31), b = __shfl_sync(kFull, myb, i & 31);
-                if (i < ns) {
-                    tpb[jj] = __ldg(reinterpret_cast<const float2*>(QB + (size_t)rx * F) + lane);
-                    th[jj] = reinterpret_cast<const float2*>(TH3 + (size_t)b * F)[lane];
+        for (int i0 = 0; i0 < kSlots; i0 += 4) {
+            if (i0 < ns) {
+                float2 tpb[4], th[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {  // four slots' rows in flight
+                    const int i = i0 + jj;
+                    const int rx = __shfl_sync(kFull, rxm, i), b = __shfl_sync(kFull, myb, i);
+                    if (i < ns) {
+                        tpb[jj] = __ldg(reinterpret_cast<const float2*>(QB + (size_t)rx * F) + lane);
+                        th[jj] = reinterpret_cast<const float2*>(TH3 + (size_t)b * F)[lane];
+                    }
                 }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int i = i0 + jj;
+                    part[i] = 0.f;
+                    if (i < ns) {
+                        const float4 d0 = S.du[wq][i][0], d1 = S.du[wq][i][1];
+                        const float du[K] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+                        const float2 fcd = S.fcd[wq][i];
+                        const float2 ds = p3dot(P32, du);
+                        const float dbf = fmaf(tpb[jj].x * th[jj].x, fcd.y, (tpb[jj].y * th[jj].y) * fcd.y);
+                        const float da = fmaf(tpb[jj].x, ds.x, tpb[jj].y * ds.y);
+                        part[i] = dbf + da;
+                        const float2 y = make_float2(tpb[jj].x * fcd.x * (1.0f - th[jj].x * th[jj].x),
+                                                     tpb[jj].y * fcd.x * (1.0f - th[jj].y * th[jj].y));
+                        stage_row(S, row0 + i, lane, y);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) part[i0 + jj] = 0.f;
             }
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int i = i0 + jj;
-                const float qx = __shfl_sync(kFull, qm.x, i & 31), qy = __shfl_sync(kFull, qm.y, i & 31),
-                            qz = __shfl_sync(kFull, qm.z, i & 31), qw = __shfl_sync(kFull, qm.w, i & 31);
-                const int b = __shfl_sync(kFull, myb, i & 31);
-                if (i >= ns) continue;
-                float fc, dfc, du[K];
-                fcut3w(b3, qw, fc, dfc);
-                u3l(b3, qw, lane, du, true);
-                const float2 ds = p3dot(P32, du);
-                float dbf = fmaf(tpb[jj].x * th[jj].x, dfc, (tpb[jj].y * th[jj].y) * dfc);
-                float da = fmaf(tpb[jj].x, ds.x, tpb[jj].y * ds.y);
-                dbf = gwarp_sum(dbf);
-                da = gwarp_sum(da);
-                const float2 y = make_float2(tpb[jj].x * fc * (1.0f - th[jj].x * th[jj].x),
-                                             tpb[jj].y * fc * (1.0f - th[jj].y * th[jj].y));
-                stage_row(S, row0 + i, lane, y);
-                if (lane == 0) {
-                    S.slot_b[wq][i] = b;
-                    const float c0 = -(dbf + da) / qw;
-                    VOUT[b] = make_float4(qx * c0, qy * c0, qz * c0, 0.f);
-                }
+        }
+        {
+            const float tot = transpose_reduce<kSlots>(part, lane);  // lanes i, i + 16: slot i
+            if (myb >= 0) {
+                const float c0 = -tot / qm.w;
+                VOUT[myb] = make_float4(qm.x * c0, qm.y * c0, qm.z * c0, 0.f);
             }
         }
         __syncwarp();

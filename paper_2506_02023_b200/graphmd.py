@@ -907,6 +907,73 @@ def forward_distributed(dist: Distributed, params: ToyPotentialParams,
     return PotentialOutput(e.value, pa, fo, st.reshape(3, 3))
 
 
+def forward_serial(system: AtomicSystem, params: ToyPotentialParams, device: int = 0) -> PotentialOutput:
+    """forward_serial (potential.cpp:563): one partition, one worker."""
+    r3 = params.r_3body if params.threebody() else None
+    d = Distributed.create_distributed(system, params.r_atom, r3, 1, 1, True, device=device)
+    return forward_distributed(d, params)
+
+
+def ensure_periodic(system: AtomicSystem, cutoff: float, device: int = 0) -> AtomicSystem:
+    """ensure_periodic (system.cpp:242-270) on the device: non-periodic axes
+    padded to extent + 2 cutoff, positions shifted by cutoff - lo."""
+    h = _Handle(device)
+    n = system.size()
+    out_pos = np.zeros((n, 3))
+    out_lat = np.zeros((3, 3))
+    pbc = np.array([1 if b else 0 for b in system.pbc], np.uint8)
+    h.check(lib().gmd_util_ensure_periodic(h.h, n, _p(system.positions), _p(system.lattice), _p(pbc),
+                                           cutoff, _p(out_pos), _p(out_lat)))
+    return AtomicSystem(out_pos, out_lat, system.species.copy(), (True, True, True))
+
+
+def finite_difference_forces(system: AtomicSystem, params: ToyPotentialParams, eps: float,
+                             device: int = 0) -> np.ndarray:
+    """finite_difference_forces (potential.cpp:991-1009): central differences
+    of the GPU energy.  The energy sums fp32-computed per-atom terms, so the
+    quotient carries ~1e-6 eV / (2 eps) of rounding noise (an fp32-level
+    check, not the reference's fp64 1e-6 eV/A)."""
+    if eps < 1e-6 or eps > 1e-2:
+        raise Error("finite-difference step must lie in [1e-6, 1e-2] A")
+    out = np.zeros((system.size(), 3))
+    probe = AtomicSystem(system.positions.copy(), system.lattice, system.species, system.pbc)
+    for i in range(system.size()):
+        for k in range(3):
+            x0 = system.positions[i, k]
+            probe.positions[i, k] = x0 + eps
+            ep = forward_serial(probe, params, device).energy
+            probe.positions[i, k] = x0 - eps
+            em = forward_serial(probe, params, device).energy
+            probe.positions[i, k] = x0
+            out[i, k] = -(ep - em) / (2.0 * eps)
+    return out
+
+
+def finite_difference_stress(system: AtomicSystem, params: ToyPotentialParams, eps: float,
+                             device: int = 0) -> np.ndarray:
+    """finite_difference_stress (potential.cpp:1011-1037): symmetrised strain
+    derivative of the GPU energy over the volume."""
+    if not (0.0 < eps <= 1e-3):
+        raise Error("strain step must lie in (0, 1e-3]")
+    base = ensure_periodic(system, params.r_atom, device)
+    volume = abs(np.linalg.det(base.lattice))
+
+    def deform(a, b, strain):  # x_a += strain x_b for every position and lattice row
+        pos = base.positions.copy()
+        lat = base.lattice.copy()
+        pos[:, a] += strain * pos[:, b]
+        lat[:, a] += strain * lat[:, b]
+        return AtomicSystem(pos, lat, base.species, base.pbc)
+
+    raw = np.zeros((3, 3))
+    for a in range(3):
+        for b in range(3):
+            ep = forward_serial(deform(a, b, eps), params, device).energy
+            em = forward_serial(deform(a, b, -eps), params, device).energy
+            raw[a, b] = (ep - em) / (2.0 * eps * volume)
+    return 0.5 * (raw + raw.T)
+
+
 def build_neighbor_list(system: AtomicSystem, cutoff: float, n_threads: int = 0,
                         device: int = 0) -> AtomGraph:
     """build_neighbor_list (neighborlist.cpp:108-197) on the GPU."""
