@@ -83,7 +83,7 @@ def bytes_model(n, ne, nb, L, threebody, F=16):
 # profiler label (gmd_profile) -> CUDA kernel of the default path
 KERNEL_OF = {"bwd_edge": "k_bwd_edge2", "conv": "k_conv2", "nl_search": "k_nl_search",
              "nl_emit": "k_nl_emit", "bwd_node": "k_bwd_node"}
-KERNEL_OF_WIDE = {"bwd_edge": "k_wide_bwd_edge", "conv": "k_wide_conv", "bwd_node": "k_wide_bwd_node",
+KERNEL_OF_WIDE = {"bwd_edge": "k_wide_bwd_edge_sm", "conv": "k_wide_conv", "bwd_node": "k_wide_bwd_node",
                   "tb_forward": "k_wide_tb_forward", "tb_backward": "k_wide_tb_back2"}
 
 
