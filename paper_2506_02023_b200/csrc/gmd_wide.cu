@@ -1090,6 +1090,41 @@ __device__ __forceinline__ void tmem_row64(uint32_t trow, float z[F]) {
     tc::tmem_ld32(trow + 32, z + 32);
 }
 
+// The warp's centers k = gw + j nw (j < my) and their bond ranges, fetched
+// by the lanes 32 centers at a time: one dependent load chain (nodes ->
+// brow) per 32 centers instead of one per center.  j is warp-uniform.
+struct CenterMeta {
+    int b0 = 0, nb = 0;  // lane l: center jbase + l
+    int64_t jbase = -64;
+};
+__device__ __forceinline__ void center_bonds(const BondArgs& a, int64_t gw, int64_t nw, int64_t my, int lane,
+                                             CenterMeta& m, int64_t j, int& b0, int& nb) {
+    if (j < m.jbase || j >= m.jbase + 32) {
+        m.jbase = j;
+        const int64_t jj = j + lane;
+        m.b0 = 0;
+        m.nb = 0;
+        if (jj < my) {
+            const int64_t kk = gw + jj * nw;
+            const int64_t c = a.nodes ? (int64_t)a.nodes[kk] : kk;
+            m.b0 = a.brow[c];
+            m.nb = a.brow[c + 1] - m.b0;
+        }
+    }
+    b0 = __shfl_sync(kFull, m.b0, (int)(j - m.jbase));
+    nb = __shfl_sync(kFull, m.nb, (int)(j - m.jbase));
+}
+// first center at or after j with bonds (my if none)
+__device__ __forceinline__ int64_t next_center(const BondArgs& a, int64_t gw, int64_t nw, int64_t my, int lane,
+                                               CenterMeta& m, int64_t j, int& b0, int& nb) {
+    for (; j < my; ++j) {
+        center_bonds(a, gw, nw, my, lane, m, j, b0, nb);
+        if (nb > 0) return j;
+    }
+    b0 = nb = 0;
+    return my;
+}
+
 // CTA-wide step count: every step packs 16 slots of a warp's consecutive
 // centers, so a warp needs ceil(sum_centers n / 16) steps; max over warps
 // (packed = false: every step holds slots of one center, sum of ceil(n / 16))
@@ -1141,19 +1176,27 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Bas
     const int steps = tb_steps(a, gw, nw, my, lane, wq, S.steps_w, false);
 
     uint32_t phase = 0;
-    int64_t jn = 0;
-    int b0 = 0, nb = 0, jpos = 0;  // current center: bonds [b0, b0 + nb), next slot jpos
+    // current center: bonds [b0, b0 + nb), next slot jpos; the next center's
+    // bond edges (en) and vectors (qn) are fetched one step ahead
+    CenterMeta cmeta;
+    int b0 = 0, nb = 0, jpos = 0, b0n = 0, nbn = 0;
+    int64_t jcur = next_center(a, gw, nw, my, lane, cmeta, 0, b0, nb);
+    if (lane < min(nb, 32)) S.sq[wq][lane] = a.vd[a.bedge[b0 + lane]];
+    __syncwarp();
+    int64_t jnext = next_center(a, gw, nw, my, lane, cmeta, jcur + 1, b0n, nbn);
+    int en = lane < min(nbn, 32) ? __ldg(a.bedge + b0n + lane) : 0;
+    float4 qn = make_float4(0.f, 0.f, 0.f, 1.f);
     for (int step = 0; step < steps; ++step) {
-        while (jpos >= nb && jn < my) {  // next center with bonds
-            const int64_t kk = gw + jn * nw;
-            ++jn;
-            const int64_t s = a.nodes ? (int64_t)a.nodes[kk] : kk;
-            b0 = a.brow[s];
-            nb = a.brow[s + 1] - b0;
+        if (jpos >= nb && jcur < my) {  // advance to the prefetched center
+            __syncwarp();
+            if (lane < min(nbn, 32)) S.sq[wq][lane] = qn;
+            __syncwarp();
+            jcur = jnext;
+            b0 = b0n;
+            nb = nbn;
             jpos = 0;
-            __syncwarp();
-            for (int o = lane; o < nb && o < 32; o += 32) S.sq[wq][o] = a.vd[a.bedge[b0 + o]];
-            __syncwarp();
+            jnext = next_center(a, gw, nw, my, lane, cmeta, jcur + 1, b0n, nbn);
+            en = lane < min(nbn, 32) ? __ldg(a.bedge + b0n + lane) : 0;
         }
         // slots jpos .. jpos + ns - 1 of this center; o outer so each t_o row
         // is read once per step, m3 of the step's slots in registers.  The
@@ -1202,6 +1245,7 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_forward(GenModel g, Bas
                 }
             }
         }
+        if (lane < min(nbn, 32)) qn = __ldg(a.vd + en);  // next center's vectors (en has landed)
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < kSlots; ++i)
@@ -1290,36 +1334,46 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
     const int steps = tb_steps(a, gw, nw, my, lane, wq, S.steps_w);
 
     uint32_t phase = 0;
-    int64_t jn = 0;
+    // slot schedule (consecutive bonds of consecutive centers, 16 per step):
+    // lane i takes slot i's bond.  The next step's indices are fetched one
+    // step ahead in three stages (bond edge; vector and source atom; source
+    // row), each under the current step's work
+    CenterMeta cmeta;
+    int64_t jcur = -1;
     int b0 = 0, nb = 0, jpos = 0;
-    for (int step = 0; step < steps; ++step) {
-        // this step's slots (consecutive bonds of consecutive centers): lane i
-        // takes slot i's bond and loads its indices, all slots in parallel
-        int ns = 0, myb = -1;
-        while (ns < kSlots) {
+    auto schedule = [&](int& ns_o, int& myb_o) {
+        ns_o = 0;
+        myb_o = -1;
+        while (ns_o < kSlots) {
             if (jpos >= nb) {
-                if (jn >= my) break;
-                const int64_t kk = gw + jn * nw;
-                ++jn;
-                const int64_t s = a.nodes ? (int64_t)a.nodes[kk] : kk;
-                b0 = a.brow[s];
-                nb = a.brow[s + 1] - b0;
+                if (jcur >= my) break;
+                jcur = next_center(a, gw, nw, my, lane, cmeta, jcur + 1, b0, nb);
                 jpos = 0;
+                if (nb == 0) break;
                 continue;
             }
-            const int take = min(kSlots - ns, nb - jpos);
-            if (lane >= ns && lane < ns + take) myb = b0 + jpos + (lane - ns);
-            ns += take;
+            const int take = min(kSlots - ns_o, nb - jpos);
+            if (lane >= ns_o && lane < ns_o + take) myb_o = b0 + jpos + (lane - ns_o);
+            ns_o += take;
             jpos += take;
         }
+    };
+    int ns, myb;
+    schedule(ns, myb);
+    float4 qm = make_float4(0.f, 0.f, 0.f, 1.f);
+    int rxm = 0;
+    if (myb >= 0) {
+        const int e = a.bedge[myb];
+        qm = a.vd[e];
+        const int x = a.esrc[e];
+        rxm = a.crow ? a.crow[x] : x;
+    }
+    int nsn, mybn;
+    schedule(nsn, mybn);
+    int en = mybn >= 0 ? __ldg(a.bedge + mybn) : 0;
+    for (int step = 0; step < steps; ++step) {
         // lane i: slot i's bond, its radial scalars into shared memory
-        float4 qm = make_float4(0.f, 0.f, 0.f, 1.f);
-        int rxm = 0;
         if (myb >= 0) {
-            const int e = a.bedge[myb];
-            qm = a.vd[e];
-            const int x = a.esrc[e];
-            rxm = a.crow ? a.crow[x] : x;
             float fc, dfc, du[K];
             fcut3w(b3, qm.w, fc, dfc);
             u3w(b3, qm.w, du, true);
@@ -1367,6 +1421,13 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
                 for (int jj = 0; jj < 4; ++jj) part[i0 + jj] = 0.f;
             }
         }
+        // next step's vector and source atom (its bond edge has landed)
+        float4 qn = make_float4(0.f, 0.f, 0.f, 1.f);
+        int xn = 0;
+        if (mybn >= 0) {
+            qn = __ldg(a.vd + en);
+            xn = __ldg(a.esrc + en);
+        }
         {
             const float tot = transpose_reduce<kSlots>(part, lane);  // lanes i, i + 16: slot i
             if (myb >= 0) {
@@ -1383,6 +1444,13 @@ __global__ void __launch_bounds__(kTW * 32, 2) k_wide_tb_back1(GenModel g, Basis
             ep[0] = make_float4(ev[0], ev[1], ev[2], ev[3]);
             ep[1] = make_float4(ev[4], ev[5], ev[6], ev[7]);
         }
+        // rotate the pipeline: next step's source row, then the step after's bond edge
+        ns = nsn;
+        myb = mybn;
+        qm = qn;
+        rxm = mybn >= 0 ? (a.crow ? __ldg(a.crow + xn) : xn) : 0;
+        schedule(nsn, mybn);
+        en = mybn >= 0 ? __ldg(a.bedge + mybn) : 0;
     }
     tc::fence_before();
     __syncthreads();
