@@ -1887,6 +1887,16 @@ int gmd_set_params(gmd_handle* h, int F, int K, int L, double r_atom, double r3,
                 m.W4T[g * F + f] = m.W4[f * F + g];
             }
         }
+        {   // B3 = W3 P3 in fp64 from the blob (three-body backward, E = B3^T y)
+            const double* W3d = blob + 119 * F + (size_t)L * F * F + (size_t)L * F + (size_t)F * K + (size_t)F * K;
+            const double* P3d = blob + 119 * F + (size_t)L * F * F + (size_t)L * F + (size_t)F * K;
+            for (int f = 0; f < F; ++f)
+                for (int k = 0; k < K; ++k) {
+                    double acc = 0.0;
+                    for (int g = 0; g < F; ++g) acc += W3d[f * F + g] * P3d[g * K + k];
+                    m.B3[f * K + k] = (float)acc;
+                }
+        }
         for (int i = 0; i < F; ++i) m.ro[i] = (float)*q++;
         m.rc = (float)r_atom;
         m.inv_rc = (float)(1.0 / r_atom);

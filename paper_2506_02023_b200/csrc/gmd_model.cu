@@ -1232,7 +1232,7 @@ constexpr int kTbWarps = 4;
 // a 16-lane group per center: centers have ~11 in-bonds (C4: 11.3), so a
 // warp per center left two thirds of its lanes idle
 constexpr int kTbGroups = kTbWarps * 2;
-constexpr size_t kTbSlotBytes = 2 * sizeof(float) * kF + sizeof(float4);  // st + sm + sv
+constexpr size_t kTbSlotBytes = 6 * sizeof(float4) + sizeof(float4);  // backward: u3, u3', E (8 each) + v
 
 // The three-body contractions run on packed FP32 like the atom channel
 // (FFMA2 over feature pairs, constant pairs from uniform registers); each
@@ -1410,13 +1410,14 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
                                                                float4* __restrict__ VIN,
                                                                float4* __restrict__ VOUT,
                                                                double* vir_part, int kc) {
-    // per-group staging of kc >= max in-bonds slots: st/sm [slot][f], sv [slot]
+    // per-group staging of kc >= max in-bonds slots: bond vector, basis u3,
+    // its derivative u3' and E = P3^T m_bar_3 (8 floats each)
     extern __shared__ __align__(16) unsigned char tb_smem[];
     const int gl = threadIdx.x & 15, grp = threadIdx.x >> 4;
-    float(*st)[kF] = reinterpret_cast<float(*)[kF]>(tb_smem) + (size_t)grp * kc;
-    float(*sm)[kF] = reinterpret_cast<float(*)[kF]>(tb_smem) + (size_t)(kTbGroups + grp) * kc;
-    float4* sv = reinterpret_cast<float4*>(tb_smem + 2 * sizeof(float) * kF * kTbGroups * kc) +
-                 (size_t)grp * kc;
+    float4* sv = reinterpret_cast<float4*>(tb_smem) + (size_t)grp * kc;
+    float4* su = reinterpret_cast<float4*>(tb_smem) + (size_t)kTbGroups * kc + (size_t)grp * kc * 2;
+    float4* sdu = su + (size_t)kTbGroups * kc * 2;
+    float4* sE = sdu + (size_t)kTbGroups * kc * 2;
     const int64_t w0 = (int64_t)blockIdx.x * kTbGroups + grp;
     const int64_t nw = (int64_t)gridDim.x * kTbGroups;
     const int64_t iters = (a.n + nw - 1) / nw;  // same count for both groups of a warp
@@ -1434,10 +1435,12 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
             const int e = a.bedge[b0 + j];
             const float4 q = __ldg(a.vd + e);
             sv[j] = q;
-            float t[kF];
-            bond_t(q.w, t);
-#pragma unroll
-            for (int f = 0; f < kF; ++f) st[j][f] = t[f];
+            float u[kK], du[kK];
+            basis_d(q.w, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u, du);
+            su[2 * j] = make_float4(u[0], u[1], u[2], u[3]);
+            su[2 * j + 1] = make_float4(u[4], u[5], u[6], u[7]);
+            sdu[2 * j] = make_float4(du[0], du[1], du[2], du[3]);
+            sdu[2 * j + 1] = make_float4(du[4], du[5], du[6], du[7]);
             // stage 2: adjoints of the reverse bond e'_j
             float tpb[kF], th[kF], ds[kF];
             const int x = __ldg(a.esrc + e);
@@ -1445,7 +1448,7 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
             load_row16(TH3 + (size_t)(b0 + j) * kF, th);
             float fc, dfc;
             fcut3(q.w, fc, dfc);
-            bond_dt(q.w, ds);
+            fk_pairs(c_m.P3T, du, ds);  // ds = P3 u3'
             float dbf = 0.f, da = 0.f, y[kF];
 #pragma unroll
             for (int f = 0; f < kF; ++f) {
@@ -1453,22 +1456,36 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
                 da = fmaf(tpb[f], ds[f], da);
                 y[f] = tpb[f] * fc * (1.0f - th[f] * th[f]);
             }
-            float w3y[kF];
-            ff_pairs(c_m.W3, y, w3y);  // sum_f W3[f][g] y_f
+            // E = P3^T m_bar_3 = (W3 P3)^T y: phase 2 needs m_bar_3 only
+            // through m_bar_3 . t = E . u3 and m_bar_3 . ds = E . u3'
+            const float2* B2 = reinterpret_cast<const float2*>(c_m.B3);
+            float2 E2[kK / 2];
 #pragma unroll
-            for (int g = 0; g < kF; ++g) sm[j][g] = w3y[g];
+            for (int i = 0; i < kK / 2; ++i) E2[i] = f2mul(B2[i], bcast(y[0]));
+#pragma unroll
+            for (int f = 1; f < kF; ++f)
+#pragma unroll
+                for (int i = 0; i < kK / 2; ++i) E2[i] = f2fma(B2[f * (kK / 2) + i], bcast(y[f]), E2[i]);
+            sE[2 * j] = make_float4(E2[0].x, E2[0].y, E2[1].x, E2[1].y);
+            sE[2 * j + 1] = make_float4(E2[2].x, E2[2].y, E2[3].x, E2[3].y);
             const float c0 = -(dbf + da) / q.w;
             VOUT[b0 + j] = make_float4(q.x * c0, q.y * c0, q.z * c0, 0.f);
         }
         __syncwarp();
+        auto dot8 = [](float4 a0, float4 a1, float4 b0_, float4 b1_) {
+            float2 r = f2mul(make_float2(a0.x, a0.y), make_float2(b0_.x, b0_.y));
+            r = f2fma(make_float2(a0.z, a0.w), make_float2(b0_.z, b0_.w), r);
+            r = f2fma(make_float2(a1.x, a1.y), make_float2(b1_.x, b1_.y), r);
+            r = f2fma(make_float2(a1.z, a1.w), make_float2(b1_.z, b1_.w), r);
+            return r.x + r.y;
+        };
         for (int j = gl; j < k; j += 16) {
             const float4 qj = sv[j];
             const float idj = 1.0f / qj.w;
-            float2 tb2[kF / 2];
-#pragma unroll
-            for (int i = 0; i < kF / 2; ++i) tb2[i] = make_float2(0.f, 0.f);
-            const float2* stj = reinterpret_cast<const float2*>(st[j]);
-            const float2* smj = reinterpret_cast<const float2*>(sm[j]);
+            const float4 uj0 = su[2 * j], uj1 = su[2 * j + 1];
+            const float4 dj0 = sdu[2 * j], dj1 = sdu[2 * j + 1];
+            const float4 Ej0 = sE[2 * j], Ej1 = sE[2 * j + 1];
+            float db = 0.f;
             float vix = 0.f, viy = 0.f, viz = 0.f;  // as incoming bond e = e_j
             float4 vo = VOUT[b0 + j];                // as outgoing bond e' = e'_j
             for (int o = 0; o < k; ++o) {
@@ -1476,17 +1493,13 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
                 const float4 qo = sv[o];
                 const float ido = 1.0f / qo.w;
                 const float dotjo = qj.x * qo.x + qj.y * qo.y + qj.z * qo.z;
-                // (a) line edge (e_j, e'_o): c = v_j.v_o/(d_j d_o), a = v_j, b = -v_o
+                const float c = dotjo * idj * ido;
+                const float4 Eo0 = sE[2 * o], Eo1 = sE[2 * o + 1];
+                // (a) line edge (e_j, e'_o): c = v_j.v_o/(d_j d_o), a = v_j, b = -v_o;
+                //     t_bar_j += c m_bar_3,o (contracted with ds_j below)
                 {
-                    const float c = dotjo * idj * ido;
-                    const float2* smo = reinterpret_cast<const float2*>(sm[o]);
-                    float2 cb2 = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int i = 0; i < kF / 2; ++i) {
-                        tb2[i] = f2fma(bcast(c), smo[i], tb2[i]);
-                        cb2 = f2fma(smo[i], stj[i], cb2);
-                    }
-                    const float cb = cb2.x + cb2.y;
+                    const float cb = dot8(Eo0, Eo1, uj0, uj1);  // m_bar_3,o . t_j
+                    db = fmaf(c, dot8(Eo0, Eo1, dj0, dj1), db);  // c m_bar_3,o . ds_j
                     // dc/da = -(b^ + a^ c)/|a|
                     vix += -(-qo.x * ido + qj.x * idj * c) * idj * cb;
                     viy += -(-qo.y * ido + qj.y * idj * c) * idj * cb;
@@ -1494,25 +1507,12 @@ __global__ void __launch_bounds__(kTbWarps * 32, MINB) k_tb_backward(BondArgs a,
                 }
                 // (b) line edge (e_o, e'_j): a = v_o, b = -v_j
                 {
-                    const float c = dotjo * idj * ido;
-                    const float2* sto = reinterpret_cast<const float2*>(st[o]);
-                    float2 cb2 = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int i = 0; i < kF / 2; ++i) cb2 = f2fma(smj[i], sto[i], cb2);
-                    const float cb = cb2.x + cb2.y;
+                    const float cb = dot8(Ej0, Ej1, su[2 * o], su[2 * o + 1]);  // m_bar_3,j . t_o
                     // dc/db = -(a^ + b^ c)/|b|
                     vo.x += -(qo.x * ido - qj.x * idj * c) * idj * cb;
                     vo.y += -(qo.y * ido - qj.y * idj * c) * idj * cb;
                     vo.z += -(qo.z * ido - qj.z * idj * c) * idj * cb;
                 }
-            }
-            float ds[kF];
-            bond_dt(qj.w, ds);
-            float db = 0.f;
-#pragma unroll
-            for (int i = 0; i < kF / 2; ++i) {
-                db = fmaf(tb2[i].x, ds[2 * i], db);
-                db = fmaf(tb2[i].y, ds[2 * i + 1], db);
             }
             vix += qj.x * db * idj;
             viy += qj.y * db * idj;

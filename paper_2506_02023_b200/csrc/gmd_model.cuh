@@ -24,6 +24,7 @@ struct ModelConst {
     alignas(16) float W3T[kF * kF];  // W3T[g][f] = W3[f][g]
     alignas(16) float W4[kF * kF];
     alignas(16) float W4T[kF * kF];
+    alignas(16) float B3[kF * kK];   // (W3 P3)[f][k], fp64 product rounded once: E = B3^T y
     float ro[kF];
     float rc, inv_rc, inv_sigma, mu_step;     // atom radial basis
     float a2, pi_rc;                          // sqrt(log2 e)/sigma, pi/rc
