@@ -35,11 +35,18 @@ __device__ __forceinline__ int find_group(const SelState& st, unsigned long long
     return -1;
 }
 
-__global__ void k_sel_hist(const unsigned long long* __restrict__ keys, int64_t n,
-                           const SelState* __restrict__ stp, unsigned int* __restrict__ hist,
-                           int shift) {
+// One radix pass as one launch: every CTA histograms its keys (shared-memory
+// privatized), and the last CTA to finish (atomic ticket) performs the
+// update -- per rank, a warp prefix-scans the 256 digit counts to find the
+// digit holding the rank -- then clears the histogram and regroups the
+// ranks by prefix.  One launch per pass
+// and no serial 256-step scan per pass (the two-launch form cost 0.24 ms
+// per build at C5, 8 x (hist 10 us + update 19 us)).
+__global__ void k_sel_pass(const unsigned long long* __restrict__ keys, int64_t n, SelState* stp,
+                           unsigned int* hist, unsigned int* ticket, int shift, double* out, int last) {
     __shared__ SelState st;
     __shared__ unsigned int sh[kSelSmemGroups * 256];
+    __shared__ bool am_last;
     for (int k = threadIdx.x; k < (int)(sizeof(SelState) / 4); k += blockDim.x)
         reinterpret_cast<int*>(&st)[k] = reinterpret_cast<const int*>(stp)[k];
     __syncthreads();
@@ -50,10 +57,10 @@ __global__ void k_sel_hist(const unsigned long long* __restrict__ keys, int64_t 
     const unsigned long long mask_hi = shift >= 56 ? 0ull : ~((1ull << (shift + 8)) - 1ull);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long key = keys[i];
-        int g = find_group(st, key & mask_hi);
+        const unsigned long long key = keys[i];
+        const int g = find_group(st, key & mask_hi);
         if (g < 0) continue;
-        int slot = g * 256 + (int)((key >> shift) & 255ull);
+        const int slot = g * 256 + (int)((key >> shift) & 255ull);
         if (use_sm)
             atomicAdd(&sh[slot], 1u);
         else
@@ -64,36 +71,65 @@ __global__ void k_sel_hist(const unsigned long long* __restrict__ keys, int64_t 
         for (int k = threadIdx.x; k < st.ng * 256; k += blockDim.x)
             if (sh[k]) atomicAdd(&hist[k], sh[k]);
     }
-}
-
-__global__ void k_sel_update(SelState* st, unsigned int* hist, int shift, double* out, int last) {
-    const int k = threadIdx.x;
-    const int ng_old = st->ng;
-    if (k < st->nr) {
-        const unsigned int* h = hist + st->gmap[k] * 256;
-        long long cum = 0;
-        int digit = 255;
-        for (int d = 0; d < 256; ++d) {
-            if (cum + (long long)h[d] > st->rem[k]) {
-                digit = d;
-                break;
-            }
-            cum += h[d];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) am_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int k = warp; k < st.nr; k += nwarp) {
+        const unsigned int* h = hist + st.gmap[k] * 256;
+        unsigned int c[8];
+        long long mine = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            c[i] = __ldcg(h + 8 * lane + i);
+            mine += c[i];
         }
-        st->prefix[k] |= (unsigned long long)digit << shift;
-        st->rem[k] -= cum;
+        long long incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        const long long rem = st.rem[k], excl = incl - mine;
+        const long long total = __shfl_sync(0xffffffffu, incl, 31);
+        // first digit d with cum(d) + h[d] > rem (else 255, cum = total)
+        const unsigned owner = __ballot_sync(0xffffffffu, excl <= rem && rem < incl);
+        if (owner == 0u) {
+            if (lane == 0) {
+                stp->prefix[k] = st.prefix[k] | (255ull << shift);
+                stp->rem[k] = rem - total;
+            }
+        } else if (lane == __ffs(owner) - 1) {
+            long long cum = excl;
+            int digit = 8 * lane + 7;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (cum + (long long)c[i] > rem) {
+                    digit = 8 * lane + i;
+                    break;
+                } else {
+                    cum += c[i];
+                }
+            stp->prefix[k] = st.prefix[k] | ((unsigned long long)digit << shift);
+            stp->rem[k] = rem - cum;
+        }
     }
     __syncthreads();
-    for (int i = k; i < ng_old * 256; i += blockDim.x) hist[i] = 0;
-    if (k == 0) {
+    for (int i = threadIdx.x; i < st.ng * 256; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) {
+        *ticket = 0u;
         int ng = 0;
-        for (int r = 0; r < st->nr; ++r) {
-            if (ng == 0 || st->ugroup[ng - 1] != st->prefix[r]) st->ugroup[ng++] = st->prefix[r];
-            st->gmap[r] = ng - 1;
+        for (int r = 0; r < st.nr; ++r) {
+            const unsigned long long pr = stp->prefix[r];
+            if (ng == 0 || stp->ugroup[ng - 1] != pr) stp->ugroup[ng++] = pr;
+            stp->gmap[r] = ng - 1;
+            if (last) out[r] = __longlong_as_double((long long)pr);
         }
-        st->ng = ng;
+        stp->ng = ng;
     }
-    if (last && k < st->nr) out[k] = __longlong_as_double((long long)st->prefix[k]);
 }
 
 // ---------------------------------------------------------------------------
@@ -375,11 +411,12 @@ void launch_select(const double* keys, int64_t n, const int64_t* ranks_host, int
     GMD_CUDA(cudaMemsetAsync(hist, 0, (size_t)kSelMaxRanks * 256 * 4, s));
     const auto* k64 = reinterpret_cast<const unsigned long long*>(keys);
     int grid = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (n + 255) / 256));
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(hist) +
+                                                           (size_t)kSelMaxRanks * 256 * 4);
+    GMD_CUDA(cudaMemsetAsync(ticket, 0, 4, s));
     for (int pass = 0; pass < 8; ++pass) {
-        int shift = 56 - 8 * pass;
-        k_sel_hist<<<grid, 256, 0, s>>>(k64, n, dst, hist, shift);
-        GMD_LAUNCH_CHECK();
-        k_sel_update<<<1, 128, 0, s>>>(dst, hist, shift, out_dev, pass == 7 ? 1 : 0);
+        const int shift = 56 - 8 * pass;
+        k_sel_pass<<<grid, 256, 0, s>>>(k64, n, dst, hist, ticket, shift, out_dev, pass == 7 ? 1 : 0);
         GMD_LAUNCH_CHECK();
     }
 }
