@@ -878,7 +878,13 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     gd.vd = h->vd.get<float4>(h->ne);
     gd.d = h->ed.get<float>(h->ne);
     gd.bond = r3 > 0.0 ? h->ebond.get<uint8_t>(h->ne) : nullptr;  // three-body bonds only
-    { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s); }
+    // p > 1 in one process: the requirement masks are OR-ed in by the emit
+    unsigned long long* req_emit = nullptr;
+    if (p > 1 && !rank_mode) {
+        req_emit = A.req.get<unsigned long long>(n);
+        GMD_CUDA(cudaMemsetAsync(req_emit, 0, sizeof(unsigned long long) * n, s));
+    }
+    { PROF("nl_emit"); launch_nl_emit(g, n, cap, h->slab.as<unsigned long long>(), b, gd, s, ownp, req_emit); }
 
     // ---- requirement masks, span layouts, local edge ends (partitioner.cpp:110-218)
     h->n_own = n;
@@ -893,14 +899,11 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         A.h_nodes.clear();
     } else {
         auto* reqp = A.req.get<unsigned long long>(n);
-        GMD_CUDA(cudaMemsetAsync(reqp, 0, sizeof(unsigned long long) * n, s));
         if (rank_mode) {
+            GMD_CUDA(cudaMemsetAsync(reqp, 0, sizeof(unsigned long long) * n, s));
             PROF("part_required");
             launch_required_rank(rowp, gd.src, n, ownp, myrank, reqp, s);
-        } else {
-            PROF("part_required");
-            launch_required(rowp, gd.src, n, ownp, reqp, s);
-        }
+        }  // else: written by the emit
         build_layout(h, A, ownp, reqp, n, p, myrank);
         {
             PROF("part_edge_lsrc");

@@ -444,7 +444,8 @@ __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, 
                           const int32_t* __restrict__ cell, int32_t* __restrict__ e_src,
                           uint32_t* __restrict__ e_img, float4* __restrict__ e_vd,
                           float* __restrict__ e_d, uint8_t* __restrict__ e_bond,
-                          int32_t* __restrict__ bcnt, int32_t* __restrict__ flags) {
+                          int32_t* __restrict__ bcnt, int32_t* __restrict__ flags,
+                          const int32_t* __restrict__ owner, unsigned long long* __restrict__ req) {
     const int64_t i0 = (int64_t)blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
     const bool live = i0 < n;
     const int64_t i = live ? i0 : 0;
@@ -485,6 +486,12 @@ __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, 
             e_d[e] = (float)dd;
             isb = g.bond_bound >= 0.0 && !(dd > g.bond_bound);
             if (e_bond) e_bond[e] = isb ? 1 : 0;
+            // p > 1 in one process: requirement masks (partitioner.cpp:124-134,
+            // the same atomicOr set as k_required) from the edges emitted here
+            if (req) {
+                const int oi = owner[i], oj = owner[j];
+                if (oj != oi) atomicOr(&req[j], 1ull << oi);
+            }
         }
         nb += __popc(__ballot_sync(0xffffffffu, isb) & gmask);
     }
@@ -687,7 +694,8 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, flo
 }
 
 void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long* slab,
-                    NLBuffers& b, GraphDev& gd, cudaStream_t s) {
+                    NLBuffers& b, GraphDev& gd, cudaStream_t s, const int32_t* owner,
+                    unsigned long long* req) {
     if (n == 0) return;
     // 16 lanes per row: ~45-edge rows fill 3 x 16 slots (94 %) instead of
     // 2 x 32 (70 %); C5 0.70 -> 0.53 ms
@@ -695,7 +703,7 @@ void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long*
     // 12 CTAs per SM (40 registers): 0.480 -> 0.472 ms at C5 (16 CTAs / 32
     // registers spill: 0.595 ms)
     k_nl_emit<16, 12><<<div_up(n, 8), 128, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src,
-                                               gd.img, gd.vd, gd.d, gd.bond, b.bcnt, b.flags);
+                                               gd.img, gd.vd, gd.d, gd.bond, b.bcnt, b.flags, owner, req);
     GMD_LAUNCH_CHECK();
 }
 

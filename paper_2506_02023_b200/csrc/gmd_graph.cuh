@@ -65,8 +65,11 @@ void launch_nl_search(const Geom& g, float thr32, float acc32, float zero32, flo
                       NLBuffers& b, unsigned long long* slab, const int32_t* owner, int only,
                       cudaStream_t s);
 // emit: slab rows -> CSR (row must hold the scanned degrees)
+// owner / req (optional): requirement masks of p > 1 partitions in one
+// process, OR-ed in from the emitted edges (replaces launch_required)
 void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long* slab,
-                    NLBuffers& b, GraphDev& gd, cudaStream_t s);
+                    NLBuffers& b, GraphDev& gd, cudaStream_t s, const int32_t* owner = nullptr,
+                    unsigned long long* req = nullptr);
 void launch_minmax_proj(const double* pos, int64_t n, const double dir[3], double* out2,
                         cudaStream_t s);
 void launch_shift(double* pos, int64_t n, const double add[3], cudaStream_t s);

@@ -356,11 +356,12 @@ __global__ void k_edge_lsrc(const int32_t* __restrict__ row, const int32_t* __re
                             const int32_t* __restrict__ crow, const int32_t* __restrict__ node_array,
                             const int32_t* __restrict__ list_off, int p,
                             int32_t* __restrict__ lsrc, int32_t* __restrict__ flags) {
-    int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    // 16 lanes per row (~45-edge rows fill 3 x 16 slots instead of 2 x 32)
+    int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4);
     if (v >= n) return;
     const int i = owner[v];
     const int stride = 1 + 2 * p;
-    for (int e = row[v] + (threadIdx.x & 31); e < row[v + 1]; e += 32) {
+    for (int e = row[v] + (threadIdx.x & 15); e < row[v + 1]; e += 16) {
         int u = src[e];
         int ou = owner[u];
         int r;
@@ -517,7 +518,7 @@ void launch_from_src(const int32_t* node_array, const int32_t* crow, const int32
 void launch_edge_lsrc(const int32_t* row, const int32_t* src, int64_t n, const int32_t* owner,
                       const int32_t* crow, const int32_t* node_array, const int32_t* list_off,
                       int p, int32_t* lsrc, int32_t* flags, cudaStream_t s) {
-    k_edge_lsrc<<<div_up(n, 8), 256, 0, s>>>(row, src, n, owner, crow, node_array, list_off, p,
+    k_edge_lsrc<<<div_up(n, 16), 256, 0, s>>>(row, src, n, owner, crow, node_array, list_off, p,
                                              lsrc, flags);
     GMD_LAUNCH_CHECK();
 }
