@@ -167,3 +167,29 @@ def test_far_pairs_at_cutoff(oracle_c, shift):
     pos = np.array(pos) + shift * lat[0] - (shift // 3) * lat[2]
     s = G.AtomicSystem(pos, lat, np.ones(len(pos), np.int32))
     assert_same_graph(gpu_graph(s, rc), oracle_c.neighbor_list(*S.as_args(s), rc))
+
+
+def test_slab_capacity_retry_and_growth(oracle_c):
+    """The search writes each destination's keys into a fixed-capacity slab
+    row sized from a density estimate (first build) or the previous build's
+    maximum degree; a row that overflows is detected and the search reruns
+    with the exact capacity (gmd_api.cu build_impl).  A dense blob in a dilute
+    gas overflows the first estimate; a denser blob on the same handle then
+    overflows the carried capacity.  Both graphs are bit-exact."""
+    rng = np.random.default_rng(3)
+    box = 60.0
+    gas = rng.uniform(0, box, (1500, 3))
+
+    def with_blob(k, radius):
+        blob = 30.0 + rng.normal(0, radius, (k, 3))
+        pos = np.concatenate([gas, blob])
+        return G.AtomicSystem(pos, np.eye(3) * box, np.full(len(pos), 8, np.int32))
+
+    h = G._Handle(0)
+    for s in (with_blob(150, 1.2), with_blob(400, 1.0)):
+        d = G.Distributed.create_distributed(s, 4.0, None, 1, 1, True, handle=h)
+        g = d.graph()
+        o = oracle_c.neighbor_list(*S.as_args(s), 4.0)
+        assert_same_graph(g, o)
+        deg = np.bincount(g.dst, minlength=s.size())
+        assert deg.max() > 4 * deg.mean()  # well above the density estimate
