@@ -244,6 +244,61 @@ __device__ __forceinline__ float transpose_reduce16_g16(float v[kF], int gl) {
     return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
+// Shared-memory transpose of a 16-lane group's per-lane partial sums: lane gl
+// stores its values as one row (STS.128), then sums column gl over the 16 rows
+// in the shuffle butterfly's pairwise order (the node's result does not depend on where it
+// runs).  ~35 instructions per group for 16 features instead of the 60 of the
+// shuffle butterfly (15 SHFL, 15 FADD, 30 FSEL).  Row stride S floats: S a
+// multiple of 4 with S/4 odd keeps every 8-lane LDS.128/STS.128 phase on
+// distinct bank quads; the 16-float gap between the two groups of a warp puts
+// their column reads on opposite bank halves.
+template <int S>
+struct GroupT {
+    static constexpr int kGroup = 16 * S + 16;  // floats per group
+};
+template <int S>
+__device__ __forceinline__ float column_sum16(const float* sT, int col) {
+    float r[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = sT[j * S + col];
+    // the xor-butterfly's tree (pairs l, l^8 first): bitwise the shuffle
+    // reduction, which is invariant under reversing a row of <= 8 edges
+    // (the reference's permutation-equivariance test, test_potential.cpp:146)
+#pragma unroll
+    for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) r[j] += r[j + w];
+    return r[0];
+}
+
+// Conv node update from the group's per-lane partial sums: m_gl (column sum),
+// z_gl = b_gl + sum_g W[gl][g] m_g with m broadcast from shared memory and W
+// rows read as float4 (sW row stride 20).  Used by both conv kernel families
+// (bitwise-equal energies).
+constexpr int kConvTS = 20;
+__device__ __forceinline__ float conv_node_z(const float acc[kF], int gl, float* sT, float* sM,
+                                             const float* sW, float b) {
+    float4* row = reinterpret_cast<float4*>(sT + gl * kConvTS);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        row[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+    __syncwarp();
+    sM[gl] = column_sum16<kConvTS>(sT, gl);
+    __syncwarp();
+    const float4* mv = reinterpret_cast<const float4*>(sM);
+    const float4* wr = reinterpret_cast<const float4*>(sW + gl * kConvTS);
+    float z = b;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float4 m4 = mv[c], w4 = wr[c];
+        z = fmaf(w4.x, m4.x, z);
+        z = fmaf(w4.y, m4.y, z);
+        z = fmaf(w4.z, m4.z, z);
+        z = fmaf(w4.w, m4.w, z);
+    }
+    return z;
+}
+
 __device__ __forceinline__ float group_sum16(float v) {
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -302,9 +357,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
                                                       float* __restrict__ Hout,
                                                       float* __restrict__ TH, double* per_atom,
                                                       double* e_part) {
-    __shared__ float sW[kF][kF + 1];
+    __shared__ __align__(16) float sW[kF * kConvTS];
+    __shared__ __align__(16) float sT[kNodesPerCta * GroupT<kConvTS>::kGroup];
+    __shared__ __align__(16) float sM[kNodesPerCta][kF];
     __shared__ float sb[kF], sro[kF];
-    for (int i = threadIdx.x; i < kF * kF; i += kThreads) sW[i / kF][i % kF] = c_m.W[layer][i];
+    for (int i = threadIdx.x; i < kF * kF; i += kThreads) sW[(i / kF) * kConvTS + i % kF] = c_m.W[layer][i];
     if (threadIdx.x < kF) {
         sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
         sro[threadIdx.x] = c_m.ro[threadIdx.x];
@@ -335,11 +392,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_conv(ConvArgs a, int layer,
             if (ha) conv_edge(da, Hin + (size_t)ia * kF, acc);
             if (__any_sync(0xffffffffu, hb) && hb) conv_edge(db, Hin + (size_t)ib * kF, acc);
         }
-        const float m = transpose_reduce16_g16(acc, gl);  // feature gl
-        float z = sb[gl];
-#pragma unroll
-        for (int g = 0; g < kF; ++g)
-            z = fmaf(sW[gl][g], __shfl_sync(0xffffffffu, m, (lane & 16) + g), z);
+        const int grp = threadIdx.x >> 4;
+        const float z = conv_node_z(acc, gl, sT + grp * GroupT<kConvTS>::kGroup, sM[grp], sW, sb[gl]);
         const float th = tanhf(z);
         float ev = 0.0f;
         if (valid) {
@@ -621,9 +675,11 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
                                                        float* __restrict__ Hout,
                                                        float* __restrict__ TH, double* per_atom,
                                                        double* e_part) {
-    __shared__ float sW[kF][kF + 1];
+    __shared__ __align__(16) float sW[kF * kConvTS];
+    __shared__ __align__(16) float sT[(NT / 16) * GroupT<kConvTS>::kGroup];
+    __shared__ __align__(16) float sM[NT / 16][kF];
     __shared__ float sb[kF], sro[kF];
-    for (int i = threadIdx.x; i < kF * kF; i += NT) sW[i / kF][i % kF] = c_m.W[layer][i];
+    for (int i = threadIdx.x; i < kF * kF; i += NT) sW[(i / kF) * kConvTS + i % kF] = c_m.W[layer][i];
     if (threadIdx.x < kF) {
         sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
         sro[threadIdx.x] = c_m.ro[threadIdx.x];
@@ -681,11 +737,8 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
             accf[2 * i] = acc[i].x;
             accf[2 * i + 1] = acc[i].y;
         }
-        const float m = transpose_reduce16_g16(accf, gl);  // feature gl
-        float z = sb[gl];
-#pragma unroll
-        for (int g = 0; g < kF; ++g)
-            z = fmaf(sW[gl][g], __shfl_sync(0xffffffffu, m, (lane & 16) + g), z);
+        const int grp = threadIdx.x >> 4;
+        const float z = conv_node_z(accf, gl, sT + grp * GroupT<kConvTS>::kGroup, sM[grp], sW, sb[gl]);
         const float th = tanhf(z);
         float ev = 0.0f;
         if (valid) {
@@ -815,6 +868,7 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
     vr[5] = fmaf(ch * q.y, q.z, vr[5]);
 }
 
+constexpr int kBwdTS = 28;  // transpose row: h_bar 16 | virial 6 | gradient 3 | pad
 template <int CTAS, int NT, typename Acc>
 __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
                                                            const float* __restrict__ Hl,
@@ -823,6 +877,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
                                                            double* vir_part, double* vir_grp) {
     __shared__ __align__(16) float sU[(NT / 16)][2][kF];  // [group][m_bar_u, h_u][f]
     __shared__ double sVir[(NT / 16)][6];
+    extern __shared__ __align__(16) float sT[];  // fp32 path: (NT / 16) transpose groups
     const int lane = threadIdx.x & 31;
     const int gl = lane & 15, grp = threadIdx.x >> 4;
     const int64_t g0 = (int64_t)blockIdx.x * (NT / 16) + grp;
@@ -882,6 +937,30 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
             }
         }
         prefetch(k + ng);
+        if constexpr (sizeof(Acc) == 4) {
+            // one shared-memory transpose for h_bar (16), the virial (6) and
+            // the gradient (3): lane gl sums column gl, lanes 0..8 column 16+gl
+            float* T = sT + grp * GroupT<kBwdTS>::kGroup;
+            float4* rw = reinterpret_cast<float4*>(T + gl * kBwdTS);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                rw[c] = make_float4(acc[2 * c].x, acc[2 * c].y, acc[2 * c + 1].x, acc[2 * c + 1].y);
+            rw[4] = make_float4(vr[0], vr[1], vr[2], vr[3]);
+            rw[5] = make_float4(vr[4], vr[5], (float)gx, (float)gy);
+            T[gl * kBwdTS + 24] = (float)gz;
+            __syncwarp();
+            const float hb = column_sum16<kBwdTS>(T, gl);
+            const float xs = column_sum16<kBwdTS>(T, 16 + (gl < 9 ? gl : 0));
+            if (gl < 6) sVir[grp][gl] += (double)xs;
+            // one writer per element (node k belongs to this group alone):
+            // deterministic; reductions (RED, fire-and-forget) keep the
+            // register budget
+            if (valid) {
+                atomicAdd(HB + k * kF + gl, hb);
+                if (gl >= 6 && gl < 9) atomicAdd(reinterpret_cast<double*>(GRAD + k) + (gl - 6), (double)xs);
+            }
+            continue;
+        }
 #pragma unroll
         for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
         if (gl == 0)
@@ -1706,6 +1785,22 @@ bool bwd_edge_ranges() { return bwd_variant() != 1; }
 
 int64_t bwd_edge_stride(int grid) { return (int64_t)grid * (bwd_threads() / 16); }
 
+// dynamic shared memory of the fp32 backward (the epilogue's transpose
+// groups), opted in once per instantiation
+template <int NT>
+static size_t bwd_smem() {
+    constexpr size_t bytes = sizeof(float) * (NT / 16) * GroupT<kBwdTS>::kGroup;
+    static bool done[64] = {};
+    int dev = 0;
+    GMD_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || !done[dev]) {
+        GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge2<1, NT, float>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        if (dev >= 0 && dev < 64) done[dev] = true;
+    }
+    return bytes;
+}
+
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
                      double* vir_part, cudaStream_t s, double* vir_grp, int grid) {
     if (a.n - a.k0 <= 0) return;
@@ -1718,10 +1813,10 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
         k_bwd_edge2<1, kBwdThreadsExact, double><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
                                                                                 vir_grp);
     else if (bwd_threads() == kBwdThreads2)
-        k_bwd_edge2<1, kBwdThreads2, float><<<g, kBwdThreads2, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
+        k_bwd_edge2<1, kBwdThreads2, float><<<g, kBwdThreads2, bwd_smem<kBwdThreads2>(), s>>>(a, MB, Hl, HB, GRAD, vir_part,
                                                                        vir_grp);
     else
-        k_bwd_edge2<1, kBwdThreads, float><<<g, kBwdThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
+        k_bwd_edge2<1, kBwdThreads, float><<<g, kBwdThreads, bwd_smem<kBwdThreads>(), s>>>(a, MB, Hl, HB, GRAD, vir_part,
                                                               vir_grp);
     GMD_LAUNCH_CHECK();
 }
