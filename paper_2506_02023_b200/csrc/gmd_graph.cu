@@ -153,34 +153,36 @@ struct WarpNL {             // per-warp shared state of the search
 __device__ __forceinline__ uint32_t cmpx(uint32_t a, uint32_t b, bool keep_min) {
     return (keep_min == (a < b)) ? a : b;
 }
-__device__ __forceinline__ uint32_t bitonic32(uint32_t k, int lane) {
+// Bitonic network over 16 R keys held by a 16-lane half-warp, R per lane:
+// element i = hl * R + r (r = register), so the strides below R are register
+// compare-exchanges and only the strides >= R shuffle (log2(16) * (log2(16) +
+// 1) / 2 = 10 shuffle stages whatever R).  The two halves of a warp sort two
+// destination rows at once.  Keys are unique; padding slots hold ~0 and sort
+// last.  Ascending.
+template <int R>
+__device__ __forceinline__ void bitonic_half(uint32_t (&k)[R], int hl) {
+    constexpr int N = 16 * R;
 #pragma unroll
-    for (int size = 2; size <= 32; size <<= 1)
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const uint32_t o = __shfl_xor_sync(0xffffffffu, k, stride);
-            const bool asc = (lane & size) == 0, lower = (lane & stride) == 0;
-            k = cmpx(k, o, asc == lower);
-        }
-    return k;
-}
-// 64 keys: element lane in k0, element lane + 32 in k1
-__device__ __forceinline__ void bitonic64(uint32_t& k0, uint32_t& k1, int lane) {
-#pragma unroll
-    for (int size = 2; size <= 64; size <<= 1)
+    for (int size = 2; size <= N; size <<= 1)
 #pragma unroll
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            if (stride == 32) {  // partner is the other register of this lane
-                const uint32_t lo = min(k0, k1), hi = max(k0, k1);
-                k0 = lo;  // size == 64: ascending
-                k1 = hi;
+            if (stride >= R) {
+                const int ls = stride / R;
+                const bool keep_min = (((hl * R) & size) == 0) == ((hl & ls) == 0);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, k[r], ls);
+                    k[r] = keep_min ? min(k[r], o) : max(k[r], o);
+                }
             } else {
-                const uint32_t o0 = __shfl_xor_sync(0xffffffffu, k0, stride);
-                const uint32_t o1 = __shfl_xor_sync(0xffffffffu, k1, stride);
-                const bool lower = (lane & stride) == 0;
-                const bool asc0 = (lane & size) == 0, asc1 = ((lane + 32) & size) == 0;
-                k0 = cmpx(k0, o0, asc0 == lower);
-                k1 = cmpx(k1, o1, asc1 == lower);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & stride) continue;
+                    const bool up = ((hl * R + r) & size) == 0;
+                    const uint32_t a = k[r], b = k[r + stride];
+                    k[r] = up ? min(a, b) : max(a, b);
+                    k[r + stride] = up ? max(a, b) : min(a, b);
+                }
             }
         }
 }
@@ -378,9 +380,8 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
                     __syncwarp();
                 }
             }
-            // canonical (src, image) order (neighborlist.cpp:21-24): warp bitonic
-            // network for rows of <= 64 keys (keys are unique), rank sort above
-            // slab key of a sorted row entry: src << 24 | code of the image of
+            // canonical (src, image) order (neighborlist.cpp:21-24), below.
+            // Slab key of a sorted row entry: src << 24 | code of the image of
             // its stencil cell (neighborlist.cpp:165-170)
             auto slab_key = [&](uint32_t k) {
                 const int c = (int)(k & ((1u << cbits) - 1u));
@@ -395,37 +396,45 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
                 }
                 return ((unsigned long long)(k >> cbits) << 24) | qcode(qv[0], qv[1], qv[2]);
             };
-            for (int t = 0; t < nd; ++t) {
-                const int full = d_cnt[t];
+            // two destination rows per warp, one per half-warp: R keys per
+            // lane in a half-warp bitonic network (rows of <= 128 keys), a
+            // rank sort above
+            const int hl = lane & 15, half = lane >> 4;
+            for (int t0 = 0; t0 < nd; t0 += 2) {
+                const int t = t0 + half;
+                const int full = t < nd ? d_cnt[t] : 0;
                 const int cnt = min(full, cap);
+                const int cmax = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, 16));
                 const uint32_t* kk = keys + (size_t)t * cap;
-                unsigned long long* dst = slab + (size_t)d_id[t] * cap;
-                if (cnt <= 64) {
-                    uint32_t k0 = lane < cnt ? kk[lane] : ~0u;
-                    uint32_t k1 = lane + 32 < cnt ? kk[lane + 32] : ~0u;
-                    if (cnt <= 32) {
-                        k0 = bitonic32(k0, lane);
-                    } else {
-                        bitonic64(k0, k1, lane);
-                        if (lane + 32 < cnt) dst[lane + 32] = slab_key(k1);
-                    }
-                    if (lane < cnt) dst[lane] = slab_key(k0);
+                unsigned long long* dst = slab + (size_t)(t < nd ? d_id[t] : 0) * cap;
+                if (cmax <= 64) {
+                    uint32_t k4[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) k4[r] = hl * 4 + r < cnt ? kk[hl * 4 + r] : ~0u;
+                    bitonic_half<4>(k4, hl);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (hl * 4 + r < cnt) dst[hl * 4 + r] = slab_key(k4[r]);
+                } else if (cmax <= 128) {
+                    uint32_t k8[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) k8[r] = hl * 8 + r < cnt ? kk[hl * 8 + r] : ~0u;
+                    bitonic_half<8>(k8, hl);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (hl * 8 + r < cnt) dst[hl * 8 + r] = slab_key(k8[r]);
                 } else {
-                    for (int k0 = 0; k0 < cnt; k0 += 64) {
-                        const int ka = k0 + lane, kb2 = k0 + 32 + lane;
+                    // rare long rows: rank of each key among the row's keys,
+                    // 16 keys per half-warp step
+                    for (int k0 = 0; k0 < cmax; k0 += 16) {
+                        const int ka = k0 + hl;
                         const uint32_t ma = ka < cnt ? kk[ka] : ~0u;
-                        const uint32_t mb = kb2 < cnt ? kk[kb2] : ~0u;
-                        int ra = 0, rb = 0;
-                        for (int i = 0; i < cnt; ++i) {
-                            const uint32_t x = kk[i];
-                            ra += x < ma;
-                            rb += x < mb;
-                        }
+                        int ra = 0;
+                        for (int i = 0; i < cnt; ++i) ra += kk[i] < ma;
                         if (ka < cnt) dst[ra] = slab_key(ma);
-                        if (kb2 < cnt) dst[rb] = slab_key(mb);
                     }
                 }
-                if (lane == 0) {
+                if (hl == 0 && t < nd) {
                     deg[d_id[t]] = full;
                     atomicMax(&flags[0], full);
                 }
