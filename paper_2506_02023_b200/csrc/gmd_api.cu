@@ -1421,6 +1421,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     if (gen && !wide) launch_gen_init_hbar(h->gm, n, HB, s);  // (tuned, wide: fused into the first bwd_node)
     GMD_CUDA(cudaMemsetAsync(GRAD, 0, sizeof(double4) * n, s));
     for (int l = L - 1; l >= 0; --l) {
+        // layer 0's h_bar is the embedding gradient (no position dependence,
+        // never read) unless the three-body backward follows it (L = 1)
+        const bool need_hbar = l > 0 || (tb && l == L - 1);
         {
             PROF("bwd_node");
             if (wide)
@@ -1440,11 +1443,11 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 ar.nodes += k0;
                 double* vp = v_part + ((size_t)l * 2 + hf) * vgrid * 6;
                 if (wide)
-                    launch_wide_bwd_edge(h->gm, ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
+                    launch_wide_bwd_edge(h->gm, ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s, need_hbar);
                 else if (gen)
                     launch_gen_bwd_edge(h->gm, ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
                 else
-                    launch_bwd_edge(ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
+                    launch_bwd_edge(ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s, nullptr, 0, need_hbar);
             };
             exchange_begin(MB);
             edge(0, h->n_int, 0);
@@ -1454,14 +1457,14 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             exchange(MB);
             PROF("bwd_edge");
             if (wide)
-                launch_wide_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+                launch_wide_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s, need_hbar);
             else if (gen)
                 launch_gen_bwd_edge(h->gm, a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
             else if (use_tc)
                 launch_bwd_edge_tc(a, h->ctab.as<int4>(), h->ccta.as<int32_t>(), vgrid, MB, H[l], HB,
                                    GRAD, v_part + (size_t)l * vgrid * 6, s);
             else if (l > 0 || nchunk == 1)
-                launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s);
+                launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s, nullptr, 0, need_hbar);
             else {  // l = 0 in node chunks, forces streamed out per chunk
                 double* fd = h->forces.get<double>(3 * n_all);
                 // chunk starts on multiples of the grid's node stride and one
@@ -1473,7 +1476,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                     ac.k0 = (n * c / nchunk) / stride * stride;
                     ac.n = c + 1 == nchunk ? n : (n * (c + 1) / nchunk) / stride * stride;
                     if (ac.n <= ac.k0) continue;
-                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part, s, vg, vgrid);
+                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part, s, vg, vgrid, need_hbar);
                     launch_forces_out(ac.n - ac.k0, nullptr, GRAD + ac.k0, fd + 3 * ac.k0, nullptr, s);
                     GMD_CUDA(cudaEventRecord(h->ev[7], s));
                     GMD_CUDA(cudaStreamWaitEvent(h->side, h->ev[7], 0));

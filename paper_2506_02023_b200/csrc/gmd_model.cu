@@ -782,7 +782,7 @@ __device__ __forceinline__ void bwd_load2(const float* __restrict__ MB, const fl
     ldg256(hw + 8, x.h[2], x.h[3]);
 }
 
-template <typename Acc>
+template <typename Acc, bool HBAR = true>
 __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m,
                                           const float4* su_h, float isg, float mus,
                                           float2 acc[kF / 2], Acc& gx, Acc& gy, Acc& gz,
@@ -844,16 +844,19 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
         s2 = f2fma(f2mul(make_float2(phi[2 * j], phi[2 * j + 1]), ck), G[j], s2);
     }
     const float dsum = sizeof(Acc) == 8 ? 0.5f * (s2.x + s2.y) : s2.x + s2.y;
-    // hbar_u += mbar_w (.) s_e, s = fc P phi
-    float php[kK];
+    // hbar_u += mbar_w (.) s_e, s = fc P phi (not for layer 0: the gradient
+    // with respect to the embeddings carries no position dependence)
+    if constexpr (HBAR) {
+        float php[kK];
 #pragma unroll
-    for (int k = 0; k < kK; ++k) php[k] = fc * phi[k];
-    float2 A[kF / 2];
-    radial_pairs(php, A);
+        for (int k = 0; k < kK; ++k) php[k] = fc * phi[k];
+        float2 A[kF / 2];
+        radial_pairs(php, A);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        acc[2 * c] = f2fma(make_float2(x.m[c].x, x.m[c].y), A[2 * c], acc[2 * c]);
-        acc[2 * c + 1] = f2fma(make_float2(x.m[c].z, x.m[c].w), A[2 * c + 1], acc[2 * c + 1]);
+        for (int c = 0; c < 4; ++c) {
+            acc[2 * c] = f2fma(make_float2(x.m[c].x, x.m[c].y), A[2 * c], acc[2 * c]);
+            acc[2 * c + 1] = f2fma(make_float2(x.m[c].z, x.m[c].w), A[2 * c + 1], acc[2 * c + 1]);
+        }
     }
     const float coef = dsum / q.w;
     gx -= (Acc)(q.x * coef);
@@ -869,7 +872,7 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
 }
 
 constexpr int kBwdTS = 28;  // transpose row: h_bar 16 | virial 6 | gradient 3 | pad
-template <int CTAS, int NT, typename Acc>
+template <int CTAS, int NT, typename Acc, bool HBAR = true>
 __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
                                                            const float* __restrict__ Hl,
                                                            float* __restrict__ HB,
@@ -933,7 +936,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
                 xa.q = qa;
                 wa = src_of(a, e + 16, e1);
                 qa = vd_of(a, e + 16, e1);
-                bwd_math2(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
+                bwd_math2<Acc, HBAR>(xa, su_m, su_h, isg, mus, acc, gx, gy, gz, vr);
             }
         }
         prefetch(k + ng);
@@ -949,14 +952,14 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
             rw[5] = make_float4(vr[4], vr[5], (float)gx, (float)gy);
             T[gl * kBwdTS + 24] = (float)gz;
             __syncwarp();
-            const float hb = column_sum16<kBwdTS>(T, gl);
+            const float hb = HBAR ? column_sum16<kBwdTS>(T, gl) : 0.f;
             const float xs = column_sum16<kBwdTS>(T, 16 + (gl < 9 ? gl : 0));
             if (gl < 6) sVir[grp][gl] += (double)xs;
             // one writer per element (node k belongs to this group alone):
             // deterministic; reductions (RED, fire-and-forget) keep the
             // register budget
             if (valid) {
-                atomicAdd(HB + k * kF + gl, hb);
+                if (HBAR) atomicAdd(HB + k * kF + gl, hb);
                 if (gl >= 6 && gl < 9) atomicAdd(reinterpret_cast<double*>(GRAD + k) + (gl - 6), (double)xs);
             }
             continue;
@@ -988,7 +991,7 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
                     atomicAdd(gp + 2, sz);
                 }
             } else {
-                HB[k * kF + gl] += hb;
+                if (HBAR) HB[k * kF + gl] += hb;
                 if (gl == 0) grad_add(GRAD, k, sx, sy, sz);
             }
         }
@@ -1787,14 +1790,14 @@ int64_t bwd_edge_stride(int grid) { return (int64_t)grid * (bwd_threads() / 16);
 
 // dynamic shared memory of the fp32 backward (the epilogue's transpose
 // groups), opted in once per instantiation
-template <int NT>
+template <int NT, bool HBAR>
 static size_t bwd_smem() {
     constexpr size_t bytes = sizeof(float) * (NT / 16) * GroupT<kBwdTS>::kGroup;
     static bool done[64] = {};
     int dev = 0;
     GMD_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !done[dev]) {
-        GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge2<1, NT, float>,
+        GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge2<1, NT, float, HBAR>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         if (dev >= 0 && dev < 64) done[dev] = true;
     }
@@ -1802,22 +1805,35 @@ static size_t bwd_smem() {
 }
 
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
-                     double* vir_part, cudaStream_t s, double* vir_grp, int grid) {
+                     double* vir_part, cudaStream_t s, double* vir_grp, int grid, bool hbar) {
     if (a.n - a.k0 <= 0) return;
     const int variant = bwd_variant();
     if (variant == 1 && a.k0 != 0) raise(kRuntime, "internal: node ranges need the default kernel");
     const int g = grid > 0 ? grid : bwd_edge_grid(a.n - a.k0);
-    if (variant == 1)  // scalar-FFMA kernel (A/B reference)
+    if (variant == 1)  // scalar-FFMA kernel (A/B reference; always forms h_bar)
         k_bwd_edge<<<g, kThreads, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part);
-    else if (exact_forces())
-        k_bwd_edge2<1, kBwdThreadsExact, double><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD, vir_part,
-                                                                                vir_grp);
-    else if (bwd_threads() == kBwdThreads2)
-        k_bwd_edge2<1, kBwdThreads2, float><<<g, kBwdThreads2, bwd_smem<kBwdThreads2>(), s>>>(a, MB, Hl, HB, GRAD, vir_part,
-                                                                       vir_grp);
-    else
-        k_bwd_edge2<1, kBwdThreads, float><<<g, kBwdThreads, bwd_smem<kBwdThreads>(), s>>>(a, MB, Hl, HB, GRAD, vir_part,
-                                                              vir_grp);
+    else if (exact_forces()) {
+        if (hbar)
+            k_bwd_edge2<1, kBwdThreadsExact, double, true><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD,
+                                                                                      vir_part, vir_grp);
+        else
+            k_bwd_edge2<1, kBwdThreadsExact, double, false><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD,
+                                                                                       vir_part, vir_grp);
+    } else if (bwd_threads() == kBwdThreads2) {
+        if (hbar)
+            k_bwd_edge2<1, kBwdThreads2, float, true><<<g, kBwdThreads2, bwd_smem<kBwdThreads2, true>(), s>>>(
+                a, MB, Hl, HB, GRAD, vir_part, vir_grp);
+        else
+            k_bwd_edge2<1, kBwdThreads2, float, false><<<g, kBwdThreads2, bwd_smem<kBwdThreads2, false>(), s>>>(
+                a, MB, Hl, HB, GRAD, vir_part, vir_grp);
+    } else {
+        if (hbar)
+            k_bwd_edge2<1, kBwdThreads, float, true><<<g, kBwdThreads, bwd_smem<kBwdThreads, true>(), s>>>(
+                a, MB, Hl, HB, GRAD, vir_part, vir_grp);
+        else
+            k_bwd_edge2<1, kBwdThreads, float, false><<<g, kBwdThreads, bwd_smem<kBwdThreads, false>(), s>>>(
+                a, MB, Hl, HB, GRAD, vir_part, vir_grp);
+    }
     GMD_LAUNCH_CHECK();
 }
 

@@ -81,8 +81,11 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 // virial sums; with chunk starts k0 that are multiples of
 // bwd_edge_stride(grid) every node meets the same CTA group in the same order
 // as in one launch, so the virial (and everything else) is bitwise the same
+// hbar = false: skip h_bar (the last backward layer, layer 0, whose h_bar is
+// the embedding gradient -- no position dependence, never read)
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
-                     double* vir_part, cudaStream_t s, double* vir_grp = nullptr, int grid = 0);
+                     double* vir_part, cudaStream_t s, double* vir_grp = nullptr, int grid = 0,
+                     bool hbar = true);
 // the default kernel takes node ranges (a.k0 > 0); grid = bwd_edge_grid(n - k0)
 bool bwd_edge_ranges();
 // nodes per sweep of the default kernel's grid (node k -> group k mod stride)

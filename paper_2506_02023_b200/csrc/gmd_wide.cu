@@ -754,7 +754,7 @@ struct BwdSmSmem {
     float part[kFW][32][kPartLd];
 };
 
-template <int BATCH, int MINB>
+template <int BATCH, int MINB, bool HBAR = true>
 __global__ void __launch_bounds__(kFW * 32, MINB) k_wide_bwd_edge_sm(GenModel g, Basis bs, ConvArgs a,
                                                                      const float* __restrict__ MB,
                                                                      const float* __restrict__ Hl,
@@ -803,8 +803,10 @@ __global__ void __launch_bounds__(kFW * 32, MINB) k_wide_bwd_edge_sm(GenModel g,
                 for (int kk = 0; kk < K; ++kk) psi[kk] = phi[kk] * fmaf(cb, (float)kk, ca);
                 S.psi[wq][lane][0] = make_float4(psi[0], psi[1], psi[2], psi[3]);
                 S.psi[wq][lane][1] = make_float4(psi[4], psi[5], psi[6], psi[7]);
-                S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
-                S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+                if (HBAR) {
+                    S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
+                    S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+                }
                 S.src[wq][lane] = a.lsrc[eb + lane];
             } else if (lane < nep) {
                 const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -824,16 +826,18 @@ __global__ void __launch_bounds__(kFW * 32, MINB) k_wide_bwd_edge_sm(GenModel g,
 #pragma unroll
                 for (int j = 0; j < BATCH; ++j) {
                     const int i = i0 + j;
-                    const float4 ua = S.u[wq][i][0], ub = S.u[wq][i][1];
-                    float2 sv = f2mul(P2[0], bc2(ua.x));
-                    sv = f2fma(P2[1], bc2(ua.y), sv);
-                    sv = f2fma(P2[2], bc2(ua.z), sv);
-                    sv = f2fma(P2[3], bc2(ua.w), sv);
-                    sv = f2fma(P2[4], bc2(ub.x), sv);
-                    sv = f2fma(P2[5], bc2(ub.y), sv);
-                    sv = f2fma(P2[6], bc2(ub.z), sv);
-                    sv = f2fma(P2[7], bc2(ub.w), sv);
-                    hb = f2fma(mw[j], sv, hb);
+                    if constexpr (HBAR) {  // layer 0: the embedding gradient is never read
+                        const float4 ua = S.u[wq][i][0], ub = S.u[wq][i][1];
+                        float2 sv = f2mul(P2[0], bc2(ua.x));
+                        sv = f2fma(P2[1], bc2(ua.y), sv);
+                        sv = f2fma(P2[2], bc2(ua.z), sv);
+                        sv = f2fma(P2[3], bc2(ua.w), sv);
+                        sv = f2fma(P2[4], bc2(ub.x), sv);
+                        sv = f2fma(P2[5], bc2(ub.y), sv);
+                        sv = f2fma(P2[6], bc2(ub.z), sv);
+                        sv = f2fma(P2[7], bc2(ub.w), sv);
+                        hb = f2fma(mw[j], sv, hb);
+                    }
                     const float4 pa = S.psi[wq][i][0], pb = S.psi[wq][i][1];
                     float2 sp = f2mul(P2[0], bc2(pa.x));
                     sp = f2fma(P2[1], bc2(pa.y), sp);
@@ -877,9 +881,11 @@ __global__ void __launch_bounds__(kFW * 32, MINB) k_wide_bwd_edge_sm(GenModel g,
             __syncwarp();
         }
         // node complete: one writer per element
-        float2* hbp = reinterpret_cast<float2*>(HB + (size_t)k * F) + lane;
-        const float2 old = *hbp;
-        *hbp = make_float2(old.x + hb.x, old.y + hb.y);
+        if (HBAR) {
+            float2* hbp = reinterpret_cast<float2*>(HB + (size_t)k * F) + lane;
+            const float2 old = *hbp;
+            *hbp = make_float2(old.x + hb.x, old.y + hb.y);
+        }
         const double sx = gwarp_sumd(gx), sy = gwarp_sumd(gy), sz = gwarp_sumd(gz);
 #pragma unroll
         for (int c = 0; c < 6; ++c) vr[c] = gwarp_sum(vr[c]);
@@ -1719,7 +1725,7 @@ void launch_wide_tb_backward(const GenModel& g, const BondArgs& a, const float* 
 }
 
 void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
-                          float* HB, double4* GRAD, double* vir_part, cudaStream_t s) {
+                          float* HB, double4* GRAD, double* vir_part, cudaStream_t s, bool hbar) {
     const int grid = wide_bwd_grid(a.n);
     if (a.n <= 0) {
         GMD_CUDA(cudaMemsetAsync(vir_part, 0, sizeof(double) * 6 * grid, s));
@@ -1746,10 +1752,14 @@ void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB,
         static bool attr_sm = false;
         if (!attr_sm) {
             GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge_sm<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge_sm<4, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sm));
             GMD_CUDA(cudaFuncSetAttribute(k_wide_bwd_edge_sm<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             attr_sm = true;
         }
-        if (var == kBwdSm4)
+        if (var == kBwdSm4 && !hbar)
+            k_wide_bwd_edge_sm<4, 3, false><<<grid, kFW * 32, sm, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);
+        else if (var == kBwdSm4)
             k_wide_bwd_edge_sm<4, 3><<<grid, kFW * 32, sm, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);
         else if (var == kBwdSm8)
             k_wide_bwd_edge_sm<8, 2><<<grid, kFW * 32, sm, s>>>(g, bs, a, MB, Hl, HB, GRAD, vir_part);

@@ -29,7 +29,7 @@ void launch_wide_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, co
                           cudaStream_t s);
 // HB += gathered adjoints, GRAD += positional gradient, virial records
 void launch_wide_bwd_edge(const GenModel& g, const ConvArgs& a, const float* MB, const float* Hl,
-                          float* HB, double4* GRAD, double* vir_part, cudaStream_t s);
+                          float* HB, double4* GRAD, double* vir_part, cudaStream_t s, bool hbar = true);
 
 // three-body stage (potential.cpp:664-741, 850-961), slot conventions of
 // the width-generic kernels; W3 / W3^T per bond on tcgen05
