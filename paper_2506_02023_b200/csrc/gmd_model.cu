@@ -943,6 +943,14 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
         if constexpr (sizeof(Acc) == 4) {
             // one shared-memory transpose for h_bar (16), the virial (6) and
             // the gradient (3): lane gl sums column gl, lanes 0..8 column 16+gl
+            // the node's current h_bar / gradient words: read first, written
+            // back after the transpose (one writer per element, no atomics)
+            float hbo = 0.f;
+            double gro = 0.0;
+            if (valid) {
+                if (HBAR) hbo = HB[k * kF + gl];
+                if (gl >= 6 && gl < 9) gro = reinterpret_cast<const double*>(GRAD + k)[gl - 6];
+            }
             float* T = sT + grp * GroupT<kBwdTS>::kGroup;
             float4* rw = reinterpret_cast<float4*>(T + gl * kBwdTS);
 #pragma unroll
@@ -955,12 +963,10 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
             const float hb = HBAR ? column_sum16<kBwdTS>(T, gl) : 0.f;
             const float xs = column_sum16<kBwdTS>(T, 16 + (gl < 9 ? gl : 0));
             if (gl < 6) sVir[grp][gl] += (double)xs;
-            // one writer per element (node k belongs to this group alone):
-            // deterministic; reductions (RED, fire-and-forget) keep the
-            // register budget
+            // node k belongs to this group alone and each kernel adds once
             if (valid) {
-                if (HBAR) atomicAdd(HB + k * kF + gl, hb);
-                if (gl >= 6 && gl < 9) atomicAdd(reinterpret_cast<double*>(GRAD + k) + (gl - 6), (double)xs);
+                if (HBAR) HB[k * kF + gl] = hbo + hb;
+                if (gl >= 6 && gl < 9) reinterpret_cast<double*>(GRAD + k)[gl - 6] = gro + (double)xs;
             }
             continue;
         }
@@ -977,23 +983,9 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
         }
         const float hb = transpose_reduce16_g16(accf, gl);
         const double sx = group_sum16a(gx), sy = group_sum16a(gy), sz = group_sum16a(gz);
-        if (valid) {
-            // one writer per element (node k belongs to this group alone):
-            // deterministic either way.  The fp32 kernel uses reductions
-            // (RED, fire-and-forget: at its 80-register budget a read-add-
-            // write spills); the fp64 kernel a plain read-add-write
-            if (sizeof(Acc) == 4) {
-                atomicAdd(HB + k * kF + gl, hb);
-                if (gl == 0) {
-                    double* gp = reinterpret_cast<double*>(GRAD + k);
-                    atomicAdd(gp, sx);
-                    atomicAdd(gp + 1, sy);
-                    atomicAdd(gp + 2, sz);
-                }
-            } else {
-                if (HBAR) HB[k * kF + gl] += hb;
-                if (gl == 0) grad_add(GRAD, k, sx, sy, sz);
-            }
+        if (valid) {  // fp64 gradient lanes: one writer per element
+            if (HBAR) HB[k * kF + gl] += hb;
+            if (gl == 0) grad_add(GRAD, k, sx, sy, sz);
         }
     }
     __syncwarp();

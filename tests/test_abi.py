@@ -93,3 +93,21 @@ def test_oracle_is_test_only():
                 txt = open(os.path.join(dirpath, f)).read()
                 for b in banned:
                     assert b not in txt, f"{f} references {b}"
+
+
+def test_no_float_atomics():
+    """north_star (3): segment sums without float atomics.  Every per-node sum
+    is a fixed-order row reduction written by one thread (plain read-add-write);
+    the SASS of the whole library holds no floating-point atomic or reduction
+    (integer counters and the order-preserving u64 encodings of doubles used
+    for exact min/max are allowed)."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", G.LIB_PATH], capture_output=True, text=True).stdout
+    ops = set(re.findall(r"\b((?:RED|ATOM)[A-Z]*\.[A-Z0-9_.]+)", sass))
+    assert ops, "no atomics at all: SASS listing empty?"
+    bad = sorted(o for o in ops if re.search(r"\.(F16|BF16|F32|F64|FADD)\b|\.F32\.|\.F64\.", o))
+    assert not bad, bad
