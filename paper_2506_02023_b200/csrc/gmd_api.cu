@@ -270,6 +270,10 @@ struct gmd_handle {
     LayoutState atoms, bonds;
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
+    DBuf pos4, cell4;  // per-atom records of the neighbour-list emit
+    // the free builders' own wrap buffers (a built graph's pos / cell / fw /
+    // flags stay intact: its export re-runs the emit from them)
+    DBuf fr_pos, fr_cell, fr_fw, fr_bin, fr_cnt, fr_flags;
     DBuf row, src, img, vd, ed, ebond, edst, lsrc, counts, scan_tmp, sel_ws, sel_out, small;
     DBuf brow, bedge, brev, lcnt, lpairs, slab, feat_tmp, flagtmp, ebid;
     int nl_cap = 0;
@@ -736,6 +740,8 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     NLBuffers b{};
     b.pos = dpos;
     b.cell = h->cell.get<int32_t>(3 * n);
+    b.pos4 = h->pos4.get<double4>(n);
+    b.cell4 = h->cell4.get<int4>(n);
     b.fw_axis = h->fw.get<double>(n);
     b.bin = h->bin.get<int32_t>(n);
     b.bin_cnt = h->bin_cnt.get<int32_t>(nbins);
@@ -1702,7 +1708,8 @@ void gmd_destroy(gmd_handle* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    DBuf* bufs[] = {&h->pos, &h->Z, &h->cell, &h->fw, &h->bin, &h->bin_cnt, &h->bin_start,
+    DBuf* bufs[] = {&h->pos, &h->pos4, &h->cell4, &h->fr_pos, &h->fr_cell, &h->fr_fw, &h->fr_bin,
+                    &h->fr_cnt, &h->fr_flags, &h->Z, &h->cell, &h->fw, &h->bin, &h->bin_cnt, &h->bin_start,
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ed, &h->ebond, &h->edst, &h->lsrc, &h->counts,
                     &h->scan_tmp, &h->sel_ws, &h->sel_out, &h->small, &h->brow, &h->bedge, &h->ebid,
@@ -1974,6 +1981,8 @@ int gmd_get_graph(gmd_handle* h, int64_t* src, int64_t* dst, int32_t* off, doubl
             NLBuffers b{};
             b.pos = h->pos.as<double>();
             b.cell = h->cell.as<int32_t>();
+            b.pos4 = h->pos4.as<double4>();
+            b.cell4 = h->cell4.as<int4>();
             b.bcnt = h->bcnt.as<int32_t>();
             b.flags = h->flags.as<int32_t>();
             GraphDev ge;
@@ -2027,7 +2036,7 @@ namespace {
 const double* wrapped_fracs(gmd_handle* h, int64_t n, const double* pos, const double* lat, int axis) {
     cudaStream_t s = h->stream;
     if (std::abs(det3(lat)) < 1e-10) raise(kConfig, "degenerate cell");
-    double* dpos = h->pos.get<double>(3 * n);
+    double* dpos = h->fr_pos.get<double>(3 * n);
     GMD_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
     Geom g{};
     std::memcpy(g.L, lat, sizeof g.L);
@@ -2036,11 +2045,11 @@ const double* wrapped_fracs(gmd_handle* h, int64_t n, const double* pos, const d
     g.axis = axis;
     NLBuffers b{};
     b.pos = dpos;
-    b.cell = h->cell.get<int32_t>(3 * n);
-    b.fw_axis = h->fw.get<double>(n);
-    b.bin = h->bin.get<int32_t>(n);
-    b.bin_cnt = h->bin_cnt.get<int32_t>(1);
-    b.flags = h->flags.get<int32_t>(4);
+    b.cell = h->fr_cell.get<int32_t>(3 * n);
+    b.fw_axis = h->fr_fw.get<double>(n);
+    b.bin = h->fr_bin.get<int32_t>(n);
+    b.bin_cnt = h->fr_cnt.get<int32_t>(1);
+    b.flags = h->fr_flags.get<int32_t>(4);
     GMD_CUDA(cudaMemsetAsync(b.bin_cnt, 0, 4, s));
     GMD_CUDA(cudaMemsetAsync(b.flags, 0, 16, s));
     launch_wrap(g, n, b, s);

@@ -53,7 +53,8 @@ __device__ __forceinline__ int64_t bin_of(const Geom& g, const double fw[3], int
 __global__ void k_wrap(const Geom g, int64_t n, const double* __restrict__ pos,
                        int32_t* __restrict__ cell, double* __restrict__ fw_axis,
                        int32_t* __restrict__ bin, int32_t* __restrict__ bin_cnt,
-                       int32_t* __restrict__ flags) {
+                       int32_t* __restrict__ flags, double4* __restrict__ pos4,
+                       int4* __restrict__ cell4) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // max |coordinate| over the input (rounded up to fp32) -> flags[3]: the
     // search's fast-accept band is only sound while the wrapped and raw
@@ -72,6 +73,10 @@ __global__ void k_wrap(const Geom g, int64_t n, const double* __restrict__ pos,
     cell[3 * i] = c[0];
     cell[3 * i + 1] = c[1];
     cell[3 * i + 2] = c[2];
+    if (pos4) {
+        pos4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], 0.0);
+        cell4[i] = make_int4(c[0], c[1], c[2], 0);
+    }
     fw_axis[i] = fw[g.axis];
     int64_t bi = bin_of(g, fw, b);
     bin[i] = (int32_t)bi;
@@ -450,7 +455,8 @@ template <int G, int MINB = 1>  // lanes per destination row (16 or 32)
 __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, int cap,
                           const unsigned long long* __restrict__ slab,
                           const int32_t* __restrict__ row, const double* __restrict__ pos,
-                          const int32_t* __restrict__ cell, int32_t* __restrict__ e_src,
+                          const int32_t* __restrict__ cell, const double4* __restrict__ pos4,
+                          const int4* __restrict__ cell4, int32_t* __restrict__ e_src,
                           uint32_t* __restrict__ e_img, float4* __restrict__ e_vd,
                           float* __restrict__ e_d, uint8_t* __restrict__ e_bond,
                           int32_t* __restrict__ bcnt, int32_t* __restrict__ flags,
@@ -462,8 +468,10 @@ __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, 
     // lanes of this row (both rows of a warp iterate together for the ballot)
     const unsigned gmask = G == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
     const int e0 = row[i], cnt = live ? row[i + 1] - e0 : 0;
-    const double pix = pos[3 * i], piy = pos[3 * i + 1], piz = pos[3 * i + 2];
-    const int cix = cell[3 * i], ciy = cell[3 * i + 1], ciz = cell[3 * i + 2];
+    const double4 pi4 = pos4[i];
+    const int4 ci4 = cell4[i];
+    const double pix = pi4.x, piy = pi4.y, piz = pi4.z;
+    const int cix = ci4.x, ciy = ci4.y, ciz = ci4.z;
     int nb = 0;
     // the next slot's key is requested before this slot's gathers complete
     unsigned long long knext = lane < cnt ? __ldg(slab + (size_t)i * cap + lane) : 0ull;
@@ -477,16 +485,23 @@ __global__ void __launch_bounds__(128, MINB) k_nl_emit(const Geom g, int64_t n, 
             const int q0 = (int)((key >> 16) & 255) - 128;
             const int q1 = (int)((key >> 8) & 255) - 128;
             const int q2 = (int)(key & 255) - 128;
+            // the source's raw position and cell_of: one 32-byte and one
+            // 16-byte load
+            const double4 pj = pos4[j];
+            const int4 cj = cell4[j];
             // off = image - cell_of[j] + cell_of[i] (neighborlist.cpp:179-180)
-            const int o0 = q0 - cell[3 * j] + cix;
-            const int o1 = q1 - cell[3 * j + 1] + ciy;
-            const int o2 = q2 - cell[3 * j + 2] + ciz;
+            const int o0 = q0 - cj.x + cix;
+            const int o1 = q1 - cj.y + ciy;
+            const int o2 = q2 - cj.z + ciz;
             if (!img_in_range(o0) || !img_in_range(o1) || !img_in_range(o2))
                 atomicOr(&flags[1], kErrImgRange);
-            const d3 raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
-            const d3 vr = {add_rn(sub_rn(pos[3 * j], pix), raw.x),
-                           add_rn(sub_rn(pos[3 * j + 1], piy), raw.y),
-                           add_rn(sub_rn(pos[3 * j + 2], piz), raw.z)};
+            // off = 0 (most edges): off L is a sum of signed zeros, and
+            // x + (+-0) == x for every x the subtraction below can produce
+            // (x - x is +0), so skipping it is bitwise the reference
+            d3 raw = {0.0, 0.0, 0.0};
+            if (o0 | o1 | o2) raw = rowvec_rn(g.L, (double)o0, (double)o1, (double)o2);
+            const d3 vr = {add_rn(sub_rn(pj.x, pix), raw.x), add_rn(sub_rn(pj.y, piy), raw.y),
+                           add_rn(sub_rn(pj.z, piz), raw.z)};
             const double dd = __dsqrt_rn(dot_rn(vr, vr));
             const int e = e0 + k;
             e_src[e] = j;
@@ -647,7 +662,7 @@ int nl_grid(int64_t nbins) {
 
 void launch_wrap(const Geom& g, int64_t n, NLBuffers& b, cudaStream_t s) {
     k_wrap<<<div_up(n, 256), 256, 0, s>>>(g, n, b.pos, b.cell, b.fw_axis, b.bin, b.bin_cnt,
-                                          b.flags);
+                                          b.flags, b.pos4, b.cell4);
     GMD_LAUNCH_CHECK();
 }
 
@@ -706,12 +721,13 @@ void launch_nl_emit(const Geom& g, int64_t n, int cap, const unsigned long long*
                     NLBuffers& b, GraphDev& gd, cudaStream_t s, const int32_t* owner,
                     unsigned long long* req) {
     if (n == 0) return;
+    if (!b.pos4 || !b.cell4) raise(kRuntime, "internal: emit needs the per-atom records");
     // 16 lanes per row: ~45-edge rows fill 3 x 16 slots (94 %) instead of
     // 2 x 32 (70 %); C5 0.70 -> 0.53 ms
     // 128-thread blocks (C5: 128 0.516 ms, 256 0.527, 512 0.624, 1024 0.656)
     // 12 CTAs per SM (40 registers): 0.480 -> 0.472 ms at C5 (16 CTAs / 32
     // registers spill: 0.595 ms)
-    k_nl_emit<16, 12><<<div_up(n, 8), 128, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, gd.src,
+    k_nl_emit<16, 12><<<div_up(n, 8), 128, 0, s>>>(g, n, cap, slab, gd.row, b.pos, b.cell, b.pos4, b.cell4, gd.src,
                                                gd.img, gd.vd, gd.d, gd.bond, b.bcnt, b.flags, owner, req);
     GMD_LAUNCH_CHECK();
 }

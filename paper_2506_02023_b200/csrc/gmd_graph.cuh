@@ -47,6 +47,11 @@ struct NLBuffers {
     int32_t* bcnt;       // n (per-dst bond count)
     int32_t* flags;      // [0] max degree, [1] error bits, [2] max in-bonds,
                          // [3] max |input coordinate| (fp32 bits, k_wrap)
+    // optional 32-byte / 16-byte per-atom records (raw position, cell_of)
+    // written by k_wrap: the emit gathers an edge's source with two vector
+    // loads instead of six scalar ones (required by launch_nl_emit)
+    double4* pos4 = nullptr;
+    int4* cell4 = nullptr;
 };
 
 enum : int { kErrImgRange = 1, kErrQRange = 2, kErrCap = 4 };
