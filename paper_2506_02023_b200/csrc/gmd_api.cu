@@ -685,6 +685,10 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         GMD_CUDA(cudaMemcpyAsync(dZ, Z, sizeof(int32_t) * n, kind, s));
         h->z_pending = false;
     } else {
+        // after the positions: the two host copies would otherwise share the
+        // H2D link while the build waits for the positions
+        GMD_CUDA(cudaEventRecord(h->ev[6], s));
+        GMD_CUDA(cudaStreamWaitEvent(h->side, h->ev[6], 0));
         GMD_CUDA(cudaMemcpyAsync(dZ, Z, sizeof(int32_t) * n, kind, h->side));
         GMD_CUDA(cudaEventRecord(h->ev[6], h->side));
         h->z_pending = true;
