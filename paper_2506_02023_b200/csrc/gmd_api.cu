@@ -1211,7 +1211,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     };
     const int nchunk = (!gen && !rank_mode && forces && !(flags & GMD_OUTPUT_DEVICE) && pinned(forces) &&
                         !(flags & GMD_OUTPUT_F32) && !use_tc && bwd_edge_ranges() &&
-                        !(tb && L == 1) && bwd_edge_grid(n / kForceChunks) == vgrid)
+                        !(tb && L == 1) && bwd_edge_grid(n / 10) == vgrid)
                            ? kForceChunks
                            : 1;
     // one rank per GPU: interior atoms (h->nodes_x[0, n_int)) compute while
@@ -1481,10 +1481,14 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 // carried per-group virial: bitwise the unchunked launch
                 const int64_t stride = bwd_edge_stride(vgrid);
                 double* vg = h->v_grp.get<double>((size_t)stride * 6);
+                // shrinking chunks (40/30/20/10 %): each chunk's force copy
+                // hides under the next chunk's edge pass, and the last one,
+                // exposed after the pass, is the smallest
+                static const int cum[kForceChunks + 1] = {0, 4, 7, 9, 10};
                 for (int c = 0; c < nchunk; ++c) {
                     ConvArgs ac = a;
-                    ac.k0 = (n * c / nchunk) / stride * stride;
-                    ac.n = c + 1 == nchunk ? n : (n * (c + 1) / nchunk) / stride * stride;
+                    ac.k0 = (n * cum[c] / 10) / stride * stride;
+                    ac.n = c + 1 == nchunk ? n : (n * cum[c + 1] / 10) / stride * stride;
                     if (ac.n <= ac.k0) continue;
                     launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part, s, vg, vgrid, need_hbar);
                     launch_forces_out(ac.n - ac.k0, nullptr, GRAD + ac.k0, fd + 3 * ac.k0, nullptr, s);
