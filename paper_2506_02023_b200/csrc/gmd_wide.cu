@@ -1082,6 +1082,15 @@ __device__ __forceinline__ void tb_mma(TbSmem& S, uint32_t tmem, uint32_t& phase
     tc::fence_after();
 }
 
+__device__ __forceinline__ void stage_row_x(unsigned char* x_hi, unsigned char* x_lo, int row, int lane,
+                                            float2 x) {
+    float2 xh, xl;
+    split2(x, xh, xl);
+    const int off = xoff(row, 2 * lane);
+    *reinterpret_cast<float2*>(x_hi + off) = xh;
+    *reinterpret_cast<float2*>(x_lo + off) = xl;
+}
+
 __device__ __forceinline__ void stage_row(TbSmem& S, int row, int lane, float2 x) {
     float2 xh, xl;
     split2(x, xh, xl);
@@ -1635,13 +1644,151 @@ void launch_wide_conv(const GenModel& g, const ConvArgs& a, int layer, const flo
     GMD_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// Per-node W^T y on tcgen05 (bwd_node and the three-body q_bar, potential.cpp
+// :816-822, :460-470): m_bar = W^T (h_bar (.) (1 - th^2)) for 128 nodes per
+// tile, D[r][g] = sum_f y[r][f] W[f][g] as M = 128, N = 64, K = 64 3xTF32
+// into TMEM; warps stage rows (lanes over feature pairs, coalesced row
+// reads), thread r writes node r's row from its TMEM lane.  Every row is an
+// independent dot product, so results do not depend on the tile a node lands
+// in (partition-invariant).  Persistent CTAs, W staged once.
+// ---------------------------------------------------------------------------
+struct NodeTcSmem {
+    unsigned char x_hi[kXBytes];
+    unsigned char x_lo[kXBytes];
+    unsigned char w_hi[kWBytes];
+    unsigned char w_lo[kWBytes];
+    uint64_t mbar;
+    uint32_t tbase;
+};
+constexpr int kNodeTcRows = 8;  // rows a warp loads before staging them
+
+__global__ void __launch_bounds__(128, 2) k_wide_node_tc(GenModel g, int64_t n, const int32_t* __restrict__ nodes,
+                                                        const int32_t* __restrict__ crow,
+                                                        const float* __restrict__ W, float* __restrict__ HB,
+                                                        const float* __restrict__ TH, float* __restrict__ MB,
+                                                        int init) {
+    extern __shared__ __align__(1024) unsigned char wsm[];
+    NodeTcSmem& S = *reinterpret_cast<NodeTcSmem*>(wsm);
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    // B[n][k] = W[k][n]: D[r][n] = sum_k y[r][k] W[k][n]
+    for (int t = tid; t < F * F; t += blockDim.x) {
+        const int nn = t / F, kk = t % F;
+        float hv, lv;
+        tc::split_tf32(W[kk * F + nn], hv, lv);
+        *reinterpret_cast<float*>(S.w_hi + poff(nn, kk)) = hv;
+        *reinterpret_cast<float*>(S.w_lo + poff(nn, kk)) = lv;
+    }
+    if (tid == 0) {
+        tc::mbar_init(&S.mbar, 1);
+        tc::fence_mbar_init();
+    }
+    if (wq == 0) tc::tmem_alloc(&S.tbase, F);
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = S.tbase;
+    const uint32_t trow = tmem + ((uint32_t)(32 * wq) << 16);
+    const float2 ro2 = make_float2(g.ro[2 * lane], g.ro[2 * lane + 1]);
+    uint32_t phase = 0;
+    const int64_t ntiles = (n + 127) / 128;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t k0 = tile * 128;
+        // warp wq stages rows 32 wq .. 32 wq + 31, kNodeTcRows rows' loads in flight
+        for (int j0 = 0; j0 < 32; j0 += kNodeTcRows) {
+            float2 hb[kNodeTcRows], th[kNodeTcRows];
+#pragma unroll
+            for (int j = 0; j < kNodeTcRows; ++j) {
+                const int64_t k = k0 + wq * 32 + j0 + j;
+                hb[j] = make_float2(0.f, 0.f);
+                th[j] = make_float2(0.f, 0.f);
+                if (k < n) {
+                    hb[j] = init ? ro2 : reinterpret_cast<const float2*>(HB + (size_t)k * F)[lane];
+                    th[j] = reinterpret_cast<const float2*>(TH + (size_t)k * F)[lane];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kNodeTcRows; ++j) {
+                const int row = wq * 32 + j0 + j;
+                const int64_t k = k0 + row;
+                if (init && k < n) reinterpret_cast<float2*>(HB + (size_t)k * F)[lane] = hb[j];
+                const float2 y = make_float2(hb[j].x * (1.0f - th[j].x * th[j].x),
+                                             hb[j].y * (1.0f - th[j].y * th[j].y));
+                stage_row_x(S.x_hi, S.x_lo, row, lane, y);
+            }
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (tid == 0) {
+            const uint32_t idesc = tc::idesc_tf32(128, F);
+#pragma unroll
+            for (int ks = 0; ks < F / 8; ++ks) {
+                const uint64_t ah = sdesc2(S.x_hi + ks * 2 * kXLbo, kXLbo, kXSbo);
+                const uint64_t al = sdesc2(S.x_lo + ks * 2 * kXLbo, kXLbo, kXSbo);
+                const uint64_t bh = sdesc2(S.w_hi + ks * 2 * kPLbo, kPLbo, kPSbo);
+                const uint64_t bl = sdesc2(S.w_lo + ks * 2 * kPLbo, kPLbo, kPSbo);
+                tc::mma_tf32(tmem, ah, bh, idesc, ks > 0);
+                tc::mma_tf32(tmem, al, bh, idesc, true);
+                tc::mma_tf32(tmem, ah, bl, idesc, true);
+            }
+            tc::commit(&S.mbar);
+        }
+        tc::mbar_wait(&S.mbar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        // thread tid holds row tid of the tile in its TMEM lane
+        float z[F];
+        tc::tmem_ld32(trow, z);
+        tc::tmem_ld32(trow + 32, z + 32);
+        const int64_t k = k0 + tid;
+        if (k < n) {
+            const int64_t v = nodes ? (int64_t)nodes[k] : k;
+            const int64_t r = crow ? (int64_t)crow[v] : v;
+            float4* dst = reinterpret_cast<float4*>(MB + (size_t)r * F);
+#pragma unroll
+            for (int c = 0; c < F / 4; ++c) dst[c] = make_float4(z[4 * c], z[4 * c + 1], z[4 * c + 2], z[4 * c + 3]);
+        }
+        // the next tile restages x and overwrites TMEM
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+    }
+    if (wq == 0) tc::tmem_free(tmem, F);
+}
+
+static bool node_tc() {  // GMD_WIDE_NODE_TC=0: the FFMA2 warp-per-node kernel (A/B, tests)
+    const char* v = std::getenv("GMD_WIDE_NODE_TC");
+    return !(v && v[0] == '0');
+}
+
+static void launch_node(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
+                        const float* W, float* HB, const float* TH, float* MB, bool init, cudaStream_t s) {
+    if (node_tc()) {
+        static bool attr[64] = {};
+        int dev = 0;
+        GMD_CUDA(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= 64 || !attr[dev]) {
+            GMD_CUDA(cudaFuncSetAttribute(k_wide_node_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(NodeTcSmem)));
+            if (dev >= 0 && dev < 64) attr[dev] = true;
+        }
+        int64_t gr = (n + 127) / 128;
+        if (gr > 148 * 2) gr = 148 * 2;
+        k_wide_node_tc<<<(int)gr, 128, sizeof(NodeTcSmem), s>>>(g, n, nodes, crow, W, HB, TH, MB, init ? 1 : 0);
+    } else {
+        k_wide_bwd_node<<<wide_conv_grid(n), kConvWarps * 32, 0, s>>>(g, n, nodes, crow, W, HB, TH, MB,
+                                                                      init ? 1 : 0);
+    }
+    GMD_LAUNCH_CHECK();
+}
+
 void launch_wide_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
                           int layer, float* HB, const float* TH, float* MB, bool init, cudaStream_t s) {
     if (n <= 0) return;
-    k_wide_bwd_node<<<wide_conv_grid(n), kConvWarps * 32, 0, s>>>(g, n, nodes, crow,
-                                                                  g.W + (size_t)layer * F * F, HB, TH,
-                                                                  MB, init ? 1 : 0);
-    GMD_LAUNCH_CHECK();
+    launch_node(g, n, nodes, crow, g.W + (size_t)layer * F * F, HB, TH, MB, init, s);
 }
 
 static int back2_grid(int64_t n) {  // four CTAs of 8 warps per SM, one wave
@@ -1670,9 +1817,7 @@ void launch_wide_tb_inject(const GenModel& g, const BondArgs& a, const float* TP
 void launch_wide_tb_bwd_q(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
                           const float* HB, const float* TH4, float* QB, cudaStream_t s) {
     if (n <= 0) return;
-    k_wide_bwd_node<<<wide_conv_grid(n), kConvWarps * 32, 0, s>>>(g, n, nodes, crow, g.W4,
-                                                                  const_cast<float*>(HB), TH4, QB, 0);
-    GMD_LAUNCH_CHECK();
+    launch_node(g, n, nodes, crow, g.W4, const_cast<float*>(HB), TH4, QB, false, s);
 }
 
 static int tb_tc_grid(int64_t n) {  // two CTAs per SM (shared memory), one wave
