@@ -859,35 +859,42 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     int32_t* rowp = h->row.get<int32_t>(n + 1);
     int32_t hdr[2];
     int32_t ne32 = 0;
+    // p = 1: the edge arrays are sized n x cap, so the emit follows the search
+    // without a host round trip; the edge count and the slab-overflow check
+    // ride on the build's final flag read (an overflowing row, rare with the
+    // carried capacity, rebuilds at the larger capacity)
+    const bool defer = p == 1 && !rank_mode && (int64_t)n * cap < INT32_MAX;
     for (int attempt = 0; attempt < 2; ++attempt) {
         auto* slab = h->slab.get<unsigned long long>((size_t)n * cap);
         { PROF("nl_search"); launch_nl_search(g, thr32, acc32, zero32, pos_gate, nbins, n, cap, b, slab, ownp, myrank, s); }
         { PROF("scan"); scan_i32(h, b.deg, rowp, n); }
+        if (defer) break;
         GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
         read_flags(h, hdr);
         if (hdr[0] <= cap) break;
         cap = (hdr[0] + 7) & ~7;  // rare: an atom exceeded the slab row
         GMD_CUDA(cudaMemsetAsync(b.flags, 0, 8, s));  // keeps k_wrap's flags[3]
     }
-    {   // next build: size the slab from this one's maximum degree
-        h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
+    if (!defer) {
+        h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;  // next build: this one's max degree
+        if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
+        h->ne = ne32;
     }
-    if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
-    h->ne = ne32;
+    const int64_t ecap = std::max<int64_t>(1, defer ? (int64_t)n * cap : (int64_t)ne32);
     GraphDev gd;
     gd.n = n;
-    gd.ne = h->ne;
+    gd.ne = defer ? -1 : h->ne;  // (the emit and the bond kernels read row[], not ne)
     gd.row = rowp;
-    gd.src = h->src.get<int32_t>(h->ne);
+    gd.src = h->src.get<int32_t>(ecap);
     // packed image offsets: the three-body stage needs them; otherwise they
     // are only read by the graph export, which re-derives them from the slab
     // (4 B per edge not written per step)
     h->emit_cap = cap;
     h->img_ok = r3 > 0.0;
-    gd.img = h->img_ok ? h->img.get<uint32_t>(h->ne) : nullptr;
-    gd.vd = h->vd.get<float4>(h->ne);
-    gd.d = h->ed.get<float>(h->ne);
-    gd.bond = r3 > 0.0 ? h->ebond.get<uint8_t>(h->ne) : nullptr;  // three-body bonds only
+    gd.img = h->img_ok ? h->img.get<uint32_t>(ecap) : nullptr;
+    gd.vd = h->vd.get<float4>(ecap);
+    gd.d = h->ed.get<float>(ecap);
+    gd.bond = r3 > 0.0 ? h->ebond.get<uint8_t>(ecap) : nullptr;  // three-body bonds only
     // p > 1 in one process: the requirement masks are OR-ed in by the emit
     unsigned long long* req_emit = nullptr;
     if (p > 1 && !rank_mode) {
@@ -918,7 +925,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         {
             PROF("part_edge_lsrc");
             launch_edge_lsrc(rowp, gd.src, n, ownp, A.crow.as<int32_t>(), A.node_array.as<int32_t>(),
-                             A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(h->ne), b.flags, s);
+                             A.list_off_d.as<int32_t>(), p, h->lsrc.get<int32_t>(ecap), b.flags, s);
         }
         if (rank_mode) build_rank_plan(h, ownp, myrank);
     }
@@ -937,7 +944,7 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         h->max_bonds = fl[2];
         int32_t* be = h->bedge.get<int32_t>(h->nb);
         int32_t* bv = h->brev.get<int32_t>(h->nb);
-        int32_t* ebid = h->ebid.get<int32_t>(std::max<int64_t>(1, h->ne));
+        int32_t* ebid = h->ebid.get<int32_t>(ecap);
         { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, ebid, s); }
         { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, ebid, bv, b.flags, ownp, myrank, s); }
         if (rank_mode) build_bond_rank_plan(h, ownp, myrank);
@@ -948,6 +955,20 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     // the global bonds), so they are built here only on request
     if ((flags & GMD_LINE_PARTS) && h->has_lg && !rank_mode) build_line_edges_dev(h);
     GMD_CUDA(cudaEventRecord(h->ev[1], s));
+    if (defer) {
+        GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaMemcpyAsync(hdr, b.flags, 8, cudaMemcpyDeviceToHost, s));
+        sync(h);
+        if (hdr[0] > cap) {  // truncated slab rows: everything above is void
+            h->built = false;
+            h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
+            build_impl(h, n, pos, Z, lat, pbc, rc, r3, tau, p, flags);
+            return;
+        }
+        h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;  // next build: this one's max degree
+        if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
+        h->ne = ne32;
+    }
     read_flags(h, hdr);
     float ms = 0.f;
     GMD_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
