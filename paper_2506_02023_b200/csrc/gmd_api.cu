@@ -365,10 +365,16 @@ struct Prof {
 
 void sync(gmd_handle* h) { GMD_CUDA(cudaStreamSynchronize(h->stream)); }
 
+void check_flags(int e);
+
 void read_flags(gmd_handle* h, int32_t out[2]) {
     GMD_CUDA(cudaMemcpyAsync(out, h->flags.as<int32_t>(), 8, cudaMemcpyDeviceToHost, h->stream));
     sync(h);
-    int e = out[1];
+    check_flags(out[1]);
+}
+
+// error bits of the device flag word (flags[1])
+void check_flags(int e) {
     if (e & kErrImgRange)
         raise(kConfig, "periodic image offset exceeds the packed range (+-511 cells)");
     if (e & kErrQRange) raise(kConfig, "neighbour stencil exceeds 127 cell images per axis");
@@ -936,14 +942,21 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     if (h->has_lg) {
         int32_t* br = h->brow.get<int32_t>(n + 1);
         { PROF("scan"); scan_i32(h, b.bcnt, br, n); }
-        int32_t nb32 = 0, fl[4];
-        GMD_CUDA(cudaMemcpyAsync(&nb32, br + n, 4, cudaMemcpyDeviceToHost, s));
-        GMD_CUDA(cudaMemcpyAsync(fl, b.flags, 16, cudaMemcpyDeviceToHost, s));
-        sync(h);
-        h->nb = nb32;
-        h->max_bonds = fl[2];
-        int32_t* be = h->bedge.get<int32_t>(h->nb);
-        int32_t* bv = h->brev.get<int32_t>(h->nb);
+        // deferred like the edge count: bond arrays sized by the edge
+        // capacity, the bond count and max in-bonds read with the final flags
+        const bool defer_b = defer && !(flags & GMD_LINE_PARTS);
+        int64_t bcap = ecap;
+        if (!defer_b) {
+            int32_t nb32 = 0, fl[4];
+            GMD_CUDA(cudaMemcpyAsync(&nb32, br + n, 4, cudaMemcpyDeviceToHost, s));
+            GMD_CUDA(cudaMemcpyAsync(fl, b.flags, 16, cudaMemcpyDeviceToHost, s));
+            sync(h);
+            h->nb = nb32;
+            h->max_bonds = fl[2];
+            bcap = std::max<int64_t>(1, h->nb);
+        }
+        int32_t* be = h->bedge.get<int32_t>(bcap);
+        int32_t* bv = h->brev.get<int32_t>(bcap);
         int32_t* ebid = h->ebid.get<int32_t>(ecap);
         { PROF("bond_edges"); launch_bond_edges(rowp, gd.bond, n, br, be, ebid, s); }
         { PROF("bond_rev"); launch_bond_rev(n, gd, br, be, ebid, bv, b.flags, ownp, myrank, s); }
@@ -956,9 +969,17 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
     if ((flags & GMD_LINE_PARTS) && h->has_lg && !rank_mode) build_line_edges_dev(h);
     GMD_CUDA(cudaEventRecord(h->ev[1], s));
     if (defer) {
+        int32_t fl[4] = {0, 0, 0, 0}, nb32 = 0;
         GMD_CUDA(cudaMemcpyAsync(&ne32, rowp + n, 4, cudaMemcpyDeviceToHost, s));
-        GMD_CUDA(cudaMemcpyAsync(hdr, b.flags, 8, cudaMemcpyDeviceToHost, s));
+        GMD_CUDA(cudaMemcpyAsync(fl, b.flags, 16, cudaMemcpyDeviceToHost, s));
+        if (h->has_lg) GMD_CUDA(cudaMemcpyAsync(&nb32, h->brow.as<int32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
         sync(h);
+        hdr[0] = fl[0];
+        hdr[1] = fl[1];
+        if (h->has_lg && !(flags & GMD_LINE_PARTS)) {
+            h->nb = nb32;
+            h->max_bonds = fl[2];
+        }
         if (hdr[0] > cap) {  // truncated slab rows: everything above is void
             h->built = false;
             h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;
@@ -968,8 +989,10 @@ void build_impl(gmd_handle* h, int64_t n, const double* pos, const int32_t* Z, c
         h->nl_cap = (hdr[0] + hdr[0] / 8 + 4 + 7) & ~7;  // next build: this one's max degree
         if (ne32 < 0) raise(kConfig, "edge count exceeds the int32 index range");
         h->ne = ne32;
+        check_flags(hdr[1]);
+    } else {
+        read_flags(h, hdr);
     }
-    read_flags(h, hdr);
     float ms = 0.f;
     GMD_CUDA(cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
     h->t_graph = ms * 1e-3;

@@ -440,7 +440,10 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
                     }
                 }
                 if (hl == 0 && t < nd) {
-                    deg[d_id[t]] = full;
+                    // the row as stored (<= cap: the emit never reads past a
+                    // slab row); the true maximum goes to flags[0], and a
+                    // build whose maximum exceeds cap is redone
+                    deg[d_id[t]] = cnt;
                     atomicMax(&flags[0], full);
                 }
             }

@@ -58,8 +58,9 @@ enum : int { kErrImgRange = 1, kErrQRange = 2, kErrCap = 4 };
 
 void launch_wrap(const Geom& g, int64_t n, NLBuffers& b, cudaStream_t s);
 void launch_bin_scatter(const Geom& g, int64_t n, NLBuffers& b, int32_t* fill, cudaStream_t s);
-// search: per-destination sorted (src, image) keys into slab[n x cap], true
-// degrees into deg, max degree into flags[0] (slab rows truncated at cap)
+// search: per-destination sorted (src, image) keys into slab[n x cap], stored
+// row lengths min(degree, cap) into deg, the true max degree into flags[0]
+// (slab rows truncated at cap; a build whose max exceeds cap is redone)
 // only >= 0: rows only for destination atoms with owner[i] == only (the
 // other rows stay empty; deg must be zeroed by the caller)
 // pos_gate: the fast-accept band is disabled on the device when any input
