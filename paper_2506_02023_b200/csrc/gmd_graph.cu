@@ -153,11 +153,6 @@ struct WarpNL {             // per-warp shared state of the search
     uint32_t code[kCodeCap];      // image q code per stencil cell of the bin
 };
 
-// Warp bitonic sorting networks (ascending) on unique 32-bit keys; padding
-// slots hold ~0 and sort last.
-__device__ __forceinline__ uint32_t cmpx(uint32_t a, uint32_t b, bool keep_min) {
-    return (keep_min == (a < b)) ? a : b;
-}
 // Bitonic network over 16 R keys held by a 16-lane half-warp, R per lane:
 // element i = hl * R + r (r = register), so the strides below R are register
 // compare-exchanges and only the strides >= R shuffle (log2(16) * (log2(16) +

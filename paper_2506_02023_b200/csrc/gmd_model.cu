@@ -123,44 +123,6 @@ __device__ __forceinline__ void store_row16(float* p, const float h[kF]) {
     for (int i = 0; i < 4; ++i) q[i] = make_float4(h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3]);
 }
 
-// Sum 16 per-lane values over the warp; lane l ends with feature (l >> 1).
-__device__ __forceinline__ float transpose_reduce16(float v[kF], int lane) {
-    float w8[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        bool up = lane & 16;
-        float send = up ? v[i] : v[i + 8];
-        float keep = up ? v[i + 8] : v[i];
-        w8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    float w4[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        bool up = lane & 8;
-        float send = up ? w8[i] : w8[i + 4];
-        float keep = up ? w8[i + 4] : w8[i];
-        w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    float w2[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        bool up = lane & 4;
-        float send = up ? w4[i] : w4[i + 2];
-        float keep = up ? w4[i + 2] : w4[i];
-        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    bool up = lane & 2;
-    float send = up ? w2[0] : w2[1];
-    float keep = up ? w2[1] : w2[0];
-    float w1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    return w1 + __shfl_xor_sync(0xffffffffu, w1, 1);
-}
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -309,8 +271,7 @@ __device__ __forceinline__ double group_sum16d(double v) {
     for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-__device__ __forceinline__ double group_sum16a(float v) { return (double)group_sum16(v); }
-__device__ __forceinline__ double group_sum16a(double v) { return group_sum16d(v); }
+
 // Newton's third law, exactly: an edge and its reverse produce bitwise
 // opposite fp32 gradient terms (symmetric dsum, negated vector), which are
 // summed per node in fp64 -- exact for terms within 2^29 of each other -- so
@@ -968,24 +929,24 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
                 if (HBAR) HB[k * kF + gl] = hbo + hb;
                 if (gl >= 6 && gl < 9) reinterpret_cast<double*>(GRAD + k)[gl - 6] = gro + (double)xs;
             }
-            continue;
-        }
+        } else {
 #pragma unroll
-        for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
-        if (gl == 0)
+            for (int c = 0; c < 6; ++c) vr[c] = group_sum16(vr[c]);
+            if (gl == 0)
 #pragma unroll
-            for (int c = 0; c < 6; ++c) sVir[grp][c] += (double)vr[c];
-        float accf[kF];
+                for (int c = 0; c < 6; ++c) sVir[grp][c] += (double)vr[c];
+            float accf[kF];
 #pragma unroll
-        for (int i = 0; i < kF / 2; ++i) {
-            accf[2 * i] = acc[i].x;
-            accf[2 * i + 1] = acc[i].y;
-        }
-        const float hb = transpose_reduce16_g16(accf, gl);
-        const double sx = group_sum16a(gx), sy = group_sum16a(gy), sz = group_sum16a(gz);
-        if (valid) {  // fp64 gradient lanes: one writer per element
-            if (HBAR) HB[k * kF + gl] += hb;
-            if (gl == 0) grad_add(GRAD, k, sx, sy, sz);
+            for (int i = 0; i < kF / 2; ++i) {
+                accf[2 * i] = acc[i].x;
+                accf[2 * i + 1] = acc[i].y;
+            }
+            const float hb = transpose_reduce16_g16(accf, gl);
+            const double sx = group_sum16d(gx), sy = group_sum16d(gy), sz = group_sum16d(gz);
+            if (valid) {  // fp64 gradient lanes: one writer per element
+                if (HBAR) HB[k * kF + gl] += hb;
+                if (gl == 0) grad_add(GRAD, k, sx, sy, sz);
+            }
         }
     }
     __syncwarp();
@@ -1349,12 +1310,6 @@ __device__ __forceinline__ void bond_t(float d, float t[kF]) {
     float u[kK];
     basis(d, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u);
     fk_pairs(c_m.P3T, u, t);  // t_f = sum_k P3[f][k] u_k
-}
-
-__device__ __forceinline__ void bond_dt(float d, float ds[kF]) {
-    float u[kK], du[kK];
-    basis_d(d, c_m.r3, c_m.inv_r3, c_m.inv_sigma3, c_m.mu_step3, u, du);
-    fk_pairs(c_m.P3T, du, ds);
 }
 
 // per center s: for each in-bond slot j (bond e1 = (w->s)), compute t' of the
