@@ -234,7 +234,7 @@ __global__ void k_send_rows(int32_t t0, int32_t t1, const int32_t* __restrict__ 
 // ---------------------------------------------------------------------------
 // stable multi-list compaction (build_span_layout, partitioner.cpp:153-180)
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 1024;  // ids per warp-chunk
+constexpr int kChunk = 256;  // ids per warp-chunk (C5 p = 8: 3888 warps, ~26 per SM; 1024: 972)
 
 // smallest list id > last that node (owner o, mask m) belongs to, or INT_MAX
 __device__ __forceinline__ int next_list(int o, unsigned long long m, int p, int last) {
