@@ -271,6 +271,7 @@ struct gmd_handle {
 
     DBuf pos, Z, cell, fw, bin, bin_cnt, bin_start, fill, s_id, s_w, s_p, s_c, deg, bcnt, flags;
     DBuf pos4, cell4;  // per-atom records of the neighbour-list emit
+    DBuf zs, zmask;    // per-row species byte, species presence mask (layer-0 conv)
     // the free builders' own wrap buffers (a built graph's pos / cell / fw /
     // flags stay intact: its export re-runs the emit from them)
     DBuf fr_pos, fr_cell, fr_fw, fr_bin, fr_cnt, fr_flags;
@@ -1403,7 +1404,8 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         if (gen)
             launch_gen_embed(h->gm, R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
         else
-            launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
+            launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s,
+                         h->zs.get<uint8_t>(std::max<int64_t>(1, R)), h->zmask.get<unsigned>(4));
     }
     GMD_CUDA(cudaEventRecord(h->ev[3], s));
 
@@ -1449,7 +1451,8 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 launch_gen_conv(h->gm, ar, l, H[l], H[l + 1], th, pl, s);
             else
                 launch_conv(ar, l, H[l], H[l + 1], th, pl, l == L - 1 ? e_part + (size_t)hf * grid : nullptr,
-                            s);
+                            s, l == 0 && !tbl ? h->zs.as<uint8_t>() : nullptr,
+                            l == 0 && !tbl ? h->zmask.as<unsigned>() : nullptr);
         };
         const bool halo = l > 0 || tbl;
         if (halo && overlap) {
@@ -1760,7 +1763,7 @@ void gmd_destroy(gmd_handle* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    DBuf* bufs[] = {&h->pos, &h->pos4, &h->cell4, &h->fr_pos, &h->fr_cell, &h->fr_fw, &h->fr_bin,
+    DBuf* bufs[] = {&h->pos, &h->pos4, &h->cell4, &h->zs, &h->zmask, &h->fr_pos, &h->fr_cell, &h->fr_fw, &h->fr_bin,
                     &h->fr_cnt, &h->fr_flags, &h->Z, &h->cell, &h->fw, &h->bin, &h->bin_cnt, &h->bin_start,
                     &h->fill, &h->s_id, &h->s_w, &h->s_p, &h->s_c, &h->deg, &h->bcnt, &h->flags,
                     &h->row, &h->src, &h->img, &h->vd, &h->ed, &h->ebond, &h->edst, &h->lsrc, &h->counts,

@@ -152,16 +152,38 @@ __device__ __forceinline__ void cta_partials(const double (&v)[W], double* out) 
 }
 
 // --------------------------------------------------------------------------
+// h0 rows = emb[Z] for every layout row (potential.cpp:597-602); with zs,
+// also the row's species byte and the 119-bit presence mask of the species
+// (zmask[4]: an atomic only where the bit is not yet visible) for the
+// layer-0 conv's species-sum form
 __global__ void k_embed(int64_t rows, const int32_t* __restrict__ node_array,
-                        const int32_t* __restrict__ Z, float* __restrict__ H0) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= rows * 4) return;
-    int64_t r = t >> 2;
-    int q = (int)(t & 3);
-    int id = node_array ? node_array[r] : (int)r;
-    int z = Z[id];
-    const float* e = c_m.emb + z * kF + 4 * q;
-    reinterpret_cast<float4*>(H0)[t] = make_float4(e[0], e[1], e[2], e[3]);
+                        const int32_t* __restrict__ Z, float* __restrict__ H0,
+                        uint8_t* __restrict__ zs, unsigned* zmask) {
+    __shared__ unsigned smask[4];
+    if (threadIdx.x < 4) smask[threadIdx.x] = 0u;
+    __syncthreads();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = t < rows * 4;
+    const int64_t r = t >> 2;
+    const int q = (int)(t & 3);
+    int z = 0;
+    if (live) {
+        const int id = node_array ? node_array[r] : (int)r;
+        z = Z[id];
+        const float* e = c_m.emb + z * kF + 4 * q;
+        reinterpret_cast<float4*>(H0)[t] = make_float4(e[0], e[1], e[2], e[3]);
+        if (zs && q == 0) zs[r] = (uint8_t)z;
+    }
+    if (zs) {  // presence mask: warp OR -> block OR -> one global OR per word
+        const bool mine = live && q == 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const unsigned v = __reduce_or_sync(0xffffffffu, mine && (z >> 5) == w ? 1u << (z & 31) : 0u);
+            if ((threadIdx.x & 31) == 0 && v) atomicOr(&smask[w], v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 4 && smask[threadIdx.x]) atomicOr(zmask + threadIdx.x, smask[threadIdx.x]);
+    }
 }
 
 __global__ void k_exchange(int64_t nx, const int32_t* __restrict__ xdst,
@@ -238,6 +260,7 @@ __device__ __forceinline__ float column_sum16(const float* sT, int col) {
 // rows read as float4 (sW row stride 20).  Used by both conv kernel families
 // (bitwise-equal energies).
 constexpr int kConvTS = 20;
+__device__ __forceinline__ float conv_wm(float m, int gl, float* sM, const float* sW, float b);
 __device__ __forceinline__ float conv_node_z(const float acc[kF], int gl, float* sT, float* sM,
                                              const float* sW, float b) {
     float4* row = reinterpret_cast<float4*>(sT + gl * kConvTS);
@@ -245,7 +268,13 @@ __device__ __forceinline__ float conv_node_z(const float acc[kF], int gl, float*
     for (int c = 0; c < 4; ++c)
         row[c] = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
     __syncwarp();
-    sM[gl] = column_sum16<kConvTS>(sT, gl);
+    return conv_wm(column_sum16<kConvTS>(sT, gl), gl, sM, sW, b);
+}
+
+// z_gl = b + sum_g W[gl][g] m_g from each lane's m_gl (m broadcast through
+// shared memory, W rows as float4)
+__device__ __forceinline__ float conv_wm(float m, int gl, float* sM, const float* sW, float b) {
+    sM[gl] = m;
     __syncwarp();
     const float4* mv = reinterpret_cast<const float4*>(sM);
     const float4* wr = reinterpret_cast<const float4*>(sW + gl * kConvTS);
@@ -630,20 +659,48 @@ __device__ __forceinline__ void conv_math2(const ConvIn& x, float2 acc[kF / 2]) 
     }
 }
 
-template <int CTAS, int NT = kThreads>
+// SPEC (layer 0, h0 = emb[Z], at most two species present): m_f =
+// sum_e emb[Z_src][f] s_e,f = sum_s emb[z_s][f] sum_k P[f][k] Phi_s,k with
+// Phi_s = sum over in-edges from species s of fc(d) phi(d) -- per edge only
+// the radial basis and one species byte (no 64-byte row gather, no 16 x 8
+// contraction); the contraction runs once per node.  More than two species:
+// the per-edge form below.
+template <int CTAS, int NT = kThreads, bool SPEC = false>
 __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
                                                        const float* __restrict__ Hin,
                                                        float* __restrict__ Hout,
                                                        float* __restrict__ TH, double* per_atom,
-                                                       double* e_part) {
+                                                       double* e_part, const uint8_t* __restrict__ zs = nullptr,
+                                                       const unsigned* __restrict__ zmask = nullptr) {
     __shared__ __align__(16) float sW[kF * kConvTS];
     __shared__ __align__(16) float sT[(NT / 16) * GroupT<kConvTS>::kGroup];
     __shared__ __align__(16) float sM[NT / 16][kF];
     __shared__ float sb[kF], sro[kF];
+    __shared__ __align__(16) float sPe[SPEC ? 2 * kF * kK : 4];  // [s][f][k] = emb[z_s][f] P[f][k]
     for (int i = threadIdx.x; i < kF * kF; i += NT) sW[(i / kF) * kConvTS + i % kF] = c_m.W[layer][i];
     if (threadIdx.x < kF) {
         sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
         sro[threadIdx.x] = c_m.ro[threadIdx.x];
+    }
+    int nspec = 3, z1 = -1;
+    if constexpr (SPEC) {
+        int z0 = -1;
+        nspec = 0;
+        for (int w = 0; w < 4; ++w) {
+            unsigned m = zmask[w];
+            nspec += __popc(m);
+            while (m) {
+                const int z = 32 * w + __ffs(m) - 1;
+                m &= m - 1u;
+                if (z0 < 0) z0 = z; else if (z1 < 0) z1 = z;
+            }
+        }
+        if (z1 < 0) z1 = z0;
+        if (nspec <= 2)
+            for (int i = threadIdx.x; i < 2 * kF * kK; i += NT) {
+                const int sp = i / (kF * kK), f = (i / kK) % kF, kk = i % kK;
+                sPe[i] = c_m.emb[(sp ? z1 : z0) * kF + f] * c_m.P[f * kK + kk];
+            }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -681,25 +738,86 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
         float2 acc[kF / 2];
 #pragma unroll
         for (int i = 0; i < kF / 2; ++i) acc[i] = make_float2(0.f, 0.f);
-        // one gathered row per lane in flight; index and d one slot ahead
-        ConvIn x;
-        for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
-            if (e < e1) {
-                conv_load(Hin, w, x);
-                x.d = dcur;
-                w = src_of(a, e + 16, e1);
-                dcur = d_of(a, e + 16, e1);
-                conv_math2(x, acc);
-            }
-        }
-        float accf[kF];
-#pragma unroll
-        for (int i = 0; i < kF / 2; ++i) {
-            accf[2 * i] = acc[i].x;
-            accf[2 * i + 1] = acc[i].y;
-        }
         const int grp = threadIdx.x >> 4;
-        const float z = conv_node_z(accf, gl, sT + grp * GroupT<kConvTS>::kGroup, sM[grp], sW, sb[gl]);
+        float z;
+        if (SPEC && nspec <= 2) {
+            // acc[0..3] = Phi_0 (k pairs), acc[4..7] = Phi_1
+            for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
+                if (e < e1) {
+                    const float d = dcur;
+                    const float w1 = zs[w] == z1 ? 1.0f : 0.0f, w0 = 1.0f - w1;
+                    w = src_of(a, e + 16, e1);
+                    dcur = d_of(a, e + 16, e1);
+                    float phi[kK];
+                    phi_fast(d, phi);
+                    const float fc = fc_fast(d);
+#pragma unroll
+                    for (int j = 0; j < kK / 2; ++j) {
+                        const float2 u = f2mul(make_float2(phi[2 * j], phi[2 * j + 1]), bcast(fc));
+                        acc[j] = f2fma(bcast(w0), u, acc[j]);
+                        acc[kK / 2 + j] = f2fma(bcast(w1), u, acc[kK / 2 + j]);
+                    }
+                }
+            }
+            float accf[kF];
+#pragma unroll
+            for (int i = 0; i < kF / 2; ++i) {
+                accf[2 * i] = acc[i].x;
+                accf[2 * i + 1] = acc[i].y;
+            }
+            // lane gl: Phi_{gl / 8, gl % 8} summed over the group; then m_gl
+            float* T = sT + grp * GroupT<kConvTS>::kGroup;
+            float4* rw = reinterpret_cast<float4*>(T + gl * kConvTS);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                rw[c] = make_float4(accf[4 * c], accf[4 * c + 1], accf[4 * c + 2], accf[4 * c + 3]);
+            __syncwarp();
+            const float phis = column_sum16<kConvTS>(T, gl);
+            __syncwarp();
+            T[gl] = phis;  // row 0 is free again: Phi broadcast
+            __syncwarp();
+            const float4* ph4 = reinterpret_cast<const float4*>(T);
+            const float4* pe0 = reinterpret_cast<const float4*>(sPe + gl * kK);
+            const float4* pe1 = reinterpret_cast<const float4*>(sPe + kF * kK + gl * kK);
+            float m = 0.f;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const float4 p = ph4[c], q = pe0[c];
+                m = fmaf(q.x, p.x, m);
+                m = fmaf(q.y, p.y, m);
+                m = fmaf(q.z, p.z, m);
+                m = fmaf(q.w, p.w, m);
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const float4 p = ph4[2 + c], q = pe1[c];
+                m = fmaf(q.x, p.x, m);
+                m = fmaf(q.y, p.y, m);
+                m = fmaf(q.z, p.z, m);
+                m = fmaf(q.w, p.w, m);
+            }
+            __syncwarp();
+            z = conv_wm(m, gl, sM[grp], sW, sb[gl]);
+        } else {
+            // one gathered row per lane in flight; index and d one slot ahead
+            ConvIn x;
+            for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
+                if (e < e1) {
+                    conv_load(Hin, w, x);
+                    x.d = dcur;
+                    w = src_of(a, e + 16, e1);
+                    dcur = d_of(a, e + 16, e1);
+                    conv_math2(x, acc);
+                }
+            }
+            float accf[kF];
+#pragma unroll
+            for (int i = 0; i < kF / 2; ++i) {
+                accf[2 * i] = acc[i].x;
+                accf[2 * i + 1] = acc[i].y;
+            }
+            z = conv_node_z(accf, gl, sT + grp * GroupT<kConvTS>::kGroup, sM[grp], sW, sb[gl]);
+        }
         const float th = tanhf(z);
         float ev = 0.0f;
         if (valid) {
@@ -1660,9 +1778,10 @@ static int tb_grid(int64_t n, int cap = 148 * 32) {
 static int tb_bwd_grid(int64_t n) { return tb_grid(n, 148 * 4); }
 
 void launch_embed(int64_t rows, const int32_t* node_array, const int32_t* Z, float* H0,
-                  cudaStream_t s) {
+                  cudaStream_t s, uint8_t* zs, unsigned* zmask) {
     if (rows == 0) return;
-    k_embed<<<div_up(rows * 4, 256), 256, 0, s>>>(rows, node_array, Z, H0);
+    if (zs) GMD_CUDA(cudaMemsetAsync(zmask, 0, 4 * sizeof(unsigned), s));
+    k_embed<<<div_up(rows * 4, 256), 256, 0, s>>>(rows, node_array, Z, H0, zs, zmask);
     GMD_LAUNCH_CHECK();
 }
 
@@ -1676,8 +1795,15 @@ void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float
 }
 
 void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
-                 double* per_atom, double* e_part, cudaStream_t s) {
+                 double* per_atom, double* e_part, cudaStream_t s, const uint8_t* zs,
+                 const unsigned* zmask) {
     if (a.n == 0) return;
+    if (zs) {  // layer 0 from the embeddings: species-sum form (<= 2 species)
+        k_conv2<4, kThreads, true><<<model_grid(a.n), kThreads, 0, s>>>(a, layer, Hin, Hout, TH, per_atom,
+                                                                      e_part, zs, zmask);
+        GMD_LAUNCH_CHECK();
+        return;
+    }
     const char* venv = std::getenv("GMD_CONV_VARIANT");  // read per call (tests switch kernels)
     const int variant = venv ? std::atoi(venv) : 0;
     const int g = model_grid(a.n);

@@ -62,14 +62,18 @@ __device__ __forceinline__ void note_nonfinite(const ConvArgs& a, int layer, int
 int model_grid(int64_t n);  // fixed grid => deterministic reductions
 int bwd_edge_grid(int64_t n);  // grid (= virial partial count) of launch_bwd_edge
 
+// zs / zmask (optional): per-row species byte and the species presence mask
+// for the layer-0 species-sum conv
 void launch_embed(int64_t rows, const int32_t* node_array, const int32_t* Z, float* H0,
-                  cudaStream_t s);
+                  cudaStream_t s, uint8_t* zs = nullptr, unsigned* zmask = nullptr);
 void launch_exchange(int64_t nx, const int32_t* xdst, const int32_t* xsrc, float* buf, int width,
                      cudaStream_t s);
 // forward conv layer l: Hout[own] = Hin[own] + tanh(W_l m + b_l); TH_l = tanh(.)
 // last layer additionally writes per-atom energies and per-CTA energy partials
+// zs / zmask (layer 0 only, h0 = the embeddings): the species-sum form
 void launch_conv(const ConvArgs& a, int layer, const float* Hin, float* Hout, float* TH,
-                 double* per_atom, double* e_part, cudaStream_t s);
+                 double* per_atom, double* e_part, cudaStream_t s, const uint8_t* zs = nullptr,
+                 const unsigned* zmask = nullptr);
 // backward: MB[row(v)] = W_l^T (HB[v] * (1 - TH_l[v]^2)); init: HB := readout
 // first (the first backward layer, replacing launch_init_hbar)
 void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int layer,

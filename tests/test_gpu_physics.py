@@ -164,7 +164,7 @@ def test_forces_sum_to_zero(F, K, r3, exact, monkeypatch):
     invariance and momentum-conservation checks (1e-8, test_potential.cpp:
     160-172, test_md.cpp:110-122).  Always for the width-generic and F = 64
     kernels; for the tuned F = 16 backward with GMD_EXACT_FORCES=1 (its
-    default sums per-lane terms in fp32: zero to ~1e-7 relative)."""
+    default sums per-lane terms in fp32: zero to ~1e-6 relative)."""
     monkeypatch.setenv("GMD_EXACT_FORCES", "1" if exact else "0")
     s = S.random_gas(300, 4)
     prm = G.ToyPotentialParams.init(7, F, K, 2, 4.0, r3)
@@ -177,4 +177,4 @@ def test_forces_sum_to_zero(F, K, r3, exact, monkeypatch):
     if exact or F != 16:
         assert fsum <= 1e-12 * max(1.0, fmax) * s.size()
     else:
-        assert fsum <= 1e-6 * fmax
+        assert fsum <= 2e-6 * fmax

@@ -41,13 +41,17 @@ FP32_TIGHT = {
     "forces match finite differences": "FD of an fp32-feature energy: noise ~1e-6 eV / 2e-4 A",
     "stress matches strain finite differences": "same, strain FD to 1e-6",
     "rotation invariance and force equivariance": "1e-9 relative energy, 1e-8 eV/A forces",
+    # the bound 0.5 a_max t^2 (+1e-12) is the displacement of the max-force
+    # atom under a constant force: it holds with equality up to how that force
+    # drifts over 10 steps, so fp32 force noise decides it (it passed or
+    # failed with the rounding order of the forward's reductions)
+    "zero temperature perfect crystal stays put": "equality bound, 1e-12 A slack (test_md.cpp:76-94)",
 }
 # pass only in exact-forces mode (GMD_EXACT_FORCES=1: fp64 per-lane gradient
 # sums in the tuned F = 16 backward, Newton's third law to the last bit)
 EXACT_ONLY = {
     "translation invariance: forces sum to zero": "|sum F| <= 1e-8",
     "momentum conservation": "|P| <= 1e-8 after 100 steps",
-    "zero temperature perfect crystal stays put": "residual net force of a perfect crystal",
 }
 # acceptance criteria: 6 = finite differences at 1e-6 (fp32, as above);
 # 7 = CPU thread scaling of p partitions (one GPU: partitions add no compute)
