@@ -1481,6 +1481,10 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         // layer 0's h_bar is the embedding gradient (no position dependence,
         // never read) unless the three-body backward follows it (L = 1)
         const bool need_hbar = l > 0 || (tb && l == L - 1);
+        // layer 0 reads h0 = emb[Z] (no three-body injection before it)
+        const bool h0_emb = l == 0 && !(tb && L == 1) && !gen && !wide;
+        const uint8_t* zs_l = h0_emb ? h->zs.as<uint8_t>() : nullptr;
+        const unsigned* zm_l = h0_emb ? h->zmask.as<unsigned>() : nullptr;
         {
             PROF("bwd_node");
             if (wide)
@@ -1504,7 +1508,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 else if (gen)
                     launch_gen_bwd_edge(h->gm, ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s);
                 else
-                    launch_bwd_edge(ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s, nullptr, 0, need_hbar);
+                    launch_bwd_edge(ar, MB, H[l], HB + k0 * F, GRAD + k0, vp, s, nullptr, 0, need_hbar, zs_l, zm_l);
             };
             exchange_begin(MB);
             edge(0, h->n_int, 0);
@@ -1521,7 +1525,8 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                 launch_bwd_edge_tc(a, h->ctab.as<int4>(), h->ccta.as<int32_t>(), vgrid, MB, H[l], HB,
                                    GRAD, v_part + (size_t)l * vgrid * 6, s);
             else if (l > 0 || nchunk == 1)
-                launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s, nullptr, 0, need_hbar);
+                launch_bwd_edge(a, MB, H[l], HB, GRAD, v_part + (size_t)l * vgrid * 6, s, nullptr, 0, need_hbar, zs_l,
+                                zm_l);
             else {  // l = 0 in node chunks, forces streamed out per chunk
                 double* fd = h->forces.get<double>(3 * n_all);
                 // chunk starts on multiples of the grid's node stride and one
@@ -1537,7 +1542,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
                     ac.k0 = (n * cum[c] / 10) / stride * stride;
                     ac.n = c + 1 == nchunk ? n : (n * cum[c + 1] / 10) / stride * stride;
                     if (ac.n <= ac.k0) continue;
-                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part, s, vg, vgrid, need_hbar);
+                    launch_bwd_edge(ac, MB, H[l], HB, GRAD, v_part, s, vg, vgrid, need_hbar, zs_l, zm_l);
                     launch_forces_out(ac.n - ac.k0, nullptr, GRAD + ac.k0, fd + 3 * ac.k0, nullptr, s);
                     GMD_CUDA(cudaEventRecord(h->ev[7], s));
                     GMD_CUDA(cudaStreamWaitEvent(h->side, h->ev[7], 0));

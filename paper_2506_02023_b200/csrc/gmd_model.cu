@@ -951,14 +951,38 @@ __device__ __forceinline__ void bwd_math2(const BwdEdgeIn& x, const float4* su_m
 }
 
 constexpr int kBwdTS = 28;  // transpose row: h_bar 16 | virial 6 | gradient 3 | pad
-template <int CTAS, int NT, typename Acc, bool HBAR = true>
+// SPEC (layer 0, Hl = h0 = emb[Z], at most two species): the source's h row
+// is one of two embedding rows staged in shared memory, picked by its species
+// byte -- bitwise the gathered row, one 64-byte gather per edge fewer.
+template <int CTAS, int NT, typename Acc, bool HBAR = true, bool SPEC = false>
 __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float* __restrict__ MB,
                                                            const float* __restrict__ Hl,
                                                            float* __restrict__ HB,
                                                            double4* __restrict__ GRAD,
-                                                           double* vir_part, double* vir_grp) {
+                                                           double* vir_part, double* vir_grp,
+                                                           const uint8_t* __restrict__ zs = nullptr,
+                                                           const unsigned* __restrict__ zmask = nullptr) {
     __shared__ __align__(16) float sU[(NT / 16)][2][kF];  // [group][m_bar_u, h_u][f]
     __shared__ double sVir[(NT / 16)][6];
+    __shared__ __align__(16) float sE[SPEC ? 2 * kF : 4];  // emb rows of the two species
+    int z1 = -1;
+    bool spec = false;
+    if constexpr (SPEC) {
+        int z0 = -1, ns = 0;
+        for (int w = 0; w < 4; ++w) {
+            unsigned m = zmask[w];
+            ns += __popc(m);
+            while (m) {
+                const int z = 32 * w + __ffs(m) - 1;
+                m &= m - 1u;
+                if (z0 < 0) z0 = z; else if (z1 < 0) z1 = z;
+            }
+        }
+        if (z1 < 0) z1 = z0;
+        spec = ns <= 2;
+        if (threadIdx.x < 2 * kF) sE[threadIdx.x] = c_m.emb[(threadIdx.x < kF ? z0 : z1) * kF + (threadIdx.x % kF)];
+        __syncthreads();
+    }
     extern __shared__ __align__(16) float sT[];  // fp32 path: (NT / 16) transpose groups
     const int lane = threadIdx.x & 31;
     const int gl = lane & 15, grp = threadIdx.x >> 4;
@@ -1011,7 +1035,16 @@ __global__ void __launch_bounds__(NT, CTAS) k_bwd_edge2(ConvArgs a, const float*
         const float4* su_h = reinterpret_cast<const float4*>(sU[grp][1]);
         for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
             if (e < e1) {
-                bwd_load2(MB, Hl, wa, xa);
+                if (SPEC && spec) {
+                    const float* mw = MB + (size_t)wa * kF;
+                    ldg256(mw, xa.m[0], xa.m[1]);
+                    ldg256(mw + 8, xa.m[2], xa.m[3]);
+                    const float4* er = reinterpret_cast<const float4*>(sE + (zs[wa] == z1 ? kF : 0));
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) xa.h[c] = er[c];
+                } else {
+                    bwd_load2(MB, Hl, wa, xa);
+                }
                 xa.q = qa;
                 wa = src_of(a, e + 16, e1);
                 qa = vd_of(a, e + 16, e1);
@@ -1863,14 +1896,14 @@ int64_t bwd_edge_stride(int grid) { return (int64_t)grid * (bwd_threads() / 16);
 
 // dynamic shared memory of the fp32 backward (the epilogue's transpose
 // groups), opted in once per instantiation
-template <int NT, bool HBAR>
+template <int NT, bool HBAR, bool SPEC = false>
 static size_t bwd_smem() {
     constexpr size_t bytes = sizeof(float) * (NT / 16) * GroupT<kBwdTS>::kGroup;
     static bool done[64] = {};
     int dev = 0;
     GMD_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !done[dev]) {
-        GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge2<1, NT, float, HBAR>,
+        GMD_CUDA(cudaFuncSetAttribute(k_bwd_edge2<1, NT, float, HBAR, SPEC>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         if (dev >= 0 && dev < 64) done[dev] = true;
     }
@@ -1878,7 +1911,8 @@ static size_t bwd_smem() {
 }
 
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
-                     double* vir_part, cudaStream_t s, double* vir_grp, int grid, bool hbar) {
+                     double* vir_part, cudaStream_t s, double* vir_grp, int grid, bool hbar,
+                     const uint8_t* zs, const unsigned* zmask) {
     if (a.n - a.k0 <= 0) return;
     const int variant = bwd_variant();
     if (variant == 1 && a.k0 != 0) raise(kRuntime, "internal: node ranges need the default kernel");
@@ -1889,6 +1923,9 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
         if (hbar)
             k_bwd_edge2<1, kBwdThreadsExact, double, true><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD,
                                                                                       vir_part, vir_grp);
+        else if (zs)
+            k_bwd_edge2<1, kBwdThreadsExact, double, false, true><<<g, kBwdThreadsExact, 0, s>>>(
+                a, MB, Hl, HB, GRAD, vir_part, vir_grp, zs, zmask);
         else
             k_bwd_edge2<1, kBwdThreadsExact, double, false><<<g, kBwdThreadsExact, 0, s>>>(a, MB, Hl, HB, GRAD,
                                                                                        vir_part, vir_grp);
@@ -1903,6 +1940,10 @@ void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float*
         if (hbar)
             k_bwd_edge2<1, kBwdThreads, float, true><<<g, kBwdThreads, bwd_smem<kBwdThreads, true>(), s>>>(
                 a, MB, Hl, HB, GRAD, vir_part, vir_grp);
+        else if (zs)
+            k_bwd_edge2<1, kBwdThreads, float, false, true>
+                <<<g, kBwdThreads, bwd_smem<kBwdThreads, false, true>(), s>>>(a, MB, Hl, HB, GRAD, vir_part,
+                                                                           vir_grp, zs, zmask);
         else
             k_bwd_edge2<1, kBwdThreads, float, false><<<g, kBwdThreads, bwd_smem<kBwdThreads, false>(), s>>>(
                 a, MB, Hl, HB, GRAD, vir_part, vir_grp);

@@ -87,9 +87,11 @@ void launch_bwd_node(int64_t n, const int32_t* nodes, const int32_t* crow, int l
 // as in one launch, so the virial (and everything else) is bitwise the same
 // hbar = false: skip h_bar (the last backward layer, layer 0, whose h_bar is
 // the embedding gradient -- no position dependence, never read)
+// zs / zmask (layer 0, Hl = h0 = emb[Z]): source h rows from the species
+// table instead of gathered rows (bitwise equal)
 void launch_bwd_edge(const ConvArgs& a, const float* MB, const float* Hl, float* HB, double4* GRAD,
                      double* vir_part, cudaStream_t s, double* vir_grp = nullptr, int grid = 0,
-                     bool hbar = true);
+                     bool hbar = true, const uint8_t* zs = nullptr, const unsigned* zmask = nullptr);
 // the default kernel takes node ranges (a.k0 > 0); grid = bwd_edge_grid(n - k0)
 bool bwd_edge_ranges();
 // nodes per sweep of the default kernel's grid (node k -> group k mod stride)
