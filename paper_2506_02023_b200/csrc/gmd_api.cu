@@ -1402,7 +1402,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
     {
         PROF("embed");
         if (gen)
-            launch_gen_embed(h->gm, R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s);
+            launch_gen_embed(h->gm, R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s,
+                             wide ? h->zs.get<uint8_t>(std::max<int64_t>(1, R)) : nullptr,
+                             wide ? h->zmask.get<unsigned>(4) : nullptr);
         else
             launch_embed(R, part ? A.node_array.as<int32_t>() : nullptr, h->Z.as<int32_t>(), H[0], s,
                          h->zs.get<uint8_t>(std::max<int64_t>(1, R)), h->zmask.get<unsigned>(4));
@@ -1446,7 +1448,9 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
             float* th = TH + ((size_t)l * n + k0) * F;
             double* pl = l == L - 1 ? pa : nullptr;
             if (wide)
-                launch_wide_conv(h->gm, ar, l, H[l], H[l + 1], th, pl, s);
+                launch_wide_conv(h->gm, ar, l, H[l], H[l + 1], th, pl, s,
+                                 l == 0 && !tbl ? h->zs.as<uint8_t>() : nullptr,
+                                 l == 0 && !tbl ? h->zmask.as<unsigned>() : nullptr);
             else if (gen)
                 launch_gen_conv(h->gm, ar, l, H[l], H[l + 1], th, pl, s);
             else
@@ -1485,6 +1489,7 @@ void forward_impl(gmd_handle* h, double* energy, void* per_atom, void* forces, d
         const bool h0_emb = l == 0 && !(tb && L == 1) && !gen && !wide;
         const uint8_t* zs_l = h0_emb ? h->zs.as<uint8_t>() : nullptr;
         const unsigned* zm_l = h0_emb ? h->zmask.as<unsigned>() : nullptr;
+
         {
             PROF("bwd_node");
             if (wide)

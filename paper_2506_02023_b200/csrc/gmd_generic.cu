@@ -26,14 +26,36 @@ __device__ __forceinline__ double gwarp_sumd(double v) {
     return v;
 }
 
+// with zs: also each row's species byte and the species presence mask
+// (warp OR -> block OR -> one global OR per word), for the F = 64 layer-0
+// species-sum kernels
 __global__ void k_gen_embed(GenModel g, int64_t rows, const int32_t* __restrict__ node_array,
-                            const int32_t* __restrict__ Z, float* __restrict__ H0) {
+                            const int32_t* __restrict__ Z, float* __restrict__ H0,
+                            uint8_t* __restrict__ zs, unsigned* zmask) {
+    __shared__ unsigned smask[4];
+    if (threadIdx.x < 4) smask[threadIdx.x] = 0u;
+    __syncthreads();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= rows * g.F) return;
+    const bool live = t < rows * g.F;
     const int64_t r = t / g.F;
     const int f = (int)(t - r * g.F);
-    const int id = node_array ? node_array[r] : (int)r;
-    H0[t] = g.emb[(size_t)Z[id] * g.F + f];
+    int z = 0;
+    if (live) {
+        const int id = node_array ? node_array[r] : (int)r;
+        z = Z[id];
+        H0[t] = g.emb[(size_t)z * g.F + f];
+        if (zs && f == 0) zs[r] = (uint8_t)z;
+    }
+    if (zs) {
+        const bool mine = live && f == 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const unsigned v = __reduce_or_sync(0xffffffffu, mine && (z >> 5) == w ? 1u << (z & 31) : 0u);
+            if ((threadIdx.x & 31) == 0 && v) atomicOr(&smask[w], v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 4 && smask[threadIdx.x]) atomicOr(zmask + threadIdx.x, smask[threadIdx.x]);
+    }
 }
 
 __global__ void k_gen_init_hbar(GenModel g, int64_t n, float* __restrict__ HB) {
@@ -621,9 +643,10 @@ int gen_grid(int64_t n) {
 }
 
 void launch_gen_embed(const GenModel& g, int64_t rows, const int32_t* node_array, const int32_t* Z,
-                      float* H0, cudaStream_t s) {
+                      float* H0, cudaStream_t s, uint8_t* zs, unsigned* zmask) {
     if (rows == 0) return;
-    k_gen_embed<<<div_up(rows * g.F, 256), 256, 0, s>>>(g, rows, node_array, Z, H0);
+    if (zs) GMD_CUDA(cudaMemsetAsync(zmask, 0, 4 * sizeof(unsigned), s));
+    k_gen_embed<<<div_up(rows * g.F, 256), 256, 0, s>>>(g, rows, node_array, Z, H0, zs, zmask);
     GMD_LAUNCH_CHECK();
 }
 

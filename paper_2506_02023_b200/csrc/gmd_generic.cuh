@@ -34,7 +34,7 @@ struct GenModel {
 
 int gen_grid(int64_t n);  // CTAs of the warp-per-node kernels (8 warps each)
 void launch_gen_embed(const GenModel& g, int64_t rows, const int32_t* node_array, const int32_t* Z,
-                      float* H0, cudaStream_t s);
+                      float* H0, cudaStream_t s, uint8_t* zs = nullptr, unsigned* zmask = nullptr);
 // Hout[own] = Hin[own] + tanh(W_l m + b_l); TH_l; per-atom energies on the last layer
 void launch_gen_conv(const GenModel& g, const ConvArgs& a, int layer, const float* Hin, float* Hout,
                      float* TH, double* per_atom, cudaStream_t s);

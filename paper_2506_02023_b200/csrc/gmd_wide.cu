@@ -80,13 +80,40 @@ struct ConvSmem {
     float4 m[kConvWarps][F / 4];   // the node's m row (broadcast reads)
 };
 
+// SPEC (layer 0, h0 = emb[Z], at most two species): m = sum_s emb[z_s] (.)
+// (P Phi_s), Phi_s = the per-species sum of the in-edges' fc phi -- the
+// feature lanes do no per-edge work (F = 16's species-sum form, gmd_model.cu)
+template <bool SPEC = false>
 __global__ void __launch_bounds__(kConvWarps * 32) k_wide_conv(GenModel g, Basis bs, ConvArgs a,
                                                                int layer, const float* __restrict__ Hin,
                                                                float* __restrict__ Hout,
                                                                float* __restrict__ TH,
-                                                               double* __restrict__ per_atom) {
+                                                               double* __restrict__ per_atom,
+                                                               const uint8_t* __restrict__ zs = nullptr,
+                                                               const unsigned* __restrict__ zmask = nullptr) {
     __shared__ __align__(16) ConvSmem S;
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    int z1 = -1;
+    bool spec = false;
+    float2 e0s = make_float2(0.f, 0.f), e1s = make_float2(0.f, 0.f);  // emb[z_s] feature pair
+    if constexpr (SPEC) {
+        int z0 = -1, ns = 0;
+        for (int w = 0; w < 4; ++w) {
+            unsigned m = zmask[w];
+            ns += __popc(m);
+            while (m) {
+                const int z = 32 * w + __ffs(m) - 1;
+                m &= m - 1u;
+                if (z0 < 0) z0 = z; else if (z1 < 0) z1 = z;
+            }
+        }
+        if (z1 < 0) z1 = z0;
+        spec = ns <= 2;
+        if (spec) {
+            e0s = make_float2(g.emb[z0 * F + 2 * lane], g.emb[z0 * F + 2 * lane + 1]);
+            e1s = make_float2(g.emb[z1 * F + 2 * lane], g.emb[z1 * F + 2 * lane + 1]);
+        }
+    }
     const float* W = g.W + (size_t)layer * F * F;  // W[f][q]
     for (int t = threadIdx.x; t < F * F / 2; t += blockDim.x) {
         const int q = t / (F / 2), l = t % (F / 2);
@@ -104,7 +131,44 @@ __global__ void __launch_bounds__(kConvWarps * 32) k_wide_conv(GenModel g, Basis
         const int64_t r = a.crow ? (int64_t)a.crow[v] : v;
         const int e0 = a.row[v], e1 = a.row[v + 1];
         float2 m = make_float2(0.f, 0.f);
-        for (int eb = e0; eb < e1; eb += 32) {
+        if (SPEC && spec) {
+            // lane j: Phi column (s, k) = (j >> 3 & 1, j & 7) over the chunk's
+            // even (j < 16) or odd (j >= 16) edges, halves combined at the end
+            const int col = lane & 15, half = lane >> 4;
+            const int want = col >> 3, kk = col & 7;
+            float ph = 0.f;
+            for (int eb = e0; eb < e1; eb += 32) {
+                const int ne = min(32, e1 - eb);
+                if (lane < ne) {
+                    const float d = a.d[eb + lane];
+                    float phi[K];
+                    phi8(bs, d, phi);
+                    const float fc = d < bs.rc ? 0.5f * __cosf(d * bs.pi_rc) + 0.5f : 0.0f;
+                    S.u[wq][lane][0] = make_float4(fc * phi[0], fc * phi[1], fc * phi[2], fc * phi[3]);
+                    S.u[wq][lane][1] = make_float4(fc * phi[4], fc * phi[5], fc * phi[6], fc * phi[7]);
+                    S.src[wq][lane] = zs[a.lsrc[eb + lane]] == z1 ? 1 : 0;
+                }
+                __syncwarp();
+                for (int i = half; i < ne; i += 2) {
+                    const float u = reinterpret_cast<const float*>(S.u[wq][i])[kk];
+                    ph += S.src[wq][i] == want ? u : 0.f;
+                }
+                __syncwarp();
+            }
+            ph += __shfl_xor_sync(0xffffffffu, ph, 16);
+            float* phs = reinterpret_cast<float*>(S.m[wq]);
+            if (lane < 16) phs[lane] = ph;
+            __syncwarp();
+            float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k2 = 0; k2 < K; ++k2) {
+                s0 = f2fma(P2[k2], bc2(phs[k2]), s0);
+                s1 = f2fma(P2[k2], bc2(phs[K + k2]), s1);
+            }
+            m = f2fma(e0s, s0, f2mul(e1s, s1));
+            __syncwarp();
+        }
+        for (int eb = e0; !(SPEC && spec) && eb < e1; eb += 32) {
             const int ne = min(32, e1 - eb);
             if (lane < ne) {
                 const float d = a.d[eb + lane];
@@ -1637,10 +1701,15 @@ int wide_bwd_grid(int64_t n) {  // one wave
 }
 
 void launch_wide_conv(const GenModel& g, const ConvArgs& a, int layer, const float* Hin, float* Hout,
-                      float* TH, double* per_atom, cudaStream_t s) {
+                      float* TH, double* per_atom, cudaStream_t s, const uint8_t* zs,
+                      const unsigned* zmask) {
     if (a.n <= 0) return;
-    k_wide_conv<<<wide_conv_grid(a.n), kConvWarps * 32, 0, s>>>(g, make_basis(g), a, layer, Hin, Hout,
-                                                                TH, per_atom);
+    if (zs)
+        k_wide_conv<true><<<wide_conv_grid(a.n), kConvWarps * 32, 0, s>>>(g, make_basis(g), a, layer, Hin, Hout,
+                                                                      TH, per_atom, zs, zmask);
+    else
+        k_wide_conv<<<wide_conv_grid(a.n), kConvWarps * 32, 0, s>>>(g, make_basis(g), a, layer, Hin, Hout,
+                                                                    TH, per_atom);
     GMD_LAUNCH_CHECK();
 }
 

@@ -21,8 +21,10 @@ int wide_conv_grid(int64_t n);
 int wide_bwd_grid(int64_t n);  // = number of 6-double virial records of launch_wide_bwd_edge
 
 // Hout[own] = Hin[own] + tanh(W_l m + b_l); TH_l; per-atom energies on the last layer
+// zs / zmask (layer 0, h0 = the embeddings): the species-sum form
 void launch_wide_conv(const GenModel& g, const ConvArgs& a, int layer, const float* Hin, float* Hout,
-                      float* TH, double* per_atom, cudaStream_t s);
+                      float* TH, double* per_atom, cudaStream_t s, const uint8_t* zs = nullptr,
+                      const unsigned* zmask = nullptr);
 // MB[row] = W_l^T (HB (.) (1 - TH_l^2)); init: HB := readout first
 void launch_wide_bwd_node(const GenModel& g, int64_t n, const int32_t* nodes, const int32_t* crow,
                           int layer, float* HB, const float* TH, float* MB, bool init,
