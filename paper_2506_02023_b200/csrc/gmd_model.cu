@@ -663,8 +663,8 @@ __device__ __forceinline__ void conv_math2(const ConvIn& x, float2 acc[kF / 2]) 
 // sum_e emb[Z_src][f] s_e,f = sum_s emb[z_s][f] sum_k P[f][k] Phi_s,k with
 // Phi_s = sum over in-edges from species s of fc(d) phi(d) -- per edge only
 // the radial basis and one species byte (no 64-byte row gather, no 16 x 8
-// contraction); the contraction runs once per node.  More than two species:
-// the per-edge form below.
+// contraction); per node z = b + sum_s (W diag(emb[z_s]) P) Phi_s, the two
+// 16 x 8 matrices staged per CTA.  More than two species: the per-edge form.
 template <int CTAS, int NT = kThreads, bool SPEC = false>
 __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
                                                        const float* __restrict__ Hin,
@@ -676,7 +676,8 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
     __shared__ __align__(16) float sT[(NT / 16) * GroupT<kConvTS>::kGroup];
     __shared__ __align__(16) float sM[NT / 16][kF];
     __shared__ float sb[kF], sro[kF];
-    __shared__ __align__(16) float sPe[SPEC ? 2 * kF * kK : 4];  // [s][f][k] = emb[z_s][f] P[f][k]
+    // [s][g][k] = (W diag(emb[z_s]) P)[g][k]: z = b + sum_s M_s Phi_s directly
+    __shared__ __align__(16) float sPe[SPEC ? 2 * kF * kK : 4];
     for (int i = threadIdx.x; i < kF * kF; i += NT) sW[(i / kF) * kConvTS + i % kF] = c_m.W[layer][i];
     if (threadIdx.x < kF) {
         sb[threadIdx.x] = c_m.b[layer][threadIdx.x];
@@ -698,8 +699,11 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
         if (z1 < 0) z1 = z0;
         if (nspec <= 2)
             for (int i = threadIdx.x; i < 2 * kF * kK; i += NT) {
-                const int sp = i / (kF * kK), f = (i / kK) % kF, kk = i % kK;
-                sPe[i] = c_m.emb[(sp ? z1 : z0) * kF + f] * c_m.P[f * kK + kk];
+                const int sp = i / (kF * kK), gg = (i / kK) % kF, kk = i % kK;
+                const float* e = c_m.emb + (sp ? z1 : z0) * kF;
+                float acc = 0.f;
+                for (int f = 0; f < kF; ++f) acc = fmaf(c_m.W[layer][gg * kF + f], e[f] * c_m.P[f * kK + kk], acc);
+                sPe[i] = acc;
             }
     }
     __syncthreads();
@@ -779,25 +783,25 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
             const float4* ph4 = reinterpret_cast<const float4*>(T);
             const float4* pe0 = reinterpret_cast<const float4*>(sPe + gl * kK);
             const float4* pe1 = reinterpret_cast<const float4*>(sPe + kF * kK + gl * kK);
-            float m = 0.f;
+            float zz = sb[gl];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const float4 p = ph4[c], q = pe0[c];
-                m = fmaf(q.x, p.x, m);
-                m = fmaf(q.y, p.y, m);
-                m = fmaf(q.z, p.z, m);
-                m = fmaf(q.w, p.w, m);
+                zz = fmaf(q.x, p.x, zz);
+                zz = fmaf(q.y, p.y, zz);
+                zz = fmaf(q.z, p.z, zz);
+                zz = fmaf(q.w, p.w, zz);
             }
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const float4 p = ph4[2 + c], q = pe1[c];
-                m = fmaf(q.x, p.x, m);
-                m = fmaf(q.y, p.y, m);
-                m = fmaf(q.z, p.z, m);
-                m = fmaf(q.w, p.w, m);
+                zz = fmaf(q.x, p.x, zz);
+                zz = fmaf(q.y, p.y, zz);
+                zz = fmaf(q.z, p.z, zz);
+                zz = fmaf(q.w, p.w, zz);
             }
             __syncwarp();
-            z = conv_wm(m, gl, sM[grp], sW, sb[gl]);
+            z = zz;
         } else {
             // one gathered row per lane in flight; index and d one slot ahead
             ConvIn x;

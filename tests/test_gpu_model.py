@@ -182,3 +182,25 @@ def test_streamed_force_chunks_match_device_output():
     np.testing.assert_array_equal(pa_h.numpy(), pa_d.cpu().numpy())
     assert e1.value == e2.value
     np.testing.assert_allclose(st2, st1, rtol=1e-12, atol=1e-18)
+
+
+@pytest.mark.parametrize("species,F,r3", [((14, 8), 16, 0.0), ((14, 8, 1), 16, 0.0), ((8,), 16, 0.0),
+                                          ((14, 8, 1), 16, 3.0), ((14, 8), 64, 3.0), ((14, 8, 1, 6), 64, 3.0)])
+def test_layer0_species_forms(oracle_c, species, F, r3):
+    """Layer 0 reads h0 = emb[Z]: with <= 2 species present the conv runs in
+    the species-sum form and the layer-0 backward takes h0 from the staged
+    embedding rows; with more species the same kernels fall back to the
+    per-edge form.  Both against the fp64 oracle, one to four species, F =
+    16 and 64, with and without the three-body stage; p = 2 bitwise p = 1."""
+    s = S.random_system(300, (14.0, 14.0, 14.0), 5, species=species)
+    prm = G.ToyPotentialParams.init(17, F, 8, 3, 5.0, r3)
+    ref = oracle_c.forward_serial(*S.as_args(s), prm.blob, F, 8, 3, 5.0, r3)
+    a = run_gpu(s, prm, r3=r3 if r3 > 0 else None)
+    scale = np.sqrt(F / 16)
+    dea = np.abs(a.per_atom - ref["per_atom"]).max()
+    df = np.abs(a.forces - ref["forces"]).max()
+    assert dea <= TOL_EA * scale, dea
+    assert df <= TOL_F * scale and df <= max(TOL_FREL * scale * np.abs(ref["forces"]).max(), 1e-6), df
+    b = run_gpu(s, prm, p=2, r3=r3 if r3 > 0 else None)
+    np.testing.assert_array_equal(b.per_atom, a.per_atom)
+    np.testing.assert_array_equal(b.forces, a.forces)
