@@ -745,16 +745,19 @@ __global__ void __launch_bounds__(NT, CTAS) k_conv2(ConvArgs a, int layer,
         const int grp = threadIdx.x >> 4;
         float z;
         if (SPEC && nspec <= 2) {
-            // acc[0..3] = Phi_0 (k pairs), acc[4..7] = Phi_1
+            // acc[0..3] = Phi_0 (k pairs), acc[4..7] = Phi_1; the species
+            // byte is read one slot ahead, after the slot's radial math
+            int zc = e0 + gl < e1 ? zs[w] : 0;
             for (int e = e0 + gl; __any_sync(0xffffffffu, e < e1); e += 16) {
                 if (e < e1) {
                     const float d = dcur;
-                    const float w1 = zs[w] == z1 ? 1.0f : 0.0f, w0 = 1.0f - w1;
+                    const float w1 = zc == z1 ? 1.0f : 0.0f, w0 = 1.0f - w1;
                     w = src_of(a, e + 16, e1);
                     dcur = d_of(a, e + 16, e1);
                     float phi[kK];
                     phi_fast(d, phi);
                     const float fc = fc_fast(d);
+                    zc = e + 16 < e1 ? zs[w] : 0;
 #pragma unroll
                     for (int j = 0; j < kK / 2; ++j) {
                         const float2 u = f2mul(make_float2(phi[2 * j], phi[2 * j + 1]), bcast(fc));
