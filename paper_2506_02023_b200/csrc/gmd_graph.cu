@@ -151,6 +151,7 @@ struct WarpNL {             // per-warp shared state of the search
     int sc_q[kWSCap][3];
     double sc_shift[kWSCap][3];
     uint32_t code[kCodeCap];      // image q code per stencil cell of the bin
+    int cstart[32];               // per candidate chunk: non-empty cell starting at each slot
 };
 
 // Bitonic network over 16 R keys held by a 16-lane half-warp, R per lane:
@@ -309,21 +310,33 @@ __global__ void __launch_bounds__(kThreads, CTAS) k_nl_search(
                 if (lane < nc) S.sc_pre[lane + 1] = incl;
                 if (lane == 0) S.sc_pre[0] = 0;
                 const int total = __shfl_sync(0xffffffffu, incl, 31);
+                const int pre_c = incl - cntc;  // lane c < nc: first candidate of cell c
+                int carry = 0;                  // cell holding the chunk's first candidate
                 __syncwarp();
                 for (int kb = 0; kb < total; kb += 32) {
                     const int k = kb + lane;
                     const bool valid = k < total;
+                    // cell of candidate k: the last non-empty cell starting at or
+                    // before k (non-empty cells start at distinct slots) -- a
+                    // warp max-scan over the chunk's cell starts
+                    S.cstart[lane] = -1;
+                    __syncwarp();
+                    if (cntc > 0 && pre_c >= kb && pre_c < kb + 32) S.cstart[pre_c - kb] = lane;
+                    __syncwarp();
+                    int cm = S.cstart[lane];
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const int u = __shfl_up_sync(0xffffffffu, cm, off);
+                        if (lane >= off) cm = max(cm, u);
+                    }
+                    cm = max(cm, carry);
+                    carry = __shfl_sync(0xffffffffu, cm, 31);
                     float c32x = 0.f, c32y = 0.f, c32z = 0.f;
                     double cv[3] = {0.0, 0.0, 0.0};
                     int ci = 0, slot = 0;
                     uint32_t key = 0u;
                     if (valid) {
-                        int lo = 0, hi = nc - 1;  // last stencil cell with pre <= k
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (S.sc_pre[mid] <= k) lo = mid; else hi = mid - 1;
-                        }
-                        ci = lo;
+                        ci = cm;
                         slot = bin_start[S.sc_bin[ci]] + (k - S.sc_pre[ci]);
 #pragma unroll
                         for (int d = 0; d < 3; ++d)  // wrapped_j + shift (neighborlist.cpp:176)
